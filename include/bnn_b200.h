@@ -1,0 +1,166 @@
+/*
+ * bnn_b200.h -- C ABI of the B200-native binarise -> bit-pack -> xnor-popcount
+ * path (BMXNet, arXiv 1705.09864).
+ *
+ * Every entry point takes plain device pointers allocated by the caller
+ * (PyTorch in the Python host layer), sizes as int64_t, and an explicit CUDA
+ * stream.  Nothing allocates device memory internally, there is no global
+ * mutable state apart from the thread-local error message, and every call is
+ * asynchronous on `stream`.  Return value: 0 on success, a negative BNN_E*
+ * code for an invalid argument (the reference raises ValueError for these),
+ * or BNN_ECUDA (> 0) when a CUDA launch failed.  bnn_last_error() returns a
+ * thread-local message for the last failing call.
+ *
+ * Word format (reference bitpack.py:1-16): bit k of a packed vector is bit
+ * k % 64 of u64 word k / 64 (LSB-first); bit 1 <=> sign +1, bit 0 <=> -1.
+ * A layout-'a' matrix is [rows, ceil(K/64)] words, row-major.
+ *
+ * Reference interface each entry point replaces (paths relative to
+ * /root/reference/pkg/src/bitnn):
+ *   bnn_binarize_f32        bitpack.binarize              bitpack.py:30-42
+ *   bnn_pack_rows_f32       bitpack.pack_matrix_a(binarize(x)) / pack_row
+ *                                                         bitpack.py:144-149,172-182
+ *   bnn_pack_cols_f32       bitpack.pack_matrix_b         bitpack.py:152-169
+ *   bnn_pack_nchw_f32       tensor.im2col + binarize + pack_matrix_b, the
+ *                           activation side of QConv2d.forward
+ *                                                         layers.py:230-236
+ *   bnn_words_transpose     BitMatrix layout 'b' <-> 'a'  bitpack.py:90-141
+ *   bnn_audit_padding       bitpack.audit_padding         bitpack.py:197-215
+ *   bnn_xnor_gemm           gemm.xnor_gemm_{base,blocked,unrolled,parallel}
+ *                                                         gemm.py:226-291
+ *   bnn_conv_weights_reorder QConv2d.pack (load-time re-layout only)
+ *                                                         layers.py:215-223
+ *   bnn_bconv2d             QConv2d.forward(INFER_PACKED) layers.py:225-245
+ */
+#ifndef BNN_B200_H
+#define BNN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* cudaStream_t-compatible opaque handle (0 = legacy default stream). */
+typedef struct CUstream_st *bnn_stream_t;
+
+enum bnn_status {
+    BNN_OK = 0,
+    BNN_EINVAL = -1,   /* bad pointer / negative size / bad enum           */
+    BNN_EDIMS = -2,    /* GemmDims: M, N, K must be >= 1 (gemm.py:170-172)  */
+    BNN_EKEXACT = -3,  /* K >= 2^24 loses f32 exactness (gemm.py:173-177)   */
+    BNN_EPAD = -4,     /* pad fill must be 0 or 1 (bitpack.py:109-111)      */
+    BNN_EALIGN = -5,   /* leading dimension smaller than the row            */
+    BNN_EGEOM = -6,    /* conv geometry (tensor.py:15-27)                   */
+    BNN_EUNSUP = -7,   /* algorithm not available for this shape           */
+    BNN_ECUDA = 1      /* CUDA launch / runtime error                      */
+};
+
+/* Output domain of the GEMM epilogue (qmath.py:87-109). */
+enum bnn_domain {
+    BNN_POPCOUNT = 0,  /* P = popcount(xnor(a, b)) in [0, K] (gemm.py:3-8) */
+    BNN_DOT = 1        /* 2P - K, the signed dot product                    */
+};
+
+/* Inner-product engine.  AUTO picks the measured winner for the shape. */
+enum bnn_algo {
+    BNN_ALGO_AUTO = 0,
+    BNN_ALGO_POPC = 1, /* CUDA cores: LOP3 xor + POPC                        */
+    BNN_ALGO_BMMA = 2, /* warp mma.sync m16n8k256 b1 .and.popc               */
+    BNN_ALGO_UMMA = 3  /* tcgen05.mma kind::i8 on bits expanded in SMEM      */
+};
+
+/* Flags written (OR-ed) by the pack kernels into a caller int32. */
+enum bnn_flags {
+    BNN_FLAG_NONFINITE = 1, /* NaN/Inf seen: binarize raises ValueError    */
+    BNN_FLAG_NOTSIGN = 2    /* strict mode: an entry was not exactly +-1     */
+};
+
+/* Pack-kernel input modes. */
+enum bnn_pack_mode {
+    BNN_PACK_SIGN = 0,  /* binarize on the fly: x >= 0 -> 1 (sign(-0) = +1) */
+    BNN_PACK_STRICT = 1 /* input must already be +-1 (_validate_signs)      */
+};
+
+int bnn_abi_version(void);
+const char *bnn_last_error(void);
+const char *bnn_status_string(int status);
+/* number of SMs of the current device (0 if none) */
+int bnn_device_sm_count(void);
+
+/* bitpack.binarize: out[i] = x[i] >= 0 ? +1 : -1 (f32).  Sets
+ * BNN_FLAG_NONFINITE in *flags (if non-null) when an input is not finite. */
+int bnn_binarize_f32(const float *x, int64_t n, float *out, int32_t *flags,
+                     bnn_stream_t stream);
+
+/* pack_matrix_a(binarize(x)): x [R, K] f32, row stride ldx elements ->
+ * out [R, ldo] u64 words (ldo >= ceil(K/64)); tail bits of the last word =
+ * pad_bit.  Optional row_popc[R] receives popcount of each row's valid bits. */
+int bnn_pack_rows_f32(const float *x, int64_t R, int64_t K, int64_t ldx, uint64_t *out,
+                      int64_t ldo, int pad_bit, int mode, int32_t *row_popc, int32_t *flags,
+                      bnn_stream_t stream);
+
+/* pack_matrix_b: x [K, N] f32 (row stride ldx) -> out [ceil(K/64), ldo] u64
+ * words (layout 'b', column n packed along K), tail bits = pad_bit. */
+int bnn_pack_cols_f32(const float *x, int64_t K, int64_t N, int64_t ldx, uint64_t *out,
+                      int64_t ldo, int pad_bit, int mode, int32_t *flags, bnn_stream_t stream);
+
+/* Activation side of the binary conv: x NCHW [B, C, H, W] f32 -> packed
+ * NHWC words out [B*H*W, ceil(C/64)] (channel c at bit c%64 of word c/64,
+ * channel tail bits 0). */
+int bnn_pack_nchw_f32(const float *x, int64_t B, int64_t C, int64_t H, int64_t W, uint64_t *out,
+                      int mode, int32_t *flags, bnn_stream_t stream);
+
+/* out[c, r] = in[r, c] for a [rows, cols] u64 word matrix (layout 'b' <-> K-contiguous). */
+int bnn_words_transpose(const uint64_t *in, int64_t rows, int64_t cols, int64_t ldi,
+                        uint64_t *out, int64_t ldo, bnn_stream_t stream);
+
+/* audit_padding over `vectors` packed vectors of n_bits each: vector v's
+ * last word is words[v * ld_vec + (W-1) * ld_word].  Sets *bad (device
+ * int32, caller-zeroed) to 1 when a tail bit differs from pad_fill. */
+int bnn_audit_padding(const uint64_t *words, int64_t vectors, int64_t n_bits, int64_t ld_vec,
+                      int64_t ld_word, int pad_fill, int32_t *bad, bnn_stream_t stream);
+
+/* xnor-popcount GEMM, both operands K-contiguous:
+ *   A [M, lda] u64 (weights, layout 'a'), tail fill a_pad
+ *   B [N, ldb] u64 (activations, one packed vector per row), tail fill b_pad
+ *   P[m, n] = #{k < K : bit_k(A[m]) == bit_k(B[n])}
+ *   C[m * ldc_m + n * ldc_n] = (domain == DOT ? 2P - K : P) * scale[m] + shift[m]
+ * scale/shift are optional (null = 1 / 0).  K < 2^24. */
+int bnn_xnor_gemm(const uint64_t *A, int64_t lda, const uint64_t *B, int64_t ldb, int64_t M,
+                  int64_t N, int64_t K, int a_pad, int b_pad, float *C, int64_t ldc_m,
+                  int64_t ldc_n, int domain, const float *scale, const float *shift, int algo,
+                  bnn_stream_t stream);
+
+/* Words per pixel of the packed NHWC activation layout: ceil(C / 64). */
+int64_t bnn_conv_channel_words(int64_t C);
+
+/* Load-time re-layout of QConv2d.pack() words (layout 'a' of
+ * W.reshape(F, C*kh*kw), bit order (c, i, j), layers.py:221) into the device
+ * tap-major order [F, kh*kw, ceil(C/64)] (bit order (i, j, c), channel tail
+ * 0).  Popcount is permutation-invariant, so outputs are unchanged. */
+int bnn_conv_weights_reorder(const uint64_t *w_ref, int64_t F, int64_t C, int64_t kh,
+                             int64_t kw, uint64_t *w_dev, bnn_stream_t stream);
+
+/* Implicit-im2col binary convolution (QConv2d.forward INFER_PACKED):
+ *   x_words  packed NHWC [B, H, W, ceil(C/64)] (bnn_pack_nchw_f32)
+ *   w_dev    [F, kh*kw*ceil(C/64)] (bnn_conv_weights_reorder)
+ *   y        f32 NCHW [B, F, oh, ow]
+ * Spatial padding follows the reference composition im2col(zero pad) ->
+ * binarize: a pad position is sign(0) = +1. */
+int bnn_bconv2d(const uint64_t *x_words, int64_t B, int64_t C, int64_t H, int64_t W,
+                const uint64_t *w_dev, int64_t F, int64_t kh, int64_t kw, int64_t sh, int64_t sw,
+                int64_t ph, int64_t pw, float *y, int domain, const float *scale,
+                const float *shift, int algo, bnn_stream_t stream);
+
+/* Roofline probe (synchronous): measured issue rate of a pipe on the
+ * current device.  pipe 0 = POPC (32-bit population counts per second).
+ * `sink` is a caller-allocated device u32 the kernel may write. */
+int bnn_probe_pipe_peak(int pipe, int64_t iters, uint32_t *sink, double *ops_per_sec,
+                        bnn_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BNN_B200_H */

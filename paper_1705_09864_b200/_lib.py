@@ -1,0 +1,101 @@
+"""ctypes binding of libbnn_b200.so (the C ABI declared in include/bnn_b200.h).
+
+The library is the product path: if it is missing or no CUDA device is
+present, every op raises instead of falling back to a CPU implementation.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libbnn_b200.so")
+
+# enum values mirrored from include/bnn_b200.h
+OK, EINVAL, EDIMS, EKEXACT, EPAD, EALIGN, EGEOM, EUNSUP, ECUDA = 0, -1, -2, -3, -4, -5, -6, -7, 1
+POPCOUNT, DOT = 0, 1
+ALGO_AUTO, ALGO_POPC, ALGO_BMMA, ALGO_UMMA = 0, 1, 2, 3
+ALGOS = {"auto": ALGO_AUTO, "popc": ALGO_POPC, "bmma": ALGO_BMMA, "umma": ALGO_UMMA}
+FLAG_NONFINITE, FLAG_NOTSIGN = 1, 2
+PACK_SIGN, PACK_STRICT = 0, 1
+
+# every exported symbol and its ctypes signature (restype, argtypes)
+_i64, _i32, _vp, _cp = ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_char_p
+SIGNATURES = {
+    "bnn_abi_version": (_i32, []),
+    "bnn_last_error": (_cp, []),
+    "bnn_status_string": (_cp, [_i32]),
+    "bnn_device_sm_count": (_i32, []),
+    "bnn_binarize_f32": (_i32, [_vp, _i64, _vp, _vp, _vp]),
+    "bnn_pack_rows_f32": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _i32, _i32, _vp, _vp, _vp]),
+    "bnn_pack_cols_f32": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _i32, _i32, _vp, _vp]),
+    "bnn_pack_nchw_f32": (_i32, [_vp, _i64, _i64, _i64, _i64, _vp, _i32, _vp, _vp]),
+    "bnn_words_transpose": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _vp]),
+    "bnn_audit_padding": (_i32, [_vp, _i64, _i64, _i64, _i64, _i32, _vp, _vp]),
+    "bnn_xnor_gemm": (_i32, [_vp, _i64, _vp, _i64, _i64, _i64, _i64, _i32, _i32, _vp, _i64,
+                             _i64, _i32, _vp, _vp, _i32, _vp]),
+    "bnn_conv_channel_words": (_i64, [_i64]),
+    "bnn_conv_weights_reorder": (_i32, [_vp, _i64, _i64, _i64, _i64, _vp, _vp]),
+    "bnn_bconv2d": (_i32, [_vp, _i64, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _i64,
+                           _i64, _vp, _i32, _vp, _vp, _i32, _vp]),
+    "bnn_probe_pipe_peak": (_i32, [_i32, _i64, _vp, _vp, _vp]),
+}
+
+
+class BnnError(RuntimeError):
+    """A CUDA-side failure inside libbnn_b200 (status > 0)."""
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load the shared library and bind every symbol (no CUDA calls made)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(
+            f"{path} is missing: build it with `python -m paper_1705_09864_b200.build` "
+            "(there is no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def require_cuda(t: torch.Tensor | None = None) -> None:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1705_09864_b200 needs a CUDA device (B200); no CPU fallback")
+    if t is not None and not t.is_cuda:
+        raise ValueError("expected a CUDA tensor")
+
+
+def stream_ptr(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else int(t.data_ptr())
+
+
+def check(status: int, what: str = "") -> None:
+    """Map a C-ABI status to the reference's exception types."""
+    if status == OK:
+        return
+    msg = (_lib.bnn_last_error() or b"").decode() if _lib is not None else ""
+    if status > 0:
+        raise BnnError(f"{what}: {msg}")
+    raise ValueError(msg or what)
+
+
+def call(name: str, *args) -> None:
+    lib = load()
+    check(getattr(lib, name)(*args), name)

@@ -1,0 +1,219 @@
+// extern "C" boundary of libbnn_b200.so: argument validation (mirroring the
+// reference's ValueError cases), thread-local error reporting, and engine
+// dispatch.  See include/bnn_b200.h for the contract of each entry point.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "bnn_common.cuh"
+
+namespace bnn {
+
+static thread_local char g_err[512] = "";
+
+int set_error(int status, const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return status;
+}
+
+int check_launch(const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_error(BNN_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+    return BNN_OK;
+}
+
+// engines (defined in the kernel translation units)
+int launch_binarize(const float *, int64_t, float *, int32_t *, cudaStream_t);
+int launch_pack_rows(const float *, int64_t, int64_t, int64_t, uint64_t *, int64_t, int, int,
+                     int32_t *, int32_t *, cudaStream_t);
+int launch_pack_cols(const float *, int64_t, int64_t, int64_t, uint64_t *, int64_t, int, int,
+                     int32_t *, cudaStream_t);
+int launch_pack_nchw(const float *, int64_t, int64_t, int64_t, int64_t, uint64_t *, int,
+                     int32_t *, cudaStream_t);
+int launch_words_transpose(const uint64_t *, int64_t, int64_t, int64_t, uint64_t *, int64_t,
+                           cudaStream_t);
+int launch_audit_padding(const uint64_t *, int64_t, int64_t, int64_t, int64_t, int, int32_t *,
+                         cudaStream_t);
+int launch_conv_weights_reorder(const uint64_t *, int64_t, int64_t, int64_t, int64_t,
+                                uint64_t *, cudaStream_t);
+int launch_xnor_gemm_popc(const uint64_t *, int64_t, const uint64_t *, int64_t, int64_t,
+                          int64_t, int64_t, float *, int64_t, int64_t, const Epilogue &,
+                          cudaStream_t);
+int launch_bconv2d_popc(const uint64_t *, int64_t, int64_t, int64_t, int64_t, const uint64_t *,
+                        int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,
+                        int64_t, float *, const Epilogue &, cudaStream_t);
+
+}  // namespace bnn
+
+using namespace bnn;
+
+#define BNN_REQUIRE(cond, status, ...) \
+    do {                               \
+        if (!(cond)) return set_error(status, __VA_ARGS__); \
+    } while (0)
+
+static const int64_t kMaxKExact = 1 << 24;  // gemm.py:43-44
+
+extern "C" {
+
+int bnn_abi_version(void) { return 1; }
+
+const char *bnn_last_error(void) { return g_err; }
+
+const char *bnn_status_string(int status) {
+    switch (status) {
+        case BNN_OK: return "ok";
+        case BNN_EINVAL: return "invalid argument";
+        case BNN_EDIMS: return "GEMM dims must be positive";
+        case BNN_EKEXACT: return "K exceeds the float32-exact range";
+        case BNN_EPAD: return "pad fill must be 0 or 1";
+        case BNN_EALIGN: return "leading dimension too small";
+        case BNN_EGEOM: return "invalid convolution geometry";
+        case BNN_EUNSUP: return "unsupported configuration";
+        case BNN_ECUDA: return "CUDA error";
+        default: return "unknown status";
+    }
+}
+
+int bnn_device_sm_count(void) {
+    int dev = 0, n = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+    return n;
+}
+
+int bnn_binarize_f32(const float *x, int64_t n, float *out, int32_t *flags, bnn_stream_t stream) {
+    BNN_REQUIRE(n >= 0, BNN_EINVAL, "n must be non-negative");
+    BNN_REQUIRE(n == 0 || (x && out), BNN_EINVAL, "null pointer");
+    return launch_binarize(x, n, out, flags, as_stream(stream));
+}
+
+int bnn_pack_rows_f32(const float *x, int64_t R, int64_t K, int64_t ldx, uint64_t *out,
+                      int64_t ldo, int pad_bit, int mode, int32_t *row_popc, int32_t *flags,
+                      bnn_stream_t stream) {
+    BNN_REQUIRE(R >= 0 && K >= 0, BNN_EINVAL, "negative size");
+    BNN_REQUIRE(pad_bit == 0 || pad_bit == 1, BNN_EPAD, "pad_fill must be 0 or 1, got %d", pad_bit);
+    BNN_REQUIRE(mode == BNN_PACK_SIGN || mode == BNN_PACK_STRICT, BNN_EINVAL, "bad mode");
+    BNN_REQUIRE(ldx >= K && ldo >= ceil_div(K, 64), BNN_EALIGN, "leading dimension too small");
+    BNN_REQUIRE(R * K == 0 || (x && out), BNN_EINVAL, "null pointer");
+    return launch_pack_rows(x, R, K, ldx, out, ldo, pad_bit, mode, row_popc, flags,
+                            as_stream(stream));
+}
+
+int bnn_pack_cols_f32(const float *x, int64_t K, int64_t N, int64_t ldx, uint64_t *out,
+                      int64_t ldo, int pad_bit, int mode, int32_t *flags, bnn_stream_t stream) {
+    BNN_REQUIRE(K >= 0 && N >= 0, BNN_EINVAL, "negative size");
+    BNN_REQUIRE(pad_bit == 0 || pad_bit == 1, BNN_EPAD, "pad_fill must be 0 or 1, got %d", pad_bit);
+    BNN_REQUIRE(mode == BNN_PACK_SIGN || mode == BNN_PACK_STRICT, BNN_EINVAL, "bad mode");
+    BNN_REQUIRE(ldx >= N && ldo >= N, BNN_EALIGN, "leading dimension too small");
+    BNN_REQUIRE(K * N == 0 || (x && out), BNN_EINVAL, "null pointer");
+    return launch_pack_cols(x, K, N, ldx, out, ldo, pad_bit, mode, flags, as_stream(stream));
+}
+
+int bnn_pack_nchw_f32(const float *x, int64_t B, int64_t C, int64_t H, int64_t W, uint64_t *out,
+                      int mode, int32_t *flags, bnn_stream_t stream) {
+    BNN_REQUIRE(B >= 0 && C >= 0 && H >= 0 && W >= 0, BNN_EINVAL, "negative size");
+    BNN_REQUIRE(mode == BNN_PACK_SIGN || mode == BNN_PACK_STRICT, BNN_EINVAL, "bad mode");
+    BNN_REQUIRE(B * C * H * W == 0 || (x && out), BNN_EINVAL, "null pointer");
+    BNN_REQUIRE(ceil_div(C, 64) <= 65535 && B <= 65535, BNN_EUNSUP, "C or B too large");
+    return launch_pack_nchw(x, B, C, H, W, out, mode, flags, as_stream(stream));
+}
+
+int bnn_words_transpose(const uint64_t *in, int64_t rows, int64_t cols, int64_t ldi,
+                        uint64_t *out, int64_t ldo, bnn_stream_t stream) {
+    BNN_REQUIRE(rows >= 0 && cols >= 0, BNN_EINVAL, "negative size");
+    BNN_REQUIRE(ldi >= cols && ldo >= rows, BNN_EALIGN, "leading dimension too small");
+    BNN_REQUIRE(rows * cols == 0 || (in && out), BNN_EINVAL, "null pointer");
+    return launch_words_transpose(in, rows, cols, ldi, out, ldo, as_stream(stream));
+}
+
+int bnn_audit_padding(const uint64_t *words, int64_t vectors, int64_t n_bits, int64_t ld_vec,
+                      int64_t ld_word, int pad_fill, int32_t *bad, bnn_stream_t stream) {
+    BNN_REQUIRE(vectors >= 0 && n_bits >= 0, BNN_EINVAL, "negative size");
+    BNN_REQUIRE(pad_fill == 0 || pad_fill == 1, BNN_EPAD, "pad_fill must be 0 or 1");
+    BNN_REQUIRE(bad != nullptr, BNN_EINVAL, "null flag pointer");
+    return launch_audit_padding(words, vectors, n_bits, ld_vec, ld_word, pad_fill, bad,
+                                as_stream(stream));
+}
+
+static int check_gemm_dims(int64_t M, int64_t N, int64_t K) {
+    // GemmDims.__post_init__ (gemm.py:170-177)
+    BNN_REQUIRE(M >= 1 && N >= 1 && K >= 1, BNN_EDIMS,
+                "GEMM dims must be positive, got M=%lld N=%lld K=%lld", (long long)M,
+                (long long)N, (long long)K);
+    BNN_REQUIRE(K < kMaxKExact, BNN_EKEXACT,
+                "K=%lld exceeds %lld; popcounts would lose exactness in float32 outputs",
+                (long long)K, (long long)(kMaxKExact - 1));
+    return BNN_OK;
+}
+
+int bnn_xnor_gemm(const uint64_t *A, int64_t lda, const uint64_t *B, int64_t ldb, int64_t M,
+                  int64_t N, int64_t K, int a_pad, int b_pad, float *C, int64_t ldc_m,
+                  int64_t ldc_n, int domain, const float *scale, const float *shift, int algo,
+                  bnn_stream_t stream) {
+    int rc = check_gemm_dims(M, N, K);
+    if (rc) return rc;
+    BNN_REQUIRE((a_pad == 0 || a_pad == 1) && (b_pad == 0 || b_pad == 1), BNN_EPAD,
+                "pad fills must be 0 or 1");
+    const int64_t W = ceil_div(K, 64);
+    BNN_REQUIRE(lda >= W && ldb >= W, BNN_EALIGN, "lda/ldb smaller than ceil(K/64)=%lld",
+                (long long)W);
+    BNN_REQUIRE(A && B && C, BNN_EINVAL, "null pointer");
+    BNN_REQUIRE(domain == BNN_POPCOUNT || domain == BNN_DOT, BNN_EINVAL, "bad domain %d", domain);
+    // Tail correction (bitpack.py:12-15): positions K..64W-1 contribute
+    // popc(a_pad ^ b_pad) each to X, so P = K - (X - tail) = k_eff - X.
+    const int64_t tail = (64 * W - K) * (int64_t)(a_pad ^ b_pad);
+    Epilogue ep{(int32_t)(K + tail), (int32_t)K, domain, scale, shift};
+    switch (algo) {
+        case BNN_ALGO_AUTO:
+        case BNN_ALGO_POPC:
+            return launch_xnor_gemm_popc(A, lda, B, ldb, M, N, K, C, ldc_m, ldc_n, ep,
+                                         as_stream(stream));
+        default:
+            return set_error(BNN_EUNSUP, "algorithm %d not available", algo);
+    }
+}
+
+int64_t bnn_conv_channel_words(int64_t C) { return C > 0 ? ceil_div(C, 64) : 0; }
+
+int bnn_conv_weights_reorder(const uint64_t *w_ref, int64_t F, int64_t C, int64_t kh,
+                             int64_t kw, uint64_t *w_dev, bnn_stream_t stream) {
+    BNN_REQUIRE(F >= 1 && C >= 1 && kh >= 1 && kw >= 1, BNN_EGEOM, "invalid conv weight shape");
+    BNN_REQUIRE(w_ref && w_dev, BNN_EINVAL, "null pointer");
+    return launch_conv_weights_reorder(w_ref, F, C, kh, kw, w_dev, as_stream(stream));
+}
+
+int bnn_bconv2d(const uint64_t *x_words, int64_t B, int64_t C, int64_t H, int64_t W,
+                const uint64_t *w_dev, int64_t F, int64_t kh, int64_t kw, int64_t sh, int64_t sw,
+                int64_t ph, int64_t pw, float *y, int domain, const float *scale,
+                const float *shift, int algo, bnn_stream_t stream) {
+    // tensor.conv_output_hw (tensor.py:15-27)
+    BNN_REQUIRE(B >= 1 && C >= 1 && H >= 1 && W >= 1 && F >= 1 && kh >= 1 && kw >= 1 &&
+                    sh >= 1 && sw >= 1 && ph >= 0 && pw >= 0,
+                BNN_EGEOM, "invalid convolution geometry");
+    const int64_t oh = (H + 2 * ph - kh) / sh + 1, ow = (W + 2 * pw - kw) / sw + 1;
+    BNN_REQUIRE(H + 2 * ph >= kh && W + 2 * pw >= kw && oh >= 1 && ow >= 1, BNN_EGEOM,
+                "kernel %lldx%lld does not fit input %lldx%lld with pad %lld,%lld",
+                (long long)kh, (long long)kw, (long long)H, (long long)W, (long long)ph,
+                (long long)pw);
+    const int64_t K = C * kh * kw;
+    int rc = check_gemm_dims(F, B * oh * ow, K);
+    if (rc) return rc;
+    BNN_REQUIRE(x_words && w_dev && y, BNN_EINVAL, "null pointer");
+    BNN_REQUIRE(domain == BNN_POPCOUNT || domain == BNN_DOT, BNN_EINVAL, "bad domain %d", domain);
+    BNN_REQUIRE(H * W * bnn_conv_channel_words(C) < (1ll << 31), BNN_EUNSUP, "image too large");
+    Epilogue ep{(int32_t)K, (int32_t)K, domain, scale, shift};  // all tails are 0
+    switch (algo) {
+        case BNN_ALGO_AUTO:
+        case BNN_ALGO_POPC:
+            return launch_bconv2d_popc(x_words, B, C, H, W, w_dev, F, kh, kw, sh, sw, ph, pw, oh,
+                                       ow, y, ep, as_stream(stream));
+        default:
+            return set_error(BNN_EUNSUP, "algorithm %d not available", algo);
+    }
+}
+
+}  // extern "C"

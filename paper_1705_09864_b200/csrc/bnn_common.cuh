@@ -1,0 +1,39 @@
+// Internal helpers shared by the sm_100a kernels of libbnn_b200.so.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/bnn_b200.h"
+
+namespace bnn {
+
+// thread-local last error (bnn_last_error); set_error returns the status
+int set_error(int status, const char *fmt, ...);
+int check_launch(const char *what);
+
+inline cudaStream_t as_stream(bnn_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Epilogue parameters common to the GEMM and conv kernels.
+//   X  = sum over all stored words of popc(a ^ b)
+//   P  = k_eff - X     (k_eff absorbs the tail correction, see capi)
+//   v  = domain == DOT ? 2P - K : P ;  out = v * scale[m] + shift[m]
+struct Epilogue {
+    int32_t k_eff;
+    int32_t k_logical;
+    int32_t domain;
+    const float *scale;
+    const float *shift;
+    __device__ __forceinline__ float apply(int32_t x, int m) const {
+        int32_t p = k_eff - x;
+        int32_t v = domain == BNN_DOT ? 2 * p - k_logical : p;
+        float f = (float)v;
+        if (scale) f = f * __ldg(scale + m);
+        if (shift) f = f + __ldg(shift + m);
+        return f;
+    }
+};
+
+}  // namespace bnn

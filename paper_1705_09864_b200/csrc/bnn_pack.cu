@@ -1,0 +1,279 @@
+// Sign-binarise + bit-pack kernels (HBM-bound) and word re-layout helpers.
+//
+// Reference functions replaced (paths under /root/reference/pkg/src/bitnn):
+//   binarize            bitpack.py:30-42    x >= 0 -> +1 (so -0.0 -> +1)
+//   pack_matrix_a       bitpack.py:144-149  rows along K, LSB-first, tail fill
+//   pack_matrix_b       bitpack.py:152-169  columns along K -> [W, N]
+//   _validate_signs     bitpack.py:69-75    (STRICT mode flag)
+//   audit_padding       bitpack.py:197-215
+//   im2col + pack_matrix_b activation side of QConv2d (layers.py:230-236),
+//                       here as a NCHW -> packed NHWC transpose-pack.
+#include <cstdio>
+
+#include "bnn_common.cuh"
+
+namespace bnn {
+
+__device__ __forceinline__ uint32_t sign_bit(float v) { return v >= 0.0f ? 1u : 0u; }
+
+// Per-element checks: bit0 = non-finite, bit1 = not exactly +-1 (strict mode).
+__device__ __forceinline__ int elem_flags(float v, int mode) {
+    int f = isfinite(v) ? 0 : BNN_FLAG_NONFINITE;
+    if (mode == BNN_PACK_STRICT && v != 1.0f && v != -1.0f) f |= BNN_FLAG_NOTSIGN;
+    return f;
+}
+
+__device__ __forceinline__ void flush_flags(int f, int32_t *flags) {
+    // one atomic per warp at most
+    int any = __reduce_or_sync(0xffffffffu, f);
+    if (any && flags && (threadIdx.x & 31) == 0) atomicOr(flags, any);
+}
+
+// ---------------------------------------------------------------- binarize
+__global__ void binarize_kernel(const float *__restrict__ x, int64_t n, float *__restrict__ out,
+                                int32_t *flags) {
+    int f = 0;
+    int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+        float v = x[i];
+        f |= elem_flags(v, BNN_PACK_SIGN);
+        out[i] = v >= 0.0f ? 1.0f : -1.0f;
+    }
+    flush_flags(f, flags);
+}
+
+// ---------------------------------------------------------------- pack rows
+// One warp per row; each iteration covers 128 consecutive elements (4 per
+// lane, float4 when aligned) and emits 2 u64 words.  Lane l owns elements
+// 4l..4l+3, i.e. nibble l%8 of u32 word l/8; an OR-butterfly over the 8
+// lanes of a group assembles each u32 word.
+template <bool kVec4>
+__global__ void pack_rows_kernel(const float *__restrict__ x, int64_t R, int64_t K, int64_t ldx,
+                                 uint64_t *__restrict__ out, int64_t ldo, int pad_bit, int mode,
+                                 int32_t *__restrict__ row_popc, int32_t *flags) {
+    const int lane = threadIdx.x & 31;
+    const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    if (row >= R) return;  // warp-uniform
+    const float *xr = x + row * ldx;
+    const int64_t W = ceil_div(K, 64);
+    int f = 0;
+    int popc = 0;
+    for (int64_t base = 0; base < W * 64; base += 128) {
+        const int64_t e = base + 4 * lane;
+        float v[4];
+        if (kVec4 && e + 3 < K) {
+            float4 q = __ldg(reinterpret_cast<const float4 *>(xr + e));
+            v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+        } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) v[i] = e + i < K ? __ldg(xr + e + i) : 0.0f;
+        }
+        uint32_t nib = 0, valid = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            bool in = e + i < K;
+            uint32_t b = in ? sign_bit(v[i]) : (uint32_t)pad_bit;
+            nib |= b << i;
+            valid |= (in ? 1u : 0u) << i;
+            if (in) f |= elem_flags(v[i], mode);
+        }
+        popc += __popc(nib & valid);
+        uint32_t w = nib << (4 * (lane & 7));
+        w |= __shfl_xor_sync(0xffffffffu, w, 1);
+        w |= __shfl_xor_sync(0xffffffffu, w, 2);
+        w |= __shfl_xor_sync(0xffffffffu, w, 4);
+        uint32_t hi = __shfl_down_sync(0xffffffffu, w, 8);
+        const int64_t wi = base / 64 + (lane >> 4);
+        if ((lane & 15) == 0 && wi < W) out[row * ldo + wi] = (uint64_t)w | ((uint64_t)hi << 32);
+    }
+    flush_flags(f, flags);
+    if (row_popc) {
+        popc = __reduce_add_sync(0xffffffffu, popc);
+        if (lane == 0) row_popc[row] = popc;
+    }
+}
+
+// ---------------------------------------------------------------- pack cols
+// layout 'b': thread per (word w, column n); 64 coalesced loads along K.
+__global__ void pack_cols_kernel(const float *__restrict__ x, int64_t K, int64_t N, int64_t ldx,
+                                 uint64_t *__restrict__ out, int64_t ldo, int pad_bit, int mode,
+                                 int32_t *flags) {
+    const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t w = blockIdx.y;
+    int f = 0;
+    if (n < N) {
+        uint64_t word = 0;
+#pragma unroll 16
+        for (int b = 0; b < 64; ++b) {
+            int64_t k = w * 64 + b;
+            uint64_t bit;
+            if (k < K) {
+                float v = __ldg(x + k * ldx + n);
+                f |= elem_flags(v, mode);
+                bit = sign_bit(v);
+            } else {
+                bit = (uint64_t)pad_bit;
+            }
+            word |= bit << b;
+        }
+        out[w * ldo + n] = word;
+    }
+    flush_flags(f, flags);
+}
+
+// ---------------------------------------------------------------- pack NCHW
+// x [B, C, H, W] -> out [B*H*W, Cw] u64 (NHWC words, channel tail 0).
+// Thread per (pixel, channel word); a warp covers 32 consecutive pixels of
+// one (b, cw) so every load instruction reads 128 contiguous bytes.
+__global__ void pack_nchw_kernel(const float *__restrict__ x, int64_t B, int64_t C, int64_t HW,
+                                 int64_t Cw, uint64_t *__restrict__ out, int mode,
+                                 int32_t *flags) {
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t cw = blockIdx.y;
+    const int64_t b = blockIdx.z;
+    int f = 0;
+    if (p < HW) {
+        const float *src = x + (b * C + cw * 64) * HW + p;
+        const int nc = (int)(C - cw * 64 < 64 ? C - cw * 64 : 64);
+        uint64_t word = 0;
+        if (nc == 64) {
+#pragma unroll 16
+            for (int i = 0; i < 64; ++i) {
+                float v = __ldg(src + (int64_t)i * HW);
+                f |= elem_flags(v, mode);
+                word |= (uint64_t)sign_bit(v) << i;
+            }
+        } else {
+            for (int i = 0; i < nc; ++i) {
+                float v = __ldg(src + (int64_t)i * HW);
+                f |= elem_flags(v, mode);
+                word |= (uint64_t)sign_bit(v) << i;
+            }
+        }
+        out[(b * HW + p) * Cw + cw] = word;
+    }
+    flush_flags(f, flags);
+}
+
+// ---------------------------------------------------------------- transpose
+__global__ void words_transpose_kernel(const uint64_t *__restrict__ in, int64_t rows,
+                                       int64_t cols, int64_t ldi, uint64_t *__restrict__ out,
+                                       int64_t ldo) {
+    __shared__ uint64_t tile[32][33];
+    const int64_t c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        int64_t r = r0 + i, c = c0 + threadIdx.x;
+        if (r < rows && c < cols) tile[i][threadIdx.x] = in[r * ldi + c];
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        int64_t c = c0 + i, r = r0 + threadIdx.x;
+        if (r < rows && c < cols) out[c * ldo + r] = tile[threadIdx.x][i];
+    }
+}
+
+// ---------------------------------------------------------------- audit
+__global__ void audit_padding_kernel(const uint64_t *__restrict__ words, int64_t vectors,
+                                     int64_t last_off, int64_t ld_vec, uint64_t mask,
+                                     uint64_t expect, int32_t *bad) {
+    const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int f = 0;
+    if (v < vectors) f = ((words[v * ld_vec + last_off] & mask) != expect) ? 1 : 0;
+    if (__any_sync(0xffffffffu, f) && (threadIdx.x & 31) == 0) atomicOr(bad, 1);
+}
+
+// ---------------------------------------------------------------- conv weights
+// w_ref: [F, ceil(C*kh*kw/64)] with bit (c*kh + i)*kw + j  (layers.py:221)
+// w_dev: [F, kh*kw, Cw] with bit c%64 of word (i*kw + j)*Cw + c/64
+__global__ void conv_weights_reorder_kernel(const uint64_t *__restrict__ w_ref, int64_t F,
+                                            int64_t C, int64_t kh, int64_t kw, int64_t Cw,
+                                            uint64_t *__restrict__ w_dev) {
+    const int64_t per_f = kh * kw * Cw;
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= F * per_f) return;
+    const int64_t f = idx / per_f, r = idx % per_f;
+    const int64_t tap = r / Cw, cw = r % Cw;
+    const int64_t i = tap / kw, j = tap % kw;
+    const int64_t wref = ceil_div(C * kh * kw, 64);
+    const uint64_t *src = w_ref + f * wref;
+    uint64_t word = 0;
+    for (int b = 0; b < 64; ++b) {
+        int64_t c = cw * 64 + b;
+        if (c >= C) break;
+        int64_t bit = (c * kh + i) * kw + j;
+        word |= ((src[bit >> 6] >> (bit & 63)) & 1ull) << b;
+    }
+    w_dev[idx] = word;
+}
+
+// ================================================================ launchers
+int launch_binarize(const float *x, int64_t n, float *out, int32_t *flags, cudaStream_t s) {
+    if (n == 0) return BNN_OK;
+    int blocks = (int)(ceil_div(n, 256) < 148 * 16 ? ceil_div(n, 256) : 148 * 16);
+    binarize_kernel<<<blocks, 256, 0, s>>>(x, n, out, flags);
+    return check_launch("binarize_kernel");
+}
+
+int launch_pack_rows(const float *x, int64_t R, int64_t K, int64_t ldx, uint64_t *out,
+                     int64_t ldo, int pad_bit, int mode, int32_t *row_popc, int32_t *flags,
+                     cudaStream_t s) {
+    if (R == 0 || K == 0) return BNN_OK;
+    const int64_t blocks = ceil_div(R * 32, 256);
+    const bool vec = (ldx % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+    if (vec)
+        pack_rows_kernel<true><<<(unsigned)blocks, 256, 0, s>>>(x, R, K, ldx, out, ldo, pad_bit,
+                                                               mode, row_popc, flags);
+    else
+        pack_rows_kernel<false><<<(unsigned)blocks, 256, 0, s>>>(x, R, K, ldx, out, ldo, pad_bit,
+                                                                mode, row_popc, flags);
+    return check_launch("pack_rows_kernel");
+}
+
+int launch_pack_cols(const float *x, int64_t K, int64_t N, int64_t ldx, uint64_t *out,
+                     int64_t ldo, int pad_bit, int mode, int32_t *flags, cudaStream_t s) {
+    if (K == 0 || N == 0) return BNN_OK;
+    dim3 grid((unsigned)ceil_div(N, 256), (unsigned)ceil_div(K, 64));
+    pack_cols_kernel<<<grid, 256, 0, s>>>(x, K, N, ldx, out, ldo, pad_bit, mode, flags);
+    return check_launch("pack_cols_kernel");
+}
+
+int launch_pack_nchw(const float *x, int64_t B, int64_t C, int64_t H, int64_t W, uint64_t *out,
+                     int mode, int32_t *flags, cudaStream_t s) {
+    const int64_t HW = H * W, Cw = ceil_div(C, 64);
+    if (B == 0 || HW == 0 || C == 0) return BNN_OK;
+    dim3 grid((unsigned)ceil_div(HW, 128), (unsigned)Cw, (unsigned)B);
+    pack_nchw_kernel<<<grid, 128, 0, s>>>(x, B, C, HW, Cw, out, mode, flags);
+    return check_launch("pack_nchw_kernel");
+}
+
+int launch_words_transpose(const uint64_t *in, int64_t rows, int64_t cols, int64_t ldi,
+                           uint64_t *out, int64_t ldo, cudaStream_t s) {
+    if (rows == 0 || cols == 0) return BNN_OK;
+    dim3 grid((unsigned)ceil_div(cols, 32), (unsigned)ceil_div(rows, 32));
+    words_transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(in, rows, cols, ldi, out, ldo);
+    return check_launch("words_transpose_kernel");
+}
+
+int launch_audit_padding(const uint64_t *words, int64_t vectors, int64_t n_bits, int64_t ld_vec,
+                         int64_t ld_word, int pad_fill, int32_t *bad, cudaStream_t s) {
+    const int rem = (int)(n_bits % 64);
+    if (rem == 0 || vectors == 0) return BNN_OK;
+    const uint64_t mask = ~((1ull << rem) - 1ull);
+    const uint64_t expect = pad_fill ? mask : 0ull;
+    const int64_t last_off = (ceil_div(n_bits, 64) - 1) * ld_word;
+    audit_padding_kernel<<<(unsigned)ceil_div(vectors, 256), 256, 0, s>>>(
+        words, vectors, last_off, ld_vec, mask, expect, bad);
+    return check_launch("audit_padding_kernel");
+}
+
+int launch_conv_weights_reorder(const uint64_t *w_ref, int64_t F, int64_t C, int64_t kh,
+                                int64_t kw, uint64_t *w_dev, cudaStream_t s) {
+    const int64_t Cw = ceil_div(C, 64);
+    const int64_t total = F * kh * kw * Cw;
+    if (total == 0) return BNN_OK;
+    conv_weights_reorder_kernel<<<(unsigned)ceil_div(total, 256), 256, 0, s>>>(w_ref, F, C, kh,
+                                                                              kw, Cw, w_dev);
+    return check_launch("conv_weights_reorder_kernel");
+}
+
+}  // namespace bnn

@@ -1,0 +1,353 @@
+"""Quantized layers with a bit-packed xnor-popcount inference path on the B200.
+
+Drop-in for the hot-path layers of the reference ``bitnn.layers``
+(``/root/reference/pkg/src/bitnn/layers.py``): ``QActivation`` (:392-419),
+``QConv2d`` (:159-263) and ``QDense`` (:320-389), with the same constructor
+arguments, modes (``train_float`` / ``infer_float`` / ``infer_packed``,
+:31-34), ``ModeError`` rules and popcount-domain outputs.  ``infer_packed``
+runs the sm_100a kernels (fused sign+pack, implicit-im2col conv, xnor GEMM);
+``infer_float`` keeps the reference's float semantics on the GPU (used as the
+in-framework equivalence check, as in the reference).  Training/backward is
+out of scope (OUT OF SCOPE) and raises ModeError.
+
+BMXNet names: ``QConvolution`` / ``QFullyConnected`` take ``act_bit`` /
+``weight_bit`` and fuse the preceding sign activation
+into the pack kernel; ``QConvolution`` accepts spatial padding with the
+reference-composition semantics "zero-pad, then binarize" (pad = +1, G2).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.nn.functional as F
+
+from . import _lib, qmath
+from .bitpack import (BitMatrix, pack_matrix_a, pack_nchw, pack_rows_device, raise_on_flags,
+                      to_device_f32, to_device_words, words_per_bits)
+from .gemm import xnor_rows_gemm
+
+TRAIN_FLOAT = "train_float"
+INFER_FLOAT = "infer_float"
+INFER_PACKED = "infer_packed"
+MODES = (TRAIN_FLOAT, INFER_FLOAT, INFER_PACKED)
+BN_EPS = 1e-5  # layers.py:36
+
+
+class ModeError(RuntimeError):
+    """A layer was asked to run in a mode its current state cannot serve (layers.py:40-41)."""
+
+
+def _check_mode(mode):
+    if mode not in MODES:
+        raise ValueError(f"unknown mode {mode!r}; choose from {MODES}")
+    if mode == TRAIN_FLOAT:
+        raise ModeError("training is out of scope for the B200 inference path")
+
+
+def _uniform_init(rng, shape, fan_in, fan_out):
+    """layers._uniform_init (layers.py:49-51), NumPy RNG for seed parity."""
+    bound = np.sqrt(6.0 / (fan_in + fan_out))
+    return rng.uniform(-bound, bound, size=shape).astype(np.float32)
+
+
+def _ret(t: torch.Tensor, was_np: bool):
+    return t.cpu().numpy() if was_np else t
+
+
+def _float_matmul(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        return a @ b
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+
+
+def _float_conv(x, w, stride):
+    prev = torch.backends.cudnn.allow_tf32
+    torch.backends.cudnn.allow_tf32 = False
+    try:
+        return F.conv2d(x, w, stride=stride)
+    finally:
+        torch.backends.cudnn.allow_tf32 = prev
+
+
+class QActivation:
+    """Quantize activations to ``bits`` (sign at 1 bit) -- layers.py:392-419."""
+
+    kind = "qactivation"
+
+    def __init__(self, bits=1):
+        self.bits = int(bits)
+        qmath.QuantSpec(self.bits)
+
+    def spec(self):
+        return {"kind": self.kind, "bits": self.bits}
+
+    def forward(self, x, mode=INFER_FLOAT):
+        _check_mode(mode)
+        t, was_np = to_device_f32(x)
+        if self.bits == 1:
+            # binarize(clip(x)) == binarize(x); one fused sign kernel
+            out = torch.empty_like(t)
+            flags = torch.zeros(1, dtype=torch.int32, device=t.device)
+            _lib.call("bnn_binarize_f32", _lib.ptr(t), t.numel(), _lib.ptr(out), _lib.ptr(flags),
+                      _lib.stream_ptr())
+            raise_on_flags(flags, "quantize_signed requires finite inputs")
+            return _ret(out, was_np)
+        return _ret(qmath.quantize_signed(t, self.bits), was_np)
+
+
+class _QLayer:
+    """Shared packed-weight state of the quantized conv / dense layers."""
+
+    def _set_packed(self, bm: BitMatrix):
+        self.packed = bm
+        self._dev_words = None
+
+    def pack(self):
+        """Freeze sign(weight) into packed words for ``infer_packed`` (layers.py:215-223)."""
+        if self.bits != 1:
+            raise ModeError("packed inference supports 1-bit weights only")
+        if self.weight is None:
+            raise ModeError("no float weights to pack")
+        w = torch.from_numpy(np.ascontiguousarray(self._flat_weight_np())).cuda()
+        flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+        words = pack_rows_device(w, 0, strict=False, flags=flags)
+        raise_on_flags(flags)
+        self._set_packed(BitMatrix(words=words, vectors=w.shape[0], n_bits=w.shape[1],
+                                   layout="a", pad_fill=0))
+        return self.packed
+
+    def load_packed(self, words, n_bits=None):
+        """Install layout-'a' words from storage (``.bmx`` payload, modelio.py:221-237)."""
+        k = self.k_reduce if n_bits is None else n_bits
+        w = to_device_words(words)
+        self._set_packed(BitMatrix(words=w, vectors=w.shape[0], n_bits=k, layout="a",
+                                   pad_fill=0))
+
+    def _require_packed(self):
+        if self.bits != 1:
+            raise ModeError("packed inference supports 1-bit weights only")
+        if self.packed is None:
+            raise ModeError("layer has no packed weights; pack() or load a converted model")
+
+
+class QConv2d(_QLayer):
+    """Binary convolution -- layers.py:159-263 (popcount-domain outputs).
+
+    ``infer_packed`` requires +-1 inputs (the reference validates them in
+    pack_matrix_b, bitpack.py:69-75) and, like the reference, rejects padding.
+    """
+
+    kind = "qconv"
+    _allow_pad = False
+    _fuse_sign = False  # the reference QConv2d consumes QActivation's output as-is
+
+    def __init__(self, in_channels, filters, kernel, stride=(1, 1), pad=(0, 0), bits=1,
+                 rng=None):
+        self.in_channels = in_channels
+        self.filters = filters
+        self.kernel = tuple(kernel)
+        self.stride = tuple(stride)
+        self.pad = tuple(pad)
+        if self.pad != (0, 0) and not self._allow_pad:
+            raise ValueError("quantized convolution does not support padding")
+        self.bits = int(bits)
+        qmath.QuantSpec(self.bits)
+        kh, kw = self.kernel
+        self.k_reduce = in_channels * kh * kw
+        if rng is not None:
+            self.weight = _uniform_init(rng, (filters, in_channels, kh, kw), self.k_reduce,
+                                        filters * kh * kw)
+        else:
+            self.weight = None
+        self.packed = None
+        self._dev_words = None
+        self.domain = _lib.POPCOUNT
+        self.algo = "auto"
+
+    def spec(self):
+        return {"kind": self.kind, "in_channels": self.in_channels, "filters": self.filters,
+                "kernel": list(self.kernel), "stride": list(self.stride), "pad": list(self.pad),
+                "bits": self.bits}
+
+    def _flat_weight_np(self):
+        return np.asarray(self.weight, np.float32).reshape(self.filters, self.k_reduce)
+
+    def device_weights(self) -> torch.Tensor:
+        """Tap-major re-layout of the packed words (load-time, cached)."""
+        self._require_packed()
+        if self._dev_words is None:
+            kh, kw = self.kernel
+            cw = words_per_bits(self.in_channels)
+            out = torch.empty((self.filters, kh * kw * cw), dtype=torch.uint64, device="cuda")
+            _lib.call("bnn_conv_weights_reorder", _lib.ptr(self.packed.words), self.filters,
+                      self.in_channels, kh, kw, _lib.ptr(out), _lib.stream_ptr())
+            self._dev_words = out
+        return self._dev_words
+
+    def output_hw(self, h, w):
+        kh, kw = self.kernel
+        oh = (h + 2 * self.pad[0] - kh) // self.stride[0] + 1
+        ow = (w + 2 * self.pad[1] - kw) // self.stride[1] + 1
+        if min(h, w) < 1 or oh < 1 or ow < 1 or h + 2 * self.pad[0] < kh or \
+                w + 2 * self.pad[1] < kw:
+            raise ValueError(f"kernel {kh}x{kw} does not fit input {h}x{w} with pad "
+                             f"{self.pad[0]},{self.pad[1]}")
+        return oh, ow
+
+    def forward_packed_words(self, x_words: torch.Tensor, b: int, h: int, w: int,
+                             out: torch.Tensor | None = None, scale=None, shift=None):
+        """Conv on already-packed NHWC words -> f32 NCHW (no host sync)."""
+        kh, kw = self.kernel
+        oh, ow = self.output_hw(h, w)
+        if out is None:
+            out = torch.empty((b, self.filters, oh, ow), dtype=torch.float32, device="cuda")
+        wd = self.device_weights()
+        algo = _lib.ALGOS[self.algo] if isinstance(self.algo, str) else self.algo
+        _lib.call("bnn_bconv2d", _lib.ptr(x_words), b, self.in_channels, h, w, _lib.ptr(wd),
+                  self.filters, kh, kw, self.stride[0], self.stride[1], self.pad[0], self.pad[1],
+                  _lib.ptr(out), self.domain, _lib.ptr(scale), _lib.ptr(shift), algo,
+                  _lib.stream_ptr())
+        return out
+
+    def _strict_input(self) -> bool:
+        return True
+
+    def forward(self, x, mode=INFER_FLOAT):
+        _check_mode(mode)
+        t, was_np = to_device_f32(x)
+        if t.dim() != 4:
+            raise ValueError(f"expected [B, C, H, W] input, got ndim={t.dim()}")
+        b, c, h, w = t.shape
+        self.output_hw(h, w)
+        if mode == INFER_PACKED:
+            self._require_packed()
+            flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+            xw = pack_nchw(t, strict=self._strict_input(), flags=flags)
+            y = self.forward_packed_words(xw, b, h, w)
+            raise_on_flags(flags)
+            return _ret(y, was_np)
+        if self.weight is None:
+            raise ModeError("layer holds packed weights only; float modes unavailable")
+        wq = qmath.quantize_signed(torch.from_numpy(np.asarray(self.weight, np.float32)).cuda(),
+                                   self.bits)
+        if self.pad != (0, 0):
+            # G2: the reference composition zero-pads, then binarizes
+            t = F.pad(t, (self.pad[1], self.pad[1], self.pad[0], self.pad[0]))
+        if self._fuse_sign:
+            t = qmath.quantize_signed(t, self.act_bit)
+        dot = _float_conv(t, wq, self.stride)
+        if self.bits == 1 and self.domain == _lib.POPCOUNT:
+            return _ret((dot + self.k_reduce) * 0.5, was_np)
+        return _ret(dot, was_np)
+
+
+class QDense(_QLayer):
+    """Binary fully connected layer -- layers.py:320-389 (popcount domain)."""
+
+    kind = "qfc"
+    _fuse_sign = False
+
+    def __init__(self, in_features, units, bits=1, rng=None):
+        self.in_features = in_features
+        self.units = units
+        self.bits = int(bits)
+        qmath.QuantSpec(self.bits)
+        self.k_reduce = in_features
+        if rng is not None:
+            self.weight = _uniform_init(rng, (units, in_features), in_features, units)
+        else:
+            self.weight = None
+        self.packed = None
+        self._dev_words = None
+        self.domain = _lib.POPCOUNT
+        self.algo = "auto"
+
+    def spec(self):
+        return {"kind": self.kind, "in_features": self.in_features, "units": self.units,
+                "bits": self.bits}
+
+    def _flat_weight_np(self):
+        return np.asarray(self.weight, np.float32)
+
+    def _strict_input(self) -> bool:
+        return True
+
+    def forward_packed_rows(self, x_words: torch.Tensor, out=None, scale=None, shift=None):
+        """[B, W] packed activations (tail 0) -> f32 [B, units] (no host sync)."""
+        self._require_packed()
+        return xnor_rows_gemm(self.packed.words, x_words, self.in_features, a_pad=0, b_pad=0,
+                              domain=self.domain, out=out, transpose_out=True, scale=scale,
+                              shift=shift, algo=self.algo)
+
+    def forward(self, x, mode=INFER_FLOAT):
+        _check_mode(mode)
+        t, was_np = to_device_f32(x)
+        if mode == INFER_PACKED:
+            self._require_packed()
+            if t.dim() != 2 or t.shape[1] != self.in_features:
+                raise ValueError(f"expected [B, {self.in_features}] input")
+            flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+            xw = pack_rows_device(t, 0, strict=self._strict_input(), flags=flags)
+            y = self.forward_packed_rows(xw)
+            raise_on_flags(flags)
+            return _ret(y, was_np)
+        if self.weight is None:
+            raise ModeError("layer holds packed weights only; float modes unavailable")
+        wq = qmath.quantize_signed(torch.from_numpy(np.asarray(self.weight, np.float32)).cuda(),
+                                   self.bits)
+        if self._fuse_sign:
+            t = qmath.quantize_signed(t, self.act_bit)
+        dot = _float_matmul(t, wq.T)
+        if self.bits == 1 and self.domain == _lib.DOT:
+            return _ret(dot, was_np)
+        y = (dot + self.in_features) * 0.5 if self.bits == 1 else dot
+        return _ret(y, was_np)
+
+
+# ----------------------------------------------------------------- BMXNet names
+class QConvolution(QConv2d):
+    """BMXNet ``QConvolution`` (act_bit / weight_bit), sign of the input fused.
+
+    Accepts raw float input: the sign activation (QActivation(act_bit=1)) is
+    folded into the pack kernel.  Spatial padding is allowed and means
+    "zero-pad then binarize" (pad positions are +1).
+    """
+
+    kind = "qconvolution"
+    _allow_pad = True
+    _fuse_sign = True
+
+    def __init__(self, in_channels, num_filter, kernel, stride=(1, 1), pad=(0, 0), act_bit=1,
+                 weight_bit=1, rng=None, domain="popcount"):
+        if int(act_bit) != int(weight_bit):
+            raise ValueError("act_bit != weight_bit has no reference packed path (G4)")
+        super().__init__(in_channels, num_filter, kernel, stride, pad, bits=weight_bit, rng=rng)
+        self.act_bit = int(act_bit)
+        self.weight_bit = int(weight_bit)
+        self.domain = _lib.DOT if domain == "dot" else _lib.POPCOUNT
+
+    def _strict_input(self) -> bool:
+        return False
+
+
+class QFullyConnected(QDense):
+    """BMXNet ``QFullyConnected`` (act_bit / weight_bit), sign of the input fused."""
+
+    kind = "qfullyconnected"
+    _fuse_sign = True
+
+    def __init__(self, in_features, num_hidden, act_bit=1, weight_bit=1, rng=None,
+                 domain="popcount"):
+        if int(act_bit) != int(weight_bit):
+            raise ValueError("act_bit != weight_bit has no reference packed path (G4)")
+        super().__init__(in_features, num_hidden, bits=weight_bit, rng=rng)
+        self.act_bit = int(act_bit)
+        self.weight_bit = int(weight_bit)
+        self.domain = _lib.DOT if domain == "dot" else _lib.POPCOUNT
+
+    def _strict_input(self) -> bool:
+        return False

@@ -1,0 +1,176 @@
+"""Pre-allocated execution plans for the packed hot path (serving / bench).
+
+A plan binds one packed layer to one input geometry, owns every device
+buffer the step needs (packed activations, output, flag word, pinned host
+staging) and issues only the sm_100a kernels of libbnn_b200.so -- no
+allocation, no host sync -- so a step can be timed, replayed or captured in
+a CUDA graph.  ``run_host`` is the end-to-end call a user makes with host
+memory: H2D copy, sign+pack, xnor kernel, D2H copy, one synchronize, and the
+reference's ValueError on non-finite input (bitpack.py:37-38).
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from .bitpack import words_per_bits
+from .layers import QConv2d, QDense
+
+
+class _Plan:
+    launches_per_step = 2
+
+    def _alloc_common(self):
+        self.flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.flags_host = torch.zeros(1, dtype=torch.int32).pin_memory()
+
+    def check_flags(self):
+        f = int(self.flags.item())
+        if f & _lib.FLAG_NONFINITE:
+            raise ValueError("binarize requires finite inputs")
+        if f & _lib.FLAG_NOTSIGN:
+            raise ValueError("matrix entries must all be -1 or +1")
+
+    def run_host(self, x_host: torch.Tensor, y_host: torch.Tensor) -> torch.Tensor:
+        """End to end from pinned host memory: H2D, pack, kernel, D2H, one sync."""
+        self.x.copy_(x_host, non_blocking=True)
+        self.run_device()
+        y_host.copy_(self.y, non_blocking=True)
+        self.flags_host.copy_(self.flags, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        f = int(self.flags_host[0])
+        if f & _lib.FLAG_NONFINITE:
+            raise ValueError("binarize requires finite inputs")
+        return y_host
+
+    @property
+    def h2d_bytes(self) -> int:
+        return self.x.numel() * self.x.element_size()
+
+    @property
+    def d2h_bytes(self) -> int:
+        return self.y.numel() * self.y.element_size()
+
+
+class ConvPlan(_Plan):
+    """sign+pack (bnn_pack_nchw_f32) -> implicit-im2col conv (bnn_bconv2d)."""
+
+    def __init__(self, layer: QConv2d, batch: int, h: int, w: int, strict: bool = False):
+        self.layer = layer
+        self.b, self.h, self.w = batch, h, w
+        self.oh, self.ow = layer.output_hw(h, w)
+        c = layer.in_channels
+        self.x = torch.empty((batch, c, h, w), dtype=torch.float32, device="cuda")
+        self.xw = torch.empty((batch, h, w, words_per_bits(c)), dtype=torch.uint64, device="cuda")
+        self.y = torch.empty((batch, layer.filters, self.oh, self.ow), dtype=torch.float32,
+                             device="cuda")
+        self.wd = layer.device_weights()
+        self.mode = _lib.PACK_STRICT if strict else _lib.PACK_SIGN
+        self.algo = _lib.ALGOS[layer.algo] if isinstance(layer.algo, str) else layer.algo
+        self._alloc_common()
+        self.lib = _lib.load()
+        kh, kw = layer.kernel
+        self.m, self.n, self.k = layer.filters, batch * self.oh * self.ow, c * kh * kw
+
+    @property
+    def binary_ops(self) -> int:
+        return 2 * self.m * self.n * self.k
+
+    def pack(self, stream: int | None = None):
+        s = _lib.stream_ptr() if stream is None else stream
+        L = self.layer
+        _lib.check(self.lib.bnn_pack_nchw_f32(self.x.data_ptr(), self.b, L.in_channels, self.h,
+                                              self.w, self.xw.data_ptr(), self.mode,
+                                              self.flags.data_ptr(), s), "pack")
+
+    def kernel(self, stream: int | None = None):
+        s = _lib.stream_ptr() if stream is None else stream
+        L = self.layer
+        kh, kw = L.kernel
+        _lib.check(self.lib.bnn_bconv2d(self.xw.data_ptr(), self.b, L.in_channels, self.h,
+                                        self.w, self.wd.data_ptr(), L.filters, kh, kw,
+                                        L.stride[0], L.stride[1], L.pad[0], L.pad[1],
+                                        self.y.data_ptr(), L.domain, None, None, self.algo, s),
+                   "bconv2d")
+
+    def run_device(self):
+        self.pack()
+        self.kernel()
+        return self.y
+
+
+class DensePlan(_Plan):
+    """sign+pack rows (bnn_pack_rows_f32) -> xnor GEMM (bnn_xnor_gemm), out [B, units]."""
+
+    def __init__(self, layer: QDense, batch: int, strict: bool = False):
+        self.layer = layer
+        self.b = batch
+        k = layer.in_features
+        self.x = torch.empty((batch, k), dtype=torch.float32, device="cuda")
+        self.xw = torch.empty((batch, words_per_bits(k)), dtype=torch.uint64, device="cuda")
+        self.y = torch.empty((batch, layer.units), dtype=torch.float32, device="cuda")
+        layer._require_packed()
+        self.wa = layer.packed.words
+        self.mode = _lib.PACK_STRICT if strict else _lib.PACK_SIGN
+        self.algo = _lib.ALGOS[layer.algo] if isinstance(layer.algo, str) else layer.algo
+        self._alloc_common()
+        self.lib = _lib.load()
+        self.m, self.n, self.k = layer.units, batch, k
+
+    @property
+    def binary_ops(self) -> int:
+        return 2 * self.m * self.n * self.k
+
+    def pack(self, stream: int | None = None):
+        s = _lib.stream_ptr() if stream is None else stream
+        _lib.check(self.lib.bnn_pack_rows_f32(self.x.data_ptr(), self.b, self.k, self.k,
+                                              self.xw.data_ptr(), self.xw.shape[1], 0, self.mode,
+                                              None, self.flags.data_ptr(), s), "pack")
+
+    def kernel(self, stream: int | None = None):
+        s = _lib.stream_ptr() if stream is None else stream
+        _lib.check(self.lib.bnn_xnor_gemm(self.wa.data_ptr(), self.wa.shape[1], self.xw.data_ptr(),
+                                          self.xw.shape[1], self.m, self.n, self.k, 0, 0,
+                                          self.y.data_ptr(), 1, self.m, self.layer.domain, None,
+                                          None, self.algo, s), "xnor_gemm")
+
+    def run_device(self):
+        self.pack()
+        self.kernel()
+        return self.y
+
+
+class GemmPlan(_Plan):
+    """Square / long-K binary GEMM on pre-packed operands (config 5): one kernel."""
+
+    launches_per_step = 1
+
+    def __init__(self, a_rows: torch.Tensor, b_rows: torch.Tensor, k: int, algo="auto",
+                 domain: int = _lib.POPCOUNT):
+        self.a, self.bw = a_rows, b_rows
+        self.m, self.n, self.k = a_rows.shape[0], b_rows.shape[0], k
+        self.x = b_rows  # the per-step input is the packed activation matrix
+        self.y = torch.empty((self.m, self.n), dtype=torch.float32, device="cuda")
+        self.algo = _lib.ALGOS[algo] if isinstance(algo, str) else algo
+        self.domain = domain
+        self._alloc_common()
+        self.lib = _lib.load()
+
+    @property
+    def binary_ops(self) -> int:
+        return 2 * self.m * self.n * self.k
+
+    def pack(self, stream=None):
+        pass
+
+    def kernel(self, stream: int | None = None):
+        s = _lib.stream_ptr() if stream is None else stream
+        _lib.check(self.lib.bnn_xnor_gemm(self.a.data_ptr(), self.a.stride(0), self.bw.data_ptr(),
+                                          self.bw.stride(0), self.m, self.n, self.k, 0, 0,
+                                          self.y.data_ptr(), self.n, 1, self.domain, None, None,
+                                          self.algo, s), "xnor_gemm")
+
+    def run_device(self):
+        self.kernel()
+        return self.y

@@ -1,0 +1,162 @@
+"""C-ABI and host-logic tests that run without a GPU.
+
+The library must load and export every symbol include/bnn_b200.h declares;
+argument validation happens before any CUDA call, so the reference's
+ValueError cases can be checked here.
+"""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "bnn_b200.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_1705_09864_b200 import _lib, build
+    if not os.path.exists(_lib.LIB_PATH):
+        build.build()
+    return _lib.load()
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(bnn_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_every_declared_symbol_is_exported(lib):
+    from paper_1705_09864_b200 import _lib
+    syms = declared_symbols()
+    assert len(syms) >= 14
+    raw = ctypes.CDLL(_lib.LIB_PATH)
+    for s in syms:
+        assert hasattr(raw, s), f"{s} not exported"
+        assert s in _lib.SIGNATURES, f"{s} has no ctypes signature"
+
+
+def test_library_is_sm100a_only():
+    from paper_1705_09864_b200 import _lib
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(8\d|90)", out)
+
+
+def test_status_strings(lib):
+    assert lib.bnn_abi_version() == 1
+    assert lib.bnn_status_string(0) == b"ok"
+    assert b"float32" in lib.bnn_status_string(-3)
+
+
+def _gemm(lib, **kw):
+    args = dict(A=1, lda=1, B=1, ldb=1, M=1, N=1, K=1, a_pad=0, b_pad=1, C=1, ldc_m=1, ldc_n=1,
+                domain=0, scale=None, shift=None, algo=0, stream=None)
+    args.update(kw)
+    return lib.bnn_xnor_gemm(*args.values())
+
+
+def test_gemm_validation_mirrors_gemmdims(lib):
+    # GemmDims (gemm.py:170-177): dims >= 1, K < 2^24; pads in {0, 1}
+    for bad in (dict(M=0), dict(N=0), dict(K=0), dict(M=-1)):
+        assert _gemm(lib, **bad) == -2
+    assert b"must be positive" in lib.bnn_last_error()
+    assert _gemm(lib, K=1 << 24, lda=1 << 18, ldb=1 << 18) == -3
+    assert b"exactness" in lib.bnn_last_error()
+    assert _gemm(lib, a_pad=2) == -4
+    assert _gemm(lib, K=130, lda=2) == -5  # lda < ceil(K/64)
+    assert _gemm(lib, domain=7) == -1
+    assert _gemm(lib, algo=99) == -7
+
+
+def test_conv_and_pack_validation(lib):
+    # tensor.conv_output_hw (tensor.py:15-27): kernel must fit, stride >= 1
+    rc = lib.bnn_bconv2d(1, 1, 1, 3, 3, 1, 1, 5, 5, 1, 1, 0, 0, 1, 0, None, None, 0, None)
+    assert rc == -6 and b"does not fit" in lib.bnn_last_error()
+    rc = lib.bnn_bconv2d(1, 1, 1, 3, 3, 1, 1, 2, 2, 0, 1, 0, 0, 1, 0, None, None, 0, None)
+    assert rc == -6
+    assert lib.bnn_pack_rows_f32(1, 1, 4, 4, 1, 1, 2, 0, None, None, None) == -4
+    assert lib.bnn_pack_rows_f32(1, 1, 130, 130, 1, 2, 0, 0, None, None, None) == -5
+    assert lib.bnn_pack_cols_f32(1, 4, 4, 4, 1, 4, 0, 5, None, None) == -1
+    assert lib.bnn_conv_channel_words(64) == 1 and lib.bnn_conv_channel_words(65) == 2
+    assert lib.bnn_audit_padding(1, 1, 70, 1, 1, 3, 1, None) == -4
+
+
+def test_host_gemm_dims_and_workers(monkeypatch):
+    from paper_1705_09864_b200 import gemm
+    d = gemm.GemmDims(2, 3, 65)
+    assert d.words_per_k == 2 and d.binary_ops == 2 * 2 * 3 * 65
+    for bad in ((0, 1, 1), (1, 0, 1), (1, 1, 0), (-1, 2, 2)):
+        with pytest.raises(ValueError):
+            gemm.GemmDims(*bad)
+    with pytest.raises(ValueError):
+        gemm.GemmDims(1, 1, 1 << 24)
+    # resolve_workers precedence (test_gemm.py:62-75)
+    monkeypatch.delenv(gemm.THREADS_ENV_VAR, raising=False)
+    assert gemm.resolve_workers(3) == 3
+    monkeypatch.setenv(gemm.THREADS_ENV_VAR, "5")
+    assert gemm.resolve_workers() == 5 and gemm.resolve_workers(2) == 2
+    monkeypatch.setenv(gemm.THREADS_ENV_VAR, "junk")
+    with pytest.raises(ValueError):
+        gemm.resolve_workers()
+    monkeypatch.setenv(gemm.THREADS_ENV_VAR, "0")
+    with pytest.raises(ValueError):
+        gemm.resolve_workers()
+
+
+def test_host_bitmatrix_validation():
+    from paper_1705_09864_b200.bitpack import BitMatrix, words_per_bits
+    words = np.zeros((2, 1), dtype=np.uint64)
+    with pytest.raises(ValueError):
+        BitMatrix(words, vectors=2, n_bits=10, layout="c", pad_fill=0)
+    with pytest.raises(ValueError):
+        BitMatrix(words, vectors=2, n_bits=10, layout="a", pad_fill=2)
+    with pytest.raises(ValueError):
+        BitMatrix(words, vectors=3, n_bits=10, layout="a", pad_fill=0)
+    with pytest.raises(ValueError):
+        BitMatrix(words.astype(np.int64), vectors=2, n_bits=10, layout="a", pad_fill=0)
+    with pytest.raises(ValueError):
+        BitMatrix(words, vectors=2, n_bits=80, layout="b", pad_fill=1)
+    assert [words_per_bits(n) for n in (0, 1, 63, 64, 65, 128, 129)] == [0, 1, 1, 1, 2, 2, 3]
+
+
+def test_host_csv_schema_and_checksum():
+    from paper_1705_09864_b200 import gemm
+    rec = gemm.BenchRecord("xnor_base", 2, 3, 4, 5, 1000, 10, 99, 1)
+    assert gemm.CSV_HEADER == "kernel,M,N,K,repeats,median_ns,pack_ns,checksum,seed"
+    assert rec.to_csv_row() == "xnor_base,2,3,4,5,1000,10,99,1"
+    text = gemm.records_to_csv([rec, rec])
+    assert text.splitlines()[0] == gemm.CSV_HEADER and text.endswith("\n")
+    dims = gemm.GemmDims(3, 4, 129)
+    a, b = gemm.make_operands(dims, seed=3)
+    dot = a.astype(np.float64) @ b.astype(np.float64)
+    p = (dot + 129) / 2
+    assert gemm.checksum_popcount(p, "xnor_base", dims) == int(p.sum())
+    assert gemm.checksum_popcount(dot, "naive_f32", dims) == int(p.sum())
+
+
+def test_host_layer_constructors():
+    from paper_1705_09864_b200 import layers
+    with pytest.raises(ValueError):
+        layers.QConv2d(3, 4, (3, 3), pad=(1, 1))  # layers.py:178-180
+    q = layers.QConvolution(3, 4, (3, 3), pad=(1, 1))  # BMXNet name accepts pad (G2)
+    assert q.k_reduce == 27 and q.act_bit == q.weight_bit == 1
+    with pytest.raises(ValueError):
+        layers.QDense(4, 5, bits=0)
+    with pytest.raises(ValueError):
+        layers.QFullyConnected(4, 5, act_bit=1, weight_bit=2)
+    rng = np.random.default_rng(0)
+    d = layers.QDense(100, 50, rng=rng)
+    assert np.abs(d.weight).max() <= np.sqrt(6.0 / 150)
+    qd = layers.QDense(8, 3, bits=2)
+    with pytest.raises(layers.ModeError):
+        qd.pack()
+    with pytest.raises(ValueError):
+        layers.QActivation(1).forward(np.zeros(3), "bogus")
+    with pytest.raises(layers.ModeError):
+        layers.QActivation(1).forward(np.zeros(3), layers.TRAIN_FLOAT)

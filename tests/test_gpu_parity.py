@@ -1,0 +1,336 @@
+"""Parity of the CUDA path (through the C ABI) with the reference.
+
+Golden vectors were produced by the unmodified reference in the build
+container (tests/golden/gen_golden_vectors.py); the oracle (oracle/) is the
+pinned CPU restatement used for seeded cases the fixtures do not cover.
+Bar: bit-exact for every binary / integer output.
+"""
+
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import workloads as wl
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+ALGOS = ["popc"]
+
+
+def _sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def bnn():
+    import paper_1705_09864_b200 as p
+    p.load_library()
+    return p
+
+
+@pytest.fixture(scope="module")
+def golden(golden_dir):
+    return {n: np.load(os.path.join(golden_dir, n + ".npz"))
+            for n in ("pack_cases", "gemm40", "conv_cases", "layers", "qmath")}
+
+
+# ------------------------------------------------------------------ bitpack
+def test_frozen_words_and_sign_convention(bnn):
+    # test_bitpack.py:24-43
+    assert list(bnn.pack_row(np.array([1.0, -1.0, 1.0, 1.0]), 0)) == [13]
+    assert list(bnn.pack_row(np.array([1.0, -1.0, 1.0, 1.0]), 1)) == [0xFFFFFFFFFFFFFFF0 | 13]
+    x = np.array([-0.5, 0.0, -0.0, 2.0, -3.0], np.float32)
+    assert list(bnn.binarize(x)) == [-1.0, 1.0, 1.0, 1.0, -1.0]
+    for bad in (np.nan, np.inf, -np.inf):
+        with pytest.raises(ValueError):
+            bnn.binarize(np.array([1.0, bad], np.float32))
+    with pytest.raises(ValueError):
+        bnn.pack_row(np.array([1.0, 0.0]))
+    with pytest.raises(ValueError):
+        bnn.pack_matrix_a(np.array([[2.0, 1.0]]))
+    with pytest.raises(ValueError):
+        bnn.pack_matrix_b(np.zeros((3, 3)))
+    with pytest.raises(ValueError):
+        bnn.pack_matrix_a(np.ones(4))
+
+
+def test_pack_cases_bit_exact(bnn, golden):
+    g = golden["pack_cases"]
+    i = 0
+    while f"x{i}" in g:
+        s = g[f"signs{i}"]
+        assert np.array_equal(bnn.binarize(g[f"x{i}"]), s)
+        a = bnn.pack_matrix_a(s)
+        assert np.array_equal(a.words.cpu().numpy(), g[f"a{i}"])
+        b = bnn.pack_matrix_b(np.ascontiguousarray(s.T))
+        assert np.array_equal(b.words.cpu().numpy(), g[f"b{i}"])
+        assert np.array_equal(a.unpack(), s) and np.array_equal(b.unpack(), s.T)
+        # fused sign+pack of the raw floats == pack(binarize(x))
+        xw = bnn.pack_rows_device(torch.from_numpy(g[f"x{i}"]).cuda(), 0)
+        assert np.array_equal(xw.cpu().numpy(), g[f"a{i}"])
+        bnn.audit_padding(a)
+        bnn.audit_padding(b)
+        # transposed layouts agree up to the tail fill
+        a1 = bnn.pack_rows_device(torch.from_numpy(s).cuda(), 1)
+        assert np.array_equal(bnn.words_transpose(a1).cpu().numpy(), g[f"b{i}"])
+        i += 1
+
+
+def test_audit_padding_catches_corruption(bnn):
+    rng = np.random.default_rng(6)
+    a = bnn.pack_matrix_a(wl.random_signs(rng, (4, 70)))
+    bnn.audit_padding(a)
+    a.words[2, -1] |= torch.tensor(1 << 6, dtype=torch.uint64, device="cuda")
+    with pytest.raises(ValueError):
+        bnn.audit_padding(a)
+    b = bnn.pack_matrix_b(wl.random_signs(rng, (70, 4)))
+    bnn.audit_padding(b)
+    w = b.words.cpu().numpy()
+    w[-1, 1] &= ~np.uint64(1 << 63)
+    with pytest.raises(ValueError):
+        bnn.audit_padding(bnn.BitMatrix(w, 4, 70, "b", 1))
+
+
+def test_pack_nonfinite_and_strict_flags(bnn):
+    x = torch.randn(5, 200, device="cuda")
+    x[3, 150] = float("nan")
+    flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+    bnn.pack_rows_device(x, 0, flags=flags)
+    assert int(flags.item()) & 1
+    xs = torch.where(torch.randn(3, 4, 5, 6, device="cuda") >= 0, 1.0, -1.0)
+    flags.zero_()
+    bnn.pack_nchw(xs, strict=True, flags=flags)
+    assert int(flags.item()) == 0
+    xs[1, 2, 3, 4] = 0.5
+    bnn.pack_nchw(xs, strict=True, flags=flags)
+    assert int(flags.item()) & 2
+
+
+def test_pack_nchw_matches_oracle(bnn):
+    rng = np.random.default_rng(3)
+    for b, c, h, w in ((2, 3, 5, 7), (1, 64, 4, 4), (2, 130, 3, 5), (1, 256, 28, 28)):
+        x = rng.standard_normal((b, c, h, w)).astype(np.float32)
+        x.reshape(-1)[::13] = 0.0
+        got = bnn.pack_nchw(torch.from_numpy(x).cuda()).cpu().numpy()
+        nhwc = np.ascontiguousarray(x.transpose(0, 2, 3, 1)).reshape(-1, c)
+        expect = orc.binarize_pack_rows(nhwc, 0)
+        assert np.array_equal(got.reshape(-1, got.shape[-1]), expect)
+
+
+# ------------------------------------------------------------------ gemm
+@pytest.mark.parametrize("algo", ALGOS)
+def test_gemm40_bit_exact(bnn, golden, algo):
+    g = golden["gemm40"]
+    for i, (m, n, k, seed) in enumerate(wl.gemm40_cases()):
+        a = bnn.BitMatrix(g[f"a{i}"], m, k, "a", 0)
+        b = bnn.BitMatrix(g[f"b{i}"], n, k, "b", 1)
+        c = bnn.xnor_gemm_b200(a, b, algo=algo).cpu().numpy()
+        assert c.dtype == np.float32
+        assert np.array_equal(c, g[f"c{i}"]), (m, n, k)
+
+
+def test_reference_kernel_ids_and_checksums(bnn):
+    dims = bnn.GemmDims(8, 9, 200)
+    recs = [bnn.benchmark_kernel(k, dims, repeats=2, warmup=1, seed=7) for k in bnn.KERNEL_IDS]
+    assert len({r.checksum for r in recs}) == 1
+    a, b = bnn.gemm.make_operands(bnn.GemmDims(37, 19, 257), 9)
+    ref = bnn.run_kernel("xnor_base", a, b)
+    for kid in bnn.KERNEL_IDS[1:]:
+        assert np.array_equal(bnn.run_kernel(kid, a, b), ref)
+    with pytest.raises(ValueError):
+        bnn.run_kernel("turbo", a, b)
+
+
+def test_operand_validation(bnn):
+    a, b = bnn.gemm.make_operands(bnn.GemmDims(4, 5, 70), 2)
+    abm, bbm = bnn.pack_matrix_a(a), bnn.pack_matrix_b(b)
+    with pytest.raises(ValueError):
+        bnn.xnor_gemm_base(bbm, bbm)
+    with pytest.raises(ValueError):
+        bnn.xnor_gemm_base(abm, abm)
+    short = bnn.pack_matrix_b(bnn.gemm.make_operands(bnn.GemmDims(4, 5, 64), 2)[1])
+    with pytest.raises(ValueError):
+        bnn.xnor_gemm_base(abm, short)
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_sweep504_bit_exact(bnn, golden_dir, algo):
+    rows = json.load(open(os.path.join(golden_dir, "sweep504.json")))
+    got = []
+    for m, n, k, a, b in wl.sweep504():
+        abm, bbm = bnn.pack_matrix_a(a), bnn.pack_matrix_b(b)
+        c = bnn.xnor_gemm_b200(abm, bbm, algo=algo).cpu().numpy()
+        got.append([m, n, k, _sha(c), int(c.astype(np.int64).sum())])
+    assert got == rows
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_gemm_tail_and_layout_variants(bnn, algo):
+    """Row-row operands, every pad combination, both domains, odd ld, transposed out."""
+    rng = np.random.default_rng(5)
+    for m, n, k in ((1, 1, 1), (3, 5, 63), (17, 33, 65), (130, 70, 1000), (64, 257, 4096),
+                    (300, 129, 2049)):
+        a = wl.random_signs(rng, (m, k))
+        b = wl.random_signs(rng, (n, k))
+        p = (a.astype(np.int64) == 1)[:, None, :] == (b.astype(np.int64) == 1)[None, :, :] \
+            if m * n * k < 3e6 else None
+        expect = p.sum(-1) if p is not None else (
+            k - orc.xor_popc_rowrow(orc.pack_rows(a, 0), orc.pack_rows(b, 0)))
+        for ap in (0, 1):
+            for bp in (0, 1):
+                aw = torch.from_numpy(orc.pack_rows(a, ap).view(np.uint64)).cuda()
+                bw = torch.from_numpy(orc.pack_rows(b, bp)).cuda()
+                c = bnn.xnor_rows_gemm(aw, bw, k, a_pad=ap, b_pad=bp, algo=algo)
+                assert np.array_equal(c.cpu().numpy(), expect.astype(np.float32)), (m, n, k, ap, bp)
+        # odd leading dimension (8-byte aligned rows), dot domain, [N, M] output
+        W = (k + 63) // 64
+        aw = torch.zeros((m, W + 1), dtype=torch.uint64, device="cuda")
+        aw[:, :W] = torch.from_numpy(orc.pack_rows(a, 0)).cuda()
+        bw = torch.from_numpy(orc.pack_rows(b, 0)).cuda()
+        c = bnn.xnor_rows_gemm(aw[:, :W], bw, k, domain=1, transpose_out=True, algo=algo)
+        assert np.array_equal(c.cpu().numpy(), (2 * expect - k).T.astype(np.float32))
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_gemm_epilogue_scale_shift(bnn, algo):
+    rng = np.random.default_rng(8)
+    m, n, k = 40, 50, 300
+    a, b = wl.random_signs(rng, (m, k)), wl.random_signs(rng, (n, k))
+    aw, bw = (torch.from_numpy(orc.pack_rows(x, 0)).cuda() for x in (a, b))
+    sc = torch.from_numpy(rng.standard_normal(m).astype(np.float32)).cuda()
+    sh = torch.from_numpy(rng.standard_normal(m).astype(np.float32)).cuda()
+    c = bnn.xnor_rows_gemm(aw, bw, k, scale=sc, shift=sh, algo=algo).cpu().numpy()
+    p = (k - orc.xor_popc_rowrow(orc.pack_rows(a, 0), orc.pack_rows(b, 0))).astype(np.float32)
+    expect = p * sc.cpu().numpy()[:, None] + sh.cpu().numpy()[:, None]
+    assert np.array_equal(c, expect.astype(np.float32))
+
+
+# ------------------------------------------------------------------ conv
+@pytest.mark.parametrize("algo", ALGOS)
+def test_conv_cases_bit_exact(bnn, golden, algo):
+    g = golden["conv_cases"]
+    for i, case in enumerate(wl.CONV_CASES):
+        b, c, h, w, f, kh, kw, stride, pad, seed = case
+        x, wt = wl.conv_case_inputs(case)
+        layer = bnn.QConvolution(c, f, (kh, kw), stride, pad)
+        layer.weight = wt
+        layer.pack()
+        layer.algo = algo
+        y = layer.forward(torch.from_numpy(x).cuda(), bnn.INFER_PACKED).cpu().numpy()
+        assert np.array_equal(y, g[f"y{i}"]), case
+        # the float path of the same layer agrees exactly (layers.py:237-244)
+        yf = layer.forward(torch.from_numpy(x).cuda(), bnn.INFER_FLOAT).cpu().numpy()
+        assert np.array_equal(yf, g[f"y{i}"]), case
+
+
+def test_reference_layers_bit_exact(bnn, golden):
+    g = golden["layers"]
+    qd = bnn.QDense(130, 17, bits=1)
+    qd.weight = g["qdense_w"]
+    assert np.array_equal(qd.forward(g["qdense_x"], bnn.INFER_FLOAT), g["qdense_y_float"])
+    qd.pack()
+    assert np.array_equal(qd.packed.words.cpu().numpy(), g["qdense_words"])
+    y = qd.forward(g["qdense_x"], bnn.INFER_PACKED)
+    assert isinstance(y, np.ndarray) and np.array_equal(y, g["qdense_y_packed"])
+    qc = bnn.QConv2d(3, 5, (3, 3), bits=1)
+    qc.weight = g["qconv_w"]
+    qc.pack()
+    assert np.array_equal(qc.packed.words.cpu().numpy(), g["qconv_words"])
+    assert np.array_equal(qc.forward(g["qconv_x"], bnn.INFER_PACKED), g["qconv_y_packed"])
+    assert np.array_equal(qc.forward(g["qconv_x"], bnn.INFER_FLOAT), g["qconv_y_float"])
+    # packed layer refuses non-sign inputs like pack_matrix_b (bitpack.py:69-75)
+    with pytest.raises(ValueError):
+        qc.forward(g["qconv_x"] * 0.5, bnn.INFER_PACKED)
+    assert np.array_equal(bnn.QActivation(1).forward(g["qact_x"], bnn.INFER_PACKED), g["qact_y1"])
+    assert np.array_equal(bnn.QActivation(2).forward(g["qact_x"], bnn.INFER_FLOAT), g["qact_y2"])
+    with pytest.raises(ValueError):
+        bnn.QActivation(1).forward(np.array([np.nan], np.float32), bnn.INFER_PACKED)
+    # mode errors (layers.py:217-220, 232-239)
+    q2 = bnn.QDense(8, 3, bits=2, rng=np.random.default_rng(1))
+    with pytest.raises(bnn.ModeError):
+        q2.forward(np.ones((2, 8), np.float32), bnn.INFER_PACKED)
+    with pytest.raises(bnn.ModeError):
+        bnn.QDense(8, 3, rng=np.random.default_rng(1)).forward(np.ones((2, 8)), bnn.INFER_PACKED)
+
+
+def test_qmath_bit_exact(bnn, golden):
+    g = golden["qmath"]
+    assert np.array_equal(bnn.quantize(g["x"], 2), g["q2"])
+    assert np.array_equal(bnn.quantize_signed(g["xs"], 2), g["qs2"])
+    assert np.array_equal(bnn.quantize_signed(g["xs"], 1), g["qs1"])
+
+
+# ------------------------------------------------------------------ BASELINE configs
+@pytest.mark.parametrize("algo", ALGOS)
+def test_config1_qfc_golden(bnn, golden_dir, algo):
+    cfg = json.load(open(os.path.join(golden_dir, "configs.json")))["c1"]
+    a, w = wl.config1_inputs()
+    layer = bnn.QFullyConnected(4096, 1024, domain="dot")
+    layer.weight = w
+    layer.pack()
+    layer.algo = algo
+    y = layer.forward(torch.from_numpy(a).cuda(), bnn.INFER_PACKED).cpu().numpy()
+    assert list(y.shape) == cfg["shape"]
+    assert _sha(y) == cfg["sha256"]
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_config2_qconv_golden(bnn, golden_dir, algo):
+    cfg = json.load(open(os.path.join(golden_dir, "configs.json")))["c2"]
+    x, wt = wl.config2_inputs()
+    c = wl.C2
+    layer = bnn.QConvolution(c["c"], c["f"], (c["kh"], c["kw"]), c["stride"], c["pad"])
+    layer.weight = wt
+    layer.pack()
+    layer.algo = algo
+    y = layer.forward(torch.from_numpy(x).cuda(), bnn.INFER_PACKED).cpu().numpy()
+    assert list(y.shape) == cfg["shape"]
+    assert _sha(y) == cfg["sha256"]
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("mnk", [(4096, 4096, 4096), (4096, 4096, 65536), (8192, 8192, 8192)])
+def test_large_gemm_properties(bnn, algo, mnk):
+    """Full-size C5 shapes: exact row/column checksums + sampled exact entries.
+
+    sum_n P[m, n] = sum_k (a_mk ? ones_k : N - ones_k) with ones_k = #{n : b_nk = 1}
+    is O((M + N) K) on the CPU, so it checks every output row at any size.
+    """
+    m, n, k = mnk
+    g = torch.Generator(device="cuda").manual_seed(m + n + k)
+    W = k // 64
+    aw = torch.randint(-2**63, 2**63 - 1, (m, W), device="cuda", generator=g).view(torch.uint64)
+    bw = torch.randint(-2**63, 2**63 - 1, (n, W), device="cuda", generator=g).view(torch.uint64)
+    c = bnn.xnor_rows_gemm(aw, bw, k, algo=algo)
+    assert float(c.min()) >= 0 and float(c.max()) <= k
+    a_np, b_np = aw.cpu().numpy(), bw.cpu().numpy()
+
+    def bits(x, lo, hi):
+        return np.unpackbits(x[lo:hi].view(np.uint8), axis=1, bitorder="little")
+
+    def side_sums(x, other, n_other):
+        # sum over the other operand of agreement = sum_k (n - ones_k) + x_k (2 ones_k - n)
+        ones = np.zeros(k, np.int64)
+        for lo in range(0, other.shape[0], 1024):
+            ones += bits(other, lo, lo + 1024).sum(0, dtype=np.int64)
+        coef = (2 * ones - n_other).astype(np.float64)
+        out = []
+        for lo in range(0, x.shape[0], 1024):
+            out.append(bits(x, lo, lo + 1024).astype(np.float64) @ coef)
+        return (np.concatenate(out) + float((n_other - ones).sum())).astype(np.int64)
+
+    row_got = c.to(torch.float64).sum(1).cpu().numpy().astype(np.int64)
+    assert np.array_equal(row_got, side_sums(a_np, b_np, n))
+    col_got = c.to(torch.float64).sum(0).cpu().numpy().astype(np.int64)
+    assert np.array_equal(col_got, side_sums(b_np, a_np, m))
+    rng = np.random.default_rng(0)
+    idx_m, idx_n = rng.integers(0, m, 64), rng.integers(0, n, 64)
+    cs = c.cpu().numpy()
+    for i, j in zip(idx_m, idx_n):
+        x = int(np.bitwise_count(a_np[i] ^ b_np[j]).sum())
+        assert cs[i, j] == k - x
