@@ -42,6 +42,12 @@ int launch_conv_weights_reorder(const uint64_t *, int64_t, int64_t, int64_t, int
 int launch_xnor_gemm_popc(const uint64_t *, int64_t, const uint64_t *, int64_t, int64_t,
                           int64_t, int64_t, float *, int64_t, int64_t, const Epilogue &,
                           cudaStream_t);
+int launch_xnor_gemm_umma(const uint64_t *, int64_t, const uint64_t *, int64_t, int64_t,
+                          int64_t, int64_t, float *, int64_t, int64_t, const Epilogue &,
+                          cudaStream_t);
+int launch_bconv2d_umma(const uint64_t *, int64_t, int64_t, int64_t, int64_t, const uint64_t *,
+                        int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,
+                        int64_t, float *, const Epilogue &, cudaStream_t);
 int launch_bconv2d_popc(const uint64_t *, int64_t, int64_t, int64_t, int64_t, const uint64_t *,
                         int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,
                         int64_t, float *, const Epilogue &, cudaStream_t);
@@ -168,9 +174,12 @@ int bnn_xnor_gemm(const uint64_t *A, int64_t lda, const uint64_t *B, int64_t ldb
     const int64_t tail = (64 * W - K) * (int64_t)(a_pad ^ b_pad);
     Epilogue ep{(int32_t)(K + tail), (int32_t)K, domain, scale, shift};
     switch (algo) {
-        case BNN_ALGO_AUTO:
         case BNN_ALGO_POPC:
             return launch_xnor_gemm_popc(A, lda, B, ldb, M, N, K, C, ldc_m, ldc_n, ep,
+                                         as_stream(stream));
+        case BNN_ALGO_AUTO:
+        case BNN_ALGO_UMMA:
+            return launch_xnor_gemm_umma(A, lda, B, ldb, M, N, K, C, ldc_m, ldc_n, ep,
                                          as_stream(stream));
         default:
             return set_error(BNN_EUNSUP, "algorithm %d not available", algo);
@@ -207,9 +216,12 @@ int bnn_bconv2d(const uint64_t *x_words, int64_t B, int64_t C, int64_t H, int64_
     BNN_REQUIRE(H * W * bnn_conv_channel_words(C) < (1ll << 31), BNN_EUNSUP, "image too large");
     Epilogue ep{(int32_t)K, (int32_t)K, domain, scale, shift};  // all tails are 0
     switch (algo) {
-        case BNN_ALGO_AUTO:
         case BNN_ALGO_POPC:
             return launch_bconv2d_popc(x_words, B, C, H, W, w_dev, F, kh, kw, sh, sw, ph, pw, oh,
+                                       ow, y, ep, as_stream(stream));
+        case BNN_ALGO_AUTO:
+        case BNN_ALGO_UMMA:
+            return launch_bconv2d_umma(x_words, B, C, H, W, w_dev, F, kh, kw, sh, sw, ph, pw, oh,
                                        ow, y, ep, as_stream(stream));
         default:
             return set_error(BNN_EUNSUP, "algorithm %d not available", algo);

@@ -13,127 +13,11 @@
 // 8 distinct rows a warp touches per LDS.128 land in 8 distinct bank quads.
 // Each thread owns a TM x TN register tile; lane (lm, ln) = (lane & 7,
 // lane >> 3) takes rows lm + 8i and columns ln + 4j of its warp tile.
-#include "bnn_common.cuh"
+#include "bnn_loaders.cuh"
 
 namespace bnn {
 
 constexpr int kBKWords = 32;  // u32 words per K slice (1024 bits = 128 B per row)
-
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-template <int kBytes>
-__device__ __forceinline__ void cp_async(uint32_t dst, const void *src, int src_bytes) {
-    if constexpr (kBytes == 16)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src),
-                     "r"(src_bytes));
-    else
-        asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(dst), "l"(src),
-                     "n"(kBytes), "r"(src_bytes));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
-
-// byte offset of piece p (of kVec words) of row r inside a [rows][32-word] tile
-template <int kVec>
-__device__ __forceinline__ uint32_t tile_off(int r, int p) {
-    const int byte = p * kVec * 4;  // logical byte within the 128-B row
-    const int c16 = byte >> 4;
-    return (uint32_t)(r * 128 + ((c16 ^ (r & 7)) << 4) + (byte & 15));
-}
-
-// ------------------------------------------------------------------ loaders
-// Dense operand: row r of a [rows, ld32] u32 matrix, kw32 valid words.
-struct DenseRows {
-    const uint32_t *base;
-    int64_t ld32;
-    int64_t rows;
-    int64_t kw32;
-    struct Cursor { const uint32_t *p; bool ok; };
-    __device__ Cursor row(int64_t r) const { return {base + r * ld32, r < rows}; }
-    // load kVec words at word w of this row into smem address dst
-    template <int kVec>
-    __device__ void load(const Cursor &c, int64_t w, uint32_t dst) const {
-        int64_t left = kw32 - w;
-        int bytes = (!c.ok || left <= 0) ? 0 : (int)(left >= kVec ? kVec * 4 : left * 4);
-        const uint32_t *src = bytes ? c.p + w : base;
-        cp_async<kVec * 4>(dst, src, bytes);
-    }
-};
-
-// Implicit im2col rows: row n = output pixel (b, oy, ox); word w = tap-major
-// (i, j, channel word).  Out-of-image taps read the constant "+1" word
-// (valid channel bits set, channel tail 0), the reference's zero-pad-then-
-// binarize composition (tensor.py:73-74 + bitpack.py:39).
-struct ConvRows {
-    const uint32_t *x;  // NHWC words, pixel stride cs32
-    int64_t npix;       // B * oh * ow
-    int H, W, cs32, C, kw, sh, sw, ph, pw, oh, ow;
-    int64_t kw32;       // kh * kw * cs32
-    struct Cursor { const uint32_t *img; int iy0, ix0; bool ok; };
-    __device__ Cursor row(int64_t n) const {
-        Cursor c;
-        c.ok = n < npix;
-        int64_t nn = c.ok ? n : 0;
-        int64_t ohw = (int64_t)oh * ow;
-        int64_t b = nn / ohw;
-        int pix = (int)(nn - b * ohw);
-        int oy = pix / ow, ox = pix - (pix / ow) * ow;
-        c.img = x + b * (int64_t)H * W * cs32;
-        c.iy0 = oy * sh - ph;
-        c.ix0 = ox * sw - pw;
-        return c;
-    }
-    template <int kVec>
-    __device__ void load(const Cursor &c, int64_t w, uint32_t dst) const {
-        if (!c.ok || w >= kw32) {
-            cp_async<kVec * 4>(dst, x, 0);
-            return;
-        }
-        int tap = (int)(w / cs32);
-        int cw = (int)(w - (int64_t)tap * cs32);
-        int i = tap / kw, j = tap - (tap / kw) * kw;
-        int iy = c.iy0 + i, ix = c.ix0 + j;
-        if (iy >= 0 && iy < H && ix >= 0 && ix < W) {
-            cp_async<kVec * 4>(dst, c.img + ((int64_t)iy * W + ix) * cs32 + cw, kVec * 4);
-        } else {
-            uint32_t v[kVec];
-#pragma unroll
-            for (int q = 0; q < kVec; ++q) {
-                int valid = C - 32 * (cw + q);
-                v[q] = valid >= 32 ? 0xffffffffu : (valid <= 0 ? 0u : ((1u << valid) - 1u));
-            }
-            if constexpr (kVec == 4)
-                asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};\n" ::"r"(dst), "r"(v[0]),
-                             "r"(v[1]), "r"(v[2]), "r"(v[3]));
-            else
-                asm volatile("st.shared.v2.u32 [%0], {%1, %2};\n" ::"r"(dst), "r"(v[0]),
-                             "r"(v[1]));
-        }
-    }
-};
-
-// ------------------------------------------------------------------ stores
-struct GemmStore {
-    float *C;
-    int64_t ldc_m, ldc_n, M, N;
-    __device__ bool ok(int64_t m, int64_t n) const { return m < M && n < N; }
-    __device__ void put(int64_t m, int64_t n, float v) const { C[m * ldc_m + n * ldc_n] = v; }
-};
-
-struct ConvStore {  // y NCHW [B, F, oh*ow]; m = filter, n = b*ohw + pixel
-    float *y;
-    int64_t F, ohw, npix;
-    __device__ bool ok(int64_t m, int64_t n) const { return m < F && n < npix; }
-    __device__ void put(int64_t m, int64_t n, float v) const {
-        int64_t b = n / ohw, p = n - b * ohw;
-        y[(b * F + m) * ohw + p] = v;
-    }
-};
 
 // ------------------------------------------------------------------ kernel
 template <int TM, int TN, int WARPS_M, int WARPS_N, int STAGES, int kVec, class ALoad,

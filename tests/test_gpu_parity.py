@@ -19,7 +19,7 @@ from oracle import oracle as orc
 
 pytestmark = pytest.mark.gpu
 
-ALGOS = ["popc"]
+ALGOS = ["popc", "umma"]
 
 
 def _sha(a):
@@ -85,7 +85,7 @@ def test_audit_padding_catches_corruption(bnn):
     rng = np.random.default_rng(6)
     a = bnn.pack_matrix_a(wl.random_signs(rng, (4, 70)))
     bnn.audit_padding(a)
-    a.words[2, -1] |= torch.tensor(1 << 6, dtype=torch.uint64, device="cuda")
+    a.words.view(torch.int64)[2, -1] |= 1 << 6
     with pytest.raises(ValueError):
         bnn.audit_padding(a)
     b = bnn.pack_matrix_b(wl.random_signs(rng, (70, 4)))
