@@ -264,20 +264,50 @@ def load_traffic(name, algo):
         return None
 
 
-def pipe_peak(plan):
-    """Roofline denominator for the dominant kernel (measured on this GPU)."""
+def popc_peak_tops():
+    """Measured POPC issue rate x 64 binary ops (bnn_probe_pipe_peak)."""
+    import ctypes
+
     import torch
     from paper_1705_09864_b200 import _lib
     lib = _lib.load()
-    import ctypes
     sink = torch.zeros(1, dtype=torch.int32, device="cuda")
     rate = ctypes.c_double(0)
     _lib.check(lib.bnn_probe_pipe_peak(0, 4096, sink.data_ptr(), ctypes.byref(rate),
                                        _lib.stream_ptr()), "probe")
-    popc_per_s = rate.value
-    return {"bound": "popc", "peak": popc_per_s * 64 / 1e12, "unit": "TOPS",
+    return rate.value * 64 / 1e12
+
+
+def int8_tensor_peak_tops(n=8192, reps=10):
+    """Measured dense int8 tensor-core rate: cuBLASLt via torch._int_mm, best of reps."""
+    import torch
+    a = torch.randint(-128, 127, (n, n), dtype=torch.int8, device="cuda")
+    b = torch.randint(-128, 127, (n, n), dtype=torch.int8, device="cuda")
+    for _ in range(3):
+        torch._int_mm(a, b)
+    best = float("inf")
+    for _ in range(reps):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        torch._int_mm(a, b)
+        e.record()
+        e.synchronize()
+        best = min(best, s.elapsed_time(e))
+    del a, b
+    return 2 * n ** 3 / (best * 1e-3) / 1e12
+
+
+def pipe_peak(algo):
+    """Roofline denominator for the engine that ran (both measured on this GPU)."""
+    popc = popc_peak_tops()
+    if algo in ("auto", "umma"):
+        return {"bound": "tensor", "peak": int8_tensor_peak_tops(), "unit": "TOPS",
+                "peak_source": "measured: dense int8 tensor-core GEMM 8192^3 (cuBLASLt via "
+                               "torch._int_mm), best of 10; the engine is tcgen05 kind::i8",
+                "popc_peak": popc}
+    return {"bound": "popc", "peak": popc, "unit": "TOPS",
             "peak_source": "measured: bnn_probe_pipe_peak POPC rate x 64 binary ops "
-                           "(32 bits x {xor, add})"}
+                           "(32 bits x {xor, add})", "popc_peak": popc}
 
 
 def run_gpu_arm(args, rank, world, local_rank):
@@ -353,14 +383,14 @@ def run_gpu_arm(args, rank, world, local_rank):
                "ms_per_step": e2e_ms / args.steps,
                "path": "plan.run_host: pinned H2D -> pack -> kernel -> D2H -> sync"}
 
-    peak = pipe_peak(plan)
+    peak = pipe_peak(args.algo)
     kern_avg = statistics.mean(kern_ms)
     achieved = ops / (kern_avg * 1e-3) / 1e12
     roof = {"bound": peak["bound"], "achieved": achieved, "peak": peak["peak"],
             "unit": peak["unit"], "frac": achieved / peak["peak"],
             "traffic": load_traffic(args.workload, args.algo), "kernel_ms": kern_avg,
             "pack_ms": statistics.mean(pack_ms), "peak_source": peak["peak_source"],
-            "ops_per_launch": ops}
+            "ops_per_launch": ops, "popc_pipe_peak_tops": peak["popc_peak"]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -370,7 +400,9 @@ def run_gpu_arm(args, rank, world, local_rank):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u8 (bits expanded in SMEM, s32 accumulate)" if args.algo in ("auto", "umma")
+            else "u32 (xor/popc words)",
             "data": "synthetic (seeded, BASELINE.json shapes)",
             "config": {"workload": d["workload"], "M": d["M"], "N": d["N"], "K": d["K"],
                        "batch_per_gpu": d["batch"], "parallelism": f"replicas x{world}",

@@ -174,13 +174,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ------------------------------------------------------------ producer
         const bool is_a = tid < BM;
         const int row = is_a ? tid : tid - BM;
-        const uint32_t ring = s_pk + tid * (PD * 16);
+        // private packed ring, slot-major so a warp's 16-byte slots are contiguous
+        const uint32_t ring = s_pk + tid * 16;
         typename ALoad::Cursor ca{};
         typename BLoad::Cursor cb{};
         if (is_a) ca = aload.row(m0 + row);
         else cb = bload.row(n0 + row);
         auto fetch = [&](int64_t kt) {
-            const uint32_t dst = ring + (uint32_t)(kt % PD) * 16;
+            const uint32_t dst = ring + (uint32_t)(kt % PD) * (kProducers * 16);
 #pragma unroll
             for (int p = 0; p < kWordsPerStage / kVec; ++p) {
                 const int64_t w = kt * kWordsPerStage + p * kVec;
@@ -200,7 +201,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t wv[4];
             asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n"
                          : "=r"(wv[0]), "=r"(wv[1]), "=r"(wv[2]), "=r"(wv[3])
-                         : "r"(ring + (uint32_t)(kt % PD) * 16));
+                         : "r"(ring + (uint32_t)(kt % PD) * (kProducers * 16)));
             const int s = (int)(kt % ES);
             if (kt >= ES) mbar_wait(bar_empty + 8 * s, (uint32_t)((kt / ES) - 1) & 1u);
             const uint32_t row_base = s_exp + s * kStageBytes + (is_a ? 0 : kStageA) + row * kRowBytes;

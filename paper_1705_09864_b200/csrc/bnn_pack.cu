@@ -123,34 +123,48 @@ __global__ void pack_cols_kernel(const float *__restrict__ x, int64_t K, int64_t
 
 // ---------------------------------------------------------------- pack NCHW
 // x [B, C, H, W] -> out [B*H*W, Cw] u64 (NHWC words, channel tail 0).
-// Thread per (pixel, channel word); a warp covers 32 consecutive pixels of
-// one (b, cw) so every load instruction reads 128 contiguous bytes.
+// Thread per (4 consecutive pixels, channel word): 64 float4 loads along C,
+// so a warp reads 512 contiguous bytes per instruction (HW % 4 == 0) and
+// keeps 16 of them in flight.
+template <bool kVec4>
 __global__ void pack_nchw_kernel(const float *__restrict__ x, int64_t B, int64_t C, int64_t HW,
                                  int64_t Cw, uint64_t *__restrict__ out, int mode,
                                  int32_t *flags) {
-    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t p0 = 4 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
     const int64_t cw = blockIdx.y;
     const int64_t b = blockIdx.z;
     int f = 0;
-    if (p < HW) {
-        const float *src = x + (b * C + cw * 64) * HW + p;
+    if (p0 < HW) {
+        const float *src = x + (b * C + cw * 64) * HW + p0;
         const int nc = (int)(C - cw * 64 < 64 ? C - cw * 64 : 64);
-        uint64_t word = 0;
-        if (nc == 64) {
+        const int np = (int)(HW - p0 < 4 ? HW - p0 : 4);
+        uint64_t w[4] = {0, 0, 0, 0};
+        if (kVec4 && nc == 64) {
 #pragma unroll 16
             for (int i = 0; i < 64; ++i) {
-                float v = __ldg(src + (int64_t)i * HW);
-                f |= elem_flags(v, mode);
-                word |= (uint64_t)sign_bit(v) << i;
+                const float4 v = __ldg(reinterpret_cast<const float4 *>(src + (int64_t)i * HW));
+                f |= elem_flags(v.x, mode) | elem_flags(v.y, mode) | elem_flags(v.z, mode) |
+                     elem_flags(v.w, mode);
+                w[0] |= (uint64_t)sign_bit(v.x) << i;
+                w[1] |= (uint64_t)sign_bit(v.y) << i;
+                w[2] |= (uint64_t)sign_bit(v.z) << i;
+                w[3] |= (uint64_t)sign_bit(v.w) << i;
             }
         } else {
             for (int i = 0; i < nc; ++i) {
-                float v = __ldg(src + (int64_t)i * HW);
-                f |= elem_flags(v, mode);
-                word |= (uint64_t)sign_bit(v) << i;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    if (j < np) {
+                        const float v = __ldg(src + (int64_t)i * HW + j);
+                        f |= elem_flags(v, mode);
+                        w[j] |= (uint64_t)sign_bit(v) << i;
+                    }
+                }
             }
         }
-        out[(b * HW + p) * Cw + cw] = word;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (j < np) out[(b * HW + p0 + j) * Cw + cw] = w[j];
     }
     flush_flags(f, flags);
 }
@@ -241,8 +255,12 @@ int launch_pack_nchw(const float *x, int64_t B, int64_t C, int64_t H, int64_t W,
                      int mode, int32_t *flags, cudaStream_t s) {
     const int64_t HW = H * W, Cw = ceil_div(C, 64);
     if (B == 0 || HW == 0 || C == 0) return BNN_OK;
-    dim3 grid((unsigned)ceil_div(HW, 128), (unsigned)Cw, (unsigned)B);
-    pack_nchw_kernel<<<grid, 128, 0, s>>>(x, B, C, HW, Cw, out, mode, flags);
+    dim3 grid((unsigned)ceil_div(HW, 4 * 128), (unsigned)Cw, (unsigned)B);
+    const bool vec4 = (HW % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+    if (vec4)
+        pack_nchw_kernel<true><<<grid, 128, 0, s>>>(x, B, C, HW, Cw, out, mode, flags);
+    else
+        pack_nchw_kernel<false><<<grid, 128, 0, s>>>(x, B, C, HW, Cw, out, mode, flags);
     return check_launch("pack_nchw_kernel");
 }
 

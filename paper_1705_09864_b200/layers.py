@@ -65,12 +65,18 @@ def _float_matmul(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
 
 
 def _float_conv(x, w, stride):
-    prev = torch.backends.cudnn.allow_tf32
-    torch.backends.cudnn.allow_tf32 = False
-    try:
-        return F.conv2d(x, w, stride=stride)
-    finally:
-        torch.backends.cudnn.allow_tf32 = prev
+    """im2col (unfold, rows (c, i, j) like tensor.im2col) + f32 matmul, TF32 off.
+
+    Exact for +-1 operands (integer sums < 2^24); cuDNN's Winograd/FFT
+    algorithms would round.  This is the reference float path (layers.py:240-242).
+    """
+    b = x.shape[0]
+    f, c, kh, kw = w.shape
+    oh = (x.shape[2] - kh) // stride[0] + 1
+    ow = (x.shape[3] - kw) // stride[1] + 1
+    cols = F.unfold(x, (kh, kw), stride=stride)  # [B, C*kh*kw, oh*ow]
+    out = _float_matmul(w.reshape(f, -1), cols)  # [B, F, oh*ow]
+    return out.reshape(b, f, oh, ow)
 
 
 class QActivation:
