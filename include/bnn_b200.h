@@ -153,6 +153,11 @@ int bnn_bconv2d(const uint64_t *x_words, int64_t B, int64_t C, int64_t H, int64_
                 int64_t ph, int64_t pw, float *y, int domain, const float *scale,
                 const float *shift, int algo, bnn_stream_t stream);
 
+/* Select the tcgen05 engine variant (process-wide tuning knob, default 1):
+ * 0 = 128x256 tiles, both expanded operands in SMEM; 1 = 128x192 tiles,
+ * expanded weights in TMEM (only activations cross SMEM). */
+int bnn_set_umma_variant(int variant);
+
 /* Roofline probe (synchronous): measured issue rate of a pipe on the
  * current device.  pipe 0 = POPC (32-bit population counts per second).
  * `sink` is a caller-allocated device u32 the kernel may write. */

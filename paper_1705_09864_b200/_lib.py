@@ -42,6 +42,7 @@ SIGNATURES = {
     "bnn_bconv2d": (_i32, [_vp, _i64, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _i64,
                            _i64, _vp, _i32, _vp, _vp, _i32, _vp]),
     "bnn_probe_pipe_peak": (_i32, [_i32, _i64, _vp, _vp, _vp]),
+    "bnn_set_umma_variant": (_i32, [_i32]),
 }
 
 

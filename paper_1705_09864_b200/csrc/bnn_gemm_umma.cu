@@ -4,10 +4,10 @@
 // (gemm.py:80-159, layers.py:225-245); results are bit-identical.
 //
 // B200 has no binary tensor-core MMA (b1 mma.sync is emulated on sm_100a,
-// SURVEY 0), so each CTA expands its packed operands to bytes in shared
-// memory right before the MMA consumes them.  The expansion is one LOP3 per
-// 4 bytes.  For u32 word w, register r in 0..7 and byte j in 0..3, byte j of
-// register r stands for bit 8j + r of w:
+// SURVEY 0), so each CTA expands its packed operands to bytes right before
+// the MMA consumes them.  The expansion is one LOP3 per 4 bytes.  For u32
+// word w, register r in 0..7 and byte j in 0..3, byte j of register r
+// stands for bit 8j + r of w:
 //     B (activations):  w & (0x01010101 << r)        -> bit * 2^r
 //     A (weights):      w' & (0x80808080 >> r)       -> bit * 2^(7-r)
 // where w' = w with the bits of every byte reversed (BREV + PRMT, 2 ops per
@@ -19,43 +19,63 @@
 //     X = popc(a) + popc(b) - 2C,   P = k_eff - X
 // with popc(a), popc(b) counted by the producer threads as they expand.
 //
-// CTA tile 128 (M) x 256 (N); K streamed in 128-bit slices (128 expanded
-// bytes per row = one SWIZZLE_128B K-major atom row).  Warp roles:
-//   warps 0..11  producers: one operand row each (128 A rows + 256 B rows);
-//                cp.async packed words into a private 4-deep ring, expand,
-//                st.shared into the 4-stage expanded ring, fence.proxy.async,
-//                arrive on full[s]
-//   warp 12      TMEM allocator + single-thread tcgen05.mma issuer; each
-//                stage = 4 MMAs of K=32; tcgen05.commit -> empty[s]
-//   warps 0..3   epilogue after the K loop: tcgen05.ld 32x32b.x16 (thread t
-//                owns TMEM lane t = tile row t), decode, store f32.
+// Persistent, warp-specialised CTA (one per SM) looping over 128 x BN output
+// tiles; K is streamed in 128-bit slices (128 expanded bytes per row).
+//   warps [0, P)   producers, one operand row each (128 A rows + BN B rows):
+//                  cp.async packed words into a private PD-deep ring (running
+//                  ahead across tile boundaries), expand, write the stage:
+//                  B rows -> SWIZZLE_128B K-major SMEM (st.shared.v4);
+//                  A rows -> SMEM as well (kATmem = false) or straight into
+//                  TMEM with tcgen05.st (kATmem = true: the MMA then reads A
+//                  from TMEM and only B crosses shared memory);
+//                  then arrive on full[s].
+//   warp P         TMEM allocator + single-thread tcgen05.mma issuer (4 MMAs
+//                  of K=32 per stage; commit -> empty[s]; per tile commit ->
+//                  tmem_full[buf]).
+//   warps P+1..P+4 epilogue: tcgen05.ld 32x32b.x16 of accumulator buffer
+//                  buf (double-buffered, so it overlaps the next tile's MMA),
+//                  decode, f32 store; arrive tmem_empty[buf].
+#include <cstdlib>
+
 #include "bnn_loaders.cuh"
 
 namespace bnn {
 namespace umma {
 
-constexpr int BM = 128, BN = 256;
-constexpr int kWordsPerStage = 4;                // u32 words of K per row per stage
-constexpr int kRowBytes = 128;                   // expanded bytes per row per stage
-constexpr int ES = 4;                            // expanded stages
-constexpr int PD = 4;                            // packed prefetch depth (per thread)
-constexpr int kProducers = BM + BN;              // 384
-constexpr int kThreads = kProducers + 32;        // + MMA warp
-constexpr int kMmaWarp = kProducers / 32;        // 12
-constexpr int kStageA = BM * kRowBytes;          // 16 KB
-constexpr int kStageB = BN * kRowBytes;          // 32 KB
-constexpr int kStageBytes = kStageA + kStageB;   // 48 KB
-constexpr int kTmemCols = 256;
+constexpr int BM = 128;
+constexpr int kWordsPerStage = 4;  // u32 words of K per row per stage
+constexpr int kRowBytes = 128;     // expanded bytes per row per stage
+constexpr int PD = 4;              // packed prefetch depth (per producer thread)
 
-struct Smem {  // offsets from the 1024-aligned dynamic smem base
-    static constexpr int expanded = 0;
-    static constexpr int packed = ES * kStageBytes;                       // 192 KB
-    static constexpr int popc_b = packed + PD * kProducers * 16;          // +24 KB
-    static constexpr int bars = popc_b + BN * 4;
-    static constexpr int tmem_slot = bars + (2 * ES + 1) * 8;
-    static constexpr int total = tmem_slot + 16;
+template <int BN, bool kATmem>
+struct Cfg {
+    static constexpr int kProducers = BM + BN;
+    static constexpr int kProducerWarps = kProducers / 32;
+    static constexpr int kMmaWarp = kProducerWarps;
+    static constexpr int kEpiWarp0 = kMmaWarp + 1;
+    static constexpr int kThreads = (kEpiWarp0 + 4) * 32;
+    static constexpr int kStageA = kATmem ? 0 : BM * kRowBytes;
+    static constexpr int kStageB = BN * kRowBytes;
+    static constexpr int kStageBytes = kStageA + kStageB;
+    static constexpr int ES = 4;  // expanded stages
+    // TMEM: 2 accumulator buffers of BN columns (+ ES A stages of 32 columns)
+    static constexpr int kAccCols = BN;
+    static constexpr int kAStageCol = 2 * BN;
+    static constexpr int kTmemCols = 512;
+    static_assert(2 * BN + (kATmem ? ES * 32 : 0) <= 512, "TMEM budget");
+    // shared memory carve-up (offsets from the 1024-aligned base)
+    static constexpr int off_exp = 0;
+    static constexpr int off_pk = ES * kStageBytes;
+    static constexpr int off_popc_a = off_pk + PD * kProducers * 16;
+    static constexpr int off_popc_b = off_popc_a + 2 * BM * 4;
+    static constexpr int off_bars = off_popc_b + 2 * BN * 4;
+    static constexpr int kNumBars = 2 * ES + 6;
+    static constexpr int off_tmem = off_bars + kNumBars * 8;
+    static constexpr int kSmemBytes = off_tmem + 16 + 1024;
+    static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
+    static constexpr uint32_t kIdesc = (2u << 4) | (0u << 7) | (0u << 10) |
+                                       ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 };
-constexpr int kSmemBytes = Smem::total + 1024;  // alignment slack
 
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
@@ -75,23 +95,26 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
             : "memory");
     } while (!done);
 }
+__device__ __forceinline__ void fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+}
 
 // K-major, SWIZZLE_128B UMMA shared-memory descriptor (8-row atoms of 1024 B)
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
     uint64_t d = 0;
-    d |= (uint64_t)((saddr >> 4) & 0x3FFF);        // start address
-    d |= (uint64_t)1 << 16;                         // LBO (unused for SW128 K-major)
-    d |= (uint64_t)(1024 >> 4) << 32;               // SBO: 8-row group stride
-    d |= (uint64_t)1 << 46;                         // descriptor version (sm_100)
-    d |= (uint64_t)2 << 61;                         // SWIZZLE_128B
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);  // start address
+    d |= (uint64_t)1 << 16;                   // LBO (unused for SW128 K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;         // SBO: 8-row group stride
+    d |= (uint64_t)1 << 46;                   // descriptor version (sm_100)
+    d |= (uint64_t)2 << 61;                   // SWIZZLE_128B
     return d;
 }
 
-// instruction descriptor: kind::i8, D s32, A u8, B u8, both K-major, M=128, N=256
-constexpr uint32_t kIdesc = (2u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(BN >> 3) << 17) |
-                            ((uint32_t)(BM >> 4) << 24);
-
-__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+template <uint32_t kIdesc>
+__device__ __forceinline__ void mma_ss(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
                                        uint32_t accumulate) {
     asm volatile(
         "{\n.reg .pred p;\n"
@@ -99,11 +122,20 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t
         "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
         "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate));
 }
+template <uint32_t kIdesc>
+__device__ __forceinline__ void mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                       uint32_t accumulate) {
+    asm volatile(
+        "{\n.reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(bdesc), "r"(kIdesc), "r"(accumulate));
+}
 
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                     bar)
-                 : "memory");
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar)
+        : "memory");
 }
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
@@ -117,12 +149,24 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 }
 
-// expand one packed u32 word into 32 bytes (two 16-byte chunks) of a row
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&v)[8]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(
+            taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+        : "memory");
+}
+
 template <bool kIsA>
-__device__ __forceinline__ void expand_store(uint32_t w, uint32_t row_base, int row, int q) {
-    uint32_t r[8];
+__device__ __forceinline__ void expand8(uint32_t w, uint32_t (&r)[8]) {
+    if (kIsA) w = __byte_perm(__brev(w), 0, 0x0123);  // reverse the bits of each byte
 #pragma unroll
     for (int i = 0; i < 8; ++i) r[i] = kIsA ? (w & (0x80808080u >> i)) : (w & (0x01010101u << i));
+}
+
+// 32 expanded bytes of word q -> two 16-byte chunks of a SW128 K-major row
+__device__ __forceinline__ void store_row32(const uint32_t (&r)[8], uint32_t row_base, int row,
+                                            int q) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         const int chunk = (2 * q + h) ^ (row & 7);
@@ -131,161 +175,292 @@ __device__ __forceinline__ void expand_store(uint32_t w, uint32_t row_base, int 
     }
 }
 
-template <int kVec, class ALoad, class BLoad, class Store>
-__global__ void __launch_bounds__(kThreads, 1)
-    xnor_umma_kernel(ALoad aload, BLoad bload, Store store, Epilogue ep, int64_t kw32) {
+struct TileMap {
+    int tiles_m, ntiles;
+    __device__ void decode(int t, int &tm, int &tn) const {
+        tm = t % tiles_m;
+        tn = t / tiles_m;
+    }
+};
+
+template <int BN, bool kATmem, int kVec, class ALoad, class BLoad, class Store>
+__global__ void __launch_bounds__(Cfg<BN, kATmem>::kThreads, 1)
+    xnor_umma_kernel(ALoad aload, BLoad bload, Store store, Epilogue ep, int64_t kw32,
+                     TileMap tmap) {
+    using C = Cfg<BN, kATmem>;
+    constexpr int ES = C::ES;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t sbase_raw = smem_u32(smem_raw);
     const uint32_t sbase = (sbase_raw + 1023u) & ~1023u;
     uint8_t *sgen = smem_raw + (sbase - sbase_raw);
-    const uint32_t s_exp = sbase + Smem::expanded;
-    const uint32_t s_pk = sbase + Smem::packed;
-    int32_t *s_popc_b = reinterpret_cast<int32_t *>(sgen + Smem::popc_b);
-    const uint32_t bar_full = sbase + Smem::bars;            // ES barriers
-    const uint32_t bar_empty = bar_full + ES * 8;           // ES barriers
-    const uint32_t bar_done = bar_empty + ES * 8;           // 1 barrier
-    uint32_t *s_tmem = reinterpret_cast<uint32_t *>(sgen + Smem::tmem_slot);
+    const uint32_t s_exp = sbase + C::off_exp;
+    const uint32_t s_pk = sbase + C::off_pk;
+    int32_t *s_popc_a = reinterpret_cast<int32_t *>(sgen + C::off_popc_a);
+    int32_t *s_popc_b = reinterpret_cast<int32_t *>(sgen + C::off_popc_b);
+    const uint32_t bar_full = sbase + C::off_bars;      // [ES]
+    const uint32_t bar_empty = bar_full + ES * 8;       // [ES]
+    const uint32_t bar_tfull = bar_empty + ES * 8;      // [2] MMA -> epilogue
+    const uint32_t bar_tempty = bar_tfull + 2 * 8;      // [2] epilogue -> MMA / producers
+    const uint32_t bar_pfull = bar_tempty + 2 * 8;      // [2] producers' popcounts ready
+    uint32_t *s_tmem = reinterpret_cast<uint32_t *>(sgen + C::off_tmem);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
     const int64_t ktiles = ceil_div(kw32, kWordsPerStage);
 
     if (tid == 0) {
         for (int s = 0; s < ES; ++s) {
-            mbar_init(bar_full + 8 * s, kProducers);
+            mbar_init(bar_full + 8 * s, C::kProducers);
             mbar_init(bar_empty + 8 * s, 1);
         }
-        mbar_init(bar_done, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(bar_tfull + 8 * b, 1);
+            mbar_init(bar_tempty + 8 * b, 128);
+            mbar_init(bar_pfull + 8 * b, C::kProducers);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
-    if (warp == kMmaWarp) {
+    if (warp == C::kMmaWarp) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
                          smem_u32(s_tmem)),
-                     "n"(kTmemCols));
+                     "n"(C::kTmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
-    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    fence_before();
     __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    fence_after();
     const uint32_t tmem = *s_tmem;
 
-    int32_t my_popc = 0;
-    if (warp < kMmaWarp) {
-        // ------------------------------------------------------------ producer
+    if (warp < C::kProducerWarps) {
+        // ================================================================ producers
         const bool is_a = tid < BM;
         const int row = is_a ? tid : tid - BM;
-        // private packed ring, slot-major so a warp's 16-byte slots are contiguous
-        const uint32_t ring = s_pk + tid * 16;
-        typename ALoad::Cursor ca{};
-        typename BLoad::Cursor cb{};
-        if (is_a) ca = aload.row(m0 + row);
-        else cb = bload.row(n0 + row);
-        auto fetch = [&](int64_t kt) {
-            const uint32_t dst = ring + (uint32_t)(kt % PD) * (kProducers * 16);
-#pragma unroll
-            for (int p = 0; p < kWordsPerStage / kVec; ++p) {
-                const int64_t w = kt * kWordsPerStage + p * kVec;
-                if (is_a) aload.template load<kVec>(ca, w, dst + p * kVec * 4);
-                else bload.template load<kVec>(cb, w, dst + p * kVec * 4);
-            }
+        const uint32_t ring = s_pk + tid * 16;  // slot-major private ring
+        // fetch iterator (runs PD-1 stages ahead, across tile boundaries)
+        int f_tile = blockIdx.x;
+        int64_t f_kt = 0;
+        typename ALoad::Cursor fa{};
+        typename BLoad::Cursor fb{};
+        auto set_cursor = [&](int t) {
+            if (t >= tmap.ntiles) return;
+            int tm, tn;
+            tmap.decode(t, tm, tn);
+            if (is_a) fa = aload.row((int64_t)tm * BM + row);
+            else fb = bload.row((int64_t)tn * BN + row);
         };
+        set_cursor(f_tile);
+        int64_t f_count = 0;  // stages fetched so far
+        auto fetch_next = [&]() {
+            if (f_tile < tmap.ntiles) {
+                const uint32_t dst = ring + (uint32_t)(f_count % PD) * (C::kProducers * 16);
 #pragma unroll
-        for (int p = 0; p < PD - 1; ++p) {
-            if (p < ktiles) fetch(p);
-            cp_async_commit();
-        }
-        for (int64_t kt = 0; kt < ktiles; ++kt) {
-            if (kt + PD - 1 < ktiles) fetch(kt + PD - 1);
-            cp_async_commit();
-            cp_async_wait<PD - 1>();
-            uint32_t wv[4];
-            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n"
-                         : "=r"(wv[0]), "=r"(wv[1]), "=r"(wv[2]), "=r"(wv[3])
-                         : "r"(ring + (uint32_t)(kt % PD) * (kProducers * 16)));
-            const int s = (int)(kt % ES);
-            if (kt >= ES) mbar_wait(bar_empty + 8 * s, (uint32_t)((kt / ES) - 1) & 1u);
-            const uint32_t row_base = s_exp + s * kStageBytes + (is_a ? 0 : kStageA) + row * kRowBytes;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                my_popc += __popc(wv[q]);
-                if (is_a) expand_store<true>(__byte_perm(__brev(wv[q]), 0, 0x0123), row_base, row, q);
-                else expand_store<false>(wv[q], row_base, row, q);
+                for (int p = 0; p < kWordsPerStage / kVec; ++p) {
+                    const int64_t w = f_kt * kWordsPerStage + p * kVec;
+                    if (is_a) aload.template load<kVec>(fa, w, dst + p * kVec * 4);
+                    else bload.template load<kVec>(fb, w, dst + p * kVec * 4);
+                }
+                ++f_count;
+                if (++f_kt == ktiles) {
+                    f_kt = 0;
+                    f_tile += gridDim.x;
+                    set_cursor(f_tile);
+                }
             }
-            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-            mbar_arrive(bar_full + 8 * s);
+            cp_async_commit();
+        };
+#pragma unroll 1
+        for (int p = 0; p < PD - 1; ++p) fetch_next();
+
+        int64_t gk = 0;  // global stage counter (ring / phase bookkeeping)
+        int it = 0;
+#pragma unroll 1
+        for (int tile = blockIdx.x; tile < tmap.ntiles; tile += gridDim.x, ++it) {
+            int32_t my_popc = 0;
+#pragma unroll 1
+            for (int64_t kt = 0; kt < ktiles; ++kt, ++gk) {
+                fetch_next();
+                cp_async_wait<PD - 1>();
+                uint32_t wv[4];
+                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n"
+                             : "=r"(wv[0]), "=r"(wv[1]), "=r"(wv[2]), "=r"(wv[3])
+                             : "r"(ring + (uint32_t)(gk % PD) * (C::kProducers * 16)));
+                const int s = (int)(gk % ES);
+                if (gk >= ES) mbar_wait(bar_empty + 8 * s, (uint32_t)((gk / ES) - 1) & 1u);
+                if (is_a) {
+                    if constexpr (kATmem) {
+                        // warps 0..3 own TMEM lanes 0..127 = A rows 0..127
+                        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) +
+                                               C::kAStageCol + s * 32;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            my_popc += __popc(wv[q]);
+                            uint32_t r[8];
+                            expand8<true>(wv[q], r);
+                            tmem_st8(taddr + q * 8, r);
+                        }
+                        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+                        fence_before();
+                    } else {
+                        const uint32_t row_base = s_exp + s * C::kStageBytes + row * kRowBytes;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            my_popc += __popc(wv[q]);
+                            uint32_t r[8];
+                            expand8<true>(wv[q], r);
+                            store_row32(r, row_base, row, q);
+                        }
+                        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                    }
+                } else {
+                    const uint32_t row_base =
+                        s_exp + s * C::kStageBytes + C::kStageA + row * kRowBytes;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        my_popc += __popc(wv[q]);
+                        uint32_t r[8];
+                        expand8<false>(wv[q], r);
+                        store_row32(r, row_base, row, q);
+                    }
+                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                }
+                mbar_arrive(bar_full + 8 * s);
+            }
+            // hand this tile's row popcounts to the epilogue (double-buffered)
+            const int buf = it & 1;
+            if (it >= 2) mbar_wait(bar_tempty + 8 * buf, (uint32_t)((it >> 1) - 1) & 1u);
+            if (is_a) s_popc_a[buf * BM + row] = my_popc;
+            else s_popc_b[buf * BN + row] = my_popc;
+            mbar_arrive(bar_pfull + 8 * buf);
         }
         cp_async_wait<0>();
-        if (!is_a) s_popc_b[row] = my_popc;
-        asm volatile("bar.sync 1, %0;\n" ::"n"(kProducers) : "memory");  // s_popc_b visible
-    } else if (lane == 0) {
-        // ------------------------------------------------------------ MMA issuer
-        for (int64_t kt = 0; kt < ktiles; ++kt) {
-            const int s = (int)(kt % ES);
-            mbar_wait(bar_full + 8 * s, (uint32_t)(kt / ES) & 1u);
-            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-            const uint32_t a_addr = s_exp + s * kStageBytes;
-            const uint32_t b_addr = a_addr + kStageA;
-#pragma unroll
-            for (int kk = 0; kk < kRowBytes / 32; ++kk)
-                mma_i8(tmem, sw128_desc(a_addr + kk * 32), sw128_desc(b_addr + kk * 32),
-                       (kt | kk) != 0 ? 1u : 0u);
-            umma_commit(bar_empty + 8 * s);
-        }
-        umma_commit(bar_done);
-    }
-
-    // ---------------------------------------------------------------- epilogue
-    if (warp < 4) {
-        mbar_wait(bar_done, 0);
-        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        const int64_t m = m0 + tid;  // TMEM lane tid == tile row tid
-        const bool mrow_ok = store.ok(m, n0);
-        const int32_t pa = my_popc;
-        const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
+    } else if (warp == C::kMmaWarp) {
+        // ================================================================ MMA issuer
+        if (lane == 0) {
+            int64_t gk = 0;
+            int it = 0;
 #pragma unroll 1
-        for (int c = 0; c < BN / 16; ++c) {
-            uint32_t v[16];
-            tmem_ld16(lane_addr + c * 16, v);
-            if (!mrow_ok) continue;
+            for (int tile = blockIdx.x; tile < tmap.ntiles; tile += gridDim.x, ++it) {
+                const int buf = it & 1;
+                if (it >= 2) mbar_wait(bar_tempty + 8 * buf, (uint32_t)((it >> 1) - 1) & 1u);
+                fence_after();
+                const uint32_t d = tmem + buf * C::kAccCols;
+#pragma unroll 1
+                for (int64_t kt = 0; kt < ktiles; ++kt, ++gk) {
+                    const int s = (int)(gk % ES);
+                    mbar_wait(bar_full + 8 * s, (uint32_t)(gk / ES) & 1u);
+                    fence_after();
+                    const uint32_t b_addr = s_exp + s * C::kStageBytes + C::kStageA;
 #pragma unroll
-            for (int g = 0; g < 4; ++g) {
-                float o[4];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const int nn = c * 16 + g * 4 + i;
-                    const int32_t cnt = (int32_t)(v[g * 4 + i] >> 7);
-                    const int32_t x = pa + s_popc_b[nn] - 2 * cnt;
-                    o[i] = ep.apply(x, (int)m);
+                    for (int kk = 0; kk < kRowBytes / 32; ++kk) {
+                        const uint32_t acc = (kt | kk) != 0 ? 1u : 0u;
+                        if constexpr (kATmem)
+                            mma_ts<C::kIdesc>(d, tmem + C::kAStageCol + s * 32 + kk * 8,
+                                              sw128_desc(b_addr + kk * 32), acc);
+                        else
+                            mma_ss<C::kIdesc>(d, sw128_desc(s_exp + s * C::kStageBytes + kk * 32),
+                                              sw128_desc(b_addr + kk * 32), acc);
+                    }
+                    umma_commit(bar_empty + 8 * s);
                 }
-                const int64_t n = n0 + c * 16 + g * 4;
-                if (store.ok(m, n)) store.put4(m, n, o);
+                umma_commit(bar_tfull + 8 * buf);
             }
         }
+        __syncwarp();
+    } else {
+        // ================================================================ epilogue
+        const int q = warp & 3;             // TMEM lane quadrant of this warp
+        const int r = q * 32 + lane;        // tile row == TMEM lane
+        int it = 0;
+#pragma unroll 1
+        for (int tile = blockIdx.x; tile < tmap.ntiles; tile += gridDim.x, ++it) {
+            const int buf = it & 1;
+            int tm, tn;
+            tmap.decode(tile, tm, tn);
+            const int64_t m = (int64_t)tm * BM + r, n0 = (int64_t)tn * BN;
+            mbar_wait(bar_tfull + 8 * buf, (uint32_t)(it >> 1) & 1u);
+            mbar_wait(bar_pfull + 8 * buf, (uint32_t)(it >> 1) & 1u);
+            fence_after();
+            const bool mrow_ok = store.ok(m, n0);
+            const int32_t pa = s_popc_a[buf * BM + r];
+            const int32_t *pb = s_popc_b + buf * BN;
+            const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + buf * C::kAccCols;
+#pragma unroll 1
+            for (int c = 0; c < BN / 16; ++c) {
+                uint32_t v[16];
+                tmem_ld16(taddr + c * 16, v);
+                if (!mrow_ok) continue;
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    float o[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int nn = c * 16 + g * 4 + i;
+                        const int32_t x = pa + pb[nn] - 2 * (int32_t)(v[g * 4 + i] >> 7);
+                        o[i] = ep.apply(x, (int)m);
+                    }
+                    const int64_t n = n0 + c * 16 + g * 4;
+                    if (store.ok(m, n)) store.put4(m, n, o);
+                }
+            }
+            fence_before();
+            mbar_arrive(bar_tempty + 8 * buf);
+        }
     }
-    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+
+    fence_before();
     __syncthreads();
-    if (warp == kMmaWarp) {
-        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    if (warp == C::kMmaWarp) {
+        fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
-                     "n"(kTmemCols));
+                     "n"(C::kTmemCols));
     }
 }
 
 }  // namespace umma
 
+static int sm_count() {
+    static int n = 0;
+    if (n == 0) {
+        n = bnn_device_sm_count();
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+template <int BN, bool kATmem, int kVec, class ALoad, class BLoad, class Store>
+static int launch_umma_cfg(const ALoad &a, const BLoad &b, const Store &st, const Epilogue &ep,
+                           int64_t M, int64_t N, int64_t kw32, cudaStream_t s) {
+    using C = umma::Cfg<BN, kATmem>;
+    auto kern = umma::xnor_umma_kernel<BN, kATmem, kVec, ALoad, BLoad, Store>;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+        configured = true;
+    }
+    const int64_t tiles_m = ceil_div(M, umma::BM), tiles_n = ceil_div(N, BN);
+    const int64_t ntiles = tiles_m * tiles_n;
+    if (ntiles > (1ll << 30)) return set_error(BNN_EUNSUP, "too many tiles");
+    umma::TileMap tmap{(int)tiles_m, (int)ntiles};
+    const int grid = (int)(ntiles < sm_count() ? ntiles : sm_count());
+    kern<<<grid, C::kThreads, C::kSmemBytes, s>>>(a, b, st, ep, kw32, tmap);
+    return check_launch("xnor_umma_kernel");
+}
+
+// engine variants (bnn_set_umma_variant / env BNN_UMMA_VARIANT):
+//   0: BN=256, A and B through SMEM      1: BN=192, A in TMEM, B through SMEM
+int g_umma_variant = -1;
+static int umma_variant() {
+    if (g_umma_variant < 0) {
+        const char *e = getenv("BNN_UMMA_VARIANT");
+        g_umma_variant = e ? atoi(e) : 1;
+    }
+    return g_umma_variant;
+}
+
 template <int kVec, class ALoad, class BLoad, class Store>
 static int launch_umma(const ALoad &a, const BLoad &b, const Store &st, const Epilogue &ep,
                        int64_t M, int64_t N, int64_t kw32, cudaStream_t s) {
-    auto kern = umma::xnor_umma_kernel<kVec, ALoad, BLoad, Store>;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, umma::kSmemBytes);
-        configured = true;
-    }
-    dim3 grid((unsigned)ceil_div(N, umma::BN), (unsigned)ceil_div(M, umma::BM));
-    if (grid.y > 65535) return set_error(BNN_EUNSUP, "M too large");
-    kern<<<grid, umma::kThreads, umma::kSmemBytes, s>>>(a, b, st, ep, kw32);
-    return check_launch("xnor_umma_kernel");
+    if (umma_variant() == 0) return launch_umma_cfg<256, false, kVec>(a, b, st, ep, M, N, kw32, s);
+    return launch_umma_cfg<192, true, kVec>(a, b, st, ep, M, N, kw32, s);
 }
 
 int launch_xnor_gemm_umma(const uint64_t *A, int64_t lda, const uint64_t *B, int64_t ldb,
@@ -320,3 +495,9 @@ int launch_bconv2d_umma(const uint64_t *x, int64_t B, int64_t C, int64_t H, int6
 }
 
 }  // namespace bnn
+
+extern "C" int bnn_set_umma_variant(int v) {
+    if (v < 0 || v > 1) return bnn::set_error(BNN_EINVAL, "umma variant must be 0 or 1");
+    bnn::g_umma_variant = v;
+    return BNN_OK;
+}

@@ -19,7 +19,16 @@ from oracle import oracle as orc
 
 pytestmark = pytest.mark.gpu
 
-ALGOS = ["popc", "umma"]
+ALGOS = ["popc", "umma0", "umma1"]
+
+
+def A(algo):
+    """Engine id for the C ABI; umma0/umma1 select the tcgen05 variant first."""
+    if algo.startswith("umma"):
+        from paper_1705_09864_b200 import _lib
+        _lib.call("bnn_set_umma_variant", int(algo[4:]))
+        return "umma"
+    return algo
 
 
 def _sha(a):
@@ -129,7 +138,7 @@ def test_gemm40_bit_exact(bnn, golden, algo):
     for i, (m, n, k, seed) in enumerate(wl.gemm40_cases()):
         a = bnn.BitMatrix(g[f"a{i}"], m, k, "a", 0)
         b = bnn.BitMatrix(g[f"b{i}"], n, k, "b", 1)
-        c = bnn.xnor_gemm_b200(a, b, algo=algo).cpu().numpy()
+        c = bnn.xnor_gemm_b200(a, b, algo=A(algo)).cpu().numpy()
         assert c.dtype == np.float32
         assert np.array_equal(c, g[f"c{i}"]), (m, n, k)
 
@@ -164,7 +173,7 @@ def test_sweep504_bit_exact(bnn, golden_dir, algo):
     got = []
     for m, n, k, a, b in wl.sweep504():
         abm, bbm = bnn.pack_matrix_a(a), bnn.pack_matrix_b(b)
-        c = bnn.xnor_gemm_b200(abm, bbm, algo=algo).cpu().numpy()
+        c = bnn.xnor_gemm_b200(abm, bbm, algo=A(algo)).cpu().numpy()
         got.append([m, n, k, _sha(c), int(c.astype(np.int64).sum())])
     assert got == rows
 
@@ -185,14 +194,14 @@ def test_gemm_tail_and_layout_variants(bnn, algo):
             for bp in (0, 1):
                 aw = torch.from_numpy(orc.pack_rows(a, ap).view(np.uint64)).cuda()
                 bw = torch.from_numpy(orc.pack_rows(b, bp)).cuda()
-                c = bnn.xnor_rows_gemm(aw, bw, k, a_pad=ap, b_pad=bp, algo=algo)
+                c = bnn.xnor_rows_gemm(aw, bw, k, a_pad=ap, b_pad=bp, algo=A(algo))
                 assert np.array_equal(c.cpu().numpy(), expect.astype(np.float32)), (m, n, k, ap, bp)
         # odd leading dimension (8-byte aligned rows), dot domain, [N, M] output
         W = (k + 63) // 64
         aw = torch.zeros((m, W + 1), dtype=torch.uint64, device="cuda")
         aw[:, :W] = torch.from_numpy(orc.pack_rows(a, 0)).cuda()
         bw = torch.from_numpy(orc.pack_rows(b, 0)).cuda()
-        c = bnn.xnor_rows_gemm(aw[:, :W], bw, k, domain=1, transpose_out=True, algo=algo)
+        c = bnn.xnor_rows_gemm(aw[:, :W], bw, k, domain=1, transpose_out=True, algo=A(algo))
         assert np.array_equal(c.cpu().numpy(), (2 * expect - k).T.astype(np.float32))
 
 
@@ -204,7 +213,7 @@ def test_gemm_epilogue_scale_shift(bnn, algo):
     aw, bw = (torch.from_numpy(orc.pack_rows(x, 0)).cuda() for x in (a, b))
     sc = torch.from_numpy(rng.standard_normal(m).astype(np.float32)).cuda()
     sh = torch.from_numpy(rng.standard_normal(m).astype(np.float32)).cuda()
-    c = bnn.xnor_rows_gemm(aw, bw, k, scale=sc, shift=sh, algo=algo).cpu().numpy()
+    c = bnn.xnor_rows_gemm(aw, bw, k, scale=sc, shift=sh, algo=A(algo)).cpu().numpy()
     p = (k - orc.xor_popc_rowrow(orc.pack_rows(a, 0), orc.pack_rows(b, 0))).astype(np.float32)
     expect = p * sc.cpu().numpy()[:, None] + sh.cpu().numpy()[:, None]
     assert np.array_equal(c, expect.astype(np.float32))
@@ -220,7 +229,7 @@ def test_conv_cases_bit_exact(bnn, golden, algo):
         layer = bnn.QConvolution(c, f, (kh, kw), stride, pad)
         layer.weight = wt
         layer.pack()
-        layer.algo = algo
+        layer.algo = A(algo)
         y = layer.forward(torch.from_numpy(x).cuda(), bnn.INFER_PACKED).cpu().numpy()
         assert np.array_equal(y, g[f"y{i}"]), case
         # the float path of the same layer agrees exactly (layers.py:237-244)
@@ -273,7 +282,7 @@ def test_config1_qfc_golden(bnn, golden_dir, algo):
     layer = bnn.QFullyConnected(4096, 1024, domain="dot")
     layer.weight = w
     layer.pack()
-    layer.algo = algo
+    layer.algo = A(algo)
     y = layer.forward(torch.from_numpy(a).cuda(), bnn.INFER_PACKED).cpu().numpy()
     assert list(y.shape) == cfg["shape"]
     assert _sha(y) == cfg["sha256"]
@@ -287,7 +296,7 @@ def test_config2_qconv_golden(bnn, golden_dir, algo):
     layer = bnn.QConvolution(c["c"], c["f"], (c["kh"], c["kw"]), c["stride"], c["pad"])
     layer.weight = wt
     layer.pack()
-    layer.algo = algo
+    layer.algo = A(algo)
     y = layer.forward(torch.from_numpy(x).cuda(), bnn.INFER_PACKED).cpu().numpy()
     assert list(y.shape) == cfg["shape"]
     assert _sha(y) == cfg["sha256"]
@@ -306,7 +315,7 @@ def test_large_gemm_properties(bnn, algo, mnk):
     W = k // 64
     aw = torch.randint(-2**63, 2**63 - 1, (m, W), device="cuda", generator=g).view(torch.uint64)
     bw = torch.randint(-2**63, 2**63 - 1, (n, W), device="cuda", generator=g).view(torch.uint64)
-    c = bnn.xnor_rows_gemm(aw, bw, k, algo=algo)
+    c = bnn.xnor_rows_gemm(aw, bw, k, algo=A(algo))
     assert float(c.min()) >= 0 and float(c.max()) <= k
     a_np, b_np = aw.cpu().numpy(), bw.cpu().numpy()
 

@@ -4,7 +4,7 @@ import torch
 sys.path.insert(0, ".")
 import paper_1705_09864_b200 as bnn
 
-bnn.load_library()
+lib = bnn.load_library()
 torch.manual_seed(0)
 shapes = [(128, 256, 128), (128, 256, 4096), (200, 300, 1000), (1, 1, 1), (256, 25088, 2304),
           (1024, 256, 4096), (4096, 4096, 4096)]
@@ -17,22 +17,22 @@ for m, n, k in shapes:
         a.view(torch.int64)[:, -1] &= mask
         b.view(torch.int64)[:, -1] &= mask
     cp = bnn.xnor_rows_gemm(a, b, k, algo="popc")
-    cu = bnn.xnor_rows_gemm(a, b, k, algo="umma")
-    torch.cuda.synchronize()
-    ok = torch.equal(cp, cu)
-    bad = int((cp != cu).sum())
-    ts = {}
-    for algo in ("popc", "umma"):
+    out = [f"{m}x{n}x{k}:"]
+    for variant in (0, 1):
+        lib.bnn_set_umma_variant(variant)
+        cu = bnn.xnor_rows_gemm(a, b, k, algo="umma")
+        torch.cuda.synchronize()
+        ok = torch.equal(cp, cu)
+        bad = int((cp != cu).sum())
         for _ in range(3):
-            bnn.xnor_rows_gemm(a, b, k, algo=algo)
+            bnn.xnor_rows_gemm(a, b, k, algo="umma")
         s, e = torch.cuda.Event(True), torch.cuda.Event(True)
         s.record()
         for _ in range(10):
-            bnn.xnor_rows_gemm(a, b, k, algo=algo)
+            bnn.xnor_rows_gemm(a, b, k, algo="umma")
         e.record(); e.synchronize()
-        ts[algo] = s.elapsed_time(e) / 10
-    tops = {a_: 2 * m * n * k / (t * 1e-3) / 1e12 for a_, t in ts.items()}
-    print(f"{m}x{n}x{k}: equal={ok} bad={bad} popc {ts['popc']*1e3:.1f}us {tops['popc']:.0f}T  "
-          f"umma {ts['umma']*1e3:.1f}us {tops['umma']:.0f}T", flush=True)
-    if not ok:
-        print(cp[:2, :8]); print(cu[:2, :8])
+        t = s.elapsed_time(e) / 10
+        out.append(f"v{variant} equal={ok} bad={bad} {t*1e3:.1f}us {2*m*n*k/(t*1e-3)/1e12:.0f}T")
+        if not ok:
+            out.append(str(cp[:2, :8].tolist()) + " vs " + str(cu[:2, :8].tolist()))
+    print("  ".join(out), flush=True)
