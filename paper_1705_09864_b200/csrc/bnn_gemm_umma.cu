@@ -209,13 +209,13 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem>::kThreads, 1)
 
     if (tid == 0) {
         for (int s = 0; s < ES; ++s) {
-            mbar_init(bar_full + 8 * s, C::kProducers);
+            mbar_init(bar_full + 8 * s, C::kProducerWarps);
             mbar_init(bar_empty + 8 * s, 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(bar_tfull + 8 * b, 1);
             mbar_init(bar_tempty + 8 * b, 128);
-            mbar_init(bar_pfull + 8 * b, C::kProducers);
+            mbar_init(bar_pfull + 8 * b, C::kProducerWarps);
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
@@ -322,14 +322,16 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem>::kThreads, 1)
                     }
                     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                 }
-                mbar_arrive(bar_full + 8 * s);
+                __syncwarp();  // every lane's writes + fence precede the warp's arrival
+                if (lane == 0) mbar_arrive(bar_full + 8 * s);
             }
             // hand this tile's row popcounts to the epilogue (double-buffered)
             const int buf = it & 1;
             if (it >= 2) mbar_wait(bar_tempty + 8 * buf, (uint32_t)((it >> 1) - 1) & 1u);
             if (is_a) s_popc_a[buf * BM + row] = my_popc;
             else s_popc_b[buf * BN + row] = my_popc;
-            mbar_arrive(bar_pfull + 8 * buf);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar_pfull + 8 * buf);
         }
         cp_async_wait<0>();
     } else if (warp == C::kMmaWarp) {

@@ -48,7 +48,7 @@ struct DenseRows {
     __device__ Cursor row(int64_t r) const { return {base + r * ld32, r < rows}; }
     // load kVec words at word w of this row into smem address dst
     template <int kVec>
-    __device__ void load(const Cursor &c, int64_t w, uint32_t dst) const {
+    __device__ void load(Cursor &c, int64_t w, uint32_t dst) const {
         int64_t left = kw32 - w;
         int bytes = (!c.ok || left <= 0) ? 0 : (int)(left >= kVec ? kVec * 4 : left * 4);
         const uint32_t *src = bytes ? c.p + w : base;
@@ -65,7 +65,9 @@ struct ConvRows {
     int64_t npix;       // B * oh * ow
     int H, W, cs32, C, kw, sh, sw, ph, pw, oh, ow;
     int64_t kw32;       // kh * kw * cs32
-    struct Cursor { const uint32_t *img; int iy0, ix0; bool ok; };
+    // (tap_w0, i, j) track the current kernel tap incrementally: callers walk
+    // w upwards within a row, so no division is needed per load
+    struct Cursor { const uint32_t *img; int iy0, ix0; bool ok; int64_t tap_w0; int i, j; };
     __device__ Cursor row(int64_t n) const {
         Cursor c;
         c.ok = n < npix;
@@ -77,18 +79,23 @@ struct ConvRows {
         c.img = x + b * (int64_t)H * W * cs32;
         c.iy0 = oy * sh - ph;
         c.ix0 = ox * sw - pw;
+        c.tap_w0 = 0;
+        c.i = c.j = 0;
         return c;
     }
     template <int kVec>
-    __device__ void load(const Cursor &c, int64_t w, uint32_t dst) const {
+    __device__ void load(Cursor &c, int64_t w, uint32_t dst) const {
         if (!c.ok || w >= kw32) {
             cp_async<kVec * 4>(dst, x, 0);
             return;
         }
-        int tap = (int)(w / cs32);
-        int cw = (int)(w - (int64_t)tap * cs32);
-        int i = tap / kw, j = tap - (tap / kw) * kw;
-        int iy = c.iy0 + i, ix = c.ix0 + j;
+        if (w < c.tap_w0) c.tap_w0 = 0, c.i = 0, c.j = 0;  // new pass over the row
+        while (w >= c.tap_w0 + cs32) {
+            c.tap_w0 += cs32;
+            if (++c.j == kw) c.j = 0, ++c.i;
+        }
+        const int cw = (int)(w - c.tap_w0);
+        int iy = c.iy0 + c.i, ix = c.ix0 + c.j;
         if (iy >= 0 && iy < H && ix >= 0 && ix < W) {
             cp_async<kVec * 4>(dst, c.img + ((int64_t)iy * W + ix) * cs32 + cw, kVec * 4);
         } else {

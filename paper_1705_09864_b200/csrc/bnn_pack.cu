@@ -123,49 +123,60 @@ __global__ void pack_cols_kernel(const float *__restrict__ x, int64_t K, int64_t
 
 // ---------------------------------------------------------------- pack NCHW
 // x [B, C, H, W] -> out [B*H*W, Cw] u64 (NHWC words, channel tail 0).
-// Thread per (4 consecutive pixels, channel word): 64 float4 loads along C,
-// so a warp reads 512 contiguous bytes per instruction (HW % 4 == 0) and
-// keeps 16 of them in flight.
+// CTA = (128 pixels, one 64-channel word, image b), 256 threads.  Phase 1
+// stages the 64 x 128 f32 tile in shared memory with coalesced float4 loads
+// (8 independent 16-byte loads per thread, 512 contiguous bytes per warp
+// instruction); phase 2 transposes: thread (pixel p, half h) folds channels
+// 32h..32h+31 of pixel p into a u32 and the two halves form the u64 word.
+constexpr int kPackPix = 128;
 template <bool kVec4>
-__global__ void pack_nchw_kernel(const float *__restrict__ x, int64_t B, int64_t C, int64_t HW,
-                                 int64_t Cw, uint64_t *__restrict__ out, int mode,
-                                 int32_t *flags) {
-    const int64_t p0 = 4 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
-    const int64_t cw = blockIdx.y;
-    const int64_t b = blockIdx.z;
+__global__ void __launch_bounds__(256) pack_nchw_kernel(const float *__restrict__ x, int64_t B,
+                                                        int64_t C, int64_t HW, int64_t Cw,
+                                                        uint64_t *__restrict__ out, int mode,
+                                                        int32_t *flags) {
+    __shared__ float tile[64][kPackPix + 4];
+    __shared__ uint32_t hi_half[kPackPix];
+    const int tid = threadIdx.x;
+    const int64_t p0 = (int64_t)blockIdx.x * kPackPix;
+    const int64_t cw = blockIdx.y, b = blockIdx.z;
+    const int nc = (int)(C - cw * 64 < 64 ? C - cw * 64 : 64);
+    const float *src = x + (b * C + cw * 64) * HW + p0;
     int f = 0;
-    if (p0 < HW) {
-        const float *src = x + (b * C + cw * 64) * HW + p0;
-        const int nc = (int)(C - cw * 64 < 64 ? C - cw * 64 : 64);
-        const int np = (int)(HW - p0 < 4 ? HW - p0 : 4);
-        uint64_t w[4] = {0, 0, 0, 0};
-        if (kVec4 && nc == 64) {
-#pragma unroll 16
-            for (int i = 0; i < 64; ++i) {
-                const float4 v = __ldg(reinterpret_cast<const float4 *>(src + (int64_t)i * HW));
-                f |= elem_flags(v.x, mode) | elem_flags(v.y, mode) | elem_flags(v.z, mode) |
-                     elem_flags(v.w, mode);
-                w[0] |= (uint64_t)sign_bit(v.x) << i;
-                w[1] |= (uint64_t)sign_bit(v.y) << i;
-                w[2] |= (uint64_t)sign_bit(v.z) << i;
-                w[3] |= (uint64_t)sign_bit(v.w) << i;
-            }
-        } else {
-            for (int i = 0; i < nc; ++i) {
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    if (j < np) {
-                        const float v = __ldg(src + (int64_t)i * HW + j);
-                        f |= elem_flags(v, mode);
-                        w[j] |= (uint64_t)sign_bit(v) << i;
+    for (int i = 0; i < 8; ++i) {
+        const int e = tid + 256 * i;  // 2048 float4 slots = 64 channels x 32 quads
+        const int c = e >> 5, quad = e & 31;
+        const int64_t p = 4 * quad;
+        float v[4] = {0.f, 0.f, 0.f, 0.f};
+        if (c < nc) {
+            if (kVec4 && p0 + p + 3 < HW) {
+                const float4 q = __ldg(reinterpret_cast<const float4 *>(src + c * HW + p));
+                v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+                f |= elem_flags(q.x, mode) | elem_flags(q.y, mode) | elem_flags(q.z, mode) |
+                     elem_flags(q.w, mode);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (p0 + p + j < HW) {
+                        v[j] = __ldg(src + c * HW + p + j);
+                        f |= elem_flags(v[j], mode);
                     }
-                }
             }
         }
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-            if (j < np) out[(b * HW + p0 + j) * Cw + cw] = w[j];
+        *reinterpret_cast<float4 *>(&tile[c][p]) = make_float4(v[0], v[1], v[2], v[3]);
     }
+    __syncthreads();
+    const int p = tid & (kPackPix - 1), h = tid >> 7;
+    uint32_t word = 0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        const int c = 32 * h + i;
+        word |= (c < nc ? sign_bit(tile[c][p]) : 0u) << i;
+    }
+    if (h == 1) hi_half[p] = word;
+    __syncthreads();
+    if (h == 0 && p0 + p < HW)
+        out[(b * HW + p0 + p) * Cw + cw] = (uint64_t)word | ((uint64_t)hi_half[p] << 32);
     flush_flags(f, flags);
 }
 
@@ -255,12 +266,12 @@ int launch_pack_nchw(const float *x, int64_t B, int64_t C, int64_t H, int64_t W,
                      int mode, int32_t *flags, cudaStream_t s) {
     const int64_t HW = H * W, Cw = ceil_div(C, 64);
     if (B == 0 || HW == 0 || C == 0) return BNN_OK;
-    dim3 grid((unsigned)ceil_div(HW, 4 * 128), (unsigned)Cw, (unsigned)B);
+    dim3 grid((unsigned)ceil_div(HW, kPackPix), (unsigned)Cw, (unsigned)B);
     const bool vec4 = (HW % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
     if (vec4)
-        pack_nchw_kernel<true><<<grid, 128, 0, s>>>(x, B, C, HW, Cw, out, mode, flags);
+        pack_nchw_kernel<true><<<grid, 256, 0, s>>>(x, B, C, HW, Cw, out, mode, flags);
     else
-        pack_nchw_kernel<false><<<grid, 128, 0, s>>>(x, B, C, HW, Cw, out, mode, flags);
+        pack_nchw_kernel<false><<<grid, 256, 0, s>>>(x, B, C, HW, Cw, out, mode, flags);
     return check_launch("pack_nchw_kernel");
 }
 
