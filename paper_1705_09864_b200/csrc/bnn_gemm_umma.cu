@@ -32,9 +32,10 @@
 //   warp P         TMEM allocator + single-thread tcgen05.mma issuer (4 MMAs
 //                  of K=32 per stage; commit -> empty[s]; per tile commit ->
 //                  tmem_full[buf]).
-//   warps P+1..P+4 epilogue: tcgen05.ld 32x32b.x16 of accumulator buffer
+//   warps P+1..P+8 epilogue: tcgen05.ld 32x32b.x16 of accumulator buffer
 //                  buf (double-buffered, so it overlaps the next tile's MMA),
-//                  decode, f32 store; arrive tmem_empty[buf].
+//                  decode, transpose through SMEM, sector-complete f32 stores;
+//                  arrive tmem_empty[buf].
 #include <cstdlib>
 
 #include "bnn_loaders.cuh"
@@ -49,26 +50,30 @@ constexpr int PD = 4;              // packed prefetch depth (per producer thread
 
 template <int BN, bool kATmem>
 struct Cfg {
-    static constexpr int kProducers = BM + BN;
-    static constexpr int kProducerWarps = kProducers / 32;
+    static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
+    static constexpr int kProducers = BM + BN;                 // one thread per operand row
+    static constexpr int kProducerWarps = (kProducers + 31) / 32;
     static constexpr int kMmaWarp = kProducerWarps;
     static constexpr int kEpiWarp0 = kMmaWarp + 1;
-    static constexpr int kThreads = (kEpiWarp0 + 4) * 32;
+    static constexpr int kEpiWarps = 8;                        // 2 per TMEM lane quadrant
+    static constexpr int kThreads = (kEpiWarp0 + kEpiWarps) * 32;
     static constexpr int kStageA = kATmem ? 0 : BM * kRowBytes;
     static constexpr int kStageB = BN * kRowBytes;
     static constexpr int kStageBytes = kStageA + kStageB;
-    static constexpr int ES = 4;  // expanded stages
+    static constexpr int ES = kATmem ? 4 : 3;  // expanded stages
     // TMEM: 2 accumulator buffers of BN columns (+ ES A stages of 32 columns)
     static constexpr int kAccCols = BN;
     static constexpr int kAStageCol = 2 * BN;
     static constexpr int kTmemCols = 512;
     static_assert(2 * BN + (kATmem ? ES * 32 : 0) <= 512, "TMEM budget");
     // shared memory carve-up (offsets from the 1024-aligned base)
+    static constexpr int kStageStride = 17;  // epilogue transpose buffer row pitch (words)
     static constexpr int off_exp = 0;
     static constexpr int off_pk = ES * kStageBytes;
-    static constexpr int off_popc_a = off_pk + PD * kProducers * 16;
+    static constexpr int off_popc_a = off_pk + PD * kProducerWarps * 32 * 16;
     static constexpr int off_popc_b = off_popc_a + 2 * BM * 4;
-    static constexpr int off_bars = off_popc_b + 2 * BN * 4;
+    static constexpr int off_epi = off_popc_b + 2 * BN * 4;
+    static constexpr int off_bars = off_epi + kEpiWarps * 32 * kStageStride * 4;
     static constexpr int kNumBars = 2 * ES + 6;
     static constexpr int off_tmem = off_bars + kNumBars * 8;
     static constexpr int kSmemBytes = off_tmem + 16 + 1024;
@@ -197,6 +202,7 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem>::kThreads, 1)
     const uint32_t s_pk = sbase + C::off_pk;
     int32_t *s_popc_a = reinterpret_cast<int32_t *>(sgen + C::off_popc_a);
     int32_t *s_popc_b = reinterpret_cast<int32_t *>(sgen + C::off_popc_b);
+    uint32_t *s_epi = reinterpret_cast<uint32_t *>(sgen + C::off_epi);
     const uint32_t bar_full = sbase + C::off_bars;      // [ES]
     const uint32_t bar_empty = bar_full + ES * 8;       // [ES]
     const uint32_t bar_tfull = bar_empty + ES * 8;      // [2] MMA -> epilogue
@@ -214,7 +220,7 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem>::kThreads, 1)
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(bar_tfull + 8 * b, 1);
-            mbar_init(bar_tempty + 8 * b, 128);
+            mbar_init(bar_tempty + 8 * b, C::kEpiWarps);
             mbar_init(bar_pfull + 8 * b, C::kProducerWarps);
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -233,15 +239,17 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem>::kThreads, 1)
     if (warp < C::kProducerWarps) {
         // ================================================================ producers
         const bool is_a = tid < BM;
+        const bool active = tid < C::kProducers;  // the last warp may be partly idle
         const int row = is_a ? tid : tid - BM;
         const uint32_t ring = s_pk + tid * 16;  // slot-major private ring
+        constexpr uint32_t kRingSlot = C::kProducerWarps * 32 * 16;
         // fetch iterator (runs PD-1 stages ahead, across tile boundaries)
         int f_tile = blockIdx.x;
         int64_t f_kt = 0;
         typename ALoad::Cursor fa{};
         typename BLoad::Cursor fb{};
         auto set_cursor = [&](int t) {
-            if (t >= tmap.ntiles) return;
+            if (t >= tmap.ntiles || !active) return;
             int tm, tn;
             tmap.decode(t, tm, tn);
             if (is_a) fa = aload.row((int64_t)tm * BM + row);
@@ -250,8 +258,8 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem>::kThreads, 1)
         set_cursor(f_tile);
         int64_t f_count = 0;  // stages fetched so far
         auto fetch_next = [&]() {
-            if (f_tile < tmap.ntiles) {
-                const uint32_t dst = ring + (uint32_t)(f_count % PD) * (C::kProducers * 16);
+            if (f_tile < tmap.ntiles && active) {
+                const uint32_t dst = ring + (uint32_t)(f_count % PD) * kRingSlot;
 #pragma unroll
                 for (int p = 0; p < kWordsPerStage / kVec; ++p) {
                     const int64_t w = f_kt * kWordsPerStage + p * kVec;
@@ -282,10 +290,11 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem>::kThreads, 1)
                 uint32_t wv[4];
                 asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n"
                              : "=r"(wv[0]), "=r"(wv[1]), "=r"(wv[2]), "=r"(wv[3])
-                             : "r"(ring + (uint32_t)(gk % PD) * (C::kProducers * 16)));
+                             : "r"(ring + (uint32_t)(gk % PD) * kRingSlot));
                 const int s = (int)(gk % ES);
                 if (gk >= ES) mbar_wait(bar_empty + 8 * s, (uint32_t)((gk / ES) - 1) & 1u);
-                if (is_a) {
+                if (!active) {
+                } else if (is_a) {
                     if constexpr (kATmem) {
                         // warps 0..3 own TMEM lanes 0..127 = A rows 0..127
                         const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) +
@@ -329,7 +338,7 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem>::kThreads, 1)
             const int buf = it & 1;
             if (it >= 2) mbar_wait(bar_tempty + 8 * buf, (uint32_t)((it >> 1) - 1) & 1u);
             if (is_a) s_popc_a[buf * BM + row] = my_popc;
-            else s_popc_b[buf * BN + row] = my_popc;
+            else if (active) s_popc_b[buf * BN + row] = my_popc;
             __syncwarp();
             if (lane == 0) mbar_arrive(bar_pfull + 8 * buf);
         }
@@ -369,42 +378,71 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem>::kThreads, 1)
         __syncwarp();
     } else {
         // ================================================================ epilogue
-        const int q = warp & 3;             // TMEM lane quadrant of this warp
-        const int r = q * 32 + lane;        // tile row == TMEM lane
+        // 8 warps: quadrant q = warp % 4 owns TMEM lanes (= tile rows) 32q..32q+31;
+        // the two warps of a quadrant take alternating 16-column chunks.
+        const int e = warp - C::kEpiWarp0;
+        const int q = warp & 3, h = e >> 2;
+        uint32_t *stg = s_epi + e * 32 * C::kStageStride;
         int it = 0;
 #pragma unroll 1
         for (int tile = blockIdx.x; tile < tmap.ntiles; tile += gridDim.x, ++it) {
             const int buf = it & 1;
             int tm, tn;
             tmap.decode(tile, tm, tn);
-            const int64_t m = (int64_t)tm * BM + r, n0 = (int64_t)tn * BN;
+            const int64_t mq = (int64_t)tm * BM + q * 32, n0 = (int64_t)tn * BN;
             mbar_wait(bar_tfull + 8 * buf, (uint32_t)(it >> 1) & 1u);
             mbar_wait(bar_pfull + 8 * buf, (uint32_t)(it >> 1) & 1u);
             fence_after();
-            const bool mrow_ok = store.ok(m, n0);
-            const int32_t pa = s_popc_a[buf * BM + r];
+            const int32_t *pa = s_popc_a + buf * BM + q * 32;
             const int32_t *pb = s_popc_b + buf * BN;
             const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + buf * C::kAccCols;
+            const int64_t M = store.rows(), N = store.cols();
 #pragma unroll 1
-            for (int c = 0; c < BN / 16; ++c) {
+            for (int c = h; c < BN / 16; c += 2) {
                 uint32_t v[16];
                 tmem_ld16(taddr + c * 16, v);
-                if (!mrow_ok) continue;
+                if (mq >= M) continue;
+                if (store.n_contiguous()) {
+                    // transpose through SMEM so each store instruction writes two
+                    // 64-byte row segments (whole sectors) instead of 32 scattered words
 #pragma unroll
-                for (int g = 0; g < 4; ++g) {
-                    float o[4];
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const int nn = c * 16 + g * 4 + i;
-                        const int32_t x = pa + pb[nn] - 2 * (int32_t)(v[g * 4 + i] >> 7);
-                        o[i] = ep.apply(x, (int)m);
+                    for (int j = 0; j < 16; ++j) stg[lane * C::kStageStride + j] = v[j];
+                    __syncwarp();
+                    const int jj = lane & 15, half = lane >> 4;
+                    const int64_t n = n0 + c * 16 + jj;
+                    if (n < N) {
+                        float *col = store.col_base(n);
+                        const int64_t ms = store.m_stride();
+                        const int32_t pbn = pb[c * 16 + jj];
+#pragma unroll 4
+                        for (int rr = 0; rr < 16; ++rr) {
+                            const int r = 2 * rr + half;
+                            const int64_t m = mq + r;
+                            if (m < M) {
+                                const int32_t cnt = (int32_t)(stg[r * C::kStageStride + jj] >> 7);
+                                col[m * ms] = ep.apply(pa[r] + pbn - 2 * cnt, (int)m);
+                            }
+                        }
                     }
-                    const int64_t n = n0 + c * 16 + g * 4;
-                    if (store.ok(m, n)) store.put4(m, n, o);
+                    __syncwarp();
+                } else {
+                    // rows are contiguous (e.g. an [N, M] output): lane = row stores
+                    const int64_t m = mq + lane;
+                    if (m < M) {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            const int64_t n = n0 + c * 16 + j;
+                            if (n < N) {
+                                const int32_t cnt = (int32_t)(v[j] >> 7);
+                                store.put(m, n, ep.apply(pa[lane] + pb[c * 16 + j] - 2 * cnt, (int)m));
+                            }
+                        }
+                    }
                 }
             }
             fence_before();
-            mbar_arrive(bar_tempty + 8 * buf);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar_tempty + 8 * buf);
         }
     }
 
@@ -448,7 +486,9 @@ static int launch_umma_cfg(const ALoad &a, const BLoad &b, const Store &st, cons
 }
 
 // engine variants (bnn_set_umma_variant / env BNN_UMMA_VARIANT):
-//   0: BN=256, A and B through SMEM      1: BN=192, A in TMEM, B through SMEM
+//   0: 128x256 tiles, A and B through SMEM
+//   1: A in TMEM, B through SMEM, tile N chosen per shape from {128, 160, 176, 192}
+//      to minimise (waves x N) on the SMs of this GPU
 int g_umma_variant = -1;
 static int umma_variant() {
     if (g_umma_variant < 0) {
@@ -458,11 +498,29 @@ static int umma_variant() {
     return g_umma_variant;
 }
 
+static int choose_bn(int64_t M, int64_t N) {
+    static const int cands[] = {192, 176, 160, 128};
+    const int64_t sms = sm_count(), tm = ceil_div(M, umma::BM);
+    int best = 192;
+    int64_t best_cost = -1;
+    for (int bn : cands) {
+        const int64_t waves = ceil_div(tm * ceil_div(N, bn), sms);
+        const int64_t cost = waves * (bn + 32);  // + fixed per-tile overhead in columns
+        if (best_cost < 0 || cost < best_cost) best = bn, best_cost = cost;
+    }
+    return best;
+}
+
 template <int kVec, class ALoad, class BLoad, class Store>
 static int launch_umma(const ALoad &a, const BLoad &b, const Store &st, const Epilogue &ep,
                        int64_t M, int64_t N, int64_t kw32, cudaStream_t s) {
     if (umma_variant() == 0) return launch_umma_cfg<256, false, kVec>(a, b, st, ep, M, N, kw32, s);
-    return launch_umma_cfg<192, true, kVec>(a, b, st, ep, M, N, kw32, s);
+    switch (choose_bn(M, N)) {
+        case 128: return launch_umma_cfg<128, true, kVec>(a, b, st, ep, M, N, kw32, s);
+        case 160: return launch_umma_cfg<160, true, kVec>(a, b, st, ep, M, N, kw32, s);
+        case 176: return launch_umma_cfg<176, true, kVec>(a, b, st, ep, M, N, kw32, s);
+        default: return launch_umma_cfg<192, true, kVec>(a, b, st, ep, M, N, kw32, s);
+    }
 }
 
 int launch_xnor_gemm_umma(const uint64_t *A, int64_t lda, const uint64_t *B, int64_t ldb,

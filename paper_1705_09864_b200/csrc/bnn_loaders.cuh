@@ -121,6 +121,12 @@ struct GemmStore {
     int64_t ldc_m, ldc_n, M, N;
     __device__ bool ok(int64_t m, int64_t n) const { return m < M && n < N; }
     __device__ void put(int64_t m, int64_t n, float v) const { C[m * ldc_m + n * ldc_n] = v; }
+    // column view for the staged epilogue: &C[m, n] = col_base(n) + m * m_stride()
+    __device__ bool n_contiguous() const { return ldc_n == 1; }
+    __device__ float *col_base(int64_t n) const { return C + n * ldc_n; }
+    __device__ int64_t m_stride() const { return ldc_m; }
+    __device__ int64_t rows() const { return M; }
+    __device__ int64_t cols() const { return N; }
     // four consecutive n of one row m (m < M checked by the caller)
     __device__ void put4(int64_t m, int64_t n, const float *v) const {
         float *p = C + m * ldc_m + n * ldc_n;
@@ -142,6 +148,14 @@ struct ConvStore {  // y NCHW [B, F, oh*ow]; m = filter, n = b*ohw + pixel
         int64_t b = n / ohw, p = n - b * ohw;
         y[(b * F + m) * ohw + p] = v;
     }
+    __device__ bool n_contiguous() const { return true; }  // within an image
+    __device__ float *col_base(int64_t n) const {
+        int64_t b = n / ohw, p = n - b * ohw;
+        return y + b * F * ohw + p;
+    }
+    __device__ int64_t m_stride() const { return ohw; }
+    __device__ int64_t rows() const { return F; }
+    __device__ int64_t cols() const { return npix; }
     __device__ void put4(int64_t m, int64_t n, const float *v) const {
         int64_t b = n / ohw, p = n - b * ohw;
         float *dst = y + (b * F + m) * ohw + p;

@@ -142,28 +142,34 @@ __global__ void __launch_bounds__(256) pack_nchw_kernel(const float *__restrict_
     const int nc = (int)(C - cw * 64 < 64 ? C - cw * 64 : 64);
     const float *src = x + (b * C + cw * 64) * HW + p0;
     int f = 0;
+    float4 q[8];
+    // issue all eight 16-byte loads before touching any of them (MLP = 8);
+    // the full-tile case has no per-load predicates so they batch cleanly
+    const bool full = kVec4 && nc == 64 && p0 + kPackPix <= HW;
+    if (full) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int e = tid + 256 * i;  // 2048 float4 slots = 64 channels x 32 quads
+            q[i] = __ldg(reinterpret_cast<const float4 *>(src + (e >> 5) * HW + 4 * (e & 31)));
+        }
+    } else {
+#pragma unroll 1
+        for (int i = 0; i < 8; ++i) {
+            const int e = tid + 256 * i;
+            const int c = e >> 5, p = 4 * (e & 31);
+            q[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (c < nc)
+                for (int j = 0; j < 4; ++j)
+                    if (p0 + p + j < HW) (&q[i].x)[j] = __ldg(src + c * HW + p + j);
+        }
+    }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        const int e = tid + 256 * i;  // 2048 float4 slots = 64 channels x 32 quads
-        const int c = e >> 5, quad = e & 31;
-        const int64_t p = 4 * quad;
-        float v[4] = {0.f, 0.f, 0.f, 0.f};
-        if (c < nc) {
-            if (kVec4 && p0 + p + 3 < HW) {
-                const float4 q = __ldg(reinterpret_cast<const float4 *>(src + c * HW + p));
-                v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
-                f |= elem_flags(q.x, mode) | elem_flags(q.y, mode) | elem_flags(q.z, mode) |
-                     elem_flags(q.w, mode);
-            } else {
-#pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    if (p0 + p + j < HW) {
-                        v[j] = __ldg(src + c * HW + p + j);
-                        f |= elem_flags(v[j], mode);
-                    }
-            }
-        }
-        *reinterpret_cast<float4 *>(&tile[c][p]) = make_float4(v[0], v[1], v[2], v[3]);
+        const int e = tid + 256 * i;
+        const int c = e >> 5, p = 4 * (e & 31);
+        f |= elem_flags(q[i].x, mode) | elem_flags(q[i].y, mode) | elem_flags(q[i].z, mode) |
+             elem_flags(q[i].w, mode);
+        *reinterpret_cast<float4 *>(&tile[c][p]) = q[i];
     }
     __syncthreads();
     const int p = tid & (kPackPix - 1), h = tid >> 7;
