@@ -158,6 +158,12 @@ int bnn_bconv2d(const uint64_t *x_words, int64_t B, int64_t C, int64_t H, int64_
  * expanded weights in TMEM (only activations cross SMEM). */
 int bnn_set_umma_variant(int variant);
 
+/* Debug timeline of the tcgen05 engine: buf is a device array of
+ * (#SMs x 16) u64 %globaltimer stamps written by later launches
+ * (slot 0 start, 1 setup done, 2 first stage consumed, 3/6/9 tile MMA done,
+ * 4/7/10 epilogue start, 5/8/11 epilogue end, 12 exit); null disables. */
+int bnn_umma_trace(uint64_t *buf);
+
 /* Roofline probe (synchronous): measured issue rate of a pipe on the
  * current device.  pipe 0 = POPC (32-bit population counts per second).
  * `sink` is a caller-allocated device u32 the kernel may write. */

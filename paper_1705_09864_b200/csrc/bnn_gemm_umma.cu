@@ -44,6 +44,18 @@ namespace bnn {
 namespace umma {
 
 constexpr int BM = 128;
+
+// Debug timeline (bnn_umma_trace): when set, CTA c records %globaltimer at
+// slot s into g_trace[c * kTraceSlots + s].  Null in production.
+constexpr int kTraceSlots = 16;
+__device__ uint64_t *g_trace = nullptr;
+__device__ __forceinline__ void trace(int slot) {
+    if (g_trace) {
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_trace[blockIdx.x * kTraceSlots + slot] = t;
+    }
+}
 constexpr int kWordsPerStage = 4;  // u32 words of K per row per stage
 constexpr int kRowBytes = 128;     // expanded bytes per row per stage
 constexpr int PD = 4;              // packed prefetch depth (per producer thread)
@@ -60,20 +72,23 @@ struct Cfg {
     static constexpr int kStageA = kATmem ? 0 : BM * kRowBytes;
     static constexpr int kStageB = BN * kRowBytes;
     static constexpr int kStageBytes = kStageA + kStageB;
-    static constexpr int ES = kATmem ? 4 : 3;  // expanded stages
+    static constexpr int ES = kATmem ? 4 : 2;  // expanded stages
     // TMEM: 2 accumulator buffers of BN columns (+ ES A stages of 32 columns)
     static constexpr int kAccCols = BN;
     static constexpr int kAStageCol = 2 * BN;
     static constexpr int kTmemCols = 512;
     static_assert(2 * BN + (kATmem ? ES * 32 : 0) <= 512, "TMEM budget");
     // shared memory carve-up (offsets from the 1024-aligned base)
-    static constexpr int kStageStride = 17;  // epilogue transpose buffer row pitch (words)
+    // epilogue staging: per warp 2 buffers of 32 rows x 32 f32, row pitch 144 B
+    // (16 B of padding keeps the eight 16-byte row chunks conflict-free)
+    static constexpr int kStgPitch = 144;
+    static constexpr int kStgBytes = 32 * kStgPitch;
     static constexpr int off_exp = 0;
     static constexpr int off_pk = ES * kStageBytes;
     static constexpr int off_popc_a = off_pk + PD * kProducerWarps * 32 * 16;
     static constexpr int off_popc_b = off_popc_a + 2 * BM * 4;
     static constexpr int off_epi = off_popc_b + 2 * BN * 4;
-    static constexpr int off_bars = off_epi + kEpiWarps * 32 * kStageStride * 4;
+    static constexpr int off_bars = off_epi + kEpiWarps * 2 * kStgBytes;
     static constexpr int kNumBars = 2 * ES + 6;
     static constexpr int off_tmem = off_bars + kNumBars * 8;
     static constexpr int kSmemBytes = off_tmem + 16 + 1024;
@@ -154,6 +169,35 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 }
 
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+        "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
+        "%28, %29, %30, %31}, [%32];\n"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+          "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+          "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+          "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+
+// bulk async copy SMEM -> global (TMA engine), per-thread bulk groups
+__device__ __forceinline__ void bulk_store(void *gdst, uint32_t ssrc, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gdst),
+                 "r"(ssrc), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+    asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+
 __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&v)[8]) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(
@@ -202,7 +246,7 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem>::kThreads, 1)
     const uint32_t s_pk = sbase + C::off_pk;
     int32_t *s_popc_a = reinterpret_cast<int32_t *>(sgen + C::off_popc_a);
     int32_t *s_popc_b = reinterpret_cast<int32_t *>(sgen + C::off_popc_b);
-    uint32_t *s_epi = reinterpret_cast<uint32_t *>(sgen + C::off_epi);
+    const uint32_t s_epi = sbase + C::off_epi;
     const uint32_t bar_full = sbase + C::off_bars;      // [ES]
     const uint32_t bar_empty = bar_full + ES * 8;       // [ES]
     const uint32_t bar_tfull = bar_empty + ES * 8;      // [2] MMA -> epilogue
@@ -214,6 +258,7 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem>::kThreads, 1)
     const int64_t ktiles = ceil_div(kw32, kWordsPerStage);
 
     if (tid == 0) {
+        trace(0);
         for (int s = 0; s < ES; ++s) {
             mbar_init(bar_full + 8 * s, C::kProducerWarps);
             mbar_init(bar_empty + 8 * s, 1);
@@ -235,6 +280,7 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem>::kThreads, 1)
     __syncthreads();
     fence_after();
     const uint32_t tmem = *s_tmem;
+    if (tid == 0) trace(1);
 
     if (warp < C::kProducerWarps) {
         // ================================================================ producers
@@ -358,6 +404,7 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem>::kThreads, 1)
                 for (int64_t kt = 0; kt < ktiles; ++kt, ++gk) {
                     const int s = (int)(gk % ES);
                     mbar_wait(bar_full + 8 * s, (uint32_t)(gk / ES) & 1u);
+                    if (gk == 0) trace(2);
                     fence_after();
                     const uint32_t b_addr = s_exp + s * C::kStageBytes + C::kStageA;
 #pragma unroll
@@ -373,81 +420,113 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem>::kThreads, 1)
                     umma_commit(bar_empty + 8 * s);
                 }
                 umma_commit(bar_tfull + 8 * buf);
+                if (it < 3) trace(3 + 3 * it);
             }
         }
         __syncwarp();
     } else {
         // ================================================================ epilogue
         // 8 warps: quadrant q = warp % 4 owns TMEM lanes (= tile rows) 32q..32q+31;
-        // the two warps of a quadrant take alternating 16-column chunks.
+        // the two warps of a quadrant take alternating 32-column chunks.  Lane r
+        // decodes its row's 32 accumulators, writes them to a padded SMEM row and
+        // hands contiguous 16-byte-aligned runs to the TMA engine
+        // (cp.async.bulk), so the epilogue issues no per-element global stores.
         const int e = warp - C::kEpiWarp0;
         const int q = warp & 3, h = e >> 2;
-        uint32_t *stg = s_epi + e * 32 * C::kStageStride;
+        const uint32_t stg0 = s_epi + e * 2 * C::kStgBytes;
+        const bool ncontig = store.n_contiguous();
+        const int64_t M = store.rows(), N = store.cols();
+        int nb = 0;  // staging buffer toggle
         int it = 0;
 #pragma unroll 1
         for (int tile = blockIdx.x; tile < tmap.ntiles; tile += gridDim.x, ++it) {
             const int buf = it & 1;
             int tm, tn;
             tmap.decode(tile, tm, tn);
-            const int64_t mq = (int64_t)tm * BM + q * 32, n0 = (int64_t)tn * BN;
+            const int64_t m = (int64_t)tm * BM + q * 32 + lane, n0 = (int64_t)tn * BN;
             mbar_wait(bar_tfull + 8 * buf, (uint32_t)(it >> 1) & 1u);
             mbar_wait(bar_pfull + 8 * buf, (uint32_t)(it >> 1) & 1u);
             fence_after();
-            const int32_t *pa = s_popc_a + buf * BM + q * 32;
+            if (e == 0 && lane == 0 && it < 3) trace(4 + 3 * it);
+            const bool mok = m < M;
+            // per-row constants: P = kb - pb[n] + 2 * cnt
+            const int32_t kb = ep.k_eff - s_popc_a[buf * BM + q * 32 + lane];
+            const float sc = (mok && ep.scale) ? __ldg(ep.scale + m) : 1.0f;
+            const float sh = (mok && ep.shift) ? __ldg(ep.shift + m) : 0.0f;
             const int32_t *pb = s_popc_b + buf * BN;
             const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + buf * C::kAccCols;
-            const int64_t M = store.rows(), N = store.cols();
 #pragma unroll 1
-            for (int c = h; c < BN / 16; c += 2) {
-                uint32_t v[16];
-                tmem_ld16(taddr + c * 16, v);
-                if (mq >= M) continue;
-                if (store.n_contiguous()) {
-                    // transpose through SMEM so each store instruction writes two
-                    // 64-byte row segments (whole sectors) instead of 32 scattered words
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) stg[lane * C::kStageStride + j] = v[j];
-                    __syncwarp();
-                    const int jj = lane & 15, half = lane >> 4;
-                    const int64_t n = n0 + c * 16 + jj;
-                    if (n < N) {
-                        float *col = store.col_base(n);
-                        const int64_t ms = store.m_stride();
-                        const int32_t pbn = pb[c * 16 + jj];
-#pragma unroll 4
-                        for (int rr = 0; rr < 16; ++rr) {
-                            const int r = 2 * rr + half;
-                            const int64_t m = mq + r;
-                            if (m < M) {
-                                const int32_t cnt = (int32_t)(stg[r * C::kStageStride + jj] >> 7);
-                                col[m * ms] = ep.apply(pa[r] + pbn - 2 * cnt, (int)m);
-                            }
-                        }
-                    }
-                    __syncwarp();
+            for (int c = h; c * 32 < BN; c += 2) {
+                uint32_t v[32];
+                const int w = BN - c * 32 < 32 ? BN - c * 32 : 32;
+                if (w == 32) {
+                    tmem_ld32(taddr + c * 32, v);
                 } else {
-                    // rows are contiguous (e.g. an [N, M] output): lane = row stores
-                    const int64_t m = mq + lane;
-                    if (m < M) {
+                    uint32_t v16[16];
+                    tmem_ld16(taddr + c * 32, v16);
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) {
-                            const int64_t n = n0 + c * 16 + j;
-                            if (n < N) {
-                                const int32_t cnt = (int32_t)(v[j] >> 7);
-                                store.put(m, n, ep.apply(pa[lane] + pb[c * 16 + j] - 2 * cnt, (int)m));
+                    for (int j = 0; j < 16; ++j) v[j] = v16[j], v[16 + j] = 0;
+                }
+                const int64_t nc = n0 + c * 32;
+                if (!mok || nc >= N) continue;
+                float f[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const int32_t p = kb - pb[c * 32 + j] + 2 * (int32_t)(v[j] >> 7);
+                    const int32_t val = ep.domain == BNN_DOT ? 2 * p - ep.k_logical : p;
+                    f[j] = ep.scale || ep.shift ? __fadd_rn(__fmul_rn((float)val, sc), sh)
+                                                : (float)val;
+                }
+                if (ncontig) {
+                    const uint32_t row = stg0 + nb * C::kStgBytes + lane * C::kStgPitch;
+                    bulk_wait_read<1>();  // this buffer's previous copies have read SMEM
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(row + 16 * j),
+                                     "f"(f[4 * j]), "f"(f[4 * j + 1]), "f"(f[4 * j + 2]),
+                                     "f"(f[4 * j + 3]));
+                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                    // contiguous runs of this row (split at image / matrix edges)
+                    int off = 0;
+                    int64_t n = nc;
+                    while (off < w && n < N) {
+                        float *gp;
+                        const int len = store.run(m, n, w - off, gp);
+                        if (((reinterpret_cast<uintptr_t>(gp) | (uint32_t)(off * 4) |
+                              (uint32_t)(len * 4)) & 15) == 0) {
+                            bulk_store(gp, row + off * 4, len * 4);
+                        } else {
+                            for (int i = 0; i < len; ++i) {  // unaligned run: from SMEM
+                                float t;
+                                asm volatile("ld.shared.f32 %0, [%1];\n"
+                                             : "=f"(t)
+                                             : "r"(row + (off + i) * 4));
+                                gp[i] = t;
                             }
                         }
+                        off += len;
+                        n += len;
                     }
+                    bulk_commit();
+                    nb ^= 1;
+                } else {
+                    // rows contiguous in memory (e.g. an [N, M] output): lanes = rows
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        if (j < w && nc + j < N) store.put(m, nc + j, f[j]);
                 }
             }
             fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(bar_tempty + 8 * buf);
+            if (e == 0 && lane == 0 && it < 3) trace(5 + 3 * it);
         }
+        bulk_wait_all();
     }
 
     fence_before();
     __syncthreads();
+    if (tid == 0) trace(12);
     if (warp == C::kMmaWarp) {
         fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
@@ -555,6 +634,13 @@ int launch_bconv2d_umma(const uint64_t *x, int64_t B, int64_t C, int64_t H, int6
 }
 
 }  // namespace bnn
+
+extern "C" int bnn_umma_trace(uint64_t *buf) {
+    // debug: buf = device array of (#SMs x 16) u64 timestamps, or null to disable
+    if (cudaMemcpyToSymbol(bnn::umma::g_trace, &buf, sizeof(buf)) != cudaSuccess)
+        return bnn::set_error(BNN_ECUDA, "bnn_umma_trace: cudaMemcpyToSymbol failed");
+    return BNN_OK;
+}
 
 extern "C" int bnn_set_umma_variant(int v) {
     if (v < 0 || v > 1) return bnn::set_error(BNN_EINVAL, "umma variant must be 0 or 1");

@@ -127,6 +127,11 @@ struct GemmStore {
     __device__ int64_t m_stride() const { return ldc_m; }
     __device__ int64_t rows() const { return M; }
     __device__ int64_t cols() const { return N; }
+    // contiguous output run starting at (m, n), at most maxlen columns (n_contiguous only)
+    __device__ int run(int64_t m, int64_t n, int maxlen, float *&p) const {
+        p = C + m * ldc_m + n;
+        return (int)(N - n < maxlen ? N - n : maxlen);
+    }
     // four consecutive n of one row m (m < M checked by the caller)
     __device__ void put4(int64_t m, int64_t n, const float *v) const {
         float *p = C + m * ldc_m + n * ldc_n;
@@ -156,6 +161,13 @@ struct ConvStore {  // y NCHW [B, F, oh*ow]; m = filter, n = b*ohw + pixel
     __device__ int64_t m_stride() const { return ohw; }
     __device__ int64_t rows() const { return F; }
     __device__ int64_t cols() const { return npix; }
+    __device__ int run(int64_t m, int64_t n, int maxlen, float *&p) const {
+        const int64_t b = n / ohw, pp = n - b * ohw;
+        p = y + (b * F + m) * ohw + pp;
+        int64_t len = ohw - pp;
+        if (npix - n < len) len = npix - n;
+        return (int)(len < maxlen ? len : maxlen);
+    }
     __device__ void put4(int64_t m, int64_t n, const float *v) const {
         int64_t b = n / ohw, p = n - b * ohw;
         float *dst = y + (b * F + m) * ohw + p;

@@ -160,15 +160,19 @@ __global__ void __launch_bounds__(256) pack_nchw_kernel(const float *__restrict_
             q[i] = make_float4(0.f, 0.f, 0.f, 0.f);
             if (c < nc)
                 for (int j = 0; j < 4; ++j)
-                    if (p0 + p + j < HW) (&q[i].x)[j] = __ldg(src + c * HW + p + j);
+                    if (p0 + p + j < HW) {
+                        (&q[i].x)[j] = __ldg(src + c * HW + p + j);
+                        f |= elem_flags((&q[i].x)[j], mode);  // only real elements
+                    }
         }
     }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
         const int e = tid + 256 * i;
         const int c = e >> 5, p = 4 * (e & 31);
-        f |= elem_flags(q[i].x, mode) | elem_flags(q[i].y, mode) | elem_flags(q[i].z, mode) |
-             elem_flags(q[i].w, mode);
+        if (full)
+            f |= elem_flags(q[i].x, mode) | elem_flags(q[i].y, mode) | elem_flags(q[i].z, mode) |
+                 elem_flags(q[i].w, mode);
         *reinterpret_cast<float4 *>(&tile[c][p]) = q[i];
     }
     __syncthreads();
