@@ -34,7 +34,7 @@
 //                  tmem_full[buf]).
 //   warps P+1..P+8 epilogue: tcgen05.ld 32x32b.x16 of accumulator buffer
 //                  buf (double-buffered, so it overlaps the next tile's MMA),
-//                  decode, transpose through SMEM, sector-complete f32 stores;
+//                  decode, transpose through SMEM, coalesced 128-byte stores;
 //                  arrive tmem_empty[buf].
 #include <cstdlib>
 
@@ -49,6 +49,7 @@ constexpr int BM = 128;
 // slot s into g_trace[c * kTraceSlots + s].  Null in production.
 constexpr int kTraceSlots = 16;
 __device__ uint64_t *g_trace = nullptr;
+__device__ int g_epi_mode = 0;  // debug: 0 bulk stores, 1 STG.128 from registers, 2 no stores
 __device__ __forceinline__ void trace(int slot) {
     if (g_trace) {
         uint64_t t;
@@ -72,15 +73,15 @@ struct Cfg {
     static constexpr int kStageA = kATmem ? 0 : BM * kRowBytes;
     static constexpr int kStageB = BN * kRowBytes;
     static constexpr int kStageBytes = kStageA + kStageB;
-    static constexpr int ES = kATmem ? 4 : 2;  // expanded stages
+    static constexpr int ES = kATmem ? 4 : 3;  // expanded stages
     // TMEM: 2 accumulator buffers of BN columns (+ ES A stages of 32 columns)
     static constexpr int kAccCols = BN;
     static constexpr int kAStageCol = 2 * BN;
     static constexpr int kTmemCols = 512;
     static_assert(2 * BN + (kATmem ? ES * 32 : 0) <= 512, "TMEM budget");
     // shared memory carve-up (offsets from the 1024-aligned base)
-    // epilogue staging: per warp 2 buffers of 32 rows x 32 f32, row pitch 144 B
-    // (16 B of padding keeps the eight 16-byte row chunks conflict-free)
+    // epilogue staging: per warp 32 rows x 32 f32, row pitch 144 B (16 B of
+    // padding keeps both the row writes and the transposed reads conflict-free)
     static constexpr int kStgPitch = 144;
     static constexpr int kStgBytes = 32 * kStgPitch;
     static constexpr int off_exp = 0;
@@ -88,7 +89,7 @@ struct Cfg {
     static constexpr int off_popc_a = off_pk + PD * kProducerWarps * 32 * 16;
     static constexpr int off_popc_b = off_popc_a + 2 * BM * 4;
     static constexpr int off_epi = off_popc_b + 2 * BN * 4;
-    static constexpr int off_bars = off_epi + kEpiWarps * 2 * kStgBytes;
+    static constexpr int off_bars = off_epi + kEpiWarps * kStgBytes;
     static constexpr int kNumBars = 2 * ES + 6;
     static constexpr int off_tmem = off_bars + kNumBars * 8;
     static constexpr int kSmemBytes = off_tmem + 16 + 1024;
@@ -428,28 +429,32 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem>::kThreads, 1)
         // ================================================================ epilogue
         // 8 warps: quadrant q = warp % 4 owns TMEM lanes (= tile rows) 32q..32q+31;
         // the two warps of a quadrant take alternating 32-column chunks.  Lane r
-        // decodes its row's 32 accumulators, writes them to a padded SMEM row and
-        // hands contiguous 16-byte-aligned runs to the TMA engine
-        // (cp.async.bulk), so the epilogue issues no per-element global stores.
+        // decodes its row's 32 accumulators in registers and writes them to a
+        // padded SMEM row; the warp then re-reads the 32x32 block transposed so
+        // each st.global.v4 instruction covers four full 128-byte row segments.
         const int e = warp - C::kEpiWarp0;
         const int q = warp & 3, h = e >> 2;
-        const uint32_t stg0 = s_epi + e * 2 * C::kStgBytes;
+        const uint32_t stg = s_epi + e * C::kStgBytes;
         const bool ncontig = store.n_contiguous();
         const int64_t M = store.rows(), N = store.cols();
-        int nb = 0;  // staging buffer toggle
+        const int64_t ms = store.m_stride();
+        const bool affine = ep.scale || ep.shift;
+        const bool dot = ep.domain == BNN_DOT;
+        const bool magic = ep.k_logical < (1 << 21);  // int -> f32 via the 2^23 trick
         int it = 0;
 #pragma unroll 1
         for (int tile = blockIdx.x; tile < tmap.ntiles; tile += gridDim.x, ++it) {
             const int buf = it & 1;
             int tm, tn;
             tmap.decode(tile, tm, tn);
-            const int64_t m = (int64_t)tm * BM + q * 32 + lane, n0 = (int64_t)tn * BN;
+            const int64_t mq = (int64_t)tm * BM + q * 32, n0 = (int64_t)tn * BN;
+            const int64_t m = mq + lane;
             mbar_wait(bar_tfull + 8 * buf, (uint32_t)(it >> 1) & 1u);
             mbar_wait(bar_pfull + 8 * buf, (uint32_t)(it >> 1) & 1u);
             fence_after();
             if (e == 0 && lane == 0 && it < 3) trace(4 + 3 * it);
             const bool mok = m < M;
-            // per-row constants: P = kb - pb[n] + 2 * cnt
+            // per-row constants: P = kb - pb[n] + 2C, with 2C = acc >> 6 (acc = 128 C)
             const int32_t kb = ep.k_eff - s_popc_a[buf * BM + q * 32 + lane];
             const float sc = (mok && ep.scale) ? __ldg(ep.scale + m) : 1.0f;
             const float sh = (mok && ep.shift) ? __ldg(ep.shift + m) : 0.0f;
@@ -468,48 +473,58 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem>::kThreads, 1)
                     for (int j = 0; j < 16; ++j) v[j] = v16[j], v[16 + j] = 0;
                 }
                 const int64_t nc = n0 + c * 32;
-                if (!mok || nc >= N) continue;
+                if (mq >= M || nc >= N) continue;  // warp-uniform
                 float f[32];
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const int32_t p = kb - pb[c * 32 + j] + 2 * (int32_t)(v[j] >> 7);
-                    const int32_t val = ep.domain == BNN_DOT ? 2 * p - ep.k_logical : p;
-                    f[j] = ep.scale || ep.shift ? __fadd_rn(__fmul_rn((float)val, sc), sh)
-                                                : (float)val;
+                for (int j4 = 0; j4 < 8; ++j4) {
+                    const int4 pb4 = *reinterpret_cast<const int4 *>(pb + c * 32 + 4 * j4);
+                    const int32_t pbv[4] = {pb4.x, pb4.y, pb4.z, pb4.w};
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int j = 4 * j4 + i;
+                        int32_t val = kb - pbv[i] + (int32_t)(v[j] >> 6);
+                        if (dot) val = 2 * val - ep.k_logical;
+                        float x = magic ? __int_as_float(val + 0x4B400000) - 12582912.0f
+                                        : (float)val;
+                        f[j] = affine ? __fadd_rn(__fmul_rn(x, sc), sh) : x;
+                    }
                 }
                 if (ncontig) {
-                    const uint32_t row = stg0 + nb * C::kStgBytes + lane * C::kStgPitch;
-                    bulk_wait_read<1>();  // this buffer's previous copies have read SMEM
+                    const uint32_t row = stg + lane * C::kStgPitch;
 #pragma unroll
                     for (int j = 0; j < 8; ++j)
                         asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(row + 16 * j),
                                      "f"(f[4 * j]), "f"(f[4 * j + 1]), "f"(f[4 * j + 2]),
                                      "f"(f[4 * j + 3]));
-                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-                    // contiguous runs of this row (split at image / matrix edges)
-                    int off = 0;
-                    int64_t n = nc;
-                    while (off < w && n < N) {
-                        float *gp;
-                        const int len = store.run(m, n, w - off, gp);
-                        if (((reinterpret_cast<uintptr_t>(gp) | (uint32_t)(off * 4) |
-                              (uint32_t)(len * 4)) & 15) == 0) {
-                            bulk_store(gp, row + off * 4, len * 4);
-                        } else {
-                            for (int i = 0; i < len; ++i) {  // unaligned run: from SMEM
-                                float t;
-                                asm volatile("ld.shared.f32 %0, [%1];\n"
-                                             : "=f"(t)
-                                             : "r"(row + (off + i) * 4));
-                                gp[i] = t;
+                    __syncwarp();
+                    // transposed write-out: lane = (row quarter, 4-column segment)
+                    const int seg = lane & 7, rsub = lane >> 3;
+                    const int64_t n = nc + 4 * seg;
+                    if (4 * seg < w && n < N) {
+                        float *col;
+                        const bool v4 = store.col4(n, col);
+#pragma unroll 2
+                        for (int rr = 0; rr < 8; ++rr) {
+                            const int r = 4 * rr + rsub;
+                            const int64_t mr = mq + r;
+                            if (mr < M) {
+                                float4 t;
+                                asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+                                             : "=f"(t.x), "=f"(t.y), "=f"(t.z), "=f"(t.w)
+                                             : "r"(stg + r * C::kStgPitch + 16 * seg));
+                                if (v4) {
+                                    *reinterpret_cast<float4 *>(col + mr * ms) = t;
+                                } else {
+                                    const float tv[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+                                    for (int i = 0; i < 4; ++i)
+                                        if (4 * seg + i < w && n + i < N) store.put(mr, n + i, tv[i]);
+                                }
                             }
                         }
-                        off += len;
-                        n += len;
                     }
-                    bulk_commit();
-                    nb ^= 1;
-                } else {
+                    __syncwarp();
+                } else if (mok) {
                     // rows contiguous in memory (e.g. an [N, M] output): lanes = rows
 #pragma unroll
                     for (int j = 0; j < 32; ++j)
@@ -521,7 +536,6 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem>::kThreads, 1)
             if (lane == 0) mbar_arrive(bar_tempty + 8 * buf);
             if (e == 0 && lane == 0 && it < 3) trace(5 + 3 * it);
         }
-        bulk_wait_all();
     }
 
     fence_before();
@@ -639,6 +653,12 @@ extern "C" int bnn_umma_trace(uint64_t *buf) {
     // debug: buf = device array of (#SMs x 16) u64 timestamps, or null to disable
     if (cudaMemcpyToSymbol(bnn::umma::g_trace, &buf, sizeof(buf)) != cudaSuccess)
         return bnn::set_error(BNN_ECUDA, "bnn_umma_trace: cudaMemcpyToSymbol failed");
+    return BNN_OK;
+}
+
+extern "C" int bnn_umma_debug_epilogue(int mode) {
+    if (cudaMemcpyToSymbol(bnn::umma::g_epi_mode, &mode, sizeof(mode)) != cudaSuccess)
+        return bnn::set_error(BNN_ECUDA, "cudaMemcpyToSymbol failed");
     return BNN_OK;
 }
 

@@ -132,6 +132,12 @@ struct GemmStore {
         p = C + m * ldc_m + n;
         return (int)(N - n < maxlen ? N - n : maxlen);
     }
+    // column group n..n+3: base pointer (row 0) and whether a float4 store is legal
+    // for every row (n_contiguous only)
+    __device__ bool col4(int64_t n, float *&col) const {
+        col = C + n;
+        return n + 3 < N && ((reinterpret_cast<uintptr_t>(col) | (uintptr_t)(ldc_m * 4)) & 15) == 0;
+    }
     // four consecutive n of one row m (m < M checked by the caller)
     __device__ void put4(int64_t m, int64_t n, const float *v) const {
         float *p = C + m * ldc_m + n * ldc_n;
@@ -161,6 +167,12 @@ struct ConvStore {  // y NCHW [B, F, oh*ow]; m = filter, n = b*ohw + pixel
     __device__ int64_t m_stride() const { return ohw; }
     __device__ int64_t rows() const { return F; }
     __device__ int64_t cols() const { return npix; }
+    __device__ bool col4(int64_t n, float *&col) const {
+        const int64_t b = n / ohw, pp = n - b * ohw;
+        col = y + b * F * ohw + pp;
+        return pp + 3 < ohw && n + 3 < npix &&
+               ((reinterpret_cast<uintptr_t>(col) | (uintptr_t)(ohw * 4)) & 15) == 0;
+    }
     __device__ int run(int64_t m, int64_t n, int maxlen, float *&p) const {
         const int64_t b = n / ohw, pp = n - b * ohw;
         p = y + (b * F + m) * ohw + pp;
