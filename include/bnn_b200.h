@@ -163,8 +163,7 @@ int bnn_set_umma_variant(int variant);
  * (slot 0 start, 1 setup done, 2 first stage consumed, 3/6/9 tile MMA done,
  * 4/7/10 epilogue start, 5/8/11 epilogue end, 12 exit); null disables. */
 int bnn_umma_trace(uint64_t *buf);
-/* Debug: epilogue store mode (0 TMA bulk stores, 1 STG.128, 2 none -- wrong output). */
-int bnn_umma_debug_epilogue(int mode);
+
 
 /* Roofline probe (synchronous): measured issue rate of a pipe on the
  * current device.  pipe 0 = POPC (32-bit population counts per second).

@@ -44,7 +44,6 @@ SIGNATURES = {
     "bnn_probe_pipe_peak": (_i32, [_i32, _i64, _vp, _vp, _vp]),
     "bnn_set_umma_variant": (_i32, [_i32]),
     "bnn_umma_trace": (_i32, [_vp]),
-    "bnn_umma_debug_epilogue": (_i32, [_i32]),
 }
 
 

@@ -45,16 +45,15 @@ namespace umma {
 
 constexpr int BM = 128;
 
-// Debug timeline (bnn_umma_trace): when set, CTA c records %globaltimer at
-// slot s into g_trace[c * kTraceSlots + s].  Null in production.
+// Debug timeline (bnn_umma_trace): when a buffer is set, CTA c records
+// %globaltimer at slot s into trace_buf[c * kTraceSlots + s] (kernel argument,
+// null in production).
 constexpr int kTraceSlots = 16;
-__device__ uint64_t *g_trace = nullptr;
-__device__ int g_epi_mode = 0;  // debug: 0 bulk stores, 1 STG.128 from registers, 2 no stores
-__device__ __forceinline__ void trace(int slot) {
-    if (g_trace) {
+__device__ __forceinline__ void trace_at(uint64_t *buf, int slot) {
+    if (buf) {
         uint64_t t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        g_trace[blockIdx.x * kTraceSlots + slot] = t;
+        buf[blockIdx.x * kTraceSlots + slot] = t;
     }
 }
 constexpr int kWordsPerStage = 4;  // u32 words of K per row per stage
@@ -236,7 +235,8 @@ struct TileMap {
 template <int BN, bool kATmem, int kVec, class ALoad, class BLoad, class Store>
 __global__ void __launch_bounds__(Cfg<BN, kATmem>::kThreads, 1)
     xnor_umma_kernel(ALoad aload, BLoad bload, Store store, Epilogue ep, int64_t kw32,
-                     TileMap tmap) {
+                     TileMap tmap, uint64_t *trace_buf) {
+    auto trace = [&](int slot) { trace_at(trace_buf, slot); };
     using C = Cfg<BN, kATmem>;
     constexpr int ES = C::ES;
     extern __shared__ uint8_t smem_raw[];
@@ -550,6 +550,8 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem>::kThreads, 1)
 
 }  // namespace umma
 
+static uint64_t *g_trace_buf = nullptr;  // debug timeline (bnn_umma_trace)
+
 static int sm_count() {
     static int n = 0;
     if (n == 0) {
@@ -574,7 +576,7 @@ static int launch_umma_cfg(const ALoad &a, const BLoad &b, const Store &st, cons
     if (ntiles > (1ll << 30)) return set_error(BNN_EUNSUP, "too many tiles");
     umma::TileMap tmap{(int)tiles_m, (int)ntiles};
     const int grid = (int)(ntiles < sm_count() ? ntiles : sm_count());
-    kern<<<grid, C::kThreads, C::kSmemBytes, s>>>(a, b, st, ep, kw32, tmap);
+    kern<<<grid, C::kThreads, C::kSmemBytes, s>>>(a, b, st, ep, kw32, tmap, g_trace_buf);
     return check_launch("xnor_umma_kernel");
 }
 
@@ -651,14 +653,7 @@ int launch_bconv2d_umma(const uint64_t *x, int64_t B, int64_t C, int64_t H, int6
 
 extern "C" int bnn_umma_trace(uint64_t *buf) {
     // debug: buf = device array of (#SMs x 16) u64 timestamps, or null to disable
-    if (cudaMemcpyToSymbol(bnn::umma::g_trace, &buf, sizeof(buf)) != cudaSuccess)
-        return bnn::set_error(BNN_ECUDA, "bnn_umma_trace: cudaMemcpyToSymbol failed");
-    return BNN_OK;
-}
-
-extern "C" int bnn_umma_debug_epilogue(int mode) {
-    if (cudaMemcpyToSymbol(bnn::umma::g_epi_mode, &mode, sizeof(mode)) != cudaSuccess)
-        return bnn::set_error(BNN_ECUDA, "cudaMemcpyToSymbol failed");
+    bnn::g_trace_buf = buf;
     return BNN_OK;
 }
 

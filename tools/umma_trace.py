@@ -7,8 +7,7 @@ import paper_1705_09864_b200 as bnn
 
 lib = bnn.load_library()
 m, n, k = map(int, sys.argv[1:4])
-if len(sys.argv) > 4:
-    lib.bnn_umma_debug_epilogue(int(sys.argv[4]))
+
 W = (k + 63) // 64
 a = torch.randint(-2**63, 2**63 - 1, (m, W), device="cuda").view(torch.uint64)
 b = torch.randint(-2**63, 2**63 - 1, (n, W), device="cuda").view(torch.uint64)
