@@ -503,15 +503,29 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem>::kThreads, 1)
                     if (4 * seg < w && n < N) {
                         float *col;
                         const bool v4 = store.col4(n, col);
-#pragma unroll 2
-                        for (int rr = 0; rr < 8; ++rr) {
-                            const int r = 4 * rr + rsub;
-                            const int64_t mr = mq + r;
-                            if (mr < M) {
+                        const uint32_t src = stg + rsub * C::kStgPitch + 16 * seg;
+                        if (v4 && mq + 32 <= M) {
+                            // common case: 8 unpredicated 16-byte stores, pointer bumps only
+                            float *dst = col + (mq + rsub) * ms;
+                            const int64_t step = 4 * ms;
+#pragma unroll
+                            for (int rr = 0; rr < 8; ++rr) {
                                 float4 t;
                                 asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
                                              : "=f"(t.x), "=f"(t.y), "=f"(t.z), "=f"(t.w)
-                                             : "r"(stg + r * C::kStgPitch + 16 * seg));
+                                             : "r"(src + rr * 4 * C::kStgPitch));
+                                *reinterpret_cast<float4 *>(dst) = t;
+                                dst += step;
+                            }
+                        } else {
+                            for (int rr = 0; rr < 8; ++rr) {
+                                const int r = 4 * rr + rsub;
+                                const int64_t mr = mq + r;
+                                if (mr >= M) break;
+                                float4 t;
+                                asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+                                             : "=f"(t.x), "=f"(t.y), "=f"(t.z), "=f"(t.w)
+                                             : "r"(src + rr * 4 * C::kStgPitch));
                                 if (v4) {
                                     *reinterpret_cast<float4 *>(col + mr * ms) = t;
                                 } else {
