@@ -48,6 +48,12 @@ int launch_xnor_gemm_umma(const uint64_t *, int64_t, const uint64_t *, int64_t, 
 int launch_bconv2d_umma(const uint64_t *, int64_t, int64_t, int64_t, int64_t, const uint64_t *,
                         int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,
                         int64_t, float *, const Epilogue &, cudaStream_t);
+int launch_xnor_gemm_bmma(const uint64_t *, int64_t, const uint64_t *, int64_t, int64_t,
+                          int64_t, int64_t, float *, int64_t, int64_t, const Epilogue &,
+                          cudaStream_t);
+int launch_bconv2d_bmma(const uint64_t *, int64_t, int64_t, int64_t, int64_t, const uint64_t *,
+                        int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,
+                        int64_t, float *, const Epilogue &, cudaStream_t);
 int launch_bconv2d_popc(const uint64_t *, int64_t, int64_t, int64_t, int64_t, const uint64_t *,
                         int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,
                         int64_t, float *, const Epilogue &, cudaStream_t);
@@ -177,6 +183,9 @@ int bnn_xnor_gemm(const uint64_t *A, int64_t lda, const uint64_t *B, int64_t ldb
         case BNN_ALGO_POPC:
             return launch_xnor_gemm_popc(A, lda, B, ldb, M, N, K, C, ldc_m, ldc_n, ep,
                                          as_stream(stream));
+        case BNN_ALGO_BMMA:
+            return launch_xnor_gemm_bmma(A, lda, B, ldb, M, N, K, C, ldc_m, ldc_n, ep,
+                                         as_stream(stream));
         case BNN_ALGO_AUTO:
         case BNN_ALGO_UMMA:
             return launch_xnor_gemm_umma(A, lda, B, ldb, M, N, K, C, ldc_m, ldc_n, ep,
@@ -218,6 +227,9 @@ int bnn_bconv2d(const uint64_t *x_words, int64_t B, int64_t C, int64_t H, int64_
     switch (algo) {
         case BNN_ALGO_POPC:
             return launch_bconv2d_popc(x_words, B, C, H, W, w_dev, F, kh, kw, sh, sw, ph, pw, oh,
+                                       ow, y, ep, as_stream(stream));
+        case BNN_ALGO_BMMA:
+            return launch_bconv2d_bmma(x_words, B, C, H, W, w_dev, F, kh, kw, sh, sw, ph, pw, oh,
                                        ow, y, ep, as_stream(stream));
         case BNN_ALGO_AUTO:
         case BNN_ALGO_UMMA:

@@ -72,6 +72,7 @@ def test_gemm_validation_mirrors_gemmdims(lib):
     assert _gemm(lib, K=130, lda=2) == -5  # lda < ceil(K/64)
     assert _gemm(lib, domain=7) == -1
     assert _gemm(lib, algo=99) == -7
+    assert _gemm(lib, algo=2, M=0) == -2  # validation precedes engine dispatch
 
 
 def test_conv_and_pack_validation(lib):

@@ -19,7 +19,7 @@ from oracle import oracle as orc
 
 pytestmark = pytest.mark.gpu
 
-ALGOS = ["popc", "umma0", "umma1"]
+ALGOS = ["popc", "bmma", "umma0", "umma1"]
 
 
 def A(algo):

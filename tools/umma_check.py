@@ -18,6 +18,25 @@ for m, n, k in shapes:
         b.view(torch.int64)[:, -1] &= mask
     cp = bnn.xnor_rows_gemm(a, b, k, algo="popc")
     out = [f"{m}x{n}x{k}:"]
+    cb = bnn.xnor_rows_gemm(a, b, k, algo="bmma")
+    torch.cuda.synchronize()
+    for _ in range(2):
+        bnn.xnor_rows_gemm(a, b, k, algo="bmma")
+    s0, e0 = torch.cuda.Event(True), torch.cuda.Event(True)
+    s0.record()
+    for _ in range(5):
+        bnn.xnor_rows_gemm(a, b, k, algo="bmma")
+    e0.record(); e0.synchronize()
+    tb = s0.elapsed_time(e0) / 5
+    for _ in range(2):
+        bnn.xnor_rows_gemm(a, b, k, algo="popc")
+    s0.record()
+    for _ in range(5):
+        bnn.xnor_rows_gemm(a, b, k, algo="popc")
+    e0.record(); e0.synchronize()
+    tp = s0.elapsed_time(e0) / 5
+    out.append(f"popc {tp*1e3:.1f}us {2*m*n*k/(tp*1e-3)/1e12:.0f}T bmma equal={torch.equal(cp, cb)} "
+               f"{tb*1e3:.1f}us {2*m*n*k/(tb*1e-3)/1e12:.0f}T |")
     for variant in (0, 1):
         lib.bnn_set_umma_variant(variant)
         cu = bnn.xnor_rows_gemm(a, b, k, algo="umma")
