@@ -16,6 +16,15 @@ namespace bnn {
 
 __device__ __forceinline__ uint32_t sign_bit(float v) { return v >= 0.0f ? 1u : 0u; }
 
+// streaming 16-byte load that does not allocate in L1 (the input is read once)
+__device__ __forceinline__ float4 ld_stream(const float *p) {
+    float4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                 : "l"(p));
+    return r;
+}
+
 // Per-element checks: bit0 = non-finite, bit1 = not exactly +-1 (strict mode).
 __device__ __forceinline__ int elem_flags(float v, int mode) {
     int f = isfinite(v) ? 0 : BNN_FLAG_NONFINITE;
@@ -123,70 +132,71 @@ __global__ void pack_cols_kernel(const float *__restrict__ x, int64_t K, int64_t
 
 // ---------------------------------------------------------------- pack NCHW
 // x [B, C, H, W] -> out [B*H*W, Cw] u64 (NHWC words, channel tail 0).
-// CTA = (128 pixels, one 64-channel word, image b), 256 threads.  Phase 1
-// stages the 64 x 128 f32 tile in shared memory with coalesced float4 loads
-// (8 independent 16-byte loads per thread, 512 contiguous bytes per warp
-// instruction); phase 2 transposes: thread (pixel p, half h) folds channels
-// 32h..32h+31 of pixel p into a u32 and the two halves form the u64 word.
-constexpr int kPackPix = 128;
-template <bool kVec4>
+// Warp = 32 channels x 16 pixels: lane l streams 64 contiguous bytes (4 x
+// 16-byte loads, no L1 allocation) of channel c0 + l, then one __ballot_sync
+// per pixel turns the 32 lanes' signs into that pixel's u32 channel word (the
+// low or high half of its u64).  No shared memory, ~2 instructions per 32
+// elements for the transpose; finiteness is checked per float4 with an
+// overflow-free FFMA sum that propagates NaN/Inf.
+constexpr int kPixPerLane = 16;
+template <bool kVec4, bool kStrict>
 __global__ void __launch_bounds__(256) pack_nchw_kernel(const float *__restrict__ x, int64_t B,
                                                         int64_t C, int64_t HW, int64_t Cw,
-                                                        uint64_t *__restrict__ out, int mode,
+                                                        uint32_t *__restrict__ out32,
                                                         int32_t *flags) {
-    __shared__ float tile[64][kPackPix + 4];
-    __shared__ uint32_t hi_half[kPackPix];
-    const int tid = threadIdx.x;
-    const int64_t p0 = (int64_t)blockIdx.x * kPackPix;
-    const int64_t cw = blockIdx.y, b = blockIdx.z;
-    const int nc = (int)(C - cw * 64 < 64 ? C - cw * 64 : 64);
-    const float *src = x + (b * C + cw * 64) * HW + p0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t p0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * kPixPerLane;
+    const int64_t half = blockIdx.y;  // 32-channel group: word half (half & 1) of u64 half >> 1
+    const int64_t b = blockIdx.z;
+    const int64_t c = half * 32 + lane;
+    const bool cok = c < C;
+    if (p0 >= HW) return;  // warp-uniform
+    float v[kPixPerLane];
     int f = 0;
-    float4 q[8];
-    // issue all eight 16-byte loads before touching any of them (MLP = 8);
-    // the full-tile case has no per-load predicates so they batch cleanly
-    const bool full = kVec4 && nc == 64 && p0 + kPackPix <= HW;
-    if (full) {
+    const float *src = x + (b * C + (cok ? c : 0)) * HW + p0;
+    if (kVec4 && p0 + kPixPerLane <= HW) {
+        float4 q[kPixPerLane / 4];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int e = tid + 256 * i;  // 2048 float4 slots = 64 channels x 32 quads
-            q[i] = __ldg(reinterpret_cast<const float4 *>(src + (e >> 5) * HW + 4 * (e & 31)));
+        for (int i = 0; i < kPixPerLane / 4; ++i) {
+            if (cok) {
+                asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+                             : "=f"(q[i].x), "=f"(q[i].y), "=f"(q[i].z), "=f"(q[i].w)
+                             : "l"(src + 4 * i));
+            } else {
+                q[i] = make_float4(-1.f, -1.f, -1.f, -1.f);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < kPixPerLane / 4; ++i) {
+            v[4 * i] = q[i].x; v[4 * i + 1] = q[i].y; v[4 * i + 2] = q[i].z; v[4 * i + 3] = q[i].w;
+            // NaN/Inf propagate through the scaled |.| sum; finite inputs cannot overflow
+            const float s = fmaf(fabsf(q[i].x), 0.25f, fmaf(fabsf(q[i].y), 0.25f,
+                            fmaf(fabsf(q[i].z), 0.25f, fabsf(q[i].w) * 0.25f)));
+            if (!(s <= 3.402823466e38f)) f |= BNN_FLAG_NONFINITE;
         }
     } else {
-#pragma unroll 1
-        for (int i = 0; i < 8; ++i) {
-            const int e = tid + 256 * i;
-            const int c = e >> 5, p = 4 * (e & 31);
-            q[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (c < nc)
-                for (int j = 0; j < 4; ++j)
-                    if (p0 + p + j < HW) {
-                        (&q[i].x)[j] = __ldg(src + c * HW + p + j);
-                        f |= elem_flags((&q[i].x)[j], mode);  // only real elements
-                    }
+#pragma unroll
+        for (int i = 0; i < kPixPerLane; ++i) {
+            v[i] = -1.f;
+            if (cok && p0 + i < HW) {
+                v[i] = __ldg(src + i);
+                if (!isfinite(v[i])) f |= BNN_FLAG_NONFINITE;
+            }
         }
     }
+    if (kStrict) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const int e = tid + 256 * i;
-        const int c = e >> 5, p = 4 * (e & 31);
-        if (full)
-            f |= elem_flags(q[i].x, mode) | elem_flags(q[i].y, mode) | elem_flags(q[i].z, mode) |
-                 elem_flags(q[i].w, mode);
-        *reinterpret_cast<float4 *>(&tile[c][p]) = q[i];
+        for (int i = 0; i < kPixPerLane; ++i)
+            if (cok && p0 + i < HW && v[i] != 1.0f && v[i] != -1.0f) f |= BNN_FLAG_NOTSIGN;
     }
-    __syncthreads();
-    const int p = tid & (kPackPix - 1), h = tid >> 7;
-    uint32_t word = 0;
+    uint32_t mine = 0;
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-        const int c = 32 * h + i;
-        word |= (c < nc ? sign_bit(tile[c][p]) : 0u) << i;
+    for (int i = 0; i < kPixPerLane; ++i) {
+        const uint32_t w = __ballot_sync(0xffffffffu, cok && v[i] >= 0.0f);  // sign(-0) = +1
+        if (lane == i) mine = w;
     }
-    if (h == 1) hi_half[p] = word;
-    __syncthreads();
-    if (h == 0 && p0 + p < HW)
-        out[(b * HW + p0 + p) * Cw + cw] = (uint64_t)word | ((uint64_t)hi_half[p] << 32);
+    if (lane < kPixPerLane && p0 + lane < HW)
+        out32[(b * HW + p0 + lane) * (2 * Cw) + half] = mine;
     flush_flags(f, flags);
 }
 
@@ -276,12 +286,19 @@ int launch_pack_nchw(const float *x, int64_t B, int64_t C, int64_t H, int64_t W,
                      int mode, int32_t *flags, cudaStream_t s) {
     const int64_t HW = H * W, Cw = ceil_div(C, 64);
     if (B == 0 || HW == 0 || C == 0) return BNN_OK;
-    dim3 grid((unsigned)ceil_div(HW, kPackPix), (unsigned)Cw, (unsigned)B);
+    // 8 warps x 16 pixels per block; one block row per 32-channel half-word
+    dim3 grid((unsigned)ceil_div(HW, 8 * kPixPerLane), (unsigned)(2 * Cw), (unsigned)B);
+    uint32_t *o32 = reinterpret_cast<uint32_t *>(out);
     const bool vec4 = (HW % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
-    if (vec4)
-        pack_nchw_kernel<true><<<grid, 256, 0, s>>>(x, B, C, HW, Cw, out, mode, flags);
+    const bool strict = mode == BNN_PACK_STRICT;
+    if (vec4 && !strict)
+        pack_nchw_kernel<true, false><<<grid, 256, 0, s>>>(x, B, C, HW, Cw, o32, flags);
+    else if (vec4)
+        pack_nchw_kernel<true, true><<<grid, 256, 0, s>>>(x, B, C, HW, Cw, o32, flags);
+    else if (!strict)
+        pack_nchw_kernel<false, false><<<grid, 256, 0, s>>>(x, B, C, HW, Cw, o32, flags);
     else
-        pack_nchw_kernel<false><<<grid, 256, 0, s>>>(x, B, C, HW, Cw, out, mode, flags);
+        pack_nchw_kernel<false, true><<<grid, 256, 0, s>>>(x, B, C, HW, Cw, o32, flags);
     return check_launch("pack_nchw_kernel");
 }
 
