@@ -132,71 +132,87 @@ __global__ void pack_cols_kernel(const float *__restrict__ x, int64_t K, int64_t
 
 // ---------------------------------------------------------------- pack NCHW
 // x [B, C, H, W] -> out [B*H*W, Cw] u64 (NHWC words, channel tail 0).
-// Warp = 32 channels x 16 pixels: lane l streams 64 contiguous bytes (4 x
-// 16-byte loads, no L1 allocation) of channel c0 + l, then one __ballot_sync
-// per pixel turns the 32 lanes' signs into that pixel's u32 channel word (the
-// low or high half of its u64).  No shared memory, ~2 instructions per 32
-// elements for the transpose; finiteness is checked per float4 with an
-// overflow-free FFMA sum that propagates NaN/Inf.
-constexpr int kPixPerLane = 16;
+// CTA = (128 pixels, one 64-channel word, image b), 256 threads.
+//  1. fully coalesced loads: each warp instruction reads 512 contiguous bytes
+//     (one channel, 128 pixels); 8 x 16 B per thread in flight, no L1 alloc;
+//     staged in a 64 x 128 f32 SMEM tile whose 16-byte units are XOR-swizzled
+//     by (channel & 7), so both the row writes and the column reads below are
+//     bank-conflict free.
+//  2. transpose by ballot: lane l reads 4 pixels of channel 32h + l
+//     (ld.shared.v4) and one __ballot_sync per pixel yields that pixel's u32
+//     channel word -- 32 elements per VOTE instruction.
+// Finiteness: per float4, an overflow-free FFMA sum of |x|/4 propagates NaN/Inf.
+constexpr int kPackPix = 128;
 template <bool kVec4, bool kStrict>
 __global__ void __launch_bounds__(256) pack_nchw_kernel(const float *__restrict__ x, int64_t B,
                                                         int64_t C, int64_t HW, int64_t Cw,
                                                         uint32_t *__restrict__ out32,
                                                         int32_t *flags) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t p0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * kPixPerLane;
-    const int64_t half = blockIdx.y;  // 32-channel group: word half (half & 1) of u64 half >> 1
-    const int64_t b = blockIdx.z;
-    const int64_t c = half * 32 + lane;
-    const bool cok = c < C;
-    if (p0 >= HW) return;  // warp-uniform
-    float v[kPixPerLane];
+    __shared__ __align__(16) float tile[64 * kPackPix];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t p0 = (int64_t)blockIdx.x * kPackPix;
+    const int64_t cw = blockIdx.y, b = blockIdx.z;
+    const int nc = (int)(C - cw * 64 < 64 ? C - cw * 64 : 64);
+    const float *src = x + (b * C + cw * 64) * HW + p0;
     int f = 0;
-    const float *src = x + (b * C + (cok ? c : 0)) * HW + p0;
-    if (kVec4 && p0 + kPixPerLane <= HW) {
-        float4 q[kPixPerLane / 4];
+    const bool full = kVec4 && nc == 64 && p0 + kPackPix <= HW;
+    float4 q[8];
+    if (full) {
 #pragma unroll
-        for (int i = 0; i < kPixPerLane / 4; ++i) {
-            if (cok) {
-                asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];\n"
-                             : "=f"(q[i].x), "=f"(q[i].y), "=f"(q[i].z), "=f"(q[i].w)
-                             : "l"(src + 4 * i));
-            } else {
-                q[i] = make_float4(-1.f, -1.f, -1.f, -1.f);
-            }
-        }
-#pragma unroll
-        for (int i = 0; i < kPixPerLane / 4; ++i) {
-            v[4 * i] = q[i].x; v[4 * i + 1] = q[i].y; v[4 * i + 2] = q[i].z; v[4 * i + 3] = q[i].w;
-            // NaN/Inf propagate through the scaled |.| sum; finite inputs cannot overflow
-            const float s = fmaf(fabsf(q[i].x), 0.25f, fmaf(fabsf(q[i].y), 0.25f,
-                            fmaf(fabsf(q[i].z), 0.25f, fabsf(q[i].w) * 0.25f)));
-            if (!(s <= 3.402823466e38f)) f |= BNN_FLAG_NONFINITE;
+        for (int i = 0; i < 8; ++i) {
+            const int e = tid + 256 * i;  // 2048 float4 = 64 channels x 32 quads
+            const float *pp = src + (e >> 5) * HW + 4 * (e & 31);
+            asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+                         : "=f"(q[i].x), "=f"(q[i].y), "=f"(q[i].z), "=f"(q[i].w)
+                         : "l"(pp));
         }
     } else {
-#pragma unroll
-        for (int i = 0; i < kPixPerLane; ++i) {
-            v[i] = -1.f;
-            if (cok && p0 + i < HW) {
-                v[i] = __ldg(src + i);
-                if (!isfinite(v[i])) f |= BNN_FLAG_NONFINITE;
-            }
+#pragma unroll 1
+        for (int i = 0; i < 8; ++i) {
+            const int e = tid + 256 * i;
+            const int c = e >> 5, p = 4 * (e & 31);
+            float t[4] = {-1.f, -1.f, -1.f, -1.f};  // absent channels / pixels: bit 0
+            if (c < nc)
+                for (int j = 0; j < 4; ++j)
+                    if (p0 + p + j < HW) t[j] = __ldg(src + c * HW + p + j);
+            q[i] = make_float4(t[0], t[1], t[2], t[3]);
         }
     }
-    if (kStrict) {
 #pragma unroll
-        for (int i = 0; i < kPixPerLane; ++i)
-            if (cok && p0 + i < HW && v[i] != 1.0f && v[i] != -1.0f) f |= BNN_FLAG_NOTSIGN;
-    }
-    uint32_t mine = 0;
+    for (int i = 0; i < 8; ++i) {
+        const int e = tid + 256 * i;
+        const int c = e >> 5, unit = e & 31;
+        const float sum = fmaf(fabsf(q[i].x), 0.25f, fmaf(fabsf(q[i].y), 0.25f,
+                          fmaf(fabsf(q[i].z), 0.25f, fabsf(q[i].w) * 0.25f)));
+        if (!(sum <= 3.402823466e38f)) f |= BNN_FLAG_NONFINITE;
+        if (kStrict && c < nc) {
+            const float tv[4] = {q[i].x, q[i].y, q[i].z, q[i].w};
 #pragma unroll
-    for (int i = 0; i < kPixPerLane; ++i) {
-        const uint32_t w = __ballot_sync(0xffffffffu, cok && v[i] >= 0.0f);  // sign(-0) = +1
-        if (lane == i) mine = w;
+            for (int j = 0; j < 4; ++j)
+                if (p0 + 4 * unit + j < HW && tv[j] != 1.0f && tv[j] != -1.0f)
+                    f |= BNN_FLAG_NOTSIGN;
+        }
+        *reinterpret_cast<float4 *>(&tile[c * kPackPix + 4 * (unit ^ (c & 7))]) = q[i];
     }
-    if (lane < kPixPerLane && p0 + lane < HW)
-        out32[(b * HW + p0 + lane) * (2 * Cw) + half] = mine;
+    __syncthreads();
+    // 64 items = (2 channel halves) x (32 pixel quads); 8 per warp
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+        const int item = warp * 8 + it;
+        const int h = item & 1, quad = item >> 1;
+        const int c = 32 * h + lane;
+        const float4 t = *reinterpret_cast<const float4 *>(&tile[c * kPackPix + 4 * (quad ^ (c & 7))]);
+        const bool ok = c < nc;
+        const uint32_t w0 = __ballot_sync(0xffffffffu, ok && t.x >= 0.0f);  // sign(-0) = +1
+        const uint32_t w1 = __ballot_sync(0xffffffffu, ok && t.y >= 0.0f);
+        const uint32_t w2 = __ballot_sync(0xffffffffu, ok && t.z >= 0.0f);
+        const uint32_t w3 = __ballot_sync(0xffffffffu, ok && t.w >= 0.0f);
+        if (lane < 4) {
+            const int64_t p = p0 + 4 * quad + lane;
+            const uint32_t w = lane == 0 ? w0 : lane == 1 ? w1 : lane == 2 ? w2 : w3;
+            if (p < HW) out32[(b * HW + p) * (2 * Cw) + 2 * cw + h] = w;
+        }
+    }
     flush_flags(f, flags);
 }
 
@@ -286,8 +302,7 @@ int launch_pack_nchw(const float *x, int64_t B, int64_t C, int64_t H, int64_t W,
                      int mode, int32_t *flags, cudaStream_t s) {
     const int64_t HW = H * W, Cw = ceil_div(C, 64);
     if (B == 0 || HW == 0 || C == 0) return BNN_OK;
-    // 8 warps x 16 pixels per block; one block row per 32-channel half-word
-    dim3 grid((unsigned)ceil_div(HW, 8 * kPixPerLane), (unsigned)(2 * Cw), (unsigned)B);
+    dim3 grid((unsigned)ceil_div(HW, kPackPix), (unsigned)Cw, (unsigned)B);
     uint32_t *o32 = reinterpret_cast<uint32_t *>(out);
     const bool vec4 = (HW % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
     const bool strict = mode == BNN_PACK_STRICT;
