@@ -16,6 +16,10 @@ namespace bnn {
 
 __device__ __forceinline__ uint32_t sign_bit(float v) { return v >= 0.0f ? 1u : 0u; }
 
+__device__ __forceinline__ uint32_t smem_u32_pack(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
 // streaming 16-byte load that does not allocate in L1 (the input is read once)
 __device__ __forceinline__ float4 ld_stream(const float *p) {
     float4 r;
@@ -167,7 +171,7 @@ __global__ void __launch_bounds__(256) pack_nchw_kernel(const float *__restrict_
                          : "l"(pp));
         }
     } else {
-#pragma unroll 1
+#pragma unroll
         for (int i = 0; i < 8; ++i) {
             const int e = tid + 256 * i;
             const int c = e >> 5, p = 4 * (e & 31);
@@ -267,6 +271,90 @@ __global__ void conv_weights_reorder_kernel(const uint64_t *__restrict__ w_ref, 
     w_dev[idx] = word;
 }
 
+// ---------------------------------------------------------------- pack NCHW (TMA)
+// Streaming variant for HW % 4 == 0: CTA = (image b, 32-channel group g,
+// pixel chunk).  One elected thread issues 32 cp.async.bulk copies (one
+// contiguous channel segment each, TMA engine, mbarrier complete_tx) into a
+// SMEM tile whose row pitch is chosen so lane l's 16-byte column reads fall in
+// distinct bank quads; then each warp transposes 4 pixels per ld.shared.v4
+// with four __ballot_sync (32 channels -> one u32 word per pixel).
+constexpr int kTmaPixMax = 1024;  // pixels per CTA chunk (<= 132 KB of SMEM)
+__device__ __forceinline__ int tma_pitch(int npix) { return ((npix + 31) & ~31) + 4; }
+
+template <bool kStrict>
+__global__ void __launch_bounds__(256) pack_nchw_tma_kernel(const float *__restrict__ x,
+                                                            int64_t C, int64_t HW, int64_t Cw,
+                                                            uint32_t *__restrict__ out32,
+                                                            int32_t *flags) {
+    extern __shared__ __align__(128) float tile_t[];
+    __shared__ __align__(8) uint64_t bar;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t g = blockIdx.y, b = blockIdx.z;
+    const int64_t p0 = (int64_t)blockIdx.x * kTmaPixMax;
+    const int npix = (int)(HW - p0 < kTmaPixMax ? HW - p0 : kTmaPixMax);
+    const int pitch = tma_pitch(npix);
+    const int nc = (int)(C - g * 32 < 32 ? C - g * 32 : 32);
+    const uint32_t sbar = smem_u32_pack(&bar);
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sbar));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0) {
+        const uint32_t bytes = (uint32_t)npix * 4u;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sbar),
+                     "r"(bytes * (uint32_t)nc)
+                     : "memory");
+        for (int c = 0; c < nc; ++c) {
+            const float *src = x + (b * C + g * 32 + c) * HW + p0;
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+                "[%3];\n" ::"r"(smem_u32_pack(tile_t + c * pitch)),
+                "l"(src), "r"(bytes), "r"(sbar)
+                : "memory");
+        }
+    }
+    // wait for the tile (phase 0)
+    {
+        uint32_t done = 0;
+        do {
+            asm volatile(
+                "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n"
+                "selp.u32 %0, 1, 0, p;\n}\n"
+                : "=r"(done)
+                : "r"(sbar)
+                : "memory");
+        } while (!done);
+    }
+    int f = 0;
+    const bool cok = lane < nc;
+    const int nquads = (npix + 3) >> 2;
+    for (int qd = warp; qd < nquads; qd += 8) {
+        float4 t = make_float4(-1.f, -1.f, -1.f, -1.f);
+        if (cok) t = *reinterpret_cast<const float4 *>(tile_t + lane * pitch + 4 * qd);
+        const float tv[4] = {t.x, t.y, t.z, t.w};
+        const int left = npix - 4 * qd;  // valid pixels in this quad (>= 1)
+        float sum = 0.f;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float a = (j < left && cok) ? tv[j] : 0.f;
+            sum = fmaf(fabsf(a), 0.25f, sum);
+            if (kStrict && j < left && cok && a != 1.0f && a != -1.0f) f |= BNN_FLAG_NOTSIGN;
+        }
+        if (!(sum <= 3.402823466e38f)) f |= BNN_FLAG_NONFINITE;
+        const uint32_t w0 = __ballot_sync(0xffffffffu, cok && t.x >= 0.0f);  // sign(-0) = +1
+        const uint32_t w1 = __ballot_sync(0xffffffffu, cok && t.y >= 0.0f);
+        const uint32_t w2 = __ballot_sync(0xffffffffu, cok && t.z >= 0.0f);
+        const uint32_t w3 = __ballot_sync(0xffffffffu, cok && t.w >= 0.0f);
+        if (lane < 4 && lane < left) {
+            const int64_t p = p0 + 4 * qd + lane;
+            const uint32_t w = lane == 0 ? w0 : lane == 1 ? w1 : lane == 2 ? w2 : w3;
+            out32[(b * HW + p) * (2 * Cw) + g] = w;
+        }
+    }
+    flush_flags(f, flags);
+}
+
 // ================================================================ launchers
 int launch_binarize(const float *x, int64_t n, float *out, int32_t *flags, cudaStream_t s) {
     if (n == 0) return BNN_OK;
@@ -302,18 +390,37 @@ int launch_pack_nchw(const float *x, int64_t B, int64_t C, int64_t H, int64_t W,
                      int mode, int32_t *flags, cudaStream_t s) {
     const int64_t HW = H * W, Cw = ceil_div(C, 64);
     if (B == 0 || HW == 0 || C == 0) return BNN_OK;
-    dim3 grid((unsigned)ceil_div(HW, kPackPix), (unsigned)Cw, (unsigned)B);
     uint32_t *o32 = reinterpret_cast<uint32_t *>(out);
-    const bool vec4 = (HW % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
     const bool strict = mode == BNN_PACK_STRICT;
-    if (vec4 && !strict)
-        pack_nchw_kernel<true, false><<<grid, 256, 0, s>>>(x, B, C, HW, Cw, o32, flags);
-    else if (vec4)
-        pack_nchw_kernel<true, true><<<grid, 256, 0, s>>>(x, B, C, HW, Cw, o32, flags);
-    else if (!strict)
-        pack_nchw_kernel<false, false><<<grid, 256, 0, s>>>(x, B, C, HW, Cw, o32, flags);
-    else
+    const bool aligned = (HW % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+    if (aligned) {
+        // TMA streaming path: 32-channel groups, contiguous bulk copies
+        const int chunk = (int)(HW < kTmaPixMax ? HW : kTmaPixMax);
+        const int pitch = ((chunk + 31) & ~31) + 4;
+        const int smem = 32 * pitch * 4;
+        dim3 grid((unsigned)ceil_div(HW, kTmaPixMax), (unsigned)ceil_div(C, 32), (unsigned)B);
+        if (strict) {
+            static bool cfg = false;
+            if (!cfg) cudaFuncSetAttribute(pack_nchw_tma_kernel<true>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 32 * (kTmaPixMax + 4) * 4), cfg = true;
+            pack_nchw_tma_kernel<true><<<grid, 256, smem, s>>>(x, C, HW, Cw, o32, flags);
+        } else {
+            static bool cfg = false;
+            if (!cfg) cudaFuncSetAttribute(pack_nchw_tma_kernel<false>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 32 * (kTmaPixMax + 4) * 4), cfg = true;
+            pack_nchw_tma_kernel<false><<<grid, 256, smem, s>>>(x, C, HW, Cw, o32, flags);
+        }
+        // channel-tail words of odd 32-groups (C % 64 in (0, 32]) must read 0
+        if (ceil_div(C, 32) % 2 == 1) {
+            cudaMemset2DAsync(o32 + 2 * Cw - 1, 2 * Cw * 4, 0, 4, (size_t)(B * HW), s);
+        }
+        return check_launch("pack_nchw_tma_kernel");
+    }
+    dim3 grid((unsigned)ceil_div(HW, kPackPix), (unsigned)Cw, (unsigned)B);
+    if (strict)
         pack_nchw_kernel<false, true><<<grid, 256, 0, s>>>(x, B, C, HW, Cw, o32, flags);
+    else
+        pack_nchw_kernel<false, false><<<grid, 256, 0, s>>>(x, B, C, HW, Cw, o32, flags);
     return check_launch("pack_nchw_kernel");
 }
 
