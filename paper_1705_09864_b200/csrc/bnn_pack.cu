@@ -136,86 +136,101 @@ __global__ void pack_cols_kernel(const float *__restrict__ x, int64_t K, int64_t
 
 // ---------------------------------------------------------------- pack NCHW
 // x [B, C, H, W] -> out [B*H*W, Cw] u64 (NHWC words, channel tail 0).
-// CTA = (128 pixels, one 64-channel word, image b), 256 threads.
-//  1. fully coalesced loads: each warp instruction reads 512 contiguous bytes
-//     (one channel, 128 pixels); 8 x 16 B per thread in flight, no L1 alloc;
-//     staged in a 64 x 128 f32 SMEM tile whose 16-byte units are XOR-swizzled
-//     by (channel & 7), so both the row writes and the column reads below are
-//     bank-conflict free.
-//  2. transpose by ballot: lane l reads 4 pixels of channel 32h + l
-//     (ld.shared.v4) and one __ballot_sync per pixel yields that pixel's u32
-//     channel word -- 32 elements per VOTE instruction.
+// CTA = (64 pixels of image b, all channels in chunks of 256), 256 threads.
+//  1. cp.async 16-byte pieces (a warp covers two 256-byte channel rows per
+//     instruction) into a 256 x 64 f32 SMEM tile whose 16-byte units are
+//     XOR-swizzled by (channel & 7) -- conflict-free column reads below;
+//  2. transpose by ballot: lane l reads 4 pixels of channel 32g + l
+//     (ld.shared.v4) and one __ballot_sync per pixel yields that pixel's
+//     32-channel u32 word (32 elements per VOTE);
+//  3. the words are collected in SMEM and written as one contiguous
+//     64 x (Cw u64) block with 16-byte stores (scattered 4-byte stores of the
+//     words themselves made the previous versions L2-transaction bound).
 // Finiteness: per float4, an overflow-free FFMA sum of |x|/4 propagates NaN/Inf.
-constexpr int kPackPix = 128;
+constexpr int kPackPix = 64, kPackChunkC = 256;
 template <bool kVec4, bool kStrict>
 __global__ void __launch_bounds__(256) pack_nchw_kernel(const float *__restrict__ x, int64_t B,
                                                         int64_t C, int64_t HW, int64_t Cw,
                                                         uint32_t *__restrict__ out32,
                                                         int32_t *flags) {
-    __shared__ __align__(16) float tile[64 * kPackPix];
+    extern __shared__ __align__(128) uint8_t pk_smem[];
+    float *tile = reinterpret_cast<float *>(pk_smem);                       // [256][64]
+    uint32_t *words = reinterpret_cast<uint32_t *>(pk_smem + kPackChunkC * kPackPix * 4);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t p0 = (int64_t)blockIdx.x * kPackPix;
-    const int64_t cw = blockIdx.y, b = blockIdx.z;
-    const int nc = (int)(C - cw * 64 < 64 ? C - cw * 64 : 64);
-    const float *src = x + (b * C + cw * 64) * HW + p0;
+    const int64_t b = blockIdx.y;
+    const int npix = (int)(HW - p0 < kPackPix ? HW - p0 : kPackPix);
+    const int nw32 = (int)(2 * Cw);  // u32 words per pixel
     int f = 0;
-    const bool full = kVec4 && nc == 64 && p0 + kPackPix <= HW;
-    float4 q[8];
-    if (full) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int e = tid + 256 * i;  // 2048 float4 = 64 channels x 32 quads
-            const float *pp = src + (e >> 5) * HW + 4 * (e & 31);
-            asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];\n"
-                         : "=f"(q[i].x), "=f"(q[i].y), "=f"(q[i].z), "=f"(q[i].w)
-                         : "l"(pp));
-        }
-    } else {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
+    for (int64_t c0 = 0; c0 < C; c0 += kPackChunkC) {
+        const int nc = (int)(C - c0 < kPackChunkC ? C - c0 : kPackChunkC);
+        const float *src = x + (b * C + c0) * HW + p0;
+        // 256 channels x 16 units of 16 B = 4096 pieces, 16 per thread
+#pragma unroll 4
+        for (int i = 0; i < 16; ++i) {
             const int e = tid + 256 * i;
-            const int c = e >> 5, p = 4 * (e & 31);
-            float t[4] = {-1.f, -1.f, -1.f, -1.f};  // absent channels / pixels: bit 0
-            if (c < nc)
-                for (int j = 0; j < 4; ++j)
-                    if (p0 + p + j < HW) t[j] = __ldg(src + c * HW + p + j);
-            q[i] = make_float4(t[0], t[1], t[2], t[3]);
-        }
-    }
+            const int c = e >> 4, u = e & 15;
+            const uint32_t dst = smem_u32_pack(tile + c * kPackPix + 4 * (u ^ (c & 7)));
+            if (kVec4) {
+                const int valid = (c < nc) ? (npix - 4 * u) : 0;
+                const int bytes = valid >= 4 ? 16 : (valid > 0 ? 4 * valid : 0);
+                const float *sp = bytes ? src + c * HW + 4 * u : x;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst),
+                             "l"(sp), "r"(bytes));
+            } else {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const int e = tid + 256 * i;
-        const int c = e >> 5, unit = e & 31;
-        const float sum = fmaf(fabsf(q[i].x), 0.25f, fmaf(fabsf(q[i].y), 0.25f,
-                          fmaf(fabsf(q[i].z), 0.25f, fabsf(q[i].w) * 0.25f)));
-        if (!(sum <= 3.402823466e38f)) f |= BNN_FLAG_NONFINITE;
-        if (kStrict && c < nc) {
-            const float tv[4] = {q[i].x, q[i].y, q[i].z, q[i].w};
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-                if (p0 + 4 * unit + j < HW && tv[j] != 1.0f && tv[j] != -1.0f)
-                    f |= BNN_FLAG_NOTSIGN;
+                for (int j = 0; j < 4; ++j) {
+                    const bool ok = c < nc && 4 * u + j < npix;
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(dst + 4 * j),
+                                 "l"(ok ? src + c * HW + 4 * u + j : x), "r"(ok ? 4 : 0));
+                }
+            }
         }
-        *reinterpret_cast<float4 *>(&tile[c * kPackPix + 4 * (unit ^ (c & 7))]) = q[i];
+        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+        __syncthreads();
+        // transpose: items = 16 pixel quads x (nc / 32) channel groups, 8 warps
+        const int ngroups = (nc + 31) >> 5;
+        for (int item = warp; item < 16 * ngroups; item += 8) {
+            const int q4 = item & 15, g = item >> 4;
+            const int c = 32 * g + lane;
+            const bool cok = c < nc;
+            float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (cok) t = *reinterpret_cast<const float4 *>(tile + c * kPackPix + 4 * (q4 ^ (c & 7)));
+            const int left = npix - 4 * q4;
+            if (left > 0) {
+                const float sum = fmaf(fabsf(t.x), 0.25f, fmaf(fabsf(t.y), 0.25f,
+                                  fmaf(fabsf(t.z), 0.25f, fabsf(t.w) * 0.25f)));
+                if (!(sum <= 3.402823466e38f)) f |= BNN_FLAG_NONFINITE;  // zero-filled tails are finite
+                if (kStrict && cok) {
+                    const float tv[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        if (j < left && tv[j] != 1.0f && tv[j] != -1.0f) f |= BNN_FLAG_NOTSIGN;
+                }
+            }
+            const uint32_t w0 = __ballot_sync(0xffffffffu, cok && t.x >= 0.0f);  // sign(-0) = +1
+            const uint32_t w1 = __ballot_sync(0xffffffffu, cok && t.y >= 0.0f);
+            const uint32_t w2 = __ballot_sync(0xffffffffu, cok && t.z >= 0.0f);
+            const uint32_t w3 = __ballot_sync(0xffffffffu, cok && t.w >= 0.0f);
+            if (lane < 4) {
+                const uint32_t w = lane == 0 ? w0 : lane == 1 ? w1 : lane == 2 ? w2 : w3;
+                words[(4 * q4 + lane) * nw32 + (int)(c0 >> 5) + g] = w;
+            }
+        }
+        __syncthreads();  // tile reuse by the next channel chunk
     }
+    // channel-tail u32 words past ceil(C/32) (odd group count) are zero
+    for (int i = tid; i < kPackPix; i += 256)
+        for (int g = (int)((C + 31) >> 5); g < nw32; ++g) words[i * nw32 + g] = 0;
     __syncthreads();
-    // 64 items = (2 channel halves) x (32 pixel quads); 8 per warp
-#pragma unroll
-    for (int it = 0; it < 8; ++it) {
-        const int item = warp * 8 + it;
-        const int h = item & 1, quad = item >> 1;
-        const int c = 32 * h + lane;
-        const float4 t = *reinterpret_cast<const float4 *>(&tile[c * kPackPix + 4 * (quad ^ (c & 7))]);
-        const bool ok = c < nc;
-        const uint32_t w0 = __ballot_sync(0xffffffffu, ok && t.x >= 0.0f);  // sign(-0) = +1
-        const uint32_t w1 = __ballot_sync(0xffffffffu, ok && t.y >= 0.0f);
-        const uint32_t w2 = __ballot_sync(0xffffffffu, ok && t.z >= 0.0f);
-        const uint32_t w3 = __ballot_sync(0xffffffffu, ok && t.w >= 0.0f);
-        if (lane < 4) {
-            const int64_t p = p0 + 4 * quad + lane;
-            const uint32_t w = lane == 0 ? w0 : lane == 1 ? w1 : lane == 2 ? w2 : w3;
-            if (p < HW) out32[(b * HW + p) * (2 * Cw) + 2 * cw + h] = w;
-        }
+    // contiguous write-out: npix pixels x nw32 u32 words
+    uint32_t *dst = out32 + (b * HW + p0) * nw32;
+    const int total = npix * nw32;
+    if (((reinterpret_cast<uintptr_t>(dst) & 15) == 0) && (total & 3) == 0) {
+        for (int i = tid; i < total / 4; i += 256)
+            reinterpret_cast<uint4 *>(dst)[i] = reinterpret_cast<const uint4 *>(words)[i];
+    } else {
+        for (int i = tid; i < total; i += 256) dst[i] = words[i];
     }
     flush_flags(f, flags);
 }
@@ -271,90 +286,6 @@ __global__ void conv_weights_reorder_kernel(const uint64_t *__restrict__ w_ref, 
     w_dev[idx] = word;
 }
 
-// ---------------------------------------------------------------- pack NCHW (TMA)
-// Streaming variant for HW % 4 == 0: CTA = (image b, 32-channel group g,
-// pixel chunk).  One elected thread issues 32 cp.async.bulk copies (one
-// contiguous channel segment each, TMA engine, mbarrier complete_tx) into a
-// SMEM tile whose row pitch is chosen so lane l's 16-byte column reads fall in
-// distinct bank quads; then each warp transposes 4 pixels per ld.shared.v4
-// with four __ballot_sync (32 channels -> one u32 word per pixel).
-constexpr int kTmaPixMax = 1024;  // pixels per CTA chunk (<= 132 KB of SMEM)
-__device__ __forceinline__ int tma_pitch(int npix) { return ((npix + 31) & ~31) + 4; }
-
-template <bool kStrict>
-__global__ void __launch_bounds__(256) pack_nchw_tma_kernel(const float *__restrict__ x,
-                                                            int64_t C, int64_t HW, int64_t Cw,
-                                                            uint32_t *__restrict__ out32,
-                                                            int32_t *flags) {
-    extern __shared__ __align__(128) float tile_t[];
-    __shared__ __align__(8) uint64_t bar;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t g = blockIdx.y, b = blockIdx.z;
-    const int64_t p0 = (int64_t)blockIdx.x * kTmaPixMax;
-    const int npix = (int)(HW - p0 < kTmaPixMax ? HW - p0 : kTmaPixMax);
-    const int pitch = tma_pitch(npix);
-    const int nc = (int)(C - g * 32 < 32 ? C - g * 32 : 32);
-    const uint32_t sbar = smem_u32_pack(&bar);
-    if (tid == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sbar));
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    __syncthreads();
-    if (tid == 0) {
-        const uint32_t bytes = (uint32_t)npix * 4u;
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sbar),
-                     "r"(bytes * (uint32_t)nc)
-                     : "memory");
-        for (int c = 0; c < nc; ++c) {
-            const float *src = x + (b * C + g * 32 + c) * HW + p0;
-            asm volatile(
-                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
-                "[%3];\n" ::"r"(smem_u32_pack(tile_t + c * pitch)),
-                "l"(src), "r"(bytes), "r"(sbar)
-                : "memory");
-        }
-    }
-    // wait for the tile (phase 0)
-    {
-        uint32_t done = 0;
-        do {
-            asm volatile(
-                "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n"
-                "selp.u32 %0, 1, 0, p;\n}\n"
-                : "=r"(done)
-                : "r"(sbar)
-                : "memory");
-        } while (!done);
-    }
-    int f = 0;
-    const bool cok = lane < nc;
-    const int nquads = (npix + 3) >> 2;
-    for (int qd = warp; qd < nquads; qd += 8) {
-        float4 t = make_float4(-1.f, -1.f, -1.f, -1.f);
-        if (cok) t = *reinterpret_cast<const float4 *>(tile_t + lane * pitch + 4 * qd);
-        const float tv[4] = {t.x, t.y, t.z, t.w};
-        const int left = npix - 4 * qd;  // valid pixels in this quad (>= 1)
-        float sum = 0.f;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const float a = (j < left && cok) ? tv[j] : 0.f;
-            sum = fmaf(fabsf(a), 0.25f, sum);
-            if (kStrict && j < left && cok && a != 1.0f && a != -1.0f) f |= BNN_FLAG_NOTSIGN;
-        }
-        if (!(sum <= 3.402823466e38f)) f |= BNN_FLAG_NONFINITE;
-        const uint32_t w0 = __ballot_sync(0xffffffffu, cok && t.x >= 0.0f);  // sign(-0) = +1
-        const uint32_t w1 = __ballot_sync(0xffffffffu, cok && t.y >= 0.0f);
-        const uint32_t w2 = __ballot_sync(0xffffffffu, cok && t.z >= 0.0f);
-        const uint32_t w3 = __ballot_sync(0xffffffffu, cok && t.w >= 0.0f);
-        if (lane < 4 && lane < left) {
-            const int64_t p = p0 + 4 * qd + lane;
-            const uint32_t w = lane == 0 ? w0 : lane == 1 ? w1 : lane == 2 ? w2 : w3;
-            out32[(b * HW + p) * (2 * Cw) + g] = w;
-        }
-    }
-    flush_flags(f, flags);
-}
-
 // ================================================================ launchers
 int launch_binarize(const float *x, int64_t n, float *out, int32_t *flags, cudaStream_t s) {
     if (n == 0) return BNN_OK;
@@ -392,35 +323,18 @@ int launch_pack_nchw(const float *x, int64_t B, int64_t C, int64_t H, int64_t W,
     if (B == 0 || HW == 0 || C == 0) return BNN_OK;
     uint32_t *o32 = reinterpret_cast<uint32_t *>(out);
     const bool strict = mode == BNN_PACK_STRICT;
-    const bool aligned = (HW % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
-    if (aligned) {
-        // TMA streaming path: 32-channel groups, contiguous bulk copies
-        const int chunk = (int)(HW < kTmaPixMax ? HW : kTmaPixMax);
-        const int pitch = ((chunk + 31) & ~31) + 4;
-        const int smem = 32 * pitch * 4;
-        dim3 grid((unsigned)ceil_div(HW, kTmaPixMax), (unsigned)ceil_div(C, 32), (unsigned)B);
-        if (strict) {
-            static bool cfg = false;
-            if (!cfg) cudaFuncSetAttribute(pack_nchw_tma_kernel<true>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 32 * (kTmaPixMax + 4) * 4), cfg = true;
-            pack_nchw_tma_kernel<true><<<grid, 256, smem, s>>>(x, C, HW, Cw, o32, flags);
-        } else {
-            static bool cfg = false;
-            if (!cfg) cudaFuncSetAttribute(pack_nchw_tma_kernel<false>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 32 * (kTmaPixMax + 4) * 4), cfg = true;
-            pack_nchw_tma_kernel<false><<<grid, 256, smem, s>>>(x, C, HW, Cw, o32, flags);
-        }
-        // channel-tail words of odd 32-groups (C % 64 in (0, 32]) must read 0
-        if (ceil_div(C, 32) % 2 == 1) {
-            cudaMemset2DAsync(o32 + 2 * Cw - 1, 2 * Cw * 4, 0, 4, (size_t)(B * HW), s);
-        }
-        return check_launch("pack_nchw_tma_kernel");
-    }
-    dim3 grid((unsigned)ceil_div(HW, kPackPix), (unsigned)Cw, (unsigned)B);
-    if (strict)
-        pack_nchw_kernel<false, true><<<grid, 256, 0, s>>>(x, B, C, HW, Cw, o32, flags);
-    else
-        pack_nchw_kernel<false, false><<<grid, 256, 0, s>>>(x, B, C, HW, Cw, o32, flags);
+    const bool vec4 = (HW % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+    const int smem = kPackChunkC * kPackPix * 4 + kPackPix * (int)(2 * Cw) * 4;
+    if (smem > 200 * 1024) return set_error(BNN_EUNSUP, "too many channels for the pack kernel");
+    dim3 grid((unsigned)ceil_div(HW, kPackPix), (unsigned)B);
+    auto launch = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        kern<<<grid, 256, smem, s>>>(x, B, C, HW, Cw, o32, flags);
+    };
+    if (vec4 && !strict) launch(pack_nchw_kernel<true, false>);
+    else if (vec4) launch(pack_nchw_kernel<true, true>);
+    else if (!strict) launch(pack_nchw_kernel<false, false>);
+    else launch(pack_nchw_kernel<false, true>);
     return check_launch("pack_nchw_kernel");
 }
 
