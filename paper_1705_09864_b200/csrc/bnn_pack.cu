@@ -9,6 +9,7 @@
 //   im2col + pack_matrix_b activation side of QConv2d (layers.py:230-236),
 //                       here as a NCHW -> packed NHWC transpose-pack.
 #include <cstdio>
+#include <cstdlib>
 
 #include "bnn_common.cuh"
 
@@ -147,14 +148,15 @@ __global__ void pack_cols_kernel(const float *__restrict__ x, int64_t K, int64_t
 //     64 x (Cw u64) block with 16-byte stores (scattered 4-byte stores of the
 //     words themselves made the previous versions L2-transaction bound).
 // Finiteness: per float4, an overflow-free FFMA sum of |x|/4 propagates NaN/Inf.
-constexpr int kPackPix = 64, kPackChunkC = 256;
-template <bool kVec4, bool kStrict>
+template <int kPackPix, bool kVec4, bool kStrict>
 __global__ void __launch_bounds__(256) pack_nchw_kernel(const float *__restrict__ x, int64_t B,
                                                         int64_t C, int64_t HW, int64_t Cw,
                                                         uint32_t *__restrict__ out32,
                                                         int32_t *flags) {
+    constexpr int kPackChunkC = 16384 / kPackPix;  // 64 KB of f32 per pass
+    constexpr int kUnits = kPackPix / 4;           // 16-byte units per channel row
     extern __shared__ __align__(128) uint8_t pk_smem[];
-    float *tile = reinterpret_cast<float *>(pk_smem);                       // [256][64]
+    float *tile = reinterpret_cast<float *>(pk_smem);                       // [chunkC][pix]
     uint32_t *words = reinterpret_cast<uint32_t *>(pk_smem + kPackChunkC * kPackPix * 4);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t p0 = (int64_t)blockIdx.x * kPackPix;
@@ -165,11 +167,11 @@ __global__ void __launch_bounds__(256) pack_nchw_kernel(const float *__restrict_
     for (int64_t c0 = 0; c0 < C; c0 += kPackChunkC) {
         const int nc = (int)(C - c0 < kPackChunkC ? C - c0 : kPackChunkC);
         const float *src = x + (b * C + c0) * HW + p0;
-        // 256 channels x 16 units of 16 B = 4096 pieces, 16 per thread
+        // kPackChunkC channels x kUnits units of 16 B = 4096 pieces, 16 per thread
 #pragma unroll 4
         for (int i = 0; i < 16; ++i) {
             const int e = tid + 256 * i;
-            const int c = e >> 4, u = e & 15;
+            const int c = e / kUnits, u = e % kUnits;
             const uint32_t dst = smem_u32_pack(tile + c * kPackPix + 4 * (u ^ (c & 7)));
             if (kVec4) {
                 const int valid = (c < nc) ? (npix - 4 * u) : 0;
@@ -188,40 +190,44 @@ __global__ void __launch_bounds__(256) pack_nchw_kernel(const float *__restrict_
         }
         asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
         __syncthreads();
-        // transpose: items = 16 pixel quads x (nc / 32) channel groups, 8 warps
+        // transpose: items = kUnits pixel quads x (nc / 32) channel groups, 8 warps
         const int ngroups = (nc + 31) >> 5;
-        for (int item = warp; item < 16 * ngroups; item += 8) {
-            const int q4 = item & 15, g = item >> 4;
+        const uint32_t tile_s = smem_u32_pack(tile), words_s = smem_u32_pack(words);
+        const int gbase = (int)(c0 >> 5);
+        for (int item = warp; item < kUnits * ngroups; item += 8) {
+            const int q4 = item % kUnits, g = item / kUnits;
             const int c = 32 * g + lane;
             const bool cok = c < nc;
-            float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (cok) t = *reinterpret_cast<const float4 *>(tile + c * kPackPix + 4 * (q4 ^ (c & 7)));
-            const int left = npix - 4 * q4;
-            if (left > 0) {
-                const float sum = fmaf(fabsf(t.x), 0.25f, fmaf(fabsf(t.y), 0.25f,
-                                  fmaf(fabsf(t.z), 0.25f, fabsf(t.w) * 0.25f)));
-                if (!(sum <= 3.402823466e38f)) f |= BNN_FLAG_NONFINITE;  // zero-filled tails are finite
-                if (kStrict && cok) {
-                    const float tv[4] = {t.x, t.y, t.z, t.w};
+            float4 t;
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+                         : "=f"(t.x), "=f"(t.y), "=f"(t.z), "=f"(t.w)
+                         : "r"(tile_s + (uint32_t)(c * kPackPix + 4 * (q4 ^ (c & 7))) * 4u));
+            // zero-filled tails are finite, so no per-element validity test is needed
+            const float sum = fmaf(fabsf(t.x), 0.25f, fmaf(fabsf(t.y), 0.25f,
+                              fmaf(fabsf(t.z), 0.25f, fabsf(t.w) * 0.25f)));
+            f |= (cok && !(sum <= 3.402823466e38f)) ? BNN_FLAG_NONFINITE : 0;
+            if (kStrict && cok) {
+                const int left = npix - 4 * q4;
+                const float tv[4] = {t.x, t.y, t.z, t.w};
 #pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        if (j < left && tv[j] != 1.0f && tv[j] != -1.0f) f |= BNN_FLAG_NOTSIGN;
-                }
+                for (int j = 0; j < 4; ++j)
+                    if (j < left && tv[j] != 1.0f && tv[j] != -1.0f) f |= BNN_FLAG_NOTSIGN;
             }
             const uint32_t w0 = __ballot_sync(0xffffffffu, cok && t.x >= 0.0f);  // sign(-0) = +1
             const uint32_t w1 = __ballot_sync(0xffffffffu, cok && t.y >= 0.0f);
             const uint32_t w2 = __ballot_sync(0xffffffffu, cok && t.z >= 0.0f);
             const uint32_t w3 = __ballot_sync(0xffffffffu, cok && t.w >= 0.0f);
-            if (lane < 4) {
-                const uint32_t w = lane == 0 ? w0 : lane == 1 ? w1 : lane == 2 ? w2 : w3;
-                words[(4 * q4 + lane) * nw32 + (int)(c0 >> 5) + g] = w;
-            }
+            const uint32_t w = (lane & 2) ? ((lane & 1) ? w3 : w2) : ((lane & 1) ? w1 : w0);
+            if (lane < 4)
+                asm volatile("st.shared.u32 [%0], %1;\n" ::"r"(
+                                 words_s + (uint32_t)((4 * q4 + lane) * nw32 + gbase + g) * 4u),
+                             "r"(w));
         }
         __syncthreads();  // tile reuse by the next channel chunk
     }
     // channel-tail u32 words past ceil(C/32) (odd group count) are zero
     for (int i = tid; i < kPackPix; i += 256)
-        for (int g = (int)((C + 31) >> 5); g < nw32; ++g) words[i * nw32 + g] = 0;
+        for (int g = (int)((C + 31) >> 5); g < nw32; ++g) words[i * nw32 + g] = 0;  // tail halves
     __syncthreads();
     // contiguous write-out: npix pixels x nw32 u32 words
     uint32_t *dst = out32 + (b * HW + p0) * nw32;
@@ -324,17 +330,30 @@ int launch_pack_nchw(const float *x, int64_t B, int64_t C, int64_t H, int64_t W,
     uint32_t *o32 = reinterpret_cast<uint32_t *>(out);
     const bool strict = mode == BNN_PACK_STRICT;
     const bool vec4 = (HW % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
-    const int smem = kPackChunkC * kPackPix * 4 + kPackPix * (int)(2 * Cw) * 4;
+    static int pix = 0;
+    if (pix == 0) {
+        const char *e = getenv("BNN_PACK_PIX");
+        pix = e ? atoi(e) : 64;
+        if (pix != 64 && pix != 128 && pix != 256) pix = 64;
+    }
+    const int smem = 16384 * 4 + pix * (int)(2 * Cw) * 4;
     if (smem > 200 * 1024) return set_error(BNN_EUNSUP, "too many channels for the pack kernel");
-    dim3 grid((unsigned)ceil_div(HW, kPackPix), (unsigned)B);
+    dim3 grid((unsigned)ceil_div(HW, pix), (unsigned)B);
     auto launch = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         kern<<<grid, 256, smem, s>>>(x, B, C, HW, Cw, o32, flags);
     };
-    if (vec4 && !strict) launch(pack_nchw_kernel<true, false>);
-    else if (vec4) launch(pack_nchw_kernel<true, true>);
-    else if (!strict) launch(pack_nchw_kernel<false, false>);
-    else launch(pack_nchw_kernel<false, true>);
+#define BNN_PACK_SEL(P)                                                  \
+    if (pix == P) {                                                      \
+        if (vec4 && !strict) launch(pack_nchw_kernel<P, true, false>);   \
+        else if (vec4) launch(pack_nchw_kernel<P, true, true>);          \
+        else if (!strict) launch(pack_nchw_kernel<P, false, false>);     \
+        else launch(pack_nchw_kernel<P, false, true>);                   \
+    }
+    BNN_PACK_SEL(64)
+    BNN_PACK_SEL(128)
+    BNN_PACK_SEL(256)
+#undef BNN_PACK_SEL
     return check_launch("pack_nchw_kernel");
 }
 
