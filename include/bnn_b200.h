@@ -73,7 +73,14 @@ enum bnn_algo {
 /* Flags written (OR-ed) by the pack kernels into a caller int32. */
 enum bnn_flags {
     BNN_FLAG_NONFINITE = 1, /* NaN/Inf seen: binarize raises ValueError    */
-    BNN_FLAG_NOTSIGN = 2    /* strict mode: an entry was not exactly +-1     */
+    BNN_FLAG_NOTSIGN = 2,   /* strict mode: an entry was not exactly +-1     */
+    BNN_FLAG_RANGE = 4      /* unsigned grid: an input outside [0, 1]        */
+};
+
+/* Quantization grids of the multi-bit path (qmath.py:50-84), levels L = 2^bits - 1. */
+enum bnn_grid {
+    BNN_GRID_UNSIGNED = 0, /* quantize:        v = code / L,        x in [0, 1] */
+    BNN_GRID_SIGNED = 1    /* quantize_signed: v = (2 code - L) / L, clip(x, -1, 1) */
 };
 
 /* Pack-kernel input modes. */
@@ -131,6 +138,23 @@ int bnn_xnor_gemm(const uint64_t *A, int64_t lda, const uint64_t *B, int64_t ldb
                   int64_t N, int64_t K, int a_pad, int b_pad, float *C, int64_t ldc_m,
                   int64_t ldc_n, int domain, const float *scale, const float *shift, int algo,
                   bnn_stream_t stream);
+
+/* Multi-bit path (act_bit = weight_bit = bits):
+ * k-bit quantize + bit-plane pack, x [R, K] f32 -> out[p * plane_stride + r * ldo + w]
+ * (plane p = bit p of every code).  bits == 2. */
+int bnn_pack_planes_f32(const float *x, int64_t R, int64_t K, int64_t ldx, int bits, int grid,
+                        uint64_t *out, int64_t ldo, int64_t plane_stride, int32_t *flags,
+                        bnn_stream_t stream);
+
+/* Bit-plane GEMM: out[m, n] = sum_k v_a(m, k) * v_b(n, k) where v = grid value
+ * of the code assembled from `bits` planes (A weights [bits][M][lda], B
+ * activations [bits][N][ldb]).  Exact integer numerator, one f32 rounding of
+ * the final division by L^2.  Engine: tcgen05 (codes expanded to u8 in SMEM /
+ * TMEM; the MMA accumulates sum(code_a * code_b)). */
+int bnn_bitplane_gemm(const uint64_t *A, int64_t lda, int64_t a_plane_stride, int a_grid,
+                      const uint64_t *B, int64_t ldb, int64_t b_plane_stride, int b_grid,
+                      int bits, int64_t M, int64_t N, int64_t K, float *C, int64_t ldc_m,
+                      int64_t ldc_n, bnn_stream_t stream);
 
 /* Words per pixel of the packed NHWC activation layout: ceil(C / 64). */
 int64_t bnn_conv_channel_words(int64_t C);

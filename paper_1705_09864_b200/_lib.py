@@ -19,7 +19,8 @@ OK, EINVAL, EDIMS, EKEXACT, EPAD, EALIGN, EGEOM, EUNSUP, ECUDA = 0, -1, -2, -3, 
 POPCOUNT, DOT = 0, 1
 ALGO_AUTO, ALGO_POPC, ALGO_BMMA, ALGO_UMMA = 0, 1, 2, 3
 ALGOS = {"auto": ALGO_AUTO, "popc": ALGO_POPC, "bmma": ALGO_BMMA, "umma": ALGO_UMMA}
-FLAG_NONFINITE, FLAG_NOTSIGN = 1, 2
+FLAG_NONFINITE, FLAG_NOTSIGN, FLAG_RANGE = 1, 2, 4
+GRID_UNSIGNED, GRID_SIGNED = 0, 1
 PACK_SIGN, PACK_STRICT = 0, 1
 
 # every exported symbol and its ctypes signature (restype, argtypes)
@@ -42,6 +43,9 @@ SIGNATURES = {
     "bnn_bconv2d": (_i32, [_vp, _i64, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _i64,
                            _i64, _vp, _i32, _vp, _vp, _i32, _vp]),
     "bnn_probe_pipe_peak": (_i32, [_i32, _i64, _vp, _vp, _vp]),
+    "bnn_pack_planes_f32": (_i32, [_vp, _i64, _i64, _i64, _i32, _i32, _vp, _i64, _i64, _vp, _vp]),
+    "bnn_bitplane_gemm": (_i32, [_vp, _i64, _i64, _i32, _vp, _i64, _i64, _i32, _i32, _i64, _i64,
+                                 _i64, _vp, _i64, _i64, _vp]),
     "bnn_set_umma_variant": (_i32, [_i32]),
     "bnn_umma_trace": (_i32, [_vp]),
 }

@@ -73,6 +73,8 @@ def raise_on_flags(flags: torch.Tensor, finite_msg: str = "binarize requires fin
         raise ValueError(finite_msg)
     if f & _lib.FLAG_NOTSIGN:
         raise ValueError("matrix entries must all be -1 or +1")
+    if f & _lib.FLAG_RANGE:
+        raise ValueError("quantize requires inputs in [0, 1]")
 
 
 def _out(t: torch.Tensor, was_np: bool):
@@ -241,6 +243,25 @@ def pack_nchw(x: torch.Tensor, strict: bool = False,
     out = torch.empty((b, h, w, words_per_bits(c)), dtype=torch.uint64, device=x.device)
     _lib.call("bnn_pack_nchw_f32", _lib.ptr(x), b, c, h, w, _lib.ptr(out),
               _lib.PACK_STRICT if strict else _lib.PACK_SIGN, _lib.ptr(flags), _lib.stream_ptr())
+    return out
+
+
+def pack_planes_device(x: torch.Tensor, bits: int = 2, grid: str = "signed",
+                       flags: torch.Tensor | None = None) -> torch.Tensor:
+    """k-bit quantize + bit-plane pack of a CUDA f32 [R, K] matrix -> [bits, R, W] u64.
+
+    Codes follow qmath.quantize / quantize_signed (qmath.py:50-84) bit for bit;
+    plane p holds bit p of every code.  No host sync (flags as pack_rows_device).
+    """
+    if x.dim() != 2:
+        raise ValueError(f"expected a 2-D matrix, got ndim={x.dim()}")
+    x = x.contiguous()
+    r, k = x.shape
+    w = words_per_bits(k)
+    out = torch.empty((bits, r, w), dtype=torch.uint64, device=x.device)
+    g = _lib.GRID_SIGNED if grid == "signed" else _lib.GRID_UNSIGNED
+    _lib.call("bnn_pack_planes_f32", _lib.ptr(x), r, k, k, bits, g, _lib.ptr(out), w, r * w,
+              _lib.ptr(flags), _lib.stream_ptr())
     return out
 
 

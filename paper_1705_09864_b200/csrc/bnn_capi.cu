@@ -54,6 +54,11 @@ int launch_xnor_gemm_bmma(const uint64_t *, int64_t, const uint64_t *, int64_t, 
 int launch_bconv2d_bmma(const uint64_t *, int64_t, int64_t, int64_t, int64_t, const uint64_t *,
                         int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,
                         int64_t, float *, const Epilogue &, cudaStream_t);
+int launch_pack_planes(const float *, int64_t, int64_t, int64_t, int, int, uint64_t *, int64_t,
+                       int64_t, int32_t *, cudaStream_t);
+int launch_bitplane_gemm_umma(const uint64_t *, int64_t, int64_t, const uint64_t *, int64_t,
+                              int64_t, int64_t, int64_t, int64_t, float *, int64_t, int64_t,
+                              const Epilogue &, cudaStream_t);
 int launch_bconv2d_popc(const uint64_t *, int64_t, int64_t, int64_t, int64_t, const uint64_t *,
                         int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,
                         int64_t, float *, const Epilogue &, cudaStream_t);
@@ -193,6 +198,44 @@ int bnn_xnor_gemm(const uint64_t *A, int64_t lda, const uint64_t *B, int64_t ldb
         default:
             return set_error(BNN_EUNSUP, "algorithm %d not available", algo);
     }
+}
+
+int bnn_pack_planes_f32(const float *x, int64_t R, int64_t K, int64_t ldx, int bits, int grid,
+                        uint64_t *out, int64_t ldo, int64_t plane_stride, int32_t *flags,
+                        bnn_stream_t stream) {
+    BNN_REQUIRE(R >= 0 && K >= 0, BNN_EINVAL, "negative size");
+    BNN_REQUIRE(bits == 2, BNN_EUNSUP, "bit-plane path supports bits == 2, got %d", bits);
+    BNN_REQUIRE(grid == BNN_GRID_UNSIGNED || grid == BNN_GRID_SIGNED, BNN_EINVAL, "bad grid");
+    BNN_REQUIRE(ldx >= K && ldo >= ceil_div(K, 64) && plane_stride >= R * ldo, BNN_EALIGN,
+                "leading dimension / plane stride too small");
+    BNN_REQUIRE(R * K == 0 || (x && out), BNN_EINVAL, "null pointer");
+    return launch_pack_planes(x, R, K, ldx, bits, grid, out, ldo, plane_stride, flags,
+                              as_stream(stream));
+}
+
+int bnn_bitplane_gemm(const uint64_t *A, int64_t lda, int64_t a_plane_stride, int a_grid,
+                      const uint64_t *B, int64_t ldb, int64_t b_plane_stride, int b_grid,
+                      int bits, int64_t M, int64_t N, int64_t K, float *C, int64_t ldc_m,
+                      int64_t ldc_n, bnn_stream_t stream) {
+    int rc = check_gemm_dims(M, N, K);
+    if (rc) return rc;
+    BNN_REQUIRE(bits == 2, BNN_EUNSUP, "bit-plane path supports bits == 2, got %d", bits);
+    BNN_REQUIRE((a_grid == BNN_GRID_UNSIGNED || a_grid == BNN_GRID_SIGNED) &&
+                    (b_grid == BNN_GRID_UNSIGNED || b_grid == BNN_GRID_SIGNED),
+                BNN_EINVAL, "bad grid");
+    const int64_t W = ceil_div(K, 64);
+    BNN_REQUIRE(lda >= W && ldb >= W && a_plane_stride >= M * lda && b_plane_stride >= N * ldb,
+                BNN_EALIGN, "leading dimension / plane stride too small");
+    BNN_REQUIRE(A && B && C, BNN_EINVAL, "null pointer");
+    const int L = (1 << bits) - 1;
+    Epilogue ep{(int32_t)K, (int32_t)K, BNN_POPCOUNT, nullptr, nullptr};
+    ep.a_alpha = a_grid == BNN_GRID_SIGNED ? 2 : 1;
+    ep.a_beta = a_grid == BNN_GRID_SIGNED ? -L : 0;
+    ep.b_alpha = b_grid == BNN_GRID_SIGNED ? 2 : 1;
+    ep.b_beta = b_grid == BNN_GRID_SIGNED ? -L : 0;
+    ep.inv_gamma = 1.0f / (float)(L * L);
+    return launch_bitplane_gemm_umma(A, lda, a_plane_stride, B, ldb, b_plane_stride, M, N, K, C,
+                                     ldc_m, ldc_n, ep, as_stream(stream));
 }
 
 int64_t bnn_conv_channel_words(int64_t C) { return C > 0 ? ceil_div(C, 64) : 0; }

@@ -26,6 +26,10 @@ struct Epilogue {
     int32_t domain;
     const float *scale;
     const float *shift;
+    // multi-bit (bit-plane) operands: value = (alpha * code + beta) / gamma per
+    // operand; out = (aA aB S + aA bB sumA[m] + bA aB sumB[n] + K bA bB) / (gA gB)
+    int32_t a_alpha = 1, a_beta = 0, b_alpha = 1, b_beta = 0;
+    float inv_gamma = 1.0f;
     __device__ __forceinline__ float apply(int32_t x, int m) const {
         int32_t p = k_eff - x;
         int32_t v = domain == BNN_DOT ? 2 * p - k_logical : p;

@@ -60,7 +60,7 @@ constexpr int kWordsPerStage = 4;  // u32 words of K per row per stage
 constexpr int kRowBytes = 128;     // expanded bytes per row per stage
 constexpr int PD = 4;              // packed prefetch depth (per producer thread)
 
-template <int BN, bool kATmem>
+template <int BN, bool kATmem, int kPlanes = 1>
 struct Cfg {
     static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
     static constexpr int kProducers = BM + BN;                 // one thread per operand row
@@ -85,7 +85,7 @@ struct Cfg {
     static constexpr int kStgBytes = 32 * kStgPitch;
     static constexpr int off_exp = 0;
     static constexpr int off_pk = ES * kStageBytes;
-    static constexpr int off_popc_a = off_pk + PD * kProducerWarps * 32 * 16;
+    static constexpr int off_popc_a = off_pk + PD * kProducerWarps * 32 * 16 * kPlanes;
     static constexpr int off_popc_b = off_popc_a + 2 * BM * 4;
     static constexpr int off_epi = off_popc_b + 2 * BN * 4;
     static constexpr int off_bars = off_epi + kEpiWarps * kStgBytes;
@@ -213,6 +213,14 @@ __device__ __forceinline__ void expand8(uint32_t w, uint32_t (&r)[8]) {
     for (int i = 0; i < 8; ++i) r[i] = kIsA ? (w & (0x80808080u >> i)) : (w & (0x01010101u << i));
 }
 
+// two bit planes -> u8 codes 0..3 (same K permutation as expand8; no scaling:
+// the MMA then accumulates sum(code_a * code_b) directly)
+__device__ __forceinline__ void expand_code2(uint32_t w0, uint32_t w1, uint32_t (&r)[8]) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+        r[i] = ((w0 >> i) & 0x01010101u) | (((w1 >> i) << 1) & 0x02020202u);
+}
+
 // 32 expanded bytes of word q -> two 16-byte chunks of a SW128 K-major row
 __device__ __forceinline__ void store_row32(const uint32_t (&r)[8], uint32_t row_base, int row,
                                             int q) {
@@ -232,12 +240,12 @@ struct TileMap {
     }
 };
 
-template <int BN, bool kATmem, int kVec, class ALoad, class BLoad, class Store>
-__global__ void __launch_bounds__(Cfg<BN, kATmem>::kThreads, 1)
+template <int BN, bool kATmem, int kVec, class ALoad, class BLoad, class Store, int kPlanes = 1>
+__global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes>::kThreads, 1)
     xnor_umma_kernel(ALoad aload, BLoad bload, Store store, Epilogue ep, int64_t kw32,
                      TileMap tmap, uint64_t *trace_buf) {
     auto trace = [&](int slot) { trace_at(trace_buf, slot); };
-    using C = Cfg<BN, kATmem>;
+    using C = Cfg<BN, kATmem, kPlanes>;
     constexpr int ES = C::ES;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t sbase_raw = smem_u32(smem_raw);
@@ -288,8 +296,8 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem>::kThreads, 1)
         const bool is_a = tid < BM;
         const bool active = tid < C::kProducers;  // the last warp may be partly idle
         const int row = is_a ? tid : tid - BM;
-        const uint32_t ring = s_pk + tid * 16;  // slot-major private ring
-        constexpr uint32_t kRingSlot = C::kProducerWarps * 32 * 16;
+        const uint32_t ring = s_pk + tid * 16 * kPlanes;  // slot-major private ring
+        constexpr uint32_t kRingSlot = C::kProducerWarps * 32 * 16 * kPlanes;
         // fetch iterator (runs PD-1 stages ahead, across tile boundaries)
         int f_tile = blockIdx.x;
         int64_t f_kt = 0;
@@ -308,11 +316,14 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem>::kThreads, 1)
             if (f_tile < tmap.ntiles && active) {
                 const uint32_t dst = ring + (uint32_t)(f_count % PD) * kRingSlot;
 #pragma unroll
-                for (int p = 0; p < kWordsPerStage / kVec; ++p) {
-                    const int64_t w = f_kt * kWordsPerStage + p * kVec;
-                    if (is_a) aload.template load<kVec>(fa, w, dst + p * kVec * 4);
-                    else bload.template load<kVec>(fb, w, dst + p * kVec * 4);
-                }
+                for (int pl = 0; pl < kPlanes; ++pl)
+#pragma unroll
+                    for (int p = 0; p < kWordsPerStage / kVec; ++p) {
+                        const int64_t w = f_kt * kWordsPerStage + p * kVec;
+                        const uint32_t d = dst + pl * 16 + p * kVec * 4;
+                        if (is_a) aload.template load<kVec>(fa, w, d, pl);
+                        else bload.template load<kVec>(fb, w, d, pl);
+                    }
                 ++f_count;
                 if (++f_kt == ktiles) {
                     f_kt = 0;
@@ -334,10 +345,26 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem>::kThreads, 1)
             for (int64_t kt = 0; kt < ktiles; ++kt, ++gk) {
                 fetch_next();
                 cp_async_wait<PD - 1>();
-                uint32_t wv[4];
+                uint32_t wv[4], wv1[4] = {0, 0, 0, 0};
+                const uint32_t slot = ring + (uint32_t)(gk % PD) * kRingSlot;
                 asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n"
                              : "=r"(wv[0]), "=r"(wv[1]), "=r"(wv[2]), "=r"(wv[3])
-                             : "r"(ring + (uint32_t)(gk % PD) * kRingSlot));
+                             : "r"(slot));
+                if constexpr (kPlanes == 2)
+                    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n"
+                                 : "=r"(wv1[0]), "=r"(wv1[1]), "=r"(wv1[2]), "=r"(wv1[3])
+                                 : "r"(slot + 16));
+                // expanded registers of word q for this operand side
+                auto expand = [&](int q, bool as_a, uint32_t (&r)[8]) {
+                    if constexpr (kPlanes == 2) {
+                        my_popc += __popc(wv[q]) + 2 * __popc(wv1[q]);  // code sum
+                        expand_code2(wv[q], wv1[q], r);
+                    } else {
+                        my_popc += __popc(wv[q]);
+                        if (as_a) expand8<true>(wv[q], r);
+                        else expand8<false>(wv[q], r);
+                    }
+                };
                 const int s = (int)(gk % ES);
                 if (gk >= ES) mbar_wait(bar_empty + 8 * s, (uint32_t)((gk / ES) - 1) & 1u);
                 if (!active) {
@@ -348,9 +375,8 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem>::kThreads, 1)
                                                C::kAStageCol + s * 32;
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
-                            my_popc += __popc(wv[q]);
                             uint32_t r[8];
-                            expand8<true>(wv[q], r);
+                            expand(q, true, r);
                             tmem_st8(taddr + q * 8, r);
                         }
                         asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
@@ -359,9 +385,8 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem>::kThreads, 1)
                         const uint32_t row_base = s_exp + s * C::kStageBytes + row * kRowBytes;
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
-                            my_popc += __popc(wv[q]);
                             uint32_t r[8];
-                            expand8<true>(wv[q], r);
+                            expand(q, true, r);
                             store_row32(r, row_base, row, q);
                         }
                         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -371,9 +396,8 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem>::kThreads, 1)
                         s_exp + s * C::kStageBytes + C::kStageA + row * kRowBytes;
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        my_popc += __popc(wv[q]);
                         uint32_t r[8];
-                        expand8<false>(wv[q], r);
+                        expand(q, false, r);
                         store_row32(r, row_base, row, q);
                     }
                     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -456,6 +480,10 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem>::kThreads, 1)
             const bool mok = m < M;
             // per-row constants: P = kb - pb[n] + 2C, with 2C = acc >> 6 (acc = 128 C)
             const int32_t kb = ep.k_eff - s_popc_a[buf * BM + q * 32 + lane];
+            // multi-bit decode constants (kPlanes == 2): s_popc_* hold code sums
+            const int32_t abab = ep.a_alpha * ep.b_alpha;
+            const int32_t rowterm = ep.a_alpha * ep.b_beta * s_popc_a[buf * BM + q * 32 + lane] +
+                                    ep.k_logical * ep.a_beta * ep.b_beta;
             const float sc = (mok && ep.scale) ? __ldg(ep.scale + m) : 1.0f;
             const float sh = (mok && ep.shift) ? __ldg(ep.shift + m) : 0.0f;
             const int32_t *pb = s_popc_b + buf * BN;
@@ -482,6 +510,12 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem>::kThreads, 1)
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
                         const int j = 4 * j4 + i;
+                        if constexpr (kPlanes == 2) {
+                            // exact integer numerator, one rounding: (.) / (gA gB)
+                            const int32_t num = abab * (int32_t)v[j] + rowterm + ep.a_beta * ep.b_alpha * pbv[i];
+                            f[j] = __fmul_rn((float)num, ep.inv_gamma);
+                            continue;
+                        }
                         int32_t val = kb - pbv[i] + (int32_t)(v[j] >> 6);
                         if (dot) val = 2 * val - ep.k_logical;
                         float x = magic ? __int_as_float(val + 0x4B400000) - 12582912.0f
@@ -575,11 +609,11 @@ static int sm_count() {
     return n;
 }
 
-template <int BN, bool kATmem, int kVec, class ALoad, class BLoad, class Store>
+template <int BN, bool kATmem, int kVec, class ALoad, class BLoad, class Store, int kPlanes = 1>
 static int launch_umma_cfg(const ALoad &a, const BLoad &b, const Store &st, const Epilogue &ep,
                            int64_t M, int64_t N, int64_t kw32, cudaStream_t s) {
-    using C = umma::Cfg<BN, kATmem>;
-    auto kern = umma::xnor_umma_kernel<BN, kATmem, kVec, ALoad, BLoad, Store>;
+    using C = umma::Cfg<BN, kATmem, kPlanes>;
+    auto kern = umma::xnor_umma_kernel<BN, kATmem, kVec, ALoad, BLoad, Store, kPlanes>;
     static bool configured = false;
     if (!configured) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
@@ -643,6 +677,27 @@ int launch_xnor_gemm_umma(const uint64_t *A, int64_t lda, const uint64_t *B, int
                       ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) == 0;
     return vec4 ? launch_umma<4>(a, b, st, ep, M, N, kw32, s)
                 : launch_umma<2>(a, b, st, ep, M, N, kw32, s);
+}
+
+int launch_bitplane_gemm_umma(const uint64_t *A, int64_t lda, int64_t a_plane,
+                              const uint64_t *B, int64_t ldb, int64_t b_plane, int64_t M,
+                              int64_t N, int64_t K, float *C, int64_t ldc_m, int64_t ldc_n,
+                              const Epilogue &ep, cudaStream_t s) {
+    const int64_t kw32 = 2 * ceil_div(K, 64);
+    DenseRows a{reinterpret_cast<const uint32_t *>(A), 2 * lda, M, kw32, 2 * a_plane};
+    DenseRows b{reinterpret_cast<const uint32_t *>(B), 2 * ldb, N, kw32, 2 * b_plane};
+    GemmStore st{C, ldc_m, ldc_n, M, N};
+    const bool vec4 = (lda % 2 == 0) && (ldb % 2 == 0) && (a_plane % 2 == 0) &&
+                      (b_plane % 2 == 0) &&
+                      ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) == 0;
+    switch (choose_bn(M, N)) {
+        case 128:
+            return vec4 ? launch_umma_cfg<128, true, 4, DenseRows, DenseRows, GemmStore, 2>(a, b, st, ep, M, N, kw32, s)
+                        : launch_umma_cfg<128, true, 2, DenseRows, DenseRows, GemmStore, 2>(a, b, st, ep, M, N, kw32, s);
+        default:
+            return vec4 ? launch_umma_cfg<192, true, 4, DenseRows, DenseRows, GemmStore, 2>(a, b, st, ep, M, N, kw32, s)
+                        : launch_umma_cfg<192, true, 2, DenseRows, DenseRows, GemmStore, 2>(a, b, st, ep, M, N, kw32, s);
+    }
 }
 
 int launch_bconv2d_umma(const uint64_t *x, int64_t B, int64_t C, int64_t H, int64_t W,

@@ -44,14 +44,15 @@ struct DenseRows {
     int64_t ld32;
     int64_t rows;
     int64_t kw32;
+    int64_t plane32 = 0;  // u32 stride between bit planes (multi-bit operands)
     struct Cursor { const uint32_t *p; bool ok; };
     __device__ Cursor row(int64_t r) const { return {base + r * ld32, r < rows}; }
     // load kVec words at word w of this row into smem address dst
     template <int kVec>
-    __device__ void load(Cursor &c, int64_t w, uint32_t dst) const {
+    __device__ void load(Cursor &c, int64_t w, uint32_t dst, int plane = 0) const {
         int64_t left = kw32 - w;
         int bytes = (!c.ok || left <= 0) ? 0 : (int)(left >= kVec ? kVec * 4 : left * 4);
-        const uint32_t *src = bytes ? c.p + w : base;
+        const uint32_t *src = bytes ? c.p + plane * plane32 + w : base;
         cp_async<kVec * 4>(dst, src, bytes);
     }
 };
@@ -84,7 +85,7 @@ struct ConvRows {
         return c;
     }
     template <int kVec>
-    __device__ void load(Cursor &c, int64_t w, uint32_t dst) const {
+    __device__ void load(Cursor &c, int64_t w, uint32_t dst, int plane = 0) const {
         if (!c.ok || w >= kw32) {
             cp_async<kVec * 4>(dst, x, 0);
             return;

@@ -292,6 +292,61 @@ __global__ void conv_weights_reorder_kernel(const uint64_t *__restrict__ w_ref, 
     w_dev[idx] = word;
 }
 
+// ---------------------------------------------------------------- pack planes
+// k-bit quantize + bit-plane pack (multi-bit act_bit / weight_bit):
+// x [R, K] f32 -> planes[p][R][ldo] u64, plane p holding bit p of each code.
+// Codes follow the reference's float32 op order exactly (qmath.py:44-84, no
+// FMA contraction): unsigned grid  code = floor(x * L + 0.5), x in [0, 1];
+// signed grid  code = floor((0.5 * clip(x, -1, 1) + 0.5) * L + 0.5).
+template <int kBits>
+__global__ void pack_planes_kernel(const float *__restrict__ x, int64_t R, int64_t K, int64_t ldx,
+                                   int grid_signed, uint64_t *__restrict__ out, int64_t ldo,
+                                   int64_t plane_stride, int32_t *flags) {
+    const int lane = threadIdx.x & 31;
+    const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    if (row >= R) return;  // warp-uniform
+    const float L = (float)((1 << kBits) - 1);
+    const float *xr = x + row * ldx;
+    const int64_t W = ceil_div(K, 64);
+    int f = 0;
+    for (int64_t base = 0; base < W * 64; base += 128) {
+        const int64_t e = base + 4 * lane;
+        uint32_t nib[kBits];
+#pragma unroll
+        for (int p = 0; p < kBits; ++p) nib[p] = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            if (e + i < K) {
+                const float v = __ldg(xr + e + i);
+                if (!isfinite(v)) f |= BNN_FLAG_NONFINITE;
+                float y;
+                if (grid_signed) {
+                    const float c = fminf(fmaxf(v, -1.0f), 1.0f);
+                    y = __fadd_rn(__fmul_rn(0.5f, c), 0.5f);
+                } else {
+                    if (v < 0.0f || v > 1.0f) f |= BNN_FLAG_RANGE;
+                    y = v;
+                }
+                const uint32_t code = (uint32_t)floorf(__fadd_rn(__fmul_rn(y, L), 0.5f));
+#pragma unroll
+                for (int p = 0; p < kBits; ++p) nib[p] |= ((code >> p) & 1u) << i;
+            }
+        }
+        const int64_t wi = base / 64 + (lane >> 4);
+#pragma unroll
+        for (int p = 0; p < kBits; ++p) {
+            uint32_t w = nib[p] << (4 * (lane & 7));
+            w |= __shfl_xor_sync(0xffffffffu, w, 1);
+            w |= __shfl_xor_sync(0xffffffffu, w, 2);
+            w |= __shfl_xor_sync(0xffffffffu, w, 4);
+            const uint32_t hi = __shfl_down_sync(0xffffffffu, w, 8);
+            if ((lane & 15) == 0 && wi < W)
+                out[p * plane_stride + row * ldo + wi] = (uint64_t)w | ((uint64_t)hi << 32);
+        }
+    }
+    flush_flags(f, flags);
+}
+
 // ================================================================ launchers
 int launch_binarize(const float *x, int64_t n, float *out, int32_t *flags, cudaStream_t s) {
     if (n == 0) return BNN_OK;
@@ -355,6 +410,19 @@ int launch_pack_nchw(const float *x, int64_t B, int64_t C, int64_t H, int64_t W,
     BNN_PACK_SEL(256)
 #undef BNN_PACK_SEL
     return check_launch("pack_nchw_kernel");
+}
+
+int launch_pack_planes(const float *x, int64_t R, int64_t K, int64_t ldx, int bits, int grid,
+                       uint64_t *out, int64_t ldo, int64_t plane_stride, int32_t *flags,
+                       cudaStream_t s) {
+    if (R == 0 || K == 0) return BNN_OK;
+    const int64_t blocks = ceil_div(R * 32, 256);
+    if (bits == 2)
+        pack_planes_kernel<2><<<(unsigned)blocks, 256, 0, s>>>(x, R, K, ldx, grid, out, ldo,
+                                                               plane_stride, flags);
+    else
+        return set_error(BNN_EUNSUP, "bit-plane packing supports bits == 2");
+    return check_launch("pack_planes_kernel");
 }
 
 int launch_words_transpose(const uint64_t *in, int64_t rows, int64_t cols, int64_t ldi,

@@ -115,6 +115,29 @@ def xnor_rows_gemm(a_rows: torch.Tensor, b_rows: torch.Tensor, k: int, *, a_pad:
     return out
 
 
+def bitplane_gemm(a_planes: torch.Tensor, b_planes: torch.Tensor, k: int, *,
+                  a_grid: str = "signed", b_grid: str = "signed", out: torch.Tensor | None = None,
+                  transpose_out: bool = False) -> torch.Tensor:
+    """Multi-bit (bit-plane) GEMM: sum_k v_a v_b for [bits, M, W] x [bits, N, W] planes.
+
+    The product the reference's float path computes for bits > 1
+    (layers.py:240-242, 370-377); exact integer numerator, one f32 rounding.
+    """
+    bits, m, w = a_planes.shape
+    bits_b, n, w2 = b_planes.shape
+    if bits != bits_b or w != w2:
+        raise ValueError("plane counts or word counts differ")
+    GemmDims(m, n, k)
+    if out is None:
+        out = torch.empty((n, m) if transpose_out else (m, n), dtype=torch.float32,
+                          device=a_planes.device)
+    ldc_m, ldc_n = (1, out.stride(0)) if transpose_out else (out.stride(0), 1)
+    g = {"signed": _lib.GRID_SIGNED, "unsigned": _lib.GRID_UNSIGNED}
+    _lib.call("bnn_bitplane_gemm", _lib.ptr(a_planes), w, m * w, g[a_grid], _lib.ptr(b_planes), w,
+              n * w, g[b_grid], bits, m, n, k, _lib.ptr(out), ldc_m, ldc_n, _lib.stream_ptr())
+    return out
+
+
 def xnor_gemm_b200(a: BitMatrix, b: BitMatrix, algo: int | str = "auto",
                    domain: int = _lib.POPCOUNT) -> torch.Tensor:
     """Packed product of a layout-'a' and a layout-'b' operand: f32 [M, N] on the GPU."""

@@ -23,9 +23,9 @@ import torch
 import torch.nn.functional as F
 
 from . import _lib, qmath
-from .bitpack import (BitMatrix, pack_matrix_a, pack_nchw, pack_rows_device, raise_on_flags,
-                      to_device_f32, to_device_words, words_per_bits)
-from .gemm import xnor_rows_gemm
+from .bitpack import (BitMatrix, pack_matrix_a, pack_nchw, pack_planes_device, pack_rows_device,
+                      raise_on_flags, to_device_f32, to_device_words, words_per_bits)
+from .gemm import bitplane_gemm, xnor_rows_gemm
 
 TRAIN_FLOAT = "train_float"
 INFER_FLOAT = "infer_float"
@@ -347,13 +347,58 @@ class QFullyConnected(QDense):
     _fuse_sign = True
 
     def __init__(self, in_features, num_hidden, act_bit=1, weight_bit=1, rng=None,
-                 domain="popcount"):
+                 domain="popcount", act_grid="signed", weight_grid="signed"):
         if int(act_bit) != int(weight_bit):
             raise ValueError("act_bit != weight_bit has no reference packed path (G4)")
+        if int(weight_bit) not in (1, 2):
+            raise ValueError("packed multi-bit path supports act_bit = weight_bit in {1, 2}")
         super().__init__(in_features, num_hidden, bits=weight_bit, rng=rng)
         self.act_bit = int(act_bit)
         self.weight_bit = int(weight_bit)
         self.domain = _lib.DOT if domain == "dot" else _lib.POPCOUNT
+        # multi-bit grids: "signed" = quantize_signed (the reference layers'),
+        # "unsigned" = quantize on [0, 1] (config 5's U[0,1] operands)
+        self.act_grid, self.weight_grid = act_grid, weight_grid
+
+    def pack(self):
+        if self.bits == 1:
+            return super().pack()
+        if self.weight is None:
+            raise ModeError("no float weights to pack")
+        w = torch.from_numpy(np.ascontiguousarray(self._flat_weight_np())).cuda()
+        flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.planes = pack_planes_device(w, self.bits, self.weight_grid, flags)
+        raise_on_flags(flags, "quantize_signed requires finite inputs")
+        self.packed = self.planes  # marks the layer as packed
+        return self.planes
+
+    def _require_packed(self):
+        if self.packed is None:
+            raise ModeError("layer has no packed weights; pack() or load a converted model")
+
+    def forward(self, x, mode=INFER_FLOAT):
+        if self.bits == 1 or mode != INFER_PACKED:
+            if self.bits != 1 and mode == INFER_FLOAT and self.act_grid == "unsigned":
+                _check_mode(mode)
+                t, was_np = to_device_f32(x)
+                xq = qmath.quantize(t, self.act_bit)
+                wq = qmath.quantize(torch.from_numpy(np.asarray(self.weight, np.float32)).cuda(),
+                                    self.weight_bit) if self.weight_grid == "unsigned" else \
+                    qmath.quantize_signed(torch.from_numpy(np.asarray(self.weight, np.float32)).cuda(),
+                                          self.weight_bit)
+                return _ret(_float_matmul(xq, wq.T), was_np)
+            return super().forward(x, mode)
+        _check_mode(mode)
+        self._require_packed()
+        t, was_np = to_device_f32(x)
+        if t.dim() != 2 or t.shape[1] != self.in_features:
+            raise ValueError(f"expected [B, {self.in_features}] input")
+        flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+        xp = pack_planes_device(t, self.bits, self.act_grid, flags)
+        y = bitplane_gemm(self.planes, xp, self.in_features, a_grid=self.weight_grid,
+                          b_grid=self.act_grid, transpose_out=True)
+        raise_on_flags(flags, "quantize_signed requires finite inputs")
+        return _ret(y, was_np)
 
     def _strict_input(self) -> bool:
         return False

@@ -343,3 +343,91 @@ def test_large_gemm_properties(bnn, algo, mnk):
     for i, j in zip(idx_m, idx_n):
         x = int(np.bitwise_count(a_np[i] ^ b_np[j]).sum())
         assert cs[i, j] == k - x
+
+
+# ------------------------------------------------------------------ multi-bit (bit planes)
+def _codes_np(x, grid, bits=2):
+    L = (1 << bits) - 1
+    x = np.asarray(x, np.float32)
+    if grid == "signed":
+        y = np.float32(0.5) * np.clip(x, np.float32(-1), np.float32(1)) + np.float32(0.5)
+    else:
+        y = x
+    return np.floor(y * np.float32(L) + np.float32(0.5)).astype(np.int64)
+
+
+@pytest.mark.parametrize("grid", ["signed", "unsigned"])
+def test_pack_planes_codes_exact(bnn, grid):
+    rng = np.random.default_rng(31)
+    x = (rng.random((37, 301), dtype=np.float32) if grid == "unsigned"
+         else (rng.standard_normal((37, 301)) * 1.3).astype(np.float32))
+    x.reshape(-1)[:6] = [0.0, 1.0, 1 / 6, 0.5, 5 / 6, -0.0] if grid == "unsigned" else \
+        [-1.0, 1.0, -1 / 3, 1 / 3, 0.0, -0.0]
+    planes = bnn.bitpack.pack_planes_device(torch.from_numpy(x).cuda(), 2, grid).cpu().numpy()
+    codes = _codes_np(x, grid)
+    for p in range(2):
+        expect = orc.pack_rows(np.where((codes >> p) & 1, 1.0, -1.0).astype(np.float32), 0)
+        assert np.array_equal(planes[p], expect), p
+    # the codes are the reference quantizers' grid indices
+    ref = orc.quantize(x, 2) if grid == "unsigned" else orc.quantize_signed(x, 2)
+    L = np.float32(3)
+    vals = codes.astype(np.float32) / L if grid == "unsigned" else \
+        np.float32(2) * (codes.astype(np.float32) / L) - np.float32(1)
+    assert np.array_equal(vals, ref)
+    if grid == "unsigned":
+        flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+        bad = torch.from_numpy(x).cuda()
+        bad[3, 4] = 1.5
+        bnn.bitpack.pack_planes_device(bad, 2, grid, flags)
+        assert int(flags.item()) & 4
+
+
+def test_bitplane_gemm_matches_reference_float64(bnn, golden):
+    """Config-5 2-bit semantics: U[0,1] operands on the quantize() grid (G5)."""
+    g = golden["qmath"]
+    x, w = g["x"], g["w"]  # [64, 96] activations, [40, 96] weights
+    ap = bnn.bitpack.pack_planes_device(torch.from_numpy(w).cuda(), 2, "unsigned")
+    bp = bnn.bitpack.pack_planes_device(torch.from_numpy(x).cuda(), 2, "unsigned")
+    y = bnn.gemm.bitplane_gemm(ap, bp, 96, a_grid="unsigned", b_grid="unsigned",
+                               transpose_out=True).cpu().numpy()
+    ref = g["dot2"]  # float64 product of the reference's quantize() values
+    assert np.all(np.abs(y - ref) <= 1e-5 * np.maximum(1.0, np.abs(ref)))
+
+
+@pytest.mark.parametrize("m,n,k", [(40, 64, 96), (300, 257, 1000), (1024, 512, 4096)])
+@pytest.mark.parametrize("grids", [("signed", "signed"), ("unsigned", "unsigned"),
+                                   ("signed", "unsigned")])
+def test_bitplane_gemm_exact_integer_decode(bnn, m, n, k, grids):
+    rng = np.random.default_rng(m + n + k)
+    ga, gb = grids
+    mk = lambda shape, g: (rng.random(shape, dtype=np.float32) if g == "unsigned"
+                           else rng.standard_normal(shape).astype(np.float32))
+    w, x = mk((m, k), ga), mk((n, k), gb)
+    ap = bnn.bitpack.pack_planes_device(torch.from_numpy(w).cuda(), 2, ga)
+    bp = bnn.bitpack.pack_planes_device(torch.from_numpy(x).cuda(), 2, gb)
+    y = bnn.gemm.bitplane_gemm(ap, bp, k, a_grid=ga, b_grid=gb).cpu().numpy()
+    ca, cb = _codes_np(w, ga), _codes_np(x, gb)
+    aa, ba = (2, -3) if ga == "signed" else (1, 0)
+    ab, bb = (2, -3) if gb == "signed" else (1, 0)
+    num = (aa * ca + ba) @ (ab * cb + bb).T  # exact int64
+    exact = num / 9.0
+    assert np.all(np.abs(y - exact) <= 2e-7 * np.maximum(1.0, np.abs(exact))), (m, n, k)
+
+
+def test_qfullyconnected_2bit_packed_equals_float_path(bnn):
+    rng = np.random.default_rng(4)
+    layer = bnn.QFullyConnected(300, 70, act_bit=2, weight_bit=2, rng=rng)
+    x = (rng.standard_normal((33, 300)) * 0.8).astype(np.float32)
+    yf = layer.forward(x, bnn.INFER_FLOAT)  # reference float path (layers.py:370-377)
+    layer.pack()
+    yp = layer.forward(x, bnn.INFER_PACKED)
+    # float64 oracle from the reference quantizers' f32 values
+    xq = orc.quantize_signed(x, 2).astype(np.float64)
+    wq = orc.quantize_signed(layer.weight, 2).astype(np.float64)
+    ref = xq @ wq.T
+    for y in (yf, yp):
+        assert np.all(np.abs(y - ref) <= 1e-5 * np.maximum(1.0, np.abs(ref)))
+    # the reference-compatible QDense keeps rejecting multi-bit packed inference
+    q = bnn.QDense(300, 70, bits=2, rng=rng)
+    with pytest.raises(bnn.ModeError):
+        q.forward(x, bnn.INFER_PACKED)
