@@ -34,7 +34,10 @@ sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
 
 METRIC = "xnor-popcount binary TOPS (2MNK/s)"
 UNIT = "TOPS"
-WORKLOADS = ("c2", "c1", "gemm4096", "gemm8192", "gemm16384", "gemm4096k65536")
+WORKLOADS = ("c2", "c1", "gemm4096", "gemm8192", "gemm16384", "gemm4096k65536", "gemm4096_2bit",
+             "lenet", "resnet18")
+NET_WORKLOADS = {"lenet": ("binary LeNet (BASELINE configs[2]) images/s", 1024, (1, 28, 28)),
+                 "resnet18": ("binary ResNet-18 (BASELINE configs[3]) images/s", 256, (3, 224, 224))}
 
 
 def parse():
@@ -53,6 +56,11 @@ def parse():
 # ----------------------------------------------------------------- workloads
 def workload_desc(name):
     import workloads as wl
+    if name in NET_WORKLOADS:
+        desc, batch, chw = NET_WORKLOADS[name]
+        return dict(workload=desc + f", batch {batch} per GPU, input {chw} "
+                    + ("U[0,1]" if name == "lenet" else "N(0,1)") + ", random-init weights",
+                    M=0, N=0, K=0, batch=batch, seed=3 if name == "lenet" else 4)
     if name == "c2":
         c = wl.C2
         oh = (c["h"] + 2 * c["pad"][0] - c["kh"]) // c["stride"][0] + 1
@@ -65,8 +73,12 @@ def workload_desc(name):
         return dict(workload="QFullyConnected 4096->1024, batch 256 (BASELINE configs[0])",
                     M=c["units"], N=c["batch"], K=c["k"], batch=c["batch"], seed=c["seed"])
     sizes = {"gemm4096": (4096,) * 3, "gemm8192": (8192,) * 3, "gemm16384": (16384,) * 3,
-             "gemm4096k65536": (4096, 4096, 65536)}
+             "gemm4096k65536": (4096, 4096, 65536), "gemm4096_2bit": (4096,) * 3}
     m, n, k = sizes[name]
+    if name.endswith("_2bit"):
+        return dict(workload=f"2-bit GEMM (act_bit=weight_bit=2, quantize() of U[0,1]) M={m} "
+                    f"N={n} K={k} (BASELINE configs[4]); TOPS = logical 2MNK/s",
+                    M=m, N=n, K=k, batch=n, seed=m + n + k + 2)
     return dict(workload=f"binary GEMM M={m} N={n} K={k} (BASELINE configs[4])", M=m, N=n, K=k,
                 batch=n, seed=m + n + k)
 
@@ -100,6 +112,28 @@ def build_plan(name, algo):
         plan.x.copy_(host_x)
         return plan, host_x
     d = workload_desc(name)
+    if name in NET_WORKLOADS:
+        from paper_1705_09864_b200 import nets
+        from paper_1705_09864_b200.plan import NetPlan
+        _, batch, chw = NET_WORKLOADS[name]
+        net = nets.lenet_c3(d["seed"]) if name == "lenet" else nets.resnet18_c4(d["seed"])
+        net.pack_for_inference()
+        g = torch.Generator(device="cuda").manual_seed(d["seed"])
+        plan = NetPlan(net, batch, chw)
+        if name == "lenet":
+            plan.x.copy_(torch.rand(plan.x.shape, device="cuda", generator=g))
+        else:
+            plan.x.copy_(torch.randn(plan.x.shape, device="cuda", generator=g))
+        return plan, plan.x.cpu().pin_memory()
+    if name.endswith("_2bit"):
+        from paper_1705_09864_b200.bitpack import pack_planes_device
+        from paper_1705_09864_b200.plan import BitplanePlan
+        g = torch.Generator(device="cuda").manual_seed(d["seed"])
+        wf = torch.rand((d["M"], d["K"]), device="cuda", generator=g)
+        xf = torch.rand((d["N"], d["K"]), device="cuda", generator=g)
+        ap = pack_planes_device(wf, 2, "unsigned")
+        bp = pack_planes_device(xf, 2, "unsigned")
+        return BitplanePlan(ap, bp, d["K"]), bp.cpu().pin_memory()
     g = torch.Generator(device="cuda").manual_seed(d["seed"])
     W = (d["K"] + 63) // 64
     aw = torch.randint(-2**63, 2**63 - 1, (d["M"], W), device="cuda", generator=g).view(torch.uint64)
@@ -187,6 +221,34 @@ def cpu_reference_step(name, sample_frac_hint=None):
         d = workload_desc(name)
         return dt, 2 * d["M"] * d["N"] * d["K"], "full batch: binarize+pack+xnor_gemm", y
     d = workload_desc(name)
+    if name in NET_WORKLOADS:
+        import torch
+        from oracle import nets_ref
+        from paper_1705_09864_b200 import nets
+        _, batch, chw = NET_WORKLOADS[name]
+        nb = sample_frac_hint or 1
+        net = _CPU_NETS.get(name)
+        if net is None:
+            net = nets.lenet_c3(d["seed"]) if name == "lenet" else nets.resnet18_c4(d["seed"])
+            _CPU_NETS[name] = net
+        rng = np.random.default_rng(d["seed"])
+        x = (rng.random((nb,) + chw, dtype=np.float32) if name == "lenet"
+             else rng.standard_normal((nb,) + chw, dtype=np.float32))
+        t0 = time.perf_counter()
+        y = nets_ref.forward(net, x, threads)
+        dt = time.perf_counter() - t0
+        return dt, nb, f"{nb} of {batch} images: full forward, reference layer semantics", y
+    if name.endswith("_2bit"):
+        # the reference's only multi-bit path: float BLAS on quantized values
+        # (QDense(bits=2) INFER_FLOAT, layers.py:370-377)
+        rows = sample_frac_hint or min(d["M"], 256)
+        rng = np.random.default_rng(d["seed"])
+        wq = orc.quantize(rng.random((rows, d["K"]), dtype=np.float32), 2).astype(np.float32)
+        xq = orc.quantize(rng.random((d["N"], d["K"]), dtype=np.float32), 2).astype(np.float32)
+        t0 = time.perf_counter()
+        y = xq @ wq.T
+        dt = time.perf_counter() - t0
+        return dt, 2 * rows * d["N"] * d["K"], f"{rows} of {d['M']} rows: f32 BLAS on quantize() values", y
     rows = sample_frac_hint or min(d["M"], 256)
     rng = np.random.default_rng(d["seed"])
     W = (d["K"] + 63) // 64
@@ -198,11 +260,17 @@ def cpu_reference_step(name, sample_frac_hint=None):
     return dt, 2 * rows * d["N"] * d["K"], f"{rows} of {d['M']} rows: xnor_gemm_parallel", y
 
 
+_CPU_NETS = {}
+
+
 def calibrate_cpu_sample(name, budget_s=2.0):
     """Pick a sample size whose single step takes about budget_s."""
     import workloads as wl
     if name == "c1":
         return None
+    if name in NET_WORKLOADS:
+        dt, _, _, _ = cpu_reference_step(name, 1)
+        return int(max(1, min(NET_WORKLOADS[name][1], budget_s / max(dt, 1e-3))))
     if name == "c2":
         dt, _, _, _ = cpu_reference_step(name, 1)
         return int(max(1, min(wl.C2["b"], budget_s / max(dt, 1e-3))))
@@ -221,6 +289,10 @@ def cpu_baseline(name, seconds=12.0):
         if time.perf_counter() > t_end and len(times) >= 3:
             break
     med = statistics.median(times)
+    if name in NET_WORKLOADS:
+        return {"value": ops / med, "unit": "images/s", "cores": os.cpu_count(), "kind": "port",
+                "sample": f"{desc}; median of {len(times)} runs ({med * 1e3:.1f} ms each)",
+                "seconds_per_step": med}
     return {"value": ops / med / 1e12, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
             "sample": f"{desc}; median of {len(times)} runs ({med * 1e3:.1f} ms each)",
             "seconds_per_step": med}
@@ -238,18 +310,21 @@ def run_reference_arm(args, rank, world):
         dt, ops, desc, _ = cpu_reference_step(name, sample)
         times.append(dt)
     total = sum(times)
-    value = ops * len(times) / total / 1e12
+    is_net = name in NET_WORKLOADS
+    value = ops * len(times) / total / (1.0 if is_net else 1e12)
+    metric = NET_WORKLOADS[name][0] if is_net else METRIC
+    unit = "images/s" if is_net else UNIT
     d = workload_desc(name)
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "impl": "reference", "metric": metric, "value": value, "unit": unit, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / len(times) * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
         "data": "synthetic (seeded, BASELINE.json shapes)",
         "config": {"workload": d["workload"], "M": d["M"], "N": d["N"], "K": d["K"],
                    "parallelism": "host threads"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+        "cpu_baseline": {"value": value, "unit": unit, "cores": os.cpu_count(), "kind": "port",
                          "sample": desc},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
@@ -375,7 +450,11 @@ def run_gpu_arm(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    value = world * ops / (ms_per_step * 1e-3) / 1e12
+    is_net = args.workload in NET_WORKLOADS
+    units_per_step = d["batch"] if is_net else ops / 1e12  # images or tera-ops
+    metric = NET_WORKLOADS[args.workload][0] if is_net else METRIC
+    unit = "images/s" if is_net else UNIT
+    value = world * units_per_step / (ms_per_step * 1e-3)
 
     # end to end through the public plan API with pinned host buffers
     e2e = None
@@ -398,7 +477,7 @@ def run_gpu_arm(args, rank, world, local_rank):
             t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_ms = float(t.item())
-        e2e = {"value": world * ops / (e2e_ms / args.steps * 1e-3) / 1e12, "unit": UNIT,
+        e2e = {"value": world * units_per_step / (e2e_ms / args.steps * 1e-3), "unit": unit,
                "h2d_bytes_per_step": plan.h2d_bytes, "d2h_bytes_per_step": plan.d2h_bytes,
                "ms_per_step": e2e_ms / args.steps,
                "path": "plan.run_host: pinned H2D -> pack -> kernel -> D2H -> sync"}
@@ -411,6 +490,9 @@ def run_gpu_arm(args, rank, world, local_rank):
             "traffic": load_traffic(args.workload, args.algo), "kernel_ms": kern_avg,
             "pack_ms_est": statistics.mean(pack_ms), "peak_source": peak["peak_source"],
             "ops_per_launch": ops, "popc_pipe_peak_tops": peak["popc_peak"]}
+    if is_net:
+        roof["note"] = ("whole-network step: achieved = binary ops of all binary layers / step "
+                        "time (float stem / classifier / BN / pooling included in the time)")
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -418,7 +500,7 @@ def run_gpu_arm(args, rank, world, local_rank):
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "metric": metric, "value": value, "unit": unit, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "u8 (bits expanded in SMEM, s32 accumulate)" if args.algo in ("auto", "umma")

@@ -106,7 +106,25 @@ class QActivation:
 
 
 class _QLayer:
-    """Shared packed-weight state of the quantized conv / dense layers."""
+    """Shared packed-weight state of the quantized conv / dense layers.
+
+    ``sync_checks`` (default True) reads the pack kernel's flag word after
+    every packed forward to raise the reference's ValueError on non-finite /
+    non-sign input; network runners and CUDA-graph capture set it False and
+    read ``flags`` once at the end instead (no host sync per layer).
+    """
+
+    sync_checks = True
+    flags = None
+
+    def _flags(self):
+        if self.flags is None:
+            self.flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+        return self.flags
+
+    def _finish(self, flags, msg="binarize requires finite inputs"):
+        if self.sync_checks:
+            raise_on_flags(flags, msg)
 
     def _set_packed(self, bm: BitMatrix):
         self.packed = bm
@@ -231,10 +249,11 @@ class QConv2d(_QLayer):
         self.output_hw(h, w)
         if mode == INFER_PACKED:
             self._require_packed()
-            flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+            flags = torch.zeros(1, dtype=torch.int32, device="cuda") if self.sync_checks \
+                else self._flags()
             xw = pack_nchw(t, strict=self._strict_input(), flags=flags)
             y = self.forward_packed_words(xw, b, h, w)
-            raise_on_flags(flags)
+            self._finish(flags)
             return _ret(y, was_np)
         if self.weight is None:
             raise ModeError("layer holds packed weights only; float modes unavailable")
@@ -296,10 +315,11 @@ class QDense(_QLayer):
             self._require_packed()
             if t.dim() != 2 or t.shape[1] != self.in_features:
                 raise ValueError(f"expected [B, {self.in_features}] input")
-            flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+            flags = torch.zeros(1, dtype=torch.int32, device="cuda") if self.sync_checks \
+                else self._flags()
             xw = pack_rows_device(t, 0, strict=self._strict_input(), flags=flags)
             y = self.forward_packed_rows(xw)
-            raise_on_flags(flags)
+            self._finish(flags)
             return _ret(y, was_np)
         if self.weight is None:
             raise ModeError("layer holds packed weights only; float modes unavailable")

@@ -1,0 +1,242 @@
+"""Whole-network inference runners built on the packed hot path.
+
+* ``lenet_c3`` -- BASELINE configs[2]: full-precision conv5x5(1->64, pad 2) +
+  tanh + maxpool, QActivation + QConvolution5x5(64->64, pad 2, 1 bit) + BN +
+  maxpool, QFullyConnected(3136->1000, 1 bit) + BN, full-precision FC(1000->10).
+* ``resnet18_c4`` -- BASELINE configs[3]: binary ResNet-18; the stem conv and
+  the classifier are full precision, every other conv (3x3 and the 1x1
+  downsamples) is a 1-bit QConvolution preceded by the sign activation and
+  followed by BatchNorm; basic block  out = BN(QConv(sign(BN(QConv(sign(x)))))) + shortcut.
+
+Float layers mirror the reference's inference semantics (layers.py:81-141,
+422-659): convolutions/dense in float32 with TF32 off, BatchNorm with running
+statistics in the reference's op order  gamma * ((x - mean) * inv_std) + beta
+(layers.py:596-602).  They run as torch ops -- they are not the hot path;
+every binary layer runs the sm_100a kernels in ``infer_packed`` mode and the
+float-path equivalent in ``infer_float`` mode, so the two modes must agree
+exactly at every binary layer (the reference's cross-mode property,
+test_layers.py:181-220).  Weights are random-init with NumPy generators
+(layers._uniform_init rule) -- there is no network access for checkpoints.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.nn.functional as F
+
+from . import _lib
+from .layers import (INFER_FLOAT, INFER_PACKED, QConvolution, QFullyConnected, _check_mode,
+                     _float_matmul, _uniform_init)
+
+BN_EPS = 1e-5  # layers.py:36
+
+
+def _t(a: np.ndarray) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()
+
+
+class _Lazy:
+    """Host (NumPy) parameters, uploaded to the GPU on first use (the CPU
+    reference can build the same network without a device)."""
+
+    def _dev(self, name):
+        cache = self.__dict__.setdefault("_dev_cache", {})
+        if name not in cache:
+            a = getattr(self, name)
+            cache[name] = None if a is None else _t(a)
+        return cache[name]
+
+
+class Conv2d(_Lazy):
+    """Full-precision convolution (layers.py:81-141), NCHW f32, TF32 off."""
+
+    def __init__(self, cin, cout, k, stride=1, pad=0, bias=True, rng=None):
+        self.k, self.cout, self.stride, self.pad = k, cout, stride, pad
+        fan_in, fan_out = cin * k * k, cout * k * k
+        self.weight = _uniform_init(rng, (cout, cin, k, k), fan_in, fan_out) if rng is not None \
+            else np.zeros((cout, cin, k, k), np.float32)
+        self.bias = np.zeros(cout, np.float32) if bias else None
+
+    def forward(self, x, mode=INFER_FLOAT):
+        prev = torch.backends.cudnn.allow_tf32
+        torch.backends.cudnn.allow_tf32 = False
+        try:
+            return F.conv2d(x, self._dev("weight"), self._dev("bias"), stride=self.stride,
+                            padding=self.pad)
+        finally:
+            torch.backends.cudnn.allow_tf32 = prev
+
+
+class Dense(_Lazy):
+    """Full-precision linear layer y = x W^T + b (layers.py:266-317)."""
+
+    def __init__(self, fin, fout, bias=True, rng=None):
+        self.weight = _uniform_init(rng, (fout, fin), fin, fout) if rng is not None else \
+            np.zeros((fout, fin), np.float32)
+        self.bias = np.zeros(fout, np.float32) if bias else None
+
+    def forward(self, x, mode=INFER_FLOAT):
+        y = _float_matmul(x, self._dev("weight").T)
+        b = self._dev("bias")
+        return y + b if b is not None else y
+
+
+class BatchNorm(_Lazy):
+    """Inference BatchNorm in the reference op order (layers.py:587-602)."""
+
+    def __init__(self, channels, rng=None):
+        if rng is not None:  # randomised running stats as gen_golden.py:46-52 does
+            self.gamma = (0.5 + rng.random(channels)).astype(np.float32)
+            self.beta = (rng.standard_normal(channels) * 0.1).astype(np.float32)
+            self.mean = (rng.standard_normal(channels) * 0.05).astype(np.float32)
+            self.var = (0.5 + rng.random(channels)).astype(np.float32)
+        else:
+            self.gamma = np.ones(channels, np.float32)
+            self.beta = np.zeros(channels, np.float32)
+            self.mean = np.zeros(channels, np.float32)
+            self.var = np.ones(channels, np.float32)
+        self.inv_std = (1.0 / np.sqrt(self.var + np.float32(BN_EPS))).astype(np.float32)
+
+    def forward(self, x, mode=INFER_FLOAT):
+        shape = (1, -1, 1, 1) if x.dim() == 4 else (1, -1)
+        xhat = (x - self._dev("mean").view(shape)) * self._dev("inv_std").view(shape)
+        return self._dev("gamma").view(shape) * xhat + self._dev("beta").view(shape)
+
+
+class Tanh:
+    def forward(self, x, mode=INFER_FLOAT):
+        return torch.tanh(x)
+
+
+class ReLU:
+    def forward(self, x, mode=INFER_FLOAT):
+        return torch.relu(x)
+
+
+class MaxPool2d:
+    def __init__(self, k, stride=None, pad=0):
+        self.k, self.stride, self.pad = k, stride or k, pad
+
+    def forward(self, x, mode=INFER_FLOAT):
+        return F.max_pool2d(x, self.k, self.stride, self.pad)
+
+
+class Flatten:
+    def forward(self, x, mode=INFER_FLOAT):
+        return x.reshape(x.shape[0], -1)  # NCHW flatten order (layers.py:459)
+
+
+class GlobalAvgPool:
+    def forward(self, x, mode=INFER_FLOAT):
+        return x.mean(dim=(2, 3))
+
+
+class Sequential:
+    def __init__(self, layers):
+        self.layers = list(layers)
+
+    def forward(self, x, mode=INFER_FLOAT, capture=None):
+        for layer in self.layers:
+            x = layer.forward(x, mode)
+            if capture is not None:
+                capture.append(x)
+        return x
+
+    def binary_layers(self):
+        out = []
+        for l in self.layers:
+            if isinstance(l, (QConvolution, QFullyConnected)):
+                out.append(l)
+            elif hasattr(l, "binary_layers"):
+                out.extend(l.binary_layers())
+        return out
+
+    def pack_for_inference(self):
+        for l in self.binary_layers():
+            l.pack()
+
+
+class BinaryBasicBlock:
+    """out = BN2(QConv3x3(sign(BN1(QConv3x3(sign(x), stride))))) + shortcut(x)."""
+
+    def __init__(self, cin, cout, stride, rng):
+        self.conv1 = QConvolution(cin, cout, (3, 3), (stride, stride), (1, 1), rng=rng, domain="dot")
+        self.bn1 = BatchNorm(cout, rng)
+        self.conv2 = QConvolution(cout, cout, (3, 3), (1, 1), (1, 1), rng=rng, domain="dot")
+        self.bn2 = BatchNorm(cout, rng)
+        self.down = None
+        if stride != 1 or cin != cout:
+            self.down = QConvolution(cin, cout, (1, 1), (stride, stride), (0, 0), rng=rng,
+                                     domain="dot")
+            self.bnd = BatchNorm(cout, rng)
+
+    def binary_layers(self):
+        return [self.conv1, self.conv2] + ([self.down] if self.down else [])
+
+    def forward(self, x, mode=INFER_FLOAT):
+        h = self.bn1.forward(self.conv1.forward(x, mode))
+        h = self.bn2.forward(self.conv2.forward(h, mode))
+        sc = x if self.down is None else self.bnd.forward(self.down.forward(x, mode))
+        return h + sc
+
+
+def lenet_c3(seed: int = 0) -> Sequential:
+    """BASELINE configs[2] topology, random init."""
+    rng = np.random.default_rng(seed)
+    return Sequential([
+        Conv2d(1, 64, 5, pad=2, rng=rng), Tanh(), MaxPool2d(2),
+        QConvolution(64, 64, (5, 5), (1, 1), (2, 2), rng=rng),  # sign of the input fused
+        BatchNorm(64, rng), MaxPool2d(2), Flatten(),
+        QFullyConnected(64 * 7 * 7, 1000, rng=rng), BatchNorm(1000, rng),
+        Dense(1000, 10, rng=rng),
+    ])
+
+
+def resnet18_c4(seed: int = 0, num_classes: int = 1000) -> Sequential:
+    """BASELINE configs[3]: binary ResNet-18 (stem and classifier full precision)."""
+    rng = np.random.default_rng(seed)
+    layers = [Conv2d(3, 64, 7, stride=2, pad=3, bias=False, rng=rng), BatchNorm(64, rng), ReLU(),
+              MaxPool2d(3, 2, 1)]
+    cin = 64
+    for cout, stride in ((64, 1), (128, 2), (256, 2), (512, 2)):
+        layers.append(BinaryBasicBlock(cin, cout, stride, rng))
+        layers.append(BinaryBasicBlock(cout, cout, 1, rng))
+        cin = cout
+    layers += [GlobalAvgPool(), Dense(512, num_classes, rng=rng)]
+    return Sequential(layers)
+
+
+def binary_ops_per_image(net: Sequential, chw) -> int:
+    """2*M*N*K summed over the binary layers for one image."""
+    c, h, w = chw
+    total = 0
+
+    def conv(layer, c, h, w):
+        oh, ow = layer.output_hw(h, w)
+        return layer.filters, oh, ow, 2 * layer.filters * oh * ow * layer.k_reduce
+
+    for layer in net.layers:
+        if isinstance(layer, Conv2d):
+            h = (h + 2 * layer.pad - layer.k) // layer.stride + 1
+            w = (w + 2 * layer.pad - layer.k) // layer.stride + 1
+            c = layer.cout
+        elif isinstance(layer, MaxPool2d):
+            h = (h + 2 * layer.pad - layer.k) // layer.stride + 1
+            w = (w + 2 * layer.pad - layer.k) // layer.stride + 1
+        elif isinstance(layer, QConvolution):
+            c, h, w, ops = conv(layer, c, h, w)
+            total += ops
+        elif isinstance(layer, BinaryBasicBlock):
+            c1, h1, w1, o1 = conv(layer.conv1, c, h, w)
+            _, _, _, o2 = conv(layer.conv2, c1, h1, w1)
+            total += o1 + o2
+            if layer.down is not None:
+                total += conv(layer.down, c, h, w)[3]
+            c, h, w = c1, h1, w1
+        elif isinstance(layer, (Flatten, GlobalAvgPool)):
+            c, h, w = (c * h * w if isinstance(layer, Flatten) else c), 1, 1
+        elif isinstance(layer, QFullyConnected):
+            total += 2 * layer.units * layer.in_features
+            c = layer.units
+    return total

@@ -174,3 +174,72 @@ class GemmPlan(_Plan):
     def run_device(self):
         self.kernel()
         return self.y
+
+
+class BitplanePlan(_Plan):
+    """Multi-bit (act_bit = weight_bit = 2) GEMM on pre-packed bit planes (config 5)."""
+
+    launches_per_step = 1
+
+    def __init__(self, a_planes: torch.Tensor, b_planes: torch.Tensor, k: int,
+                 a_grid: str = "unsigned", b_grid: str = "unsigned"):
+        self.a, self.bw = a_planes, b_planes
+        self.bits, self.m, _ = a_planes.shape
+        self.n, self.k = b_planes.shape[1], k
+        self.x = b_planes
+        self.y = torch.empty((self.m, self.n), dtype=torch.float32, device="cuda")
+        self.grids = (a_grid, b_grid)
+        self._alloc_common()
+
+    @property
+    def binary_ops(self) -> int:
+        return 2 * self.m * self.n * self.k  # logical 2MNK (plane ops = x bits^2)
+
+    def pack(self, stream=None):
+        pass
+
+    def kernel(self, stream=None):
+        from .gemm import bitplane_gemm
+        bitplane_gemm(self.a, self.bw, self.k, a_grid=self.grids[0], b_grid=self.grids[1],
+                      out=self.y)
+
+    def run_device(self):
+        self.kernel()
+        return self.y
+
+
+class NetPlan(_Plan):
+    """Whole-network inference step (LeNet C3 / ResNet-18 C4) on a resident batch.
+
+    Binary layers run without per-layer host syncs (sync_checks = False) and
+    share one flag word, read once by check_flags / run_host.
+    """
+
+    def __init__(self, net, batch: int, chw):
+        from .layers import INFER_PACKED
+        from .nets import binary_ops_per_image
+        self.net, self.b, self.chw = net, batch, tuple(chw)
+        self.mode = INFER_PACKED
+        self._alloc_common()
+        for layer in net.binary_layers():
+            layer.sync_checks = False
+            layer.flags = self.flags
+        self.x = torch.empty((batch,) + self.chw, dtype=torch.float32, device="cuda")
+        self.ops_per_image = binary_ops_per_image(net, self.chw)
+        self.y = net.forward(self.x, self.mode)
+        self.launches_per_step = 2 * len(net.binary_layers())
+
+    @property
+    def binary_ops(self) -> int:
+        return self.b * self.ops_per_image
+
+    def pack(self, stream=None):
+        pass
+
+    def kernel(self, stream=None):
+        out = self.net.forward(self.x, self.mode)
+        self.y.copy_(out)
+        return self.y
+
+    def run_device(self):
+        return self.kernel()

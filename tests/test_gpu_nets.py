@@ -1,0 +1,107 @@
+"""Whole-network runners: cross-mode exactness + teacher-forced oracle.
+
+As in the reference (test_layers.py:181-220), the packed path and the float
+path must agree exactly at every binary layer; the binary conv is also
+checked against the pinned CPU oracle on the GPU's own layer input
+(teacher forcing), so float-op rounding differences upstream
+cannot mask a kernel error.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def nets():
+    import paper_1705_09864_b200 as p
+    p.load_library()
+    from paper_1705_09864_b200 import nets as n
+    return n
+
+
+def _modes(net, x, bnn):
+    cap_f, cap_p = [], []
+    yf = net.forward(x, bnn.INFER_FLOAT, capture=cap_f)
+    yp = net.forward(x, bnn.INFER_PACKED, capture=cap_p)
+    return yf, yp, cap_f, cap_p
+
+
+def test_lenet_c3_cross_mode_and_oracle(nets):
+    import paper_1705_09864_b200 as bnn
+    net = nets.lenet_c3(seed=3)
+    net.pack_for_inference()
+    x = torch.rand((16, 1, 28, 28), generator=torch.Generator().manual_seed(0)).cuda()
+    yf, yp, cap_f, cap_p = _modes(net, x, bnn)
+    for i, layer in enumerate(net.layers):
+        if isinstance(layer, (bnn.QConvolution, bnn.QFullyConnected)):
+            assert torch.equal(cap_f[i], cap_p[i]), f"layer {i}"
+    assert torch.equal(yf, yp)
+    assert yp.shape == (16, 10)
+    # teacher-forced: the binary conv's GPU input through the CPU oracle
+    conv = net.layers[3]
+    xin = cap_p[2].cpu().numpy()
+    expect = orc.qconv_packed(xin, conv.weight, conv.stride, conv.pad)
+    assert np.array_equal(cap_p[3].cpu().numpy(), expect)
+    fc = net.layers[7]
+    xin = cap_p[6].cpu().numpy()
+    expect = orc.qdense_packed(orc.binarize(xin), fc.weight)
+    assert np.array_equal(cap_p[7].cpu().numpy(), expect)
+    assert nets.binary_ops_per_image(net, (1, 28, 28)) == \
+        2 * 64 * 14 * 14 * 64 * 25 + 2 * 1000 * 3136
+
+
+def test_resnet18_c4_cross_mode(nets):
+    import paper_1705_09864_b200 as bnn
+    net = nets.resnet18_c4(seed=5, num_classes=1000)
+    net.pack_for_inference()
+    g = torch.Generator().manual_seed(1)
+    x = torch.randn((2, 3, 224, 224), generator=g).cuda()
+    yf, yp, cap_f, cap_p = _modes(net, x, bnn)
+    assert yp.shape == (2, 1000)
+    # blocks are composite: compare every block output (binary layers inside are exact)
+    for i, layer in enumerate(net.layers):
+        if isinstance(layer, nets.BinaryBasicBlock):
+            assert torch.equal(cap_f[i], cap_p[i]), f"block {i}"
+    assert torch.equal(yf, yp)
+    ops = nets.binary_ops_per_image(net, (3, 224, 224))
+    assert 3.3e9 < ops < 3.5e9  # 3.391e9 binary ops / image
+
+
+def test_resnet_block_teacher_forced_oracle(nets):
+    """One stride-2 block's binary convs against the oracle on the GPU's own inputs."""
+    import paper_1705_09864_b200 as bnn
+    rng = np.random.default_rng(9)
+    blk = nets.BinaryBasicBlock(64, 128, 2, rng)
+    for c in blk.binary_layers():
+        c.pack()
+    x = torch.randn((2, 64, 20, 20), generator=torch.Generator().manual_seed(2)).cuda()
+    h1 = blk.conv1.forward(x, bnn.INFER_PACKED)
+    xn = x.cpu().numpy()
+    p = orc.qconv_packed(xn, blk.conv1.weight, (2, 2), (1, 1))
+    assert np.array_equal(h1.cpu().numpy(), 2 * p - 64 * 9)  # dot domain
+    d = blk.down.forward(x, bnn.INFER_PACKED)
+    p = orc.qconv_packed(xn, blk.down.weight, (2, 2), (0, 0))
+    assert np.array_equal(d.cpu().numpy(), 2 * p - 64)
+
+
+def test_lenet_end_to_end_vs_cpu_reference(nets):
+    """Full-network agreement with the CPU reference composition (float ops differ in
+    rounding between cuDNN/torch and NumPy, so a sign can flip near 0)."""
+    import paper_1705_09864_b200 as bnn
+    from oracle import nets_ref
+    net = nets.lenet_c3(seed=11)
+    net.pack_for_inference()
+    x = np.random.default_rng(3).random((32, 1, 28, 28), dtype=np.float32)
+    cap = []
+    y_gpu = net.forward(torch.from_numpy(x).cuda(), bnn.INFER_PACKED, capture=cap).cpu().numpy()
+    y_cpu = nets_ref.forward(net, x)
+    assert (y_gpu.argmax(1) == y_cpu.argmax(1)).mean() >= 0.9
+    # the binary conv input differs from the CPU one only by float rounding: count sign flips
+    xin_gpu = cap[2].cpu().numpy()
+    flips = np.mean((xin_gpu >= 0) != (nets_ref.forward(nets.Sequential(net.layers[:3]), x) >= 0))
+    assert flips < 1e-3
