@@ -156,6 +156,26 @@ int bnn_bitplane_gemm(const uint64_t *A, int64_t lda, int64_t a_plane_stride, in
                       int bits, int64_t M, int64_t N, int64_t K, float *C, int64_t ldc_m,
                       int64_t ldc_n, bnn_stream_t stream);
 
+/* Fused epilogue of the GEMM / conv (all fields optional except domain):
+ *   v  = domain == BNN_DOT ? 2P - K : P
+ *   v  = v * scale[m] + shift[m]                                  (affine)
+ *   v  = gamma[m] * ((v - mean[m]) * inv_std[m]) + beta[m]         (inference
+ *        BatchNorm in the reference's op order, layers.py:598-602, each op
+ *        rounded as NumPy float32 does -- bit-identical to an unfused BN)
+ *   out = v + residual[same index as out]                          (shortcut)
+ */
+typedef struct bnn_epilogue {
+    int domain;
+    const float *scale, *shift;
+    const float *bn_mean, *bn_inv_std, *bn_gamma, *bn_beta;
+    const float *residual;
+} bnn_epilogue;
+
+/* bnn_xnor_gemm / bnn_bconv2d with the full fused epilogue. */
+int bnn_xnor_gemm_ex(const uint64_t *A, int64_t lda, const uint64_t *B, int64_t ldb, int64_t M,
+                     int64_t N, int64_t K, int a_pad, int b_pad, float *C, int64_t ldc_m,
+                     int64_t ldc_n, const bnn_epilogue *ep, int algo, bnn_stream_t stream);
+
 /* Words per pixel of the packed NHWC activation layout: ceil(C / 64). */
 int64_t bnn_conv_channel_words(int64_t C);
 
@@ -194,6 +214,11 @@ int bnn_umma_trace(uint64_t *buf);
  * `sink` is a caller-allocated device u32 the kernel may write. */
 int bnn_probe_pipe_peak(int pipe, int64_t iters, uint32_t *sink, double *ops_per_sec,
                         bnn_stream_t stream);
+
+int bnn_bconv2d_ex(const uint64_t *x_words, int64_t B, int64_t C, int64_t H, int64_t W,
+                   const uint64_t *w_dev, int64_t F, int64_t kh, int64_t kw, int64_t sh,
+                   int64_t sw, int64_t ph, int64_t pw, float *y, const bnn_epilogue *ep, int algo,
+                   bnn_stream_t stream);
 
 #ifdef __cplusplus
 }

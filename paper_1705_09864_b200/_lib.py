@@ -47,8 +47,20 @@ SIGNATURES = {
     "bnn_bitplane_gemm": (_i32, [_vp, _i64, _i64, _i32, _vp, _i64, _i64, _i32, _i32, _i64, _i64,
                                  _i64, _vp, _i64, _i64, _vp]),
     "bnn_set_umma_variant": (_i32, [_i32]),
+    "bnn_xnor_gemm_ex": (_i32, [_vp, _i64, _vp, _i64, _i64, _i64, _i64, _i32, _i32, _vp, _i64,
+                                _i64, _vp, _i32, _vp]),
+    "bnn_bconv2d_ex": (_i32, [_vp, _i64, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i64,
+                              _i64, _i64, _vp, _vp, _i32, _vp]),
     "bnn_umma_trace": (_i32, [_vp]),
 }
+
+
+class Epilogue(ctypes.Structure):
+    """struct bnn_epilogue (include/bnn_b200.h)."""
+    _fields_ = [("domain", ctypes.c_int), ("scale", ctypes.c_void_p), ("shift", ctypes.c_void_p),
+                ("bn_mean", ctypes.c_void_p), ("bn_inv_std", ctypes.c_void_p),
+                ("bn_gamma", ctypes.c_void_p), ("bn_beta", ctypes.c_void_p),
+                ("residual", ctypes.c_void_p)]
 
 
 class BnnError(RuntimeError):

@@ -41,19 +41,19 @@ int launch_conv_weights_reorder(const uint64_t *, int64_t, int64_t, int64_t, int
                                 uint64_t *, cudaStream_t);
 int launch_xnor_gemm_popc(const uint64_t *, int64_t, const uint64_t *, int64_t, int64_t,
                           int64_t, int64_t, float *, int64_t, int64_t, const Epilogue &,
-                          cudaStream_t);
+                          cudaStream_t, const float *);
 int launch_xnor_gemm_umma(const uint64_t *, int64_t, const uint64_t *, int64_t, int64_t,
                           int64_t, int64_t, float *, int64_t, int64_t, const Epilogue &,
-                          cudaStream_t);
+                          cudaStream_t, const float *);
 int launch_bconv2d_umma(const uint64_t *, int64_t, int64_t, int64_t, int64_t, const uint64_t *,
                         int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,
-                        int64_t, float *, const Epilogue &, cudaStream_t);
+                        int64_t, float *, const Epilogue &, cudaStream_t, const float *);
 int launch_xnor_gemm_bmma(const uint64_t *, int64_t, const uint64_t *, int64_t, int64_t,
                           int64_t, int64_t, float *, int64_t, int64_t, const Epilogue &,
-                          cudaStream_t);
+                          cudaStream_t, const float *);
 int launch_bconv2d_bmma(const uint64_t *, int64_t, int64_t, int64_t, int64_t, const uint64_t *,
                         int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,
-                        int64_t, float *, const Epilogue &, cudaStream_t);
+                        int64_t, float *, const Epilogue &, cudaStream_t, const float *);
 int launch_pack_planes(const float *, int64_t, int64_t, int64_t, int, int, uint64_t *, int64_t,
                        int64_t, int32_t *, cudaStream_t);
 int launch_bitplane_gemm_umma(const uint64_t *, int64_t, int64_t, const uint64_t *, int64_t,
@@ -61,7 +61,7 @@ int launch_bitplane_gemm_umma(const uint64_t *, int64_t, int64_t, const uint64_t
                               const Epilogue &, cudaStream_t);
 int launch_bconv2d_popc(const uint64_t *, int64_t, int64_t, int64_t, int64_t, const uint64_t *,
                         int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,
-                        int64_t, float *, const Epilogue &, cudaStream_t);
+                        int64_t, float *, const Epilogue &, cudaStream_t, const float *);
 
 }  // namespace bnn
 
@@ -167,37 +167,59 @@ static int check_gemm_dims(int64_t M, int64_t N, int64_t K) {
     return BNN_OK;
 }
 
-int bnn_xnor_gemm(const uint64_t *A, int64_t lda, const uint64_t *B, int64_t ldb, int64_t M,
-                  int64_t N, int64_t K, int a_pad, int b_pad, float *C, int64_t ldc_m,
-                  int64_t ldc_n, int domain, const float *scale, const float *shift, int algo,
-                  bnn_stream_t stream) {
+static void fill_epilogue(Epilogue &ep, const bnn_epilogue *e) {
+    ep.scale = e->scale;
+    ep.shift = e->shift;
+    ep.bn_mean = e->bn_mean;
+    ep.bn_inv = e->bn_inv_std;
+    ep.bn_gamma = e->bn_gamma;
+    ep.bn_beta = e->bn_beta;
+}
+
+int bnn_xnor_gemm_ex(const uint64_t *A, int64_t lda, const uint64_t *B, int64_t ldb, int64_t M,
+                     int64_t N, int64_t K, int a_pad, int b_pad, float *C, int64_t ldc_m,
+                     int64_t ldc_n, const bnn_epilogue *e, int algo, bnn_stream_t stream) {
     int rc = check_gemm_dims(M, N, K);
     if (rc) return rc;
+    BNN_REQUIRE(e != nullptr, BNN_EINVAL, "null epilogue");
     BNN_REQUIRE((a_pad == 0 || a_pad == 1) && (b_pad == 0 || b_pad == 1), BNN_EPAD,
                 "pad fills must be 0 or 1");
     const int64_t W = ceil_div(K, 64);
     BNN_REQUIRE(lda >= W && ldb >= W, BNN_EALIGN, "lda/ldb smaller than ceil(K/64)=%lld",
                 (long long)W);
     BNN_REQUIRE(A && B && C, BNN_EINVAL, "null pointer");
+    const int domain = e->domain;
     BNN_REQUIRE(domain == BNN_POPCOUNT || domain == BNN_DOT, BNN_EINVAL, "bad domain %d", domain);
+    BNN_REQUIRE(!e->bn_mean || (e->bn_inv_std && e->bn_gamma && e->bn_beta), BNN_EINVAL,
+                "BatchNorm epilogue needs mean, inv_std, gamma and beta");
     // Tail correction (bitpack.py:12-15): positions K..64W-1 contribute
     // popc(a_pad ^ b_pad) each to X, so P = K - (X - tail) = k_eff - X.
     const int64_t tail = (64 * W - K) * (int64_t)(a_pad ^ b_pad);
-    Epilogue ep{(int32_t)(K + tail), (int32_t)K, domain, scale, shift};
+    Epilogue ep{(int32_t)(K + tail), (int32_t)K, domain, nullptr, nullptr};
+    fill_epilogue(ep, e);
     switch (algo) {
         case BNN_ALGO_POPC:
             return launch_xnor_gemm_popc(A, lda, B, ldb, M, N, K, C, ldc_m, ldc_n, ep,
-                                         as_stream(stream));
+                                         as_stream(stream), e->residual);
         case BNN_ALGO_BMMA:
             return launch_xnor_gemm_bmma(A, lda, B, ldb, M, N, K, C, ldc_m, ldc_n, ep,
-                                         as_stream(stream));
+                                         as_stream(stream), e->residual);
         case BNN_ALGO_AUTO:
         case BNN_ALGO_UMMA:
             return launch_xnor_gemm_umma(A, lda, B, ldb, M, N, K, C, ldc_m, ldc_n, ep,
-                                         as_stream(stream));
+                                         as_stream(stream), e->residual);
         default:
             return set_error(BNN_EUNSUP, "algorithm %d not available", algo);
     }
+}
+
+int bnn_xnor_gemm(const uint64_t *A, int64_t lda, const uint64_t *B, int64_t ldb, int64_t M,
+                  int64_t N, int64_t K, int a_pad, int b_pad, float *C, int64_t ldc_m,
+                  int64_t ldc_n, int domain, const float *scale, const float *shift, int algo,
+                  bnn_stream_t stream) {
+    bnn_epilogue e{domain, scale, shift, nullptr, nullptr, nullptr, nullptr, nullptr};
+    return bnn_xnor_gemm_ex(A, lda, B, ldb, M, N, K, a_pad, b_pad, C, ldc_m, ldc_n, &e, algo,
+                            stream);
 }
 
 int bnn_pack_planes_f32(const float *x, int64_t R, int64_t K, int64_t ldx, int bits, int grid,
@@ -247,10 +269,10 @@ int bnn_conv_weights_reorder(const uint64_t *w_ref, int64_t F, int64_t C, int64_
     return launch_conv_weights_reorder(w_ref, F, C, kh, kw, w_dev, as_stream(stream));
 }
 
-int bnn_bconv2d(const uint64_t *x_words, int64_t B, int64_t C, int64_t H, int64_t W,
-                const uint64_t *w_dev, int64_t F, int64_t kh, int64_t kw, int64_t sh, int64_t sw,
-                int64_t ph, int64_t pw, float *y, int domain, const float *scale,
-                const float *shift, int algo, bnn_stream_t stream) {
+int bnn_bconv2d_ex(const uint64_t *x_words, int64_t B, int64_t C, int64_t H, int64_t W,
+                   const uint64_t *w_dev, int64_t F, int64_t kh, int64_t kw, int64_t sh,
+                   int64_t sw, int64_t ph, int64_t pw, float *y, const bnn_epilogue *e, int algo,
+                   bnn_stream_t stream) {
     // tensor.conv_output_hw (tensor.py:15-27)
     BNN_REQUIRE(B >= 1 && C >= 1 && H >= 1 && W >= 1 && F >= 1 && kh >= 1 && kw >= 1 &&
                     sh >= 1 && sw >= 1 && ph >= 0 && pw >= 0,
@@ -263,24 +285,38 @@ int bnn_bconv2d(const uint64_t *x_words, int64_t B, int64_t C, int64_t H, int64_
     const int64_t K = C * kh * kw;
     int rc = check_gemm_dims(F, B * oh * ow, K);
     if (rc) return rc;
+    BNN_REQUIRE(e != nullptr, BNN_EINVAL, "null epilogue");
     BNN_REQUIRE(x_words && w_dev && y, BNN_EINVAL, "null pointer");
+    const int domain = e->domain;
     BNN_REQUIRE(domain == BNN_POPCOUNT || domain == BNN_DOT, BNN_EINVAL, "bad domain %d", domain);
+    BNN_REQUIRE(!e->bn_mean || (e->bn_inv_std && e->bn_gamma && e->bn_beta), BNN_EINVAL,
+                "BatchNorm epilogue needs mean, inv_std, gamma and beta");
     BNN_REQUIRE(H * W * bnn_conv_channel_words(C) < (1ll << 31), BNN_EUNSUP, "image too large");
-    Epilogue ep{(int32_t)K, (int32_t)K, domain, scale, shift};  // all tails are 0
+    Epilogue ep{(int32_t)K, (int32_t)K, domain, nullptr, nullptr};  // all tails are 0
+    fill_epilogue(ep, e);
     switch (algo) {
         case BNN_ALGO_POPC:
             return launch_bconv2d_popc(x_words, B, C, H, W, w_dev, F, kh, kw, sh, sw, ph, pw, oh,
-                                       ow, y, ep, as_stream(stream));
+                                       ow, y, ep, as_stream(stream), e->residual);
         case BNN_ALGO_BMMA:
             return launch_bconv2d_bmma(x_words, B, C, H, W, w_dev, F, kh, kw, sh, sw, ph, pw, oh,
-                                       ow, y, ep, as_stream(stream));
+                                       ow, y, ep, as_stream(stream), e->residual);
         case BNN_ALGO_AUTO:
         case BNN_ALGO_UMMA:
             return launch_bconv2d_umma(x_words, B, C, H, W, w_dev, F, kh, kw, sh, sw, ph, pw, oh,
-                                       ow, y, ep, as_stream(stream));
+                                       ow, y, ep, as_stream(stream), e->residual);
         default:
             return set_error(BNN_EUNSUP, "algorithm %d not available", algo);
     }
+}
+
+int bnn_bconv2d(const uint64_t *x_words, int64_t B, int64_t C, int64_t H, int64_t W,
+                const uint64_t *w_dev, int64_t F, int64_t kh, int64_t kw, int64_t sh, int64_t sw,
+                int64_t ph, int64_t pw, float *y, int domain, const float *scale,
+                const float *shift, int algo, bnn_stream_t stream) {
+    bnn_epilogue e{domain, scale, shift, nullptr, nullptr, nullptr, nullptr, nullptr};
+    return bnn_bconv2d_ex(x_words, B, C, H, W, w_dev, F, kh, kw, sh, sw, ph, pw, y, &e, algo,
+                          stream);
 }
 
 }  // extern "C"

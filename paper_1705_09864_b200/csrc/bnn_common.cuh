@@ -30,13 +30,21 @@ struct Epilogue {
     // operand; out = (aA aB S + aA bB sumA[m] + bA aB sumB[n] + K bA bB) / (gA gB)
     int32_t a_alpha = 1, a_beta = 0, b_alpha = 1, b_beta = 0;
     float inv_gamma = 1.0f;
+    // optional fused inference BatchNorm in the reference's op order
+    // (layers.py:598-602): gamma * ((x - mean) * inv_std) + beta, each op rounded
+    const float *bn_mean = nullptr, *bn_inv = nullptr, *bn_gamma = nullptr, *bn_beta = nullptr;
+    __device__ __forceinline__ float bn(float f, int m) const {
+        if (!bn_mean) return f;
+        const float xh = __fmul_rn(__fsub_rn(f, __ldg(bn_mean + m)), __ldg(bn_inv + m));
+        return __fadd_rn(__fmul_rn(__ldg(bn_gamma + m), xh), __ldg(bn_beta + m));
+    }
     __device__ __forceinline__ float apply(int32_t x, int m) const {
         int32_t p = k_eff - x;
         int32_t v = domain == BNN_DOT ? 2 * p - k_logical : p;
         float f = (float)v;
-        if (scale) f = f * __ldg(scale + m);
-        if (shift) f = f + __ldg(shift + m);
-        return f;
+        if (scale) f = __fmul_rn(f, __ldg(scale + m));
+        if (shift) f = __fadd_rn(f, __ldg(shift + m));
+        return bn(f, m);
     }
 };
 

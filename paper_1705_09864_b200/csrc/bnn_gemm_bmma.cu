@@ -178,11 +178,11 @@ static int launch_bmma(const ALoad &a, const BLoad &b, const Store &st, const Ep
 
 int launch_xnor_gemm_bmma(const uint64_t *A, int64_t lda, const uint64_t *B, int64_t ldb,
                           int64_t M, int64_t N, int64_t K, float *C, int64_t ldc_m, int64_t ldc_n,
-                          const Epilogue &ep, cudaStream_t s) {
+                          const Epilogue &ep, cudaStream_t s, const float *res) {
     const int64_t kw32 = 2 * ceil_div(K, 64);
     DenseRows a{reinterpret_cast<const uint32_t *>(A), 2 * lda, M, kw32};
     DenseRows b{reinterpret_cast<const uint32_t *>(B), 2 * ldb, N, kw32};
-    GemmStore st{C, ldc_m, ldc_n, M, N};
+    GemmStore st{C, ldc_m, ldc_n, M, N, res};
     const bool vec4 = (lda % 2 == 0) && (ldb % 2 == 0) &&
                       ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) == 0;
     return vec4 ? launch_bmma<4>(a, b, st, ep, M, N, kw32, s)
@@ -192,7 +192,7 @@ int launch_xnor_gemm_bmma(const uint64_t *A, int64_t lda, const uint64_t *B, int
 int launch_bconv2d_bmma(const uint64_t *x, int64_t B, int64_t C, int64_t H, int64_t W,
                         const uint64_t *w, int64_t F, int64_t kh, int64_t kw, int64_t sh,
                         int64_t sw, int64_t ph, int64_t pw, int64_t oh, int64_t ow, float *y,
-                        const Epilogue &ep, cudaStream_t s) {
+                        const Epilogue &ep, cudaStream_t s, const float *res) {
     const int64_t cw64 = ceil_div(C, 64);
     const int64_t cs32 = 2 * cw64;
     const int64_t kw32 = kh * kw * cs32;
@@ -200,7 +200,7 @@ int launch_bconv2d_bmma(const uint64_t *x, int64_t B, int64_t C, int64_t H, int6
     DenseRows a{reinterpret_cast<const uint32_t *>(w), kw32, F, kw32};
     ConvRows b{reinterpret_cast<const uint32_t *>(x), npix, (int)H, (int)W, (int)cs32, (int)C,
                (int)kw, (int)sh, (int)sw, (int)ph, (int)pw, (int)oh, (int)ow, kw32};
-    ConvStore st{y, F, oh * ow, npix};
+    ConvStore st{y, F, oh * ow, npix, res};
     const bool vec4 = (cw64 % 2 == 0) &&
                       ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w)) & 15) == 0;
     return vec4 ? launch_bmma<4>(a, b, st, ep, F, npix, kw32, s)

@@ -486,6 +486,11 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes>::kThreads, 1)
                                     ep.k_logical * ep.a_beta * ep.b_beta;
             const float sc = (mok && ep.scale) ? __ldg(ep.scale + m) : 1.0f;
             const float sh = (mok && ep.shift) ? __ldg(ep.shift + m) : 0.0f;
+            const bool has_bn = ep.bn_mean != nullptr;
+            const float bm = (mok && has_bn) ? __ldg(ep.bn_mean + m) : 0.0f;
+            const float bi = (mok && has_bn) ? __ldg(ep.bn_inv + m) : 1.0f;
+            const float bg = (mok && has_bn) ? __ldg(ep.bn_gamma + m) : 1.0f;
+            const float bb = (mok && has_bn) ? __ldg(ep.bn_beta + m) : 0.0f;
             const int32_t *pb = s_popc_b + buf * BN;
             const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + buf * C::kAccCols;
 #pragma unroll 1
@@ -520,7 +525,10 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes>::kThreads, 1)
                         if (dot) val = 2 * val - ep.k_logical;
                         float x = magic ? __int_as_float(val + 0x4B400000) - 12582912.0f
                                         : (float)val;
-                        f[j] = affine ? __fadd_rn(__fmul_rn(x, sc), sh) : x;
+                        if (affine) x = __fadd_rn(__fmul_rn(x, sc), sh);
+                        if (has_bn)
+                            x = __fadd_rn(__fmul_rn(bg, __fmul_rn(__fsub_rn(x, bm), bi)), bb);
+                        f[j] = x;
                     }
                 }
                 if (ncontig) {
@@ -548,6 +556,11 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes>::kThreads, 1)
                                 asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
                                              : "=f"(t.x), "=f"(t.y), "=f"(t.z), "=f"(t.w)
                                              : "r"(src + rr * 4 * C::kStgPitch));
+                                if (store.res) {  // fused residual add
+                                    const float4 r = __ldg(reinterpret_cast<const float4 *>(store.res_of(dst)));
+                                    t.x = __fadd_rn(t.x, r.x); t.y = __fadd_rn(t.y, r.y);
+                                    t.z = __fadd_rn(t.z, r.z); t.w = __fadd_rn(t.w, r.w);
+                                }
                                 *reinterpret_cast<float4 *>(dst) = t;
                                 dst += step;
                             }
@@ -561,7 +574,13 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes>::kThreads, 1)
                                              : "=f"(t.x), "=f"(t.y), "=f"(t.z), "=f"(t.w)
                                              : "r"(src + rr * 4 * C::kStgPitch));
                                 if (v4) {
-                                    *reinterpret_cast<float4 *>(col + mr * ms) = t;
+                                    float *dst = col + mr * ms;
+                                    if (store.res) {
+                                        const float4 r = __ldg(reinterpret_cast<const float4 *>(store.res_of(dst)));
+                                        t.x = __fadd_rn(t.x, r.x); t.y = __fadd_rn(t.y, r.y);
+                                        t.z = __fadd_rn(t.z, r.z); t.w = __fadd_rn(t.w, r.w);
+                                    }
+                                    *reinterpret_cast<float4 *>(dst) = t;
                                 } else {
                                     const float tv[4] = {t.x, t.y, t.z, t.w};
 #pragma unroll
@@ -668,11 +687,11 @@ static int launch_umma(const ALoad &a, const BLoad &b, const Store &st, const Ep
 
 int launch_xnor_gemm_umma(const uint64_t *A, int64_t lda, const uint64_t *B, int64_t ldb,
                           int64_t M, int64_t N, int64_t K, float *C, int64_t ldc_m, int64_t ldc_n,
-                          const Epilogue &ep, cudaStream_t s) {
+                          const Epilogue &ep, cudaStream_t s, const float *res) {
     const int64_t kw32 = 2 * ceil_div(K, 64);
     DenseRows a{reinterpret_cast<const uint32_t *>(A), 2 * lda, M, kw32};
     DenseRows b{reinterpret_cast<const uint32_t *>(B), 2 * ldb, N, kw32};
-    GemmStore st{C, ldc_m, ldc_n, M, N};
+    GemmStore st{C, ldc_m, ldc_n, M, N, res};
     const bool vec4 = (lda % 2 == 0) && (ldb % 2 == 0) &&
                       ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) == 0;
     return vec4 ? launch_umma<4>(a, b, st, ep, M, N, kw32, s)
@@ -703,7 +722,7 @@ int launch_bitplane_gemm_umma(const uint64_t *A, int64_t lda, int64_t a_plane,
 int launch_bconv2d_umma(const uint64_t *x, int64_t B, int64_t C, int64_t H, int64_t W,
                         const uint64_t *w, int64_t F, int64_t kh, int64_t kw, int64_t sh,
                         int64_t sw, int64_t ph, int64_t pw, int64_t oh, int64_t ow, float *y,
-                        const Epilogue &ep, cudaStream_t s) {
+                        const Epilogue &ep, cudaStream_t s, const float *res) {
     const int64_t cw64 = ceil_div(C, 64);
     const int64_t cs32 = 2 * cw64;
     const int64_t kw32 = kh * kw * cs32;
@@ -711,7 +730,7 @@ int launch_bconv2d_umma(const uint64_t *x, int64_t B, int64_t C, int64_t H, int6
     DenseRows a{reinterpret_cast<const uint32_t *>(w), kw32, F, kw32};
     ConvRows b{reinterpret_cast<const uint32_t *>(x), npix, (int)H, (int)W, (int)cs32, (int)C,
                (int)kw, (int)sh, (int)sw, (int)ph, (int)pw, (int)oh, (int)ow, kw32};
-    ConvStore st{y, F, oh * ow, npix};
+    ConvStore st{y, F, oh * ow, npix, res};
     const bool vec4 = (cw64 % 2 == 0) &&
                       ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w)) & 15) == 0;
     return vec4 ? launch_umma<4>(a, b, st, ep, F, npix, kw32, s)

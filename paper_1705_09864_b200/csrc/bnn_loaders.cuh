@@ -117,11 +117,18 @@ struct ConvRows {
 };
 
 // ------------------------------------------------------------------ stores
+// Stores optionally add a residual tensor of the output's own layout (fused
+// "+ shortcut" of a residual block; f32 add, the same rounding as x + r).
 struct GemmStore {
     float *C;
     int64_t ldc_m, ldc_n, M, N;
+    const float *res = nullptr;
     __device__ bool ok(int64_t m, int64_t n) const { return m < M && n < N; }
-    __device__ void put(int64_t m, int64_t n, float v) const { C[m * ldc_m + n * ldc_n] = v; }
+    __device__ void put(int64_t m, int64_t n, float v) const {
+        const int64_t i = m * ldc_m + n * ldc_n;
+        C[i] = res ? __fadd_rn(v, __ldg(res + i)) : v;
+    }
+    __device__ const float *res_of(const float *p) const { return res + (p - C); }
     // column view for the staged epilogue: &C[m, n] = col_base(n) + m * m_stride()
     __device__ bool n_contiguous() const { return ldc_n == 1; }
     __device__ float *col_base(int64_t n) const { return C + n * ldc_n; }
@@ -155,11 +162,14 @@ struct GemmStore {
 struct ConvStore {  // y NCHW [B, F, oh*ow]; m = filter, n = b*ohw + pixel
     float *y;
     int64_t F, ohw, npix;
+    const float *res = nullptr;
     __device__ bool ok(int64_t m, int64_t n) const { return m < F && n < npix; }
     __device__ void put(int64_t m, int64_t n, float v) const {
         int64_t b = n / ohw, p = n - b * ohw;
-        y[(b * F + m) * ohw + p] = v;
+        const int64_t i = (b * F + m) * ohw + p;
+        y[i] = res ? __fadd_rn(v, __ldg(res + i)) : v;
     }
+    __device__ const float *res_of(const float *p) const { return res + (p - y); }
     __device__ bool n_contiguous() const { return true; }  // within an image
     __device__ float *col_base(int64_t n) const {
         int64_t b = n / ohw, p = n - b * ohw;

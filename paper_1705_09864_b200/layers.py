@@ -158,6 +158,28 @@ class _QLayer:
             raise ModeError("layer has no packed weights; pack() or load a converted model")
 
 
+def make_epilogue(domain: int, bn=None, residual: torch.Tensor | None = None,
+                  scale: torch.Tensor | None = None, shift: torch.Tensor | None = None):
+    """ctypes ``bnn_epilogue`` for the fused GEMM / conv epilogue.
+
+    ``bn`` is any object with ``device_params() -> (mean, inv_std, gamma, beta)``
+    CUDA f32 tensors (e.g. ``nets.BatchNorm``); the kernel applies it in the
+    reference's op order (layers.py:598-602), bit-identical to an unfused BN.
+    """
+    e = _lib.Epilogue()
+    e.domain = domain
+    e.scale, e.shift = _lib.ptr(scale), _lib.ptr(shift)
+    keep = [scale, shift, residual]
+    if bn is not None:
+        mean, inv, gamma, beta = bn.device_params()
+        e.bn_mean, e.bn_inv_std, e.bn_gamma, e.bn_beta = (_lib.ptr(t) for t in (mean, inv, gamma, beta))
+        keep += [mean, inv, gamma, beta]
+    if residual is not None:
+        e.residual = _lib.ptr(residual)
+    e._keep = keep  # keep tensors alive with the struct
+    return e
+
+
 class QConv2d(_QLayer):
     """Binary convolution -- layers.py:159-263 (popcount-domain outputs).
 
@@ -240,6 +262,33 @@ class QConv2d(_QLayer):
     def _strict_input(self) -> bool:
         return True
 
+    def forward_fused(self, x: torch.Tensor, bn=None, residual: torch.Tensor | None = None,
+                      out: torch.Tensor | None = None) -> torch.Tensor:
+        """``infer_packed`` conv with BatchNorm (+ residual add) fused into the epilogue."""
+        import ctypes
+        self._require_packed()
+        t = x.contiguous()
+        b, c, h, w = t.shape
+        kh, kw = self.kernel
+        oh, ow = self.output_hw(h, w)
+        flags = torch.zeros(1, dtype=torch.int32, device="cuda") if self.sync_checks \
+            else self._flags()
+        xw = pack_nchw(t, strict=self._strict_input(), flags=flags)
+        if out is None:
+            out = torch.empty((b, self.filters, oh, ow), dtype=torch.float32, device="cuda")
+        if residual is not None:
+            residual = residual.contiguous()
+            if tuple(residual.shape) != tuple(out.shape):
+                raise ValueError("residual must match the conv output shape")
+        e = make_epilogue(self.domain, bn, residual)
+        wd = self.device_weights()
+        algo = _lib.ALGOS[self.algo] if isinstance(self.algo, str) else self.algo
+        _lib.call("bnn_bconv2d_ex", _lib.ptr(xw), b, self.in_channels, h, w, _lib.ptr(wd),
+                  self.filters, kh, kw, self.stride[0], self.stride[1], self.pad[0], self.pad[1],
+                  _lib.ptr(out), ctypes.byref(e), algo, _lib.stream_ptr())
+        self._finish(flags)
+        return out
+
     def forward(self, x, mode=INFER_FLOAT):
         _check_mode(mode)
         t, was_np = to_device_f32(x)
@@ -300,6 +349,25 @@ class QDense(_QLayer):
 
     def _strict_input(self) -> bool:
         return True
+
+    def forward_fused(self, x: torch.Tensor, bn=None, out: torch.Tensor | None = None):
+        """``infer_packed`` dense layer with BatchNorm fused into the epilogue ([B, units])."""
+        import ctypes
+        self._require_packed()
+        t = x.contiguous()
+        flags = torch.zeros(1, dtype=torch.int32, device="cuda") if self.sync_checks \
+            else self._flags()
+        xw = pack_rows_device(t, 0, strict=self._strict_input(), flags=flags)
+        if out is None:
+            out = torch.empty((t.shape[0], self.units), dtype=torch.float32, device="cuda")
+        e = make_epilogue(self.domain, bn)
+        algo = _lib.ALGOS[self.algo] if isinstance(self.algo, str) else self.algo
+        a = self.packed.words
+        _lib.call("bnn_xnor_gemm_ex", _lib.ptr(a), a.stride(0), _lib.ptr(xw), xw.stride(0),
+                  self.units, t.shape[0], self.in_features, 0, 0, _lib.ptr(out), 1, out.stride(0),
+                  ctypes.byref(e), algo, _lib.stream_ptr())
+        self._finish(flags)
+        return out
 
     def forward_packed_rows(self, x_words: torch.Tensor, out=None, scale=None, shift=None):
         """[B, W] packed activations (tail 0) -> f32 [B, units] (no host sync)."""

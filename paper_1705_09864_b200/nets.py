@@ -98,6 +98,10 @@ class BatchNorm(_Lazy):
             self.var = np.ones(channels, np.float32)
         self.inv_std = (1.0 / np.sqrt(self.var + np.float32(BN_EPS))).astype(np.float32)
 
+    def device_params(self):
+        """(mean, inv_std, gamma, beta) CUDA tensors for the fused conv / GEMM epilogue."""
+        return self._dev("mean"), self._dev("inv_std"), self._dev("gamma"), self._dev("beta")
+
     def forward(self, x, mode=INFER_FLOAT):
         shape = (1, -1, 1, 1) if x.dim() == 4 else (1, -1)
         xhat = (x - self._dev("mean").view(shape)) * self._dev("inv_std").view(shape)
@@ -136,11 +140,25 @@ class Sequential:
     def __init__(self, layers):
         self.layers = list(layers)
 
+    fuse_bn = True  # infer_packed: a binary layer's following BatchNorm runs in its epilogue
+
     def forward(self, x, mode=INFER_FLOAT, capture=None):
-        for layer in self.layers:
+        i, n = 0, len(self.layers)
+        while i < n:
+            layer = self.layers[i]
+            nxt = self.layers[i + 1] if i + 1 < n else None
+            if (mode == INFER_PACKED and self.fuse_bn and isinstance(nxt, BatchNorm)
+                    and isinstance(layer, (QConvolution, QFullyConnected)) and layer.bits == 1):
+                x = layer.forward_fused(x, nxt)
+                if capture is not None:  # keep per-layer capture indices aligned
+                    capture.append(None)
+                    capture.append(x)
+                i += 2
+                continue
             x = layer.forward(x, mode)
             if capture is not None:
                 capture.append(x)
+            i += 1
         return x
 
     def binary_layers(self):
@@ -174,7 +192,13 @@ class BinaryBasicBlock:
     def binary_layers(self):
         return [self.conv1, self.conv2] + ([self.down] if self.down else [])
 
+    fused = True  # infer_packed: BN and the shortcut add run in the conv epilogues
+
     def forward(self, x, mode=INFER_FLOAT):
+        if mode == INFER_PACKED and self.fused:
+            h = self.conv1.forward_fused(x, self.bn1)
+            sc = x if self.down is None else self.down.forward_fused(x, self.bnd)
+            return self.conv2.forward_fused(h, self.bn2, residual=sc)
         h = self.bn1.forward(self.conv1.forward(x, mode))
         h = self.bn2.forward(self.conv2.forward(h, mode))
         sc = x if self.down is None else self.bnd.forward(self.down.forward(x, mode))

@@ -36,12 +36,19 @@ def test_lenet_c3_cross_mode_and_oracle(nets):
     net = nets.lenet_c3(seed=3)
     net.pack_for_inference()
     x = torch.rand((16, 1, 28, 28), generator=torch.Generator().manual_seed(0)).cuda()
+    # fused BN epilogues (default) are bit-identical to the unfused float path
+    yf, yp, cap_f, cap_p = _modes(net, x, bnn)
+    for i in range(len(net.layers)):
+        if cap_p[i] is not None:
+            assert torch.equal(cap_f[i], cap_p[i]), f"layer {i}"
+    assert torch.equal(yf, yp)
+    assert yp.shape == (16, 10)
+    net.fuse_bn = False
     yf, yp, cap_f, cap_p = _modes(net, x, bnn)
     for i, layer in enumerate(net.layers):
         if isinstance(layer, (bnn.QConvolution, bnn.QFullyConnected)):
             assert torch.equal(cap_f[i], cap_p[i]), f"layer {i}"
     assert torch.equal(yf, yp)
-    assert yp.shape == (16, 10)
     # teacher-forced: the binary conv's GPU input through the CPU oracle
     conv = net.layers[3]
     xin = cap_p[2].cpu().numpy()
@@ -68,6 +75,10 @@ def test_resnet18_c4_cross_mode(nets):
         if isinstance(layer, nets.BinaryBasicBlock):
             assert torch.equal(cap_f[i], cap_p[i]), f"block {i}"
     assert torch.equal(yf, yp)
+    for layer in net.layers:  # unfused epilogues agree as well
+        if isinstance(layer, nets.BinaryBasicBlock):
+            layer.fused = False
+    assert torch.equal(net.forward(x, bnn.INFER_PACKED), yf)
     ops = nets.binary_ops_per_image(net, (3, 224, 224))
     assert 3.3e9 < ops < 3.5e9  # 3.391e9 binary ops / image
 
