@@ -176,6 +176,14 @@ int bnn_xnor_gemm_ex(const uint64_t *A, int64_t lda, const uint64_t *B, int64_t 
                      int64_t N, int64_t K, int a_pad, int b_pad, float *C, int64_t ldc_m,
                      int64_t ldc_n, const bnn_epilogue *ep, int algo, bnn_stream_t stream);
 
+/* Float post-op of a full-precision stem conv (ResNet-18, configs[3]):
+ * y = maxpool_k/stride/pad(relu?(BN(x))) with BN in the reference's op order,
+ * bit-identical to the unfused sequence.  NCHW f32. */
+int bnn_bn_relu_maxpool_f32(const float *x, int64_t B, int64_t C, int64_t H, int64_t W,
+                            const float *mean, const float *inv_std, const float *gamma,
+                            const float *beta, int relu, int k, int stride, int pad, float *y,
+                            bnn_stream_t stream);
+
 /* Words per pixel of the packed NHWC activation layout: ceil(C / 64). */
 int64_t bnn_conv_channel_words(int64_t C);
 

@@ -85,6 +85,9 @@ def forward(net, x: np.ndarray, threads=None) -> np.ndarray:
             x = x.reshape(x.shape[0], -1)
         elif isinstance(layer, nets.GlobalAvgPool):
             x = x.mean(axis=(2, 3), dtype=np.float32)
+        elif isinstance(layer, nets.StemPost):
+            x = _maxpool(np.maximum(_bn(layer.bn, x), np.float32(0)), layer.pool.k,
+                         layer.pool.stride, layer.pool.pad)
         elif isinstance(layer, QConvolution):
             x = _qconv(layer, x, threads)
         elif isinstance(layer, QFullyConnected):

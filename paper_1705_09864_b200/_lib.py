@@ -47,6 +47,8 @@ SIGNATURES = {
     "bnn_bitplane_gemm": (_i32, [_vp, _i64, _i64, _i32, _vp, _i64, _i64, _i32, _i32, _i64, _i64,
                                  _i64, _vp, _i64, _i64, _vp]),
     "bnn_set_umma_variant": (_i32, [_i32]),
+    "bnn_bn_relu_maxpool_f32": (_i32, [_vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _i32, _i32,
+                                       _i32, _i32, _vp, _vp]),
     "bnn_xnor_gemm_ex": (_i32, [_vp, _i64, _vp, _i64, _i64, _i64, _i64, _i32, _i32, _vp, _i64,
                                 _i64, _vp, _i32, _vp]),
     "bnn_bconv2d_ex": (_i32, [_vp, _i64, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i64,

@@ -59,6 +59,9 @@ int launch_pack_planes(const float *, int64_t, int64_t, int64_t, int, int, uint6
 int launch_bitplane_gemm_umma(const uint64_t *, int64_t, int64_t, const uint64_t *, int64_t,
                               int64_t, int64_t, int64_t, int64_t, float *, int64_t, int64_t,
                               const Epilogue &, cudaStream_t);
+int launch_bn_relu_maxpool(const float *, int64_t, int64_t, int64_t, int64_t, const float *,
+                           const float *, const float *, const float *, int, int, int, int,
+                           float *, cudaStream_t);
 int launch_bconv2d_popc(const uint64_t *, int64_t, int64_t, int64_t, int64_t, const uint64_t *,
                         int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,
                         int64_t, float *, const Epilogue &, cudaStream_t, const float *);
@@ -258,6 +261,18 @@ int bnn_bitplane_gemm(const uint64_t *A, int64_t lda, int64_t a_plane_stride, in
     ep.inv_gamma = 1.0f / (float)(L * L);
     return launch_bitplane_gemm_umma(A, lda, a_plane_stride, B, ldb, b_plane_stride, M, N, K, C,
                                      ldc_m, ldc_n, ep, as_stream(stream));
+}
+
+int bnn_bn_relu_maxpool_f32(const float *x, int64_t B, int64_t C, int64_t H, int64_t W,
+                            const float *mean, const float *inv_std, const float *gamma,
+                            const float *beta, int relu, int k, int stride, int pad, float *y,
+                            bnn_stream_t stream) {
+    BNN_REQUIRE(B >= 0 && C >= 0 && H >= 1 && W >= 1 && k >= 1 && stride >= 1 && pad >= 0 &&
+                    pad < k && H + 2 * pad >= k && W + 2 * pad >= k,
+                BNN_EGEOM, "invalid pooling geometry");
+    BNN_REQUIRE(x && y && mean && inv_std && gamma && beta, BNN_EINVAL, "null pointer");
+    return launch_bn_relu_maxpool(x, B, C, H, W, mean, inv_std, gamma, beta, relu, k, stride, pad,
+                                  y, as_stream(stream));
 }
 
 int64_t bnn_conv_channel_words(int64_t C) { return C > 0 ? ceil_div(C, 64) : 0; }

@@ -347,6 +347,40 @@ __global__ void pack_planes_kernel(const float *__restrict__ x, int64_t R, int64
     flush_flags(f, flags);
 }
 
+// ---------------------------------------------------------------- BN + ReLU + maxpool
+// Fused float post-op of a full-precision stem (ResNet-18 configs[3]):
+// y = maxpool_kxk/s/p(relu(gamma * ((x - mean) * inv_std) + beta)), NCHW f32.
+// Every op is the reference's float32 op (layers.py:598-602, each rounded, no
+// FMA), so the result is bit-identical to the unfused torch / NumPy sequence.
+// One thread per output element; the k*k window reads hit L1/L2.
+__global__ void bn_relu_maxpool_kernel(const float *__restrict__ x, int64_t B, int64_t C,
+                                       int64_t H, int64_t W, const float *__restrict__ mean,
+                                       const float *__restrict__ inv, const float *__restrict__ gamma,
+                                       const float *__restrict__ beta, int relu, int k, int st,
+                                       int pd, int64_t OH, int64_t OW, float *__restrict__ y) {
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t total = B * C * OH * OW;
+    if (idx >= total) return;
+    const int64_t ox = idx % OW, oy = (idx / OW) % OH, c = (idx / (OW * OH)) % C,
+                  b = idx / (OW * OH * C);
+    const float m = __ldg(mean + c), iv = __ldg(inv + c), g = __ldg(gamma + c), bt = __ldg(beta + c);
+    const float *src = x + (b * C + c) * H * W;
+    float best = -INFINITY;
+    for (int i = 0; i < k; ++i) {
+        const int64_t iy = oy * st - pd + i;
+        if (iy < 0 || iy >= H) continue;
+        for (int j = 0; j < k; ++j) {
+            const int64_t ix = ox * st - pd + j;
+            if (ix < 0 || ix >= W) continue;
+            float v = __ldg(src + iy * W + ix);
+            v = __fadd_rn(__fmul_rn(g, __fmul_rn(__fsub_rn(v, m), iv)), bt);
+            if (relu) v = fmaxf(v, 0.0f);
+            best = fmaxf(best, v);
+        }
+    }
+    y[idx] = best;
+}
+
 // ================================================================ launchers
 int launch_binarize(const float *x, int64_t n, float *out, int32_t *flags, cudaStream_t s) {
     if (n == 0) return BNN_OK;
@@ -423,6 +457,18 @@ int launch_pack_planes(const float *x, int64_t R, int64_t K, int64_t ldx, int bi
     else
         return set_error(BNN_EUNSUP, "bit-plane packing supports bits == 2");
     return check_launch("pack_planes_kernel");
+}
+
+int launch_bn_relu_maxpool(const float *x, int64_t B, int64_t C, int64_t H, int64_t W,
+                           const float *mean, const float *inv, const float *gamma,
+                           const float *beta, int relu, int k, int st, int pd, float *y,
+                           cudaStream_t s) {
+    const int64_t OH = (H + 2 * pd - k) / st + 1, OW = (W + 2 * pd - k) / st + 1;
+    const int64_t total = B * C * OH * OW;
+    if (total == 0) return BNN_OK;
+    bn_relu_maxpool_kernel<<<(unsigned)ceil_div(total, 256), 256, 0, s>>>(
+        x, B, C, H, W, mean, inv, gamma, beta, relu, k, st, pd, OH, OW, y);
+    return check_launch("bn_relu_maxpool_kernel");
 }
 
 int launch_words_transpose(const uint64_t *in, int64_t rows, int64_t cols, int64_t ldi,

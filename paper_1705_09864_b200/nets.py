@@ -61,6 +61,7 @@ class Conv2d(_Lazy):
     def forward(self, x, mode=INFER_FLOAT):
         prev = torch.backends.cudnn.allow_tf32
         torch.backends.cudnn.allow_tf32 = False
+        torch.backends.cudnn.benchmark = True  # fastest exact-fp32 algorithm for the shape
         try:
             return F.conv2d(x, self._dev("weight"), self._dev("bias"), stride=self.stride,
                             padding=self.pad)
@@ -134,6 +135,29 @@ class Flatten:
 class GlobalAvgPool:
     def forward(self, x, mode=INFER_FLOAT):
         return x.mean(dim=(2, 3))
+
+
+class StemPost:
+    """BatchNorm -> ReLU -> MaxPool of a full-precision stem as one kernel in
+    ``infer_packed`` mode (bnn_bn_relu_maxpool_f32, bit-identical); the three
+    torch ops in ``infer_float`` mode."""
+
+    def __init__(self, channels, rng, k=3, stride=2, pad=1):
+        self.bn, self.relu, self.pool = BatchNorm(channels, rng), ReLU(), MaxPool2d(k, stride, pad)
+
+    def forward(self, x, mode=INFER_FLOAT):
+        if mode != INFER_PACKED:
+            return self.pool.forward(self.relu.forward(self.bn.forward(x)))
+        x = x.contiguous()
+        b, c, h, w = x.shape
+        p = self.pool
+        oh, ow = (h + 2 * p.pad - p.k) // p.stride + 1, (w + 2 * p.pad - p.k) // p.stride + 1
+        y = torch.empty((b, c, oh, ow), dtype=torch.float32, device=x.device)
+        mean, inv, gamma, beta = self.bn.device_params()
+        _lib.call("bnn_bn_relu_maxpool_f32", _lib.ptr(x), b, c, h, w, _lib.ptr(mean),
+                  _lib.ptr(inv), _lib.ptr(gamma), _lib.ptr(beta), 1, p.k, p.stride, p.pad,
+                  _lib.ptr(y), _lib.stream_ptr())
+        return y
 
 
 class Sequential:
@@ -220,8 +244,7 @@ def lenet_c3(seed: int = 0) -> Sequential:
 def resnet18_c4(seed: int = 0, num_classes: int = 1000) -> Sequential:
     """BASELINE configs[3]: binary ResNet-18 (stem and classifier full precision)."""
     rng = np.random.default_rng(seed)
-    layers = [Conv2d(3, 64, 7, stride=2, pad=3, bias=False, rng=rng), BatchNorm(64, rng), ReLU(),
-              MaxPool2d(3, 2, 1)]
+    layers = [Conv2d(3, 64, 7, stride=2, pad=3, bias=False, rng=rng), StemPost(64, rng, 3, 2, 1)]
     cin = 64
     for cout, stride in ((64, 1), (128, 2), (256, 2), (512, 2)):
         layers.append(BinaryBasicBlock(cin, cout, stride, rng))
@@ -245,9 +268,10 @@ def binary_ops_per_image(net: Sequential, chw) -> int:
             h = (h + 2 * layer.pad - layer.k) // layer.stride + 1
             w = (w + 2 * layer.pad - layer.k) // layer.stride + 1
             c = layer.cout
-        elif isinstance(layer, MaxPool2d):
-            h = (h + 2 * layer.pad - layer.k) // layer.stride + 1
-            w = (w + 2 * layer.pad - layer.k) // layer.stride + 1
+        elif isinstance(layer, (MaxPool2d, StemPost)):
+            pl = layer if isinstance(layer, MaxPool2d) else layer.pool
+            h = (h + 2 * pl.pad - pl.k) // pl.stride + 1
+            w = (w + 2 * pl.pad - pl.k) // pl.stride + 1
         elif isinstance(layer, QConvolution):
             c, h, w, ops = conv(layer, c, h, w)
             total += ops
