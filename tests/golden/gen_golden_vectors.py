@@ -165,10 +165,30 @@ def gen_configs(out):
     (out / "configs.json").write_text(json.dumps(res, indent=1))
 
 
+def gen_bmx(out):
+    """Golden .bmx files written by the reference's own modelio (test_modelio.py:37-45)."""
+    sys.path.insert(0, os.path.join(os.path.dirname(REF_SRC), "tests", "data"))
+    import gen_golden  # the reference's fixture builder, imported (not copied)
+    from bitnn import modelio
+    net = gen_golden.build_golden_net()
+    fp, pp = out / "golden_float.bmx", out / "golden_packed.bmx"
+    modelio.save_model(net, fp)
+    modelio.convert(fp, pp)
+    x = gen_golden.probe_input()
+    probs_f = modelio.load_model(fp).forward(x, layers.INFER_FLOAT)
+    probs_p = modelio.load_model(pp).forward(x, layers.INFER_PACKED)
+    meta = {"float_sha256": hashlib.sha256(fp.read_bytes()).hexdigest(),
+            "packed_sha256": hashlib.sha256(pp.read_bytes()).hexdigest(),
+            "float_size": fp.stat().st_size, "packed_size": pp.stat().st_size,
+            "probe_seed": gen_golden.SEED + 1, "probs_float": probs_f.tolist(),
+            "probs_packed": probs_p.tolist()}
+    (out / "golden_bmx.json").write_text(json.dumps(meta, indent=1))
+
+
 def main():
     out = HERE
     for fn in (gen_pack_cases, gen_gemm40, gen_conv, gen_layers, gen_qmath, gen_sweep504,
-               gen_configs):
+               gen_configs, gen_bmx):
         t0 = time.time()
         fn(out)
         print(f"{fn.__name__}: {time.time() - t0:.1f}s", flush=True)
