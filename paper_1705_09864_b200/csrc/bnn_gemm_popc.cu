@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(WARPS_M *WARPS_N * 32)
 
     const int64_t ktiles = ceil_div(kw32, kBKWords);
     auto issue = [&](int64_t kt, int stage) {
-        const int64_t w = kt * kBKWords + lp * kVec;
+        const int w = (int)(kt * kBKWords + lp * kVec);
         const uint32_t a_base = smem_u32(sA + stage * kTileBytesA);
         const uint32_t b_base = smem_u32(sB + stage * kTileBytesB);
 #pragma unroll

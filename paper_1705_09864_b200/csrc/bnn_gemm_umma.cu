@@ -243,7 +243,7 @@ struct TileMap {
 template <int BN, bool kATmem, int kVec, class ALoad, class BLoad, class Store, int kPlanes = 1>
 __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes>::kThreads, 1)
     xnor_umma_kernel(ALoad aload, BLoad bload, Store store, Epilogue ep, int64_t kw32,
-                     TileMap tmap, uint64_t *trace_buf) {
+                     TileMap tmap, uint64_t *trace_buf, int dbg) {
     auto trace = [&](int slot) { trace_at(trace_buf, slot); };
     using C = Cfg<BN, kATmem, kPlanes>;
     constexpr int ES = C::ES;
@@ -300,7 +300,8 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes>::kThreads, 1)
         constexpr uint32_t kRingSlot = C::kProducerWarps * 32 * 16 * kPlanes;
         // fetch iterator (runs PD-1 stages ahead, across tile boundaries)
         int f_tile = blockIdx.x;
-        int64_t f_kt = 0;
+        uint32_t f_kt = 0;
+        const uint32_t kt32 = (uint32_t)ktiles;
         typename ALoad::Cursor fa{};
         typename BLoad::Cursor fb{};
         auto set_cursor = [&](int t) {
@@ -311,21 +312,21 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes>::kThreads, 1)
             else fb = bload.row((int64_t)tn * BN + row);
         };
         set_cursor(f_tile);
-        int64_t f_count = 0;  // stages fetched so far
+        uint32_t f_count = 0;  // stages fetched so far
         auto fetch_next = [&]() {
             if (f_tile < tmap.ntiles && active) {
-                const uint32_t dst = ring + (uint32_t)(f_count % PD) * kRingSlot;
+                const uint32_t dst = ring + (f_count & (PD - 1)) * kRingSlot;
 #pragma unroll
                 for (int pl = 0; pl < kPlanes; ++pl)
 #pragma unroll
                     for (int p = 0; p < kWordsPerStage / kVec; ++p) {
-                        const int64_t w = f_kt * kWordsPerStage + p * kVec;
+                        const int w = (int)(f_kt * kWordsPerStage + p * kVec);
                         const uint32_t d = dst + pl * 16 + p * kVec * 4;
                         if (is_a) aload.template load<kVec>(fa, w, d, pl);
                         else bload.template load<kVec>(fb, w, d, pl);
                     }
                 ++f_count;
-                if (++f_kt == ktiles) {
+                if (++f_kt == kt32) {
                     f_kt = 0;
                     f_tile += gridDim.x;
                     set_cursor(f_tile);
@@ -336,17 +337,17 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes>::kThreads, 1)
 #pragma unroll 1
         for (int p = 0; p < PD - 1; ++p) fetch_next();
 
-        int64_t gk = 0;  // global stage counter (ring / phase bookkeeping)
+        uint32_t gk = 0;  // global stage counter (ring / phase bookkeeping)
         int it = 0;
 #pragma unroll 1
         for (int tile = blockIdx.x; tile < tmap.ntiles; tile += gridDim.x, ++it) {
             int32_t my_popc = 0;
 #pragma unroll 1
-            for (int64_t kt = 0; kt < ktiles; ++kt, ++gk) {
+            for (uint32_t kt = 0; kt < kt32; ++kt, ++gk) {
                 fetch_next();
                 cp_async_wait<PD - 1>();
                 uint32_t wv[4], wv1[4] = {0, 0, 0, 0};
-                const uint32_t slot = ring + (uint32_t)(gk % PD) * kRingSlot;
+                const uint32_t slot = ring + (gk & (PD - 1)) * kRingSlot;
                 asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n"
                              : "=r"(wv[0]), "=r"(wv[1]), "=r"(wv[2]), "=r"(wv[3])
                              : "r"(slot));
@@ -366,7 +367,7 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes>::kThreads, 1)
                     }
                 };
                 const int s = (int)(gk % ES);
-                if (gk >= ES) mbar_wait(bar_empty + 8 * s, (uint32_t)((gk / ES) - 1) & 1u);
+                if (gk >= ES) mbar_wait(bar_empty + 8 * s, ((gk / ES) - 1) & 1u);
                 if (!active) {
                 } else if (is_a) {
                     if constexpr (kATmem) {
@@ -377,7 +378,7 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes>::kThreads, 1)
                         for (int q = 0; q < 4; ++q) {
                             uint32_t r[8];
                             expand(q, true, r);
-                            tmem_st8(taddr + q * 8, r);
+                            if (!(dbg & 4)) tmem_st8(taddr + q * 8, r);
                         }
                         asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
                         fence_before();
@@ -398,7 +399,8 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes>::kThreads, 1)
                     for (int q = 0; q < 4; ++q) {
                         uint32_t r[8];
                         expand(q, false, r);
-                        store_row32(r, row_base, row, q);
+                        if (!(dbg & 1)) store_row32(r, row_base, row, q);
+                        else if (r[0] == 0x12345678u && r[7] == 0x9abcdef0u) store_row32(r, row_base, row, q);
                     }
                     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                 }
@@ -417,7 +419,8 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes>::kThreads, 1)
     } else if (warp == C::kMmaWarp) {
         // ================================================================ MMA issuer
         if (lane == 0) {
-            int64_t gk = 0;
+            uint32_t gk = 0;
+            const uint32_t kt32 = (uint32_t)ktiles;
             int it = 0;
 #pragma unroll 1
             for (int tile = blockIdx.x; tile < tmap.ntiles; tile += gridDim.x, ++it) {
@@ -426,14 +429,15 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes>::kThreads, 1)
                 fence_after();
                 const uint32_t d = tmem + buf * C::kAccCols;
 #pragma unroll 1
-                for (int64_t kt = 0; kt < ktiles; ++kt, ++gk) {
+                for (uint32_t kt = 0; kt < kt32; ++kt, ++gk) {
                     const int s = (int)(gk % ES);
-                    mbar_wait(bar_full + 8 * s, (uint32_t)(gk / ES) & 1u);
+                    mbar_wait(bar_full + 8 * s, (gk / ES) & 1u);
                     if (gk == 0) trace(2);
                     fence_after();
                     const uint32_t b_addr = s_exp + s * C::kStageBytes + C::kStageA;
 #pragma unroll
                     for (int kk = 0; kk < kRowBytes / 32; ++kk) {
+                        if (dbg & 2) break;
                         const uint32_t acc = (kt | kk) != 0 ? 1u : 0u;
                         if constexpr (kATmem)
                             mma_ts<C::kIdesc>(d, tmem + C::kAStageCol + s * 32 + kk * 8,
@@ -618,6 +622,14 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes>::kThreads, 1)
 }  // namespace umma
 
 static uint64_t *g_trace_buf = nullptr;  // debug timeline (bnn_umma_trace)
+static int g_dbg = -1;                    // debug: BNN_UMMA_DEBUG bit flags (wrong results)
+static int umma_dbg() {
+    if (g_dbg < 0) {
+        const char *e = getenv("BNN_UMMA_DEBUG");
+        g_dbg = e ? atoi(e) : 0;
+    }
+    return g_dbg;
+}
 
 static int sm_count() {
     static int n = 0;
@@ -643,7 +655,8 @@ static int launch_umma_cfg(const ALoad &a, const BLoad &b, const Store &st, cons
     if (ntiles > (1ll << 30)) return set_error(BNN_EUNSUP, "too many tiles");
     umma::TileMap tmap{(int)tiles_m, (int)ntiles};
     const int grid = (int)(ntiles < sm_count() ? ntiles : sm_count());
-    kern<<<grid, C::kThreads, C::kSmemBytes, s>>>(a, b, st, ep, kw32, tmap, g_trace_buf);
+    kern<<<grid, C::kThreads, C::kSmemBytes, s>>>(a, b, st, ep, kw32, tmap, g_trace_buf,
+                                                  umma_dbg());
     return check_launch("xnor_umma_kernel");
 }
 

@@ -49,9 +49,9 @@ struct DenseRows {
     __device__ Cursor row(int64_t r) const { return {base + r * ld32, r < rows}; }
     // load kVec words at word w of this row into smem address dst
     template <int kVec>
-    __device__ void load(Cursor &c, int64_t w, uint32_t dst, int plane = 0) const {
-        int64_t left = kw32 - w;
-        int bytes = (!c.ok || left <= 0) ? 0 : (int)(left >= kVec ? kVec * 4 : left * 4);
+    __device__ void load(Cursor &c, int w, uint32_t dst, int plane = 0) const {
+        const int left = (int)kw32 - w;  // K < 2^24 -> word counts fit in 32 bits
+        int bytes = (!c.ok || left <= 0) ? 0 : (left >= kVec ? kVec * 4 : left * 4);
         const uint32_t *src = bytes ? c.p + plane * plane32 + w : base;
         cp_async<kVec * 4>(dst, src, bytes);
     }
@@ -85,7 +85,7 @@ struct ConvRows {
         return c;
     }
     template <int kVec>
-    __device__ void load(Cursor &c, int64_t w, uint32_t dst, int plane = 0) const {
+    __device__ void load(Cursor &c, int w, uint32_t dst, int plane = 0) const {
         if (!c.ok || w >= kw32) {
             cp_async<kVec * 4>(dst, x, 0);
             return;
@@ -95,7 +95,7 @@ struct ConvRows {
             c.tap_w0 += cs32;
             if (++c.j == kw) c.j = 0, ++c.i;
         }
-        const int cw = (int)(w - c.tap_w0);
+        const int cw = (int)(w - c.tap_w0);  // (tap_w0 is int64 for ld math)
         int iy = c.iy0 + c.i, ix = c.ix0 + c.j;
         if (iy >= 0 && iy < H && ix >= 0 && ix < W) {
             cp_async<kVec * 4>(dst, c.img + ((int64_t)iy * W + ix) * cs32 + cw, kVec * 4);
