@@ -12,7 +12,7 @@ import os
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libbnn_b200.so")
+LIB_PATH = os.environ.get("BNN_LIB_PATH") or os.path.join(_PKG, "libbnn_b200.so")  # override: dev experiments
 
 # enum values mirrored from include/bnn_b200.h
 OK, EINVAL, EDIMS, EKEXACT, EPAD, EALIGN, EGEOM, EUNSUP, ECUDA = 0, -1, -2, -3, -4, -5, -6, -7, 1

@@ -36,11 +36,55 @@
 //                  buf (double-buffered, so it overlaps the next tile's MMA),
 //                  decode, transpose through SMEM, coalesced 128-byte stores;
 //                  arrive tmem_empty[buf].
+#include <cuda.h>
+
 #include <cstdlib>
+#include <type_traits>
 
 #include "bnn_loaders.cuh"
 
 namespace bnn {
+
+// Dense packed operand [rows, ld32] u32 fetched by the tensor-memory
+// accelerator: a 2-D tensor map over the kw32 valid words of every row; one
+// cp.async.bulk.tensor per operand per superstage writes the rows' packed
+// words (row-major, 16 B per stage per row, SWIZZLE_32B when a superstage is
+// two stages) and signals an mbarrier with complete_tx.  Rows past the end and
+// words past kw32 are zero-filled by the TMA unit, which the and-popcount
+// decode ignores (a zero word matches a zero word).
+struct TmaRows {
+    static constexpr bool kTma = true;
+    CUtensorMap map;
+    const uint32_t *base;
+    int64_t ld32, rows, kw32;
+    // (the cp.async loader interface, unused on the TMA path)
+    struct Cursor {};
+    __device__ Cursor row(int64_t) const { return {}; }
+    template <int kVec>
+    __device__ void load(Cursor &, int, uint32_t, int = 0) const {}
+};
+
+// Implicit-im2col activations for the TMA path: an im2col tensor map over
+// the packed NHWC words {cs32, W, H, B}; one load per superstage fetches, for
+// BN consecutive output pixels, the 32 bytes of channel words of one filter
+// tap (cp.async.bulk.tensor.4d.im2col with the tap as the im2col offset).
+// Out-of-image taps come back zero-filled; the expander thread of that pixel
+// row knows its window corner and the superstage's tap, and substitutes the
+// all-ones word -- the reference's "+1" padding (tensor.py:73-74 +
+// bitpack.py:39).  Requires cs32 % 8 == 0 (C a multiple of 256), so a
+// superstage never straddles two taps and no channel tail exists.
+struct TmaConv {
+    static constexpr bool kTma = true;
+    CUtensorMap map;
+    const uint32_t *x;
+    int64_t npix;
+    int H, W, cs32, kw, sh, sw, ph, pw, oh, ow;
+    struct Cursor {};
+    __device__ Cursor row(int64_t) const { return {}; }
+    template <int kVec>
+    __device__ void load(Cursor &, int, uint32_t, int = 0) const {}
+};
+
 namespace umma {
 
 constexpr int BM = 128;
@@ -58,38 +102,52 @@ __device__ __forceinline__ void trace_at(uint64_t *buf, int slot) {
 }
 constexpr int kWordsPerStage = 4;  // u32 words of K per row per stage
 constexpr int kRowBytes = 128;     // expanded bytes per row per stage
-constexpr int PD = 4;              // packed prefetch depth (per producer thread)
 
-template <int BN, bool kATmem, int kPlanes = 1>
+template <int BN, bool kATmem, int kPlanes = 1, bool kTma = false>
 struct Cfg {
     static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
     static constexpr int kProducers = BM + BN;                 // one thread per operand row
     static constexpr int kProducerWarps = (kProducers + 31) / 32;
-    static constexpr int kMmaWarp = kProducerWarps;
+    static constexpr int kTmaWarp = kProducerWarps;  // one elected lane issues the TMA loads
+    static constexpr int kMmaWarp = kTmaWarp + 1;
     static constexpr int kEpiWarp0 = kMmaWarp + 1;
     static constexpr int kEpiWarps = 8;                        // 2 per TMEM lane quadrant
     static constexpr int kThreads = (kEpiWarp0 + kEpiWarps) * 32;
+    // K is consumed in 128-bit stages grouped into superstages of kSub stages:
+    // every barrier round trip (expanded-buffer wait, proxy fence, full arrival,
+    // MMA commit) is paid once per superstage
+    static constexpr int kSub = kATmem ? 2 : 1;
+    static constexpr int PD = (kATmem && kPlanes == 1) ? 8 : 4;  // per-thread packed ring (stages)
+    static_assert((PD & (PD - 1)) == 0 && PD >= 2 * kSub, "packed ring depth");
     static constexpr int kStageA = kATmem ? 0 : BM * kRowBytes;
     static constexpr int kStageB = BN * kRowBytes;
     static constexpr int kStageBytes = kStageA + kStageB;
-    static constexpr int ES = kATmem ? 4 : 3;  // expanded stages
-    // TMEM: 2 accumulator buffers of BN columns (+ ES A stages of 32 columns)
+    static constexpr int kSuperBytes = kSub * kStageBytes;
+    static constexpr int ES = kATmem ? 2 : 3;  // expanded superstage buffers
+    // TMEM: 2 accumulator buffers of BN columns (+ ES x kSub A stages of 32 columns)
     static constexpr int kAccCols = BN;
     static constexpr int kAStageCol = 2 * BN;
     static constexpr int kTmemCols = 512;
-    static_assert(2 * BN + (kATmem ? ES * 32 : 0) <= 512, "TMEM budget");
+    static_assert(2 * BN + (kATmem ? ES * kSub * 32 : 0) <= 512, "TMEM budget");
     // shared memory carve-up (offsets from the 1024-aligned base)
     // epilogue staging: per warp 32 rows x 32 f32, row pitch 144 B (16 B of
     // padding keeps both the row writes and the transposed reads conflict-free)
     static constexpr int kStgPitch = 144;
     static constexpr int kStgBytes = 32 * kStgPitch;
     static constexpr int off_exp = 0;
-    static constexpr int off_pk = ES * kStageBytes;
-    static constexpr int off_popc_a = off_pk + PD * kProducerWarps * 32 * 16 * kPlanes;
+    static constexpr int off_pk = ES * kSuperBytes;
+    // packed staging: per-thread cp.async rings (PD stages x 16 B per row), or
+    // with TMA kTmaSlots superstage slots of [A rows | B rows] x kSub x 16 B
+    static constexpr int kTmaSlots = 4;
+    static constexpr int kTmaA = BM * kSub * 16, kTmaB = BN * kSub * 16;
+    static constexpr int kTmaSlotBytes = ((kTmaA + kTmaB + 1023) / 1024) * 1024;
+    static constexpr int kPkBytes = kTma ? kTmaSlots * kTmaSlotBytes
+                                         : PD * kProducerWarps * 32 * 16 * kPlanes;
+    static constexpr int off_popc_a = off_pk + kPkBytes;
     static constexpr int off_popc_b = off_popc_a + 2 * BM * 4;
     static constexpr int off_epi = off_popc_b + 2 * BN * 4;
     static constexpr int off_bars = off_epi + kEpiWarps * kStgBytes;
-    static constexpr int kNumBars = 2 * ES + 6;
+    static constexpr int kNumBars = 2 * ES + 6 + 2 * kTmaSlots;
     static constexpr int off_tmem = off_bars + kNumBars * 8;
     static constexpr int kSmemBytes = off_tmem + 16 + 1024;
     static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
@@ -103,6 +161,28 @@ __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, int c0, int c1,
+                                            uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3}], [%4];\n" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_im2col_4d(uint32_t dst, const CUtensorMap *map, int c,
+                                                   int w, int h, int n, uint16_t off_w,
+                                                   uint16_t off_h, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3, %4, %5}], [%6], {%7, %8};\n" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c), "r"(w), "r"(h), "r"(n), "r"(bar),
+        "h"(off_w), "h"(off_h)
+        : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
     uint32_t done = 0;
     do {
@@ -112,6 +192,20 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
             "selp.u32 %0, 1, 0, p;\n}\n"
             : "=r"(done)
             : "r"(bar), "r"(phase)
+            : "memory");
+    } while (!done);
+}
+// long waits (epilogue): the thread sleeps in try_wait until the phase completes
+// instead of spinning on the issue slots the producers need
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t phase) {
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{\n.reg .pred p;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+            "selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(bar), "r"(phase), "r"(1000000u)
             : "memory");
     } while (!done);
 }
@@ -240,12 +334,27 @@ struct TileMap {
     }
 };
 
+template <class L>
+struct is_tma { static constexpr bool value = false; };
+template <>
+struct is_tma<TmaRows> { static constexpr bool value = true; };
+template <>
+struct is_tma<TmaConv> { static constexpr bool value = true; };
+
 template <int BN, bool kATmem, int kVec, class ALoad, class BLoad, class Store, int kPlanes = 1>
-__global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes>::kThreads, 1)
-    xnor_umma_kernel(ALoad aload, BLoad bload, Store store, Epilogue ep, int64_t kw32,
-                     TileMap tmap, uint64_t *trace_buf, int dbg) {
+__global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value>::kThreads, 1)
+    xnor_umma_kernel(const __grid_constant__ ALoad aload, const __grid_constant__ BLoad bload,
+                     Store store, Epilogue ep, int64_t kw32, TileMap tmap, uint64_t *trace_buf,
+                     int dbg) {
     auto trace = [&](int slot) { trace_at(trace_buf, slot); };
-    using C = Cfg<BN, kATmem, kPlanes>;
+    // per-superstage pipeline timeline of CTA 0 (debug: dbg bit 16; u64 [4096 + ev * 256 + g])
+    const bool stage_trace = trace_buf != nullptr && (dbg & 16) && blockIdx.x == 0;
+    auto tr = [&](int ev, uint32_t g) {
+        if (stage_trace && g < 256) trace_buf[4096 + ev * 256 + g] = clock64();
+    };
+    constexpr bool kTma = is_tma<ALoad>::value;
+    static_assert(kTma == is_tma<BLoad>::value && (!kTma || kPlanes == 1), "TMA: both operands");
+    using C = Cfg<BN, kATmem, kPlanes, kTma>;
     constexpr int ES = C::ES;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t sbase_raw = smem_u32(smem_raw);
@@ -261,6 +370,8 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes>::kThreads, 1)
     const uint32_t bar_tfull = bar_empty + ES * 8;      // [2] MMA -> epilogue
     const uint32_t bar_tempty = bar_tfull + 2 * 8;      // [2] epilogue -> MMA / producers
     const uint32_t bar_pfull = bar_tempty + 2 * 8;      // [2] producers' popcounts ready
+    const uint32_t bar_ld = bar_pfull + 2 * 8;          // [kTmaSlots] TMA bytes landed
+    const uint32_t bar_free = bar_ld + C::kTmaSlots * 8; // [kTmaSlots] expanders read the slot
     uint32_t *s_tmem = reinterpret_cast<uint32_t *>(sgen + C::off_tmem);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -276,6 +387,10 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes>::kThreads, 1)
             mbar_init(bar_tfull + 8 * b, 1);
             mbar_init(bar_tempty + 8 * b, C::kEpiWarps);
             mbar_init(bar_pfull + 8 * b, C::kProducerWarps);
+        }
+        for (int r = 0; r < C::kTmaSlots; ++r) {
+            mbar_init(bar_ld + 8 * r, 1);
+            mbar_init(bar_free + 8 * r, C::kProducerWarps);
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
@@ -298,7 +413,7 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes>::kThreads, 1)
         const int row = is_a ? tid : tid - BM;
         const uint32_t ring = s_pk + tid * 16 * kPlanes;  // slot-major private ring
         constexpr uint32_t kRingSlot = C::kProducerWarps * 32 * 16 * kPlanes;
-        // fetch iterator (runs PD-1 stages ahead, across tile boundaries)
+        // fetch iterator (runs PD - kSub stages ahead, across tile boundaries)
         int f_tile = blockIdx.x;
         uint32_t f_kt = 0;
         const uint32_t kt32 = (uint32_t)ktiles;
@@ -315,7 +430,7 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes>::kThreads, 1)
         uint32_t f_count = 0;  // stages fetched so far
         auto fetch_next = [&]() {
             if (f_tile < tmap.ntiles && active) {
-                const uint32_t dst = ring + (f_count & (PD - 1)) * kRingSlot;
+                const uint32_t dst = ring + (f_count & (C::PD - 1)) * kRingSlot;
 #pragma unroll
                 for (int pl = 0; pl < kPlanes; ++pl)
 #pragma unroll
@@ -334,78 +449,153 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes>::kThreads, 1)
             }
             cp_async_commit();
         };
+        if constexpr (!kTma) {
 #pragma unroll 1
-        for (int p = 0; p < PD - 1; ++p) fetch_next();
+            for (int p = 0; p < C::PD - C::kSub; ++p) fetch_next();
+        }
 
-        uint32_t gk = 0;  // global stage counter (ring / phase bookkeeping)
+        constexpr uint32_t kSub = C::kSub;
+        uint32_t gk = 0;  // global stage counter (packed ring)
+        uint32_t gs = 0;  // global superstage counter (expanded buffers / phases)
         int it = 0;
 #pragma unroll 1
         for (int tile = blockIdx.x; tile < tmap.ntiles; tile += gridDim.x, ++it) {
             int32_t my_popc = 0;
+            // im2col route: this B row's window corner and the running tap
+            int c_iy0 = 0, c_ix0 = 0, c_cw = 0, c_i = 0, c_j = 0;
+            if constexpr (std::is_same<BLoad, TmaConv>::value) {
+                int tm, tn;
+                tmap.decode(tile, tm, tn);
+                const int64_t ohw = (int64_t)bload.oh * bload.ow;
+                const int64_t n = (int64_t)tn * BN + (is_a ? 0 : row);
+                const int p = (int)(n % ohw);
+                c_iy0 = (p / bload.ow) * bload.sh - bload.ph;
+                c_ix0 = (p % bload.ow) * bload.sw - bload.pw;
+            }
 #pragma unroll 1
-            for (uint32_t kt = 0; kt < kt32; ++kt, ++gk) {
-                fetch_next();
-                cp_async_wait<PD - 1>();
-                uint32_t wv[4], wv1[4] = {0, 0, 0, 0};
-                const uint32_t slot = ring + (gk & (PD - 1)) * kRingSlot;
-                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n"
-                             : "=r"(wv[0]), "=r"(wv[1]), "=r"(wv[2]), "=r"(wv[3])
-                             : "r"(slot));
-                if constexpr (kPlanes == 2)
-                    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n"
-                                 : "=r"(wv1[0]), "=r"(wv1[1]), "=r"(wv1[2]), "=r"(wv1[3])
-                                 : "r"(slot + 16));
-                // expanded registers of word q for this operand side
-                auto expand = [&](int q, bool as_a, uint32_t (&r)[8]) {
-                    if constexpr (kPlanes == 2) {
-                        my_popc += __popc(wv[q]) + 2 * __popc(wv1[q]);  // code sum
-                        expand_code2(wv[q], wv1[q], r);
-                    } else {
-                        my_popc += __popc(wv[q]);
-                        if (as_a) expand8<true>(wv[q], r);
-                        else expand8<false>(wv[q], r);
+            for (uint32_t kt = 0; kt < kt32; kt += kSub, ++gs) {
+                const uint32_t nsub = kt32 - kt < kSub ? kt32 - kt : kSub;
+                uint32_t wv[kSub][4], wv1[kSub][4] = {};
+                if constexpr (kTma) {
+                    // this superstage's packed rows, landed by the TMA warp
+                    const uint32_t ts = gs % C::kTmaSlots;
+                    mbar_wait(bar_ld + 8 * ts, (gs / C::kTmaSlots) & 1u);
+                    if (lane == 0 && (warp == 0 || warp == C::kProducerWarps - 1)) tr(warp ? 6 : 3, gs);
+                    const uint32_t rbase = s_pk + ts * C::kTmaSlotBytes +
+                                           (is_a ? row * kSub * 16 : C::kTmaA + row * kSub * 16);
+#pragma unroll
+                    for (uint32_t u = 0; u < kSub; ++u) {
+                        // SWIZZLE_32B (kSub == 2): 16-B chunk u of row r sits at u ^ bit 2 of r
+                        const uint32_t a = rbase + (kSub == 2 ? ((u ^ ((row >> 2) & 1)) * 16) : 0);
+                        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n"
+                                     : "=r"(wv[u][0]), "=r"(wv[u][1]), "=r"(wv[u][2]), "=r"(wv[u][3])
+                                     : "r"(a)
+                                     : "memory");
                     }
-                };
-                const int s = (int)(gk % ES);
-                if (gk >= ES) mbar_wait(bar_empty + 8 * s, ((gk / ES) - 1) & 1u);
-                if (!active) {
-                } else if (is_a) {
-                    if constexpr (kATmem) {
-                        // warps 0..3 own TMEM lanes 0..127 = A rows 0..127
-                        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) +
-                                               C::kAStageCol + s * 32;
+                    if constexpr (std::is_same<BLoad, TmaConv>::value) {
+                        // padding: this pixel's window tap outside the image reads as +1
+                        if (!is_a) {
+                            const bool oob = (unsigned)(c_iy0 + c_i) >= (unsigned)bload.H ||
+                                             (unsigned)(c_ix0 + c_j) >= (unsigned)bload.W;
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            uint32_t r[8];
-                            expand(q, true, r);
-                            if (!(dbg & 4)) tmem_st8(taddr + q * 8, r);
-                        }
-                        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
-                        fence_before();
-                    } else {
-                        const uint32_t row_base = s_exp + s * C::kStageBytes + row * kRowBytes;
+                            for (uint32_t u = 0; u < kSub; ++u)
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            uint32_t r[8];
-                            expand(q, true, r);
-                            store_row32(r, row_base, row, q);
+                                for (int q = 0; q < 4; ++q)
+                                    if (oob) wv[u][q] = 0xffffffffu;
                         }
-                        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                        c_cw += 4 * kSub;
+                        if (c_cw == bload.cs32) {
+                            c_cw = 0;
+                            if (++c_j == bload.kw) c_j = 0, ++c_i;
+                        }
                     }
                 } else {
-                    const uint32_t row_base =
-                        s_exp + s * C::kStageBytes + C::kStageA + row * kRowBytes;
+                    // keep PD - kSub stages in flight beyond this superstage
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        uint32_t r[8];
-                        expand(q, false, r);
-                        if (!(dbg & 1)) store_row32(r, row_base, row, q);
-                        else if (r[0] == 0x12345678u && r[7] == 0x9abcdef0u) store_row32(r, row_base, row, q);
+                    for (uint32_t u = 0; u < kSub; ++u)
+                        if (u < nsub) fetch_next();
+                    if (lane == 0 && warp == C::kProducerWarps - 1) tr(0, gs);
+                    cp_async_wait<C::PD - C::kSub>();
+                    if (lane == 0 && (warp == 0 || warp == C::kProducerWarps - 1)) tr(warp ? 6 : 3, gs);
+#pragma unroll
+                    for (uint32_t u = 0; u < kSub; ++u) {
+                        if (u >= nsub) break;
+                        const uint32_t slot = ring + ((gk + u) & (C::PD - 1)) * kRingSlot;
+                        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n"
+                                     : "=r"(wv[u][0]), "=r"(wv[u][1]), "=r"(wv[u][2]), "=r"(wv[u][3])
+                                     : "r"(slot));
+                        if constexpr (kPlanes == 2)
+                            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n"
+                                         : "=r"(wv1[u][0]), "=r"(wv1[u][1]), "=r"(wv1[u][2]),
+                                           "=r"(wv1[u][3])
+                                         : "r"(slot + 16));
                     }
+                }
+                // expanded registers of word q of stage u for this operand side
+                auto expand = [&](uint32_t u, int q, bool as_a, uint32_t (&r)[8]) {
+                    if constexpr (kPlanes == 2) {
+                        my_popc += __popc(wv[u][q]) + 2 * __popc(wv1[u][q]);  // code sum
+                        expand_code2(wv[u][q], wv1[u][q], r);
+                    } else {
+                        my_popc += __popc(wv[u][q]);
+                        if (as_a) expand8<true>(wv[u][q], r);
+                        else expand8<false>(wv[u][q], r);
+                    }
+                };
+                const int sb = (int)(gs % ES);
+                if (gs >= ES) mbar_wait(bar_empty + 8 * sb, ((gs / ES) - 1) & 1u);
+                if (lane == 0 && (warp == 0 || warp == C::kProducerWarps - 1)) tr(warp ? 4 : 1, gs);
+#pragma unroll
+                for (uint32_t u = 0; u < kSub; ++u) {
+                    if (u >= nsub || !active) break;
+                    const uint32_t stage = s_exp + sb * C::kSuperBytes + u * C::kStageBytes;
+                    if (is_a) {
+                        if constexpr (kATmem) {
+                            // warps 0..3 own TMEM lanes 0..127 = A rows 0..127
+                            const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) +
+                                                   C::kAStageCol + (sb * kSub + u) * 32;
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                uint32_t r[8];
+                                expand(u, q, true, r);
+                                if (!(dbg & 4)) tmem_st8(taddr + q * 8, r);
+                            }
+                        } else {
+                            const uint32_t row_base = stage + row * kRowBytes;
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                uint32_t r[8];
+                                expand(u, q, true, r);
+                                store_row32(r, row_base, row, q);
+                            }
+                        }
+                    } else {
+                        const uint32_t row_base = stage + C::kStageA + row * kRowBytes;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            uint32_t r[8];
+                            expand(u, q, false, r);
+                            if (!(dbg & 1)) store_row32(r, row_base, row, q);
+                            else if (r[0] == 0x12345678u && r[7] == 0x9abcdef0u) store_row32(r, row_base, row, q);
+                        }
+                    }
+                }
+                if (kATmem && is_a) {
+                    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+                    fence_before();
+                } else {
                     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                 }
                 __syncwarp();  // every lane's writes + fence precede the warp's arrival
-                if (lane == 0) mbar_arrive(bar_full + 8 * s);
+                if (lane == 0 && (warp == 0 || warp == C::kProducerWarps - 1)) tr(warp ? 5 : 2, gs);
+                if (lane == 0) {
+                    mbar_arrive(bar_full + 8 * sb);
+                    // release the TMA slot only now: every lane's ld.shared result has
+                    // been consumed by the expansion above (in-order issue), so the
+                    // next TMA write into the slot cannot overtake a pending read
+                    if constexpr (kTma) mbar_arrive(bar_free + 8 * ((gs % C::kTmaSlots)));
+                }
+                gk += nsub;
             }
             // hand this tile's row popcounts to the epilogue (double-buffered)
             const int buf = it & 1;
@@ -416,11 +606,59 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes>::kThreads, 1)
             if (lane == 0) mbar_arrive(bar_pfull + 8 * buf);
         }
         cp_async_wait<0>();
+    } else if (warp == C::kTmaWarp) {
+        // ================================================================ TMA issuer
+        if constexpr (kTma) {
+            if (lane == 0) {
+                asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&aload.map)));
+                asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&bload.map)));
+                const uint32_t kt32 = (uint32_t)ktiles;
+                uint32_t g = 0;
+#pragma unroll 1
+                for (int tile = blockIdx.x; tile < tmap.ntiles; tile += gridDim.x) {
+                    int tm, tn;
+                    tmap.decode(tile, tm, tn);
+                    // im2col start: the tile's first output pixel (b, oy, ox) -> window corner
+                    int cw = 0, ci = 0, cj = 0, cx = 0, cy = 0, cb = 0;
+                    if constexpr (std::is_same<BLoad, TmaConv>::value) {
+                        const int64_t n0 = (int64_t)tn * BN, ohw = (int64_t)bload.oh * bload.ow;
+                        cb = (int)(n0 / ohw);
+                        const int p = (int)(n0 - (int64_t)cb * ohw);
+                        cy = (p / bload.ow) * bload.sh - bload.ph;
+                        cx = (p % bload.ow) * bload.sw - bload.pw;
+                    }
+#pragma unroll 1
+                    for (uint32_t kt = 0; kt < kt32; kt += C::kSub, ++g) {
+                        const uint32_t ts = g % C::kTmaSlots;
+                        if (g >= (uint32_t)C::kTmaSlots)
+                            mbar_wait(bar_free + 8 * ts, ((g / C::kTmaSlots) - 1) & 1u);
+                        const uint32_t dst = s_pk + ts * C::kTmaSlotBytes;
+                        mbar_arrive_expect_tx(bar_ld + 8 * ts, C::kTmaA + C::kTmaB);
+                        tma_load_2d(dst, &aload.map, (int)(kt * kWordsPerStage), tm * BM, bar_ld + 8 * ts);
+                        if constexpr (std::is_same<BLoad, TmaConv>::value) {
+                            // superstage kt: tap (ci, cj), channel words cw .. cw + 8
+                            tma_load_im2col_4d(dst + C::kTmaA, &bload.map, cw, cx, cy, cb,
+                                               (uint16_t)cj, (uint16_t)ci, bar_ld + 8 * ts);
+                            cw += 4 * C::kSub;
+                            if (cw == bload.cs32) {
+                                cw = 0;
+                                if (++cj == bload.kw) cj = 0, ++ci;
+                            }
+                        } else {
+                            tma_load_2d(dst + C::kTmaA, &bload.map, (int)(kt * kWordsPerStage),
+                                        tn * BN, bar_ld + 8 * ts);
+                        }
+                    }
+                }
+            }
+        }
+        __syncwarp();
     } else if (warp == C::kMmaWarp) {
         // ================================================================ MMA issuer
         if (lane == 0) {
-            uint32_t gk = 0;
+            uint32_t gs = 0;
             const uint32_t kt32 = (uint32_t)ktiles;
+            constexpr uint32_t kSub = C::kSub;
             int it = 0;
 #pragma unroll 1
             for (int tile = blockIdx.x; tile < tmap.ntiles; tile += gridDim.x, ++it) {
@@ -429,24 +667,32 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes>::kThreads, 1)
                 fence_after();
                 const uint32_t d = tmem + buf * C::kAccCols;
 #pragma unroll 1
-                for (uint32_t kt = 0; kt < kt32; ++kt, ++gk) {
-                    const int s = (int)(gk % ES);
-                    mbar_wait(bar_full + 8 * s, (gk / ES) & 1u);
-                    if (gk == 0) trace(2);
+                for (uint32_t kt = 0; kt < kt32; kt += kSub, ++gs) {
+                    const uint32_t nsub = kt32 - kt < kSub ? kt32 - kt : kSub;
+                    const int sb = (int)(gs % ES);
+                    mbar_wait(bar_full + 8 * sb, (gs / ES) & 1u);
+                    tr(7, gs);
+                    if (gs == 0) trace(2);
                     fence_after();
-                    const uint32_t b_addr = s_exp + s * C::kStageBytes + C::kStageA;
 #pragma unroll
-                    for (int kk = 0; kk < kRowBytes / 32; ++kk) {
-                        if (dbg & 2) break;
-                        const uint32_t acc = (kt | kk) != 0 ? 1u : 0u;
-                        if constexpr (kATmem)
-                            mma_ts<C::kIdesc>(d, tmem + C::kAStageCol + s * 32 + kk * 8,
-                                              sw128_desc(b_addr + kk * 32), acc);
-                        else
-                            mma_ss<C::kIdesc>(d, sw128_desc(s_exp + s * C::kStageBytes + kk * 32),
-                                              sw128_desc(b_addr + kk * 32), acc);
+                    for (uint32_t u = 0; u < kSub; ++u) {
+                        if (u >= nsub) break;
+                        const uint32_t stage = s_exp + sb * C::kSuperBytes + u * C::kStageBytes;
+                        const uint32_t b_addr = stage + C::kStageA;
+#pragma unroll
+                        for (int kk = 0; kk < kRowBytes / 32; ++kk) {
+                            if (dbg & 2) break;
+                            const uint32_t acc = ((kt + u) | kk) != 0 ? 1u : 0u;
+                            if constexpr (kATmem)
+                                mma_ts<C::kIdesc>(d, tmem + C::kAStageCol + (sb * kSub + u) * 32 + kk * 8,
+                                                  sw128_desc(b_addr + kk * 32), acc);
+                            else
+                                mma_ss<C::kIdesc>(d, sw128_desc(stage + kk * 32),
+                                                  sw128_desc(b_addr + kk * 32), acc);
+                        }
                     }
-                    umma_commit(bar_empty + 8 * s);
+                    umma_commit(bar_empty + 8 * sb);
+                    tr(8, gs);
                 }
                 umma_commit(bar_tfull + 8 * buf);
                 if (it < 3) trace(3 + 3 * it);
@@ -477,8 +723,8 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes>::kThreads, 1)
             tmap.decode(tile, tm, tn);
             const int64_t mq = (int64_t)tm * BM + q * 32, n0 = (int64_t)tn * BN;
             const int64_t m = mq + lane;
-            mbar_wait(bar_tfull + 8 * buf, (uint32_t)(it >> 1) & 1u);
-            mbar_wait(bar_pfull + 8 * buf, (uint32_t)(it >> 1) & 1u);
+            mbar_wait_sleep(bar_tfull + 8 * buf, (uint32_t)(it >> 1) & 1u);
+            mbar_wait_sleep(bar_pfull + 8 * buf, (uint32_t)(it >> 1) & 1u);
             fence_after();
             if (e == 0 && lane == 0 && it < 3) trace(4 + 3 * it);
             const bool mok = m < M;
@@ -640,11 +886,92 @@ static int sm_count() {
     return n;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                  const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                  const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+// [rows, kw32] u32 view with row pitch ld32 words; box = box_words x box_rows
+static int encode_rows(TmaRows &t, int box_words, int box_rows) {
+    EncodeTiledFn fn = encode_tiled();
+    if (!fn) return set_error(BNN_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t dims[2] = {(cuuint64_t)t.kw32, (cuuint64_t)t.rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)t.ld32 * 4};
+    const cuuint32_t box[2] = {(cuuint32_t)box_words, (cuuint32_t)box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUtensorMapSwizzle sw = box_words * 4 == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                                      : CU_TENSOR_MAP_SWIZZLE_NONE;
+    CUresult r = fn(&t.map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint32_t *>(t.base), dims,
+                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_error(BNN_ECUDA, "cuTensorMapEncodeTiled failed");
+    return BNN_OK;
+}
+
+typedef CUresult (*EncodeIm2colFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                   const cuuint64_t *, const cuuint64_t *, const int *, const int *,
+                                   cuuint32_t, cuuint32_t, const cuuint32_t *, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                   CUtensorMapFloatOOBfill);
+static int encode_conv(TmaConv &t, int box_words, int box_pixels, int64_t B) {
+    static EncodeIm2colFn fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeIm2colFn>(p);
+    }
+    if (!fn) return set_error(BNN_ECUDA, "cuTensorMapEncodeIm2col unavailable");
+    const cuuint64_t dims[4] = {(cuuint64_t)t.cs32, (cuuint64_t)t.W, (cuuint64_t)t.H, (cuuint64_t)B};
+    const cuuint64_t strides[3] = {(cuuint64_t)t.cs32 * 4, (cuuint64_t)t.cs32 * 4 * t.W,
+                                   (cuuint64_t)t.cs32 * 4 * t.W * t.H};
+    // window corners traversed per image: first (-ph, -pw), last ((oh-1)sh - ph, (ow-1)sw - pw),
+    // the upper corner given relative to (H - 1, W - 1); order W, H (innermost first)
+    const int lower[2] = {-t.pw, -t.ph};
+    const int upper[2] = {(t.ow - 1) * t.sw - t.pw - (t.W - 1), (t.oh - 1) * t.sh - t.ph - (t.H - 1)};
+    const cuuint32_t estr[4] = {1, (cuuint32_t)t.sw, (cuuint32_t)t.sh, 1};
+    CUresult r = fn(&t.map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, const_cast<uint32_t *>(t.x), dims,
+                    strides, lower, upper, (cuuint32_t)box_words, (cuuint32_t)box_pixels, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    box_words * 4 == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_error(BNN_ECUDA, "cuTensorMapEncodeIm2col failed");
+    return BNN_OK;
+}
+
 template <int BN, bool kATmem, int kVec, class ALoad, class BLoad, class Store, int kPlanes = 1>
-static int launch_umma_cfg(const ALoad &a, const BLoad &b, const Store &st, const Epilogue &ep,
+static int launch_umma_cfg(const ALoad &a_in, const BLoad &b_in, const Store &st, const Epilogue &ep,
                            int64_t M, int64_t N, int64_t kw32, cudaStream_t s) {
-    using C = umma::Cfg<BN, kATmem, kPlanes>;
+    constexpr bool kTma = umma::is_tma<ALoad>::value;
+    using C = umma::Cfg<BN, kATmem, kPlanes, kTma>;
     auto kern = umma::xnor_umma_kernel<BN, kATmem, kVec, ALoad, BLoad, Store, kPlanes>;
+    ALoad a = a_in;
+    BLoad b = b_in;
+    if constexpr (kTma) {
+        int rc = encode_rows(a, 4 * C::kSub, umma::BM);
+        if constexpr (std::is_same<BLoad, TmaConv>::value) {
+            static_assert(C::kSub == 2, "im2col TMA: one 32-byte tap chunk per superstage");
+            if (rc == BNN_OK) rc = encode_conv(b, 4 * C::kSub, BN, b.npix / ((int64_t)b.oh * b.ow));
+        } else {
+            if (rc == BNN_OK) rc = encode_rows(b, 4 * C::kSub, BN);
+        }
+        if (rc != BNN_OK) return rc;
+    }
     static bool configured = false;
     if (!configured) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
@@ -689,7 +1016,8 @@ static int choose_bn(int64_t M, int64_t N) {
 template <int kVec, class ALoad, class BLoad, class Store>
 static int launch_umma(const ALoad &a, const BLoad &b, const Store &st, const Epilogue &ep,
                        int64_t M, int64_t N, int64_t kw32, cudaStream_t s) {
-    if (umma_variant() == 0) return launch_umma_cfg<256, false, kVec>(a, b, st, ep, M, N, kw32, s);
+    if constexpr (!std::is_same<BLoad, TmaConv>::value)
+        if (umma_variant() == 0) return launch_umma_cfg<256, false, kVec>(a, b, st, ep, M, N, kw32, s);
     switch (choose_bn(M, N)) {
         case 128: return launch_umma_cfg<128, true, kVec>(a, b, st, ep, M, N, kw32, s);
         case 160: return launch_umma_cfg<160, true, kVec>(a, b, st, ep, M, N, kw32, s);
@@ -707,6 +1035,13 @@ int launch_xnor_gemm_umma(const uint64_t *A, int64_t lda, const uint64_t *B, int
     GemmStore st{C, ldc_m, ldc_n, M, N, res};
     const bool vec4 = (lda % 2 == 0) && (ldb % 2 == 0) &&
                       ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) == 0;
+    if (vec4 && !(umma_dbg() & 256)) {
+        // TMA needs 16-B aligned bases and row pitches (even u64 leading dims)
+        TmaRows ta{}, tb{};
+        ta.base = a.base, ta.ld32 = a.ld32, ta.rows = M, ta.kw32 = kw32;
+        tb.base = b.base, tb.ld32 = b.ld32, tb.rows = N, tb.kw32 = kw32;
+        return launch_umma<4>(ta, tb, st, ep, M, N, kw32, s);
+    }
     return vec4 ? launch_umma<4>(a, b, st, ep, M, N, kw32, s)
                 : launch_umma<2>(a, b, st, ep, M, N, kw32, s);
 }
@@ -746,6 +1081,21 @@ int launch_bconv2d_umma(const uint64_t *x, int64_t B, int64_t C, int64_t H, int6
     ConvStore st{y, F, oh * ow, npix, res};
     const bool vec4 = (cw64 % 2 == 0) &&
                       ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w)) & 15) == 0;
+    // im2col TMA: whole 32-byte tap chunks (C % 256 == 0), corner offsets and
+    // strides within the tensor-map limits, A-in-TMEM engine (superstages of 2)
+    const int64_t up_w = (ow - 1) * sw - pw - (W - 1), up_h = (oh - 1) * sh - ph - (H - 1);
+    const bool im2col = vec4 && cs32 % 8 == 0 && umma_variant() == 1 && !(umma_dbg() & 256) &&
+                        ph <= 128 && pw <= 128 && up_w >= -128 && up_w <= 127 && up_h >= -128 &&
+                        up_h <= 127 && sh <= 8 && sw <= 8 && kh <= 128 && kw <= 128;
+    if (im2col) {
+        TmaRows ta{};
+        ta.base = a.base, ta.ld32 = kw32, ta.rows = F, ta.kw32 = kw32;
+        TmaConv tb{};
+        tb.x = reinterpret_cast<const uint32_t *>(x), tb.npix = npix, tb.H = (int)H, tb.W = (int)W;
+        tb.cs32 = (int)cs32, tb.kw = (int)kw, tb.sh = (int)sh, tb.sw = (int)sw, tb.ph = (int)ph;
+        tb.pw = (int)pw, tb.oh = (int)oh, tb.ow = (int)ow;
+        return launch_umma<4>(ta, tb, st, ep, F, npix, kw32, s);
+    }
     return vec4 ? launch_umma<4>(a, b, st, ep, F, npix, kw32, s)
                 : launch_umma<2>(a, b, st, ep, F, npix, kw32, s);
 }

@@ -237,6 +237,33 @@ def test_conv_cases_bit_exact(bnn, golden, algo):
         assert np.array_equal(yf, g[f"y{i}"]), case
 
 
+# channel counts that take the im2col-TMA route of the tcgen05 engine (C % 256 == 0):
+# odd strides, asymmetric padding, pixel tiles straddling rows and images
+IM2COL_CASES = [
+    # (B, C, H, W, F, kh, kw, stride, pad, seed)
+    (2, 256, 9, 11, 40, 3, 3, (1, 1), (1, 1), 31),
+    (3, 256, 7, 5, 130, 3, 3, (2, 1), (1, 2), 32),
+    (1, 512, 6, 6, 17, 1, 1, (1, 1), (0, 0), 33),
+    (2, 256, 10, 10, 64, 5, 3, (2, 3), (2, 0), 34),
+    (5, 256, 4, 4, 256, 2, 2, (1, 1), (0, 1), 35),
+    (1, 256, 30, 30, 8, 3, 3, (1, 1), (0, 0), 36),
+]
+
+
+@pytest.mark.parametrize("case", IM2COL_CASES)
+def test_conv_im2col_route_matches_oracle(bnn, case):
+    b, c, h, w, f, kh, kw, stride, pad, seed = case
+    x, wt = wl.conv_case_inputs(case)
+    expect = orc.qconv_packed(x, wt, stride, pad)
+    for algo in ("umma1", "umma0", "popc"):
+        layer = bnn.QConvolution(c, f, (kh, kw), stride, pad)
+        layer.weight = wt
+        layer.pack()
+        layer.algo = A(algo)
+        y = layer.forward(torch.from_numpy(x).cuda(), bnn.INFER_PACKED).cpu().numpy()
+        assert np.array_equal(y, expect), (case, algo)
+
+
 def test_reference_layers_bit_exact(bnn, golden):
     g = golden["layers"]
     qd = bnn.QDense(130, 17, bits=1)
@@ -431,3 +458,20 @@ def test_qfullyconnected_2bit_packed_equals_float_path(bnn):
     q = bnn.QDense(300, 70, bits=2, rng=rng)
     with pytest.raises(bnn.ModeError):
         q.forward(x, bnn.INFER_PACKED)
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+def test_umma_repeat_runs_identical(bnn, variant):
+    """Pipeline-race guard: repeated launches of the TMA-fed tcgen05 engine on a
+    many-tile shape equal the CUDA-core engine every time (a slot released
+    before its reads landed once corrupted ~1 run in 20)."""
+    from paper_1705_09864_b200 import _lib
+    m, n, k = 4096, 4096, 4096
+    g = torch.Generator(device="cuda").manual_seed(7)
+    a = torch.randint(-2**63, 2**63 - 1, (m, k // 64), device="cuda", generator=g).view(torch.uint64)
+    b = torch.randint(-2**63, 2**63 - 1, (n, k // 64), device="cuda", generator=g).view(torch.uint64)
+    ref = bnn.xnor_rows_gemm(a, b, k, algo="popc")
+    _lib.call("bnn_set_umma_variant", variant)
+    for _ in range(12):
+        assert torch.equal(bnn.xnor_rows_gemm(a, b, k, algo="umma"), ref)
+    _lib.call("bnn_set_umma_variant", 1)
