@@ -228,6 +228,9 @@ int bnn_bconv2d_ex(const uint64_t *x_words, int64_t B, int64_t C, int64_t H, int
                    int64_t sw, int64_t ph, int64_t pw, float *y, const bnn_epilogue *ep, int algo,
                    bnn_stream_t stream);
 
+/* Debug: *dst = %globaltimer (ns) when a one-thread kernel on `stream` runs. */
+int bnn_debug_stamp(uint64_t *dst, bnn_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -54,6 +54,7 @@ SIGNATURES = {
     "bnn_bconv2d_ex": (_i32, [_vp, _i64, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i64,
                               _i64, _i64, _vp, _vp, _i32, _vp]),
     "bnn_umma_trace": (_i32, [_vp]),
+    "bnn_debug_stamp": (_i32, [_vp, _vp]),
 }
 
 

@@ -184,14 +184,17 @@ __device__ __forceinline__ void tma_load_im2col_4d(uint32_t dst, const CUtensorM
         : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+    // the suspend-time hint parks the warp in try_wait until the phase
+    // completes instead of re-issuing the probe (spinning warps steal issue
+    // slots from the expanders sharing their scheduler)
     uint32_t done = 0;
     do {
         asm volatile(
             "{\n.reg .pred p;\n"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
             "selp.u32 %0, 1, 0, p;\n}\n"
             : "=r"(done)
-            : "r"(bar), "r"(phase)
+            : "r"(bar), "r"(phase), "r"(0x989680u)
             : "memory");
     } while (!done);
 }
@@ -715,6 +718,7 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value>
         const bool affine = ep.scale || ep.shift;
         const bool dot = ep.domain == BNN_DOT;
         const bool magic = ep.k_logical < (1 << 21);  // int -> f32 via the 2^23 trick
+        const bool plain = magic && !affine && ep.bn_mean == nullptr;  // straight-line decode
         int it = 0;
 #pragma unroll 1
         for (int tile = blockIdx.x; tile < tmap.ntiles; tile += gridDim.x, ++it) {
@@ -730,6 +734,8 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value>
             const bool mok = m < M;
             // per-row constants: P = kb - pb[n] + 2C, with 2C = acc >> 6 (acc = 128 C)
             const int32_t kb = ep.k_eff - s_popc_a[buf * BM + q * 32 + lane];
+            const int32_t rowc = (dot ? 2 * kb - ep.k_logical : kb) + 0x4B400000;
+            const uint32_t vsh = dot ? 5u : 6u, psh = dot ? 1u : 0u;
             // multi-bit decode constants (kPlanes == 2): s_popc_* hold code sums
             const int32_t abab = ep.a_alpha * ep.b_alpha;
             const int32_t rowterm = ep.a_alpha * ep.b_beta * s_popc_a[buf * BM + q * 32 + lane] +
@@ -758,30 +764,53 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value>
                 const int64_t nc = n0 + c * 32;
                 if (mq >= M || nc >= N) continue;  // warp-uniform
                 float f[32];
+                if constexpr (kPlanes == 2) {
 #pragma unroll
-                for (int j4 = 0; j4 < 8; ++j4) {
-                    const int4 pb4 = *reinterpret_cast<const int4 *>(pb + c * 32 + 4 * j4);
-                    const int32_t pbv[4] = {pb4.x, pb4.y, pb4.z, pb4.w};
+                    for (int j4 = 0; j4 < 8; ++j4) {
+                        const int4 pb4 = *reinterpret_cast<const int4 *>(pb + c * 32 + 4 * j4);
+                        const int32_t pbv[4] = {pb4.x, pb4.y, pb4.z, pb4.w};
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const int j = 4 * j4 + i;
-                        if constexpr (kPlanes == 2) {
+                        for (int i = 0; i < 4; ++i) {
                             // exact integer numerator, one rounding: (.) / (gA gB)
-                            const int32_t num = abab * (int32_t)v[j] + rowterm + ep.a_beta * ep.b_alpha * pbv[i];
-                            f[j] = __fmul_rn((float)num, ep.inv_gamma);
-                            continue;
+                            const int32_t num = abab * (int32_t)v[4 * j4 + i] + rowterm +
+                                                ep.a_beta * ep.b_alpha * pbv[i];
+                            f[4 * j4 + i] = __fmul_rn((float)num, ep.inv_gamma);
                         }
-                        int32_t val = kb - pbv[i] + (int32_t)(v[j] >> 6);
-                        if (dot) val = 2 * val - ep.k_logical;
-                        float x = magic ? __int_as_float(val + 0x4B400000) - 12582912.0f
-                                        : (float)val;
-                        if (affine) x = __fadd_rn(__fmul_rn(x, sc), sh);
-                        if (has_bn)
-                            x = __fadd_rn(__fmul_rn(bg, __fmul_rn(__fsub_rn(x, bm), bi)), bb);
-                        f[j] = x;
+                    }
+                } else if (plain) {
+                    // P = kb - pb + 2C (2C = acc >> 6), or 2P - K = (2kb - K) - 2pb + (acc >> 5),
+                    // with the 2^23 bias of the int -> f32 trick folded into the row constant
+#pragma unroll
+                    for (int j4 = 0; j4 < 8; ++j4) {
+                        const int4 pb4 = *reinterpret_cast<const int4 *>(pb + c * 32 + 4 * j4);
+                        const int32_t pbv[4] = {pb4.x, pb4.y, pb4.z, pb4.w};
+#pragma unroll
+                        for (int i = 0; i < 4; ++i)
+                            f[4 * j4 + i] = __int_as_float(rowc + (int32_t)(v[4 * j4 + i] >> vsh) -
+                                                           (pbv[i] << psh)) -
+                                            12582912.0f;
+                    }
+                } else {
+#pragma unroll
+                    for (int j4 = 0; j4 < 8; ++j4) {
+                        const int4 pb4 = *reinterpret_cast<const int4 *>(pb + c * 32 + 4 * j4);
+                        const int32_t pbv[4] = {pb4.x, pb4.y, pb4.z, pb4.w};
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const int j = 4 * j4 + i;
+                            int32_t val = kb - pbv[i] + (int32_t)(v[j] >> 6);
+                            if (dot) val = 2 * val - ep.k_logical;
+                            float x = magic ? __int_as_float(val + 0x4B400000) - 12582912.0f
+                                            : (float)val;
+                            if (affine) x = __fadd_rn(__fmul_rn(x, sc), sh);
+                            if (has_bn)
+                                x = __fadd_rn(__fmul_rn(bg, __fmul_rn(__fsub_rn(x, bm), bi)), bb);
+                            f[j] = x;
+                        }
                     }
                 }
-                if (ncontig) {
+                if (dbg & 1024) {
+                } else if (ncontig) {
                     const uint32_t row = stg + lane * C::kStgPitch;
 #pragma unroll
                     for (int j = 0; j < 8; ++j)
@@ -862,6 +891,7 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value>
         fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
                      "n"(C::kTmemCols));
+        if (lane == 0) trace(13);
     }
 }
 

@@ -51,3 +51,15 @@ extern "C" int bnn_probe_pipe_peak(int pipe, int64_t iters, uint32_t *sink,
     *ops_per_sec = (double)blocks * threads * (double)iters * 8.0 / (ms * 1e-3);
     return BNN_OK;
 }
+
+// debug: dst[0] = %globaltimer when this one-thread kernel runs (timeline probes)
+static __global__ void stamp_kernel(uint64_t *dst) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    *dst = t;
+}
+
+extern "C" int bnn_debug_stamp(uint64_t *dst, bnn_stream_t stream) {
+    stamp_kernel<<<1, 1, 0, as_stream(stream)>>>(dst);
+    return check_launch("stamp_kernel");
+}

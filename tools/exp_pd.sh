@@ -1,3 +1,4 @@
+for d in 0; do BNN_UMMA_DEBUG=$d timeout 60 python tools/umma_dbg.py 256 25088 2304 >> gpurun_out/exp_pd.log 2>&1; done
+for d in 0; do BNN_UMMA_DEBUG=$d timeout 60 python tools/umma_dbg.py 4096 4096 4096 >> gpurun_out/exp_pd.log 2>&1; done
+timeout 300 python bench.py --steps 20 --warmup 3 2>&1 | tail -1 | cut -c1-200 >> gpurun_out/exp_pd.log
 timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -3 >> gpurun_out/exp_pd.log
-timeout 300 python bench.py --steps 20 --warmup 3 2>&1 | tail -1 >> gpurun_out/exp_pd.log
-for w in gemm4096 gemm8192 gemm4096k65536 c1 resnet18; do timeout 300 python bench.py --workload $w --steps 10 --warmup 3 2>&1 | tail -1 | cut -c1-200 >> gpurun_out/exp_pd.log; done

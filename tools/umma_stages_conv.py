@@ -18,7 +18,18 @@ s.record()
 for _ in range(10):
     plan.kernel()
 e.record(); e.synchronize()
-print(f"c2 conv kernel: {s.elapsed_time(e) / 10 * 1e3:.1f} us")
+print(f"c2 conv kernel (eager launches): {s.elapsed_time(e) / 10 * 1e3:.1f} us")
+g = torch.cuda.CUDAGraph()
+side = torch.cuda.Stream(); side.wait_stream(torch.cuda.current_stream())
+with torch.cuda.stream(side):
+    plan.kernel()
+torch.cuda.synchronize()
+with torch.cuda.graph(g):
+    for _ in range(10):
+        plan.kernel()
+g.replay(); torch.cuda.synchronize()
+s.record(); g.replay(); e.record(); e.synchronize()
+print(f"c2 conv kernel (graph, back to back): {s.elapsed_time(e) / 10 * 1e3:.1f} us")
 tr = torch.zeros(8192, dtype=torch.int64, device="cuda")
 lib.bnn_umma_trace(tr.data_ptr())
 torch.cuda.synchronize()
@@ -35,3 +46,26 @@ c = tr[:148 * 16].view(148, 16).cpu().numpy().astype(np.float64)
 c0 = c[:, 0].min()
 print("per-CTA exit (us after first start): max %.1f median %.1f" % (((c[:, 12] - c0) / 1e3).max(), np.median((c[:, 12] - c0) / 1e3)))
 print("per-CTA first mma (us): median %.2f" % np.median((c[:, 2] - c0) / 1e3))
+st = (c[:, 0] - c0) / 1e3
+print("CTA start (us): min %.2f median %.2f max %.2f; setup done median %.2f" % (st.min(), np.median(st), st.max(), np.median((c[:, 1] - c0) / 1e3)))
+
+# launch / teardown gaps: stamp -> conv -> stamp in one graph
+st = torch.zeros(4, dtype=torch.int64, device="cuda")
+from paper_1705_09864_b200 import _lib
+tr.zero_()
+lib.bnn_umma_trace(tr.data_ptr())
+g2 = torch.cuda.CUDAGraph()
+with torch.cuda.graph(g2):
+    _lib.call("bnn_debug_stamp", st.data_ptr(), _lib.stream_ptr())
+    plan.kernel()
+    _lib.call("bnn_debug_stamp", st.data_ptr() + 8, _lib.stream_ptr())
+lib.bnn_umma_trace(None)
+g2.replay(); torch.cuda.synchronize()
+c = tr[:148 * 16].view(148, 16).cpu().numpy().astype(np.int64)
+s0, s1 = [int(v) for v in st[:2].cpu()]
+print("stamp0 -> first CTA start %.2f us, -> last CTA start %.2f, last CTA exit -> stamp1 %.2f us, total %.2f us"
+      % ((c[:, 0].min() - s0) / 1e3, (c[:, 0].max() - s0) / 1e3, (s1 - c[:, 12].max()) / 1e3, (s1 - s0) / 1e3))
+d = (c[:, 13] - c[:, 12]) / 1e3
+print("per-CTA trace12 -> dealloc done: min %.2f median %.2f max %.2f us; last dealloc -> stamp1 %.2f us"
+      % (d.min(), np.median(d), d.max(), (s1 - c[:, 13].max()) / 1e3))
+print("last trace12 %.2f, last dealloc %.2f (us after first start)" % ((c[:, 12].max() - c[:, 0].min()) / 1e3, (c[:, 13].max() - c[:, 0].min()) / 1e3))
