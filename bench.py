@@ -397,6 +397,16 @@ def run_gpu_arm(args, rank, world, local_rank):
     d = workload_desc(args.workload)
     ops = plan.binary_ops
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MiB > L2
+    flush_rd = torch.zeros(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    flush_sink = torch.empty((), dtype=torch.float32, device="cuda")
+
+    def l2_flush():
+        # write a buffer larger than L2 (evicts every line of this step's data), then
+        # read another one so the dirty lines of the write are written back here, outside
+        # the timed region, instead of inside the next timed kernel (a steady-state L2
+        # holds clean data, not 126 MB of dirty scratch)
+        flush.zero_()
+        torch.amax(flush_rd, dim=0, out=flush_sink)
     stream = torch.cuda.current_stream()
 
     # Each step is replayed from a CUDA graph (pack + kernel) so the events time
@@ -425,7 +435,7 @@ def run_gpu_arm(args, rank, world, local_rank):
     torch.cuda.synchronize()
     with ClockSampler(local_rank) as clk:
         for i in range(args.steps):
-            flush.zero_()  # L2 flush between timed steps (outside the events)
+            l2_flush()  # L2 flush between timed steps (outside the events)
             s, e = ev[i]
             s.record(stream)
             g_step.replay()
@@ -434,7 +444,7 @@ def run_gpu_arm(args, rank, world, local_rank):
     if world > 1:
         dist.barrier()
     for i in range(args.steps):  # kernel alone, same flush discipline
-        flush.zero_()
+        l2_flush()
         s, e = evk[i]
         s.record(stream)
         g_kern.replay()
@@ -508,7 +518,8 @@ def run_gpu_arm(args, rank, world, local_rank):
             "data": "synthetic (seeded, BASELINE.json shapes)",
             "config": {"workload": d["workload"], "M": d["M"], "N": d["N"], "K": d["K"],
                        "batch_per_gpu": d["batch"], "parallelism": f"replicas x{world}",
-                       "l2": "flushed between timed steps (256 MiB write)",
+                       "l2": "flushed between timed steps (256 MiB write, then 256 MiB read so the "
+                             "write-backs land outside the timed region)",
                        "launch": "CUDA graph per step (pack + kernel)",
                        "algo": args.algo},
             "e2e": e2e, "gpu_launches": plan.launches_per_step * args.steps,

@@ -700,8 +700,16 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value>
                 umma_commit(bar_tfull + 8 * buf);
                 if (it < 3) trace(3 + 3 * it);
             }
+            // release TMEM as soon as the epilogue has drained the last two
+            // accumulators, overlapping the dealloc with the final stores
+            for (int t = it - 2; t < it; ++t)
+                if (t >= 0) mbar_wait(bar_tempty + 8 * (t & 1), (uint32_t)(t >> 1) & 1u);
         }
         __syncwarp();
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
+                     "n"(C::kTmemCols));
+        if (lane == 0) trace(13);
     } else {
         // ================================================================ epilogue
         // 8 warps: quadrant q = warp % 4 owns TMEM lanes (= tile rows) 32q..32q+31;
@@ -887,12 +895,6 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value>
     fence_before();
     __syncthreads();
     if (tid == 0) trace(12);
-    if (warp == C::kMmaWarp) {
-        fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
-                     "n"(C::kTmemCols));
-        if (lane == 0) trace(13);
-    }
 }
 
 }  // namespace umma

@@ -1,4 +1,3 @@
-for d in 0; do BNN_UMMA_DEBUG=$d timeout 60 python tools/umma_dbg.py 256 25088 2304 >> gpurun_out/exp_pd.log 2>&1; done
-for d in 0; do BNN_UMMA_DEBUG=$d timeout 60 python tools/umma_dbg.py 4096 4096 4096 >> gpurun_out/exp_pd.log 2>&1; done
-timeout 300 python bench.py --steps 20 --warmup 3 2>&1 | tail -1 | cut -c1-200 >> gpurun_out/exp_pd.log
-timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -3 >> gpurun_out/exp_pd.log
+BNN_UMMA_DEBUG=16 timeout 120 python tools/umma_stages_conv.py 2>&1 | grep -v "^ " > gpurun_out/stages_conv.log
+timeout 300 python tools/race_check.py 5 > gpurun_out/race.log 2>&1
+timeout 300 python bench.py --steps 20 --warmup 3 2>&1 | tail -1 > gpurun_out/bench_c2.json
