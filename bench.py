@@ -490,7 +490,9 @@ def run_gpu_arm(args, rank, world, local_rank):
         e2e = {"value": world * units_per_step / (e2e_ms / args.steps * 1e-3), "unit": unit,
                "h2d_bytes_per_step": plan.h2d_bytes, "d2h_bytes_per_step": plan.d2h_bytes,
                "ms_per_step": e2e_ms / args.steps,
-               "path": "plan.run_host: pinned H2D -> pack -> kernel -> D2H -> sync"}
+               "path": "plan.run_host: pinned H2D -> pack -> kernel -> D2H -> sync (one CUDA-graph "
+                       "replay per call, pipelined over "
+                       f"{getattr(plan, 'host_chunks', 1)} batch slices on 3 streams)"}
 
     peak = pipe_peak(args.algo)
     kern_avg = statistics.mean(kern_ms)

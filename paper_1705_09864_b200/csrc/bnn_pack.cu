@@ -61,37 +61,46 @@ __global__ void binarize_kernel(const float *__restrict__ x, int64_t n, float *_
 // lane, float4 when aligned) and emits 2 u64 words.  Lane l owns elements
 // 4l..4l+3, i.e. nibble l%8 of u32 word l/8; an OR-butterfly over the 8
 // lanes of a group assembles each u32 word.
-template <bool kVec4>
+template <bool kVec4, int kIters>
 __global__ void pack_rows_kernel(const float *__restrict__ x, int64_t R, int64_t K, int64_t ldx,
                                  uint64_t *__restrict__ out, int64_t ldo, int pad_bit, int mode,
-                                 int32_t *__restrict__ row_popc, int32_t *flags) {
+                                 int32_t *flags, int64_t nseg) {
+    // warp per (row, segment of kIters x 128 elements); every load of the segment is
+    // issued before the first is consumed, so a warp keeps kIters x 512 B in flight
     const int lane = threadIdx.x & 31;
-    const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t row = gw / nseg, seg = gw - row * nseg;
     if (row >= R) return;  // warp-uniform
     const float *xr = x + row * ldx;
     const int64_t W = ceil_div(K, 64);
-    int f = 0;
-    int popc = 0;
-    for (int64_t base = 0; base < W * 64; base += 128) {
-        const int64_t e = base + 4 * lane;
-        float v[4];
+    const int64_t base0 = seg * (128 * kIters);
+    float v[kIters][4];
+#pragma unroll
+    for (int it = 0; it < kIters; ++it) {
+        const int64_t e = base0 + 128 * it + 4 * lane;
         if (kVec4 && e + 3 < K) {
-            float4 q = __ldg(reinterpret_cast<const float4 *>(xr + e));
-            v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+            const float4 q = __ldg(reinterpret_cast<const float4 *>(xr + e));
+            v[it][0] = q.x; v[it][1] = q.y; v[it][2] = q.z; v[it][3] = q.w;
         } else {
 #pragma unroll
-            for (int i = 0; i < 4; ++i) v[i] = e + i < K ? __ldg(xr + e + i) : 0.0f;
+            for (int i = 0; i < 4; ++i) v[it][i] = e + i < K ? __ldg(xr + e + i) : 0.0f;
         }
+    }
+    int f = 0;
+#pragma unroll
+    for (int it = 0; it < kIters; ++it) {
+        const int64_t base = base0 + 128 * it;
+        if (base >= W * 64) break;  // warp-uniform
+        const int64_t e = base + 4 * lane;
         uint32_t nib = 0, valid = 0;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             bool in = e + i < K;
-            uint32_t b = in ? sign_bit(v[i]) : (uint32_t)pad_bit;
+            uint32_t b = in ? sign_bit(v[it][i]) : (uint32_t)pad_bit;
             nib |= b << i;
             valid |= (in ? 1u : 0u) << i;
-            if (in) f |= elem_flags(v[i], mode);
+            if (in) f |= elem_flags(v[it][i], mode);
         }
-        popc += __popc(nib & valid);
         uint32_t w = nib << (4 * (lane & 7));
         w |= __shfl_xor_sync(0xffffffffu, w, 1);
         w |= __shfl_xor_sync(0xffffffffu, w, 2);
@@ -101,10 +110,23 @@ __global__ void pack_rows_kernel(const float *__restrict__ x, int64_t R, int64_t
         if ((lane & 15) == 0 && wi < W) out[row * ldo + wi] = (uint64_t)w | ((uint64_t)hi << 32);
     }
     flush_flags(f, flags);
-    if (row_popc) {
-        popc = __reduce_add_sync(0xffffffffu, popc);
-        if (lane == 0) row_popc[row] = popc;
+}
+
+// popcount of each packed row's K valid bits (tail bits past K masked off)
+__global__ void row_popc_kernel(const uint64_t *__restrict__ words, int64_t R, int64_t W,
+                                int64_t ldo, int64_t K, int32_t *__restrict__ row_popc) {
+    const int lane = threadIdx.x & 31;
+    const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    if (row >= R) return;
+    int popc = 0;
+    for (int64_t w = lane; w < W; w += 32) {
+        uint64_t v = words[row * ldo + w];
+        const int64_t left = K - 64 * w;
+        if (left < 64) v &= (1ull << left) - 1ull;
+        popc += __popcll(v);
     }
+    popc = __reduce_add_sync(0xffffffffu, popc);
+    if (lane == 0) row_popc[row] = popc;
 }
 
 // ---------------------------------------------------------------- pack cols
@@ -393,15 +415,23 @@ int launch_pack_rows(const float *x, int64_t R, int64_t K, int64_t ldx, uint64_t
                      int64_t ldo, int pad_bit, int mode, int32_t *row_popc, int32_t *flags,
                      cudaStream_t s) {
     if (R == 0 || K == 0) return BNN_OK;
-    const int64_t blocks = ceil_div(R * 32, 256);
+    constexpr int kIters = 4;
+    const int64_t W = ceil_div(K, 64);
+    const int64_t nseg = ceil_div(W, 2 * kIters);  // warps per row
     const bool vec = (ldx % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+    const unsigned blocks = (unsigned)ceil_div(R * nseg * 32, 256);
     if (vec)
-        pack_rows_kernel<true><<<(unsigned)blocks, 256, 0, s>>>(x, R, K, ldx, out, ldo, pad_bit,
-                                                               mode, row_popc, flags);
+        pack_rows_kernel<true, kIters><<<blocks, 256, 0, s>>>(x, R, K, ldx, out, ldo, pad_bit, mode,
+                                                              flags, nseg);
     else
-        pack_rows_kernel<false><<<(unsigned)blocks, 256, 0, s>>>(x, R, K, ldx, out, ldo, pad_bit,
-                                                                mode, row_popc, flags);
-    return check_launch("pack_rows_kernel");
+        pack_rows_kernel<false, kIters><<<blocks, 256, 0, s>>>(x, R, K, ldx, out, ldo, pad_bit,
+                                                               mode, flags, nseg);
+    int rc = check_launch("pack_rows_kernel");
+    if (rc == BNN_OK && row_popc) {
+        row_popc_kernel<<<(unsigned)ceil_div(R * 32, 256), 256, 0, s>>>(out, R, W, ldo, K, row_popc);
+        rc = check_launch("row_popc_kernel");
+    }
+    return rc;
 }
 
 int launch_pack_cols(const float *x, int64_t K, int64_t N, int64_t ldx, uint64_t *out,

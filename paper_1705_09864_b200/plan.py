@@ -32,17 +32,69 @@ class _Plan:
         if f & _lib.FLAG_NOTSIGN:
             raise ValueError("matrix entries must all be -1 or +1")
 
+    # batch slices the end-to-end call is pipelined over (H2D of slice i+1, compute of
+    # slice i and D2H of slice i-1 overlap; PCIe is full duplex); 1 = no pipelining
+    host_chunks = 4
+
     def run_host(self, x_host: torch.Tensor, y_host: torch.Tensor) -> torch.Tensor:
-        """End to end from pinned host memory: H2D, pack, kernel, D2H, one sync."""
-        self.x.copy_(x_host, non_blocking=True)
-        self.run_device()
-        y_host.copy_(self.y, non_blocking=True)
-        self.flags_host.copy_(self.flags, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
+        """End to end from pinned host memory: H2D, pack, kernel, D2H, one sync.
+
+        Plans whose leading dimension is a batch of independent items (ConvPlan,
+        DensePlan) pipeline the copies against the compute over ``host_chunks``
+        batch slices on three streams; the result is identical to one pass.  With
+        pinned host buffers the whole schedule is captured once per (x_host,
+        y_host) pair into a CUDA graph and replayed, so a call costs one launch.
+        """
+        key = (x_host.data_ptr(), y_host.data_ptr(), self.host_chunks)
+        graphs = self.__dict__.setdefault("_host_graphs", {})
+        g = graphs.get(key)
+        if g is None and x_host.is_pinned() and y_host.is_pinned():
+            self._host_schedule(x_host, y_host)  # warm-up outside capture
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            try:
+                with torch.cuda.graph(g):
+                    self._host_schedule(x_host, y_host)
+                graphs[key] = g
+            except RuntimeError:
+                g = None
+        cur = torch.cuda.current_stream()
+        if g is not None:
+            g.replay()
+        else:
+            self._host_schedule(x_host, y_host)
+        cur.synchronize()
         f = int(self.flags_host[0])
         if f & _lib.FLAG_NONFINITE:
             raise ValueError("binarize requires finite inputs")
         return y_host
+
+    def _host_schedule(self, x_host: torch.Tensor, y_host: torch.Tensor):
+        chunks = min(self.host_chunks, self.b) if hasattr(self, "run_device_range") else 1
+        cur = torch.cuda.current_stream()
+        if chunks <= 1:
+            self.x.copy_(x_host, non_blocking=True)
+            self.run_device()
+            y_host.copy_(self.y, non_blocking=True)
+        else:
+            if not hasattr(self, "_streams"):
+                self._streams = (torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream())
+            h2d, comp, d2h = self._streams
+            for st in self._streams:
+                st.wait_stream(cur)
+            bounds = [self.b * i // chunks for i in range(chunks + 1)]
+            for i0, i1 in zip(bounds[:-1], bounds[1:]):
+                with torch.cuda.stream(h2d):
+                    self.x[i0:i1].copy_(x_host[i0:i1], non_blocking=True)
+                comp.wait_stream(h2d)
+                with torch.cuda.stream(comp):
+                    self.run_device_range(i0, i1, comp.cuda_stream)
+                d2h.wait_stream(comp)
+                with torch.cuda.stream(d2h):
+                    y_host[i0:i1].copy_(self.y[i0:i1], non_blocking=True)
+            for st in self._streams:
+                cur.wait_stream(st)
+        self.flags_host.copy_(self.flags, non_blocking=True)
 
     @property
     def h2d_bytes(self) -> int:
@@ -99,6 +151,22 @@ class ConvPlan(_Plan):
         self.kernel()
         return self.y
 
+    def run_device_range(self, i0: int, i1: int, stream: int):
+        """pack + conv of images [i0, i1) only (images are independent)."""
+        L = self.layer
+        kh, kw = L.kernel
+        nb = i1 - i0
+        x = self.x[i0:i1]
+        xw = self.xw[i0:i1]
+        y = self.y[i0:i1]
+        _lib.check(self.lib.bnn_pack_nchw_f32(x.data_ptr(), nb, L.in_channels, self.h, self.w,
+                                              xw.data_ptr(), self.mode, self.flags.data_ptr(),
+                                              stream), "pack")
+        _lib.check(self.lib.bnn_bconv2d(xw.data_ptr(), nb, L.in_channels, self.h, self.w,
+                                        self.wd.data_ptr(), L.filters, kh, kw, L.stride[0],
+                                        L.stride[1], L.pad[0], L.pad[1], y.data_ptr(), L.domain,
+                                        None, None, self.algo, stream), "bconv2d")
+
 
 class DensePlan(_Plan):
     """sign+pack rows (bnn_pack_rows_f32) -> xnor GEMM (bnn_xnor_gemm), out [B, units]."""
@@ -139,6 +207,18 @@ class DensePlan(_Plan):
         self.pack()
         self.kernel()
         return self.y
+
+    def run_device_range(self, i0: int, i1: int, stream: int):
+        """sign+pack and GEMM of batch rows [i0, i1) (rows are independent)."""
+        nb = i1 - i0
+        x, xw, y = self.x[i0:i1], self.xw[i0:i1], self.y[i0:i1]
+        _lib.check(self.lib.bnn_pack_rows_f32(x.data_ptr(), nb, self.k, self.k, xw.data_ptr(),
+                                              self.xw.shape[1], 0, self.mode, None,
+                                              self.flags.data_ptr(), stream), "pack")
+        _lib.check(self.lib.bnn_xnor_gemm(self.wa.data_ptr(), self.wa.shape[1], xw.data_ptr(),
+                                          self.xw.shape[1], self.m, nb, self.k, 0, 0,
+                                          y.data_ptr(), 1, self.m, self.layer.domain, None,
+                                          None, self.algo, stream), "xnor_gemm")
 
 
 class GemmPlan(_Plan):

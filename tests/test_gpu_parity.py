@@ -475,3 +475,53 @@ def test_umma_repeat_runs_identical(bnn, variant):
     for _ in range(12):
         assert torch.equal(bnn.xnor_rows_gemm(a, b, k, algo="umma"), ref)
     _lib.call("bnn_set_umma_variant", 1)
+
+
+@pytest.mark.parametrize("which", ["conv", "dense"])
+def test_plan_run_host_pipelined_equals_single_pass(bnn, which):
+    """The end-to-end host call overlaps H2D / compute / D2H over batch slices;
+    its output must equal the one-pass result and the oracle."""
+    from paper_1705_09864_b200.plan import ConvPlan, DensePlan
+    rng = np.random.default_rng(12)
+    if which == "conv":
+        b, c, h, w, f = 7, 256, 9, 9, 40
+        x = rng.standard_normal((b, c, h, w), dtype=np.float32)
+        wt = rng.standard_normal((f, c, 3, 3), dtype=np.float32)
+        layer = bnn.QConvolution(c, f, (3, 3), (1, 1), (1, 1))
+        layer.weight = wt
+        layer.pack()
+        plan = ConvPlan(layer, b, h, w)
+        expect = orc.qconv_packed(x, wt, (1, 1), (1, 1))
+    else:
+        b, k, u = 37, 1000, 70
+        x = rng.standard_normal((b, k), dtype=np.float32)
+        wt = rng.standard_normal((u, k), dtype=np.float32)
+        layer = bnn.QFullyConnected(k, u)
+        layer.weight = wt
+        layer.pack()
+        plan = DensePlan(layer, b)
+        expect = orc.qdense_packed(orc.binarize(x), wt)
+    xh = torch.from_numpy(x).pin_memory()
+    outs = []
+    for chunks in (1, 3, 8):
+        plan.host_chunks = chunks
+        yh = torch.empty(plan.y.shape, dtype=torch.float32).pin_memory()
+        outs.append(plan.run_host(xh, yh).numpy().copy())
+    assert np.array_equal(outs[0], expect)
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+
+
+@pytest.mark.parametrize("r,k,pad", [(3, 1, 0), (5, 200, 1), (256, 4096, 0), (7, 1000, 1), (2, 70000, 0)])
+def test_pack_rows_segments_and_row_popcounts(bnn, r, k, pad):
+    """Row packing split over several warps per row + the valid-bit row popcounts."""
+    from paper_1705_09864_b200.bitpack import pack_rows_device
+    rng = np.random.default_rng(r * 7 + k)
+    x = rng.standard_normal((r, k), dtype=np.float32)
+    x.reshape(-1)[::13] = 0.0
+    x.reshape(-1)[5::17] = -0.0
+    pc = torch.zeros(r, dtype=torch.int32, device="cuda")
+    got = pack_rows_device(torch.from_numpy(x).cuda(), pad_fill=pad, row_popc=pc).cpu().numpy()
+    expect = orc.pack_rows(orc.binarize(x), pad)
+    assert np.array_equal(got, expect)
+    assert np.array_equal(pc.cpu().numpy(), (x >= 0).sum(1))

@@ -1,0 +1,25 @@
+"""Host<->device copy bandwidth: H2D alone, D2H alone, both concurrently (pinned)."""
+import torch
+n = 25690112 // 4
+h_in = torch.empty(n, dtype=torch.float32).pin_memory()
+h_out = torch.empty(n, dtype=torch.float32).pin_memory()
+d_in = torch.empty(n, device="cuda"); d_out = torch.empty(n, device="cuda")
+s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+def t(fn, reps=10):
+    fn(); torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    e0.record()
+    for _ in range(reps): fn()
+    e1.record(); torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+def both():
+    cur = torch.cuda.current_stream()
+    s1.wait_stream(cur); s2.wait_stream(cur)
+    with torch.cuda.stream(s1): d_in.copy_(h_in, non_blocking=True)
+    with torch.cuda.stream(s2): h_out.copy_(d_out, non_blocking=True)
+    cur.wait_stream(s1); cur.wait_stream(s2)
+b = n * 4
+for name, fn in [("h2d", lambda: d_in.copy_(h_in, non_blocking=True)),
+                 ("d2h", lambda: h_out.copy_(d_out, non_blocking=True)), ("both", both)]:
+    ms = t(fn)
+    print(f"{name}: {ms:.3f} ms  {b / ms / 1e6:.1f} GB/s per direction")
