@@ -103,9 +103,10 @@ __device__ __forceinline__ void trace_at(uint64_t *buf, int slot) {
 constexpr int kWordsPerStage = 4;  // u32 words of K per row per stage
 constexpr int kRowBytes = 128;     // expanded bytes per row per stage
 
-template <int BN, bool kATmem, int kPlanes = 1, bool kTma = false>
+template <int BN, bool kATmem, int kPlanes = 1, bool kTma = false, bool kFp4 = false>
 struct Cfg {
     static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
+    static_assert(!kFp4 || (!kATmem && kPlanes == 1 && kTma), "fp4 engine: SS operands, TMA-fed");
     static constexpr int kProducers = BM + BN;                 // one thread per operand row
     static constexpr int kProducerWarps = (kProducers + 31) / 32;
     static constexpr int kTmaWarp = kProducerWarps;  // one elected lane issues the TMA loads
@@ -116,19 +117,24 @@ struct Cfg {
     // K is consumed in 128-bit stages grouped into superstages of kSub stages:
     // every barrier round trip (expanded-buffer wait, proxy fence, full arrival,
     // MMA commit) is paid once per superstage
-    static constexpr int kSub = kATmem ? 2 : 1;
+    static constexpr int kSub = (kATmem || kFp4) ? 2 : 1;
     static constexpr int PD = (kATmem && kPlanes == 1) ? 8 : 4;  // per-thread packed ring (stages)
     static_assert((PD & (PD - 1)) == 0 && PD >= 2 * kSub, "packed ring depth");
-    static constexpr int kStageA = kATmem ? 0 : BM * kRowBytes;
-    static constexpr int kStageB = BN * kRowBytes;
+    // bytes of one row per 128-bit stage: u8 expansion 128, e2m1 expansion 64 (an
+    // fp4 superstage row is one 128-byte SW128 row; A rows precede B rows)
+    static constexpr int kStageRow = kFp4 ? 64 : kRowBytes;
+    static constexpr int kStageA = kATmem ? 0 : BM * kStageRow;
+    static constexpr int kStageB = BN * kStageRow;
     static constexpr int kStageBytes = kStageA + kStageB;
     static constexpr int kSuperBytes = kSub * kStageBytes;
     static constexpr int ES = kATmem ? 2 : 3;  // expanded superstage buffers
+    static constexpr int kFp4A = BM * 128;      // fp4: A block of a superstage buffer
     // TMEM: 2 accumulator buffers of BN columns (+ ES x kSub A stages of 32 columns)
     static constexpr int kAccCols = BN;
     static constexpr int kAStageCol = 2 * BN;
     static constexpr int kTmemCols = 512;
-    static_assert(2 * BN + (kATmem ? ES * kSub * 32 : 0) <= 512, "TMEM budget");
+    static constexpr int kSfCol = 2 * BN;       // fp4: UE8M0 scale factors (all 1.0) from here
+    static_assert(2 * BN + (kATmem ? ES * kSub * 32 : 0) + (kFp4 ? 64 : 0) <= 512, "TMEM budget");
     // shared memory carve-up (offsets from the 1024-aligned base)
     // epilogue staging: per warp 32 rows x 32 f32, row pitch 144 B (16 B of
     // padding keeps both the row writes and the transposed reads conflict-free)
@@ -153,6 +159,9 @@ struct Cfg {
     static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
     static constexpr uint32_t kIdesc = (2u << 4) | (0u << 7) | (0u << 10) |
                                        ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+    // kind::mxf4: E2M1 x E2M1 (format 1), UE8M0 scales (bit 23), f32 accumulate
+    static constexpr uint32_t kIdescFp4 = (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                                          (1u << 23) | ((uint32_t)(BM >> 4) << 24);
 };
 
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
@@ -310,6 +319,35 @@ __device__ __forceinline__ void expand8(uint32_t w, uint32_t (&r)[8]) {
     for (int i = 0; i < 8; ++i) r[i] = kIsA ? (w & (0x80808080u >> i)) : (w & (0x01010101u << i));
 }
 
+// e2m1 (fp4) expansion, 8 nibbles per register: register r, nibble n <- bit 4n + r
+// of the word, as codes whose values multiply to 1 for every (A, B) pair of set
+// bits, so the f32 accumulator is popc(a & b) exactly:
+//     B: bit 4n+r -> 0.5, 1, 2, 2    A: bit 4n+r -> 2, 1, 0.5, 0.5
+// (e2m1 codes 1 = 0.5, 2 = 1.0, 4 = 2.0); one or two ALU ops per register
+__device__ __forceinline__ void expand_fp4_b(uint32_t w, uint32_t (&r)[4]) {
+    r[0] = w & 0x11111111u;
+    r[1] = w & 0x22222222u;
+    r[2] = w & 0x44444444u;
+    r[3] = (w >> 1) & 0x44444444u;
+}
+__device__ __forceinline__ void expand_fp4_a(uint32_t w, uint32_t (&r)[4]) {
+    r[0] = (w << 2) & 0x44444444u;
+    r[1] = w & 0x22222222u;
+    r[2] = (w >> 2) & 0x11111111u;
+    r[3] = (w >> 3) & 0x11111111u;
+}
+
+template <uint32_t kIdesc>
+__device__ __forceinline__ void mma_fp4(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                        uint32_t sfa, uint32_t sfb, uint32_t accumulate) {
+    asm volatile(
+        "{\n.reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n}\n" ::"r"(
+            tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate), "r"(sfa), "r"(sfb));
+}
+
 // two bit planes -> u8 codes 0..3 (same K permutation as expand8; no scaling:
 // the MMA then accumulates sum(code_a * code_b) directly)
 __device__ __forceinline__ void expand_code2(uint32_t w0, uint32_t w1, uint32_t (&r)[8]) {
@@ -344,8 +382,9 @@ struct is_tma<TmaRows> { static constexpr bool value = true; };
 template <>
 struct is_tma<TmaConv> { static constexpr bool value = true; };
 
-template <int BN, bool kATmem, int kVec, class ALoad, class BLoad, class Store, int kPlanes = 1>
-__global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value>::kThreads, 1)
+template <int BN, bool kATmem, int kVec, class ALoad, class BLoad, class Store, int kPlanes = 1,
+          bool kFp4 = false>
+__global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value, kFp4>::kThreads, 1)
     xnor_umma_kernel(const __grid_constant__ ALoad aload, const __grid_constant__ BLoad bload,
                      Store store, Epilogue ep, int64_t kw32, TileMap tmap, uint64_t *trace_buf,
                      int dbg) {
@@ -357,7 +396,7 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value>
     };
     constexpr bool kTma = is_tma<ALoad>::value;
     static_assert(kTma == is_tma<BLoad>::value && (!kTma || kPlanes == 1), "TMA: both operands");
-    using C = Cfg<BN, kATmem, kPlanes, kTma>;
+    using C = Cfg<BN, kATmem, kPlanes, kTma, kFp4>;
     constexpr int ES = C::ES;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t sbase_raw = smem_u32(smem_raw);
@@ -411,6 +450,19 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value>
 
     if (warp < C::kProducerWarps) {
         // ================================================================ producers
+        if constexpr (kFp4) {
+            // UE8M0 block scales = 2^0 in every TMEM column from kSfCol on (both
+            // operands' scale vectors point there); ordered before the MMAs by the
+            // first full[] arrival of these warps
+            if (warp < 4) {
+                const uint32_t one[8] = {0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu,
+                                         0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu};
+                for (int col = C::kSfCol; col < C::kTmemCols; col += 8)
+                    tmem_st8(tmem + ((uint32_t)(warp * 32) << 16) + col, one);
+                asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+                fence_before();
+            }
+        }
         const bool is_a = tid < BM;
         const bool active = tid < C::kProducers;  // the last warp may be partly idle
         const int row = is_a ? tid : tid - BM;
@@ -548,9 +600,31 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value>
                 const int sb = (int)(gs % ES);
                 if (gs >= ES) mbar_wait(bar_empty + 8 * sb, ((gs / ES) - 1) & 1u);
                 if (lane == 0 && (warp == 0 || warp == C::kProducerWarps - 1)) tr(warp ? 4 : 1, gs);
+                if constexpr (kFp4) {
+                    // one 128-byte SW128 row per superstage: word q (stage q / 4) -> chunk q
+                    const uint32_t row_base = s_exp + sb * C::kSuperBytes +
+                                              (is_a ? row * 128 : C::kFp4A + row * 128);
+#pragma unroll
+                    for (uint32_t u = 0; u < kSub; ++u) {
+                        if (u >= nsub || !active) break;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const uint32_t w = wv[u][j];
+                            my_popc += __popc(w);
+                            uint32_t r4[4];
+                            if (is_a) expand_fp4_a(w, r4);
+                            else expand_fp4_b(w, r4);
+                            const int q = 4 * (int)u + j;
+                            if (!(dbg & 1))
+                                asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};\n" ::"r"(
+                                                 row_base + ((q ^ (row & 7)) << 4)),
+                                             "r"(r4[0]), "r"(r4[1]), "r"(r4[2]), "r"(r4[3]));
+                        }
+                    }
+                }
 #pragma unroll
                 for (uint32_t u = 0; u < kSub; ++u) {
-                    if (u >= nsub || !active) break;
+                    if (kFp4 || u >= nsub || !active) break;
                     const uint32_t stage = s_exp + sb * C::kSuperBytes + u * C::kStageBytes;
                     if (is_a) {
                         if constexpr (kATmem) {
@@ -604,7 +678,8 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value>
             const int buf = it & 1;
             if (it >= 2) mbar_wait(bar_tempty + 8 * buf, (uint32_t)((it >> 1) - 1) & 1u);
             if (is_a) s_popc_a[buf * BM + row] = my_popc;
-            else if (active) s_popc_b[buf * BN + row] = my_popc;
+            else if (active)  // (f32 bits on the fp4 engine, whose epilogue decodes in f32)
+                s_popc_b[buf * BN + row] = kFp4 ? __float_as_int((float)my_popc) : my_popc;
             __syncwarp();
             if (lane == 0) mbar_arrive(bar_pfull + 8 * buf);
         }
@@ -677,9 +752,22 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value>
                     tr(7, gs);
                     if (gs == 0) trace(2);
                     fence_after();
+                    if constexpr (kFp4) {
+                        // K = 64 e2m1 per MMA = 32 bytes of the superstage row
+                        const uint32_t a_addr = s_exp + sb * C::kSuperBytes;
+                        const uint32_t b_addr = a_addr + C::kFp4A;
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk) {
+                            if ((dbg & 2) || kk >= 2 * (int)nsub) break;
+                            const uint32_t acc = (kt | kk) != 0 ? 1u : 0u;
+                            mma_fp4<C::kIdescFp4>(d, sw128_desc(a_addr + kk * 32),
+                                                  sw128_desc(b_addr + kk * 32), tmem + C::kSfCol,
+                                                  tmem + C::kSfCol, acc);
+                        }
+                    }
 #pragma unroll
                     for (uint32_t u = 0; u < kSub; ++u) {
-                        if (u >= nsub) break;
+                        if (kFp4 || u >= nsub) break;
                         const uint32_t stage = s_exp + sb * C::kSuperBytes + u * C::kStageBytes;
                         const uint32_t b_addr = stage + C::kStageA;
 #pragma unroll
@@ -726,7 +814,7 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value>
         const bool affine = ep.scale || ep.shift;
         const bool dot = ep.domain == BNN_DOT;
         const bool magic = ep.k_logical < (1 << 21);  // int -> f32 via the 2^23 trick
-        const bool plain = magic && !affine && ep.bn_mean == nullptr;  // straight-line decode
+        const bool plain = (magic || kFp4) && !affine && ep.bn_mean == nullptr;  // straight-line decode
         int it = 0;
 #pragma unroll 1
         for (int tile = blockIdx.x; tile < tmap.ntiles; tile += gridDim.x, ++it) {
@@ -744,6 +832,8 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value>
             const int32_t kb = ep.k_eff - s_popc_a[buf * BM + q * 32 + lane];
             const int32_t rowc = (dot ? 2 * kb - ep.k_logical : kb) + 0x4B400000;
             const uint32_t vsh = dot ? 5u : 6u, psh = dot ? 1u : 0u;
+            const float rowf = (float)(dot ? 2 * kb - ep.k_logical : kb);  // fp4 decode
+            const float cmul = dot ? 4.0f : 2.0f, pmul = dot ? 2.0f : 1.0f;
             // multi-bit decode constants (kPlanes == 2): s_popc_* hold code sums
             const int32_t abab = ep.a_alpha * ep.b_alpha;
             const int32_t rowterm = ep.a_alpha * ep.b_beta * s_popc_a[buf * BM + q * 32 + lane] +
@@ -783,6 +873,25 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value>
                             const int32_t num = abab * (int32_t)v[4 * j4 + i] + rowterm +
                                                 ep.a_beta * ep.b_alpha * pbv[i];
                             f[4 * j4 + i] = __fmul_rn((float)num, ep.inv_gamma);
+                        }
+                    }
+                } else if (kFp4) {
+                    // f32 accumulator C = popc(a & b): P = kb - pb + 2C, or 2P - K =
+                    // (2kb - K) - 2pb + 4C, every term an exact f32 integer
+#pragma unroll
+                    for (int j4 = 0; j4 < 8; ++j4) {
+                        const float4 pb4 = *reinterpret_cast<const float4 *>(pb + c * 32 + 4 * j4);
+                        const float pbv[4] = {pb4.x, pb4.y, pb4.z, pb4.w};
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            float x = __fmaf_rn(cmul, __uint_as_float(v[4 * j4 + i]),
+                                                __fmaf_rn(-pmul, pbv[i], rowf));
+                            if (!plain) {
+                                if (affine) x = __fadd_rn(__fmul_rn(x, sc), sh);
+                                if (has_bn)
+                                    x = __fadd_rn(__fmul_rn(bg, __fmul_rn(__fsub_rn(x, bm), bi)), bb);
+                            }
+                            f[4 * j4 + i] = x;
                         }
                     }
                 } else if (plain) {
@@ -986,12 +1095,13 @@ static int encode_conv(TmaConv &t, int box_words, int box_pixels, int64_t B) {
     return BNN_OK;
 }
 
-template <int BN, bool kATmem, int kVec, class ALoad, class BLoad, class Store, int kPlanes = 1>
+template <int BN, bool kATmem, int kVec, class ALoad, class BLoad, class Store, int kPlanes = 1,
+          bool kFp4 = false>
 static int launch_umma_cfg(const ALoad &a_in, const BLoad &b_in, const Store &st, const Epilogue &ep,
                            int64_t M, int64_t N, int64_t kw32, cudaStream_t s) {
     constexpr bool kTma = umma::is_tma<ALoad>::value;
-    using C = umma::Cfg<BN, kATmem, kPlanes, kTma>;
-    auto kern = umma::xnor_umma_kernel<BN, kATmem, kVec, ALoad, BLoad, Store, kPlanes>;
+    using C = umma::Cfg<BN, kATmem, kPlanes, kTma, kFp4>;
+    auto kern = umma::xnor_umma_kernel<BN, kATmem, kVec, ALoad, BLoad, Store, kPlanes, kFp4>;
     ALoad a = a_in;
     BLoad b = b_in;
     if constexpr (kTma) {
@@ -1020,20 +1130,35 @@ static int launch_umma_cfg(const ALoad &a_in, const BLoad &b_in, const Store &st
 }
 
 // engine variants (bnn_set_umma_variant / env BNN_UMMA_VARIANT):
-//   0: 128x256 tiles, A and B through SMEM
-//   1: A in TMEM, B through SMEM, tile N chosen per shape from {128, 160, 176, 192}
-//      to minimise (waves x N) on the SMs of this GPU
+//   0: 128x256 tiles, u8 expansion, A and B through SMEM (kind::i8)
+//   1: u8 expansion, A in TMEM, B through SMEM (kind::i8), tile N chosen per shape
+//      from {128, 160, 176, 192} to minimise (waves x N) on the SMs of this GPU
+//   2: e2m1 expansion, A and B through SMEM (kind::mxf4, 2x the i8 MMA rate and
+//      half the expanded bytes) for TMA-fed operands, tile N from {128 .. 224};
+//      cp.async-fed shapes fall back to variant 1
 int g_umma_variant = -1;
 static int umma_variant() {
     if (g_umma_variant < 0) {
         const char *e = getenv("BNN_UMMA_VARIANT");
-        g_umma_variant = e ? atoi(e) : 1;
+        g_umma_variant = e ? atoi(e) : 2;
     }
     return g_umma_variant;
 }
 
-static int choose_bn(int64_t M, int64_t N) {
+static int choose_bn(int64_t M, int64_t N, bool fp4 = false) {
     static const int cands[] = {192, 176, 160, 128};
+    static const int cands4[] = {224, 208, 192, 176, 160, 128};
+    if (fp4) {
+        const int64_t sms = sm_count(), tm = ceil_div(M, umma::BM);
+        int best = 192;
+        int64_t best_cost = -1;
+        for (int bn : cands4) {
+            const int64_t waves = ceil_div(tm * ceil_div(N, bn), sms);
+            const int64_t cost = waves * (bn + 32);
+            if (best_cost < 0 || cost < best_cost) best = bn, best_cost = cost;
+        }
+        return best;
+    }
     const int64_t sms = sm_count(), tm = ceil_div(M, umma::BM);
     int best = 192;
     int64_t best_cost = -1;
@@ -1050,6 +1175,19 @@ static int launch_umma(const ALoad &a, const BLoad &b, const Store &st, const Ep
                        int64_t M, int64_t N, int64_t kw32, cudaStream_t s) {
     if constexpr (!std::is_same<BLoad, TmaConv>::value)
         if (umma_variant() == 0) return launch_umma_cfg<256, false, kVec>(a, b, st, ep, M, N, kw32, s);
+    if constexpr (umma::is_tma<ALoad>::value) {
+        if (umma_variant() == 2) {
+            using S = Store;
+            switch (choose_bn(M, N, true)) {
+                case 128: return launch_umma_cfg<128, false, 4, ALoad, BLoad, S, 1, true>(a, b, st, ep, M, N, kw32, s);
+                case 160: return launch_umma_cfg<160, false, 4, ALoad, BLoad, S, 1, true>(a, b, st, ep, M, N, kw32, s);
+                case 176: return launch_umma_cfg<176, false, 4, ALoad, BLoad, S, 1, true>(a, b, st, ep, M, N, kw32, s);
+                case 192: return launch_umma_cfg<192, false, 4, ALoad, BLoad, S, 1, true>(a, b, st, ep, M, N, kw32, s);
+                case 208: return launch_umma_cfg<208, false, 4, ALoad, BLoad, S, 1, true>(a, b, st, ep, M, N, kw32, s);
+                default: return launch_umma_cfg<224, false, 4, ALoad, BLoad, S, 1, true>(a, b, st, ep, M, N, kw32, s);
+            }
+        }
+    }
     switch (choose_bn(M, N)) {
         case 128: return launch_umma_cfg<128, true, kVec>(a, b, st, ep, M, N, kw32, s);
         case 160: return launch_umma_cfg<160, true, kVec>(a, b, st, ep, M, N, kw32, s);
@@ -1116,7 +1254,7 @@ int launch_bconv2d_umma(const uint64_t *x, int64_t B, int64_t C, int64_t H, int6
     // im2col TMA: whole 32-byte tap chunks (C % 256 == 0), corner offsets and
     // strides within the tensor-map limits, A-in-TMEM engine (superstages of 2)
     const int64_t up_w = (ow - 1) * sw - pw - (W - 1), up_h = (oh - 1) * sh - ph - (H - 1);
-    const bool im2col = vec4 && cs32 % 8 == 0 && umma_variant() == 1 && !(umma_dbg() & 256) &&
+    const bool im2col = vec4 && cs32 % 8 == 0 && umma_variant() >= 1 && !(umma_dbg() & 256) &&
                         ph <= 128 && pw <= 128 && up_w >= -128 && up_w <= 127 && up_h >= -128 &&
                         up_h <= 127 && sh <= 8 && sw <= 8 && kh <= 128 && kw <= 128;
     if (im2col) {
@@ -1141,7 +1279,7 @@ extern "C" int bnn_umma_trace(uint64_t *buf) {
 }
 
 extern "C" int bnn_set_umma_variant(int v) {
-    if (v < 0 || v > 1) return bnn::set_error(BNN_EINVAL, "umma variant must be 0 or 1");
+    if (v < 0 || v > 2) return bnn::set_error(BNN_EINVAL, "umma variant must be 0, 1 or 2");
     bnn::g_umma_variant = v;
     return BNN_OK;
 }

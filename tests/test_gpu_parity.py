@@ -19,7 +19,7 @@ from oracle import oracle as orc
 
 pytestmark = pytest.mark.gpu
 
-ALGOS = ["popc", "bmma", "umma0", "umma1"]
+ALGOS = ["popc", "bmma", "umma0", "umma1", "umma2"]
 
 
 def A(algo):
@@ -255,7 +255,7 @@ def test_conv_im2col_route_matches_oracle(bnn, case):
     b, c, h, w, f, kh, kw, stride, pad, seed = case
     x, wt = wl.conv_case_inputs(case)
     expect = orc.qconv_packed(x, wt, stride, pad)
-    for algo in ("umma1", "umma0", "popc"):
+    for algo in ("umma2", "umma1", "umma0", "popc"):
         layer = bnn.QConvolution(c, f, (kh, kw), stride, pad)
         layer.weight = wt
         layer.pack()
@@ -460,7 +460,7 @@ def test_qfullyconnected_2bit_packed_equals_float_path(bnn):
         q.forward(x, bnn.INFER_PACKED)
 
 
-@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("variant", [0, 1, 2])
 def test_umma_repeat_runs_identical(bnn, variant):
     """Pipeline-race guard: repeated launches of the TMA-fed tcgen05 engine on a
     many-tile shape equal the CUDA-core engine every time (a slot released
@@ -474,7 +474,7 @@ def test_umma_repeat_runs_identical(bnn, variant):
     _lib.call("bnn_set_umma_variant", variant)
     for _ in range(12):
         assert torch.equal(bnn.xnor_rows_gemm(a, b, k, algo="umma"), ref)
-    _lib.call("bnn_set_umma_variant", 1)
+    _lib.call("bnn_set_umma_variant", 2)
 
 
 @pytest.mark.parametrize("which", ["conv", "dense"])

@@ -13,7 +13,7 @@ for m, n, k in shapes:
     a = torch.randint(-2**63, 2**63 - 1, (m, W), device="cuda", generator=g).view(torch.uint64)
     b = torch.randint(-2**63, 2**63 - 1, (n, W), device="cuda", generator=g).view(torch.uint64)
     ref = bnn.xnor_rows_gemm(a, b, k, algo="popc")
-    for v in (0, 1):
+    for v in (0, 1, 2):
         _lib.call("bnn_set_umma_variant", v)
         bad = 0
         for r in range(reps):
