@@ -510,179 +510,187 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
         }
 
         constexpr uint32_t kSub = C::kSub;
-        uint32_t gk = 0;  // global stage counter (packed ring)
-        uint32_t gs = 0;  // global superstage counter (expanded buffers / phases)
-        int it = 0;
-#pragma unroll 1
-        for (int tile = blockIdx.x; tile < tmap.ntiles; tile += gridDim.x, ++it) {
-            int32_t my_popc = 0;
-            // im2col route: this B row's window corner and the running tap
-            int c_iy0 = 0, c_ix0 = 0, c_cw = 0, c_i = 0, c_j = 0;
-            if constexpr (std::is_same<BLoad, TmaConv>::value) {
-                int tm, tn;
-                tmap.decode(tile, tm, tn);
-                const int64_t ohw = (int64_t)bload.oh * bload.ow;
-                const int64_t n = (int64_t)tn * BN + (is_a ? 0 : row);
-                const int p = (int)(n % ohw);
-                c_iy0 = (p / bload.ow) * bload.sh - bload.ph;
-                c_ix0 = (p % bload.ow) * bload.sw - bload.pw;
-            }
-#pragma unroll 1
-            for (uint32_t kt = 0; kt < kt32; kt += kSub, ++gs) {
-                const uint32_t nsub = kt32 - kt < kSub ? kt32 - kt : kSub;
-                uint32_t wv[kSub][4], wv1[kSub][4] = {};
-                if constexpr (kTma) {
-                    // this superstage's packed rows, landed by the TMA warp
-                    const uint32_t ts = gs % C::kTmaSlots;
-                    mbar_wait(bar_ld + 8 * ts, (gs / C::kTmaSlots) & 1u);
-                    if (lane == 0 && (warp == 0 || warp == C::kProducerWarps - 1)) tr(warp ? 6 : 3, gs);
-                    const uint32_t rbase = s_pk + ts * C::kTmaSlotBytes +
-                                           (is_a ? row * kSub * 16 : C::kTmaA + row * kSub * 16);
-#pragma unroll
-                    for (uint32_t u = 0; u < kSub; ++u) {
-                        // SWIZZLE_32B (kSub == 2): 16-B chunk u of row r sits at u ^ bit 2 of r
-                        const uint32_t a = rbase + (kSub == 2 ? ((u ^ ((row >> 2) & 1)) * 16) : 0);
-                        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n"
-                                     : "=r"(wv[u][0]), "=r"(wv[u][1]), "=r"(wv[u][2]), "=r"(wv[u][3])
-                                     : "r"(a)
-                                     : "memory");
-                    }
-                    if constexpr (std::is_same<BLoad, TmaConv>::value) {
-                        // padding: this pixel's window tap outside the image reads as +1
-                        if (!is_a) {
-                            const bool oob = (unsigned)(c_iy0 + c_i) >= (unsigned)bload.H ||
-                                             (unsigned)(c_ix0 + c_j) >= (unsigned)bload.W;
-#pragma unroll
-                            for (uint32_t u = 0; u < kSub; ++u)
-#pragma unroll
-                                for (int q = 0; q < 4; ++q)
-                                    if (oob) wv[u][q] = 0xffffffffu;
-                        }
-                        c_cw += 4 * kSub;
-                        if (c_cw == bload.cs32) {
-                            c_cw = 0;
-                            if (++c_j == bload.kw) c_j = 0, ++c_i;
-                        }
-                    }
-                } else {
-                    // keep PD - kSub stages in flight beyond this superstage
-#pragma unroll
-                    for (uint32_t u = 0; u < kSub; ++u)
-                        if (u < nsub) fetch_next();
-                    if (lane == 0 && warp == C::kProducerWarps - 1) tr(0, gs);
-                    cp_async_wait<C::PD - C::kSub>();
-                    if (lane == 0 && (warp == 0 || warp == C::kProducerWarps - 1)) tr(warp ? 6 : 3, gs);
-#pragma unroll
-                    for (uint32_t u = 0; u < kSub; ++u) {
-                        if (u >= nsub) break;
-                        const uint32_t slot = ring + ((gk + u) & (C::PD - 1)) * kRingSlot;
-                        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n"
-                                     : "=r"(wv[u][0]), "=r"(wv[u][1]), "=r"(wv[u][2]), "=r"(wv[u][3])
-                                     : "r"(slot));
-                        if constexpr (kPlanes == 2)
+        // the operand role is warp-uniform (warps 0..3 = A rows, the rest B rows):
+        // instantiate the pipeline loop per role so neither role executes the
+        // other's (if-converted) expansion code
+        auto run = [&](auto role) {
+            constexpr bool is_a = decltype(role)::value;
+            uint32_t gk = 0;  // global stage counter (packed ring)
+            uint32_t gs = 0;  // global superstage counter (expanded buffers / phases)
+            int it = 0;
+    #pragma unroll 1
+            for (int tile = blockIdx.x; tile < tmap.ntiles; tile += gridDim.x, ++it) {
+                int32_t my_popc = 0;
+                // im2col route: this B row's window corner and the running tap
+                int c_iy0 = 0, c_ix0 = 0, c_cw = 0, c_i = 0, c_j = 0;
+                if constexpr (std::is_same<BLoad, TmaConv>::value) {
+                    int tm, tn;
+                    tmap.decode(tile, tm, tn);
+                    const int64_t ohw = (int64_t)bload.oh * bload.ow;
+                    const int64_t n = (int64_t)tn * BN + (is_a ? 0 : row);
+                    const int p = (int)(n % ohw);
+                    c_iy0 = (p / bload.ow) * bload.sh - bload.ph;
+                    c_ix0 = (p % bload.ow) * bload.sw - bload.pw;
+                }
+    #pragma unroll 1
+                for (uint32_t kt = 0; kt < kt32; kt += kSub, ++gs) {
+                    const uint32_t nsub = kt32 - kt < kSub ? kt32 - kt : kSub;
+                    uint32_t wv[kSub][4], wv1[kSub][4] = {};
+                    if constexpr (kTma) {
+                        // this superstage's packed rows, landed by the TMA warp
+                        const uint32_t ts = gs % C::kTmaSlots;
+                        mbar_wait(bar_ld + 8 * ts, (gs / C::kTmaSlots) & 1u);
+                        if (lane == 0 && (warp == 0 || warp == C::kProducerWarps - 1)) tr(warp ? 6 : 3, gs);
+                        const uint32_t rbase = s_pk + ts * C::kTmaSlotBytes +
+                                               (is_a ? row * kSub * 16 : C::kTmaA + row * kSub * 16);
+    #pragma unroll
+                        for (uint32_t u = 0; u < kSub; ++u) {
+                            // SWIZZLE_32B (kSub == 2): 16-B chunk u of row r sits at u ^ bit 2 of r
+                            const uint32_t a = rbase + (kSub == 2 ? ((u ^ ((row >> 2) & 1)) * 16) : 0);
                             asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n"
-                                         : "=r"(wv1[u][0]), "=r"(wv1[u][1]), "=r"(wv1[u][2]),
-                                           "=r"(wv1[u][3])
-                                         : "r"(slot + 16));
-                    }
-                }
-                // expanded registers of word q of stage u for this operand side
-                auto expand = [&](uint32_t u, int q, bool as_a, uint32_t (&r)[8]) {
-                    if constexpr (kPlanes == 2) {
-                        my_popc += __popc(wv[u][q]) + 2 * __popc(wv1[u][q]);  // code sum
-                        expand_code2(wv[u][q], wv1[u][q], r);
+                                         : "=r"(wv[u][0]), "=r"(wv[u][1]), "=r"(wv[u][2]), "=r"(wv[u][3])
+                                         : "r"(a)
+                                         : "memory");
+                        }
+                        if constexpr (std::is_same<BLoad, TmaConv>::value) {
+                            // padding: this pixel's window tap outside the image reads as +1
+                            if (!is_a) {
+                                const bool oob = (unsigned)(c_iy0 + c_i) >= (unsigned)bload.H ||
+                                                 (unsigned)(c_ix0 + c_j) >= (unsigned)bload.W;
+    #pragma unroll
+                                for (uint32_t u = 0; u < kSub; ++u)
+    #pragma unroll
+                                    for (int q = 0; q < 4; ++q)
+                                        if (oob) wv[u][q] = 0xffffffffu;
+                            }
+                            c_cw += 4 * kSub;
+                            if (c_cw == bload.cs32) {
+                                c_cw = 0;
+                                if (++c_j == bload.kw) c_j = 0, ++c_i;
+                            }
+                        }
                     } else {
-                        my_popc += __popc(wv[u][q]);
-                        if (as_a) expand8<true>(wv[u][q], r);
-                        else expand8<false>(wv[u][q], r);
-                    }
-                };
-                const int sb = (int)(gs % ES);
-                if (gs >= ES) mbar_wait(bar_empty + 8 * sb, ((gs / ES) - 1) & 1u);
-                if (lane == 0 && (warp == 0 || warp == C::kProducerWarps - 1)) tr(warp ? 4 : 1, gs);
-                if constexpr (kFp4) {
-                    // one 128-byte SW128 row per superstage: word q (stage q / 4) -> chunk q
-                    const uint32_t row_base = s_exp + sb * C::kSuperBytes +
-                                              (is_a ? row * 128 : C::kFp4A + row * 128);
-#pragma unroll
-                    for (uint32_t u = 0; u < kSub; ++u) {
-                        if (u >= nsub || !active) break;
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            const uint32_t w = wv[u][j];
-                            my_popc += __popc(w);
-                            uint32_t r4[4];
-                            if (is_a) expand_fp4_a(w, r4);
-                            else expand_fp4_b(w, r4);
-                            const int q = 4 * (int)u + j;
-                            if (!(dbg & 1))
-                                asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};\n" ::"r"(
-                                                 row_base + ((q ^ (row & 7)) << 4)),
-                                             "r"(r4[0]), "r"(r4[1]), "r"(r4[2]), "r"(r4[3]));
+                        // keep PD - kSub stages in flight beyond this superstage
+    #pragma unroll
+                        for (uint32_t u = 0; u < kSub; ++u)
+                            if (u < nsub) fetch_next();
+                        if (lane == 0 && warp == C::kProducerWarps - 1) tr(0, gs);
+                        cp_async_wait<C::PD - C::kSub>();
+                        if (lane == 0 && (warp == 0 || warp == C::kProducerWarps - 1)) tr(warp ? 6 : 3, gs);
+    #pragma unroll
+                        for (uint32_t u = 0; u < kSub; ++u) {
+                            if (u >= nsub) break;
+                            const uint32_t slot = ring + ((gk + u) & (C::PD - 1)) * kRingSlot;
+                            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n"
+                                         : "=r"(wv[u][0]), "=r"(wv[u][1]), "=r"(wv[u][2]), "=r"(wv[u][3])
+                                         : "r"(slot));
+                            if constexpr (kPlanes == 2)
+                                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n"
+                                             : "=r"(wv1[u][0]), "=r"(wv1[u][1]), "=r"(wv1[u][2]),
+                                               "=r"(wv1[u][3])
+                                             : "r"(slot + 16));
                         }
                     }
-                }
-#pragma unroll
-                for (uint32_t u = 0; u < kSub; ++u) {
-                    if (kFp4 || u >= nsub || !active) break;
-                    const uint32_t stage = s_exp + sb * C::kSuperBytes + u * C::kStageBytes;
-                    if (is_a) {
-                        if constexpr (kATmem) {
-                            // warps 0..3 own TMEM lanes 0..127 = A rows 0..127
-                            const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) +
-                                                   C::kAStageCol + (sb * kSub + u) * 32;
-#pragma unroll
-                            for (int q = 0; q < 4; ++q) {
-                                uint32_t r[8];
-                                expand(u, q, true, r);
-                                if (!(dbg & 4)) tmem_st8(taddr + q * 8, r);
+                    // expanded registers of word q of stage u for this operand side
+                    auto expand = [&](uint32_t u, int q, bool as_a, uint32_t (&r)[8]) {
+                        if constexpr (kPlanes == 2) {
+                            my_popc += __popc(wv[u][q]) + 2 * __popc(wv1[u][q]);  // code sum
+                            expand_code2(wv[u][q], wv1[u][q], r);
+                        } else {
+                            my_popc += __popc(wv[u][q]);
+                            if (as_a) expand8<true>(wv[u][q], r);
+                            else expand8<false>(wv[u][q], r);
+                        }
+                    };
+                    const int sb = (int)(gs % ES);
+                    if (gs >= ES) mbar_wait(bar_empty + 8 * sb, ((gs / ES) - 1) & 1u);
+                    if (lane == 0 && (warp == 0 || warp == C::kProducerWarps - 1)) tr(warp ? 4 : 1, gs);
+                    if constexpr (kFp4) {
+                        // one 128-byte SW128 row per superstage: word q (stage q / 4) -> chunk q
+                        const uint32_t row_base = s_exp + sb * C::kSuperBytes +
+                                                  (is_a ? row * 128 : C::kFp4A + row * 128);
+    #pragma unroll
+                        for (uint32_t u = 0; u < kSub; ++u) {
+                            if (u >= nsub || !active) break;
+    #pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                const uint32_t w = wv[u][j];
+                                my_popc += __popc(w);
+                                uint32_t r4[4];
+                                if (is_a) expand_fp4_a(w, r4);
+                                else expand_fp4_b(w, r4);
+                                const int q = 4 * (int)u + j;
+                                if (!(dbg & 1))
+                                    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};\n" ::"r"(
+                                                     row_base + ((q ^ (row & 7)) << 4)),
+                                                 "r"(r4[0]), "r"(r4[1]), "r"(r4[2]), "r"(r4[3]));
+                            }
+                        }
+                    }
+    #pragma unroll
+                    for (uint32_t u = 0; u < kSub; ++u) {
+                        if (kFp4 || u >= nsub || !active) break;
+                        const uint32_t stage = s_exp + sb * C::kSuperBytes + u * C::kStageBytes;
+                        if (is_a) {
+                            if constexpr (kATmem) {
+                                // warps 0..3 own TMEM lanes 0..127 = A rows 0..127
+                                const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) +
+                                                       C::kAStageCol + (sb * kSub + u) * 32;
+    #pragma unroll
+                                for (int q = 0; q < 4; ++q) {
+                                    uint32_t r[8];
+                                    expand(u, q, true, r);
+                                    if (!(dbg & 4)) tmem_st8(taddr + q * 8, r);
+                                }
+                            } else {
+                                const uint32_t row_base = stage + row * kRowBytes;
+    #pragma unroll
+                                for (int q = 0; q < 4; ++q) {
+                                    uint32_t r[8];
+                                    expand(u, q, true, r);
+                                    store_row32(r, row_base, row, q);
+                                }
                             }
                         } else {
-                            const uint32_t row_base = stage + row * kRowBytes;
-#pragma unroll
+                            const uint32_t row_base = stage + C::kStageA + row * kRowBytes;
+    #pragma unroll
                             for (int q = 0; q < 4; ++q) {
                                 uint32_t r[8];
-                                expand(u, q, true, r);
-                                store_row32(r, row_base, row, q);
+                                expand(u, q, false, r);
+                                if (!(dbg & 1)) store_row32(r, row_base, row, q);
+                                else if (r[0] == 0x12345678u && r[7] == 0x9abcdef0u) store_row32(r, row_base, row, q);
                             }
                         }
-                    } else {
-                        const uint32_t row_base = stage + C::kStageA + row * kRowBytes;
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            uint32_t r[8];
-                            expand(u, q, false, r);
-                            if (!(dbg & 1)) store_row32(r, row_base, row, q);
-                            else if (r[0] == 0x12345678u && r[7] == 0x9abcdef0u) store_row32(r, row_base, row, q);
-                        }
                     }
+                    if (kATmem && is_a) {
+                        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+                        fence_before();
+                    } else {
+                        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                    }
+                    __syncwarp();  // every lane's writes + fence precede the warp's arrival
+                    if (lane == 0 && (warp == 0 || warp == C::kProducerWarps - 1)) tr(warp ? 5 : 2, gs);
+                    if (lane == 0) {
+                        mbar_arrive(bar_full + 8 * sb);
+                        // release the TMA slot only now: every lane's ld.shared result has
+                        // been consumed by the expansion above (in-order issue), so the
+                        // next TMA write into the slot cannot overtake a pending read
+                        if constexpr (kTma) mbar_arrive(bar_free + 8 * ((gs % C::kTmaSlots)));
+                    }
+                    gk += nsub;
                 }
-                if (kATmem && is_a) {
-                    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
-                    fence_before();
-                } else {
-                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-                }
-                __syncwarp();  // every lane's writes + fence precede the warp's arrival
-                if (lane == 0 && (warp == 0 || warp == C::kProducerWarps - 1)) tr(warp ? 5 : 2, gs);
-                if (lane == 0) {
-                    mbar_arrive(bar_full + 8 * sb);
-                    // release the TMA slot only now: every lane's ld.shared result has
-                    // been consumed by the expansion above (in-order issue), so the
-                    // next TMA write into the slot cannot overtake a pending read
-                    if constexpr (kTma) mbar_arrive(bar_free + 8 * ((gs % C::kTmaSlots)));
-                }
-                gk += nsub;
+                // hand this tile's row popcounts to the epilogue (double-buffered)
+                const int buf = it & 1;
+                if (it >= 2) mbar_wait(bar_tempty + 8 * buf, (uint32_t)((it >> 1) - 1) & 1u);
+                if (is_a) s_popc_a[buf * BM + row] = my_popc;
+                else if (active)  // (f32 bits on the fp4 engine, whose epilogue decodes in f32)
+                    s_popc_b[buf * BN + row] = kFp4 ? __float_as_int((float)my_popc) : my_popc;
+                __syncwarp();
+                if (lane == 0) mbar_arrive(bar_pfull + 8 * buf);
             }
-            // hand this tile's row popcounts to the epilogue (double-buffered)
-            const int buf = it & 1;
-            if (it >= 2) mbar_wait(bar_tempty + 8 * buf, (uint32_t)((it >> 1) - 1) & 1u);
-            if (is_a) s_popc_a[buf * BM + row] = my_popc;
-            else if (active)  // (f32 bits on the fp4 engine, whose epilogue decodes in f32)
-                s_popc_b[buf * BN + row] = kFp4 ? __float_as_int((float)my_popc) : my_popc;
-            __syncwarp();
-            if (lane == 0) mbar_arrive(bar_pfull + 8 * buf);
-        }
+        };
+        if (is_a) run(std::true_type{});
+        else run(std::false_type{});
         cp_async_wait<0>();
     } else if (warp == C::kTmaWarp) {
         // ================================================================ TMA issuer
