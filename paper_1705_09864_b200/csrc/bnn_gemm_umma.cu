@@ -170,6 +170,12 @@ __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
 }
+// arrive after `dep` has been computed (a register dependency orders it after the
+// instructions that produced dep, e.g. the consumers of a buffer being released)
+__device__ __forceinline__ void mbar_arrive_dep(uint32_t bar, int32_t dep) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n// dep %1\n" ::"r"(bar), "r"(dep)
+                 : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
                  : "memory");
@@ -569,6 +575,18 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                                 if (++c_j == bload.kw) c_j = 0, ++c_i;
                             }
                         }
+                        // row popcount now: it consumes every loaded word, so once the POPCs
+                        // have issued the slot's ld.shared data is in registers and the TMA
+                        // slot can be handed back before the expansion
+                        int32_t sp = 0;
+#pragma unroll
+                        for (uint32_t u = 0; u < kSub; ++u)
+#pragma unroll
+                            for (int q = 0; q < 4; ++q)
+                                if (u < nsub) sp += __popc(wv[u][q]);
+                        my_popc += sp;
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_dep(bar_free + 8 * ts, sp);
                     } else {
                         // keep PD - kSub stages in flight beyond this superstage
     #pragma unroll
@@ -597,7 +615,7 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                             my_popc += __popc(wv[u][q]) + 2 * __popc(wv1[u][q]);  // code sum
                             expand_code2(wv[u][q], wv1[u][q], r);
                         } else {
-                            my_popc += __popc(wv[u][q]);
+                            if constexpr (!kTma) my_popc += __popc(wv[u][q]);
                             if (as_a) expand8<true>(wv[u][q], r);
                             else expand8<false>(wv[u][q], r);
                         }
@@ -615,7 +633,6 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
     #pragma unroll
                             for (int j = 0; j < 4; ++j) {
                                 const uint32_t w = wv[u][j];
-                                my_popc += __popc(w);
                                 uint32_t r4[4];
                                 if (is_a) expand_fp4_a(w, r4);
                                 else expand_fp4_b(w, r4);
@@ -672,10 +689,6 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                     if (lane == 0 && (warp == 0 || warp == C::kProducerWarps - 1)) tr(warp ? 5 : 2, gs);
                     if (lane == 0) {
                         mbar_arrive(bar_full + 8 * sb);
-                        // release the TMA slot only now: every lane's ld.shared result has
-                        // been consumed by the expansion above (in-order issue), so the
-                        // next TMA write into the slot cannot overtake a pending read
-                        if constexpr (kTma) mbar_arrive(bar_free + 8 * ((gs % C::kTmaSlots)));
                     }
                     gk += nsub;
                 }
@@ -719,6 +732,7 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                         if (g >= (uint32_t)C::kTmaSlots)
                             mbar_wait(bar_free + 8 * ts, ((g / C::kTmaSlots) - 1) & 1u);
                         const uint32_t dst = s_pk + ts * C::kTmaSlotBytes;
+                        tr(0, g);
                         mbar_arrive_expect_tx(bar_ld + 8 * ts, C::kTmaA + C::kTmaB);
                         tma_load_2d(dst, &aload.map, (int)(kt * kWordsPerStage), tm * BM, bar_ld + 8 * ts);
                         if constexpr (std::is_same<BLoad, TmaConv>::value) {

@@ -20,7 +20,7 @@ bnn.xnor_rows_gemm(a, b, k, algo="umma", out=out)
 torch.cuda.synchronize()
 lib.bnn_umma_trace(None)
 t = tr[4096:].view(16, 256).cpu().numpy().astype(np.int64)
-names = ["-", "A_empty_ok", "A_done", "-", "B_empty_ok", "B_done", "-", "mma_full", "mma_commit"]
+names = ["tma_issue", "A_empty_ok", "A_done", "A_data", "B_empty_ok", "B_done", "B_data", "mma_full", "mma_commit"]
 t0 = t[7, 0]
 ns = (k + 127) // 128
 print("stage " + " ".join(f"{x:>10s}" for x in names))
