@@ -263,6 +263,122 @@ __global__ void __launch_bounds__(256) pack_nchw_kernel(const float *__restrict_
     flush_flags(f, flags);
 }
 
+// Direct NCHW -> packed NHWC: thread per (pixel, 64-channel word).  The 64
+// channel loads of a thread are independent and unrolled, and the 32 lanes of a
+// warp are 32 consecutive pixels, so every load instruction is one coalesced
+// 128-byte row segment and a warp keeps 64 x 128 B in flight -- the HBM-bound
+// shape of this pass (4 B read per 1/8 B written) with no shared memory and no
+// block barrier.  Channel tails (C % 64) are 0 bits, like the tiled kernel.
+template <bool kStrict>
+__global__ void __launch_bounds__(256) pack_nchw_direct_kernel(const float *__restrict__ x,
+                                                                 int64_t B, int64_t C, int64_t HW,
+                                                                 int64_t Cw,
+                                                                 uint64_t *__restrict__ out,
+                                                                 int32_t *flags) {
+    const int64_t gp = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // global pixel
+    const int64_t cw = blockIdx.y;                                      // 64-channel word
+    int f = 0;
+    if (gp < B * HW) {
+        const int64_t b = gp / HW, p = gp - b * HW;
+        const int64_t c0 = cw * 64;
+        const int nc = (int)(C - c0 < 64 ? C - c0 : 64);
+        const float *src = x + (b * C + c0) * HW + p;
+        uint32_t half[2] = {0u, 0u};
+        float nf = 0.0f;  // + v * 0 for every element: NaN iff some element is not finite
+        if (nc == 64) {
+            float v[64];
+#pragma unroll
+            for (int j = 0; j < 64; ++j) v[j] = __ldg(src + (int64_t)j * HW);
+#pragma unroll
+            for (int j = 0; j < 64; ++j) {
+                // bit = v >= 0 (sign(-0) = +1): the u32 image is > 0x80000000 only for
+                // negative values other than -0 (and negative NaNs, flagged below)
+                if (!(__float_as_uint(v[j]) > 0x80000000u)) half[j >> 5] |= 1u << (j & 31);
+                nf = __fmaf_rn(v[j], 0.0f, nf);
+                if (kStrict && v[j] != 1.0f && v[j] != -1.0f) f |= BNN_FLAG_NOTSIGN;
+            }
+        } else {
+            for (int j = 0; j < nc; ++j) {  // channel tail word: bits past C stay 0
+                const float v = __ldg(src + (int64_t)j * HW);
+                if (!(__float_as_uint(v) > 0x80000000u)) half[j >> 5] |= 1u << (j & 31);
+                nf = __fmaf_rn(v, 0.0f, nf);
+                if (kStrict && v != 1.0f && v != -1.0f) f |= BNN_FLAG_NOTSIGN;
+            }
+        }
+        if (nf != 0.0f) f |= BNN_FLAG_NONFINITE;
+        out[gp * Cw + cw] = (uint64_t)half[0] | ((uint64_t)half[1] << 32);
+    }
+    flush_flags(f, flags);
+}
+
+// NCHW -> packed NHWC for H*W % 4 == 0: a group of G = 32 / kCh adjacent lanes
+// owns one (4-pixel quad, 32-channel u32 word); each lane loads kCh channel rows
+// of the quad (16-byte loads, all issued before any is consumed) and the group
+// ORs its partial words with shuffles.  Many small independent loads per SM keep
+// HBM busy (the pass is 4 B read per 1/8 B written), at ~3 ALU ops per element.
+template <bool kStrict, int kCh>
+__global__ void __launch_bounds__(256) pack_nchw_quad_kernel(const float *__restrict__ x,
+                                                               int64_t B, int64_t C, int64_t HW,
+                                                               int64_t cs32,
+                                                               uint32_t *__restrict__ out32,
+                                                               int32_t *flags) {
+    constexpr int G = 32 / kCh;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int sub = (int)(t % G);
+    const int64_t gq = t / G;          // pixel quad
+    const int64_t wi = blockIdx.y;     // u32 word in pixel
+    int f = 0;
+    uint32_t w0 = 0, w1 = 0, w2 = 0, w3 = 0;
+    const bool ok = gq * 4 < B * HW;
+    const int64_t gp = gq * 4;
+    if (ok) {
+        const int64_t b = gp / HW, p = gp - b * HW;
+        const int64_t c0 = wi * 32 + sub * kCh;
+        const int nc = (int)(C - c0 < kCh ? (C - c0 > 0 ? C - c0 : 0) : kCh);
+        const float *src = x + (b * C + c0) * HW + p;
+        float nf = 0.0f;  // + v * 0 over every element: NaN iff one is not finite
+        float4 v[kCh];
+#pragma unroll
+        for (int j = 0; j < kCh; ++j)
+            v[j] = j < nc ? __ldg(reinterpret_cast<const float4 *>(src + (int64_t)j * HW))
+                          : make_float4(-1.0f, -1.0f, -1.0f, -1.0f);
+#pragma unroll
+        for (int j = 0; j < kCh; ++j) {
+            // bit = v >= 0 (sign(-0) = +1): u32 image > 0x80000000 only for values < 0;
+            // channels past C were loaded as -1 -> 0 bits
+            const int sh = sub * kCh + j;
+            w0 |= (__float_as_uint(v[j].x) > 0x80000000u ? 0u : 1u) << sh;
+            w1 |= (__float_as_uint(v[j].y) > 0x80000000u ? 0u : 1u) << sh;
+            w2 |= (__float_as_uint(v[j].z) > 0x80000000u ? 0u : 1u) << sh;
+            w3 |= (__float_as_uint(v[j].w) > 0x80000000u ? 0u : 1u) << sh;
+            nf = __fmaf_rn(v[j].x, 0.0f, __fmaf_rn(v[j].y, 0.0f, nf));
+            nf = __fmaf_rn(v[j].z, 0.0f, __fmaf_rn(v[j].w, 0.0f, nf));
+            if (kStrict && j < nc) {
+                const float tv[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    if (tv[i] != 1.0f && tv[i] != -1.0f) f |= BNN_FLAG_NOTSIGN;
+            }
+        }
+        if (nf != 0.0f) f |= BNN_FLAG_NONFINITE;
+    }
+#pragma unroll
+    for (int m = 1; m < G; m <<= 1) {  // OR the group's channel sub-blocks
+        w0 |= __shfl_xor_sync(0xffffffffu, w0, m);
+        w1 |= __shfl_xor_sync(0xffffffffu, w1, m);
+        w2 |= __shfl_xor_sync(0xffffffffu, w2, m);
+        w3 |= __shfl_xor_sync(0xffffffffu, w3, m);
+    }
+    if (ok && sub == 0) {
+        uint32_t *o = out32 + gp * cs32 + wi;
+        o[0] = w0;
+        o[cs32] = w1;
+        o[2 * cs32] = w2;
+        o[3 * cs32] = w3;
+    }
+    flush_flags(f, flags);
+}
+
 // ---------------------------------------------------------------- transpose
 __global__ void words_transpose_kernel(const uint64_t *__restrict__ in, int64_t rows,
                                        int64_t cols, int64_t ldi, uint64_t *__restrict__ out,
@@ -449,11 +565,37 @@ int launch_pack_nchw(const float *x, int64_t B, int64_t C, int64_t H, int64_t W,
     uint32_t *o32 = reinterpret_cast<uint32_t *>(out);
     const bool strict = mode == BNN_PACK_STRICT;
     const bool vec4 = (HW % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
-    static int pix = 0;
+    static int pix = -1;
+    if (pix < 0) {
+        const char *e = getenv("BNN_PACK_PIX");  // 0 (default): direct kernel
+        pix = e ? atoi(e) : 0;
+        if (pix != 0 && pix != 64 && pix != 128 && pix != 256) pix = 0;
+    }
+    if (pix == 0 && vec4) {
+        static int ch = 0;
+        if (ch == 0) {
+            const char *e = getenv("BNN_PACK_CH");  // channels per lane: 8 (default), 16, 32
+            ch = e ? atoi(e) : 8;
+            if (ch != 8 && ch != 16 && ch != 32) ch = 8;
+        }
+        const int64_t threads = ceil_div(B * HW, 4) * (32 / ch);
+        dim3 g((unsigned)ceil_div(threads, 256), (unsigned)(2 * Cw));
+#define BNN_QUAD(K)                                                                            \
+    if (ch == K) {                                                                             \
+        if (strict) pack_nchw_quad_kernel<true, K><<<g, 256, 0, s>>>(x, B, C, HW, 2 * Cw, o32, flags); \
+        else pack_nchw_quad_kernel<false, K><<<g, 256, 0, s>>>(x, B, C, HW, 2 * Cw, o32, flags);      \
+    }
+        BNN_QUAD(8)
+        BNN_QUAD(16)
+        BNN_QUAD(32)
+#undef BNN_QUAD
+        return check_launch("pack_nchw_quad_kernel");
+    }
     if (pix == 0) {
-        const char *e = getenv("BNN_PACK_PIX");
-        pix = e ? atoi(e) : 64;
-        if (pix != 64 && pix != 128 && pix != 256) pix = 64;
+        dim3 g((unsigned)ceil_div(B * HW, 256), (unsigned)Cw);
+        if (strict) pack_nchw_direct_kernel<true><<<g, 256, 0, s>>>(x, B, C, HW, Cw, out, flags);
+        else pack_nchw_direct_kernel<false><<<g, 256, 0, s>>>(x, B, C, HW, Cw, out, flags);
+        return check_launch("pack_nchw_direct_kernel");
     }
     const int smem = 16384 * 4 + pix * (int)(2 * Cw) * 4;
     if (smem > 200 * 1024) return set_error(BNN_EUNSUP, "too many channels for the pack kernel");
