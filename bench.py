@@ -372,14 +372,32 @@ def int8_tensor_peak_tops(n=8192, reps=10):
     return 2 * n ** 3 / (best * 1e-3) / 1e12
 
 
-def pipe_peak(algo):
-    """Roofline denominator for the engine that ran (both measured on this GPU)."""
+def tcgen05_peak_tops(kind):
+    """Measured dense tcgen05.mma issue rate (bnn_probe_pipe_peak pipe 1 = kind::i8,
+    2 = kind::mxf4) as binary TOPS: 2 x MAC/s (one binary op pair per MAC)."""
+    import ctypes
+
+    import torch
+    from paper_1705_09864_b200 import _lib
+    lib = _lib.load()
+    sink = torch.zeros(1, dtype=torch.int32, device="cuda")
+    rate = ctypes.c_double(0)
+    _lib.check(lib.bnn_probe_pipe_peak(1 if kind == "i8" else 2, 4096, sink.data_ptr(),
+                                       ctypes.byref(rate), _lib.stream_ptr()), "probe")
+    return 2 * rate.value / 1e12
+
+
+def pipe_peak(algo, workload="c2"):
+    """Roofline denominator for the engine that ran (all measured on this GPU)."""
     popc = popc_peak_tops()
     if algo in ("auto", "umma"):
-        return {"bound": "tensor", "peak": int8_tensor_peak_tops(), "unit": "TOPS",
-                "peak_source": "measured: dense int8 tensor-core GEMM 8192^3 (cuBLASLt via "
-                               "torch._int_mm), best of 10; the engine is tcgen05 kind::i8",
-                "popc_peak": popc}
+        # TMA-fed shapes run the kind::mxf4 engine (variant 2); the 2-bit planes run kind::i8
+        kind = "i8" if workload.endswith("2bit") else "mxf4"
+        return {"bound": "tensor", "peak": tcgen05_peak_tops(kind), "unit": "TOPS",
+                "peak_source": f"measured: dense tcgen05.mma kind::{kind} issue rate, one CTA per "
+                               "SM, 128x256 MMAs back to back (bnn_probe_pipe_peak); the engine "
+                               f"runs kind::{kind} on bits expanded in SMEM",
+                "popc_peak": popc, "cublas_int8_tops": int8_tensor_peak_tops()}
     return {"bound": "popc", "peak": popc, "unit": "TOPS",
             "peak_source": "measured: bnn_probe_pipe_peak POPC rate x 64 binary ops "
                            "(32 bits x {xor, add})", "popc_peak": popc}
@@ -494,7 +512,7 @@ def run_gpu_arm(args, rank, world, local_rank):
                        "replay per call, pipelined over "
                        f"{getattr(plan, 'host_chunks', 1)} batch slices on 3 streams)"}
 
-    peak = pipe_peak(args.algo)
+    peak = pipe_peak(args.algo, args.workload)
     kern_avg = statistics.mean(kern_ms)
     achieved = ops / (kern_avg * 1e-3) / 1e12
     roof = {"bound": peak["bound"], "achieved": achieved, "peak": peak["peak"],
@@ -502,6 +520,8 @@ def run_gpu_arm(args, rank, world, local_rank):
             "traffic": load_traffic(args.workload, args.algo), "kernel_ms": kern_avg,
             "pack_ms_est": statistics.mean(pack_ms), "peak_source": peak["peak_source"],
             "ops_per_launch": ops, "popc_pipe_peak_tops": peak["popc_peak"]}
+    if "cublas_int8_tops" in peak:
+        roof["cublas_int8_tops"] = peak["cublas_int8_tops"]
     if is_net:
         roof["note"] = ("whole-network step: achieved = binary ops of all binary layers / step "
                         "time (float stem / classifier / BN / pooling included in the time)")

@@ -218,7 +218,9 @@ int bnn_umma_trace(uint64_t *buf);
 
 
 /* Roofline probe (synchronous): measured issue rate of a pipe on the
- * current device.  pipe 0 = POPC (32-bit population counts per second).
+ * current device.  pipe 0 = POPC (32-bit population counts per second);
+ * pipe 1 = dense tcgen05.mma kind::i8 and pipe 2 = kind::mxf4 (MACs per
+ * second, one CTA per SM issuing 128x256 MMAs back to back).
  * `sink` is a caller-allocated device u32 the kernel may write. */
 int bnn_probe_pipe_peak(int pipe, int64_t iters, uint32_t *sink, double *ops_per_sec,
                         bnn_stream_t stream);

@@ -22,33 +22,139 @@ __global__ void probe_popc_kernel(uint32_t seed, int64_t iters, uint32_t *sink) 
     if (acc == 0x12345678u) sink[0] = acc;  // keep the loop alive
 }
 
+// Dense tcgen05 MMA issue rate: one CTA per SM issues `reps` back-to-back
+// 128 x 256 MMAs from fixed SMEM operands (kind::i8, K = 32, or kind::mxf4 with
+// UE8M0 scales = 1, K = 64) and waits for their completion.  The MAC rate is the
+// tensor-pipe roofline of the engine that uses that kind.
+__device__ __forceinline__ uint32_t probe_smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint64_t probe_sw128(uint32_t saddr) {
+    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+           ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+template <int kKind>
+__global__ void __launch_bounds__(128) probe_mma_kernel(int reps, uint32_t *sink) {
+    extern __shared__ __align__(1024) uint8_t psm[];
+    __shared__ uint32_t tmem_base;
+    __shared__ __align__(8) uint64_t bar;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    uint8_t *ops = psm + ((1024 - (probe_smem_u32(psm) & 1023)) & 1023);
+    for (int i = tid; i < (128 + 256) * 128 / 4; i += blockDim.x)
+        reinterpret_cast<uint32_t *>(ops)[i] = 0x11111111u * (i & 3);
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+            probe_smem_u32(&tmem_base)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(probe_smem_u32(&bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;\n");
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    const uint32_t tmem = tmem_base;
+    // UE8M0 scale factors = 1.0 in columns 384.. (kind::mxf4)
+    for (int c = 0; c < 128; c += 8) {
+        const uint32_t one = 0x7F7F7F7Fu;
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %1, %1, %1, %1, %1, %1, %1};\n" ::"r"(
+                         tmem + ((uint32_t)(warp * 32) << 16) + 384 + c),
+                     "r"(one));
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    if (tid == 0) {
+        const uint32_t a = probe_smem_u32(ops), b = a + 128 * 128;
+        for (int i = 0; i < reps; ++i) {
+            const int kk = i & 3;
+            const uint64_t ad = probe_sw128(a + kk * 32), bd = probe_sw128(b + kk * 32);
+            if (kKind == 1) {
+                const uint32_t idesc = (2u << 4) | (32u << 17) | (8u << 24);
+                asm volatile(
+                    "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                    "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+                    "l"(ad), "l"(bd), "r"(idesc), "r"(1u));
+            } else {
+                const uint32_t idesc = (1u << 7) | (1u << 10) | (32u << 17) | (1u << 23) | (8u << 24);
+                asm volatile(
+                    "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                    "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n}\n" ::"r"(
+                        tmem),
+                    "l"(ad), "l"(bd), "r"(idesc), "r"(1u), "r"(tmem + 384), "r"(tmem + 384));
+            }
+        }
+        asm volatile(
+            "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                probe_smem_u32(&bar))
+            : "memory");
+        uint32_t done = 0;
+        do {
+            asm volatile(
+                "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n"
+                "selp.u32 %0, 1, 0, p;\n}\n"
+                : "=r"(done)
+                : "r"(probe_smem_u32(&bar))
+                : "memory");
+        } while (!done);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    if (warp == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;\n");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+    }
+    if (tid == 0 && reps < 0) sink[0] = 1;
+}
+
 }  // namespace bnn
 
 using namespace bnn;
 
 extern "C" int bnn_probe_pipe_peak(int pipe, int64_t iters, uint32_t *sink,
                                    double *ops_per_sec, bnn_stream_t stream) {
-    if (pipe != 0 || iters < 1 || !ops_per_sec || !sink)
-        return set_error(BNN_EINVAL, "probe: pipe must be 0 (POPC), iters >= 1, sink non-null");
+    if (pipe < 0 || pipe > 2 || iters < 1 || !ops_per_sec || !sink)
+        return set_error(BNN_EINVAL,
+                         "probe: pipe must be 0 (POPC), 1 (tcgen05 i8) or 2 (tcgen05 mxf4), "
+                         "iters >= 1, sink non-null");
     int sms = bnn_device_sm_count();
     if (sms <= 0) return set_error(BNN_ECUDA, "probe: no CUDA device");
     cudaStream_t s = as_stream(stream);
-    const int threads = 256, blocks = sms * 8;
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    probe_popc_kernel<<<blocks, threads, 0, s>>>(1u, iters / 8 + 1, sink);  // warm-up
-    cudaEventRecord(e0, s);
-    probe_popc_kernel<<<blocks, threads, 0, s>>>(7u, iters, sink);
-    cudaEventRecord(e1, s);
-    int rc = check_launch("probe_popc_kernel");
+    double work = 0;
+    int rc = BNN_OK;
+    if (pipe == 0) {
+        const int threads = 256, blocks = sms * 8;
+        probe_popc_kernel<<<blocks, threads, 0, s>>>(1u, iters / 8 + 1, sink);  // warm-up
+        cudaEventRecord(e0, s);
+        probe_popc_kernel<<<blocks, threads, 0, s>>>(7u, iters, sink);
+        cudaEventRecord(e1, s);
+        rc = check_launch("probe_popc_kernel");
+        work = (double)blocks * threads * (double)iters * 8.0;  // 32-bit popcounts
+    } else {
+        const int smem = (128 + 256) * 128 + 1024;
+        const int reps = (int)(iters < (1 << 20) ? iters : (1 << 20));
+        auto kern = pipe == 1 ? probe_mma_kernel<1> : probe_mma_kernel<2>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        kern<<<sms, 128, smem, s>>>(reps / 8 + 1, sink);  // warm-up
+        cudaEventRecord(e0, s);
+        kern<<<sms, 128, smem, s>>>(reps, sink);
+        cudaEventRecord(e1, s);
+        rc = check_launch("probe_mma_kernel");
+        work = (double)sms * reps * 128.0 * 256.0 * (pipe == 1 ? 32.0 : 64.0);  // MACs
+    }
     cudaEventSynchronize(e1);
     float ms = 0.f;
     cudaEventElapsedTime(&ms, e0, e1);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     if (rc) return rc;
-    *ops_per_sec = (double)blocks * threads * (double)iters * 8.0 / (ms * 1e-3);
+    *ops_per_sec = work / (ms * 1e-3);
     return BNN_OK;
 }
 

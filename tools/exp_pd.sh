@@ -1,2 +1,2 @@
-python tools/pack_only.py >> gpurun_out/exp_pd.log 2>&1
-BNN_PACK_PIX=64 python tools/pack_only.py 2>&1 | head -1 >> gpurun_out/exp_pd.log
+timeout 300 python bench.py --steps 20 --warmup 3 2>&1 | tail -1 > gpurun_out/bench_c2.json
+timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -2 > gpurun_out/exp_pd.log
