@@ -34,6 +34,10 @@ sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
 
 METRIC = "xnor-popcount binary TOPS (2MNK/s)"
 UNIT = "TOPS"
+# arithmetic type of the tcgen05 engine: 1-bit operands expanded in SMEM to e2m1
+# (kind::mxf4; the 2-bit planes and cp.async-fed shapes use u8 / kind::i8), exact
+# integer counts accumulated in f32 / s32
+DTYPE = "b1 -> e2m1 x e2m1 (tcgen05 kind::mxf4), exact f32 counts"
 WORKLOADS = ("c2", "c1", "gemm4096", "gemm8192", "gemm16384", "gemm4096k65536", "gemm4096_2bit",
              "lenet", "resnet18")
 NET_WORKLOADS = {"lenet": ("binary LeNet (BASELINE configs[2]) images/s", 1024, (1, 28, 28)),
@@ -535,8 +539,8 @@ def run_gpu_arm(args, rank, world, local_rank):
             "metric": metric, "value": value, "unit": unit, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "u8 (bits expanded in SMEM, s32 accumulate)" if args.algo in ("auto", "umma")
-            else "u32 (xor/popc words)",
+            "dtype": (("b1 planes -> u8 (tcgen05 kind::i8), s32" if args.workload.endswith("2bit")
+                       else DTYPE) if args.algo in ("auto", "umma") else "u32 (xor/popc words)"),
             "data": "synthetic (seeded, BASELINE.json shapes)",
             "config": {"workload": d["workload"], "M": d["M"], "N": d["N"], "K": d["K"],
                        "batch_per_gpu": d["batch"], "parallelism": f"replicas x{world}",
