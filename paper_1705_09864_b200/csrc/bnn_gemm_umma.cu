@@ -43,6 +43,14 @@
 
 #include "bnn_loaders.cuh"
 
+// build-time tuning knobs of the kind::mxf4 engine (tools/build_variant.sh)
+#ifndef BNN_FP4_ES
+#define BNN_FP4_ES 3
+#endif
+#ifndef BNN_FP4_TMA_SLOTS
+#define BNN_FP4_TMA_SLOTS 4
+#endif
+
 namespace bnn {
 
 // Dense packed operand [rows, ld32] u32 fetched by the tensor-memory
@@ -103,16 +111,24 @@ __device__ __forceinline__ void trace_at(uint64_t *buf, int slot) {
 constexpr int kWordsPerStage = 4;  // u32 words of K per row per stage
 constexpr int kRowBytes = 128;     // expanded bytes per row per stage
 
-template <int BN, bool kATmem, int kPlanes = 1, bool kTma = false, bool kFp4 = false>
+template <int BN, bool kATmem, int kPlanes = 1, bool kTma = false, bool kFp4 = false,
+          int kSetsT = 1>
 struct Cfg {
     static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
     static_assert(!kFp4 || (!kATmem && kPlanes == 1 && kTma), "fp4 engine: SS operands, TMA-fed");
     static constexpr int kProducers = BM + BN;                 // one thread per operand row
     static constexpr int kProducerWarps = (kProducers + 31) / 32;
-    static constexpr int kTmaWarp = kProducerWarps;  // one elected lane issues the TMA loads
+    // kind::mxf4: two expander sets take alternate superstages, so each warp's
+    // barrier round trip (slot wait, popcounts, release, buffer wait, proxy fence,
+    // arrival) overlaps the other set's
+    static constexpr int kSets = kSetsT;
+    static_assert(kSets == 1 || (kSets == 2 && kFp4), "expander sets: kind::mxf4 engine only");
+    static constexpr int kExpWarps = kProducerWarps * kSets;
+    static constexpr int kTmaWarp = kExpWarps;  // one elected lane issues the TMA loads
     static constexpr int kMmaWarp = kTmaWarp + 1;
     static constexpr int kEpiWarp0 = kMmaWarp + 1;
-    static constexpr int kEpiWarps = 8;                        // 2 per TMEM lane quadrant
+    // 2 epilogue warps per TMEM lane quadrant; 1 with two expander sets (register budget)
+    static constexpr int kEpiWarps = kSets == 2 ? 4 : 8;
     static constexpr int kThreads = (kEpiWarp0 + kEpiWarps) * 32;
     // K is consumed in 128-bit stages grouped into superstages of kSub stages:
     // every barrier round trip (expanded-buffer wait, proxy fence, full arrival,
@@ -127,7 +143,7 @@ struct Cfg {
     static constexpr int kStageB = BN * kStageRow;
     static constexpr int kStageBytes = kStageA + kStageB;
     static constexpr int kSuperBytes = kSub * kStageBytes;
-    static constexpr int ES = kATmem ? 2 : 3;  // expanded superstage buffers
+    static constexpr int ES = kATmem ? 2 : ((kFp4 && BN <= 176) ? BNN_FP4_ES : 3);  // expanded superstage buffers
     static constexpr int kFp4A = BM * 128;      // fp4: A block of a superstage buffer
     // TMEM: 2 accumulator buffers of BN columns (+ ES x kSub A stages of 32 columns)
     static constexpr int kAccCols = BN;
@@ -144,14 +160,14 @@ struct Cfg {
     static constexpr int off_pk = ES * kSuperBytes;
     // packed staging: per-thread cp.async rings (PD stages x 16 B per row), or
     // with TMA kTmaSlots superstage slots of [A rows | B rows] x kSub x 16 B
-    static constexpr int kTmaSlots = 4;
+    static constexpr int kTmaSlots = (kFp4 && BN <= 176) ? BNN_FP4_TMA_SLOTS : 4;
     static constexpr int kTmaA = BM * kSub * 16, kTmaB = BN * kSub * 16;
     static constexpr int kTmaSlotBytes = ((kTmaA + kTmaB + 1023) / 1024) * 1024;
     static constexpr int kPkBytes = kTma ? kTmaSlots * kTmaSlotBytes
                                          : PD * kProducerWarps * 32 * 16 * kPlanes;
     static constexpr int off_popc_a = off_pk + kPkBytes;
-    static constexpr int off_popc_b = off_popc_a + 2 * BM * 4;
-    static constexpr int off_epi = off_popc_b + 2 * BN * 4;
+    static constexpr int off_popc_b = off_popc_a + kSets * 2 * BM * 4;  // [set][buf][row]
+    static constexpr int off_epi = off_popc_b + kSets * 2 * BN * 4;
     static constexpr int off_bars = off_epi + kEpiWarps * kStgBytes;
     static constexpr int kNumBars = 2 * ES + 6 + 2 * kTmaSlots;
     static constexpr int off_tmem = off_bars + kNumBars * 8;
@@ -389,8 +405,8 @@ template <>
 struct is_tma<TmaConv> { static constexpr bool value = true; };
 
 template <int BN, bool kATmem, int kVec, class ALoad, class BLoad, class Store, int kPlanes = 1,
-          bool kFp4 = false>
-__global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value, kFp4>::kThreads, 1)
+          bool kFp4 = false, int kSets = 1>
+__global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value, kFp4, kSets>::kThreads, 1)
     xnor_umma_kernel(const __grid_constant__ ALoad aload, const __grid_constant__ BLoad bload,
                      Store store, Epilogue ep, int64_t kw32, TileMap tmap, uint64_t *trace_buf,
                      int dbg) {
@@ -402,7 +418,7 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
     };
     constexpr bool kTma = is_tma<ALoad>::value;
     static_assert(kTma == is_tma<BLoad>::value && (!kTma || kPlanes == 1), "TMA: both operands");
-    using C = Cfg<BN, kATmem, kPlanes, kTma, kFp4>;
+    using C = Cfg<BN, kATmem, kPlanes, kTma, kFp4, kSets>;
     constexpr int ES = C::ES;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t sbase_raw = smem_u32(smem_raw);
@@ -434,7 +450,7 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
         for (int b = 0; b < 2; ++b) {
             mbar_init(bar_tfull + 8 * b, 1);
             mbar_init(bar_tempty + 8 * b, C::kEpiWarps);
-            mbar_init(bar_pfull + 8 * b, C::kProducerWarps);
+            mbar_init(bar_pfull + 8 * b, C::kExpWarps);
         }
         for (int r = 0; r < C::kTmaSlots; ++r) {
             mbar_init(bar_ld + 8 * r, 1);
@@ -454,7 +470,7 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
     const uint32_t tmem = *s_tmem;
     if (tid == 0) trace(1);
 
-    if (warp < C::kProducerWarps) {
+    if (warp < C::kExpWarps) {
         // ================================================================ producers
         if constexpr (kFp4) {
             // UE8M0 block scales = 2^0 in every TMEM column from kSfCol on (both
@@ -469,9 +485,11 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                 fence_before();
             }
         }
-        const bool is_a = tid < BM;
-        const bool active = tid < C::kProducers;  // the last warp may be partly idle
-        const int row = is_a ? tid : tid - BM;
+        const int set = warp / C::kProducerWarps;                    // expander set
+        const int ptid = tid - set * C::kProducerWarps * 32;         // thread within the set
+        const bool is_a = ptid < BM;
+        const bool active = ptid < C::kProducers;  // the last warp may be partly idle
+        const int row = is_a ? ptid : ptid - BM;
         const uint32_t ring = s_pk + tid * 16 * kPlanes;  // slot-major private ring
         constexpr uint32_t kRingSlot = C::kProducerWarps * 32 * 16 * kPlanes;
         // fetch iterator (runs PD - kSub stages ahead, across tile boundaries)
@@ -541,6 +559,19 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
     #pragma unroll 1
                 for (uint32_t kt = 0; kt < kt32; kt += kSub, ++gs) {
                     const uint32_t nsub = kt32 - kt < kSub ? kt32 - kt : kSub;
+                    if constexpr (C::kSets > 1) {
+                        if ((int)(gs % C::kSets) != set) {  // the other set's superstage
+                            if constexpr (std::is_same<BLoad, TmaConv>::value) {
+                                c_cw += 4 * kSub;
+                                if (c_cw == bload.cs32) {
+                                    c_cw = 0;
+                                    if (++c_j == bload.kw) c_j = 0, ++c_i;
+                                }
+                            }
+                            gk += nsub;
+                            continue;
+                        }
+                    }
                     uint32_t wv[kSub][4], wv1[kSub][4] = {};
                     if constexpr (kTma) {
                         // this superstage's packed rows, landed by the TMA warp
@@ -695,9 +726,9 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                 // hand this tile's row popcounts to the epilogue (double-buffered)
                 const int buf = it & 1;
                 if (it >= 2) mbar_wait(bar_tempty + 8 * buf, (uint32_t)((it >> 1) - 1) & 1u);
-                if (is_a) s_popc_a[buf * BM + row] = my_popc;
+                if (is_a) s_popc_a[(set * 2 + buf) * BM + row] = my_popc;
                 else if (active)  // (f32 bits on the fp4 engine, whose epilogue decodes in f32)
-                    s_popc_b[buf * BN + row] = kFp4 ? __float_as_int((float)my_popc) : my_popc;
+                    s_popc_b[(set * 2 + buf) * BN + row] = kFp4 ? __float_as_int((float)my_popc) : my_popc;
                 __syncwarp();
                 if (lane == 0) mbar_arrive(bar_pfull + 8 * buf);
             }
@@ -849,16 +880,24 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
             mbar_wait_sleep(bar_pfull + 8 * buf, (uint32_t)(it >> 1) & 1u);
             fence_after();
             if (e == 0 && lane == 0 && it < 3) trace(4 + 3 * it);
+            if (dbg & 2048) {  // debug: skip the whole epilogue (wrong outputs)
+                fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(bar_tempty + 8 * buf);
+                continue;
+            }
             const bool mok = m < M;
             // per-row constants: P = kb - pb[n] + 2C, with 2C = acc >> 6 (acc = 128 C)
-            const int32_t kb = ep.k_eff - s_popc_a[buf * BM + q * 32 + lane];
+            int32_t popa = s_popc_a[buf * BM + q * 32 + lane];
+            if constexpr (C::kSets > 1) popa += s_popc_a[(2 + buf) * BM + q * 32 + lane];
+            const int32_t kb = ep.k_eff - popa;
             const int32_t rowc = (dot ? 2 * kb - ep.k_logical : kb) + 0x4B400000;
             const uint32_t vsh = dot ? 5u : 6u, psh = dot ? 1u : 0u;
             const float rowf = (float)(dot ? 2 * kb - ep.k_logical : kb);  // fp4 decode
             const float cmul = dot ? 4.0f : 2.0f, pmul = dot ? 2.0f : 1.0f;
             // multi-bit decode constants (kPlanes == 2): s_popc_* hold code sums
             const int32_t abab = ep.a_alpha * ep.b_alpha;
-            const int32_t rowterm = ep.a_alpha * ep.b_beta * s_popc_a[buf * BM + q * 32 + lane] +
+            const int32_t rowterm = ep.a_alpha * ep.b_beta * popa +
                                     ep.k_logical * ep.a_beta * ep.b_beta;
             const float sc = (mok && ep.scale) ? __ldg(ep.scale + m) : 1.0f;
             const float sh = (mok && ep.shift) ? __ldg(ep.shift + m) : 0.0f;
@@ -868,9 +907,10 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
             const float bg = (mok && has_bn) ? __ldg(ep.bn_gamma + m) : 1.0f;
             const float bb = (mok && has_bn) ? __ldg(ep.bn_beta + m) : 0.0f;
             const int32_t *pb = s_popc_b + buf * BN;
+            const int32_t *pb1 = s_popc_b + (2 + buf) * BN;  // second expander set (kSets == 2)
             const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + buf * C::kAccCols;
 #pragma unroll 1
-            for (int c = h; c * 32 < BN; c += 2) {
+            for (int c = h; c * 32 < BN; c += C::kEpiWarps / 4) {
                 uint32_t v[32];
                 const int w = BN - c * 32 < 32 ? BN - c * 32 : 32;
                 if (w == 32) {
@@ -902,7 +942,11 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                     // (2kb - K) - 2pb + 4C, every term an exact f32 integer
 #pragma unroll
                     for (int j4 = 0; j4 < 8; ++j4) {
-                        const float4 pb4 = *reinterpret_cast<const float4 *>(pb + c * 32 + 4 * j4);
+                        float4 pb4 = *reinterpret_cast<const float4 *>(pb + c * 32 + 4 * j4);
+                        if constexpr (C::kSets > 1) {
+                            const float4 q4 = *reinterpret_cast<const float4 *>(pb1 + c * 32 + 4 * j4);
+                            pb4.x += q4.x; pb4.y += q4.y; pb4.z += q4.z; pb4.w += q4.w;
+                        }
                         const float pbv[4] = {pb4.x, pb4.y, pb4.z, pb4.w};
 #pragma unroll
                         for (int i = 0; i < 4; ++i) {
@@ -1118,12 +1162,12 @@ static int encode_conv(TmaConv &t, int box_words, int box_pixels, int64_t B) {
 }
 
 template <int BN, bool kATmem, int kVec, class ALoad, class BLoad, class Store, int kPlanes = 1,
-          bool kFp4 = false>
+          bool kFp4 = false, int kSets = 1>
 static int launch_umma_cfg(const ALoad &a_in, const BLoad &b_in, const Store &st, const Epilogue &ep,
                            int64_t M, int64_t N, int64_t kw32, cudaStream_t s) {
     constexpr bool kTma = umma::is_tma<ALoad>::value;
-    using C = umma::Cfg<BN, kATmem, kPlanes, kTma, kFp4>;
-    auto kern = umma::xnor_umma_kernel<BN, kATmem, kVec, ALoad, BLoad, Store, kPlanes, kFp4>;
+    using C = umma::Cfg<BN, kATmem, kPlanes, kTma, kFp4, kSets>;
+    auto kern = umma::xnor_umma_kernel<BN, kATmem, kVec, ALoad, BLoad, Store, kPlanes, kFp4, kSets>;
     ALoad a = a_in;
     BLoad b = b_in;
     if constexpr (kTma) {
@@ -1192,6 +1236,20 @@ static int choose_bn(int64_t M, int64_t N, bool fp4 = false) {
     return best;
 }
 
+template <int kSets, class ALoad, class BLoad, class Store>
+static int launch_fp4(const ALoad &a, const BLoad &b, const Store &st, const Epilogue &ep, int64_t M,
+                      int64_t N, int64_t kw32, cudaStream_t s) {
+    using S = Store;
+    switch (choose_bn(M, N, true)) {
+        case 128: return launch_umma_cfg<128, false, 4, ALoad, BLoad, S, 1, true, kSets>(a, b, st, ep, M, N, kw32, s);
+        case 160: return launch_umma_cfg<160, false, 4, ALoad, BLoad, S, 1, true, kSets>(a, b, st, ep, M, N, kw32, s);
+        case 176: return launch_umma_cfg<176, false, 4, ALoad, BLoad, S, 1, true, kSets>(a, b, st, ep, M, N, kw32, s);
+        case 192: return launch_umma_cfg<192, false, 4, ALoad, BLoad, S, 1, true, kSets>(a, b, st, ep, M, N, kw32, s);
+        case 208: return launch_umma_cfg<208, false, 4, ALoad, BLoad, S, 1, true, kSets>(a, b, st, ep, M, N, kw32, s);
+        default: return launch_umma_cfg<224, false, 4, ALoad, BLoad, S, 1, true, kSets>(a, b, st, ep, M, N, kw32, s);
+    }
+}
+
 template <int kVec, class ALoad, class BLoad, class Store>
 static int launch_umma(const ALoad &a, const BLoad &b, const Store &st, const Epilogue &ep,
                        int64_t M, int64_t N, int64_t kw32, cudaStream_t s) {
@@ -1199,15 +1257,10 @@ static int launch_umma(const ALoad &a, const BLoad &b, const Store &st, const Ep
         if (umma_variant() == 0) return launch_umma_cfg<256, false, kVec>(a, b, st, ep, M, N, kw32, s);
     if constexpr (umma::is_tma<ALoad>::value) {
         if (umma_variant() == 2) {
-            using S = Store;
-            switch (choose_bn(M, N, true)) {
-                case 128: return launch_umma_cfg<128, false, 4, ALoad, BLoad, S, 1, true>(a, b, st, ep, M, N, kw32, s);
-                case 160: return launch_umma_cfg<160, false, 4, ALoad, BLoad, S, 1, true>(a, b, st, ep, M, N, kw32, s);
-                case 176: return launch_umma_cfg<176, false, 4, ALoad, BLoad, S, 1, true>(a, b, st, ep, M, N, kw32, s);
-                case 192: return launch_umma_cfg<192, false, 4, ALoad, BLoad, S, 1, true>(a, b, st, ep, M, N, kw32, s);
-                case 208: return launch_umma_cfg<208, false, 4, ALoad, BLoad, S, 1, true>(a, b, st, ep, M, N, kw32, s);
-                default: return launch_umma_cfg<224, false, 4, ALoad, BLoad, S, 1, true>(a, b, st, ep, M, N, kw32, s);
-            }
+            // long K (>= 24 superstages per tile): two expander sets on alternate
+            // superstages; short K: one set and 8 epilogue warps (tiles end often)
+            if (kw32 >= 24 * 8) return launch_fp4<2>(a, b, st, ep, M, N, kw32, s);
+            return launch_fp4<1>(a, b, st, ep, M, N, kw32, s);
         }
     }
     switch (choose_bn(M, N)) {

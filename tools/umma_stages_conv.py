@@ -37,7 +37,7 @@ plan.kernel()
 torch.cuda.synchronize()
 lib.bnn_umma_trace(None)
 t = tr[4096:].view(16, 256).cpu().numpy().astype(np.int64)
-names = ["B_fetched", "A_empty_ok", "A_done", "A_data", "B_empty_ok", "B_done", "B_data", "mma_full", "mma_commit"]
+names = ["tma_issue", "A_empty_ok", "A_done", "A_data", "B_empty_ok", "B_done", "B_data", "mma_full", "mma_commit"]
 t0 = t[7, 0]
 print("super " + " ".join(f"{x:>10s}" for x in names))
 for g in range(0, 24):
