@@ -1213,7 +1213,8 @@ static int umma_variant() {
 
 static int choose_bn(int64_t M, int64_t N, bool fp4 = false) {
     static const int cands[] = {192, 176, 160, 128};
-    static const int cands4[] = {224, 208, 192, 176, 160, 128};
+    // (small N tiles give small problems enough CTAs: every tile runs the full K loop)
+    static const int cands4[] = {224, 208, 192, 176, 160, 128, 96, 64, 32, 16};
     if (fp4) {
         const int64_t sms = sm_count(), tm = ceil_div(M, umma::BM);
         int best = 192;
@@ -1241,6 +1242,10 @@ static int launch_fp4(const ALoad &a, const BLoad &b, const Store &st, const Epi
                       int64_t N, int64_t kw32, cudaStream_t s) {
     using S = Store;
     switch (choose_bn(M, N, true)) {
+        case 16: return launch_umma_cfg<16, false, 4, ALoad, BLoad, S, 1, true, kSets>(a, b, st, ep, M, N, kw32, s);
+        case 32: return launch_umma_cfg<32, false, 4, ALoad, BLoad, S, 1, true, kSets>(a, b, st, ep, M, N, kw32, s);
+        case 64: return launch_umma_cfg<64, false, 4, ALoad, BLoad, S, 1, true, kSets>(a, b, st, ep, M, N, kw32, s);
+        case 96: return launch_umma_cfg<96, false, 4, ALoad, BLoad, S, 1, true, kSets>(a, b, st, ep, M, N, kw32, s);
         case 128: return launch_umma_cfg<128, false, 4, ALoad, BLoad, S, 1, true, kSets>(a, b, st, ep, M, N, kw32, s);
         case 160: return launch_umma_cfg<160, false, 4, ALoad, BLoad, S, 1, true, kSets>(a, b, st, ep, M, N, kw32, s);
         case 176: return launch_umma_cfg<176, false, 4, ALoad, BLoad, S, 1, true, kSets>(a, b, st, ep, M, N, kw32, s);
