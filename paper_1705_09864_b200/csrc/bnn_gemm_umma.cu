@@ -114,7 +114,13 @@ constexpr int kRowBytes = 128;     // expanded bytes per row per stage
 template <int BN, bool kATmem, int kPlanes = 1, bool kTma = false, bool kFp4 = false,
           int kSetsT = 1>
 struct Cfg {
-    static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
+    static_assert(BN % 16 == 0 && BN >= 16 && (BN <= 256 || (kFp4 && BN % 32 == 0 && BN <= 384)),
+                  "UMMA N for M=128 (wide fp4 tiles: two MMAs of N/2)");
+    // tiles wider than one MMA (fp4, N <= 384) issue two MMAs of N/2 per K step into
+    // adjacent TMEM column ranges; their single accumulator buffer is meant for
+    // shapes that fit in one wave of CTAs
+    static constexpr int kMmaN = BN > 256 ? BN / 2 : BN;
+    static constexpr int kNMma = BN / kMmaN;
     static_assert(!kFp4 || (!kATmem && kPlanes == 1 && kTma), "fp4 engine: SS operands, TMA-fed");
     static constexpr int kProducers = BM + BN;                 // one thread per operand row
     static constexpr int kProducerWarps = (kProducers + 31) / 32;
@@ -143,14 +149,16 @@ struct Cfg {
     static constexpr int kStageB = BN * kStageRow;
     static constexpr int kStageBytes = kStageA + kStageB;
     static constexpr int kSuperBytes = kSub * kStageBytes;
-    static constexpr int ES = kATmem ? 2 : ((kFp4 && BN <= 176) ? BNN_FP4_ES : 3);  // expanded superstage buffers
+    static constexpr int ES = kATmem ? 2 : (kFp4 ? (BN > 256 ? 2 : (BN <= 176 ? BNN_FP4_ES : 3)) : 3);  // expanded superstage buffers
     static constexpr int kFp4A = BM * 128;      // fp4: A block of a superstage buffer
     // TMEM: 2 accumulator buffers of BN columns (+ ES x kSub A stages of 32 columns)
     static constexpr int kAccCols = BN;
+    static constexpr int kAccBufs = BN > 256 ? 1 : 2;  // TMEM accumulator buffers
     static constexpr int kAStageCol = 2 * BN;
     static constexpr int kTmemCols = 512;
-    static constexpr int kSfCol = 2 * BN;       // fp4: UE8M0 scale factors (all 1.0) from here
-    static_assert(2 * BN + (kATmem ? ES * kSub * 32 : 0) + (kFp4 ? 64 : 0) <= 512, "TMEM budget");
+    static constexpr int kSfCol = (BN > 256 ? 1 : 2) * BN;  // fp4: UE8M0 scales (all 1.0) from here
+    static_assert((BN > 256 ? 1 : 2) * BN + (kATmem ? ES * kSub * 32 : 0) + (kFp4 ? 64 : 0) <= 512,
+                  "TMEM budget");
     // shared memory carve-up (offsets from the 1024-aligned base)
     // epilogue staging: per warp 32 rows x 32 f32, row pitch 144 B (16 B of
     // padding keeps both the row writes and the transposed reads conflict-free)
@@ -160,8 +168,9 @@ struct Cfg {
     static constexpr int off_pk = ES * kSuperBytes;
     // packed staging: per-thread cp.async rings (PD stages x 16 B per row), or
     // with TMA kTmaSlots superstage slots of [A rows | B rows] x kSub x 16 B
-    static constexpr int kTmaSlots = (kFp4 && BN <= 176) ? BNN_FP4_TMA_SLOTS : 4;
+    static constexpr int kTmaSlots = (kFp4 && BN > 256) ? 3 : ((kFp4 && BN <= 176) ? BNN_FP4_TMA_SLOTS : 4);
     static constexpr int kTmaA = BM * kSub * 16, kTmaB = BN * kSub * 16;
+    static constexpr int kTmaBoxB = BN > 256 ? BN / 2 : BN;  // tiled TMA boxes are <= 256 rows
     static constexpr int kTmaSlotBytes = ((kTmaA + kTmaB + 1023) / 1024) * 1024;
     static constexpr int kPkBytes = kTma ? kTmaSlots * kTmaSlotBytes
                                          : PD * kProducerWarps * 32 * 16 * kPlanes;
@@ -176,7 +185,7 @@ struct Cfg {
     static constexpr uint32_t kIdesc = (2u << 4) | (0u << 7) | (0u << 10) |
                                        ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
     // kind::mxf4: E2M1 x E2M1 (format 1), UE8M0 scales (bit 23), f32 accumulate
-    static constexpr uint32_t kIdescFp4 = (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+    static constexpr uint32_t kIdescFp4 = (1u << 7) | (1u << 10) | ((uint32_t)(kMmaN >> 3) << 17) |
                                           (1u << 23) | ((uint32_t)(BM >> 4) << 24);
 };
 
@@ -724,8 +733,9 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                     gk += nsub;
                 }
                 // hand this tile's row popcounts to the epilogue (double-buffered)
-                const int buf = it & 1;
-                if (it >= 2) mbar_wait(bar_tempty + 8 * buf, (uint32_t)((it >> 1) - 1) & 1u);
+                const int buf = it % C::kAccBufs;
+                if (it >= C::kAccBufs)
+                    mbar_wait(bar_tempty + 8 * buf, (uint32_t)((it / C::kAccBufs) - 1) & 1u);
                 if (is_a) s_popc_a[(set * 2 + buf) * BM + row] = my_popc;
                 else if (active)  // (f32 bits on the fp4 engine, whose epilogue decodes in f32)
                     s_popc_b[(set * 2 + buf) * BN + row] = kFp4 ? __float_as_int((float)my_popc) : my_popc;
@@ -778,6 +788,10 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                         } else {
                             tma_load_2d(dst + C::kTmaA, &bload.map, (int)(kt * kWordsPerStage),
                                         tn * BN, bar_ld + 8 * ts);
+                            if constexpr (C::kTmaBoxB != BN)  // second box of a wide tile
+                                tma_load_2d(dst + C::kTmaA + C::kTmaBoxB * C::kSub * 16, &bload.map,
+                                            (int)(kt * kWordsPerStage), tn * BN + C::kTmaBoxB,
+                                            bar_ld + 8 * ts);
                         }
                     }
                 }
@@ -793,8 +807,9 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
             int it = 0;
 #pragma unroll 1
             for (int tile = blockIdx.x; tile < tmap.ntiles; tile += gridDim.x, ++it) {
-                const int buf = it & 1;
-                if (it >= 2) mbar_wait(bar_tempty + 8 * buf, (uint32_t)((it >> 1) - 1) & 1u);
+                const int buf = it % C::kAccBufs;
+                if (it >= C::kAccBufs)
+                    mbar_wait(bar_tempty + 8 * buf, (uint32_t)((it / C::kAccBufs) - 1) & 1u);
                 fence_after();
                 const uint32_t d = tmem + buf * C::kAccCols;
 #pragma unroll 1
@@ -816,6 +831,10 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                             mma_fp4<C::kIdescFp4>(d, sw128_desc(a_addr + kk * 32),
                                                   sw128_desc(b_addr + kk * 32), tmem + C::kSfCol,
                                                   tmem + C::kSfCol, acc);
+                            if constexpr (C::kNMma == 2)  // columns [N/2, N): B rows N/2..N-1
+                                mma_fp4<C::kIdescFp4>(d + C::kMmaN, sw128_desc(a_addr + kk * 32),
+                                                      sw128_desc(b_addr + C::kMmaN * 128 + kk * 32),
+                                                      tmem + C::kSfCol, tmem + C::kSfCol, acc);
                         }
                     }
 #pragma unroll
@@ -843,8 +862,9 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
             }
             // release TMEM as soon as the epilogue has drained the last two
             // accumulators, overlapping the dealloc with the final stores
-            for (int t = it - 2; t < it; ++t)
-                if (t >= 0) mbar_wait(bar_tempty + 8 * (t & 1), (uint32_t)(t >> 1) & 1u);
+            for (int t = it - C::kAccBufs; t < it; ++t)
+                if (t >= 0)
+                    mbar_wait(bar_tempty + 8 * (t % C::kAccBufs), (uint32_t)(t / C::kAccBufs) & 1u);
         }
         __syncwarp();
         fence_after();
@@ -871,13 +891,13 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
         int it = 0;
 #pragma unroll 1
         for (int tile = blockIdx.x; tile < tmap.ntiles; tile += gridDim.x, ++it) {
-            const int buf = it & 1;
+            const int buf = it % C::kAccBufs;
             int tm, tn;
             tmap.decode(tile, tm, tn);
             const int64_t mq = (int64_t)tm * BM + q * 32, n0 = (int64_t)tn * BN;
             const int64_t m = mq + lane;
-            mbar_wait_sleep(bar_tfull + 8 * buf, (uint32_t)(it >> 1) & 1u);
-            mbar_wait_sleep(bar_pfull + 8 * buf, (uint32_t)(it >> 1) & 1u);
+            mbar_wait_sleep(bar_tfull + 8 * buf, (uint32_t)(it / C::kAccBufs) & 1u);
+            mbar_wait_sleep(bar_pfull + 8 * buf, (uint32_t)(it / C::kAccBufs) & 1u);
             fence_after();
             if (e == 0 && lane == 0 && it < 3) trace(4 + 3 * it);
             if (dbg & 2048) {  // debug: skip the whole epilogue (wrong outputs)
@@ -1176,7 +1196,7 @@ static int launch_umma_cfg(const ALoad &a_in, const BLoad &b_in, const Store &st
             static_assert(C::kSub == 2, "im2col TMA: one 32-byte tap chunk per superstage");
             if (rc == BNN_OK) rc = encode_conv(b, 4 * C::kSub, BN, b.npix / ((int64_t)b.oh * b.ow));
         } else {
-            if (rc == BNN_OK) rc = encode_rows(b, 4 * C::kSub, BN);
+            if (rc == BNN_OK) rc = encode_rows(b, 4 * C::kSub, C::kTmaBoxB);
         }
         if (rc != BNN_OK) return rc;
     }
@@ -1211,7 +1231,7 @@ static int umma_variant() {
     return g_umma_variant;
 }
 
-static int choose_bn(int64_t M, int64_t N, bool fp4 = false) {
+static int choose_bn(int64_t M, int64_t N, bool fp4 = false, bool wide = false) {
     static const int cands[] = {192, 176, 160, 128};
     // (small N tiles give small problems enough CTAs: every tile runs the full K loop)
     static const int cands4[] = {224, 208, 192, 176, 160, 128, 96, 64, 32, 16};
@@ -1224,6 +1244,14 @@ static int choose_bn(int64_t M, int64_t N, bool fp4 = false) {
             const int64_t cost = waves * (bn + 32);
             if (best_cost < 0 || cost < best_cost) best = bn, best_cost = cost;
         }
+        // wide tiles (two MMAs, one accumulator buffer): only when they fit in one wave
+        static const int wide_cands[] = {320, 352, 384};
+        if (wide)
+            for (int bn : wide_cands) {
+                if (tm * ceil_div(N, bn) > sms) continue;
+                const int64_t cost = bn + 32;
+                if (cost < best_cost) best = bn, best_cost = cost;
+            }
         return best;
     }
     const int64_t sms = sm_count(), tm = ceil_div(M, umma::BM);
@@ -1241,7 +1269,10 @@ template <int kSets, class ALoad, class BLoad, class Store>
 static int launch_fp4(const ALoad &a, const BLoad &b, const Store &st, const Epilogue &ep, int64_t M,
                       int64_t N, int64_t kw32, cudaStream_t s) {
     using S = Store;
-    switch (choose_bn(M, N, true)) {
+    switch (choose_bn(M, N, true, kSets == 1)) {
+        case 320: if constexpr (kSets == 1) return launch_umma_cfg<320, false, 4, ALoad, BLoad, S, 1, true, 1>(a, b, st, ep, M, N, kw32, s); else break;
+        case 352: if constexpr (kSets == 1) return launch_umma_cfg<352, false, 4, ALoad, BLoad, S, 1, true, 1>(a, b, st, ep, M, N, kw32, s); else break;
+        case 384: if constexpr (kSets == 1) return launch_umma_cfg<384, false, 4, ALoad, BLoad, S, 1, true, 1>(a, b, st, ep, M, N, kw32, s); else break;
         case 16: return launch_umma_cfg<16, false, 4, ALoad, BLoad, S, 1, true, kSets>(a, b, st, ep, M, N, kw32, s);
         case 32: return launch_umma_cfg<32, false, 4, ALoad, BLoad, S, 1, true, kSets>(a, b, st, ep, M, N, kw32, s);
         case 64: return launch_umma_cfg<64, false, 4, ALoad, BLoad, S, 1, true, kSets>(a, b, st, ep, M, N, kw32, s);
