@@ -473,10 +473,20 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                      "n"(C::kTmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
+    if constexpr (kTma) {
+        if (tid == 0) {  // descriptor prefetch does not depend on the previous kernel
+            asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&aload.map)));
+            asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&bload.map)));
+        }
+    }
     fence_before();
     __syncthreads();
     fence_after();
     const uint32_t tmem = *s_tmem;
+    // programmatic dependent launch: the setup above (barriers, TMEM allocation,
+    // descriptor prefetch) overlaps the previous kernel's tail; operand reads and
+    // output writes start only once that kernel's results are visible
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
     if (tid == 0) trace(1);
 
     if (warp < C::kExpWarps) {
@@ -1210,8 +1220,17 @@ static int launch_umma_cfg(const ALoad &a_in, const BLoad &b_in, const Store &st
     if (ntiles > (1ll << 30)) return set_error(BNN_EUNSUP, "too many tiles");
     umma::TileMap tmap{(int)tiles_m, (int)ntiles};
     const int grid = (int)(ntiles < sm_count() ? ntiles : sm_count());
-    kern<<<grid, C::kThreads, C::kSmemBytes, s>>>(a, b, st, ep, kw32, tmap, g_trace_buf,
-                                                  umma_dbg());
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(C::kThreads);
+    cfg.dynamicSmemBytes = C::kSmemBytes;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, a, b, st, ep, kw32, tmap, g_trace_buf, umma_dbg());
     return check_launch("xnor_umma_kernel");
 }
 

@@ -323,6 +323,9 @@ __global__ void __launch_bounds__(256) pack_nchw_quad_kernel(const float *__rest
                                                                uint32_t *__restrict__ out32,
                                                                int32_t *flags) {
     constexpr int G = 32 / kCh;
+    // let a programmatic-dependent consumer (the conv kernel) launch and run its setup
+    // while this pass finishes; it waits for our results in griddepcontrol.wait
+    asm volatile("griddepcontrol.launch_dependents;\n");
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int sub = (int)(t % G);
     const int64_t gq = t / G;          // pixel quad

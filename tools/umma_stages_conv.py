@@ -43,9 +43,11 @@ print("super " + " ".join(f"{x:>10s}" for x in names))
 for g in range(0, 24):
     print(f"{g:5d} " + " ".join(f"{(t[ev, g] - t0) if t[ev, g] else -1:10d}" for ev in range(len(names))))
 c = tr[:148 * 16].view(148, 16).cpu().numpy().astype(np.float64)
+c = c[c[:, 0] > 0]  # CTAs of the launch (grid may be < 148)
 c0 = c[:, 0].min()
 print("per-CTA exit (us after first start): max %.1f median %.1f" % (((c[:, 12] - c0) / 1e3).max(), np.median((c[:, 12] - c0) / 1e3)))
 print("per-CTA first mma (us): median %.2f" % np.median((c[:, 2] - c0) / 1e3))
+print("tile 0: MMA done median %.2f, epilogue start median %.2f, epilogue end median %.2f (us)" % tuple(np.median((c[:, j] - c0) / 1e3) for j in (3, 4, 5)))
 st = (c[:, 0] - c0) / 1e3
 print("CTA start (us): min %.2f median %.2f max %.2f; setup done median %.2f" % (st.min(), np.median(st), st.max(), np.median((c[:, 1] - c0) / 1e3)))
 
@@ -62,6 +64,7 @@ with torch.cuda.graph(g2):
 lib.bnn_umma_trace(None)
 g2.replay(); torch.cuda.synchronize()
 c = tr[:148 * 16].view(148, 16).cpu().numpy().astype(np.int64)
+c = c[c[:, 0] > 0]
 s0, s1 = [int(v) for v in st[:2].cpu()]
 print("stamp0 -> first CTA start %.2f us, -> last CTA start %.2f, last CTA exit -> stamp1 %.2f us, total %.2f us"
       % ((c[:, 0].min() - s0) / 1e3, (c[:, 0].max() - s0) / 1e3, (s1 - c[:, 12].max()) / 1e3, (s1 - s0) / 1e3))
