@@ -160,10 +160,10 @@ struct Cfg {
     static_assert((BN > 256 ? 1 : 2) * BN + (kATmem ? ES * kSub * 32 : 0) + (kFp4 ? 64 : 0) <= 512,
                   "TMEM budget");
     // shared memory carve-up (offsets from the 1024-aligned base)
-    // epilogue staging: per warp 32 rows x 32 f32, row pitch 144 B (16 B of
-    // padding keeps both the row writes and the transposed reads conflict-free)
-    static constexpr int kStgPitch = 144;
-    static constexpr int kStgBytes = 32 * kStgPitch;
+    // epilogue staging: per warp 32 rows x 32 f32 = 4 KB in the SWIZZLE_128B layout
+    // (16-B chunk c of row r at (c ^ (r & 7))): conflict-free row writes and
+    // transposed reads, and the layout a TMA store consumes
+    static constexpr int kStgBytes = 32 * 128;
     static constexpr int off_exp = 0;
     static constexpr int off_pk = ES * kSuperBytes;
     // packed staging: per-thread cp.async rings (PD stages x 16 B per row), or
@@ -176,7 +176,7 @@ struct Cfg {
                                          : PD * kProducerWarps * 32 * 16 * kPlanes;
     static constexpr int off_popc_a = off_pk + kPkBytes;
     static constexpr int off_popc_b = off_popc_a + kSets * 2 * BM * 4;  // [set][buf][row]
-    static constexpr int off_epi = off_popc_b + kSets * 2 * BN * 4;
+    static constexpr int off_epi = ((off_popc_b + kSets * 2 * BN * 4 + 1023) / 1024) * 1024;
     static constexpr int off_bars = off_epi + kEpiWarps * kStgBytes;
     static constexpr int kNumBars = 2 * ES + 6 + 2 * kTmaSlots;
     static constexpr int off_tmem = off_bars + kNumBars * 8;
@@ -417,8 +417,8 @@ template <int BN, bool kATmem, int kVec, class ALoad, class BLoad, class Store, 
           bool kFp4 = false, int kSets = 1>
 __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value, kFp4, kSets>::kThreads, 1)
     xnor_umma_kernel(const __grid_constant__ ALoad aload, const __grid_constant__ BLoad bload,
-                     Store store, Epilogue ep, int64_t kw32, TileMap tmap, uint64_t *trace_buf,
-                     int dbg) {
+                     const __grid_constant__ Store store, Epilogue ep, int64_t kw32, TileMap tmap,
+                     uint64_t *trace_buf, int dbg) {
     auto trace = [&](int slot) { trace_at(trace_buf, slot); };
     // per-superstage pipeline timeline of CTA 0 (debug: dbg bit 16; u64 [4096 + ev * 256 + g])
     const bool stage_trace = trace_buf != nullptr && (dbg & 16) && blockIdx.x == 0;
@@ -1024,12 +1024,45 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                 }
                 if (dbg & 1024) {
                 } else if (ncontig) {
-                    const uint32_t row = stg + lane * C::kStgPitch;
+                    // staged 32 x 32 block: lane r writes its row (SW128 chunk swizzle)
+                    const uint32_t row = stg + lane * 128;
 #pragma unroll
                     for (int j = 0; j < 8; ++j)
-                        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(row + 16 * j),
+                        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(
+                                         row + ((j ^ (lane & 7)) << 4)),
                                      "f"(f[4 * j]), "f"(f[4 * j + 1]), "f"(f[4 * j + 2]),
                                      "f"(f[4 * j + 3]));
+                    // TMA store of the whole block when the output has a map and the block
+                    // does not straddle an image (conv) -- the TMA unit clips rows past M
+                    // and columns past N
+                    bool tma_st = store.has_map && !store.res && w == 32;  // (whole block in the tile)
+                    int64_t tb = 0, tp = nc;
+                    if constexpr (std::is_same<Store, ConvStore>::value) {
+                        tb = nc / store.ohw;
+                        tp = nc - tb * store.ohw;
+                        tma_st = tma_st && tp + 32 <= store.ohw;
+                    }
+                    if (tma_st) {
+                        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                        __syncwarp();
+                        if (lane == 0) {
+                            const uint64_t map = reinterpret_cast<uint64_t>(&store.omap);
+                            if constexpr (std::is_same<Store, ConvStore>::value)
+                                asm volatile(
+                                    "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(map),
+                                    "r"((int)tp), "r"((int)mq), "r"((int)tb), "r"(stg)
+                                    : "memory");
+                            else
+                                asm volatile(
+                                    "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(map),
+                                    "r"((int)tp), "r"((int)mq), "r"(stg)
+                                    : "memory");
+                            bulk_commit();
+                            bulk_wait_read<0>();  // staging reusable for the next block
+                        }
+                        __syncwarp();
+                        continue;
+                    }
                     __syncwarp();
                     // transposed write-out: lane = (row quarter, 4-column segment)
                     const int seg = lane & 7, rsub = lane >> 3;
@@ -1037,7 +1070,11 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                     if (4 * seg < w && n < N) {
                         float *col;
                         const bool v4 = store.col4(n, col);
-                        const uint32_t src = stg + rsub * C::kStgPitch + 16 * seg;
+                        // row 4 rr + rsub, chunk seg (rows 4 rr + rsub have r & 7 = 4 (rr & 1) + rsub)
+                        auto src_of = [&](int rr) {
+                            const int r = 4 * rr + rsub;
+                            return stg + r * 128 + ((seg ^ (r & 7)) << 4);
+                        };
                         if (v4 && mq + 32 <= M) {
                             // common case: 8 unpredicated 16-byte stores, pointer bumps only
                             float *dst = col + (mq + rsub) * ms;
@@ -1047,7 +1084,7 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                                 float4 t;
                                 asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
                                              : "=f"(t.x), "=f"(t.y), "=f"(t.z), "=f"(t.w)
-                                             : "r"(src + rr * 4 * C::kStgPitch));
+                                             : "r"(src_of(rr)));
                                 if (store.res) {  // fused residual add
                                     const float4 r = __ldg(reinterpret_cast<const float4 *>(store.res_of(dst)));
                                     t.x = __fadd_rn(t.x, r.x); t.y = __fadd_rn(t.y, r.y);
@@ -1064,7 +1101,7 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                                 float4 t;
                                 asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
                                              : "=f"(t.x), "=f"(t.y), "=f"(t.z), "=f"(t.w)
-                                             : "r"(src + rr * 4 * C::kStgPitch));
+                                             : "r"(src_of(rr)));
                                 if (v4) {
                                     float *dst = col + mr * ms;
                                     if (store.res) {
@@ -1095,6 +1132,7 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
             if (lane == 0) mbar_arrive(bar_tempty + 8 * buf);
             if (e == 0 && lane == 0 && it < 3) trace(5 + 3 * it);
         }
+        if (lane == 0) bulk_wait_all();  // TMA stores of this warp complete before exit
     }
 
     fence_before();
@@ -1189,6 +1227,34 @@ static int encode_conv(TmaConv &t, int box_words, int box_pixels, int64_t B) {
                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return set_error(BNN_ECUDA, "cuTensorMapEncodeIm2col failed");
     return BNN_OK;
+}
+
+// TMA store maps of the epilogue (32 x 32 f32 boxes, SWIZZLE_128B); silently
+// skipped (regular stores) when the output does not meet the TMA constraints
+static void encode_out(GemmStore &st) {
+    EncodeTiledFn fn = encode_tiled();
+    if (!fn || st.res || st.ldc_n != 1 || (st.ldc_m * 4) % 16 ||
+        (reinterpret_cast<uintptr_t>(st.C) & 15) || st.N > (1ll << 32) || st.M > (1ll << 32))
+        return;
+    const cuuint64_t dims[2] = {(cuuint64_t)st.N, (cuuint64_t)st.M};
+    const cuuint64_t strides[1] = {(cuuint64_t)st.ldc_m * 4};
+    const cuuint32_t box[2] = {32, 32}, estr[2] = {1, 1};
+    if (fn(&st.omap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, st.C, dims, strides, box, estr,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+           CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+        st.has_map = 1;
+}
+static void encode_out(ConvStore &st) {
+    EncodeTiledFn fn = encode_tiled();
+    if (!fn || st.res || (st.ohw * 4) % 16 || (reinterpret_cast<uintptr_t>(st.y) & 15)) return;
+    const int64_t B = st.npix / st.ohw;
+    const cuuint64_t dims[3] = {(cuuint64_t)st.ohw, (cuuint64_t)st.F, (cuuint64_t)B};
+    const cuuint64_t strides[2] = {(cuuint64_t)st.ohw * 4, (cuuint64_t)(st.F * st.ohw * 4)};
+    const cuuint32_t box[3] = {32, 32, 1}, estr[3] = {1, 1, 1};
+    if (fn(&st.omap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, st.y, dims, strides, box, estr,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+           CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+        st.has_map = 1;
 }
 
 template <int BN, bool kATmem, int kVec, class ALoad, class BLoad, class Store, int kPlanes = 1,
@@ -1333,6 +1399,7 @@ int launch_xnor_gemm_umma(const uint64_t *A, int64_t lda, const uint64_t *B, int
     DenseRows a{reinterpret_cast<const uint32_t *>(A), 2 * lda, M, kw32};
     DenseRows b{reinterpret_cast<const uint32_t *>(B), 2 * ldb, N, kw32};
     GemmStore st{C, ldc_m, ldc_n, M, N, res};
+    if (!(umma_dbg() & 4096)) encode_out(st);
     const bool vec4 = (lda % 2 == 0) && (ldb % 2 == 0) &&
                       ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) == 0;
     if (vec4 && !(umma_dbg() & 256)) {
@@ -1379,6 +1446,7 @@ int launch_bconv2d_umma(const uint64_t *x, int64_t B, int64_t C, int64_t H, int6
     ConvRows b{reinterpret_cast<const uint32_t *>(x), npix, (int)H, (int)W, (int)cs32, (int)C,
                (int)kw, (int)sh, (int)sw, (int)ph, (int)pw, (int)oh, (int)ow, kw32};
     ConvStore st{y, F, oh * ow, npix, res};
+    if (!(umma_dbg() & 4096)) encode_out(st);
     const bool vec4 = (cw64 % 2 == 0) &&
                       ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w)) & 15) == 0;
     // im2col TMA: whole 32-byte tap chunks (C % 256 == 0), corner offsets and

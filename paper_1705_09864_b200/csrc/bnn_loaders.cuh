@@ -6,6 +6,8 @@
 // store maps (m, n) of the GEMM view to the output tensor.
 #pragma once
 
+#include <cuda.h>
+
 #include "bnn_common.cuh"
 
 namespace bnn {
@@ -123,6 +125,10 @@ struct GemmStore {
     float *C;
     int64_t ldc_m, ldc_n, M, N;
     const float *res = nullptr;
+    // optional TMA store map over C ([M, N] f32, 32 x 32 boxes, SWIZZLE_128B);
+    // the tcgen05 epilogue uses it when has_map (row-major, no residual)
+    int has_map = 0;
+    CUtensorMap omap;
     __device__ bool ok(int64_t m, int64_t n) const { return m < M && n < N; }
     __device__ void put(int64_t m, int64_t n, float v) const {
         const int64_t i = m * ldc_m + n * ldc_n;
@@ -163,6 +169,9 @@ struct ConvStore {  // y NCHW [B, F, oh*ow]; m = filter, n = b*ohw + pixel
     float *y;
     int64_t F, ohw, npix;
     const float *res = nullptr;
+    // optional TMA store map over y ({ohw, F, B} f32, 32 x 32 x 1 boxes, SWIZZLE_128B)
+    int has_map = 0;
+    CUtensorMap omap;
     __device__ bool ok(int64_t m, int64_t n) const { return m < F && n < npix; }
     __device__ void put(int64_t m, int64_t n, float v) const {
         int64_t b = n / ohw, p = n - b * ohw;
