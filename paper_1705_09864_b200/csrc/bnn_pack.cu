@@ -498,28 +498,31 @@ __global__ void bn_relu_maxpool_kernel(const float *__restrict__ x, int64_t B, i
                                        int64_t H, int64_t W, const float *__restrict__ mean,
                                        const float *__restrict__ inv, const float *__restrict__ gamma,
                                        const float *__restrict__ beta, int relu, int k, int st,
-                                       int pd, int64_t OH, int64_t OW, float *__restrict__ y) {
-    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const int64_t total = B * C * OH * OW;
-    if (idx >= total) return;
-    const int64_t ox = idx % OW, oy = (idx / OW) % OH, c = (idx / (OW * OH)) % C,
-                  b = idx / (OW * OH * C);
+                                       int pd, int64_t OH, int64_t OW, float *__restrict__ y,
+                                       int bpp) {
+    // bpp blocks per (image, channel) plane; 32-bit index math inside the plane
+    const int64_t plane = blockIdx.x / bpp;
+    const int c = (int)(plane % C);
+    const int p = (int)(blockIdx.x - plane * bpp) * blockDim.x + threadIdx.x;
+    const int oh = (int)OH, ow = (int)OW, h = (int)H, w = (int)W;
+    if (p >= oh * ow) return;
+    const int oy = p / ow, ox = p - (p / ow) * ow;
     const float m = __ldg(mean + c), iv = __ldg(inv + c), g = __ldg(gamma + c), bt = __ldg(beta + c);
-    const float *src = x + (b * C + c) * H * W;
+    const float *src = x + plane * H * W;
     float best = -INFINITY;
     for (int i = 0; i < k; ++i) {
-        const int64_t iy = oy * st - pd + i;
-        if (iy < 0 || iy >= H) continue;
+        const int iy = oy * st - pd + i;
+        if (iy < 0 || iy >= h) continue;
         for (int j = 0; j < k; ++j) {
-            const int64_t ix = ox * st - pd + j;
-            if (ix < 0 || ix >= W) continue;
-            float v = __ldg(src + iy * W + ix);
+            const int ix = ox * st - pd + j;
+            if (ix < 0 || ix >= w) continue;
+            float v = __ldg(src + iy * w + ix);
             v = __fadd_rn(__fmul_rn(g, __fmul_rn(__fsub_rn(v, m), iv)), bt);
             if (relu) v = fmaxf(v, 0.0f);
             best = fmaxf(best, v);
         }
     }
-    y[idx] = best;
+    y[plane * OH * OW + p] = best;
 }
 
 // ================================================================ launchers
@@ -641,8 +644,11 @@ int launch_bn_relu_maxpool(const float *x, int64_t B, int64_t C, int64_t H, int6
     const int64_t OH = (H + 2 * pd - k) / st + 1, OW = (W + 2 * pd - k) / st + 1;
     const int64_t total = B * C * OH * OW;
     if (total == 0) return BNN_OK;
-    bn_relu_maxpool_kernel<<<(unsigned)ceil_div(total, 256), 256, 0, s>>>(
-        x, B, C, H, W, mean, inv, gamma, beta, relu, k, st, pd, OH, OW, y);
+    const int64_t bpp = ceil_div(OH * OW, 256);
+    if (OH * OW > (1ll << 30) || H * W > (1ll << 30) || B * C * bpp > 0x7fffffffll)
+        return set_error(BNN_EUNSUP, "bn_relu_maxpool: tensor too large");
+    bn_relu_maxpool_kernel<<<(unsigned)(B * C * bpp), 256, 0, s>>>(
+        x, B, C, H, W, mean, inv, gamma, beta, relu, k, st, pd, OH, OW, y, (int)bpp);
     return check_launch("bn_relu_maxpool_kernel");
 }
 

@@ -116,3 +116,14 @@ def test_lenet_end_to_end_vs_cpu_reference(nets):
     xin_gpu = cap[2].cpu().numpy()
     flips = np.mean((xin_gpu >= 0) != (nets_ref.forward(nets.Sequential(net.layers[:3]), x) >= 0))
     assert flips < 1e-3
+
+
+@pytest.mark.parametrize("shape,k,st,pd", [((2, 5, 17, 13), 3, 2, 1), ((1, 3, 8, 8), 2, 2, 0),
+                                           ((3, 4, 9, 11), 3, 1, 1)])
+def test_stem_post_kernel_equals_torch_ops(nets, shape, k, st, pd):
+    """bnn_bn_relu_maxpool_f32 is bit-identical to BatchNorm -> ReLU -> MaxPool."""
+    import paper_1705_09864_b200 as bnn
+    rng = np.random.default_rng(4)
+    post = nets.StemPost(shape[1], rng, k, st, pd)
+    x = torch.randn(shape, generator=torch.Generator().manual_seed(3)).cuda()
+    assert torch.equal(post.forward(x, bnn.INFER_PACKED), post.forward(x, bnn.INFER_FLOAT))

@@ -525,3 +525,44 @@ def test_pack_rows_segments_and_row_popcounts(bnn, r, k, pad):
     expect = orc.pack_rows(orc.binarize(x), pad)
     assert np.array_equal(got, expect)
     assert np.array_equal(pc.cpu().numpy(), (x >= 0).sum(1))
+
+
+def test_randomized_shapes_umma_routes_equal_popc(bnn):
+    """Seeded sweep over shapes that hit every tcgen05 route (cp.async i8, TMA kind::mxf4
+    with narrow / wide tiles, TMA-store and regular epilogues, dot domain, im2col convs
+    straddling images): the result equals the independently tested POPC engine."""
+    from paper_1705_09864_b200 import _lib
+    rng = np.random.default_rng(2024)
+    dense = [(1, 1, 64), (3, 5, 100), (128, 16, 256), (130, 300, 512), (256, 20000, 2304),
+             (200, 37, 4096), (640, 1000, 1000), (96, 4097, 768), (1024, 256, 4096)]
+    for m, n, k in dense:
+        W = (k + 63) // 64
+        g = torch.Generator(device="cuda").manual_seed(m * 7 + n + k)
+        a = torch.randint(-2**63, 2**63 - 1, (m, W), device="cuda", generator=g).view(torch.uint64)
+        b = torch.randint(-2**63, 2**63 - 1, (n, W), device="cuda", generator=g).view(torch.uint64)
+        if k % 64:  # layout 'a' tails 0 (both operands, the rows API)
+            mask = (1 << (k % 64)) - 1
+            a.view(torch.int64)[:, -1] &= mask
+            b.view(torch.int64)[:, -1] &= mask
+        for dom in (_lib.POPCOUNT, _lib.DOT):
+            ref = bnn.xnor_rows_gemm(a, b, k, algo="popc", domain=dom)
+            for v in (2, 1):
+                A(f"umma{v}")
+                got = bnn.xnor_rows_gemm(a, b, k, algo="umma", domain=dom)
+                assert torch.equal(got, ref), (m, n, k, dom, v)
+            A("umma2")
+    convs = [(3, 256, 13, 9, 70, 3, 3, (1, 1), (1, 1)), (8, 256, 28, 28, 256, 3, 3, (1, 1), (1, 1)),
+             (4, 512, 7, 7, 96, 1, 1, (1, 1), (0, 0)), (2, 256, 15, 15, 300, 3, 3, (2, 2), (1, 1))]
+    for i, (b_, c, h, w, f, kh, kw, st, pd) in enumerate(convs):
+        x = rng.standard_normal((b_, c, h, w), dtype=np.float32)
+        wt = rng.standard_normal((f, c, kh, kw), dtype=np.float32)
+        outs = []
+        for algo in ("popc", "umma2", "umma1"):
+            layer = bnn.QConvolution(c, f, (kh, kw), st, pd)
+            layer.weight = wt
+            layer.pack()
+            layer.algo = A(algo)
+            outs.append(layer.forward(torch.from_numpy(x).cuda(), bnn.INFER_PACKED).cpu().numpy())
+        A("umma2")
+        assert np.array_equal(outs[1], outs[0]), ("conv", i)
+        assert np.array_equal(outs[2], outs[0]), ("conv", i)
