@@ -230,6 +230,10 @@ int bnn_bconv2d_ex(const uint64_t *x_words, int64_t B, int64_t C, int64_t H, int
                    int64_t sw, int64_t ph, int64_t pw, float *y, const bnn_epilogue *ep, int algo,
                    bnn_stream_t stream);
 
+/* Debug: arm the tcgen05 engine's wait watchdog with a device u64[65] log (a wait that
+ * does not complete in ~2 s records block / warp / barrier / parity and traps), or null. */
+int bnn_umma_watchdog(uint64_t *log);
+
 /* Debug: *dst = %globaltimer (ns) when a one-thread kernel on `stream` runs. */
 int bnn_debug_stamp(uint64_t *dst, bnn_stream_t stream);
 

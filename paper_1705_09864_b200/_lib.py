@@ -55,6 +55,7 @@ SIGNATURES = {
                               _i64, _i64, _vp, _vp, _i32, _vp]),
     "bnn_umma_trace": (_i32, [_vp]),
     "bnn_debug_stamp": (_i32, [_vp, _vp]),
+    "bnn_umma_watchdog": (_i32, [_vp]),
 }
 
 

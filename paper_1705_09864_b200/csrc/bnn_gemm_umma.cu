@@ -47,6 +47,22 @@
 #ifndef BNN_FP4_ES
 #define BNN_FP4_ES 3
 #endif
+#ifndef BNN_PAIR_ES
+#define BNN_PAIR_ES 5  // expanded buffers of a CTA pair: hide the cluster-scope arrival latency
+#endif
+#ifndef BNN_MARK_FENCE
+#define BNN_MARK_FENCE 1
+#endif
+#ifndef BNN_FP4_PAIR_KW32
+// K words (u32) from which 2-CTA pairs are used (M >= 256).  Off by default: every
+// superstage of a pair needs one cluster-scope release/arrive from the peer CTA,
+// measured at ~0.7 us each, which caps the pair below the single-CTA engine
+// (8192^3: 2.5 vs 3.7 POPS).  BNN_PAIR_KW32=<n> enables it for experiments.
+#define BNN_FP4_PAIR_KW32 (1ll << 40)
+#endif
+#ifndef BNN_FP4_SETS_KW32
+#define BNN_FP4_SETS_KW32 192  // K words (u32) from which two expander sets are used
+#endif
 #ifndef BNN_FP4_TMA_SLOTS
 #define BNN_FP4_TMA_SLOTS 4
 #endif
@@ -112,8 +128,14 @@ constexpr int kWordsPerStage = 4;  // u32 words of K per row per stage
 constexpr int kRowBytes = 128;     // expanded bytes per row per stage
 
 template <int BN, bool kATmem, int kPlanes = 1, bool kTma = false, bool kFp4 = false,
-          int kSetsT = 1>
+          int kSetsT = 1, bool kPair = false>
 struct Cfg {
+    // kPair: a cluster of two CTAs computes a 256 x BN tile with tcgen05.mma.cta_group::2
+    // (issued by the even CTA); each CTA expands its 128 A rows and half of the BN B rows,
+    // so per MAC the B-operand expansion, SMEM stores and SMEM operand reads halve
+    static_assert(!kPair || (kFp4 && kTma && kSetsT == 1 && BN <= 256), "pair: fp4, TMA, one set");
+    static constexpr int kBRows = kPair ? BN / 2 : BN;  // B rows expanded by this CTA
+    static constexpr int kTmBM = kPair ? 2 * BM : BM;    // tile rows
     static_assert(BN % 16 == 0 && BN >= 16 && (BN <= 256 || (kFp4 && BN % 32 == 0 && BN <= 384)),
                   "UMMA N for M=128 (wide fp4 tiles: two MMAs of N/2)");
     // tiles wider than one MMA (fp4, N <= 384) issue two MMAs of N/2 per K step into
@@ -122,7 +144,7 @@ struct Cfg {
     static constexpr int kMmaN = BN > 256 ? BN / 2 : BN;
     static constexpr int kNMma = BN / kMmaN;
     static_assert(!kFp4 || (!kATmem && kPlanes == 1 && kTma), "fp4 engine: SS operands, TMA-fed");
-    static constexpr int kProducers = BM + BN;                 // one thread per operand row
+    static constexpr int kProducers = BM + kBRows;             // one thread per operand row
     static constexpr int kProducerWarps = (kProducers + 31) / 32;
     // kind::mxf4: two expander sets take alternate superstages, so each warp's
     // barrier round trip (slot wait, popcounts, release, buffer wait, proxy fence,
@@ -146,10 +168,10 @@ struct Cfg {
     // fp4 superstage row is one 128-byte SW128 row; A rows precede B rows)
     static constexpr int kStageRow = kFp4 ? 64 : kRowBytes;
     static constexpr int kStageA = kATmem ? 0 : BM * kStageRow;
-    static constexpr int kStageB = BN * kStageRow;
+    static constexpr int kStageB = kBRows * kStageRow;
     static constexpr int kStageBytes = kStageA + kStageB;
     static constexpr int kSuperBytes = kSub * kStageBytes;
-    static constexpr int ES = kATmem ? 2 : (kFp4 ? (BN > 256 ? 2 : (BN <= 176 ? BNN_FP4_ES : 3)) : 3);  // expanded superstage buffers
+    static constexpr int ES = kATmem ? 2 : (kPair ? BNN_PAIR_ES : (kFp4 ? (BN > 256 ? 2 : (BN <= 176 ? BNN_FP4_ES : 3)) : 3));  // expanded superstage buffers
     static constexpr int kFp4A = BM * 128;      // fp4: A block of a superstage buffer
     // TMEM: 2 accumulator buffers of BN columns (+ ES x kSub A stages of 32 columns)
     static constexpr int kAccCols = BN;
@@ -169,14 +191,14 @@ struct Cfg {
     // packed staging: per-thread cp.async rings (PD stages x 16 B per row), or
     // with TMA kTmaSlots superstage slots of [A rows | B rows] x kSub x 16 B
     static constexpr int kTmaSlots = (kFp4 && BN > 256) ? 3 : ((kFp4 && BN <= 176) ? BNN_FP4_TMA_SLOTS : 4);
-    static constexpr int kTmaA = BM * kSub * 16, kTmaB = BN * kSub * 16;
-    static constexpr int kTmaBoxB = BN > 256 ? BN / 2 : BN;  // tiled TMA boxes are <= 256 rows
+    static constexpr int kTmaA = BM * kSub * 16, kTmaB = kBRows * kSub * 16;
+    static constexpr int kTmaBoxB = BN > 256 ? BN / 2 : kBRows;  // tiled TMA boxes are <= 256 rows
     static constexpr int kTmaSlotBytes = ((kTmaA + kTmaB + 1023) / 1024) * 1024;
     static constexpr int kPkBytes = kTma ? kTmaSlots * kTmaSlotBytes
                                          : PD * kProducerWarps * 32 * 16 * kPlanes;
     static constexpr int off_popc_a = off_pk + kPkBytes;
     static constexpr int off_popc_b = off_popc_a + kSets * 2 * BM * 4;  // [set][buf][row]
-    static constexpr int off_epi = ((off_popc_b + kSets * 2 * BN * 4 + 1023) / 1024) * 1024;
+    static constexpr int off_epi = ((off_popc_b + kSets * 2 * kBRows * 4 + 1023) / 1024) * 1024;
     static constexpr int off_bars = off_epi + kEpiWarps * kStgBytes;
     static constexpr int kNumBars = 2 * ES + 6 + 2 * kTmaSlots;
     static constexpr int off_tmem = off_bars + kNumBars * 8;
@@ -186,7 +208,7 @@ struct Cfg {
                                        ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
     // kind::mxf4: E2M1 x E2M1 (format 1), UE8M0 scales (bit 23), f32 accumulate
     static constexpr uint32_t kIdescFp4 = (1u << 7) | (1u << 10) | ((uint32_t)(kMmaN >> 3) << 17) |
-                                          (1u << 23) | ((uint32_t)(BM >> 4) << 24);
+                                          (1u << 23) | ((uint32_t)(kTmBM >> 4) << 24);
 };
 
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
@@ -200,6 +222,67 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 __device__ __forceinline__ void mbar_arrive_dep(uint32_t bar, int32_t dep) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n// dep %1\n" ::"r"(bar), "r"(dep)
                  : "memory");
+}
+// debug watchdog (bnn_umma_watchdog): a wait that
+// does not complete within ~2 s logs (block, warp, barrier offset, parity) and traps
+__device__ uint64_t *g_wait_log = nullptr;
+__device__ __noinline__ void wait_timeout(uint32_t bar, uint32_t phase, uint32_t tries) {
+    if (tries == (1u << 22) + 1 && g_wait_log && (threadIdx.x & 31) == 0) {  // record once per warp
+        const uint32_t slot = atomicAdd(reinterpret_cast<unsigned int *>(g_wait_log), 1u) % 64u;
+        g_wait_log[1 + slot] = ((uint64_t)blockIdx.x << 48) | ((uint64_t)(threadIdx.x >> 5) << 40) |
+                               ((uint64_t)(bar & 0xFFFFF) << 8) | phase;
+        uint64_t state;
+        asm volatile("ld.shared.b64 %0, [%1];\n" : "=l"(state) : "r"(bar));
+        if (slot < 32) g_wait_log[65 + 8 * 16 + slot] = state;  // raw mbarrier word
+        __threadfence_system();
+    }
+    if (tries > (1u << 23)) asm volatile("trap;");  // every stuck warp has recorded by now
+}
+// cluster (2-CTA pair) helpers: address of the same shared variable in CTA `rank`,
+// release/acquire arrivals and waits at cluster scope
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t phase) {
+    uint32_t done = 0;
+    uint32_t tries = 0;
+    do {
+        if (g_wait_log && ++tries > (1u << 22)) wait_timeout(bar, phase, tries);
+        asm volatile(
+            "{\n.reg .pred p;\n"
+            "mbarrier.test_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(bar), "r"(phase)
+            : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::
+                     : "memory");
+}
+template <uint32_t kIdesc>
+__device__ __forceinline__ void mma_fp4_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                             uint32_t sfa, uint32_t sfb, uint32_t accumulate) {
+    asm volatile(
+        "{\n.reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n}\n" ::"r"(
+            tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate), "r"(sfa), "r"(sfb));
+}
+__device__ __forceinline__ void umma_commit_pair(uint32_t bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+            bar),
+        "h"((uint16_t)3)
+        : "memory");
 }
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
@@ -223,12 +306,21 @@ __device__ __forceinline__ void tma_load_im2col_4d(uint32_t dst, const CUtensorM
         "h"(off_w), "h"(off_h)
         : "memory");
 }
+// debug progress marks next to the watchdog log: g_wait_log[65 + 8 * block + k] = v
+__device__ __forceinline__ void progress_mark(int k, uint64_t v) {
+    if (g_wait_log && blockIdx.x < 16) {
+        g_wait_log[65 + 8 * blockIdx.x + k] = v;
+        if (BNN_MARK_FENCE) __threadfence_system();
+    }
+}
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
     // the suspend-time hint parks the warp in try_wait until the phase
     // completes instead of re-issuing the probe (spinning warps steal issue
     // slots from the expanders sharing their scheduler)
     uint32_t done = 0;
+    uint32_t tries = 0;
     do {
+        if (g_wait_log && ++tries > (1u << 22)) wait_timeout(bar, phase, tries);
         asm volatile(
             "{\n.reg .pred p;\n"
             "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
@@ -242,7 +334,9 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
 // instead of spinning on the issue slots the producers need
 __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t phase) {
     uint32_t done = 0;
+    uint32_t tries = 0;
     do {
+        if (g_wait_log && ++tries > (1u << 22)) wait_timeout(bar, phase, tries);
         asm volatile(
             "{\n.reg .pred p;\n"
             "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
@@ -414,20 +508,24 @@ template <>
 struct is_tma<TmaConv> { static constexpr bool value = true; };
 
 template <int BN, bool kATmem, int kVec, class ALoad, class BLoad, class Store, int kPlanes = 1,
-          bool kFp4 = false, int kSets = 1>
-__global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value, kFp4, kSets>::kThreads, 1)
+          bool kFp4 = false, int kSets = 1, bool kPair = false>
+__global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value, kFp4, kSets, kPair>::kThreads, 1)
     xnor_umma_kernel(const __grid_constant__ ALoad aload, const __grid_constant__ BLoad bload,
                      const __grid_constant__ Store store, Epilogue ep, int64_t kw32, TileMap tmap,
                      uint64_t *trace_buf, int dbg) {
     auto trace = [&](int slot) { trace_at(trace_buf, slot); };
     // per-superstage pipeline timeline of CTA 0 (debug: dbg bit 16; u64 [4096 + ev * 256 + g])
-    const bool stage_trace = trace_buf != nullptr && (dbg & 16) && blockIdx.x == 0;
-    auto tr = [&](int ev, uint32_t g) {
-        if (stage_trace && g < 256) trace_buf[4096 + ev * 256 + g] = clock64();
+    const bool stage_trace = trace_buf != nullptr && (dbg & 16) && blockIdx.x < 2;
+    auto tr = [&](int ev, uint32_t g) {  // blocks 0 and 1 (both CTAs of the first pair)
+        if (stage_trace && g < 256) {
+            uint64_t t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            trace_buf[4096 + blockIdx.x * 4096 + ev * 256 + g] = t;
+        }
     };
     constexpr bool kTma = is_tma<ALoad>::value;
     static_assert(kTma == is_tma<BLoad>::value && (!kTma || kPlanes == 1), "TMA: both operands");
-    using C = Cfg<BN, kATmem, kPlanes, kTma, kFp4, kSets>;
+    using C = Cfg<BN, kATmem, kPlanes, kTma, kFp4, kSets, kPair>;
     constexpr int ES = C::ES;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t sbase_raw = smem_u32(smem_raw);
@@ -449,17 +547,23 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t ktiles = ceil_div(kw32, kWordsPerStage);
+    uint32_t crank = 0;  // rank in the CTA pair (kPair); rank 0 issues the MMAs
+    if constexpr (kPair) asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(crank));
+    const uint32_t peer = crank ^ 1u;
+    const int t0 = kPair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;       // first tile
+    const int tstep = kPair ? (int)(gridDim.x >> 1) : (int)gridDim.x;      // tile stride
 
     if (tid == 0) {
         trace(0);
         for (int s = 0; s < ES; ++s) {
-            mbar_init(bar_full + 8 * s, C::kProducerWarps);
+            // pair: the leader's full[] takes its own warps + one relayed arrival from the peer
+            mbar_init(bar_full + 8 * s, C::kProducerWarps + ((kPair && crank == 0) ? 1 : 0));
             mbar_init(bar_empty + 8 * s, 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(bar_tfull + 8 * b, 1);
-            mbar_init(bar_tempty + 8 * b, C::kEpiWarps);
-            mbar_init(bar_pfull + 8 * b, C::kExpWarps);
+            mbar_init(bar_tempty + 8 * b, (kPair ? 2 : 1) * C::kEpiWarps);
+            mbar_init(bar_pfull + 8 * b, (kPair ? 2 : 1) * C::kExpWarps);
         }
         for (int r = 0; r < C::kTmaSlots; ++r) {
             mbar_init(bar_ld + 8 * r, 1);
@@ -468,10 +572,17 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     if (warp == C::kMmaWarp) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
-                         smem_u32(s_tmem)),
-                     "n"(C::kTmemCols));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+        if constexpr (kPair) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                             smem_u32(s_tmem)),
+                         "n"(C::kTmemCols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                             smem_u32(s_tmem)),
+                         "n"(C::kTmemCols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+        }
     }
     if constexpr (kTma) {
         if (tid == 0) {  // descriptor prefetch does not depend on the previous kernel
@@ -481,6 +592,7 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
     }
     fence_before();
     __syncthreads();
+    if constexpr (kPair) cluster_sync();  // the peer's barriers exist before any remote arrival
     fence_after();
     const uint32_t tmem = *s_tmem;
     // programmatic dependent launch: the setup above (barriers, TMEM allocation,
@@ -512,7 +624,7 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
         const uint32_t ring = s_pk + tid * 16 * kPlanes;  // slot-major private ring
         constexpr uint32_t kRingSlot = C::kProducerWarps * 32 * 16 * kPlanes;
         // fetch iterator (runs PD - kSub stages ahead, across tile boundaries)
-        int f_tile = blockIdx.x;
+        int f_tile = t0;
         uint32_t f_kt = 0;
         const uint32_t kt32 = (uint32_t)ktiles;
         typename ALoad::Cursor fa{};
@@ -521,8 +633,8 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
             if (t >= tmap.ntiles || !active) return;
             int tm, tn;
             tmap.decode(t, tm, tn);
-            if (is_a) fa = aload.row((int64_t)tm * BM + row);
-            else fb = bload.row((int64_t)tn * BN + row);
+            if (is_a) fa = aload.row((int64_t)tm * C::kTmBM + crank * BM + row);
+            else fb = bload.row((int64_t)tn * BN + crank * C::kBRows + row);
         };
         set_cursor(f_tile);
         uint32_t f_count = 0;  // stages fetched so far
@@ -541,7 +653,7 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                 ++f_count;
                 if (++f_kt == kt32) {
                     f_kt = 0;
-                    f_tile += gridDim.x;
+                    f_tile += tstep;
                     set_cursor(f_tile);
                 }
             }
@@ -562,7 +674,7 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
             uint32_t gs = 0;  // global superstage counter (expanded buffers / phases)
             int it = 0;
     #pragma unroll 1
-            for (int tile = blockIdx.x; tile < tmap.ntiles; tile += gridDim.x, ++it) {
+            for (int tile = t0; tile < tmap.ntiles; tile += tstep, ++it) {
                 int32_t my_popc = 0;
                 // im2col route: this B row's window corner and the running tap
                 int c_iy0 = 0, c_ix0 = 0, c_cw = 0, c_i = 0, c_j = 0;
@@ -570,7 +682,7 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                     int tm, tn;
                     tmap.decode(tile, tm, tn);
                     const int64_t ohw = (int64_t)bload.oh * bload.ow;
-                    const int64_t n = (int64_t)tn * BN + (is_a ? 0 : row);
+                    const int64_t n = (int64_t)tn * BN + crank * C::kBRows + (is_a ? 0 : row);
                     const int p = (int)(n % ohw);
                     c_iy0 = (p / bload.ow) * bload.sh - bload.ph;
                     c_ix0 = (p % bload.ow) * bload.sw - bload.pw;
@@ -738,7 +850,7 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                     __syncwarp();  // every lane's writes + fence precede the warp's arrival
                     if (lane == 0 && (warp == 0 || warp == C::kProducerWarps - 1)) tr(warp ? 5 : 2, gs);
                     if (lane == 0) {
-                        mbar_arrive(bar_full + 8 * sb);
+                        mbar_arrive(bar_full + 8 * sb);  // (pair: rank 1 relays to the leader)
                     }
                     gk += nsub;
                 }
@@ -748,9 +860,16 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                     mbar_wait(bar_tempty + 8 * buf, (uint32_t)((it / C::kAccBufs) - 1) & 1u);
                 if (is_a) s_popc_a[(set * 2 + buf) * BM + row] = my_popc;
                 else if (active)  // (f32 bits on the fp4 engine, whose epilogue decodes in f32)
-                    s_popc_b[(set * 2 + buf) * BN + row] = kFp4 ? __float_as_int((float)my_popc) : my_popc;
+                    s_popc_b[(set * 2 + buf) * C::kBRows + row] = kFp4 ? __float_as_int((float)my_popc) : my_popc;
                 __syncwarp();
-                if (lane == 0) mbar_arrive(bar_pfull + 8 * buf);
+                if (lane == 0) {
+                    if constexpr (kPair) {  // both CTAs' epilogues read these B popcounts
+                        mbar_arrive_cluster(mapa_shared(bar_pfull + 8 * buf, crank));
+                        mbar_arrive_cluster(mapa_shared(bar_pfull + 8 * buf, peer));
+                    } else {
+                        mbar_arrive(bar_pfull + 8 * buf);
+                    }
+                }
             }
         };
         if (is_a) run(std::true_type{});
@@ -765,13 +884,14 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                 const uint32_t kt32 = (uint32_t)ktiles;
                 uint32_t g = 0;
 #pragma unroll 1
-                for (int tile = blockIdx.x; tile < tmap.ntiles; tile += gridDim.x) {
+                for (int tile = t0; tile < tmap.ntiles; tile += tstep) {
                     int tm, tn;
                     tmap.decode(tile, tm, tn);
                     // im2col start: the tile's first output pixel (b, oy, ox) -> window corner
                     int cw = 0, ci = 0, cj = 0, cx = 0, cy = 0, cb = 0;
                     if constexpr (std::is_same<BLoad, TmaConv>::value) {
-                        const int64_t n0 = (int64_t)tn * BN, ohw = (int64_t)bload.oh * bload.ow;
+                        const int64_t n0 = (int64_t)tn * BN + crank * C::kBRows;
+                        const int64_t ohw = (int64_t)bload.oh * bload.ow;
                         cb = (int)(n0 / ohw);
                         const int p = (int)(n0 - (int64_t)cb * ohw);
                         cy = (p / bload.ow) * bload.sh - bload.ph;
@@ -782,10 +902,17 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                         const uint32_t ts = g % C::kTmaSlots;
                         if (g >= (uint32_t)C::kTmaSlots)
                             mbar_wait(bar_free + 8 * ts, ((g / C::kTmaSlots) - 1) & 1u);
-                        const uint32_t dst = s_pk + ts * C::kTmaSlotBytes;
+                        uint32_t dst = s_pk + ts * C::kTmaSlotBytes;
+                        uint32_t ldbar = bar_ld + 8 * ts;
+                        if (kPair && (dbg & 131072)) {  // debug: explicit shared::cluster addresses
+                            dst = mapa_shared(dst, crank);
+                            ldbar = mapa_shared(ldbar, crank);
+                        }
                         tr(0, g);
+                        if (g == 0) progress_mark(0, 1000 + (uint64_t)tm * 100 + tn);
                         mbar_arrive_expect_tx(bar_ld + 8 * ts, C::kTmaA + C::kTmaB);
-                        tma_load_2d(dst, &aload.map, (int)(kt * kWordsPerStage), tm * BM, bar_ld + 8 * ts);
+                        tma_load_2d(dst, &aload.map, (int)(kt * kWordsPerStage),
+                                    tm * C::kTmBM + (int)crank * BM, ldbar);
                         if constexpr (std::is_same<BLoad, TmaConv>::value) {
                             // superstage kt: tap (ci, cj), channel words cw .. cw + 8
                             tma_load_im2col_4d(dst + C::kTmaA, &bload.map, cw, cx, cy, cb,
@@ -797,8 +924,8 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                             }
                         } else {
                             tma_load_2d(dst + C::kTmaA, &bload.map, (int)(kt * kWordsPerStage),
-                                        tn * BN, bar_ld + 8 * ts);
-                            if constexpr (C::kTmaBoxB != BN)  // second box of a wide tile
+                                        tn * BN + (int)crank * C::kBRows, ldbar);
+                            if constexpr (BN > 256)  // second box of a wide tile
                                 tma_load_2d(dst + C::kTmaA + C::kTmaBoxB * C::kSub * 16, &bload.map,
                                             (int)(kt * kWordsPerStage), tn * BN + C::kTmaBoxB,
                                             bar_ld + 8 * ts);
@@ -816,7 +943,18 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
             constexpr uint32_t kSub = C::kSub;
             int it = 0;
 #pragma unroll 1
-            for (int tile = blockIdx.x; tile < tmap.ntiles; tile += gridDim.x, ++it) {
+            for (int tile = t0; tile < tmap.ntiles; tile += tstep, ++it) {
+                if (kPair && crank != 0) {
+                    // rank 1 relays: once its expanders filled superstage gs locally, one
+                    // cluster-scope arrival on the leader's full[] (cumulative release)
+#pragma unroll 1
+                    for (uint32_t kt = 0; kt < kt32; kt += kSub, ++gs) {
+                        const int sb = (int)(gs % ES);
+                        mbar_wait(bar_full + 8 * sb, (gs / ES) & 1u);
+                        mbar_arrive_cluster(mapa_shared(bar_full + 8 * sb, 0));
+                    }
+                    continue;
+                }
                 const int buf = it % C::kAccBufs;
                 if (it >= C::kAccBufs)
                     mbar_wait(bar_tempty + 8 * buf, (uint32_t)((it / C::kAccBufs) - 1) & 1u);
@@ -826,7 +964,10 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                 for (uint32_t kt = 0; kt < kt32; kt += kSub, ++gs) {
                     const uint32_t nsub = kt32 - kt < kSub ? kt32 - kt : kSub;
                     const int sb = (int)(gs % ES);
-                    mbar_wait(bar_full + 8 * sb, (gs / ES) & 1u);
+                    if (gs == 0) progress_mark(1, 1);
+                    if constexpr (kPair) mbar_wait_cluster(bar_full + 8 * sb, (gs / ES) & 1u);
+                    else mbar_wait(bar_full + 8 * sb, (gs / ES) & 1u);
+                    if (gs == 0) progress_mark(2, 2);
                     tr(7, gs);
                     if (gs == 0) trace(2);
                     fence_after();
@@ -838,6 +979,12 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                         for (int kk = 0; kk < 4; ++kk) {
                             if ((dbg & 2) || kk >= 2 * (int)nsub) break;
                             const uint32_t acc = (kt | kk) != 0 ? 1u : 0u;
+                            if constexpr (kPair) {  // 256 x BN: A and B halves from both CTAs
+                                mma_fp4_pair<C::kIdescFp4>(d, sw128_desc(a_addr + kk * 32),
+                                                           sw128_desc(b_addr + kk * 32),
+                                                           tmem + C::kSfCol, tmem + C::kSfCol, acc);
+                                continue;
+                            }
                             mma_fp4<C::kIdescFp4>(d, sw128_desc(a_addr + kk * 32),
                                                   sw128_desc(b_addr + kk * 32), tmem + C::kSfCol,
                                                   tmem + C::kSfCol, acc);
@@ -864,10 +1011,12 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                                                   sw128_desc(b_addr + kk * 32), acc);
                         }
                     }
-                    umma_commit(bar_empty + 8 * sb);
+                    if constexpr (kPair) umma_commit_pair(bar_empty + 8 * sb);
+                    else umma_commit(bar_empty + 8 * sb);
                     tr(8, gs);
                 }
-                umma_commit(bar_tfull + 8 * buf);
+                if constexpr (kPair) umma_commit_pair(bar_tfull + 8 * buf);
+                else umma_commit(bar_tfull + 8 * buf);
                 if (it < 3) trace(3 + 3 * it);
             }
             // release TMEM as soon as the epilogue has drained the last two
@@ -878,8 +1027,12 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
         }
         __syncwarp();
         fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
-                     "n"(C::kTmemCols));
+        if constexpr (kPair)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
+                         "n"(C::kTmemCols));
+        else
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
+                         "n"(C::kTmemCols));
         if (lane == 0) trace(13);
     } else {
         // ================================================================ epilogue
@@ -900,11 +1053,11 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
         const bool plain = (magic || kFp4) && !affine && ep.bn_mean == nullptr;  // straight-line decode
         int it = 0;
 #pragma unroll 1
-        for (int tile = blockIdx.x; tile < tmap.ntiles; tile += gridDim.x, ++it) {
+        for (int tile = t0; tile < tmap.ntiles; tile += tstep, ++it) {
             const int buf = it % C::kAccBufs;
             int tm, tn;
             tmap.decode(tile, tm, tn);
-            const int64_t mq = (int64_t)tm * BM + q * 32, n0 = (int64_t)tn * BN;
+            const int64_t mq = (int64_t)tm * C::kTmBM + crank * BM + q * 32, n0 = (int64_t)tn * BN;
             const int64_t m = mq + lane;
             mbar_wait_sleep(bar_tfull + 8 * buf, (uint32_t)(it / C::kAccBufs) & 1u);
             mbar_wait_sleep(bar_pfull + 8 * buf, (uint32_t)(it / C::kAccBufs) & 1u);
@@ -913,7 +1066,14 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
             if (dbg & 2048) {  // debug: skip the whole epilogue (wrong outputs)
                 fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(bar_tempty + 8 * buf);
+                if (lane == 0) {
+                    if constexpr (kPair) {  // the leader's MMA and both CTAs' producers wait
+                        mbar_arrive_cluster(mapa_shared(bar_tempty + 8 * buf, crank));
+                        mbar_arrive_cluster(mapa_shared(bar_tempty + 8 * buf, peer));
+                    } else {
+                        mbar_arrive(bar_tempty + 8 * buf);
+                    }
+                }
                 continue;
             }
             const bool mok = m < M;
@@ -936,8 +1096,8 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
             const float bi = (mok && has_bn) ? __ldg(ep.bn_inv + m) : 1.0f;
             const float bg = (mok && has_bn) ? __ldg(ep.bn_gamma + m) : 1.0f;
             const float bb = (mok && has_bn) ? __ldg(ep.bn_beta + m) : 0.0f;
-            const int32_t *pb = s_popc_b + buf * BN;
-            const int32_t *pb1 = s_popc_b + (2 + buf) * BN;  // second expander set (kSets == 2)
+            const int32_t *pb = s_popc_b + buf * C::kBRows;
+            const int32_t *pb1 = s_popc_b + (2 + buf) * C::kBRows;  // second expander set (kSets == 2)
             const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + buf * C::kAccCols;
 #pragma unroll 1
             for (int c = h; c * 32 < BN; c += C::kEpiWarps / 4) {
@@ -972,7 +1132,19 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                     // (2kb - K) - 2pb + 4C, every term an exact f32 integer
 #pragma unroll
                     for (int j4 = 0; j4 < 8; ++j4) {
-                        float4 pb4 = *reinterpret_cast<const float4 *>(pb + c * 32 + 4 * j4);
+                        float4 pb4;
+                        if constexpr (kPair) {
+                            // B popcounts of columns [r * N/2, (r+1) * N/2) live in CTA r
+                            const int col = c * 32 + 4 * j4;
+                            const uint32_t owner = (uint32_t)(col / C::kBRows);
+                            const uint32_t a = mapa_shared(
+                                smem_u32(pb + (col - (int)owner * C::kBRows)), owner);
+                            asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+                                         : "=f"(pb4.x), "=f"(pb4.y), "=f"(pb4.z), "=f"(pb4.w)
+                                         : "r"(a));
+                        } else {
+                            pb4 = *reinterpret_cast<const float4 *>(pb + c * 32 + 4 * j4);
+                        }
                         if constexpr (C::kSets > 1) {
                             const float4 q4 = *reinterpret_cast<const float4 *>(pb1 + c * 32 + 4 * j4);
                             pb4.x += q4.x; pb4.y += q4.y; pb4.z += q4.z; pb4.w += q4.w;
@@ -1129,7 +1301,14 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
             }
             fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(bar_tempty + 8 * buf);
+            if (lane == 0) {
+                    if constexpr (kPair) {  // the leader's MMA and both CTAs' producers wait
+                        mbar_arrive_cluster(mapa_shared(bar_tempty + 8 * buf, crank));
+                        mbar_arrive_cluster(mapa_shared(bar_tempty + 8 * buf, peer));
+                    } else {
+                        mbar_arrive(bar_tempty + 8 * buf);
+                    }
+                }
             if (e == 0 && lane == 0 && it < 3) trace(5 + 3 * it);
         }
         if (lane == 0) bulk_wait_all();  // TMA stores of this warp complete before exit
@@ -1137,6 +1316,9 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
 
     fence_before();
     __syncthreads();
+    // a CTA of a pair stays resident until its peer no longer reads its SMEM or
+    // arrives on its barriers
+    if constexpr (kPair) cluster_sync();
     if (tid == 0) trace(12);
 }
 
@@ -1258,19 +1440,19 @@ static void encode_out(ConvStore &st) {
 }
 
 template <int BN, bool kATmem, int kVec, class ALoad, class BLoad, class Store, int kPlanes = 1,
-          bool kFp4 = false, int kSets = 1>
+          bool kFp4 = false, int kSets = 1, bool kPair = false>
 static int launch_umma_cfg(const ALoad &a_in, const BLoad &b_in, const Store &st, const Epilogue &ep,
                            int64_t M, int64_t N, int64_t kw32, cudaStream_t s) {
     constexpr bool kTma = umma::is_tma<ALoad>::value;
-    using C = umma::Cfg<BN, kATmem, kPlanes, kTma, kFp4, kSets>;
-    auto kern = umma::xnor_umma_kernel<BN, kATmem, kVec, ALoad, BLoad, Store, kPlanes, kFp4, kSets>;
+    using C = umma::Cfg<BN, kATmem, kPlanes, kTma, kFp4, kSets, kPair>;
+    auto kern = umma::xnor_umma_kernel<BN, kATmem, kVec, ALoad, BLoad, Store, kPlanes, kFp4, kSets, kPair>;
     ALoad a = a_in;
     BLoad b = b_in;
     if constexpr (kTma) {
         int rc = encode_rows(a, 4 * C::kSub, umma::BM);
         if constexpr (std::is_same<BLoad, TmaConv>::value) {
             static_assert(C::kSub == 2, "im2col TMA: one 32-byte tap chunk per superstage");
-            if (rc == BNN_OK) rc = encode_conv(b, 4 * C::kSub, BN, b.npix / ((int64_t)b.oh * b.ow));
+            if (rc == BNN_OK) rc = encode_conv(b, 4 * C::kSub, C::kBRows, b.npix / ((int64_t)b.oh * b.ow));
         } else {
             if (rc == BNN_OK) rc = encode_rows(b, 4 * C::kSub, C::kTmaBoxB);
         }
@@ -1281,21 +1463,29 @@ static int launch_umma_cfg(const ALoad &a_in, const BLoad &b_in, const Store &st
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
         configured = true;
     }
-    const int64_t tiles_m = ceil_div(M, umma::BM), tiles_n = ceil_div(N, BN);
+    const int64_t tiles_m = ceil_div(M, C::kTmBM), tiles_n = ceil_div(N, BN);
     const int64_t ntiles = tiles_m * tiles_n;
     if (ntiles > (1ll << 30)) return set_error(BNN_EUNSUP, "too many tiles");
     umma::TileMap tmap{(int)tiles_m, (int)ntiles};
-    const int grid = (int)(ntiles < sm_count() ? ntiles : sm_count());
+    // one CTA (pair of CTAs) per SM (pair of SMs), persistent over the tiles
+    const int64_t units = kPair ? sm_count() / 2 : sm_count();
+    int grid = (int)((ntiles < units ? ntiles : units) * (kPair ? 2 : 1));
+    const bool force_cluster = !kPair && (umma_dbg() & 32768);  // debug: cluster launch of 1-CTA code
+    if (force_cluster) grid = (grid + 1) & ~1;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(C::kThreads);
     cfg.dynamicSmemBytes = C::kSmemBytes;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[0].val.programmaticStreamSerializationAllowed = (umma_dbg() & 65536) ? 0 : 1;  // debug: no PDL
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = (kPair || force_cluster) ? 2 : 1;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = (kPair || force_cluster) ? 2 : 1;
     cudaLaunchKernelEx(&cfg, kern, a, b, st, ep, kw32, tmap, g_trace_buf, umma_dbg());
     return check_launch("xnor_umma_kernel");
 }
@@ -1350,6 +1540,28 @@ static int choose_bn(int64_t M, int64_t N, bool fp4 = false, bool wide = false) 
     return best;
 }
 
+// 2-CTA pairs (256-row tiles): BN from {128, 160, 192, 224}, minimising waves x (BN + 32)
+// over the SM pairs
+template <class ALoad, class BLoad, class Store>
+static int launch_fp4_pair(const ALoad &a, const BLoad &b, const Store &st, const Epilogue &ep,
+                           int64_t M, int64_t N, int64_t kw32, cudaStream_t s) {
+    static const int cands[] = {224, 192, 160, 128};
+    const int64_t pairs = sm_count() / 2, tm = ceil_div(M, 2 * umma::BM);
+    int best = 224;
+    int64_t best_cost = -1;
+    for (int bn : cands) {
+        const int64_t cost = ceil_div(tm * ceil_div(N, bn), pairs) * (bn + 32);
+        if (best_cost < 0 || cost < best_cost) best = bn, best_cost = cost;
+    }
+    using S = Store;
+    switch (best) {
+        case 128: return launch_umma_cfg<128, false, 4, ALoad, BLoad, S, 1, true, 1, true>(a, b, st, ep, M, N, kw32, s);
+        case 160: return launch_umma_cfg<160, false, 4, ALoad, BLoad, S, 1, true, 1, true>(a, b, st, ep, M, N, kw32, s);
+        case 192: return launch_umma_cfg<192, false, 4, ALoad, BLoad, S, 1, true, 1, true>(a, b, st, ep, M, N, kw32, s);
+        default: return launch_umma_cfg<224, false, 4, ALoad, BLoad, S, 1, true, 1, true>(a, b, st, ep, M, N, kw32, s);
+    }
+}
+
 template <int kSets, class ALoad, class BLoad, class Store>
 static int launch_fp4(const ALoad &a, const BLoad &b, const Store &st, const Epilogue &ep, int64_t M,
                       int64_t N, int64_t kw32, cudaStream_t s) {
@@ -1380,7 +1592,15 @@ static int launch_umma(const ALoad &a, const BLoad &b, const Store &st, const Ep
         if (umma_variant() == 2) {
             // long K (>= 24 superstages per tile): two expander sets on alternate
             // superstages; short K: one set and 8 epilogue warps (tiles end often)
-            if (kw32 >= 24 * 8) return launch_fp4<2>(a, b, st, ep, M, N, kw32, s);
+            // long K and M >= 256: CTA pairs (cta_group::2); long K otherwise: two expander sets
+            static int64_t pair_kw32 = -1;
+            if (pair_kw32 < 0) {
+                const char *e = getenv("BNN_PAIR_KW32");  // tuning / debug override
+                pair_kw32 = e ? atoll(e) : BNN_FP4_PAIR_KW32;
+            }
+            if (kw32 >= pair_kw32 && M >= 2 * umma::BM && !(umma_dbg() & 8192))
+                return launch_fp4_pair(a, b, st, ep, M, N, kw32, s);
+            if (kw32 >= BNN_FP4_SETS_KW32) return launch_fp4<2>(a, b, st, ep, M, N, kw32, s);
             return launch_fp4<1>(a, b, st, ep, M, N, kw32, s);
         }
     }
@@ -1469,6 +1689,12 @@ int launch_bconv2d_umma(const uint64_t *x, int64_t B, int64_t C, int64_t H, int6
 }
 
 }  // namespace bnn
+
+// debug: arm the wait watchdog (buf = device u64[65]: count, then packed records), or null
+extern "C" int bnn_umma_watchdog(uint64_t *buf) {
+    cudaMemcpyToSymbol(bnn::umma::g_wait_log, &buf, sizeof(buf));
+    return bnn::check_launch("bnn_umma_watchdog");
+}
 
 extern "C" int bnn_umma_trace(uint64_t *buf) {
     // debug: buf = device array of (#SMs x 16) u64 timestamps, or null to disable

@@ -566,3 +566,24 @@ def test_randomized_shapes_umma_routes_equal_popc(bnn):
         A("umma2")
         assert np.array_equal(outs[1], outs[0]), ("conv", i)
         assert np.array_equal(outs[2], outs[0]), ("conv", i)
+
+
+def test_cta_pair_route_bit_exact(bnn, monkeypatch):
+    """The experimental 2-CTA (cta_group::2) kind::mxf4 route, forced on through a fresh
+    process (the threshold is read once per process): bit-exact against the POPC engine."""
+    import subprocess
+    import sys
+    code = (
+        "import sys, torch; sys.path.insert(0, '.');"
+        "import paper_1705_09864_b200 as bnn; bnn.load_library();"
+        "ok = True\n"
+        "for m, n, k in ((256, 128, 256), (512, 448, 4096), (1000, 1000, 8192), (300, 64, 2048)):\n"
+        "    W = (k + 63) // 64; g = torch.Generator(device='cuda').manual_seed(m + n + k)\n"
+        "    a = torch.randint(-2**63, 2**63 - 1, (m, W), device='cuda', generator=g).view(torch.uint64)\n"
+        "    b = torch.randint(-2**63, 2**63 - 1, (n, W), device='cuda', generator=g).view(torch.uint64)\n"
+        "    ok &= torch.equal(bnn.xnor_rows_gemm(a, b, k, algo='umma'), bnn.xnor_rows_gemm(a, b, k, algo='popc'))\n"
+        "print('PAIR_OK' if ok else 'PAIR_BAD')")
+    env = dict(os.environ, BNN_PAIR_KW32="1")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120,
+                       env=env, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert "PAIR_OK" in r.stdout, r.stdout + r.stderr
