@@ -163,12 +163,25 @@ int bnn_bitplane_gemm(const uint64_t *A, int64_t lda, int64_t a_plane_stride, in
  *        BatchNorm in the reference's op order, layers.py:598-602, each op
  *        rounded as NumPy float32 does -- bit-identical to an unfused BN)
  *   out = v + residual[same index as out]                          (shortcut)
+ *   sign-pack (tcgen05 engine only; the next layer's QActivation + pack,
+ *   layers.py:409-413 -> bitpack.py:30-42,78-87, fused):
+ *        bit m % 64 of pack_out[n * pack_ld + m / 64] = (out[m, n] >= 0)
+ *        (-0.0 -> 1 like binarize), bits m >= M are 0, words past ceil(M/64)
+ *        are not written; n is the output column:
+ *        the NHWC pixel b*oh*ow + y*ow + x of a conv (packed NHWC input of the
+ *        next bnn_bconv2d), the batch row of a GEMM (K-contiguous rows of the
+ *        next layer).  pack_flags[0] is set to 1 when an out value is NaN/Inf
+ *        (binarize's ValueError, bitpack.py:37-38).  The f32 output pointer may
+ *        be null when only the packed words are wanted.
  */
 typedef struct bnn_epilogue {
     int domain;
     const float *scale, *shift;
     const float *bn_mean, *bn_inv_std, *bn_gamma, *bn_beta;
     const float *residual;
+    uint64_t *pack_out;   /* optional sign-packed copy of out, [cols][pack_ld] u64 */
+    int64_t pack_ld;      /* >= ceil(M / 64) */
+    int32_t *pack_flags;  /* optional non-finite flag word */
 } bnn_epilogue;
 
 /* bnn_xnor_gemm / bnn_bconv2d with the full fused epilogue. */
@@ -183,6 +196,18 @@ int bnn_bn_relu_maxpool_f32(const float *x, int64_t B, int64_t C, int64_t H, int
                             const float *mean, const float *inv_std, const float *gamma,
                             const float *beta, int relu, int k, int stride, int pad, float *y,
                             bnn_stream_t stream);
+
+/* Full-precision convolution of a network's float stem layer (reference
+ * Conv2d, layers.py:81-141; ResNet-18 conv7x7/2 3->64, LeNet conv5x5 1->64):
+ * y[B, F, oh, ow] = conv(x[B, C, H, W], w[F, C, kh, kw]) (+ bias[F]), zero
+ * padding, NCHW f32.  tcgen05 kind::tf32 with a three-term hi/lo split
+ * (x_hi w_hi + x_hi w_lo + x_lo w_hi, f32 accumulate): f32 accuracy, rounding
+ * differs from a CUDA-core f32 conv only in summation order.  F == 64 and
+ * C*kh*kw <= 320 (BNN_EUNSUP otherwise). */
+int bnn_conv2d_f32_tc(const float *x, int64_t B, int64_t C, int64_t H, int64_t W,
+                      const float *w, const float *bias, int64_t F, int64_t kh, int64_t kw,
+                      int64_t sh, int64_t sw, int64_t ph, int64_t pw, float *y,
+                      bnn_stream_t stream);
 
 /* Words per pixel of the packed NHWC activation layout: ceil(C / 64). */
 int64_t bnn_conv_channel_words(int64_t C);

@@ -49,6 +49,8 @@ SIGNATURES = {
     "bnn_set_umma_variant": (_i32, [_i32]),
     "bnn_bn_relu_maxpool_f32": (_i32, [_vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _i32, _i32,
                                        _i32, _i32, _vp, _vp]),
+    "bnn_conv2d_f32_tc": (_i32, [_vp, _i64, _i64, _i64, _i64, _vp, _vp, _i64, _i64, _i64, _i64,
+                                 _i64, _i64, _i64, _vp, _vp]),
     "bnn_xnor_gemm_ex": (_i32, [_vp, _i64, _vp, _i64, _i64, _i64, _i64, _i32, _i32, _vp, _i64,
                                 _i64, _vp, _i32, _vp]),
     "bnn_bconv2d_ex": (_i32, [_vp, _i64, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i64,
@@ -64,7 +66,8 @@ class Epilogue(ctypes.Structure):
     _fields_ = [("domain", ctypes.c_int), ("scale", ctypes.c_void_p), ("shift", ctypes.c_void_p),
                 ("bn_mean", ctypes.c_void_p), ("bn_inv_std", ctypes.c_void_p),
                 ("bn_gamma", ctypes.c_void_p), ("bn_beta", ctypes.c_void_p),
-                ("residual", ctypes.c_void_p)]
+                ("residual", ctypes.c_void_p), ("pack_out", ctypes.c_void_p),
+                ("pack_ld", ctypes.c_int64), ("pack_flags", ctypes.c_void_p)]
 
 
 class BnnError(RuntimeError):

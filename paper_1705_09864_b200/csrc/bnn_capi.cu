@@ -62,6 +62,9 @@ int launch_bitplane_gemm_umma(const uint64_t *, int64_t, int64_t, const uint64_t
 int launch_bn_relu_maxpool(const float *, int64_t, int64_t, int64_t, int64_t, const float *,
                            const float *, const float *, const float *, int, int, int, int,
                            float *, cudaStream_t);
+int launch_conv2d_f32_tc(const float *, int64_t, int64_t, int64_t, int64_t, const float *,
+                         const float *, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,
+                         int64_t, int64_t, int64_t, float *, cudaStream_t);
 int launch_bconv2d_popc(const uint64_t *, int64_t, int64_t, int64_t, int64_t, const uint64_t *,
                         int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,
                         int64_t, float *, const Epilogue &, cudaStream_t, const float *);
@@ -177,6 +180,22 @@ static void fill_epilogue(Epilogue &ep, const bnn_epilogue *e) {
     ep.bn_inv = e->bn_inv_std;
     ep.bn_gamma = e->bn_gamma;
     ep.bn_beta = e->bn_beta;
+    ep.pack_out = reinterpret_cast<uint32_t *>(e->pack_out);
+    ep.pack_ld32 = 2 * e->pack_ld;
+    ep.pack_flags = e->pack_flags;
+}
+
+// the fused sign-pack output (tcgen05 engine only) and the optional f32 output
+static int check_pack_out(const bnn_epilogue *e, int64_t M, int algo, const float *out) {
+    if (!e->pack_out) {
+        BNN_REQUIRE(out, BNN_EINVAL, "null pointer");
+        return BNN_OK;
+    }
+    BNN_REQUIRE(algo == BNN_ALGO_AUTO || algo == BNN_ALGO_UMMA, BNN_EUNSUP,
+                "the fused sign-pack epilogue runs on the tcgen05 engine only");
+    BNN_REQUIRE(e->pack_ld >= ceil_div(M, 64), BNN_EALIGN, "pack_ld=%lld smaller than ceil(M/64)=%lld",
+                (long long)e->pack_ld, (long long)ceil_div(M, 64));
+    return BNN_OK;
 }
 
 int bnn_xnor_gemm_ex(const uint64_t *A, int64_t lda, const uint64_t *B, int64_t ldb, int64_t M,
@@ -190,7 +209,9 @@ int bnn_xnor_gemm_ex(const uint64_t *A, int64_t lda, const uint64_t *B, int64_t 
     const int64_t W = ceil_div(K, 64);
     BNN_REQUIRE(lda >= W && ldb >= W, BNN_EALIGN, "lda/ldb smaller than ceil(K/64)=%lld",
                 (long long)W);
-    BNN_REQUIRE(A && B && C, BNN_EINVAL, "null pointer");
+    BNN_REQUIRE(A && B, BNN_EINVAL, "null pointer");
+    rc = check_pack_out(e, M, algo, C);
+    if (rc) return rc;
     const int domain = e->domain;
     BNN_REQUIRE(domain == BNN_POPCOUNT || domain == BNN_DOT, BNN_EINVAL, "bad domain %d", domain);
     BNN_REQUIRE(!e->bn_mean || (e->bn_inv_std && e->bn_gamma && e->bn_beta), BNN_EINVAL,
@@ -275,6 +296,20 @@ int bnn_bn_relu_maxpool_f32(const float *x, int64_t B, int64_t C, int64_t H, int
                                   y, as_stream(stream));
 }
 
+int bnn_conv2d_f32_tc(const float *x, int64_t B, int64_t C, int64_t H, int64_t W,
+                      const float *w, const float *bias, int64_t F, int64_t kh, int64_t kw,
+                      int64_t sh, int64_t sw, int64_t ph, int64_t pw, float *y,
+                      bnn_stream_t stream) {
+    BNN_REQUIRE(B >= 0 && C >= 1 && H >= 1 && W >= 1 && F >= 1 && kh >= 1 && kw >= 1 &&
+                    sh >= 1 && sw >= 1 && ph >= 0 && pw >= 0 && H + 2 * ph >= kh &&
+                    W + 2 * pw >= kw,
+                BNN_EGEOM, "invalid convolution geometry");
+    BNN_REQUIRE(x && w && y, BNN_EINVAL, "null pointer");
+    const int64_t oh = (H + 2 * ph - kh) / sh + 1, ow = (W + 2 * pw - kw) / sw + 1;
+    return launch_conv2d_f32_tc(x, B, C, H, W, w, bias, F, kh, kw, sh, sw, ph, pw, oh, ow, y,
+                                as_stream(stream));
+}
+
 int64_t bnn_conv_channel_words(int64_t C) { return C > 0 ? ceil_div(C, 64) : 0; }
 
 int bnn_conv_weights_reorder(const uint64_t *w_ref, int64_t F, int64_t C, int64_t kh,
@@ -301,7 +336,9 @@ int bnn_bconv2d_ex(const uint64_t *x_words, int64_t B, int64_t C, int64_t H, int
     int rc = check_gemm_dims(F, B * oh * ow, K);
     if (rc) return rc;
     BNN_REQUIRE(e != nullptr, BNN_EINVAL, "null epilogue");
-    BNN_REQUIRE(x_words && w_dev && y, BNN_EINVAL, "null pointer");
+    BNN_REQUIRE(x_words && w_dev, BNN_EINVAL, "null pointer");
+    rc = check_pack_out(e, F, algo, y);
+    if (rc) return rc;
     const int domain = e->domain;
     BNN_REQUIRE(domain == BNN_POPCOUNT || domain == BNN_DOT, BNN_EINVAL, "bad domain %d", domain);
     BNN_REQUIRE(!e->bn_mean || (e->bn_inv_std && e->bn_gamma && e->bn_beta), BNN_EINVAL,

@@ -33,6 +33,11 @@ struct Epilogue {
     // optional fused inference BatchNorm in the reference's op order
     // (layers.py:598-602): gamma * ((x - mean) * inv_std) + beta, each op rounded
     const float *bn_mean = nullptr, *bn_inv = nullptr, *bn_gamma = nullptr, *bn_beta = nullptr;
+    // optional sign-pack of the final value (next layer's QActivation + pack):
+    // u32 word (n * pack_ld32 + m / 32), bit m % 32 = out[m, n] >= 0
+    uint32_t *pack_out = nullptr;
+    int64_t pack_ld32 = 0;
+    int32_t *pack_flags = nullptr;
     __device__ __forceinline__ float bn(float f, int m) const {
         if (!bn_mean) return f;
         const float xh = __fmul_rn(__fsub_rn(f, __ldg(bn_mean + m)), __ldg(bn_inv + m));

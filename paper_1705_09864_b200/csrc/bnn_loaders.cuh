@@ -122,6 +122,8 @@ struct ConvRows {
 // Stores optionally add a residual tensor of the output's own layout (fused
 // "+ shortcut" of a residual block; f32 add, the same rounding as x + r).
 struct GemmStore {
+    static constexpr bool kConv = false;
+    static constexpr bool kPack = false;  // fused sign-pack epilogue instantiations
     float *C;
     int64_t ldc_m, ldc_n, M, N;
     const float *res = nullptr;
@@ -134,7 +136,16 @@ struct GemmStore {
         const int64_t i = m * ldc_m + n * ldc_n;
         C[i] = res ? __fadd_rn(v, __ldg(res + i)) : v;
     }
+    __device__ void put_raw(int64_t m, int64_t n, float v) const { C[m * ldc_m + n * ldc_n] = v; }
     __device__ const float *res_of(const float *p) const { return res + (p - C); }
+    __device__ bool has_out() const { return C != nullptr; }
+    // g[j] += res[m, n + j] for the first w columns (j < w, n + j < N)
+    __device__ void add_res_row(int64_t m, int64_t n, int w, float *g) const {
+        const float *r = res + m * ldc_m + n * ldc_n;
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            if (j < w && n + j < N) g[j] = __fadd_rn(g[j], __ldg(r + j * ldc_n));
+    }
     // column view for the staged epilogue: &C[m, n] = col_base(n) + m * m_stride()
     __device__ bool n_contiguous() const { return ldc_n == 1; }
     __device__ float *col_base(int64_t n) const { return C + n * ldc_n; }
@@ -166,6 +177,8 @@ struct GemmStore {
 };
 
 struct ConvStore {  // y NCHW [B, F, oh*ow]; m = filter, n = b*ohw + pixel
+    static constexpr bool kConv = true;
+    static constexpr bool kPack = false;
     float *y;
     int64_t F, ohw, npix;
     const float *res = nullptr;
@@ -178,7 +191,38 @@ struct ConvStore {  // y NCHW [B, F, oh*ow]; m = filter, n = b*ohw + pixel
         const int64_t i = (b * F + m) * ohw + p;
         y[i] = res ? __fadd_rn(v, __ldg(res + i)) : v;
     }
+    __device__ void put_raw(int64_t m, int64_t n, float v) const {
+        int64_t b = n / ohw, p = n - b * ohw;
+        y[(b * F + m) * ohw + p] = v;
+    }
     __device__ const float *res_of(const float *p) const { return res + (p - y); }
+    __device__ bool has_out() const { return y != nullptr; }
+    // g[j] += res[m, n + j] for the first w columns (j < w, n + j < npix); the
+    // run of 32 pixels may straddle images
+    __device__ void add_res_row(int64_t m, int64_t n, int w, float *g) const {
+        int64_t b = n / ohw, p = n - b * ohw;
+        const float *r = res + (b * F + m) * ohw + p;
+        if (w == 32 && p + 32 <= ohw && n + 32 <= npix && (reinterpret_cast<uintptr_t>(r) & 15) == 0) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const float4 t = __ldg(reinterpret_cast<const float4 *>(r) + j);
+                g[4 * j] = __fadd_rn(g[4 * j], t.x);
+                g[4 * j + 1] = __fadd_rn(g[4 * j + 1], t.y);
+                g[4 * j + 2] = __fadd_rn(g[4 * j + 2], t.z);
+                g[4 * j + 3] = __fadd_rn(g[4 * j + 3], t.w);
+            }
+            return;
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            if (j < w && n + j < npix) g[j] = __fadd_rn(g[j], __ldg(r));
+            ++r;
+            if (++p == ohw) {  // next image: same channel m
+                p = 0;
+                r += (F - 1) * ohw;
+            }
+        }
+    }
     __device__ bool n_contiguous() const { return true; }  // within an image
     __device__ float *col_base(int64_t n) const {
         int64_t b = n / ohw, p = n - b * ohw;
@@ -211,6 +255,14 @@ struct ConvStore {  // y NCHW [B, F, oh*ow]; m = filter, n = b*ohw + pixel
                 if (n + i < npix) put(m, n + i, v[i]);
         }
     }
+};
+
+// the same stores, instantiating the tcgen05 epilogue's sign-pack output
+struct GemmStorePk : GemmStore {
+    static constexpr bool kPack = true;
+};
+struct ConvStorePk : ConvStore {
+    static constexpr bool kPack = true;
 };
 
 }  // namespace bnn

@@ -525,6 +525,71 @@ __global__ void bn_relu_maxpool_kernel(const float *__restrict__ x, int64_t B, i
     y[plane * OH * OW + p] = best;
 }
 
+// Banded variant of the same post-op (the product path for the ResNet stem):
+// one CTA per (plane, band of R output rows) stages the band's input rows in
+// SMEM with coalesced loads, pools first and applies BatchNorm + ReLU once per
+// output.  Exact: f(v) = relu?(bt + g * ((v - m) * iv)) with every op rounded is
+// monotone non-decreasing in v for g >= 0 and non-increasing for g < 0 (iv > 0),
+// so max over the window of f(v) = f(max v) (g >= 0) or f(min v) (g < 0) --
+// bit-identical to applying f to every element first.  Out-of-image window
+// positions are skipped (-inf padding of maxpool).
+__global__ void bn_relu_maxpool_band_kernel(const float *__restrict__ x, int C, int H, int W,
+                                            const float *__restrict__ mean,
+                                            const float *__restrict__ inv,
+                                            const float *__restrict__ gamma,
+                                            const float *__restrict__ beta, int relu, int k,
+                                            int st, int pd, int OH, int OW, int R, int nbands,
+                                            float *__restrict__ y) {
+    extern __shared__ float band[];
+    const int64_t plane = blockIdx.x / nbands;
+    const int c = (int)(plane % C);
+    const int r0 = (int)(blockIdx.x - plane * nbands) * R;
+    const int rows = min(R, OH - r0);
+    const int iy0 = r0 * st - pd;
+    const int nrows = (rows - 1) * st + k;
+    const float *src = x + plane * H * W;
+    // stage input rows iy0 .. iy0 + nrows - 1 (rows outside the image are skipped later)
+    const bool vec = (W % 4 == 0) && ((reinterpret_cast<uintptr_t>(src) & 15) == 0);
+    if (vec) {
+        const int w4 = W / 4;
+        for (int i = threadIdx.x; i < nrows * w4; i += blockDim.x) {
+            const int r = i / w4, j = i - r * w4, iy = iy0 + r;
+            if (iy >= 0 && iy < H)
+                reinterpret_cast<float4 *>(band)[i] =
+                    __ldcs(reinterpret_cast<const float4 *>(src + (int64_t)iy * W) + j);
+        }
+    } else {
+        for (int i = threadIdx.x; i < nrows * W; i += blockDim.x) {
+            const int r = i / W, j = i - r * W, iy = iy0 + r;
+            if (iy >= 0 && iy < H) band[i] = __ldcs(src + (int64_t)iy * W + j);
+        }
+    }
+    __syncthreads();
+    const float m = __ldg(mean + c), iv = __ldg(inv + c), g = __ldg(gamma + c), bt = __ldg(beta + c);
+    const bool up = !(g < 0.0f);
+    float *dst = y + plane * OH * OW + (int64_t)r0 * OW;
+    for (int o = threadIdx.x; o < rows * OW; o += blockDim.x) {
+        const int oy = o / OW, ox = o - oy * OW;
+        float hi = -INFINITY, lo = INFINITY;
+        for (int i = 0; i < k; ++i) {
+            const int iy = (r0 + oy) * st - pd + i;
+            if (iy < 0 || iy >= H) continue;
+            const float *row = band + (oy * st + i) * W;
+            for (int j = 0; j < k; ++j) {
+                const int ix = ox * st - pd + j;
+                if (ix < 0 || ix >= W) continue;
+                const float v = row[ix];
+                hi = fmaxf(hi, v);
+                lo = fminf(lo, v);
+            }
+        }
+        float v = up ? hi : lo;
+        v = __fadd_rn(__fmul_rn(g, __fmul_rn(__fsub_rn(v, m), iv)), bt);
+        if (relu) v = fmaxf(v, 0.0f);
+        dst[o] = v;
+    }
+}
+
 // ================================================================ launchers
 int launch_binarize(const float *x, int64_t n, float *out, int32_t *flags, cudaStream_t s) {
     if (n == 0) return BNN_OK;
@@ -644,6 +709,18 @@ int launch_bn_relu_maxpool(const float *x, int64_t B, int64_t C, int64_t H, int6
     const int64_t OH = (H + 2 * pd - k) / st + 1, OW = (W + 2 * pd - k) / st + 1;
     const int64_t total = B * C * OH * OW;
     if (total == 0) return BNN_OK;
+    // banded SMEM kernel: R output rows per CTA (~8 KB+ of input rows per band)
+    int64_t R = (8192 / 4) / (W * st > 0 ? W * st : 1);
+    R = R < 1 ? 1 : (R > OH ? OH : R);
+    const int64_t band_bytes = (((R - 1) * st + k) * W) * 4;
+    const int64_t nbands = ceil_div(OH, R);
+    if (band_bytes <= 48 * 1024 && OH * OW < (1ll << 31) && H * W < (1ll << 31) &&
+        B * C * nbands <= 0x7fffffffll && !getenv("BNN_STEMPOST_SIMPLE")) {
+        bn_relu_maxpool_band_kernel<<<(unsigned)(B * C * nbands), 256, (size_t)band_bytes, s>>>(
+            x, (int)C, (int)H, (int)W, mean, inv, gamma, beta, relu, k, st, pd, (int)OH, (int)OW,
+            (int)R, (int)nbands, y);
+        return check_launch("bn_relu_maxpool_band_kernel");
+    }
     const int64_t bpp = ceil_div(OH * OW, 256);
     if (OH * OW > (1ll << 30) || H * W > (1ll << 30) || B * C * bpp > 0x7fffffffll)
         return set_error(BNN_EUNSUP, "bn_relu_maxpool: tensor too large");

@@ -158,8 +158,36 @@ class _QLayer:
             raise ModeError("layer has no packed weights; pack() or load a converted model")
 
 
+class PackedNHWC:
+    """A sign-binarised activation kept packed between binary layers.
+
+    ``words``: u64 [B, H, W, ceil(C/64)] -- channel c at bit c % 64 of word
+    c // 64, bit 1 = (x >= 0) (binarize, bitpack.py:30-42), channel tail 0: the
+    layout ``pack_nchw`` writes and ``bnn_bconv2d`` reads.  ``f32`` is the same
+    activation before the sign in NCHW f32 when a consumer needs it (a residual
+    shortcut, a float layer), else None.  The packed words are written by the
+    producing conv's epilogue, so no standalone pack pass runs.
+    """
+
+    __slots__ = ("words", "shape", "f32")
+
+    def __init__(self, words: torch.Tensor, shape, f32: torch.Tensor | None = None):
+        self.words, self.shape, self.f32 = words, tuple(int(v) for v in shape), f32
+
+    @classmethod
+    def from_f32(cls, x: torch.Tensor, flags: torch.Tensor | None = None) -> "PackedNHWC":
+        x = x.contiguous()
+        return cls(pack_nchw(x, strict=False, flags=flags), x.shape, x)
+
+    def float(self) -> torch.Tensor:
+        if self.f32 is None:
+            raise ValueError("this packed activation kept no f32 copy")
+        return self.f32
+
+
 def make_epilogue(domain: int, bn=None, residual: torch.Tensor | None = None,
-                  scale: torch.Tensor | None = None, shift: torch.Tensor | None = None):
+                  scale: torch.Tensor | None = None, shift: torch.Tensor | None = None,
+                  pack_out: torch.Tensor | None = None, pack_flags: torch.Tensor | None = None):
     """ctypes ``bnn_epilogue`` for the fused GEMM / conv epilogue.
 
     ``bn`` is any object with ``device_params() -> (mean, inv_std, gamma, beta)``
@@ -176,6 +204,10 @@ def make_epilogue(domain: int, bn=None, residual: torch.Tensor | None = None,
         keep += [mean, inv, gamma, beta]
     if residual is not None:
         e.residual = _lib.ptr(residual)
+    if pack_out is not None:  # sign-pack of the final value, [cols, pack_ld] u64
+        e.pack_out, e.pack_ld = _lib.ptr(pack_out), pack_out.shape[-1]
+        e.pack_flags = _lib.ptr(pack_flags)
+        keep += [pack_out, pack_flags]
     e._keep = keep  # keep tensors alive with the struct
     return e
 
@@ -262,31 +294,54 @@ class QConv2d(_QLayer):
     def _strict_input(self) -> bool:
         return True
 
-    def forward_fused(self, x: torch.Tensor, bn=None, residual: torch.Tensor | None = None,
-                      out: torch.Tensor | None = None) -> torch.Tensor:
-        """``infer_packed`` conv with BatchNorm (+ residual add) fused into the epilogue."""
+    def forward_fused(self, x, bn=None, residual: torch.Tensor | None = None,
+                      out: torch.Tensor | None = None, pack_out: bool = False,
+                      f32_out: bool = True):
+        """``infer_packed`` conv with BatchNorm (+ residual add) fused into the epilogue.
+
+        ``x``: f32 NCHW (packed here, sign fused) or a ``PackedNHWC`` from a
+        previous layer's epilogue (no pack pass).  ``pack_out``: also emit the
+        sign-packed output for the next binary layer (the next QActivation and
+        pack fused into this epilogue) and return a ``PackedNHWC`` whose ``f32``
+        is the f32 output (None when ``f32_out`` is False).
+        """
         import ctypes
         self._require_packed()
-        t = x.contiguous()
-        b, c, h, w = t.shape
-        kh, kw = self.kernel
-        oh, ow = self.output_hw(h, w)
         flags = torch.zeros(1, dtype=torch.int32, device="cuda") if self.sync_checks \
             else self._flags()
-        xw = pack_nchw(t, strict=self._strict_input(), flags=flags)
-        if out is None:
+        if isinstance(x, PackedNHWC):
+            b, c, h, w = x.shape
+            if c != self.in_channels:
+                raise ValueError(f"expected {self.in_channels} channels, got {c}")
+            xw = x.words
+        else:
+            t = x.contiguous()
+            b, c, h, w = t.shape
+            xw = pack_nchw(t, strict=self._strict_input(), flags=flags)
+        kh, kw = self.kernel
+        oh, ow = self.output_hw(h, w)
+        if not (f32_out or pack_out):
+            raise ValueError("nothing to compute: f32_out and pack_out are both False")
+        if out is None and f32_out:
             out = torch.empty((b, self.filters, oh, ow), dtype=torch.float32, device="cuda")
+        if not f32_out:
+            out = None
+        pw_out = torch.empty((b, oh, ow, words_per_bits(self.filters)), dtype=torch.uint64,
+                             device="cuda") if pack_out else None
         if residual is not None:
             residual = residual.contiguous()
-            if tuple(residual.shape) != tuple(out.shape):
+            if tuple(residual.shape) != (b, self.filters, oh, ow):
                 raise ValueError("residual must match the conv output shape")
-        e = make_epilogue(self.domain, bn, residual)
+        e = make_epilogue(self.domain, bn, residual, pack_out=pw_out,
+                          pack_flags=flags if pack_out else None)
         wd = self.device_weights()
         algo = _lib.ALGOS[self.algo] if isinstance(self.algo, str) else self.algo
         _lib.call("bnn_bconv2d_ex", _lib.ptr(xw), b, self.in_channels, h, w, _lib.ptr(wd),
                   self.filters, kh, kw, self.stride[0], self.stride[1], self.pad[0], self.pad[1],
                   _lib.ptr(out), ctypes.byref(e), algo, _lib.stream_ptr())
         self._finish(flags)
+        if pack_out:
+            return PackedNHWC(pw_out, (b, self.filters, oh, ow), out)
         return out
 
     def forward(self, x, mode=INFER_FLOAT):

@@ -26,8 +26,8 @@ import torch
 import torch.nn.functional as F
 
 from . import _lib
-from .layers import (INFER_FLOAT, INFER_PACKED, QConvolution, QFullyConnected, _check_mode,
-                     _float_matmul, _uniform_init)
+from .layers import (INFER_FLOAT, INFER_PACKED, PackedNHWC, QConvolution, QFullyConnected,
+                     _check_mode, _float_matmul, _uniform_init)
 
 BN_EPS = 1e-5  # layers.py:36
 
@@ -49,16 +49,38 @@ class _Lazy:
 
 
 class Conv2d(_Lazy):
-    """Full-precision convolution (layers.py:81-141), NCHW f32, TF32 off."""
+    """Full-precision convolution (layers.py:81-141), NCHW f32.
+
+    ``engine="tc"`` (default where supported: 64 filters, C*k*k <= 320 -- the
+    ResNet-18 and LeNet stems): ``bnn_conv2d_f32_tc``, tcgen05 kind::tf32 with a
+    three-term hi/lo split (f32 accuracy).  ``engine="cudnn"``: cuDNN f32 with
+    TF32 off.  Both modes of a network use the same engine, so the cross-mode
+    exactness of the binary layers is unaffected.
+    """
+
+    engine = "tc"
 
     def __init__(self, cin, cout, k, stride=1, pad=0, bias=True, rng=None):
-        self.k, self.cout, self.stride, self.pad = k, cout, stride, pad
+        self.cin, self.k, self.cout, self.stride, self.pad = cin, k, cout, stride, pad
         fan_in, fan_out = cin * k * k, cout * k * k
         self.weight = _uniform_init(rng, (cout, cin, k, k), fan_in, fan_out) if rng is not None \
             else np.zeros((cout, cin, k, k), np.float32)
         self.bias = np.zeros(cout, np.float32) if bias else None
 
+    def tc_supported(self) -> bool:
+        return self.cout == 64 and self.cin * self.k * self.k <= 320
+
     def forward(self, x, mode=INFER_FLOAT):
+        if self.engine == "tc" and self.tc_supported():
+            x = x.contiguous()
+            b, c, h, w = x.shape
+            oh = (h + 2 * self.pad - self.k) // self.stride + 1
+            ow = (w + 2 * self.pad - self.k) // self.stride + 1
+            y = torch.empty((b, self.cout, oh, ow), dtype=torch.float32, device=x.device)
+            _lib.call("bnn_conv2d_f32_tc", _lib.ptr(x), b, c, h, w, _lib.ptr(self._dev("weight")),
+                      _lib.ptr(self._dev("bias")), self.cout, self.k, self.k, self.stride,
+                      self.stride, self.pad, self.pad, _lib.ptr(y), _lib.stream_ptr())
+            return y
         prev = torch.backends.cudnn.allow_tf32
         torch.backends.cudnn.allow_tf32 = False
         torch.backends.cudnn.benchmark = True  # fastest exact-fp32 algorithm for the shape
@@ -171,6 +193,8 @@ class Sequential:
         while i < n:
             layer = self.layers[i]
             nxt = self.layers[i + 1] if i + 1 < n else None
+            if isinstance(x, PackedNHWC) and not isinstance(layer, BinaryBasicBlock):
+                x = x.float()  # a float consumer of a packed activation
             if (mode == INFER_PACKED and self.fuse_bn and isinstance(nxt, BatchNorm)
                     and isinstance(layer, (QConvolution, QFullyConnected)) and layer.bits == 1):
                 x = layer.forward_fused(x, nxt)
@@ -181,9 +205,9 @@ class Sequential:
                 continue
             x = layer.forward(x, mode)
             if capture is not None:
-                capture.append(x)
+                capture.append(x.float() if isinstance(x, PackedNHWC) else x)
             i += 1
-        return x
+        return x.float() if isinstance(x, PackedNHWC) else x
 
     def binary_layers(self):
         out = []
@@ -217,8 +241,22 @@ class BinaryBasicBlock:
         return [self.conv1, self.conv2] + ([self.down] if self.down else [])
 
     fused = True  # infer_packed: BN and the shortcut add run in the conv epilogues
+    # infer_packed: activations stay sign-packed between the binary convs -- conv1
+    # writes only the packed sign of BN1's output (its f32 has no other consumer),
+    # conv2 writes the f32 block output (next shortcut) and its packed sign (next
+    # block's convs), so no standalone pack pass runs inside the network
+    packed_io = True
+    emit_packed = True  # False for the last block (a float layer consumes it)
 
     def forward(self, x, mode=INFER_FLOAT):
+        if mode == INFER_PACKED and self.fused and self.packed_io:
+            if not isinstance(x, PackedNHWC):
+                x = PackedNHWC.from_f32(x, self.conv1._flags())
+            h = self.conv1.forward_fused(x, self.bn1, pack_out=True, f32_out=False)
+            sc = x.float() if self.down is None else self.down.forward_fused(x, self.bnd)
+            return self.conv2.forward_fused(h, self.bn2, residual=sc, pack_out=self.emit_packed)
+        if isinstance(x, PackedNHWC):
+            x = x.float()
         if mode == INFER_PACKED and self.fused:
             h = self.conv1.forward_fused(x, self.bn1)
             sc = x if self.down is None else self.down.forward_fused(x, self.bnd)
@@ -250,6 +288,7 @@ def resnet18_c4(seed: int = 0, num_classes: int = 1000) -> Sequential:
         layers.append(BinaryBasicBlock(cin, cout, stride, rng))
         layers.append(BinaryBasicBlock(cout, cout, 1, rng))
         cin = cout
+    layers[-1].emit_packed = False  # the average pool reads the f32 output
     layers += [GlobalAvgPool(), Dense(512, num_classes, rng=rng)]
     return Sequential(layers)
 

@@ -75,6 +75,12 @@ def test_resnet18_c4_cross_mode(nets):
         if isinstance(layer, nets.BinaryBasicBlock):
             assert torch.equal(cap_f[i], cap_p[i]), f"block {i}"
     assert torch.equal(yf, yp)
+    # activations kept sign-packed between the binary convs (conv epilogues emit the
+    # packed words) == a pack pass over every f32 block output
+    for layer in net.layers:
+        if isinstance(layer, nets.BinaryBasicBlock):
+            layer.packed_io = False
+    assert torch.equal(net.forward(x, bnn.INFER_PACKED), yf)
     for layer in net.layers:  # unfused epilogues agree as well
         if isinstance(layer, nets.BinaryBasicBlock):
             layer.fused = False
@@ -119,11 +125,50 @@ def test_lenet_end_to_end_vs_cpu_reference(nets):
 
 
 @pytest.mark.parametrize("shape,k,st,pd", [((2, 5, 17, 13), 3, 2, 1), ((1, 3, 8, 8), 2, 2, 0),
-                                           ((3, 4, 9, 11), 3, 1, 1)])
+                                           ((3, 4, 9, 11), 3, 1, 1), ((2, 6, 40, 36), 3, 2, 1),
+                                           ((1, 4, 112, 112), 3, 2, 1), ((1, 2, 7, 2000), 3, 2, 1)])
 def test_stem_post_kernel_equals_torch_ops(nets, shape, k, st, pd):
-    """bnn_bn_relu_maxpool_f32 is bit-identical to BatchNorm -> ReLU -> MaxPool."""
+    """bnn_bn_relu_maxpool_f32 is bit-identical to BatchNorm -> ReLU -> MaxPool (the
+    banded kernel pools first and applies BN once: exact by monotonicity, also for
+    negative and zero gammas)."""
     import paper_1705_09864_b200 as bnn
     rng = np.random.default_rng(4)
     post = nets.StemPost(shape[1], rng, k, st, pd)
+    post.bn.gamma[::2] *= -1.0
+    post.bn.gamma[1] = 0.0
+    if shape[1] > 3:
+        post.bn.gamma[3] = -0.0
     x = torch.randn(shape, generator=torch.Generator().manual_seed(3)).cuda()
     assert torch.equal(post.forward(x, bnn.INFER_PACKED), post.forward(x, bnn.INFER_FLOAT))
+
+
+@pytest.mark.parametrize("case", [
+    # (B, C, H, W, F, k, stride, pad, bias): ResNet-18 stem, LeNet conv1, ragged shapes
+    (2, 3, 224, 224, 64, 7, 2, 3, False),
+    (3, 1, 28, 28, 64, 5, 1, 2, True),
+    (1, 3, 37, 29, 64, 7, 2, 3, True),
+    (2, 5, 9, 13, 64, 3, 1, 1, True),
+    (1, 6, 20, 20, 64, 7, 3, 0, False),
+])
+def test_conv2d_f32_tensor_core_accuracy(nets, case):
+    """bnn_conv2d_f32_tc (3xTF32 on tcgen05) against a float64 convolution: f32-level
+    error (|d| <= 1e-5 * max(1, |ref|), the tolerance of test_layers.py:68), no worse
+    than cuDNN's f32 conv by more than a small factor."""
+    import torch.nn.functional as F
+    b, c, h, w, f, k, st, pd, bias = case
+    rng = np.random.default_rng(sum(case[:8]))
+    x = rng.standard_normal((b, c, h, w)).astype(np.float32)
+    conv = nets.Conv2d(c, f, k, stride=st, pad=pd, bias=bias, rng=rng)
+    if bias:
+        conv.bias = rng.standard_normal(f).astype(np.float32)
+    assert conv.tc_supported()
+    xd = torch.from_numpy(x).cuda()
+    y = conv.forward(xd).cpu().double()
+    ref = F.conv2d(torch.from_numpy(x).double(), torch.from_numpy(conv.weight).double(),
+                   torch.from_numpy(conv.bias).double() if bias else None, stride=st, padding=pd)
+    err = (y - ref).abs()
+    assert y.shape == ref.shape
+    assert bool((err <= 1e-5 * ref.abs().clamp(min=1.0)).all()), float(err.max())
+    conv.engine = "cudnn"
+    y_cudnn = conv.forward(xd).cpu().double()
+    assert float(err.max()) <= 4 * float((y_cudnn - ref).abs().max()) + 1e-6

@@ -1,0 +1,183 @@
+"""Fused sign-pack epilogue: the next layer's QActivation + pack
+(layers.py:409-413 -> bitpack.binarize :30-42 -> _pack_last_axis :78-87) run in
+the GEMM / conv epilogue, so activations stay 1 bit per element between binary
+layers.
+
+The packed words must equal the oracle's pack of sign(f32 output) bit for bit
+(channel tail 0, sign(-0) = +1), and the f32 output must be unchanged by the
+extra output.
+"""
+
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+import workloads as wl
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def bnn():
+    import paper_1705_09864_b200 as p
+    p.load_library()
+    return p
+
+
+class _BN:
+    """BatchNorm parameters whose mean hits exact dot-domain integers, so some
+    outputs are exactly +0 / -0 (negative gammas give -0 products)."""
+
+    def __init__(self, f, k, seed):
+        rng = np.random.default_rng(seed)
+        self.mean = (2 * rng.integers(-4, 5, f) + (k % 2)).astype(np.float32)
+        self.inv = (0.5 + rng.random(f)).astype(np.float32)
+        self.gamma = (rng.standard_normal(f)).astype(np.float32)
+        self.beta = np.where(rng.random(f) < 0.5, 0.0, -0.0).astype(np.float32)
+        self.beta[::5] = rng.standard_normal(len(self.beta[::5])).astype(np.float32) * 3
+
+    def device_params(self):
+        return tuple(torch.from_numpy(a).cuda() for a in (self.mean, self.inv, self.gamma, self.beta))
+
+
+def _oracle_pack_nhwc(y_nchw: np.ndarray) -> np.ndarray:
+    b, f, h, w = y_nchw.shape
+    rows = np.ascontiguousarray(y_nchw.transpose(0, 2, 3, 1).reshape(-1, f))
+    return orc.binarize_pack_rows(rows, pad_fill=0).reshape(b, h, w, -1)
+
+
+# (B, C, H, W, F, kh, kw, stride, pad, seed): cp.async route (C % 256 != 0) and the
+# im2col-TMA route (C % 256 == 0); F not a multiple of 64 / 32; images of fewer
+# than 32 pixels (32-column blocks straddle images)
+CASES = [
+    (2, 64, 9, 9, 64, 3, 3, (1, 1), (1, 1), 1),
+    (3, 64, 7, 7, 96, 3, 3, (1, 1), (1, 1), 2),
+    (2, 128, 8, 8, 24, 3, 3, (2, 2), (1, 1), 3),
+    (2, 256, 7, 7, 160, 3, 3, (1, 1), (1, 1), 4),
+    (4, 256, 5, 5, 256, 3, 3, (1, 1), (1, 1), 5),
+    (1, 512, 9, 11, 200, 1, 1, (2, 2), (0, 0), 6),
+    (2, 100, 12, 12, 70, 3, 3, (1, 1), (1, 1), 7),
+]
+
+
+@pytest.mark.parametrize("case", CASES)
+@pytest.mark.parametrize("variant", [2, 1, 0])
+@pytest.mark.parametrize("with_res", [False, True])
+def test_conv_sign_pack_epilogue(bnn, case, variant, with_res):
+    from paper_1705_09864_b200 import _lib
+    from paper_1705_09864_b200.layers import PackedNHWC
+    b, c, h, w, f, kh, kw, stride, pad, seed = case
+    _lib.call("bnn_set_umma_variant", variant)
+    try:
+        x, wt = wl.conv_case_inputs(case)
+        layer = bnn.QConvolution(c, f, (kh, kw), stride, pad, domain="dot")
+        layer.weight = wt
+        layer.pack()
+        bn = _BN(f, c * kh * kw, seed)
+        oh, ow = layer.output_hw(h, w)
+        res = None
+        if with_res:
+            res = torch.from_numpy(np.random.default_rng(seed + 50).standard_normal(
+                (b, f, oh, ow)).astype(np.float32)).cuda()
+            res.view(-1)[::9] = 0.0
+        xd = torch.from_numpy(x).cuda()
+        plain = layer.forward_fused(xd, bn, residual=res)
+        out = layer.forward_fused(xd, bn, residual=res, pack_out=True)
+        assert isinstance(out, PackedNHWC) and out.shape == (b, f, oh, ow)
+        y = plain.cpu().numpy()
+        assert np.array_equal(out.f32.cpu().numpy(), y)  # f32 output unchanged
+        # the unfused composition: conv -> BN -> (+ res) in the reference op order
+        p = orc.qconv_packed(x, wt, stride, pad).astype(np.float32)
+        ref = 2 * p - np.float32(c * kh * kw)
+        sh = (1, -1, 1, 1)
+        ref = bn.gamma.reshape(sh) * ((ref - bn.mean.reshape(sh)) * bn.inv.reshape(sh)) + \
+            bn.beta.reshape(sh)
+        if with_res:
+            ref = ref + res.cpu().numpy()
+        assert np.array_equal(y, ref.astype(np.float32))
+        words = out.words.cpu().numpy()
+        assert np.array_equal(words, _oracle_pack_nhwc(y))
+        assert np.array_equal(words, bnn.pack_nchw(plain).cpu().numpy())
+        # packed-only output (the f32 tensor is never written)
+        only = layer.forward_fused(xd, bn, residual=res, pack_out=True, f32_out=False)
+        assert only.f32 is None and np.array_equal(only.words.cpu().numpy(), words)
+        # a consumer conv reading the packed words == reading the f32 tensor
+        nxt = bnn.QConvolution(f, 40, (3, 3), (1, 1), (1, 1), domain="dot")
+        nxt.weight = np.random.default_rng(seed + 9).standard_normal((40, f, 3, 3)).astype(np.float32)
+        nxt.pack()
+        assert torch.equal(nxt.forward_fused(only), nxt.forward_fused(plain))
+    finally:
+        _lib.call("bnn_set_umma_variant", 2)
+
+
+def _gemm_ex(bnn, a, bw, m, n, k, c, ldc_m, ldc_n, e, algo="auto"):
+    from paper_1705_09864_b200 import _lib
+    _lib.call("bnn_xnor_gemm_ex", _lib.ptr(a), a.stride(0), _lib.ptr(bw), bw.stride(0), m, n, k,
+              0, 0, _lib.ptr(c), ldc_m, ldc_n, ctypes.byref(e), _lib.ALGOS[algo],
+              _lib.stream_ptr())
+
+
+@pytest.mark.parametrize("m,n,k", [(64, 40, 300), (1000, 256, 4096), (130, 77, 64), (32, 500, 1)])
+@pytest.mark.parametrize("transposed", [False, True])
+def test_dense_sign_pack_epilogue(bnn, m, n, k, transposed):
+    """QFullyConnected -> BN -> sign -> pack: words of the [N, M] layer output
+    rows (the K-contiguous rows the next dense layer reads)."""
+    from paper_1705_09864_b200.layers import make_epilogue
+    rng = np.random.default_rng(m + n + k)
+    w = rng.uniform(-1, 1, (m, k)).astype(np.float32)
+    x = rng.uniform(-1, 1, (n, k)).astype(np.float32)
+    wa = torch.from_numpy(orc.binarize_pack_rows(w)).cuda()
+    xb = torch.from_numpy(orc.binarize_pack_rows(x)).cuda()
+    bn = _BN(m, k, m)
+    words = torch.full((n, (m + 63) // 64 + 1), 0x5A5A, dtype=torch.int64).cuda().view(torch.uint64)
+    if transposed:  # layer output [N, M]
+        c = torch.empty((n, m), dtype=torch.float32, device="cuda")
+        ldc_m, ldc_n = 1, m
+    else:
+        c = torch.empty((m, n), dtype=torch.float32, device="cuda")
+        ldc_m, ldc_n = n, 1
+    flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+    e = make_epilogue(bnn._lib.DOT, bn, pack_out=words, pack_flags=flags)
+    _gemm_ex(bnn, wa, xb, m, n, k, c, ldc_m, ldc_n, e)
+    y = c.cpu().numpy() if transposed else c.cpu().numpy().T  # [N, M]
+    dot = np.float32(k) - 2 * orc.xor_popc_rowrow(orc.binarize_pack_rows(w),
+                                                   orc.binarize_pack_rows(x)).astype(np.float32)
+    ref = bn.gamma * ((dot.T - bn.mean) * bn.inv) + bn.beta
+    assert np.array_equal(y, ref.astype(np.float32))
+    got = words.cpu().numpy()
+    wpk = (m + 63) // 64
+    assert np.array_equal(got[:, :wpk], orc.binarize_pack_rows(np.ascontiguousarray(y)))
+    assert np.all(got[:, wpk:] == 0x5A5A)  # past ceil(M/64): untouched
+    assert int(flags.item()) == 0
+
+
+def test_sign_pack_flags_nonfinite_and_validation(bnn):
+    from paper_1705_09864_b200 import _lib
+    from paper_1705_09864_b200.layers import make_epilogue
+    m, n, k = 70, 33, 128
+    rng = np.random.default_rng(0)
+    wa = torch.from_numpy(orc.binarize_pack_rows(rng.uniform(-1, 1, (m, k)).astype(np.float32))).cuda()
+    xb = torch.from_numpy(orc.binarize_pack_rows(rng.uniform(-1, 1, (n, k)).astype(np.float32))).cuda()
+    bn = _BN(m, k, 1)
+    bn.mean[5] = np.nan  # channel 5 -> NaN outputs: binarize's ValueError case
+    c = torch.empty((m, n), dtype=torch.float32, device="cuda")
+    words = torch.empty((n, 2), dtype=torch.uint64, device="cuda")
+    flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+    e = make_epilogue(_lib.DOT, bn, pack_out=words, pack_flags=flags)
+    _gemm_ex(bnn, wa, xb, m, n, k, c, n, 1, e)
+    assert int(flags.item()) == 1
+    # the CUDA-core engines have no fused sign-pack
+    with pytest.raises(ValueError, match="tcgen05"):
+        _gemm_ex(bnn, wa, xb, m, n, k, c, n, 1, e, algo="popc")
+    small = torch.empty((n, 1), dtype=torch.uint64, device="cuda")
+    e2 = make_epilogue(_lib.DOT, None, pack_out=small, pack_flags=flags)
+    with pytest.raises(ValueError, match="pack_ld"):
+        _gemm_ex(bnn, wa, xb, m, n, k, c, n, 1, e2)
+    # a null f32 output is legal only with a packed output
+    e3 = make_epilogue(_lib.DOT, None)
+    with pytest.raises(ValueError, match="null"):
+        _lib.call("bnn_xnor_gemm_ex", _lib.ptr(wa), wa.stride(0), _lib.ptr(xb), xb.stride(0), m, n,
+                  k, 0, 0, None, n, 1, ctypes.byref(e3), _lib.ALGOS["auto"], _lib.stream_ptr())
