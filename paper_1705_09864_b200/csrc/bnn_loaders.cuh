@@ -137,6 +137,7 @@ struct GemmStore {
         C[i] = res ? __fadd_rn(v, __ldg(res + i)) : v;
     }
     __device__ void put_raw(int64_t m, int64_t n, float v) const { C[m * ldc_m + n * ldc_n] = v; }
+    __device__ float res_at(int64_t m, int64_t n) const { return __ldg(res + m * ldc_m + n * ldc_n); }
     __device__ const float *res_of(const float *p) const { return res + (p - C); }
     __device__ bool has_out() const { return C != nullptr; }
     // g[j] += res[m, n + j] for the first w columns (j < w, n + j < N)
@@ -194,6 +195,10 @@ struct ConvStore {  // y NCHW [B, F, oh*ow]; m = filter, n = b*ohw + pixel
     __device__ void put_raw(int64_t m, int64_t n, float v) const {
         int64_t b = n / ohw, p = n - b * ohw;
         y[(b * F + m) * ohw + p] = v;
+    }
+    __device__ float res_at(int64_t m, int64_t n) const {
+        int64_t b = n / ohw, p = n - b * ohw;
+        return __ldg(res + (b * F + m) * ohw + p);
     }
     __device__ const float *res_of(const float *p) const { return res + (p - y); }
     __device__ bool has_out() const { return y != nullptr; }

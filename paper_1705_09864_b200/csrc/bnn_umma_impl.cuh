@@ -1208,41 +1208,48 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                 }
                 // fused residual add in the row layout when the sign-pack needs the
                 // final values (the staged stores then skip their own residual add)
-                bool res_added = false;
-                if constexpr (Store::kPack) {
-                    if (store.res) {
-                        if (mok) store.add_res_row(m, nc, w, f);
-                        res_added = true;
-                    }
-                    // next layer's QActivation + pack: column j's 32 rows -> one u32
-                    // word (ballot); lane j keeps column j's word.  Rows past M pack
-                    // as 0 (their f values are not stored); columns past the tile / N
-                    // hold garbage and are zeroed (warp-uniform, tail chunks only) so
-                    // that nf = sum of 0 * f is NaN iff a stored value is NaN / Inf
+                // next layer's QActivation + pack: column j's 32 rows -> one u32 word
+                // (ballot); lane j keeps column j's word.  Rows past M pack as 0 (their
+                // values are not stored); columns past the tile / N hold garbage and
+                // are zeroed (warp-uniform, tail chunks only) so that nf = sum of 0 * g
+                // is NaN iff a stored value is NaN / Inf
+                auto emit_pack = [&](float (&g)[32]) {
                     if (!mok) {
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) f[j] = -1.0f;
+                        for (int j = 0; j < 32; ++j) g[j] = -1.0f;
                     }
                     const int64_t nvalid = N - nc < w ? N - nc : w;
                     if (nvalid < 32) {
 #pragma unroll
                         for (int j = 0; j < 32; ++j)
-                            if (j >= nvalid) f[j] = 0.0f;
+                            if (j >= nvalid) g[j] = 0.0f;
                     }
                     uint32_t word = 0;
                     float nf = 0.0f;
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
-                        const uint32_t bits = __ballot_sync(0xffffffffu, f[j] >= 0.0f);
-                        nf = __fmaf_rn(f[j], 0.0f, nf);
+                        const uint32_t bits = __ballot_sync(0xffffffffu, g[j] >= 0.0f);
+                        nf = __fmaf_rn(g[j], 0.0f, nf);
                         if (lane == j) word = bits;
                     }
                     if (lane < w && nc + lane < N)
                         ep.pack_out[(nc + lane) * ep.pack_ld32 + (mq >> 5)] = word;
                     if (ep.pack_flags && __any_sync(0xffffffffu, nf != 0.0f) && lane == 0)
                         atomicOr(ep.pack_flags, 1);
+                };
+                // residual + sign-pack: row-layout outputs add the residual here; staged
+                // (column-contiguous) outputs add it in the coalesced transposed phase,
+                // write the sums back to the staging block and pack from there (late)
+                bool res_added = false, pack_late = false;
+                if constexpr (Store::kPack) {
+                    if (store.res && !ncontig) {
+                        if (mok) store.add_res_row(m, nc, w, f);
+                        res_added = true;
+                    }
+                    pack_late = store.res && ncontig;
+                    if (!pack_late) emit_pack(f);
                 }
-                if ((dbg & 1024) || (Store::kPack && !store.has_out())) {
+                if ((dbg & 1024) || (Store::kPack && !store.has_out() && !pack_late)) {
                 } else if (ncontig) {
                     // staged 32 x 32 block: lane r writes its row (SW128 chunk swizzle)
                     const uint32_t row = stg + lane * 128;
@@ -1255,7 +1262,7 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                     // TMA store of the whole block when the output has a map and the block
                     // does not straddle an image (conv) -- the TMA unit clips rows past M
                     // and columns past N
-                    bool tma_st = store.has_map && (!store.res || (Store::kPack && res_added)) && w == 32;  // (whole block in the tile)
+                    bool tma_st = store.has_map && !store.res && w == 32;  // (whole block in the tile)
                     int64_t tb = 0, tp = nc;
                     if constexpr (Store::kConv) {
                         tb = nc / store.ohw;
@@ -1287,13 +1294,20 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                     // transposed write-out: lane = (row quarter, 4-column segment)
                     const int seg = lane & 7, rsub = lane >> 3;
                     const int64_t n = nc + 4 * seg;
+                    const bool out_f32 = !Store::kPack || store.has_out();
                     if (4 * seg < w && n < N) {
-                        float *col;
-                        const bool v4 = store.col4(n, col);
+                        float *col = nullptr;
+                        const bool v4 = out_f32 ? store.col4(n, col) : false;
                         // row 4 rr + rsub, chunk seg (rows 4 rr + rsub have r & 7 = 4 (rr & 1) + rsub)
                         auto src_of = [&](int rr) {
                             const int r = 4 * rr + rsub;
                             return stg + r * 128 + ((seg ^ (r & 7)) << 4);
+                        };
+                        // late sign-pack: the residual sums go back to the staging block
+                        auto keep = [&](int rr, const float4 &t) {
+                            if (Store::kPack && pack_late)
+                                asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(src_of(rr)),
+                                             "f"(t.x), "f"(t.y), "f"(t.z), "f"(t.w));
                         };
                         if (v4 && mq + 32 <= M) {
                             // common case: 8 unpredicated 16-byte stores, pointer bumps only
@@ -1305,12 +1319,13 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                                 asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
                                              : "=f"(t.x), "=f"(t.y), "=f"(t.z), "=f"(t.w)
                                              : "r"(src_of(rr)));
-                                if (store.res && !(Store::kPack && res_added)) {  // fused residual add
+                                if (store.res) {  // fused residual add
                                     const float4 r = __ldg(reinterpret_cast<const float4 *>(store.res_of(dst)));
                                     t.x = __fadd_rn(t.x, r.x); t.y = __fadd_rn(t.y, r.y);
                                     t.z = __fadd_rn(t.z, r.z); t.w = __fadd_rn(t.w, r.w);
                                 }
                                 *reinterpret_cast<float4 *>(dst) = t;
+                                keep(rr, t);
                                 dst += step;
                             }
                         } else {
@@ -1324,31 +1339,45 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                                              : "r"(src_of(rr)));
                                 if (v4) {
                                     float *dst = col + mr * ms;
-                                    if (store.res && !(Store::kPack && res_added)) {
+                                    if (store.res) {
                                         const float4 r = __ldg(reinterpret_cast<const float4 *>(store.res_of(dst)));
                                         t.x = __fadd_rn(t.x, r.x); t.y = __fadd_rn(t.y, r.y);
                                         t.z = __fadd_rn(t.z, r.z); t.w = __fadd_rn(t.w, r.w);
                                     }
                                     *reinterpret_cast<float4 *>(dst) = t;
                                 } else {
-                                    const float tv[4] = {t.x, t.y, t.z, t.w};
+                                    float tv[4] = {t.x, t.y, t.z, t.w};
 #pragma unroll
                                     for (int i = 0; i < 4; ++i)
                                         if (4 * seg + i < w && n + i < N) {
-                                            if (Store::kPack && res_added) store.put_raw(mr, n + i, tv[i]);
-                                            else store.put(mr, n + i, tv[i]);
+                                            if (store.res) tv[i] = __fadd_rn(tv[i], store.res_at(mr, n + i));
+                                            if (out_f32) store.put_raw(mr, n + i, tv[i]);
                                         }
+                                    t = make_float4(tv[0], tv[1], tv[2], tv[3]);
                                 }
+                                keep(rr, t);
                             }
                         }
                     }
                     __syncwarp();
+                    if constexpr (Store::kPack) {
+                        if (pack_late) {  // lane r re-reads its row: the final values
+#pragma unroll
+                            for (int j = 0; j < 8; ++j)
+                                asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+                                             : "=f"(f[4 * j]), "=f"(f[4 * j + 1]), "=f"(f[4 * j + 2]),
+                                               "=f"(f[4 * j + 3])
+                                             : "r"(row + ((j ^ (lane & 7)) << 4)));
+                            emit_pack(f);
+                            __syncwarp();
+                        }
+                    }
                 } else if (mok) {
                     // rows contiguous in memory (e.g. an [N, M] output): lanes = rows
 #pragma unroll
                     for (int j = 0; j < 32; ++j)
                         if (j < w && nc + j < N) {
-                            if (Store::kPack && res_added) store.put_raw(m, nc + j, f[j]);
+                            if (res_added) store.put_raw(m, nc + j, f[j]);
                             else store.put(m, nc + j, f[j]);
                         }
                 }
