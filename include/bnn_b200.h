@@ -209,6 +209,18 @@ int bnn_conv2d_f32_tc(const float *x, int64_t B, int64_t C, int64_t H, int64_t W
                       int64_t sh, int64_t sw, int64_t ph, int64_t pw, float *y,
                       bnn_stream_t stream);
 
+/* The ResNet-18 stem as one kernel: y = maxpool_3x3/2/1(relu?(BN(conv(x, w))))
+ * (bnn_conv2d_f32_tc's conv, bnn_bn_relu_maxpool_f32's post-op; no bias).  The
+ * pool runs on sign-adjusted conv outputs before the BatchNorm -- exact, since
+ * the rounded BN + ReLU is monotone per channel -- so only the pooled tensor
+ * is written.  BNN_EUNSUP outside F == 64, C*kh*kw <= 320, conv width <= 128,
+ * W % 4 == 0 (run the two calls instead). */
+int bnn_conv_bn_relu_maxpool_f32_tc(const float *x, int64_t B, int64_t C, int64_t H, int64_t W,
+                                    const float *w, int64_t F, int64_t kh, int64_t kw,
+                                    int64_t sh, int64_t sw, int64_t ph, int64_t pw,
+                                    const float *mean, const float *inv_std, const float *gamma,
+                                    const float *beta, int relu, float *y, bnn_stream_t stream);
+
 /* Words per pixel of the packed NHWC activation layout: ceil(C / 64). */
 int64_t bnn_conv_channel_words(int64_t C);
 

@@ -49,6 +49,9 @@ SIGNATURES = {
     "bnn_set_umma_variant": (_i32, [_i32]),
     "bnn_bn_relu_maxpool_f32": (_i32, [_vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _i32, _i32,
                                        _i32, _i32, _vp, _vp]),
+    "bnn_conv_bn_relu_maxpool_f32_tc": (_i32, [_vp, _i64, _i64, _i64, _i64, _vp, _i64, _i64, _i64,
+                                               _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _i32,
+                                               _vp, _vp]),
     "bnn_conv2d_f32_tc": (_i32, [_vp, _i64, _i64, _i64, _i64, _vp, _vp, _i64, _i64, _i64, _i64,
                                  _i64, _i64, _i64, _vp, _vp]),
     "bnn_xnor_gemm_ex": (_i32, [_vp, _i64, _vp, _i64, _i64, _i64, _i64, _i32, _i32, _vp, _i64,
@@ -124,3 +127,8 @@ def check(status: int, what: str = "") -> None:
 def call(name: str, *args) -> None:
     lib = load()
     check(getattr(lib, name)(*args), name)
+
+
+def call_status(name: str, *args) -> int:
+    """Call without raising: the status code (callers that handle BNN_EUNSUP)."""
+    return int(getattr(load(), name)(*args))

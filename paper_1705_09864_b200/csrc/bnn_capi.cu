@@ -65,6 +65,10 @@ int launch_bn_relu_maxpool(const float *, int64_t, int64_t, int64_t, int64_t, co
 int launch_conv2d_f32_tc(const float *, int64_t, int64_t, int64_t, int64_t, const float *,
                          const float *, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,
                          int64_t, int64_t, int64_t, float *, cudaStream_t);
+int launch_conv_bn_relu_maxpool_tc(const float *, int64_t, int64_t, int64_t, int64_t,
+                                   const float *, int64_t, int64_t, int64_t, int64_t, int64_t,
+                                   int64_t, int64_t, const float *, const float *, const float *,
+                                   const float *, int, float *, cudaStream_t);
 int launch_bconv2d_popc(const uint64_t *, int64_t, int64_t, int64_t, int64_t, const uint64_t *,
                         int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,
                         int64_t, float *, const Epilogue &, cudaStream_t, const float *);
@@ -308,6 +312,20 @@ int bnn_conv2d_f32_tc(const float *x, int64_t B, int64_t C, int64_t H, int64_t W
     const int64_t oh = (H + 2 * ph - kh) / sh + 1, ow = (W + 2 * pw - kw) / sw + 1;
     return launch_conv2d_f32_tc(x, B, C, H, W, w, bias, F, kh, kw, sh, sw, ph, pw, oh, ow, y,
                                 as_stream(stream));
+}
+
+int bnn_conv_bn_relu_maxpool_f32_tc(const float *x, int64_t B, int64_t C, int64_t H, int64_t W,
+                                    const float *w, int64_t F, int64_t kh, int64_t kw,
+                                    int64_t sh, int64_t sw, int64_t ph, int64_t pw,
+                                    const float *mean, const float *inv_std, const float *gamma,
+                                    const float *beta, int relu, float *y, bnn_stream_t stream) {
+    BNN_REQUIRE(B >= 0 && C >= 1 && H >= 1 && W >= 1 && F >= 1 && kh >= 1 && kw >= 1 &&
+                    sh >= 1 && sw >= 1 && ph >= 0 && pw >= 0 && H + 2 * ph >= kh &&
+                    W + 2 * pw >= kw,
+                BNN_EGEOM, "invalid convolution geometry");
+    BNN_REQUIRE(x && w && y && mean && inv_std && gamma && beta, BNN_EINVAL, "null pointer");
+    return launch_conv_bn_relu_maxpool_tc(x, B, C, H, W, w, F, kh, kw, sh, sw, ph, pw, mean,
+                                          inv_std, gamma, beta, relu, y, as_stream(stream));
 }
 
 int64_t bnn_conv_channel_words(int64_t C) { return C > 0 ? ceil_div(C, 64) : 0; }

@@ -52,7 +52,9 @@ struct Geom {
 };
 
 __device__ __forceinline__ uint32_t tf32_hi(float v) {
-    return (__float_as_uint(v) + 0x1000u) & 0xFFFFE000u;  // round to 10 mantissa bits
+    // truncate to 10 mantissa bits: lo = v - hi (exact) has |lo| < 2^-10 |v| and
+    // loses only its own bits below TF32 in the MMA (~2^-21 relative)
+    return __float_as_uint(v) & 0xFFFFE000u;
 }
 
 __device__ __forceinline__ void mma_tf32_ts(uint32_t d, uint32_t a_tmem, uint64_t bdesc,
@@ -74,6 +76,16 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32
         "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]),
         "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]),
         "r"(v[29]), "r"(v[30]), "r"(v[31])
+        : "memory");
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+        "%11, %12, %13, %14, %15, %16};\n" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+        "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),
+        "r"(v[15])
         : "memory");
 }
 
@@ -252,6 +264,401 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tf32x3_kernel(const __grid_c
 
 }  // namespace stem
 
+// ---------------------------------------------------------------------------
+// Fused stem: conv (3xTF32, as above) -> BatchNorm -> ReLU -> maxpool 3x3/2/1
+// (ResNet-18's stem, nets.StemPost; reference BN op order layers.py:598-602).
+// The pool runs before the BatchNorm on sign-adjusted values: with s_c = +1
+// (gamma >= 0) or -1 (gamma < 0), f(v) = relu?(bn(v)) is monotone in s_c v, so
+//     maxpool(f(v)) = f(s_c * maxpool(s_c * v))
+// exactly (negation is exact; the rounded BN ops are monotone), and the conv
+// output never leaves the SM: only the pooled tensor is written.
+//
+// Work item = (image, band of pooled rows); tile = one conv output row (OW <= 128
+// pixels = TMEM lanes), processed top to bottom so that the pooled rows are
+// completed in registers:
+//   warps 0-7   gather from the SMEM-staged input rows (zero-padded; for stride 2
+//               the columns are stored de-interleaved by parity, so the 32 lanes
+//               of a warp read 32 consecutive words), split hi/lo, tcgen05.st
+//   warps 8-9   loader: the C x kh input rows of the next conv row -> SMEM
+//               (double buffered)
+//   warp 10     TMEM allocator + MMA issuer (3 x 4 MMAs per 32-wide K chunk)
+//   warps 11-14 epilogue: TMEM -> s_c * v into a row buffer, horizontal 3-max,
+//               vertical running max in registers, BN + ReLU, pooled NCHW stores
+namespace stem {
+
+constexpr int kPLoadWarp0 = 8, kPLoadWarps = 4, kPMmaWarp = 12, kPEpiWarp0 = 13;
+constexpr int kPLoadBatch = 12;  // float4 loads in flight per loader thread (C*kh <= 24 rows)
+constexpr int kPThreads = (kPEpiWarp0 + kEpiWarps) * 32;
+constexpr int kRowPitchR = 132;  // epilogue row buffer pitch (floats)
+
+struct PoolGeom {
+    const float *x, *w, *mean, *inv, *gamma, *beta;
+    float *y;
+    int relu;
+    int C, H, W, kh, kw, sh, sw, ph, pw, OH, OW, PH, PW;
+    int K, nch;
+    int par;        // stride-2 parity layout of the staged rows
+    int rpitch;     // staged row pitch (floats)
+    int xs_floats;  // one staging buffer: C * kh * rpitch
+    int pyb, nbands, items;
+    int dbg;  // debug (BNN_STEM_DEBUG, wrong results): 1 no gather loads, 2 no MMAs,
+              // 4 no epilogue work, 8 no loader loads
+};
+
+struct PoolSmem {
+    int off_bhi, off_blo, off_ktab, off_xs, off_r, off_bn, off_bars, off_tmem, bytes;
+    __host__ __device__ PoolSmem(int nch, int xs_floats) {
+        off_bhi = 0;
+        off_blo = nch * NF * 128;
+        off_ktab = 2 * nch * NF * 128;
+        off_xs = off_ktab + nch * KC * 4;
+        off_r = off_xs + 2 * xs_floats * 4;
+        off_bn = off_r + NF * kRowPitchR * 4;
+        off_bars = off_bn + 5 * NF * 4;
+        off_tmem = off_bars + (2 * S + 8) * 8;
+        bytes = off_tmem + 16 + 1024;
+    }
+};
+
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
+
+// compile-time stem geometry (gather offsets become immediates); kStatic = false:
+// the runtime table
+struct GeoDyn {
+    static constexpr bool kStatic = false;
+};
+template <int kC, int kKH, int kKW, int kPitch>
+struct GeoStride2 {  // stride 2, parity layout, pitch kPitch
+    static constexpr bool kStatic = true;
+    static constexpr int K = kC * kKH * kKW;
+    __device__ static constexpr int off(int k) {
+        return k >= K ? 0
+                      : ((k / (kKH * kKW)) * kKH + (k % (kKH * kKW)) / kKW) * kPitch +
+                            ((k % kKW) & 1) * (kPitch / 2) + ((k % kKW) >> 1);
+    }
+};
+
+template <class Geo, int kChunk>
+__device__ __forceinline__ void gather_static(const float *src, uint32_t ta) {
+    if constexpr (kChunk * KC < Geo::K) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            uint32_t hi[16], lo[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const float v = src[Geo::off(kChunk * KC + 16 * h + j)];
+                hi[j] = tf32_hi(v);
+                lo[j] = __float_as_uint(v - __uint_as_float(hi[j]));
+            }
+            tmem_st16(ta + 16 * h, hi);
+            tmem_st16(ta + KC + 16 * h, lo);
+        }
+    }
+}
+
+template <class Geo>
+__global__ void __launch_bounds__(kPThreads, 1) conv_pool_kernel(const __grid_constant__ PoolGeom g) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    uint8_t *smem = smem_raw + (base - raw);
+    const PoolSmem L(g.nch, g.xs_floats);
+    const uint32_t s_bhi = base + L.off_bhi, s_blo = base + L.off_blo;
+    int *ktab = reinterpret_cast<int *>(smem + L.off_ktab);
+    float *xs = reinterpret_cast<float *>(smem + L.off_xs);
+    float *rbuf = reinterpret_cast<float *>(smem + L.off_r);
+    float *bnt = reinterpret_cast<float *>(smem + L.off_bn);  // sign, mean, inv, gamma, beta
+    const uint32_t bar_full = base + L.off_bars, bar_empty = bar_full + 8 * S;
+    const uint32_t bar_tfull = bar_empty + 8 * S, bar_tempty = bar_tfull + 16;
+    const uint32_t bar_xfull = bar_tempty + 16, bar_xempty = bar_xfull + 16;
+    uint32_t *s_tmem = reinterpret_cast<uint32_t *>(smem + L.off_tmem);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int kpad = g.nch * KC;
+
+    for (int i = tid; i < NF * kpad; i += kPThreads) {
+        const int r = i / kpad, k = i - r * kpad;
+        const float v = k < g.K ? __ldg(g.w + (int64_t)r * g.K + k) : 0.0f;
+        const uint32_t hi = tf32_hi(v);
+        const float lo = v - __uint_as_float(hi);
+        const int kb = (k & 31) * 4;
+        const uint32_t off = (uint32_t)((k >> 5) * (NF * 128) + (r >> 3) * 1024 + (r & 7) * 128 +
+                                        ((((kb >> 4) ^ (r & 7)) << 4) | (kb & 15)));
+        asm volatile("st.shared.u32 [%0], %1;\n" ::"r"(s_bhi + off), "r"(hi));
+        asm volatile("st.shared.f32 [%0], %1;\n" ::"r"(s_blo + off), "f"(lo));
+    }
+    // gather offsets relative to the pixel's base word; K padding reads the pixel's
+    // first tap (finite; its weights are zero)
+    for (int k = tid; k < kpad; k += kPThreads) {
+        int off = 0;
+        if (k < g.K) {
+            const int taps = g.kh * g.kw, ci = k / taps, r = k - ci * taps;
+            const int ky = r / g.kw, kx = r - ky * g.kw;
+            off = (ci * g.kh + ky) * g.rpitch + (g.par ? (kx & 1) * (g.rpitch >> 1) + (kx >> 1) : kx);
+        }
+        ktab[k] = off;
+    }
+    for (int i = tid; i < 2 * g.xs_floats; i += kPThreads) xs[i] = 0.0f;  // zero borders
+    for (int c = tid; c < NF; c += kPThreads) {
+        const float gm = __ldg(g.gamma + c);
+        bnt[c] = gm < 0.0f ? -1.0f : 1.0f;
+        bnt[NF + c] = __ldg(g.mean + c);
+        bnt[2 * NF + c] = __ldg(g.inv + c);
+        bnt[3 * NF + c] = gm;
+        bnt[4 * NF + c] = __ldg(g.beta + c);
+    }
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(bar_full + 8 * s, 4);
+            mbar_init(bar_empty + 8 * s, 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(bar_tfull + 8 * b, 1);
+            mbar_init(bar_tempty + 8 * b, kEpiWarps);
+            mbar_init(bar_xfull + 8 * b, kPLoadWarps);
+            mbar_init(bar_xempty + 8 * b, kProdWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    if (warp == kPMmaWarp) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+            smem_u32(s_tmem)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *s_tmem;
+
+    // the tile sequence every role walks: items (image, band) -> conv rows oy
+#define POOL_ITEMS_BEGIN                                                              \
+    for (int item = blockIdx.x; item < g.items; item += gridDim.x) {                  \
+        const int b = item / g.nbands, band = item - b * g.nbands;                    \
+        const int py0 = band * g.pyb, py1 = min(g.PH, py0 + g.pyb);                   \
+        const int oy_s = max(0, 2 * py0 - 1), oy_e = min(g.OH - 1, 2 * py1 - 1);
+#define POOL_ITEMS_END }
+
+    if (warp < kProdWarps) {
+        // ------------------------------------------------------------ gather
+        const int grp = warp >> 2, q = warp & 3, ox = q * 32 + lane;
+        const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16) + kAStage0;
+        const int pb = ox < g.OW ? (g.par ? ox : ox * g.sw) : 0;
+        int gch = 0, it = 0;
+        POOL_ITEMS_BEGIN
+        for (int oy = oy_s; oy <= oy_e; ++oy, ++it) {
+            const int xb = it & 1;
+            mbar_wait(bar_xfull + 8 * xb, (it >> 1) & 1);
+            const float *src = xs + xb * g.xs_floats + pb;
+            for (int c = 0; c < g.nch; ++c, ++gch) {
+                if ((gch & 1) != grp) continue;
+                const int st = gch % S;
+                mbar_wait(bar_empty + 8 * st, ((gch / S) & 1) ^ 1);
+                fence_after();
+                const uint32_t ta = tq + st * 2 * KC;
+                if (g.dbg & 1) {
+                } else if constexpr (Geo::kStatic) {
+                    switch (c) {  // compile-time gather offsets: LDS [base + imm]
+                        case 0: gather_static<Geo, 0>(src, ta); break;
+                        case 1: gather_static<Geo, 1>(src, ta); break;
+                        case 2: gather_static<Geo, 2>(src, ta); break;
+                        case 3: gather_static<Geo, 3>(src, ta); break;
+                        case 4: gather_static<Geo, 4>(src, ta); break;
+                        case 5: gather_static<Geo, 5>(src, ta); break;
+                        case 6: gather_static<Geo, 6>(src, ta); break;
+                        case 7: gather_static<Geo, 7>(src, ta); break;
+                        case 8: gather_static<Geo, 8>(src, ta); break;
+                        default: gather_static<Geo, 9>(src, ta); break;
+                    }
+                } else {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {  // 16 K values at a time (register budget)
+                        uint32_t hi[16], lo[16];
+#pragma unroll
+                        for (int j4 = 0; j4 < 4; ++j4) {
+                            const int4 o = reinterpret_cast<const int4 *>(ktab + c * KC + 16 * h)[j4];
+                            const int oo[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) {
+                                const float v = src[oo[i]];
+                                hi[4 * j4 + i] = tf32_hi(v);
+                                lo[4 * j4 + i] = __float_as_uint(v - __uint_as_float(hi[4 * j4 + i]));
+                            }
+                        }
+                        tmem_st16(ta + 16 * h, hi);
+                        tmem_st16(ta + KC + 16 * h, lo);
+                    }
+                }
+                asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+                fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(bar_full + 8 * st);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar_xempty + 8 * xb);
+        }
+        POOL_ITEMS_END
+    } else if (warp < kPMmaWarp) {
+        // ------------------------------------------------------------ loader
+        const int t = tid - kPLoadWarp0 * 32;
+        const int half = g.rpitch >> 1;
+        const int jcol = t & 63, rg = t >> 6, w4 = g.W >> 2;
+        auto scol = [&](int sc) { return g.par ? (sc & 1) * half + (sc >> 1) : sc; };
+        const int sa0 = scol(4 * jcol + g.pw), sa1 = scol(4 * jcol + 1 + g.pw);
+        const int sa2 = scol(4 * jcol + 2 + g.pw), sa3 = scol(4 * jcol + 3 + g.pw);
+        int it = 0;
+        POOL_ITEMS_BEGIN
+        const float *xb0 = g.x + (int64_t)b * g.C * g.H * g.W;
+        for (int oy = oy_s; oy <= oy_e; ++oy, ++it) {
+            const int xb = it & 1;
+            mbar_wait(bar_xempty + 8 * xb, ((it >> 1) & 1) ^ 1);
+            float *dst = xs + xb * g.xs_floats;
+            const int iy0 = oy * g.sh - g.ph;
+            // thread = (row parity rg, float4 column j): rows rg, rg + 2, ... of the
+            // C x kh staged rows; all loads of a row group in flight before the stores
+            const int rows = g.C * g.kh;
+            for (int j = jcol; j < w4; j += 64) {
+                float4 v[kPLoadBatch];
+#pragma unroll
+                for (int u = 0; u < kPLoadBatch; ++u) {
+                    const int r = rg + 2 * u;
+                    v[u] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+                    if (r < rows && !(g.dbg & 8)) {
+                        const int ci = r / g.kh, iy = iy0 + (r - ci * g.kh);
+                        if ((unsigned)iy < (unsigned)g.H)
+                            v[u] = __ldg(reinterpret_cast<const float4 *>(
+                                             xb0 + ((int64_t)ci * g.H + iy) * g.W) + j);
+                    }
+                }
+                const int a0 = j == jcol ? sa0 : scol(4 * j + g.pw), a1 = j == jcol ? sa1 : scol(4 * j + 1 + g.pw);
+                const int a2 = j == jcol ? sa2 : scol(4 * j + 2 + g.pw), a3 = j == jcol ? sa3 : scol(4 * j + 3 + g.pw);
+#pragma unroll
+                for (int u = 0; u < kPLoadBatch; ++u) {
+                    const int r = rg + 2 * u;
+                    if (r >= rows) break;
+                    float *row = dst + r * g.rpitch;
+                    row[a0] = v[u].x, row[a1] = v[u].y, row[a2] = v[u].z, row[a3] = v[u].w;
+                }
+            }
+            __syncwarp();
+            if ((t & 31) == 0) mbar_arrive(bar_xfull + 8 * xb);
+        }
+        POOL_ITEMS_END
+    } else if (warp == kPMmaWarp) {
+        // ------------------------------------------------------------ MMA issue
+        if (lane == 0) {
+            int gch = 0, it = 0;
+            POOL_ITEMS_BEGIN
+            for (int oy = oy_s; oy <= oy_e; ++oy, ++it) {
+                const int buf = it & 1;
+                mbar_wait(bar_tempty + 8 * buf, ((it >> 1) & 1) ^ 1);
+                fence_after();
+                const uint32_t d = tmem + buf * NF;
+                for (int c = 0; c < g.nch; ++c, ++gch) {
+                    const int st = gch % S;
+                    mbar_wait(bar_full + 8 * st, (gch / S) & 1);
+                    fence_after();
+                    const uint32_t a = tmem + kAStage0 + st * 2 * KC;
+                    const int nkk = (g.dbg & 2) ? 0 : min(KC / 8, (g.K - c * KC + 7) / 8);  // skip all-zero K steps
+                    for (int kk = 0; kk < nkk; ++kk) {
+                        const uint32_t boff = (uint32_t)(c * NF * 128 + kk * 32);
+                        const uint64_t bh = sw128_desc(s_bhi + boff), bl = sw128_desc(s_blo + boff);
+                        mma_tf32_ts(d, a + kk * 8, bh, (c | kk) != 0);
+                        mma_tf32_ts(d, a + kk * 8, bl, 1u);
+                        mma_tf32_ts(d, a + KC + kk * 8, bh, 1u);
+                    }
+                    umma_commit(bar_empty + 8 * st);
+                }
+                umma_commit(bar_tfull + 8 * buf);
+            }
+            POOL_ITEMS_END
+        }
+        __syncwarp();
+    } else {
+        // ------------------------------------------------------------ epilogue
+        const int q = warp & 3, et = tid - kPEpiWarp0 * 32;
+        const int ox = q * 32 + lane;
+        const int px = et & 63, c0 = et >> 6;  // pooled column, channel parity
+        float cur[32];
+        int it = 0;
+        POOL_ITEMS_BEGIN
+#pragma unroll
+        for (int i = 0; i < 32; ++i) cur[i] = -INFINITY;
+        float *yb = g.y + (int64_t)b * NF * g.PH * g.PW;
+        auto emit = [&](int py) {
+            if (px >= g.PW) return;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                const int c = c0 + 2 * i;
+                float v = __fmul_rn(cur[i], bnt[c]);
+                v = __fadd_rn(__fmul_rn(bnt[3 * NF + c], __fmul_rn(__fsub_rn(v, bnt[NF + c]),
+                                                                    bnt[2 * NF + c])),
+                              bnt[4 * NF + c]);
+                if (g.relu) v = fmaxf(v, 0.0f);
+                yb[((int64_t)c * g.PH + py) * g.PW + px] = v;
+            }
+        };
+        for (int oy = oy_s; oy <= oy_e; ++oy, ++it) {
+            const int buf = it & 1;
+            mbar_wait_sleep(bar_tfull + 8 * buf, (it >> 1) & 1);
+            fence_after();
+            const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + buf * NF;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                uint32_t v[32];
+                tmem_ld32(ta + 32 * h, v);
+                if (ox < g.OW) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        rbuf[(32 * h + j) * kRowPitchR + ox] =
+                            __fmul_rn(__uint_as_float(v[j]), bnt[32 * h + j]);
+                }
+            }
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar_tempty + 8 * buf);
+            epi_bar();
+            // horizontal 3-max (window 2px-1 .. 2px+1, clipped) of this conv row, folded
+            // into the pooled rows: an odd conv row completes pooled row (oy - 1) / 2
+            // and starts (oy + 1) / 2, an even one is the middle row of oy / 2
+            if (px < g.PW && !(g.dbg & 4)) {
+                const int xl = 2 * px - 1, xr = 2 * px + 1;
+                const bool odd = oy & 1, done = odd && ((oy - 1) >> 1) >= py0;
+                float *yrow = yb + (int64_t)((oy - 1) >> 1) * g.PW + px;
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    const int c = c0 + 2 * i;
+                    const float *rr = rbuf + c * kRowPitchR;
+                    float m = rr[2 * px];
+                    if (xl >= 0) m = fmaxf(m, rr[xl]);
+                    if (xr < g.OW) m = fmaxf(m, rr[xr]);
+                    if (done) {
+                        float v = __fmul_rn(fmaxf(cur[i], m), bnt[c]);
+                        v = __fadd_rn(__fmul_rn(bnt[3 * NF + c],
+                                                __fmul_rn(__fsub_rn(v, bnt[NF + c]), bnt[2 * NF + c])),
+                                      bnt[4 * NF + c]);
+                        if (g.relu) v = fmaxf(v, 0.0f);
+                        yrow[(int64_t)c * g.PH * g.PW] = v;
+                    }
+                    cur[i] = odd ? m : fmaxf(cur[i], m);
+                }
+            }
+            epi_bar();  // the row buffer is free for the next conv row
+        }
+        if (!(oy_e & 1) && (oy_e >> 1) < py1) emit(oy_e >> 1);  // last pooled row without a row below
+        POOL_ITEMS_END
+    }
+#undef POOL_ITEMS_BEGIN
+#undef POOL_ITEMS_END
+    fence_before();
+    __syncthreads();
+    if (warp == kPMmaWarp) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+    }
+}
+
+}  // namespace stem
+
 int launch_conv2d_f32_tc(const float *x, int64_t B, int64_t C, int64_t H, int64_t W,
                          const float *w, const float *bias, int64_t F, int64_t kh, int64_t kw,
                          int64_t sh, int64_t sw, int64_t ph, int64_t pw, int64_t oh, int64_t ow,
@@ -281,6 +688,72 @@ int launch_conv2d_f32_tc(const float *x, int64_t B, int64_t C, int64_t H, int64_
     const int grid = g.ntiles < sm_count() ? g.ntiles : sm_count();
     conv_tf32x3_kernel<<<grid, kThreads, Smem::kBytes, s>>>(g);
     return check_launch("conv_tf32x3_kernel");
+}
+
+
+// conv (3xTF32) + BN + ReLU + maxpool 3x3/2/1 fused; BNN_EUNSUP when the shape
+// does not fit (the caller then runs the conv and the post-op separately)
+int launch_conv_bn_relu_maxpool_tc(const float *x, int64_t B, int64_t C, int64_t H, int64_t W,
+                                   const float *w, int64_t F, int64_t kh, int64_t kw, int64_t sh,
+                                   int64_t sw, int64_t ph, int64_t pw, const float *mean,
+                                   const float *inv, const float *gamma, const float *beta,
+                                   int relu, float *y, cudaStream_t s) {
+    using namespace stem;
+    const int64_t K = C * kh * kw;
+    const int64_t OH = (H + 2 * ph - kh) / sh + 1, OW = (W + 2 * pw - kw) / sw + 1;
+    const int64_t PH = (OH + 2 - 3) / 2 + 1, PW = (OW + 2 - 3) / 2 + 1;
+    if (F != NF || K > kMaxChunks * KC || OW > stem::BM || OW < 2 || OH < 2 || W % 4 != 0 ||
+        (reinterpret_cast<uintptr_t>(x) & 15) || PW > 64 || C * H * W >= (1ll << 31) ||
+        C * kh > 2 * kPLoadBatch || W / 4 > 64 * 8)
+        return set_error(BNN_EUNSUP, "fused stem: unsupported shape");
+    PoolGeom g{};
+    g.x = x, g.w = w, g.mean = mean, g.inv = inv, g.gamma = gamma, g.beta = beta, g.y = y;
+    g.relu = relu;
+    {
+        const char *e = getenv("BNN_STEM_DEBUG");
+        g.dbg = e ? atoi(e) : 0;
+    }
+    g.C = (int)C, g.H = (int)H, g.W = (int)W, g.kh = (int)kh, g.kw = (int)kw, g.sh = (int)sh;
+    g.sw = (int)sw, g.ph = (int)ph, g.pw = (int)pw, g.OH = (int)OH, g.OW = (int)OW;
+    g.PH = (int)PH, g.PW = (int)PW, g.K = (int)K, g.nch = (int)ceil_div(K, KC);
+    g.par = sw == 2;
+    const int64_t ws = (OW - 1) * sw + kw;  // staged columns per row (incl. padding)
+    int64_t pitch = g.par ? 2 * ceil_div(ws, 2) : ws;
+    pitch = ceil_div(pitch, 4) * 4 + (g.par ? 2 : 1);  // spread rows over banks
+    if (g.par && (pitch & 1)) pitch += 1;
+    if (pw + W > ws + 0 && pw + W > pitch) return set_error(BNN_EUNSUP, "fused stem: row pitch");
+    g.rpitch = (int)pitch;
+    g.xs_floats = (int)(C * kh * pitch);
+    // pooled-row bands: about 4 items per SM-wave unit of work, 14 rows for ResNet
+    int64_t pyb = PH >= 14 ? 14 : PH;
+    g.pyb = (int)pyb;
+    g.nbands = (int)ceil_div(PH, pyb);
+    if (B * g.nbands >= (1ll << 31)) return set_error(BNN_EUNSUP, "fused stem: too many items");
+    g.items = (int)(B * g.nbands);
+    const PoolSmem L(g.nch, g.xs_floats);
+    if (L.bytes > 227 * 1024) return set_error(BNN_EUNSUP, "fused stem: shared memory");
+    if (B == 0) return BNN_OK;
+    const int grid = g.items < sm_count() ? g.items : sm_count();
+    if (C == 3 && kh == 7 && kw == 7 && g.par && pitch <= 234) {  // ResNet stem: static offsets
+        using G = GeoStride2<3, 7, 7, 234>;
+        g.rpitch = 234;
+        g.xs_floats = (int)(C * kh * 234);
+        const PoolSmem L2(g.nch, g.xs_floats);
+        static bool configured = false;
+        if (!configured) {
+            cudaFuncSetAttribute(conv_pool_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+            configured = true;
+        }
+        conv_pool_kernel<G><<<grid, kPThreads, L2.bytes, s>>>(g);
+    } else {
+        static bool configured = false;
+        if (!configured) {
+            cudaFuncSetAttribute(conv_pool_kernel<GeoDyn>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+            configured = true;
+        }
+        conv_pool_kernel<GeoDyn><<<grid, kPThreads, L.bytes, s>>>(g);
+    }
+    return check_launch("conv_pool_kernel");
 }
 
 }  // namespace bnn

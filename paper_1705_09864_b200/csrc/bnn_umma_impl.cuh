@@ -1313,20 +1313,38 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                             // common case: 8 unpredicated 16-byte stores, pointer bumps only
                             float *dst = col + (mq + rsub) * ms;
                             const int64_t step = 4 * ms;
+                            if (store.res) {
+                                // fused residual add: all 8 loads in flight before the
+                                // stores (the output may alias nothing, but the compiler
+                                // cannot know, and would serialise load -> store pairs)
+                                float4 r[8];
+                                const float *rs = store.res_of(dst);
 #pragma unroll
-                            for (int rr = 0; rr < 8; ++rr) {
-                                float4 t;
-                                asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
-                                             : "=f"(t.x), "=f"(t.y), "=f"(t.z), "=f"(t.w)
-                                             : "r"(src_of(rr)));
-                                if (store.res) {  // fused residual add
-                                    const float4 r = __ldg(reinterpret_cast<const float4 *>(store.res_of(dst)));
-                                    t.x = __fadd_rn(t.x, r.x); t.y = __fadd_rn(t.y, r.y);
-                                    t.z = __fadd_rn(t.z, r.z); t.w = __fadd_rn(t.w, r.w);
+                                for (int rr = 0; rr < 8; ++rr)
+                                    r[rr] = __ldg(reinterpret_cast<const float4 *>(rs + rr * step));
+#pragma unroll
+                                for (int rr = 0; rr < 8; ++rr) {
+                                    float4 t;
+                                    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+                                                 : "=f"(t.x), "=f"(t.y), "=f"(t.z), "=f"(t.w)
+                                                 : "r"(src_of(rr)));
+                                    t.x = __fadd_rn(t.x, r[rr].x); t.y = __fadd_rn(t.y, r[rr].y);
+                                    t.z = __fadd_rn(t.z, r[rr].z); t.w = __fadd_rn(t.w, r[rr].w);
+                                    *reinterpret_cast<float4 *>(dst) = t;
+                                    keep(rr, t);
+                                    dst += step;
                                 }
-                                *reinterpret_cast<float4 *>(dst) = t;
-                                keep(rr, t);
-                                dst += step;
+                            } else {
+#pragma unroll
+                                for (int rr = 0; rr < 8; ++rr) {
+                                    float4 t;
+                                    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+                                                 : "=f"(t.x), "=f"(t.y), "=f"(t.z), "=f"(t.w)
+                                                 : "r"(src_of(rr)));
+                                    *reinterpret_cast<float4 *>(dst) = t;
+                                    keep(rr, t);
+                                    dst += step;
+                                }
                             }
                         } else {
                             for (int rr = 0; rr < 8; ++rr) {

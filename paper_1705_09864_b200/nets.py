@@ -167,6 +167,34 @@ class StemPost:
     def __init__(self, channels, rng, k=3, stride=2, pad=1):
         self.bn, self.relu, self.pool = BatchNorm(channels, rng), ReLU(), MaxPool2d(k, stride, pad)
 
+    def fusable(self, conv: "Conv2d") -> bool:
+        """The fused conv + post-op kernel covers the tensor-core conv with a 3x3/2/1
+        pool (ResNet-18's stem)."""
+        p = self.pool
+        return (conv.engine == "tc" and conv.tc_supported() and conv.bias is None and
+                (p.k, p.stride, p.pad) == (3, 2, 1))
+
+    def forward_fused_conv(self, conv: "Conv2d", x: torch.Tensor) -> torch.Tensor:
+        """maxpool(relu(BN(conv(x)))) in one kernel (bnn_conv_bn_relu_maxpool_f32_tc):
+        the pool runs on sign-adjusted conv outputs before the BatchNorm, which is
+        exact because the rounded BN + ReLU is monotone per channel."""
+        x = x.contiguous()
+        b, c, h, w = x.shape
+        oh = (h + 2 * conv.pad - conv.k) // conv.stride + 1
+        ow = (w + 2 * conv.pad - conv.k) // conv.stride + 1
+        ph, pw = (oh - 1) // 2 + 1, (ow - 1) // 2 + 1
+        y = torch.empty((b, conv.cout, ph, pw), dtype=torch.float32, device=x.device)
+        mean, inv, gamma, beta = self.bn.device_params()
+        st = _lib.call_status("bnn_conv_bn_relu_maxpool_f32_tc", _lib.ptr(x), b, c, h, w,
+                              _lib.ptr(conv._dev("weight")), conv.cout, conv.k, conv.k,
+                              conv.stride, conv.stride, conv.pad, conv.pad, _lib.ptr(mean),
+                              _lib.ptr(inv), _lib.ptr(gamma), _lib.ptr(beta), 1, _lib.ptr(y),
+                              _lib.stream_ptr())
+        if st == _lib.EUNSUP:  # shape outside the fused kernel: two kernels
+            return self.forward(conv.forward(x), INFER_PACKED)
+        _lib.check(st, "bnn_conv_bn_relu_maxpool_f32_tc")
+        return y
+
     def forward(self, x, mode=INFER_FLOAT):
         if mode != INFER_PACKED:
             return self.pool.forward(self.relu.forward(self.bn.forward(x)))
@@ -187,6 +215,7 @@ class Sequential:
         self.layers = list(layers)
 
     fuse_bn = True  # infer_packed: a binary layer's following BatchNorm runs in its epilogue
+    fuse_stem = True  # infer_packed: float stem conv + StemPost as one tensor-core kernel
 
     def forward(self, x, mode=INFER_FLOAT, capture=None):
         i, n = 0, len(self.layers)
@@ -195,6 +224,14 @@ class Sequential:
             nxt = self.layers[i + 1] if i + 1 < n else None
             if isinstance(x, PackedNHWC) and not isinstance(layer, BinaryBasicBlock):
                 x = x.float()  # a float consumer of a packed activation
+            if (mode == INFER_PACKED and self.fuse_stem and isinstance(layer, Conv2d)
+                    and isinstance(nxt, StemPost) and nxt.fusable(layer)):
+                x = nxt.forward_fused_conv(layer, x)  # conv + BN + ReLU + maxpool, one kernel
+                if capture is not None:
+                    capture.append(None)
+                    capture.append(x)
+                i += 2
+                continue
             if (mode == INFER_PACKED and self.fuse_bn and isinstance(nxt, BatchNorm)
                     and isinstance(layer, (QConvolution, QFullyConnected)) and layer.bits == 1):
                 x = layer.forward_fused(x, nxt)

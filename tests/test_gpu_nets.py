@@ -172,3 +172,23 @@ def test_conv2d_f32_tensor_core_accuracy(nets, case):
     conv.engine = "cudnn"
     y_cudnn = conv.forward(xd).cpu().double()
     assert float(err.max()) <= 4 * float((y_cudnn - ref).abs().max()) + 1e-6
+
+
+@pytest.mark.parametrize("shape", [(2, 3, 224, 224), (3, 3, 36, 36), (2, 3, 30, 44), (1, 5, 20, 16)])
+def test_fused_stem_conv_pool_bit_identical(nets, shape):
+    """bnn_conv_bn_relu_maxpool_f32_tc == bnn_conv2d_f32_tc followed by BatchNorm ->
+    ReLU -> MaxPool 3x3/2/1 bit for bit (pool-before-BN by monotonicity, negative and
+    zero gammas included); the first case is ResNet-18's stem."""
+    import paper_1705_09864_b200 as bnn
+    rng = np.random.default_rng(shape[2])
+    conv = nets.Conv2d(shape[1], 64, 7, stride=2, pad=3, bias=False, rng=rng)
+    post = nets.StemPost(64, rng, 3, 2, 1)
+    post.bn.gamma[::3] *= -1.0
+    post.bn.gamma[1] = 0.0
+    post.bn.gamma[4] = -0.0
+    assert post.fusable(conv)
+    x = torch.randn(shape, generator=torch.Generator().manual_seed(shape[3])).cuda()
+    fused = post.forward_fused_conv(conv, x)
+    conv_out = conv.forward(x)
+    assert torch.equal(fused, post.forward(conv_out, bnn.INFER_PACKED))
+    assert torch.equal(fused, post.forward(conv_out, bnn.INFER_FLOAT))

@@ -1,24 +1,37 @@
-"""fp32 stem conv (7x7/2, 3->64, 224^2, batch 256): cuDNN NCHW vs channels_last, TF32 off."""
+"""Stem timing (ResNet-18 conv7x7/2 3->64 + BN + ReLU + maxpool, batch 256): the fused
+tensor-core kernel, the unfused tensor-core conv + StemPost, and cuDNN f32 (TF32 off)."""
+import sys
+
+import numpy as np
 import torch
-torch.backends.cudnn.allow_tf32 = False
-torch.backends.cuda.matmul.allow_tf32 = False
-torch.backends.cudnn.benchmark = True
-x = torch.randn(256, 3, 224, 224, device="cuda")
-w = torch.randn(64, 3, 7, 7, device="cuda")
+
+sys.path.insert(0, ".")
+import paper_1705_09864_b200 as bnn  # noqa: E402
+from paper_1705_09864_b200 import nets  # noqa: E402
+
+
 def t(fn, n=5):
-    for _ in range(2): fn()
+    for _ in range(2):
+        fn()
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(True), torch.cuda.Event(True)
     s.record()
-    for _ in range(n): fn()
-    e.record(); e.synchronize()
+    for _ in range(n):
+        fn()
+    e.record()
+    e.synchronize()
     return s.elapsed_time(e) / n
-f = torch.nn.functional.conv2d
-print("nchw ms", t(lambda: f(x, w, stride=2, padding=3)))
-xc, wc = x.to(memory_format=torch.channels_last), w.to(memory_format=torch.channels_last)
-print("nhwc ms", t(lambda: f(xc, wc, stride=2, padding=3)))
-y1 = f(x, w, stride=2, padding=3); y2 = f(xc, wc, stride=2, padding=3)
-print("max |diff| nchw vs nhwc", (y1 - y2).abs().max().item())
-# reference: fp64 on a slice
-y64 = f(x[:2].double(), w.double(), stride=2, padding=3)
-print("max rel err nchw", ((y1[:2].double() - y64).abs().max() / y64.abs().max()).item(), "nhwc", ((y2[:2].double() - y64).abs().max() / y64.abs().max()).item())
+
+
+bnn.load_library()
+b = int(sys.argv[1]) if len(sys.argv) > 1 else 256
+rng = np.random.default_rng(0)
+conv = nets.Conv2d(3, 64, 7, stride=2, pad=3, bias=False, rng=rng)
+post = nets.StemPost(64, rng, 3, 2, 1)
+x = torch.randn(b, 3, 224, 224, device="cuda")
+print("fused ms", t(lambda: post.forward_fused_conv(conv, x)))
+print("tc conv ms", t(lambda: conv.forward(x)))
+y = conv.forward(x)
+print("stempost ms", t(lambda: post.forward(y, bnn.INFER_PACKED)))
+conv.engine = "cudnn"
+print("cudnn conv ms", t(lambda: conv.forward(x)))
