@@ -161,3 +161,36 @@ def test_host_layer_constructors():
         layers.QActivation(1).forward(np.zeros(3), "bogus")
     with pytest.raises(layers.ModeError):
         layers.QActivation(1).forward(np.zeros(3), layers.TRAIN_FLOAT)
+
+
+def test_sign_pack_and_stem_validation(lib):
+    """Argument checks of the fused sign-pack epilogue and the float stem entry
+    points (no CUDA call is made before validation fails)."""
+    import ctypes
+    from paper_1705_09864_b200 import _lib as L
+    e = L.Epilogue()
+    e.domain = 1
+    e.pack_out, e.pack_ld = 16, 1
+    rc = lib.bnn_xnor_gemm_ex(16, 2, 16, 2, 70, 8, 128, 0, 0, 16, 8, 1, ctypes.byref(e), 1, None)
+    assert rc == -7 and b"tcgen05" in lib.bnn_last_error()  # CUDA-core engines: no sign-pack
+    rc = lib.bnn_xnor_gemm_ex(16, 2, 16, 2, 70, 8, 128, 0, 0, 16, 8, 1, ctypes.byref(e), 0, None)
+    assert rc == -5 and b"pack_ld" in lib.bnn_last_error()  # ceil(70/64) = 2 words needed
+    e2 = L.Epilogue()
+    e2.domain = 1
+    rc = lib.bnn_xnor_gemm_ex(16, 2, 16, 2, 70, 8, 128, 0, 0, None, 8, 1, ctypes.byref(e2), 0, None)
+    assert rc == -1  # a null f32 output needs a packed output
+    rc = lib.bnn_bconv2d_ex(16, 1, 64, 8, 8, 16, 64, 3, 3, 1, 1, 1, 1, None, ctypes.byref(e2), 0,
+                            None)
+    assert rc == -1
+    # float stem conv: geometry, pointers, supported shapes
+    assert lib.bnn_conv2d_f32_tc(16, 1, 3, 4, 4, 16, None, 64, 7, 7, 2, 2, 0, 0, 16, None) == -6
+    assert lib.bnn_conv2d_f32_tc(None, 1, 3, 8, 8, 16, None, 64, 7, 7, 2, 2, 3, 3, 16, None) == -1
+    assert lib.bnn_conv2d_f32_tc(16, 1, 3, 8, 8, 16, None, 32, 7, 7, 2, 2, 3, 3, 16, None) == -7
+    assert lib.bnn_conv2d_f32_tc(16, 1, 9, 8, 8, 16, None, 64, 7, 7, 2, 2, 3, 3, 16, None) == -7
+    args = [16, 1, 3, 16, 16, 16, 64, 7, 7, 2, 2, 3, 3, 16, 16, 16, 16, 1, 16, None]
+    args[6] = 48  # F != 64
+    assert lib.bnn_conv_bn_relu_maxpool_f32_tc(*args) == -7
+    args[6], args[4] = 64, 18  # W % 4 != 0
+    assert lib.bnn_conv_bn_relu_maxpool_f32_tc(*args) == -7
+    args[4], args[13] = 16, None
+    assert lib.bnn_conv_bn_relu_maxpool_f32_tc(*args) == -1
