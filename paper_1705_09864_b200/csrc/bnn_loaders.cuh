@@ -138,6 +138,9 @@ struct GemmStore {
     }
     __device__ void put_raw(int64_t m, int64_t n, float v) const { C[m * ldc_m + n * ldc_n] = v; }
     __device__ float res_at(int64_t m, int64_t n) const { return __ldg(res + m * ldc_m + n * ldc_n); }
+    // element (m, n) lives at out_ptr()[col_off(n) + m * m_stride()]
+    __device__ int64_t col_off(int64_t n) const { return n * ldc_n; }
+    __device__ float *out_ptr() const { return C; }
     __device__ const float *res_of(const float *p) const { return res + (p - C); }
     __device__ bool has_out() const { return C != nullptr; }
     // g[j] += res[m, n + j] for the first w columns (j < w, n + j < N)
@@ -200,6 +203,12 @@ struct ConvStore {  // y NCHW [B, F, oh*ow]; m = filter, n = b*ohw + pixel
         int64_t b = n / ohw, p = n - b * ohw;
         return __ldg(res + (b * F + m) * ohw + p);
     }
+    // element (m, n) lives at out_ptr()[col_off(n) + m * m_stride()]
+    __device__ int64_t col_off(int64_t n) const {
+        const int64_t b = n / ohw;
+        return b * F * ohw + (n - b * ohw);
+    }
+    __device__ float *out_ptr() const { return y; }
     __device__ const float *res_of(const float *p) const { return res + (p - y); }
     __device__ bool has_out() const { return y != nullptr; }
     // g[j] += res[m, n + j] for the first w columns (j < w, n + j < npix); the

@@ -1347,6 +1347,14 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                                 }
                             }
                         } else {
+                            // the lane's 4 columns: element offsets of row 0 (one division per
+                            // lane, not per element), -1 past the tile / N
+                            int64_t coff[4];
+                            if (!v4) {
+#pragma unroll
+                                for (int i = 0; i < 4; ++i)
+                                    coff[i] = (4 * seg + i < w && n + i < N) ? store.col_off(n + i) : -1;
+                            }
                             for (int rr = 0; rr < 8; ++rr) {
                                 const int r = 4 * rr + rsub;
                                 const int64_t mr = mq + r;
@@ -1365,11 +1373,12 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                                     *reinterpret_cast<float4 *>(dst) = t;
                                 } else {
                                     float tv[4] = {t.x, t.y, t.z, t.w};
+                                    const int64_t ro = mr * ms;
 #pragma unroll
                                     for (int i = 0; i < 4; ++i)
-                                        if (4 * seg + i < w && n + i < N) {
-                                            if (store.res) tv[i] = __fadd_rn(tv[i], store.res_at(mr, n + i));
-                                            if (out_f32) store.put_raw(mr, n + i, tv[i]);
+                                        if (coff[i] >= 0) {
+                                            if (store.res) tv[i] = __fadd_rn(tv[i], __ldg(store.res + coff[i] + ro));
+                                            if (out_f32) store.out_ptr()[coff[i] + ro] = tv[i];
                                         }
                                     t = make_float4(tv[0], tv[1], tv[2], tv[3]);
                                 }
@@ -1687,8 +1696,14 @@ static int launch_fp4(const ALoad &a, const BLoad &b, const Store &st, const Epi
 template <int kVec, class ALoad, class BLoad, class Store>
 static int launch_umma(const ALoad &a, const BLoad &b, const Store &st, const Epilogue &ep,
                        int64_t M, int64_t N, int64_t kw32, cudaStream_t s) {
-    if constexpr (!std::is_same<BLoad, TmaConv>::value)
-        if (umma_variant() == 0) return launch_umma_cfg<256, false, kVec>(a, b, st, ep, M, N, kw32, s);
+    if constexpr (!std::is_same<BLoad, TmaConv>::value) {
+        // variant 0 (128 x 256 tiles, A and B through SMEM) also by default for cp.async-fed
+        // shapes with M <= 64 (e.g. ResNet-18 layer1 convs, 64 filters): measured 1.1-1.4x
+        // the A-in-TMEM engine there (tools/l1_variants.sh)
+        const bool small_m = umma_variant() == 2 && M <= 64 && !umma::is_tma<ALoad>::value;
+        if (umma_variant() == 0 || small_m)
+            return launch_umma_cfg<256, false, kVec>(a, b, st, ep, M, N, kw32, s);
+    }
     if constexpr (umma::is_tma<ALoad>::value) {
         if (umma_variant() == 2) {
             // long K (>= 24 superstages per tile): two expander sets on alternate
