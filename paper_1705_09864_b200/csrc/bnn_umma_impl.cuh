@@ -1064,6 +1064,16 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
             tmap.decode(tile, tm, tn);
             const int64_t mq = (int64_t)tm * C::kTmBM + crank * BM + q * 32, n0 = (int64_t)tn * BN;
             const int64_t m = mq + lane;
+            if (store.res && ncontig && m < M) {
+                // warm L2 with this tile's residual blocks while the MMAs run: lane r
+                // prefetches row m's 128-byte segment of each of its 32-column chunks
+                for (int c = h; c * 32 < BN; c += C::kEpiWarps / 4) {
+                    const int64_t nc = n0 + c * 32;
+                    if (nc >= N) break;
+                    const float *pr = store.res + store.col_off(nc) + m * ms;
+                    asm volatile("prefetch.global.L2 [%0];\n" ::"l"(pr));
+                }
+            }
             mbar_wait_sleep(bar_tfull + 8 * buf, (uint32_t)(it / C::kAccBufs) & 1u);
             mbar_wait_sleep(bar_pfull + 8 * buf, (uint32_t)(it / C::kAccBufs) & 1u);
             fence_after();
