@@ -148,7 +148,7 @@ struct Cfg {
     // shapes that fit in one wave of CTAs
     static constexpr int kMmaN = BN > 256 ? BN / 2 : BN;
     static constexpr int kNMma = BN / kMmaN;
-    static_assert(!kFp4 || (!kATmem && kPlanes == 1 && kTma), "fp4 engine: SS operands, TMA-fed");
+    static_assert(!kFp4 || (kPlanes == 1 && kTma && !(kATmem && kPair)), "fp4 engine: TMA-fed");
     static constexpr int kProducers = BM + kBRows;             // one thread per operand row
     static constexpr int kProducerWarps = (kProducers + 31) / 32;
     // kind::mxf4: two expander sets take alternate superstages, so each warp's
@@ -176,15 +176,19 @@ struct Cfg {
     static constexpr int kStageB = kBRows * kStageRow;
     static constexpr int kStageBytes = kStageA + kStageB;
     static constexpr int kSuperBytes = kSub * kStageBytes;
-    static constexpr int ES = kATmem ? 2 : (kPair ? BNN_PAIR_ES : (kFp4 ? (BN > 256 ? 2 : (BN <= 176 ? BNN_FP4_ES : 3)) : 3));  // expanded superstage buffers
-    static constexpr int kFp4A = BM * 128;      // fp4: A block of a superstage buffer
+    static constexpr int ES = (kATmem && !kFp4) ? 2 : (kATmem ? ((512 - 2 * BN - 32) / 32 < 4 ? (512 - 2 * BN - 32) / 32 : 4) : (kPair ? BNN_PAIR_ES : (kFp4 ? (BN > 256 ? 2 : (BN <= 176 ? BNN_FP4_ES : 3)) : 3)));  // expanded superstage buffers
+    static constexpr int kFp4A = kATmem ? 0 : BM * 128;  // fp4: A block of a superstage buffer
+    // fp4 with A in TMEM: one 128-byte row per superstage = 32 TMEM columns per stage buffer
+    static constexpr int kAStageCols = kFp4 ? 32 : kSub * 32;
     // TMEM: 2 accumulator buffers of BN columns (+ ES x kSub A stages of 32 columns)
     static constexpr int kAccCols = BN;
     static constexpr int kAccBufs = BN > 256 ? 1 : 2;  // TMEM accumulator buffers
     static constexpr int kAStageCol = 2 * BN;
     static constexpr int kTmemCols = 512;
-    static constexpr int kSfCol = (BN > 256 ? 1 : 2) * BN;  // fp4: UE8M0 scales (all 1.0) from here
-    static_assert((BN > 256 ? 1 : 2) * BN + (kATmem ? ES * kSub * 32 : 0) + (kFp4 ? 64 : 0) <= 512,
+    static constexpr int kSfCol = (BN > 256 ? 1 : 2) * BN + (kATmem ? ES * kAStageCols : 0);  // fp4: UE8M0 scales (all 1.0) from here
+    // (fp4 scale factors: 64 columns reserved, 32 with A in TMEM -- every byte from kSfCol
+    // on holds the UE8M0 value 1.0, and SFA / SFB of one MMA span a few columns)
+    static_assert((BN > 256 ? 1 : 2) * BN + (kATmem ? ES * kAStageCols : 0) + (kFp4 ? (kATmem ? 32 : 64) : 0) <= 512,
                   "TMEM budget");
     // shared memory carve-up (offsets from the 1024-aligned base)
     // epilogue staging: per warp 32 rows x 32 f32 = 4 KB in the SWIZZLE_128B layout
@@ -478,6 +482,18 @@ __device__ __forceinline__ void mma_fp4(uint32_t tmem_d, uint64_t adesc, uint64_
         "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate), "r"(sfa), "r"(sfb));
 }
 
+// kind::mxf4 with the expanded A operand in TMEM (32 columns per 128-byte K row)
+template <uint32_t kIdesc>
+__device__ __forceinline__ void mma_fp4_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                           uint32_t sfa, uint32_t sfb, uint32_t accumulate) {
+    asm volatile(
+        "{\n.reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], [%1], %2, %3, [%5], [%6], p;\n}\n" ::"r"(
+            tmem_d),
+        "r"(tmem_a), "l"(bdesc), "r"(kIdesc), "r"(accumulate), "r"(sfa), "r"(sfb));
+}
+
 // two bit planes -> u8 codes 0..3 (same K permutation as expand8; no scaling:
 // the MMA then accumulates sum(code_a * code_b) directly)
 __device__ __forceinline__ void expand_code2(uint32_t w0, uint32_t w1, uint32_t (&r)[8]) {
@@ -625,7 +641,9 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
         const int ptid = tid - set * C::kProducerWarps * 32;         // thread within the set
         const bool is_a = ptid < BM;
         const bool active = ptid < C::kProducers;  // the last warp may be partly idle
-        const int row = is_a ? ptid : ptid - BM;
+        // A rows written to TMEM belong to the warp's lane quadrant (warp % 4): with two
+        // expander sets the second set's A warps start at a quadrant offset
+        const int row = is_a ? ((kATmem && kFp4) ? (warp & 3) * 32 + lane : ptid) : ptid - BM;
         const uint32_t ring = s_pk + tid * 16 * kPlanes;  // slot-major private ring
         constexpr uint32_t kRingSlot = C::kProducerWarps * 32 * 16 * kPlanes;
         // fetch iterator (runs PD - kSub stages ahead, across tile boundaries)
@@ -790,13 +808,29 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                     const int sb = (int)(gs % ES);
                     if (gs >= ES) mbar_wait(bar_empty + 8 * sb, ((gs / ES) - 1) & 1u);
                     if (lane == 0 && (warp == 0 || warp == C::kProducerWarps - 1)) tr(warp ? 4 : 1, gs);
+                    if constexpr (kFp4 && kATmem) {
+                        if (is_a) {  // e2m1 A row -> this lane's TMEM lane, 32 columns per superstage
+                            const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16) +
+                                                   C::kAStageCol + sb * C::kAStageCols;
+#pragma unroll
+                            for (uint32_t u = 0; u < kSub; ++u) {
+                                uint32_t r8[8];
+#pragma unroll
+                                for (int j = 0; j < 4; j += 2) {
+                                    expand_fp4_a(u < nsub ? wv[u][j] : 0u, *reinterpret_cast<uint32_t(*)[4]>(&r8[0]));
+                                    expand_fp4_a(u < nsub ? wv[u][j + 1] : 0u, *reinterpret_cast<uint32_t(*)[4]>(&r8[4]));
+                                    if (!(dbg & 4)) tmem_st8(taddr + (4 * u + j) * 4, r8);
+                                }
+                            }
+                        }
+                    }
                     if constexpr (kFp4) {
                         // one 128-byte SW128 row per superstage: word q (stage q / 4) -> chunk q
                         const uint32_t row_base = s_exp + sb * C::kSuperBytes +
                                                   (is_a ? row * 128 : C::kFp4A + row * 128);
     #pragma unroll
                         for (uint32_t u = 0; u < kSub; ++u) {
-                            if (u >= nsub || !active) break;
+                            if (u >= nsub || !active || (kATmem && is_a)) break;
     #pragma unroll
                             for (int j = 0; j < 4; ++j) {
                                 const uint32_t w = wv[u][j];
@@ -990,9 +1024,14 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                                                            tmem + C::kSfCol, tmem + C::kSfCol, acc);
                                 continue;
                             }
-                            mma_fp4<C::kIdescFp4>(d, sw128_desc(a_addr + kk * 32),
-                                                  sw128_desc(b_addr + kk * 32), tmem + C::kSfCol,
-                                                  tmem + C::kSfCol, acc);
+                            if constexpr (kATmem)
+                                mma_fp4_ts<C::kIdescFp4>(d, tmem + C::kAStageCol + sb * C::kAStageCols + kk * 8,
+                                                         sw128_desc(b_addr + kk * 32), tmem + C::kSfCol,
+                                                         tmem + C::kSfCol, acc);
+                            else
+                                mma_fp4<C::kIdescFp4>(d, sw128_desc(a_addr + kk * 32),
+                                                      sw128_desc(b_addr + kk * 32), tmem + C::kSfCol,
+                                                      tmem + C::kSfCol, acc);
                             if constexpr (C::kNMma == 2)  // columns [N/2, N): B rows N/2..N-1
                                 mma_fp4<C::kIdescFp4>(d + C::kMmaN, sw128_desc(a_addr + kk * 32),
                                                       sw128_desc(b_addr + C::kMmaN * 128 + kk * 32),
@@ -1703,6 +1742,29 @@ static int launch_fp4(const ALoad &a, const BLoad &b, const Store &st, const Epi
     }
 }
 
+// variant 3: kind::mxf4 with the expanded A operand in TMEM (tcgen05.st) instead of
+// SMEM -- per superstage the SMEM data path then carries only the B operand's
+// expansion and MMA reads (the A side moves to TMEM); N <= 192 (TMEM budget)
+template <int kSets, class ALoad, class BLoad, class Store>
+static int launch_fp4_tm(const ALoad &a, const BLoad &b, const Store &st, const Epilogue &ep,
+                         int64_t M, int64_t N, int64_t kw32, cudaStream_t s) {
+    static const int cands[] = {192, 160, 128, 64};
+    const int64_t sms = sm_count(), tm = ceil_div(M, umma::BM);
+    int best = 192;
+    int64_t best_cost = -1;
+    for (int bn : cands) {
+        const int64_t cost = ceil_div(tm * ceil_div(N, bn), sms) * (bn + 32);
+        if (best_cost < 0 || cost < best_cost) best = bn, best_cost = cost;
+    }
+    using S = Store;
+    switch (best) {
+        case 64: return launch_umma_cfg<64, true, 4, ALoad, BLoad, S, 1, true, kSets>(a, b, st, ep, M, N, kw32, s);
+        case 128: return launch_umma_cfg<128, true, 4, ALoad, BLoad, S, 1, true, kSets>(a, b, st, ep, M, N, kw32, s);
+        case 160: return launch_umma_cfg<160, true, 4, ALoad, BLoad, S, 1, true, kSets>(a, b, st, ep, M, N, kw32, s);
+        default: return launch_umma_cfg<192, true, 4, ALoad, BLoad, S, 1, true, kSets>(a, b, st, ep, M, N, kw32, s);
+    }
+}
+
 template <int kVec, class ALoad, class BLoad, class Store>
 static int launch_umma(const ALoad &a, const BLoad &b, const Store &st, const Epilogue &ep,
                        int64_t M, int64_t N, int64_t kw32, cudaStream_t s) {
@@ -1715,6 +1777,10 @@ static int launch_umma(const ALoad &a, const BLoad &b, const Store &st, const Ep
             return launch_umma_cfg<256, false, kVec>(a, b, st, ep, M, N, kw32, s);
     }
     if constexpr (umma::is_tma<ALoad>::value) {
+        if (umma_variant() == 3) {
+            if (kw32 >= BNN_FP4_SETS_KW32) return launch_fp4_tm<2>(a, b, st, ep, M, N, kw32, s);
+            return launch_fp4_tm<1>(a, b, st, ep, M, N, kw32, s);
+        }
         if (umma_variant() == 2) {
             // long K (>= 24 superstages per tile): two expander sets on alternate
             // superstages; short K: one set and 8 epilogue warps (tiles end often)

@@ -19,7 +19,7 @@ from oracle import oracle as orc
 
 pytestmark = pytest.mark.gpu
 
-ALGOS = ["popc", "bmma", "umma0", "umma1", "umma2"]
+ALGOS = ["popc", "bmma", "umma0", "umma1", "umma2", "umma3"]
 
 
 def A(algo):
@@ -255,7 +255,7 @@ def test_conv_im2col_route_matches_oracle(bnn, case):
     b, c, h, w, f, kh, kw, stride, pad, seed = case
     x, wt = wl.conv_case_inputs(case)
     expect = orc.qconv_packed(x, wt, stride, pad)
-    for algo in ("umma2", "umma1", "umma0", "popc"):
+    for algo in ("umma3", "umma2", "umma1", "umma0", "popc"):
         layer = bnn.QConvolution(c, f, (kh, kw), stride, pad)
         layer.weight = wt
         layer.pack()
@@ -460,7 +460,7 @@ def test_qfullyconnected_2bit_packed_equals_float_path(bnn):
         q.forward(x, bnn.INFER_PACKED)
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3])
 def test_umma_repeat_runs_identical(bnn, variant):
     """Pipeline-race guard: repeated launches of the TMA-fed tcgen05 engine on a
     many-tile shape equal the CUDA-core engine every time (a slot released
@@ -557,7 +557,7 @@ def test_randomized_shapes_umma_routes_equal_popc(bnn):
         x = rng.standard_normal((b_, c, h, w), dtype=np.float32)
         wt = rng.standard_normal((f, c, kh, kw), dtype=np.float32)
         outs = []
-        for algo in ("popc", "umma2", "umma1"):
+        for algo in ("popc", "umma2", "umma1", "umma3"):
             layer = bnn.QConvolution(c, f, (kh, kw), st, pd)
             layer.weight = wt
             layer.pack()

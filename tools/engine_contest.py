@@ -10,7 +10,7 @@ shapes = [(1024, 256, 4096), (256, 25088, 2304), (4096, 4096, 4096), (8192, 8192
           (4096, 4096, 65536)]
 engines = [("popc", "popc", None), ("bmma (b1 mma.sync)", "bmma", None),
            ("tcgen05 i8, SMEM A (v0)", "umma", 0), ("tcgen05 i8, TMEM A (v1)", "umma", 1),
-           ("tcgen05 mxf4 (v2)", "umma", 2)]
+           ("tcgen05 mxf4 (v2)", "umma", 2), ("tcgen05 mxf4, TMEM A (v3)", "umma", 3)]
 
 
 def timed(fn, reps):
