@@ -71,7 +71,7 @@ extern "C" int bnn_umma_trace(uint64_t *buf) {
 }
 
 extern "C" int bnn_set_umma_variant(int v) {
-    if (v < 0 || v > 3) return bnn::set_error(BNN_EINVAL, "umma variant must be 0, 1, 2 or 3");
+    if (v < 0 || v > 4) return bnn::set_error(BNN_EINVAL, "umma variant must be 0 .. 4");
     bnn::g_umma_variant = v;
     return BNN_OK;
 }

@@ -124,6 +124,7 @@ struct ConvRows {
 struct GemmStore {
     static constexpr bool kConv = false;
     static constexpr bool kPack = false;  // fused sign-pack epilogue instantiations
+    static constexpr bool kSwap = false;  // rows = output pixels, columns = filters
     float *C;
     int64_t ldc_m, ldc_n, M, N;
     const float *res = nullptr;
@@ -183,6 +184,7 @@ struct GemmStore {
 struct ConvStore {  // y NCHW [B, F, oh*ow]; m = filter, n = b*ohw + pixel
     static constexpr bool kConv = true;
     static constexpr bool kPack = false;
+    static constexpr bool kSwap = false;
     float *y;
     int64_t F, ohw, npix;
     const float *res = nullptr;
@@ -269,6 +271,35 @@ struct ConvStore {  // y NCHW [B, F, oh*ow]; m = filter, n = b*ohw + pixel
                 if (n + i < npix) put(m, n + i, v[i]);
         }
     }
+};
+
+// Swapped conv orientation (filters <= 64): GEMM rows m = output pixels
+// (b * ohw + p, implicit im2col rows, one TMEM lane each), columns n = filters.
+// Element (m, n) of y NCHW [B, F, ohw] sits at row_off(m) + n * ohw, so for a
+// fixed filter the 32 lanes of a warp store 32 consecutive pixels.  The
+// per-filter epilogue parameters (BN) are per column; the sign-pack word of a
+// pixel is built in its own lane.
+struct ConvStoreT {
+    static constexpr bool kConv = true;
+    static constexpr bool kPack = false;
+    static constexpr bool kSwap = true;
+    float *y;
+    int64_t F, ohw, npix;
+    const float *res = nullptr;
+    int has_map = 0;
+    CUtensorMap omap;
+    __device__ int64_t rows() const { return npix; }
+    __device__ int64_t cols() const { return F; }
+    __device__ int64_t m_stride() const { return 1; }
+    __device__ bool n_contiguous() const { return false; }
+    __device__ bool has_out() const { return y != nullptr; }
+    __device__ int64_t row_off(int64_t m) const {
+        const int64_t b = m / ohw;
+        return b * F * ohw + (m - b * ohw);
+    }
+};
+struct ConvStoreTPk : ConvStoreT {
+    static constexpr bool kPack = true;
 };
 
 // the same stores, instantiating the tcgen05 epilogue's sign-pack output

@@ -1091,10 +1091,12 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
         const bool ncontig = store.n_contiguous();
         const int64_t M = store.rows(), N = store.cols();
         const int64_t ms = store.m_stride();
-        const bool affine = ep.scale || ep.shift;
+        // (swapped conv orientation: the per-filter parameters are per column, applied
+        // after the decode)
+        const bool affine = (ep.scale || ep.shift) && !Store::kSwap;
         const bool dot = ep.domain == BNN_DOT;
         const bool magic = ep.k_logical < (1 << 21);  // int -> f32 via the 2^23 trick
-        const bool plain = (magic || kFp4) && !affine && ep.bn_mean == nullptr;  // straight-line decode
+        const bool plain = (magic || kFp4) && !affine && (ep.bn_mean == nullptr || Store::kSwap);  // straight-line decode
         int it = 0;
 #pragma unroll 1
         for (int tile = t0; tile < tmap.ntiles; tile += tstep, ++it) {
@@ -1103,14 +1105,16 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
             tmap.decode(tile, tm, tn);
             const int64_t mq = (int64_t)tm * C::kTmBM + crank * BM + q * 32, n0 = (int64_t)tn * BN;
             const int64_t m = mq + lane;
-            if (store.res && ncontig && m < M) {
+            if (!Store::kSwap && store.res && ncontig && m < M) {
                 // warm L2 with this tile's residual blocks while the MMAs run: lane r
                 // prefetches row m's 128-byte segment of each of its 32-column chunks
-                for (int c = h; c * 32 < BN; c += C::kEpiWarps / 4) {
-                    const int64_t nc = n0 + c * 32;
-                    if (nc >= N) break;
-                    const float *pr = store.res + store.col_off(nc) + m * ms;
-                    asm volatile("prefetch.global.L2 [%0];\n" ::"l"(pr));
+                if constexpr (!Store::kSwap) {
+                    for (int c = h; c * 32 < BN; c += C::kEpiWarps / 4) {
+                        const int64_t nc = n0 + c * 32;
+                        if (nc >= N) break;
+                        const float *pr = store.res + store.col_off(nc) + m * ms;
+                        asm volatile("prefetch.global.L2 [%0];\n" ::"l"(pr));
+                    }
                 }
             }
             mbar_wait_sleep(bar_tfull + 8 * buf, (uint32_t)(it / C::kAccBufs) & 1u);
@@ -1145,7 +1149,7 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                                     ep.k_logical * ep.a_beta * ep.b_beta;
             const float sc = (mok && ep.scale) ? __ldg(ep.scale + m) : 1.0f;
             const float sh = (mok && ep.shift) ? __ldg(ep.shift + m) : 0.0f;
-            const bool has_bn = ep.bn_mean != nullptr;
+            const bool has_bn = ep.bn_mean != nullptr && !Store::kSwap;
             const float bm = (mok && has_bn) ? __ldg(ep.bn_mean + m) : 0.0f;
             const float bi = (mok && has_bn) ? __ldg(ep.bn_inv + m) : 1.0f;
             const float bg = (mok && has_bn) ? __ldg(ep.bn_gamma + m) : 1.0f;
@@ -1169,9 +1173,13 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                 if (mq >= M || nc >= N) {  // warp-uniform
                     // a quadrant past M inside the last packed word: its 32 bits are 0
                     // (words from ceil(M/64) on are not touched)
-                    if (Store::kPack && ep.pack_out && nc < N && (mq >> 6) < ((M + 63) >> 6) &&
-                        lane < w && nc + lane < N)
+                    if constexpr (Store::kSwap) {  // filters past F inside the last word: 0
+                        if (Store::kPack && m < M && nc >= N && (nc >> 6) < ((N + 63) >> 6))
+                            ep.pack_out[m * ep.pack_ld32 + (nc >> 5)] = 0u;
+                    } else if (Store::kPack && ep.pack_out && nc < N && (mq >> 6) < ((M + 63) >> 6) &&
+                               lane < w && nc + lane < N) {
                         ep.pack_out[(nc + lane) * ep.pack_ld32 + (mq >> 5)] = 0u;
+                    }
                     continue;
                 }
                 float f[32];
@@ -1257,6 +1265,56 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                 }
                 // fused residual add in the row layout when the sign-pack needs the
                 // final values (the staged stores then skip their own residual add)
+                if constexpr (Store::kSwap) {
+                    // rows = pixels (lane m), columns = filters nc + j: per-filter affine /
+                    // BN in the reference op order, then (shortcut,) sign-pack of the
+                    // pixel's 32 filters in-lane, and coalesced NCHW stores (for each
+                    // filter the warp writes 32 consecutive pixels)
+                    const int64_t nvalid = N - nc < w ? N - nc : w;
+                    if (ep.scale || ep.shift || ep.bn_mean) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            const int64_t p = nc + (j < nvalid ? j : 0);
+                            float x = f[j];
+                            if (ep.scale) x = __fmul_rn(x, __ldg(ep.scale + p));
+                            if (ep.shift) x = __fadd_rn(x, __ldg(ep.shift + p));
+                            if (ep.bn_mean)
+                                x = __fadd_rn(__fmul_rn(__ldg(ep.bn_gamma + p),
+                                                        __fmul_rn(__fsub_rn(x, __ldg(ep.bn_mean + p)),
+                                                                  __ldg(ep.bn_inv + p))),
+                                              __ldg(ep.bn_beta + p));
+                            f[j] = x;
+                        }
+                    }
+                    if (mok) {
+                        const int64_t ro = store.row_off(m) + nc * store.ohw;
+                        if (store.res) {  // all 32 loads in flight before any store
+                            float r[32];
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                r[j] = j < nvalid ? __ldg(store.res + ro + j * store.ohw) : 0.0f;
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) f[j] = __fadd_rn(f[j], r[j]);
+                        }
+                        if (!Store::kPack || store.has_out()) {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                if (j < nvalid) store.y[ro + j * store.ohw] = f[j];
+                        }
+                        if constexpr (Store::kPack) {
+                            uint32_t word = 0;
+                            float nf = 0.0f;
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                if (j < nvalid) {
+                                    word |= (f[j] >= 0.0f ? 1u : 0u) << j;
+                                    nf = __fmaf_rn(f[j], 0.0f, nf);
+                                }
+                            ep.pack_out[m * ep.pack_ld32 + (nc >> 5)] = word;
+                            if (ep.pack_flags && nf != 0.0f) atomicOr(ep.pack_flags, 1);
+                        }
+                    }
+                } else {
                 // next layer's QActivation + pack: column j's 32 rows -> one u32 word
                 // (ballot); lane j keeps column j's word.  Rows past M pack as 0 (their
                 // values are not stored); columns past the tile / N hold garbage and
@@ -1457,6 +1515,7 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                             else store.put(m, nc + j, f[j]);
                         }
                 }
+                }
             }
             fence_before();
             __syncwarp();
@@ -1655,7 +1714,11 @@ static int launch_umma_cfg(const ALoad &a_in, const BLoad &b_in, const Store &st
 //      from {128, 160, 176, 192} to minimise (waves x N) on the SMs of this GPU
 //   2: e2m1 expansion, A and B through SMEM (kind::mxf4, 2x the i8 MMA rate and
 //      half the expanded bytes) for TMA-fed operands, tile N from {128 .. 224};
-//      cp.async-fed shapes fall back to variant 1
+//      cp.async-fed shapes fall back to variant 1 (variant 0 for <= 64 filters)
+//   3: kind::mxf4 with the expanded A operand in TMEM (TMA-fed shapes, N tiles <= 192)
+//   4: variant 2, and convs with <= 64 filters always in the swapped orientation
+//      (rows = pixels, 128 x 64 tiles); variant 2 takes it only for convs with a
+//      fused shortcut add, where it beats variant 0
 extern int g_umma_variant;
 static int umma_variant() {
     if (g_umma_variant < 0) {
@@ -1772,7 +1835,8 @@ static int launch_umma(const ALoad &a, const BLoad &b, const Store &st, const Ep
         // variant 0 (128 x 256 tiles, A and B through SMEM) also by default for cp.async-fed
         // shapes with M <= 64 (e.g. ResNet-18 layer1 convs, 64 filters): measured 1.1-1.4x
         // the A-in-TMEM engine there (tools/l1_variants.sh)
-        const bool small_m = umma_variant() == 2 && M <= 64 && !umma::is_tma<ALoad>::value;
+        const bool small_m = (umma_variant() == 2 || umma_variant() == 4) && M <= 64 &&
+                             !umma::is_tma<ALoad>::value;
         if (umma_variant() == 0 || small_m)
             return launch_umma_cfg<256, false, kVec>(a, b, st, ep, M, N, kw32, s);
     }
@@ -1781,7 +1845,7 @@ static int launch_umma(const ALoad &a, const BLoad &b, const Store &st, const Ep
             if (kw32 >= BNN_FP4_SETS_KW32) return launch_fp4_tm<2>(a, b, st, ep, M, N, kw32, s);
             return launch_fp4_tm<1>(a, b, st, ep, M, N, kw32, s);
         }
-        if (umma_variant() == 2) {
+        if (umma_variant() == 2 || umma_variant() == 4) {
             // long K (>= 24 superstages per tile): two expander sets on alternate
             // superstages; short K: one set and 8 epilogue warps (tiles end often)
             // long K and M >= 256: CTA pairs (cta_group::2); long K otherwise: two expander sets
@@ -1858,6 +1922,18 @@ static int launch_bconv2d_umma_t(const uint64_t *x, int64_t B, int64_t C, int64_
         tb.cs32 = (int)cs32, tb.kw = (int)kw, tb.sh = (int)sh, tb.sw = (int)sw, tb.ph = (int)ph;
         tb.pw = (int)pw, tb.oh = (int)oh, tb.ow = (int)ow;
         return launch_umma<4>(ta, tb, st, ep, F, npix, kw32, s);
+    }
+    // <= 64 filters: swapped orientation (rows = pixels, cp.async im2col rows as the A
+    // operand, 128 x 64 tiles with A in TMEM): every TMEM lane and epilogue warp busy
+    // instead of half of them (tools/layer_bench.py)
+    // (measured on ResNet's layer 1: the swapped route wins with a shortcut add --
+    // 333 vs 381 us --, variant 0 without -- 200 vs 242 us; profiles/r01)
+    if (F <= 64 && (umma_variant() == 4 || (umma_variant() == 2 && res != nullptr))) {
+        using ST = typename std::conditional<CS::kPack, ConvStoreTPk, ConvStoreT>::type;
+        ST ts{};
+        ts.y = y, ts.F = F, ts.ohw = oh * ow, ts.npix = npix, ts.res = res;
+        return vec4 ? launch_umma_cfg<64, true, 4, ConvRows, DenseRows, ST>(b, a, ts, ep, npix, F, kw32, s)
+                    : launch_umma_cfg<64, true, 2, ConvRows, DenseRows, ST>(b, a, ts, ep, npix, F, kw32, s);
     }
     return vec4 ? launch_umma<4>(a, b, st, ep, F, npix, kw32, s)
                 : launch_umma<2>(a, b, st, ep, F, npix, kw32, s);

@@ -19,7 +19,7 @@ from oracle import oracle as orc
 
 pytestmark = pytest.mark.gpu
 
-ALGOS = ["popc", "bmma", "umma0", "umma1", "umma2", "umma3"]
+ALGOS = ["popc", "bmma", "umma0", "umma1", "umma2", "umma3", "umma4"]
 
 
 def A(algo):

@@ -64,7 +64,7 @@ CASES = [
 
 
 @pytest.mark.parametrize("case", CASES)
-@pytest.mark.parametrize("variant", [2, 1, 0])
+@pytest.mark.parametrize("variant", [2, 1, 0, 4])
 @pytest.mark.parametrize("with_res", [False, True])
 def test_conv_sign_pack_epilogue(bnn, case, variant, with_res):
     from paper_1705_09864_b200 import _lib
