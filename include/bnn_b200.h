@@ -221,6 +221,22 @@ int bnn_conv_bn_relu_maxpool_f32_tc(const float *x, int64_t B, int64_t C, int64_
                                     const float *mean, const float *inv_std, const float *gamma,
                                     const float *beta, int relu, float *y, bnn_stream_t stream);
 
+/* LeNet's float stem as one kernel: y = maxpool_2x2/2(tanh(conv(x, w) + bias))
+ * (reference Conv2d -> Tanh -> MaxPool2d, layers.py:81-141, 480-540), the same
+ * per-element f32 ops as the unfused sequence; bias may be null.  BNN_EUNSUP
+ * outside F == 64, C*kh*kw <= 320, conv width <= 128, W % 4 == 0. */
+int bnn_conv_tanh_maxpool2_f32_tc(const float *x, int64_t B, int64_t C, int64_t H, int64_t W,
+                                  const float *w, const float *bias, int64_t F, int64_t kh,
+                                  int64_t kw, int64_t sh, int64_t sw, int64_t ph, int64_t pw,
+                                  float *y, bnn_stream_t stream);
+
+/* Max pooling of sign-packed NHWC words: out bit = OR over the k x k / stride
+ * window (no padding) = sign(maxpool(x)) (x >= 0 is monotone: the max is >= 0
+ * iff some element is) -- the pool between a binary layer's packed output and
+ * the next binary layer. in [B, H, W, Cw] u64 -> out [B, OH, OW, Cw]. */
+int bnn_maxpool_packed(const uint64_t *in, int64_t B, int64_t H, int64_t W, int64_t Cw, int k,
+                       int stride, uint64_t *out, bnn_stream_t stream);
+
 /* Words per pixel of the packed NHWC activation layout: ceil(C / 64). */
 int64_t bnn_conv_channel_words(int64_t C);
 

@@ -68,7 +68,9 @@ int launch_conv2d_f32_tc(const float *, int64_t, int64_t, int64_t, int64_t, cons
 int launch_conv_bn_relu_maxpool_tc(const float *, int64_t, int64_t, int64_t, int64_t,
                                    const float *, int64_t, int64_t, int64_t, int64_t, int64_t,
                                    int64_t, int64_t, const float *, const float *, const float *,
-                                   const float *, int, float *, cudaStream_t);
+                                   const float *, int, float *, cudaStream_t, int);
+int launch_maxpool_packed(const uint64_t *, int64_t, int64_t, int64_t, int64_t, int, int,
+                          uint64_t *, cudaStream_t);
 int launch_bconv2d_popc(const uint64_t *, int64_t, int64_t, int64_t, int64_t, const uint64_t *,
                         int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,
                         int64_t, float *, const Epilogue &, cudaStream_t, const float *);
@@ -325,7 +327,30 @@ int bnn_conv_bn_relu_maxpool_f32_tc(const float *x, int64_t B, int64_t C, int64_
                 BNN_EGEOM, "invalid convolution geometry");
     BNN_REQUIRE(x && w && y && mean && inv_std && gamma && beta, BNN_EINVAL, "null pointer");
     return launch_conv_bn_relu_maxpool_tc(x, B, C, H, W, w, F, kh, kw, sh, sw, ph, pw, mean,
-                                          inv_std, gamma, beta, relu, y, as_stream(stream));
+                                          inv_std, gamma, beta, relu, y, as_stream(stream), 0);
+}
+
+int bnn_conv_tanh_maxpool2_f32_tc(const float *x, int64_t B, int64_t C, int64_t H, int64_t W,
+                                  const float *w, const float *bias, int64_t F, int64_t kh,
+                                  int64_t kw, int64_t sh, int64_t sw, int64_t ph, int64_t pw,
+                                  float *y, bnn_stream_t stream) {
+    BNN_REQUIRE(B >= 0 && C >= 1 && H >= 1 && W >= 1 && F >= 1 && kh >= 1 && kw >= 1 &&
+                    sh >= 1 && sw >= 1 && ph >= 0 && pw >= 0 && H + 2 * ph >= kh &&
+                    W + 2 * pw >= kw,
+                BNN_EGEOM, "invalid convolution geometry");
+    BNN_REQUIRE(x && w && y, BNN_EINVAL, "null pointer");
+    return launch_conv_bn_relu_maxpool_tc(x, B, C, H, W, w, F, kh, kw, sh, sw, ph, pw, bias,
+                                          nullptr, nullptr, nullptr, 0, y, as_stream(stream), 1);
+}
+
+int bnn_maxpool_packed(const uint64_t *in, int64_t B, int64_t H, int64_t W, int64_t Cw, int k,
+                       int stride, uint64_t *out, bnn_stream_t stream) {
+    BNN_REQUIRE(B >= 0 && H >= 1 && W >= 1 && Cw >= 1 && k >= 1 && stride >= 1 && H >= k &&
+                    W >= k,
+                BNN_EGEOM, "invalid pooling geometry");
+    BNN_REQUIRE(B == 0 || (in && out), BNN_EINVAL, "null pointer");
+    BNN_REQUIRE(ceil_div(B * H * W * Cw, 256) < (1ll << 31), BNN_EUNSUP, "tensor too large");
+    return launch_maxpool_packed(in, B, H, W, Cw, k, stride, out, as_stream(stream));
 }
 
 int64_t bnn_conv_channel_words(int64_t C) { return C > 0 ? ceil_div(C, 64) : 0; }

@@ -590,7 +590,33 @@ __global__ void bn_relu_maxpool_band_kernel(const float *__restrict__ x, int C, 
     }
 }
 
+// Max pooling of sign-packed NHWC words (no padding): out = OR of the window's
+// words.  sign(max(v)) = OR(sign(v_i)) for the predicate v >= 0, so this equals
+// packing the max-pooled f32 tensor.  One thread per output word.
+__global__ void maxpool_packed_kernel(const uint64_t *__restrict__ in, int64_t H, int64_t W,
+                                      int64_t Cw, int k, int st, int64_t OH, int64_t OW,
+                                      int64_t total, uint64_t *__restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= total) return;
+    const int64_t cw = i % Cw, p = i / Cw;
+    const int64_t ox = p % OW, oy = (p / OW) % OH, b = p / (OW * OH);
+    const uint64_t *src = in + ((b * H + oy * st) * W + ox * st) * Cw + cw;
+    uint64_t v = 0;
+    for (int r = 0; r < k; ++r)
+        for (int c = 0; c < k; ++c) v |= __ldg(src + ((int64_t)r * W + c) * Cw);
+    out[i] = v;
+}
+
 // ================================================================ launchers
+int launch_maxpool_packed(const uint64_t *in, int64_t B, int64_t H, int64_t W, int64_t Cw, int k,
+                          int st, uint64_t *out, cudaStream_t s) {
+    const int64_t OH = (H - k) / st + 1, OW = (W - k) / st + 1;
+    const int64_t total = B * OH * OW * Cw;
+    if (total == 0) return BNN_OK;
+    maxpool_packed_kernel<<<(unsigned)ceil_div(total, 256), 256, 0, s>>>(in, H, W, Cw, k, st, OH,
+                                                                        OW, total, out);
+    return check_launch("maxpool_packed_kernel");
+}
 int launch_binarize(const float *x, int64_t n, float *out, int32_t *flags, cudaStream_t s) {
     if (n == 0) return BNN_OK;
     int blocks = (int)(ceil_div(n, 256) < 148 * 16 ? ceil_div(n, 256) : 148 * 16);

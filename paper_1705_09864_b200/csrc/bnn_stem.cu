@@ -301,6 +301,9 @@ struct PoolGeom {
     int rpitch;     // staged row pitch (floats)
     int xs_floats;  // one staging buffer: C * kh * rpitch
     int pyb, nbands, items;
+    int mode;  // 0: BN + ReLU? + maxpool 3x3/2/1; 1: + bias, tanh, maxpool 2x2/2/0 (LeNet)
+    int R;     // conv rows per tile (mode 1: an even number of narrow rows fills the lanes)
+    int NR;    // staged input rows per channel: (R - 1) * sh + kh
     int dbg;  // debug (BNN_STEM_DEBUG, wrong results): 1 no gather loads, 2 no MMAs,
               // 4 no epilogue work, 8 no loader loads
 };
@@ -393,12 +396,16 @@ __global__ void __launch_bounds__(kPThreads, 1) conv_pool_kernel(const __grid_co
         if (k < g.K) {
             const int taps = g.kh * g.kw, ci = k / taps, r = k - ci * taps;
             const int ky = r / g.kw, kx = r - ky * g.kw;
-            off = (ci * g.kh + ky) * g.rpitch + (g.par ? (kx & 1) * (g.rpitch >> 1) + (kx >> 1) : kx);
+            off = (ci * g.NR + ky) * g.rpitch + (g.par ? (kx & 1) * (g.rpitch >> 1) + (kx >> 1) : kx);
         }
         ktab[k] = off;
     }
     for (int i = tid; i < 2 * g.xs_floats; i += kPThreads) xs[i] = 0.0f;  // zero borders
-    for (int c = tid; c < NF; c += kPThreads) {
+    for (int c = tid; c < NF && g.mode == 1; c += kPThreads) {  // bias, no sign flip
+        bnt[c] = 1.0f;
+        bnt[NF + c] = g.mean ? __ldg(g.mean + c) : 0.0f;
+    }
+    for (int c = tid; c < NF && g.mode == 0; c += kPThreads) {
         const float gm = __ldg(g.gamma + c);
         bnt[c] = gm < 0.0f ? -1.0f : 1.0f;
         bnt[NF + c] = __ldg(g.mean + c);
@@ -435,17 +442,18 @@ __global__ void __launch_bounds__(kPThreads, 1) conv_pool_kernel(const __grid_co
     for (int item = blockIdx.x; item < g.items; item += gridDim.x) {                  \
         const int b = item / g.nbands, band = item - b * g.nbands;                    \
         const int py0 = band * g.pyb, py1 = min(g.PH, py0 + g.pyb);                   \
-        const int oy_s = max(0, 2 * py0 - 1), oy_e = min(g.OH - 1, 2 * py1 - 1);
+        const int oy_s = g.mode ? 2 * py0 : max(0, 2 * py0 - 1), oy_e = min(g.OH - 1, 2 * py1 - 1);
 #define POOL_ITEMS_END }
 
     if (warp < kProdWarps) {
         // ------------------------------------------------------------ gather
         const int grp = warp >> 2, q = warp & 3, ox = q * 32 + lane;
         const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16) + kAStage0;
-        const int pb = ox < g.OW ? (g.par ? ox : ox * g.sw) : 0;
+        const int prow = ox / g.OW, pcol = ox - prow * g.OW;  // conv row within the tile
+        const int pb = prow < g.R ? prow * g.sh * g.rpitch + (g.par ? pcol : pcol * g.sw) : 0;
         int gch = 0, it = 0;
         POOL_ITEMS_BEGIN
-        for (int oy = oy_s; oy <= oy_e; ++oy, ++it) {
+        for (int oy = oy_s; oy <= oy_e; oy += g.R, ++it) {
             const int xb = it & 1;
             mbar_wait(bar_xfull + 8 * xb, (it >> 1) & 1);
             const float *src = xs + xb * g.xs_floats + pb;
@@ -508,14 +516,14 @@ __global__ void __launch_bounds__(kPThreads, 1) conv_pool_kernel(const __grid_co
         int it = 0;
         POOL_ITEMS_BEGIN
         const float *xb0 = g.x + (int64_t)b * g.C * g.H * g.W;
-        for (int oy = oy_s; oy <= oy_e; ++oy, ++it) {
+        for (int oy = oy_s; oy <= oy_e; oy += g.R, ++it) {
             const int xb = it & 1;
             mbar_wait(bar_xempty + 8 * xb, ((it >> 1) & 1) ^ 1);
             float *dst = xs + xb * g.xs_floats;
             const int iy0 = oy * g.sh - g.ph;
             // thread = (row parity rg, float4 column j): rows rg, rg + 2, ... of the
             // C x kh staged rows; all loads of a row group in flight before the stores
-            const int rows = g.C * g.kh;
+            const int rows = g.C * g.NR;
             for (int j = jcol; j < w4; j += 64) {
                 float4 v[kPLoadBatch];
 #pragma unroll
@@ -523,7 +531,7 @@ __global__ void __launch_bounds__(kPThreads, 1) conv_pool_kernel(const __grid_co
                     const int r = rg + 2 * u;
                     v[u] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
                     if (r < rows && !(g.dbg & 8)) {
-                        const int ci = r / g.kh, iy = iy0 + (r - ci * g.kh);
+                        const int ci = r / g.NR, iy = iy0 + (r - ci * g.NR);
                         if ((unsigned)iy < (unsigned)g.H)
                             v[u] = __ldg(reinterpret_cast<const float4 *>(
                                              xb0 + ((int64_t)ci * g.H + iy) * g.W) + j);
@@ -548,7 +556,7 @@ __global__ void __launch_bounds__(kPThreads, 1) conv_pool_kernel(const __grid_co
         if (lane == 0) {
             int gch = 0, it = 0;
             POOL_ITEMS_BEGIN
-            for (int oy = oy_s; oy <= oy_e; ++oy, ++it) {
+            for (int oy = oy_s; oy <= oy_e; oy += g.R, ++it) {
                 const int buf = it & 1;
                 mbar_wait(bar_tempty + 8 * buf, ((it >> 1) & 1) ^ 1);
                 fence_after();
@@ -597,7 +605,7 @@ __global__ void __launch_bounds__(kPThreads, 1) conv_pool_kernel(const __grid_co
                 yb[((int64_t)c * g.PH + py) * g.PW + px] = v;
             }
         };
-        for (int oy = oy_s; oy <= oy_e; ++oy, ++it) {
+        for (int oy = oy_s; oy <= oy_e; oy += g.R, ++it) {
             const int buf = it & 1;
             mbar_wait_sleep(bar_tfull + 8 * buf, (it >> 1) & 1);
             fence_after();
@@ -606,11 +614,18 @@ __global__ void __launch_bounds__(kPThreads, 1) conv_pool_kernel(const __grid_co
             for (int h = 0; h < 2; ++h) {
                 uint32_t v[32];
                 tmem_ld32(ta + 32 * h, v);
-                if (ox < g.OW) {
+                if (ox < g.R * g.OW) {  // lanes = R conv rows of OW pixels
+                    if (g.mode == 1) {  // conv + bias -> tanh (torch.tanh's tanhf), then the pool
 #pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        rbuf[(32 * h + j) * kRowPitchR + ox] =
-                            __fmul_rn(__uint_as_float(v[j]), bnt[32 * h + j]);
+                        for (int j = 0; j < 32; ++j)
+                            rbuf[(32 * h + j) * kRowPitchR + ox] =
+                                tanhf(__fadd_rn(__uint_as_float(v[j]), bnt[NF + 32 * h + j]));
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            rbuf[(32 * h + j) * kRowPitchR + ox] =
+                                __fmul_rn(__uint_as_float(v[j]), bnt[32 * h + j]);
+                    }
                 }
             }
             fence_before();
@@ -620,7 +635,20 @@ __global__ void __launch_bounds__(kPThreads, 1) conv_pool_kernel(const __grid_co
             // horizontal 3-max (window 2px-1 .. 2px+1, clipped) of this conv row, folded
             // into the pooled rows: an odd conv row completes pooled row (oy - 1) / 2
             // and starts (oy + 1) / 2, an even one is the middle row of oy / 2
-            if (px < g.PW && !(g.dbg & 4)) {
+            if (g.mode == 1 && px < g.PW && !(g.dbg & 4)) {
+                // 2x2/2 pool inside the tile: conv rows (2r, 2r + 1) -> pooled row oy / 2 + r
+                for (int r = 0; 2 * r + 1 < g.R && oy + 2 * r + 1 <= oy_e; ++r) {
+                    float *yrow = yb + (int64_t)((oy >> 1) + r) * g.PW + px;
+                    const int o0 = 2 * r * g.OW + 2 * px, o1 = o0 + g.OW;
+#pragma unroll 8
+                    for (int i = 0; i < 32; ++i) {
+                        const int c = c0 + 2 * i;
+                        const float *rr = rbuf + c * kRowPitchR;
+                        yrow[(int64_t)c * g.PH * g.PW] =
+                            fmaxf(fmaxf(rr[o0], rr[o0 + 1]), fmaxf(rr[o1], rr[o1 + 1]));
+                    }
+                }
+            } else if (px < g.PW && !(g.dbg & 4)) {
                 const int xl = 2 * px - 1, xr = 2 * px + 1;
                 const bool odd = oy & 1, done = odd && ((oy - 1) >> 1) >= py0;
                 float *yrow = yb + (int64_t)((oy - 1) >> 1) * g.PW + px;
@@ -644,7 +672,7 @@ __global__ void __launch_bounds__(kPThreads, 1) conv_pool_kernel(const __grid_co
             }
             epi_bar();  // the row buffer is free for the next conv row
         }
-        if (!(oy_e & 1) && (oy_e >> 1) < py1) emit(oy_e >> 1);  // last pooled row without a row below
+        if (g.mode == 0 && !(oy_e & 1) && (oy_e >> 1) < py1) emit(oy_e >> 1);  // last pooled row without a row below
         POOL_ITEMS_END
     }
 #undef POOL_ITEMS_BEGIN
@@ -697,11 +725,12 @@ int launch_conv_bn_relu_maxpool_tc(const float *x, int64_t B, int64_t C, int64_t
                                    const float *w, int64_t F, int64_t kh, int64_t kw, int64_t sh,
                                    int64_t sw, int64_t ph, int64_t pw, const float *mean,
                                    const float *inv, const float *gamma, const float *beta,
-                                   int relu, float *y, cudaStream_t s) {
+                                   int relu, float *y, cudaStream_t s, int mode) {
     using namespace stem;
     const int64_t K = C * kh * kw;
     const int64_t OH = (H + 2 * ph - kh) / sh + 1, OW = (W + 2 * pw - kw) / sw + 1;
-    const int64_t PH = (OH + 2 - 3) / 2 + 1, PW = (OW + 2 - 3) / 2 + 1;
+    const int64_t PH = mode ? OH / 2 : (OH + 2 - 3) / 2 + 1, PW = mode ? OW / 2 : (OW + 2 - 3) / 2 + 1;
+    if (mode && (PH < 1 || PW < 1)) return set_error(BNN_EUNSUP, "fused stem: pool does not fit");
     if (F != NF || K > kMaxChunks * KC || OW > stem::BM || OW < 2 || OH < 2 || W % 4 != 0 ||
         (reinterpret_cast<uintptr_t>(x) & 15) || PW > 64 || C * H * W >= (1ll << 31) ||
         C * kh > 2 * kPLoadBatch || W / 4 > 64 * 8)
@@ -709,6 +738,7 @@ int launch_conv_bn_relu_maxpool_tc(const float *x, int64_t B, int64_t C, int64_t
     PoolGeom g{};
     g.x = x, g.w = w, g.mean = mean, g.inv = inv, g.gamma = gamma, g.beta = beta, g.y = y;
     g.relu = relu;
+    g.mode = mode;
     {
         const char *e = getenv("BNN_STEM_DEBUG");
         g.dbg = e ? atoi(e) : 0;
@@ -717,13 +747,17 @@ int launch_conv_bn_relu_maxpool_tc(const float *x, int64_t B, int64_t C, int64_t
     g.sw = (int)sw, g.ph = (int)ph, g.pw = (int)pw, g.OH = (int)OH, g.OW = (int)OW;
     g.PH = (int)PH, g.PW = (int)PW, g.K = (int)K, g.nch = (int)ceil_div(K, KC);
     g.par = sw == 2;
+    g.R = mode ? (int)((stem::BM / OW) & ~1ll) : 1;
+    if (g.R < 1) return set_error(BNN_EUNSUP, "fused stem: conv width");
+    g.NR = (int)((g.R - 1) * sh + kh);
+    if (C * g.NR > 2 * kPLoadBatch) return set_error(BNN_EUNSUP, "fused stem: staged rows");
     const int64_t ws = (OW - 1) * sw + kw;  // staged columns per row (incl. padding)
     int64_t pitch = g.par ? 2 * ceil_div(ws, 2) : ws;
     pitch = ceil_div(pitch, 4) * 4 + (g.par ? 2 : 1);  // spread rows over banks
     if (g.par && (pitch & 1)) pitch += 1;
     if (pw + W > ws + 0 && pw + W > pitch) return set_error(BNN_EUNSUP, "fused stem: row pitch");
     g.rpitch = (int)pitch;
-    g.xs_floats = (int)(C * kh * pitch);
+    g.xs_floats = (int)(C * g.NR * pitch);
     // pooled-row bands: about 4 items per SM-wave unit of work, 14 rows for ResNet
     int64_t pyb = PH >= 14 ? 14 : PH;
     g.pyb = (int)pyb;
@@ -737,7 +771,7 @@ int launch_conv_bn_relu_maxpool_tc(const float *x, int64_t B, int64_t C, int64_t
     if (C == 3 && kh == 7 && kw == 7 && g.par && pitch <= 234) {  // ResNet stem: static offsets
         using G = GeoStride2<3, 7, 7, 234>;
         g.rpitch = 234;
-        g.xs_floats = (int)(C * kh * 234);
+        g.xs_floats = (int)(C * g.NR * 234);
         const PoolSmem L2(g.nch, g.xs_floats);
         static bool configured = false;
         if (!configured) {

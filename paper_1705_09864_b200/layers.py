@@ -424,6 +424,38 @@ class QDense(_QLayer):
         self._finish(flags)
         return out
 
+    def device_words_hwc(self, chw) -> torch.Tensor:
+        """Packed weights with K re-ordered from the reference's NCHW flatten order
+        (c, h, w) (layers.py:459) to (h, w, c): the order of pooled packed NHWC words.
+        Load-time permutation, cached; popcounts are permutation invariant."""
+        self._require_packed()
+        cache = self.__dict__.setdefault("_hwc_cache", {})
+        key = tuple(chw)
+        if key not in cache:
+            c, h, w = key
+            if c * h * w != self.in_features or c % 64:
+                raise ValueError("(h, w, c) re-order needs whole 64-channel words")
+            words = self.packed.words.cpu().numpy().view(np.uint8)
+            bits = np.unpackbits(words, axis=1, bitorder="little")[:, :self.in_features]
+            bits = bits.reshape(self.units, c, h, w).transpose(0, 2, 3, 1).reshape(self.units, -1)
+            packed = np.packbits(bits, axis=1, bitorder="little").view(np.uint64)
+            cache[key] = torch.from_numpy(np.ascontiguousarray(packed)).cuda()
+        return cache[key]
+
+    def forward_packed_hwc(self, x_words: torch.Tensor, chw, bn=None) -> torch.Tensor:
+        """[B, in_features / 64] packed activation rows in (h, w, c) order (pooled packed
+        NHWC words) -> f32 [B, units] with the fused BatchNorm epilogue."""
+        import ctypes
+        a = self.device_words_hwc(chw)
+        n = x_words.shape[0]
+        out = torch.empty((n, self.units), dtype=torch.float32, device="cuda")
+        e = make_epilogue(self.domain, bn)
+        algo = _lib.ALGOS[self.algo] if isinstance(self.algo, str) else self.algo
+        _lib.call("bnn_xnor_gemm_ex", _lib.ptr(a), a.stride(0), _lib.ptr(x_words),
+                  x_words.stride(0), self.units, n, self.in_features, 0, 0, _lib.ptr(out), 1,
+                  out.stride(0), ctypes.byref(e), algo, _lib.stream_ptr())
+        return out
+
     def forward_packed_rows(self, x_words: torch.Tensor, out=None, scale=None, shift=None):
         """[B, W] packed activations (tail 0) -> f32 [B, units] (no host sync)."""
         self._require_packed()

@@ -224,6 +224,20 @@ class Sequential:
             nxt = self.layers[i + 1] if i + 1 < n else None
             if isinstance(x, PackedNHWC) and not isinstance(layer, BinaryBasicBlock):
                 x = x.float()  # a float consumer of a packed activation
+            if mode == INFER_PACKED and self.fuse_stem and _lenet_stem(self.layers[i:i + 3]):
+                x = _lenet_stem_forward(self.layers[i], x)  # conv + tanh + maxpool, one kernel
+                if capture is not None:
+                    capture += [None, None, x]
+                i += 3
+                continue
+            if mode == INFER_PACKED and self.fuse_bn and _binary_pool_fc(self.layers[i:i + 6]):
+                # QConv -> BN -> maxpool -> flatten -> QFC -> BN with 1-bit activations
+                # between the two binary layers (sign-pack epilogue, packed OR-pool)
+                x = _binary_pool_fc_forward(self.layers[i:i + 6], x)
+                if capture is not None:
+                    capture += [None] * 5 + [x]
+                i += 6
+                continue
             if (mode == INFER_PACKED and self.fuse_stem and isinstance(layer, Conv2d)
                     and isinstance(nxt, StemPost) and nxt.fusable(layer)):
                 x = nxt.forward_fused_conv(layer, x)  # conv + BN + ReLU + maxpool, one kernel
@@ -258,6 +272,61 @@ class Sequential:
     def pack_for_inference(self):
         for l in self.binary_layers():
             l.pack()
+
+
+def _lenet_stem(ls) -> bool:
+    """Conv2d (tensor-core engine) -> Tanh -> MaxPool2d(2, 2, 0)."""
+    return (len(ls) == 3 and isinstance(ls[0], Conv2d) and isinstance(ls[1], Tanh) and
+            isinstance(ls[2], MaxPool2d) and (ls[2].k, ls[2].stride, ls[2].pad) == (2, 2, 0) and
+            ls[0].engine == "tc" and ls[0].tc_supported())
+
+
+def _lenet_stem_forward(conv: "Conv2d", x: torch.Tensor) -> torch.Tensor:
+    """maxpool2x2(tanh(conv(x) + b)) in one kernel (bnn_conv_tanh_maxpool2_f32_tc): the
+    same per-element f32 ops as the three torch calls, the conv output never written."""
+    x = x.contiguous()
+    b, c, h, w = x.shape
+    oh = (h + 2 * conv.pad - conv.k) // conv.stride + 1
+    ow = (w + 2 * conv.pad - conv.k) // conv.stride + 1
+    y = torch.empty((b, conv.cout, oh // 2, ow // 2), dtype=torch.float32, device=x.device)
+    st = _lib.call_status("bnn_conv_tanh_maxpool2_f32_tc", _lib.ptr(x), b, c, h, w,
+                          _lib.ptr(conv._dev("weight")), _lib.ptr(conv._dev("bias")), conv.cout,
+                          conv.k, conv.k, conv.stride, conv.stride, conv.pad, conv.pad,
+                          _lib.ptr(y), _lib.stream_ptr())
+    if st == _lib.EUNSUP:
+        return MaxPool2d(2).forward(torch.tanh(conv.forward(x)))
+    _lib.check(st, "bnn_conv_tanh_maxpool2_f32_tc")
+    return y
+
+
+def _binary_pool_fc(ls) -> bool:
+    """QConvolution -> BatchNorm -> MaxPool2d(k, k, 0) -> Flatten -> QFullyConnected ->
+    BatchNorm, 1-bit, the conv's filters a multiple of 64 (whole channel words)."""
+    return (len(ls) == 6 and isinstance(ls[0], QConvolution) and isinstance(ls[1], BatchNorm) and
+            isinstance(ls[2], MaxPool2d) and ls[2].pad == 0 and ls[2].stride == ls[2].k and
+            isinstance(ls[3], Flatten) and isinstance(ls[4], QFullyConnected) and
+            isinstance(ls[5], BatchNorm) and ls[0].bits == 1 and ls[4].bits == 1 and
+            ls[0].filters % 64 == 0)
+
+
+def _binary_pool_fc_forward(ls, x) -> torch.Tensor:
+    """sign(maxpool(BN(conv))) == OR-pool of sign(BN(conv)): the conv epilogue writes only
+    the packed sign words, bnn_maxpool_packed ORs the windows, and the FC reads the pooled
+    NHWC words as its K-contiguous rows -- its weights permuted once from the reference's
+    (c, h, w) flatten order (layers.py:459) to (h, w, c) (popcounts are permutation
+    invariant, the outputs are unchanged)."""
+    conv, bn1, pool, _, fc, bn2 = ls
+    t = x.contiguous() if not isinstance(x, PackedNHWC) else x
+    h = conv.forward_fused(t, bn1, pack_out=True, f32_out=False)
+    b, c, hh, ww = h.shape
+    oh, ow = (hh - pool.k) // pool.k + 1, (ww - pool.k) // pool.k + 1
+    cw = h.words.shape[-1]
+    pooled = torch.empty((b, oh, ow, cw), dtype=torch.uint64, device="cuda")
+    _lib.call("bnn_maxpool_packed", _lib.ptr(h.words), b, hh, ww, cw, pool.k, pool.k,
+              _lib.ptr(pooled), _lib.stream_ptr())
+    if fc.in_features != c * oh * ow:
+        raise ValueError(f"expected {fc.in_features} features, got {c * oh * ow}")
+    return fc.forward_packed_hwc(pooled.view(b, oh * ow * cw), (c, oh, ow), bn2)
 
 
 class BinaryBasicBlock:

@@ -194,3 +194,13 @@ def test_sign_pack_and_stem_validation(lib):
     assert lib.bnn_conv_bn_relu_maxpool_f32_tc(*args) == -7
     args[4], args[13] = 16, None
     assert lib.bnn_conv_bn_relu_maxpool_f32_tc(*args) == -1
+
+
+def test_lenet_stem_and_packed_pool_validation(lib):
+    assert lib.bnn_maxpool_packed(16, 1, 1, 4, 1, 2, 2, 16, None) == -6  # window taller than H
+    assert lib.bnn_maxpool_packed(16, 1, 4, 4, 1, 2, 0, 16, None) == -6  # stride 0
+    assert lib.bnn_maxpool_packed(None, 1, 4, 4, 1, 2, 2, 16, None) == -1
+    args = [16, 1, 1, 28, 28, 16, None, 64, 5, 5, 1, 1, 2, 2, 16, None]
+    assert lib.bnn_conv_tanh_maxpool2_f32_tc(*args[:5], None, *args[6:]) == -1
+    args[7] = 32  # F != 64
+    assert lib.bnn_conv_tanh_maxpool2_f32_tc(*args) == -7

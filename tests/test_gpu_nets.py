@@ -192,3 +192,48 @@ def test_fused_stem_conv_pool_bit_identical(nets, shape):
     conv_out = conv.forward(x)
     assert torch.equal(fused, post.forward(conv_out, bnn.INFER_PACKED))
     assert torch.equal(fused, post.forward(conv_out, bnn.INFER_FLOAT))
+
+
+def test_lenet_fused_stem_bit_identical(nets):
+    """bnn_conv_tanh_maxpool2_f32_tc == tensor-core conv -> torch.tanh -> max_pool2d."""
+    import torch.nn.functional as F
+    rng = np.random.default_rng(21)
+    conv = nets.Conv2d(1, 64, 5, pad=2, rng=rng)
+    conv.bias = rng.standard_normal(64).astype(np.float32) * 0.1
+    x = torch.rand((5, 1, 28, 28), generator=torch.Generator().manual_seed(1)).cuda()
+    fused = nets._lenet_stem_forward(conv, x)
+    ref = F.max_pool2d(torch.tanh(conv.forward(x)), 2)
+    assert fused.shape == ref.shape and torch.equal(fused, ref)
+
+
+@pytest.mark.parametrize("shape,k", [((3, 14, 14, 1), 2), ((2, 9, 7, 3), 3), ((1, 6, 10, 2), 2)])
+def test_maxpool_packed_is_pack_of_maxpool(nets, shape, k):
+    """OR-pooling sign-packed words == packing the max-pooled floats (sign(-0) = +1)."""
+    import paper_1705_09864_b200 as bnn
+    import torch.nn.functional as F
+    from paper_1705_09864_b200 import _lib
+    b, h, w, cw = shape
+    c = 64 * cw
+    x = torch.randn((b, c, h, w), generator=torch.Generator().manual_seed(h * w)).cuda()
+    x.view(-1)[::7] = 0.0
+    x.view(-1)[3::11] = -0.0
+    words = bnn.pack_nchw(x)
+    oh, ow = (h - k) // k + 1, (w - k) // k + 1
+    out = torch.empty((b, oh, ow, cw), dtype=torch.uint64, device="cuda")
+    _lib.call("bnn_maxpool_packed", _lib.ptr(words), b, h, w, cw, k, k, _lib.ptr(out),
+              _lib.stream_ptr())
+    expect = bnn.pack_nchw(F.max_pool2d(x, k)).cpu().numpy()
+    assert np.array_equal(out.cpu().numpy(), expect)
+
+
+def test_lenet_packed_tail_equals_float_path(nets):
+    """QConv -> BN -> maxpool -> flatten -> QFC -> BN with 1-bit activations between the
+    binary layers == the same layers on f32 tensors (infer_float), bit for bit."""
+    import paper_1705_09864_b200 as bnn
+    net = nets.lenet_c3(seed=8)
+    net.pack_for_inference()
+    tail = nets.Sequential(net.layers[3:9])
+    assert nets._binary_pool_fc(tail.layers)
+    x = torch.randn((6, 64, 14, 14), generator=torch.Generator().manual_seed(5)).cuda()
+    x.view(-1)[::13] = 0.0
+    assert torch.equal(tail.forward(x, bnn.INFER_PACKED), tail.forward(x, bnn.INFER_FLOAT))
