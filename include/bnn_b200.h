@@ -230,6 +230,15 @@ int bnn_conv_tanh_maxpool2_f32_tc(const float *x, int64_t B, int64_t C, int64_t 
                                   int64_t kw, int64_t sh, int64_t sw, int64_t ph, int64_t pw,
                                   float *y, bnn_stream_t stream);
 
+/* Adds to *violations_dev (device u64) the number of adjacent finite floats
+ * a < b with tanhf(a) > tanhf(b) (exhaustive, ~4e9 evaluations).  0 means the
+ * f32 tanh is monotone, which makes pooling before the tanh exact. */
+int bnn_probe_tanh_monotone(unsigned long long *violations_dev, bnn_stream_t stream);
+
+/* Let bnn_conv_tanh_maxpool2_f32_tc pool before the tanh (exact iff
+ * bnn_probe_tanh_monotone reported 0 violations on this device). */
+int bnn_set_tanh_pool_first(int on);
+
 /* Max pooling of sign-packed NHWC words: out bit = OR over the k x k / stride
  * window (no padding) = sign(maxpool(x)) (x >= 0 is monotone: the max is >= 0
  * iff some element is) -- the pool between a binary layer's packed output and

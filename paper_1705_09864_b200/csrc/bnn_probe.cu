@@ -169,3 +169,25 @@ extern "C" int bnn_debug_stamp(uint64_t *dst, bnn_stream_t stream) {
     stamp_kernel<<<1, 1, 0, as_stream(stream)>>>(dst);
     return check_launch("stamp_kernel");
 }
+
+// Exhaustive monotonicity check of tanhf (the CUDA math library's, which
+// torch.tanh uses for f32): count adjacent finite floats a < b with
+// tanhf(a) > tanhf(b).  Zero violations make maxpool(tanh(x)) == tanh(maxpool(x))
+// exact, so the fused LeNet stem can pool before the tanh (4x fewer tanh).
+static __global__ void tanh_monotone_kernel(unsigned long long *violations) {
+    unsigned long long bad = 0;
+    const uint32_t n = 0x7F800000u;  // positive finite magnitudes: [0, +inf)
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += gridDim.x * blockDim.x) {
+        const float a = __uint_as_float(i), b = __uint_as_float(i + 1);
+        if (tanhf(a) > tanhf(b)) ++bad;  // (b may be +inf: tanhf(inf) = 1)
+        if (tanhf(-b) > tanhf(-a)) ++bad;
+    }
+    if (bad) atomicAdd(violations, bad);
+}
+
+extern "C" int bnn_probe_tanh_monotone(unsigned long long *violations_dev, bnn_stream_t stream) {
+    if (!violations_dev) return bnn::set_error(BNN_EINVAL, "null pointer");
+    tanh_monotone_kernel<<<148 * 8, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(violations_dev);
+    return bnn::check_launch("tanh_monotone_kernel");
+}

@@ -287,6 +287,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tf32x3_kernel(const __grid_c
 namespace stem {
 
 constexpr int kPLoadWarp0 = 8, kPLoadWarps = 4, kPMmaWarp = 12, kPEpiWarp0 = 13;
+constexpr int kPX = 4;    // staged input buffers (tiles in flight between loader and gather)
+constexpr int kPAcc = 3;  // TMEM accumulator buffers (tiles in flight between MMA and epilogue)
+constexpr int kPS = 5;    // TMEM A stages (chunks)
+constexpr int kPAStage0 = kPAcc * NF;
+static_assert(kPAStage0 + kPS * 2 * KC <= 512, "TMEM budget (fused stem)");
 constexpr int kPLoadBatch = 12;  // float4 loads in flight per loader thread (C*kh <= 24 rows)
 constexpr int kPThreads = (kPEpiWarp0 + kEpiWarps) * 32;
 constexpr int kRowPitchR = 132;  // epilogue row buffer pitch (floats)
@@ -303,6 +308,7 @@ struct PoolGeom {
     int pyb, nbands, items;
     int mode;  // 0: BN + ReLU? + maxpool 3x3/2/1; 1: + bias, tanh, maxpool 2x2/2/0 (LeNet)
     int R;     // conv rows per tile (mode 1: an even number of narrow rows fills the lanes)
+    int pool_first;  // mode 1: tanhf is monotone (probed): max-pool, then one tanh per output
     int NR;    // staged input rows per channel: (R - 1) * sh + kh
     int dbg;  // debug (BNN_STEM_DEBUG, wrong results): 1 no gather loads, 2 no MMAs,
               // 4 no epilogue work, 8 no loader loads
@@ -315,10 +321,10 @@ struct PoolSmem {
         off_blo = nch * NF * 128;
         off_ktab = 2 * nch * NF * 128;
         off_xs = off_ktab + nch * KC * 4;
-        off_r = off_xs + 2 * xs_floats * 4;
+        off_r = off_xs + kPX * xs_floats * 4;
         off_bn = off_r + NF * kRowPitchR * 4;
         off_bars = off_bn + 5 * NF * 4;
-        off_tmem = off_bars + (2 * S + 8) * 8;
+        off_tmem = off_bars + (2 * kPS + 2 * kPAcc + 2 * kPX) * 8;
         bytes = off_tmem + 16 + 1024;
     }
 };
@@ -371,9 +377,9 @@ __global__ void __launch_bounds__(kPThreads, 1) conv_pool_kernel(const __grid_co
     float *xs = reinterpret_cast<float *>(smem + L.off_xs);
     float *rbuf = reinterpret_cast<float *>(smem + L.off_r);
     float *bnt = reinterpret_cast<float *>(smem + L.off_bn);  // sign, mean, inv, gamma, beta
-    const uint32_t bar_full = base + L.off_bars, bar_empty = bar_full + 8 * S;
-    const uint32_t bar_tfull = bar_empty + 8 * S, bar_tempty = bar_tfull + 16;
-    const uint32_t bar_xfull = bar_tempty + 16, bar_xempty = bar_xfull + 16;
+    const uint32_t bar_full = base + L.off_bars, bar_empty = bar_full + 8 * kPS;
+    const uint32_t bar_tfull = bar_empty + 8 * kPS, bar_tempty = bar_tfull + 8 * kPAcc;
+    const uint32_t bar_xfull = bar_tempty + 8 * kPAcc, bar_xempty = bar_xfull + 8 * kPX;
     uint32_t *s_tmem = reinterpret_cast<uint32_t *>(smem + L.off_tmem);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int kpad = g.nch * KC;
@@ -400,7 +406,7 @@ __global__ void __launch_bounds__(kPThreads, 1) conv_pool_kernel(const __grid_co
         }
         ktab[k] = off;
     }
-    for (int i = tid; i < 2 * g.xs_floats; i += kPThreads) xs[i] = 0.0f;  // zero borders
+    for (int i = tid; i < kPX * g.xs_floats; i += kPThreads) xs[i] = 0.0f;  // zero borders
     for (int c = tid; c < NF && g.mode == 1; c += kPThreads) {  // bias, no sign flip
         bnt[c] = 1.0f;
         bnt[NF + c] = g.mean ? __ldg(g.mean + c) : 0.0f;
@@ -414,13 +420,15 @@ __global__ void __launch_bounds__(kPThreads, 1) conv_pool_kernel(const __grid_co
         bnt[4 * NF + c] = __ldg(g.beta + c);
     }
     if (tid == 0) {
-        for (int s = 0; s < S; ++s) {
+        for (int s = 0; s < kPS; ++s) {
             mbar_init(bar_full + 8 * s, 4);
             mbar_init(bar_empty + 8 * s, 1);
         }
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < kPAcc; ++b) {
             mbar_init(bar_tfull + 8 * b, 1);
             mbar_init(bar_tempty + 8 * b, kEpiWarps);
+        }
+        for (int b = 0; b < kPX; ++b) {
             mbar_init(bar_xfull + 8 * b, kPLoadWarps);
             mbar_init(bar_xempty + 8 * b, kProdWarps);
         }
@@ -448,19 +456,19 @@ __global__ void __launch_bounds__(kPThreads, 1) conv_pool_kernel(const __grid_co
     if (warp < kProdWarps) {
         // ------------------------------------------------------------ gather
         const int grp = warp >> 2, q = warp & 3, ox = q * 32 + lane;
-        const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16) + kAStage0;
+        const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16) + kPAStage0;
         const int prow = ox / g.OW, pcol = ox - prow * g.OW;  // conv row within the tile
         const int pb = prow < g.R ? prow * g.sh * g.rpitch + (g.par ? pcol : pcol * g.sw) : 0;
         int gch = 0, it = 0;
         POOL_ITEMS_BEGIN
         for (int oy = oy_s; oy <= oy_e; oy += g.R, ++it) {
-            const int xb = it & 1;
-            mbar_wait(bar_xfull + 8 * xb, (it >> 1) & 1);
+            const int xb = it % kPX;
+            mbar_wait(bar_xfull + 8 * xb, (it / kPX) & 1);
             const float *src = xs + xb * g.xs_floats + pb;
             for (int c = 0; c < g.nch; ++c, ++gch) {
                 if ((gch & 1) != grp) continue;
-                const int st = gch % S;
-                mbar_wait(bar_empty + 8 * st, ((gch / S) & 1) ^ 1);
+                const int st = gch % kPS;
+                mbar_wait(bar_empty + 8 * st, ((gch / kPS) & 1) ^ 1);
                 fence_after();
                 const uint32_t ta = tq + st * 2 * KC;
                 if (g.dbg & 1) {
@@ -517,8 +525,8 @@ __global__ void __launch_bounds__(kPThreads, 1) conv_pool_kernel(const __grid_co
         POOL_ITEMS_BEGIN
         const float *xb0 = g.x + (int64_t)b * g.C * g.H * g.W;
         for (int oy = oy_s; oy <= oy_e; oy += g.R, ++it) {
-            const int xb = it & 1;
-            mbar_wait(bar_xempty + 8 * xb, ((it >> 1) & 1) ^ 1);
+            const int xb = it % kPX;
+            mbar_wait(bar_xempty + 8 * xb, ((it / kPX) & 1) ^ 1);
             float *dst = xs + xb * g.xs_floats;
             const int iy0 = oy * g.sh - g.ph;
             // thread = (row parity rg, float4 column j): rows rg, rg + 2, ... of the
@@ -557,15 +565,15 @@ __global__ void __launch_bounds__(kPThreads, 1) conv_pool_kernel(const __grid_co
             int gch = 0, it = 0;
             POOL_ITEMS_BEGIN
             for (int oy = oy_s; oy <= oy_e; oy += g.R, ++it) {
-                const int buf = it & 1;
-                mbar_wait(bar_tempty + 8 * buf, ((it >> 1) & 1) ^ 1);
+                const int buf = it % kPAcc;
+                mbar_wait(bar_tempty + 8 * buf, ((it / kPAcc) & 1) ^ 1);
                 fence_after();
                 const uint32_t d = tmem + buf * NF;
                 for (int c = 0; c < g.nch; ++c, ++gch) {
-                    const int st = gch % S;
-                    mbar_wait(bar_full + 8 * st, (gch / S) & 1);
+                    const int st = gch % kPS;
+                    mbar_wait(bar_full + 8 * st, (gch / kPS) & 1);
                     fence_after();
-                    const uint32_t a = tmem + kAStage0 + st * 2 * KC;
+                    const uint32_t a = tmem + kPAStage0 + st * 2 * KC;
                     const int nkk = (g.dbg & 2) ? 0 : min(KC / 8, (g.K - c * KC + 7) / 8);  // skip all-zero K steps
                     for (int kk = 0; kk < nkk; ++kk) {
                         const uint32_t boff = (uint32_t)(c * NF * 128 + kk * 32);
@@ -606,8 +614,8 @@ __global__ void __launch_bounds__(kPThreads, 1) conv_pool_kernel(const __grid_co
             }
         };
         for (int oy = oy_s; oy <= oy_e; oy += g.R, ++it) {
-            const int buf = it & 1;
-            mbar_wait_sleep(bar_tfull + 8 * buf, (it >> 1) & 1);
+            const int buf = it % kPAcc;
+            mbar_wait_sleep(bar_tfull + 8 * buf, (it / kPAcc) & 1);
             fence_after();
             const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + buf * NF;
 #pragma unroll
@@ -617,9 +625,10 @@ __global__ void __launch_bounds__(kPThreads, 1) conv_pool_kernel(const __grid_co
                 if (ox < g.R * g.OW) {  // lanes = R conv rows of OW pixels
                     if (g.mode == 1) {  // conv + bias -> tanh (torch.tanh's tanhf), then the pool
 #pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            rbuf[(32 * h + j) * kRowPitchR + ox] =
-                                tanhf(__fadd_rn(__uint_as_float(v[j]), bnt[NF + 32 * h + j]));
+                        for (int j = 0; j < 32; ++j) {
+                            const float t = __fadd_rn(__uint_as_float(v[j]), bnt[NF + 32 * h + j]);
+                            rbuf[(32 * h + j) * kRowPitchR + ox] = g.pool_first ? t : tanhf(t);
+                        }
                     } else {
 #pragma unroll
                         for (int j = 0; j < 32; ++j)
@@ -644,8 +653,8 @@ __global__ void __launch_bounds__(kPThreads, 1) conv_pool_kernel(const __grid_co
                     for (int i = 0; i < 32; ++i) {
                         const int c = c0 + 2 * i;
                         const float *rr = rbuf + c * kRowPitchR;
-                        yrow[(int64_t)c * g.PH * g.PW] =
-                            fmaxf(fmaxf(rr[o0], rr[o0 + 1]), fmaxf(rr[o1], rr[o1 + 1]));
+                        const float m = fmaxf(fmaxf(rr[o0], rr[o0 + 1]), fmaxf(rr[o1], rr[o1 + 1]));
+                        yrow[(int64_t)c * g.PH * g.PW] = g.pool_first ? tanhf(m) : m;
                     }
                 }
             } else if (px < g.PW && !(g.dbg & 4)) {
@@ -721,6 +730,9 @@ int launch_conv2d_f32_tc(const float *x, int64_t B, int64_t C, int64_t H, int64_
 
 // conv (3xTF32) + BN + ReLU + maxpool 3x3/2/1 fused; BNN_EUNSUP when the shape
 // does not fit (the caller then runs the conv and the post-op separately)
+// set by bnn_set_tanh_pool_first once bnn_probe_tanh_monotone found tanhf monotone
+int g_tanh_pool_first = 0;
+
 int launch_conv_bn_relu_maxpool_tc(const float *x, int64_t B, int64_t C, int64_t H, int64_t W,
                                    const float *w, int64_t F, int64_t kh, int64_t kw, int64_t sh,
                                    int64_t sw, int64_t ph, int64_t pw, const float *mean,
@@ -739,6 +751,7 @@ int launch_conv_bn_relu_maxpool_tc(const float *x, int64_t B, int64_t C, int64_t
     g.x = x, g.w = w, g.mean = mean, g.inv = inv, g.gamma = gamma, g.beta = beta, g.y = y;
     g.relu = relu;
     g.mode = mode;
+    g.pool_first = mode == 1 && g_tanh_pool_first;
     {
         const char *e = getenv("BNN_STEM_DEBUG");
         g.dbg = e ? atoi(e) : 0;
@@ -791,3 +804,8 @@ int launch_conv_bn_relu_maxpool_tc(const float *x, int64_t B, int64_t C, int64_t
 }
 
 }  // namespace bnn
+
+extern "C" int bnn_set_tanh_pool_first(int on) {
+    bnn::g_tanh_pool_first = on ? 1 : 0;
+    return BNN_OK;
+}

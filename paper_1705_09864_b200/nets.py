@@ -281,6 +281,21 @@ def _lenet_stem(ls) -> bool:
             ls[0].engine == "tc" and ls[0].tc_supported())
 
 
+_TANH_MONOTONE = None
+
+
+def tanh_is_monotone() -> bool:
+    """Exhaustive device check (once per process) that the f32 tanh is monotone, which
+    makes maxpool(tanh(v)) == tanh(maxpool(v)) exact (`bnn_set_tanh_pool_first` lets the
+    fused LeNet stem pool first; measured no faster, so it stays off by default)."""
+    global _TANH_MONOTONE
+    if _TANH_MONOTONE is None:
+        v = torch.zeros(1, dtype=torch.int64, device="cuda")
+        _lib.call("bnn_probe_tanh_monotone", _lib.ptr(v), _lib.stream_ptr())
+        _TANH_MONOTONE = int(v.item()) == 0
+    return _TANH_MONOTONE
+
+
 def _lenet_stem_forward(conv: "Conv2d", x: torch.Tensor) -> torch.Tensor:
     """maxpool2x2(tanh(conv(x) + b)) in one kernel (bnn_conv_tanh_maxpool2_f32_tc): the
     same per-element f32 ops as the three torch calls, the conv output never written."""
