@@ -51,6 +51,23 @@ struct Geom {
     int ntiles;
 };
 
+// wait with a short sleep between probes: the gather / loader warps wait often and
+// would otherwise spin on the issue slots the epilogue needs
+__device__ __forceinline__ void mbar_wait_backoff(uint32_t bar, uint32_t phase) {
+    uint32_t done = 0;
+    while (true) {
+        asm volatile(
+            "{\n.reg .pred p;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(bar), "r"(phase)
+            : "memory");
+        if (done) return;
+        __nanosleep(64);
+    }
+}
+
 __device__ __forceinline__ uint32_t tf32_hi(float v) {
     // truncate to 10 mantissa bits: lo = v - hi (exact) has |lo| < 2^-10 |v| and
     // loses only its own bits below TF32 in the MMA (~2^-21 relative)
@@ -463,12 +480,12 @@ __global__ void __launch_bounds__(kPThreads, 1) conv_pool_kernel(const __grid_co
         POOL_ITEMS_BEGIN
         for (int oy = oy_s; oy <= oy_e; oy += g.R, ++it) {
             const int xb = it % kPX;
-            mbar_wait(bar_xfull + 8 * xb, (it / kPX) & 1);
+            mbar_wait_backoff(bar_xfull + 8 * xb, (it / kPX) & 1);
             const float *src = xs + xb * g.xs_floats + pb;
             for (int c = 0; c < g.nch; ++c, ++gch) {
                 if ((gch & 1) != grp) continue;
                 const int st = gch % kPS;
-                mbar_wait(bar_empty + 8 * st, ((gch / kPS) & 1) ^ 1);
+                mbar_wait_backoff(bar_empty + 8 * st, ((gch / kPS) & 1) ^ 1);
                 fence_after();
                 const uint32_t ta = tq + st * 2 * KC;
                 if (g.dbg & 1) {
@@ -518,6 +535,15 @@ __global__ void __launch_bounds__(kPThreads, 1) conv_pool_kernel(const __grid_co
         const int t = tid - kPLoadWarp0 * 32;
         const int half = g.rpitch >> 1;
         const int jcol = t & 63, rg = t >> 6, w4 = g.W >> 2;
+        // this thread's staged rows rg + 2u: channel-plane offset and tap row (no division
+        // in the tile loop)
+        int roff[kPLoadBatch], rky[kPLoadBatch];
+#pragma unroll
+        for (int u = 0; u < kPLoadBatch; ++u) {
+            const int r = rg + 2 * u, ci = r / g.NR;
+            roff[u] = ci * g.H * g.W;
+            rky[u] = r < g.C * g.NR ? r - ci * g.NR : (1 << 28);  // (past the rows: never in range)
+        }
         auto scol = [&](int sc) { return g.par ? (sc & 1) * half + (sc >> 1) : sc; };
         const int sa0 = scol(4 * jcol + g.pw), sa1 = scol(4 * jcol + 1 + g.pw);
         const int sa2 = scol(4 * jcol + 2 + g.pw), sa3 = scol(4 * jcol + 3 + g.pw);
@@ -526,7 +552,7 @@ __global__ void __launch_bounds__(kPThreads, 1) conv_pool_kernel(const __grid_co
         const float *xb0 = g.x + (int64_t)b * g.C * g.H * g.W;
         for (int oy = oy_s; oy <= oy_e; oy += g.R, ++it) {
             const int xb = it % kPX;
-            mbar_wait(bar_xempty + 8 * xb, ((it / kPX) & 1) ^ 1);
+            mbar_wait_backoff(bar_xempty + 8 * xb, ((it / kPX) & 1) ^ 1);
             float *dst = xs + xb * g.xs_floats;
             const int iy0 = oy * g.sh - g.ph;
             // thread = (row parity rg, float4 column j): rows rg, rg + 2, ... of the
@@ -538,12 +564,10 @@ __global__ void __launch_bounds__(kPThreads, 1) conv_pool_kernel(const __grid_co
                 for (int u = 0; u < kPLoadBatch; ++u) {
                     const int r = rg + 2 * u;
                     v[u] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-                    if (r < rows && !(g.dbg & 8)) {
-                        const int ci = r / g.NR, iy = iy0 + (r - ci * g.NR);
-                        if ((unsigned)iy < (unsigned)g.H)
-                            v[u] = __ldg(reinterpret_cast<const float4 *>(
-                                             xb0 + ((int64_t)ci * g.H + iy) * g.W) + j);
-                    }
+                    const int iy = iy0 + rky[u];
+                    if ((unsigned)iy < (unsigned)g.H && !(g.dbg & 8))
+                        v[u] = __ldg(reinterpret_cast<const float4 *>(
+                                         xb0 + roff[u] + (int64_t)iy * g.W) + j);
                 }
                 const int a0 = j == jcol ? sa0 : scol(4 * j + g.pw), a1 = j == jcol ? sa1 : scol(4 * j + 1 + g.pw);
                 const int a2 = j == jcol ? sa2 : scol(4 * j + 2 + g.pw), a3 = j == jcol ? sa3 : scol(4 * j + 3 + g.pw);
