@@ -261,8 +261,9 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
 __device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t phase) {
     uint32_t done = 0;
     uint32_t tries = 0;
+    const bool watch = g_wait_log != nullptr;  // (one global load per wait, not per probe)
     do {
-        if (g_wait_log && ++tries > (1u << 22)) wait_timeout(bar, phase, tries);
+        if (watch && ++tries > (1u << 22)) wait_timeout(bar, phase, tries);
         asm volatile(
             "{\n.reg .pred p;\n"
             "mbarrier.test_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
@@ -328,8 +329,9 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
     // slots from the expanders sharing their scheduler)
     uint32_t done = 0;
     uint32_t tries = 0;
+    const bool watch = g_wait_log != nullptr;  // (one global load per wait, not per probe)
     do {
-        if (g_wait_log && ++tries > (1u << 22)) wait_timeout(bar, phase, tries);
+        if (watch && ++tries > (1u << 22)) wait_timeout(bar, phase, tries);
         asm volatile(
             "{\n.reg .pred p;\n"
             "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
@@ -344,8 +346,9 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
 __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t phase) {
     uint32_t done = 0;
     uint32_t tries = 0;
+    const bool watch = g_wait_log != nullptr;  // (one global load per wait, not per probe)
     do {
-        if (g_wait_log && ++tries > (1u << 22)) wait_timeout(bar, phase, tries);
+        if (watch && ++tries > (1u << 22)) wait_timeout(bar, phase, tries);
         asm volatile(
             "{\n.reg .pred p;\n"
             "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
