@@ -24,4 +24,13 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"xno
 G="python tools/prof_one.py gemm 8192 8192 8192 2"
 timeout 300 $G > gpurun_out/p2.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:"xnor_umma" -s 1 -c 1 -o gpurun_out/prof_gemm8k $G > gpurun_out/ncu2.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"conv_pool_kernel" -s 1 -c 1 -o gpurun_out/prof_stem python tools/stem_bench.py > gpurun_out/ncu3.log 2>&1
+# keep gpurun_out/ under the copy-back limit: raw-page CSVs instead of the reports
+for r in gpurun_out/prof_bench_c2 gpurun_out/prof_gemm8k gpurun_out/prof_stem; do
+  if [ -f $r.ncu-rep ]; then
+    ncu -i $r.ncu-rep --page raw --csv > $r.raw.csv 2>/dev/null
+    ncu -i $r.ncu-rep --page details > $r.details.txt 2>/dev/null
+    rm -f $r.ncu-rep
+  fi
+done
+du -sh gpurun_out
 echo done
