@@ -310,7 +310,10 @@ constexpr int kPS = 5;    // TMEM A stages (chunks)
 constexpr int kPAStage0 = kPAcc * NF;
 static_assert(kPAStage0 + kPS * 2 * KC <= 512, "TMEM budget (fused stem)");
 constexpr int kPLoadBatch = 12;  // float4 loads in flight per loader thread (C*kh <= 24 rows)
-constexpr int kPThreads = (kPEpiWarp0 + kEpiWarps) * 32;
+constexpr int kPEpiW = 8;                  // epilogue warps: 2 per TMEM lane quadrant
+constexpr int kPCG = kPEpiW * 32 / 64;      // channel groups of the pooling phase
+constexpr int kPCPer = NF / kPCG;           // channels per pooling thread
+constexpr int kPThreads = (kPEpiWarp0 + kPEpiW) * 32;
 constexpr int kRowPitchR = 132;  // epilogue row buffer pitch (floats)
 
 struct PoolGeom {
@@ -346,7 +349,7 @@ struct PoolSmem {
     }
 };
 
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;\n" ::"n"(kPEpiW * 32) : "memory"); }
 
 // compile-time stem geometry (gather offsets become immediates); kStatic = false:
 // the runtime table
@@ -443,7 +446,7 @@ __global__ void __launch_bounds__(kPThreads, 1) conv_pool_kernel(const __grid_co
         }
         for (int b = 0; b < kPAcc; ++b) {
             mbar_init(bar_tfull + 8 * b, 1);
-            mbar_init(bar_tempty + 8 * b, kEpiWarps);
+            mbar_init(bar_tempty + 8 * b, kPEpiW);
         }
         for (int b = 0; b < kPX; ++b) {
             mbar_init(bar_xfull + 8 * b, kPLoadWarps);
@@ -616,19 +619,20 @@ __global__ void __launch_bounds__(kPThreads, 1) conv_pool_kernel(const __grid_co
     } else {
         // ------------------------------------------------------------ epilogue
         const int q = warp & 3, et = tid - kPEpiWarp0 * 32;
+        const int hsel = (warp - kPEpiWarp0) >> 2;  // TMEM columns [32 hsel, 32 hsel + 32)
         const int ox = q * 32 + lane;
-        const int px = et & 63, c0 = et >> 6;  // pooled column, channel parity
-        float cur[32];
+        const int px = et & 63, c0 = et >> 6;  // pooled column, channel group (c = c0 + kPCG i)
+        float cur[kPCPer];
         int it = 0;
         POOL_ITEMS_BEGIN
 #pragma unroll
-        for (int i = 0; i < 32; ++i) cur[i] = -INFINITY;
+        for (int i = 0; i < kPCPer; ++i) cur[i] = -INFINITY;
         float *yb = g.y + (int64_t)b * NF * g.PH * g.PW;
         auto emit = [&](int py) {
             if (px >= g.PW) return;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                const int c = c0 + 2 * i;
+            for (int i = 0; i < kPCPer; ++i) {
+                const int c = c0 + kPCG * i;
                 float v = __fmul_rn(cur[i], bnt[c]);
                 v = __fadd_rn(__fmul_rn(bnt[3 * NF + c], __fmul_rn(__fsub_rn(v, bnt[NF + c]),
                                                                     bnt[2 * NF + c])),
@@ -643,7 +647,7 @@ __global__ void __launch_bounds__(kPThreads, 1) conv_pool_kernel(const __grid_co
             fence_after();
             const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + buf * NF;
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
+            for (int h = hsel; h < 2; h += kPEpiW / 4) {
                 uint32_t v[32];
                 tmem_ld32(ta + 32 * h, v);
                 if (ox < g.R * g.OW) {  // lanes = R conv rows of OW pixels
@@ -674,8 +678,8 @@ __global__ void __launch_bounds__(kPThreads, 1) conv_pool_kernel(const __grid_co
                     float *yrow = yb + (int64_t)((oy >> 1) + r) * g.PW + px;
                     const int o0 = 2 * r * g.OW + 2 * px, o1 = o0 + g.OW;
 #pragma unroll 8
-                    for (int i = 0; i < 32; ++i) {
-                        const int c = c0 + 2 * i;
+                    for (int i = 0; i < kPCPer; ++i) {
+                        const int c = c0 + kPCG * i;
                         const float *rr = rbuf + c * kRowPitchR;
                         const float m = fmaxf(fmaxf(rr[o0], rr[o0 + 1]), fmaxf(rr[o1], rr[o1 + 1]));
                         yrow[(int64_t)c * g.PH * g.PW] = g.pool_first ? tanhf(m) : m;
@@ -686,8 +690,8 @@ __global__ void __launch_bounds__(kPThreads, 1) conv_pool_kernel(const __grid_co
                 const bool odd = oy & 1, done = odd && ((oy - 1) >> 1) >= py0;
                 float *yrow = yb + (int64_t)((oy - 1) >> 1) * g.PW + px;
 #pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    const int c = c0 + 2 * i;
+                for (int i = 0; i < kPCPer; ++i) {
+                    const int c = c0 + kPCG * i;
                     const float *rr = rbuf + c * kRowPitchR;
                     float m = rr[2 * px];
                     if (xl >= 0) m = fmaxf(m, rr[xl]);
