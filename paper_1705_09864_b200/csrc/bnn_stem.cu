@@ -310,10 +310,16 @@ constexpr int kPS = 5;    // TMEM A stages (chunks)
 constexpr int kPAStage0 = kPAcc * NF;
 static_assert(kPAStage0 + kPS * 2 * KC <= 512, "TMEM budget (fused stem)");
 constexpr int kPLoadBatch = 12;  // float4 loads in flight per loader thread (C*kh <= 24 rows)
-constexpr int kPEpiW = 8;                  // epilogue warps: 2 per TMEM lane quadrant
-constexpr int kPCG = kPEpiW * 32 / 64;      // channel groups of the pooling phase
-constexpr int kPCPer = NF / kPCG;           // channels per pooling thread
-constexpr int kPThreads = (kPEpiWarp0 + kPEpiW) * 32;
+// epilogue warps kEW (a template parameter): kEW / 4 per TMEM lane quadrant, each
+// with NF / (kEW / 4) accumulator columns; the pooling phase spreads (channel group,
+// pooled column) over the kEW * 32 threads.  8 for the ResNet stem, 16 for LeNet's
+// (tanh per element, measured)
+template <int kEW>
+struct PEpi {
+    static constexpr int kCG = kEW * 32 / 64;         // channel groups of the pooling phase
+    static constexpr int kCPer = NF / kCG;            // channels per pooling thread
+    static constexpr int kThreads = (kPEpiWarp0 + kEW) * 32;
+};
 constexpr int kRowPitchR = 132;  // epilogue row buffer pitch (floats)
 
 struct PoolGeom {
@@ -349,7 +355,8 @@ struct PoolSmem {
     }
 };
 
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;\n" ::"n"(kPEpiW * 32) : "memory"); }
+template <int kEW>
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;\n" ::"n"(kEW * 32) : "memory"); }
 
 // compile-time stem geometry (gather offsets become immediates); kStatic = false:
 // the runtime table
@@ -385,8 +392,10 @@ __device__ __forceinline__ void gather_static(const float *src, uint32_t ta) {
     }
 }
 
-template <class Geo>
-__global__ void __launch_bounds__(kPThreads, 1) conv_pool_kernel(const __grid_constant__ PoolGeom g) {
+template <class Geo, int kEW>
+__global__ void __launch_bounds__(PEpi<kEW>::kThreads, 1) conv_pool_kernel(const __grid_constant__ PoolGeom g) {
+    constexpr int kPEpiW = kEW, kPCG = PEpi<kEW>::kCG, kPCPer = PEpi<kEW>::kCPer;
+    constexpr int kPThreads = PEpi<kEW>::kThreads;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
@@ -647,28 +656,31 @@ __global__ void __launch_bounds__(kPThreads, 1) conv_pool_kernel(const __grid_co
             fence_after();
             const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + buf * NF;
 #pragma unroll
-            for (int h = hsel; h < 2; h += kPEpiW / 4) {
-                uint32_t v[32];
-                tmem_ld32(ta + 32 * h, v);
+            {
+                constexpr int kCols = NF / (kPEpiW / 4);  // TMEM columns per epilogue warp
+                uint32_t v[kCols];
+                const int c0col = hsel * kCols;
+                if constexpr (kCols == 32) tmem_ld32(ta + c0col, *reinterpret_cast<uint32_t(*)[32]>(v));
+                else tmem_ld16(ta + c0col, *reinterpret_cast<uint32_t(*)[16]>(v));
                 if (ox < g.R * g.OW) {  // lanes = R conv rows of OW pixels
                     if (g.mode == 1) {  // conv + bias -> tanh (torch.tanh's tanhf), then the pool
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            const float t = __fadd_rn(__uint_as_float(v[j]), bnt[NF + 32 * h + j]);
-                            rbuf[(32 * h + j) * kRowPitchR + ox] = g.pool_first ? t : tanhf(t);
+                        for (int j = 0; j < kCols; ++j) {
+                            const float t = __fadd_rn(__uint_as_float(v[j]), bnt[NF + c0col + j]);
+                            rbuf[(c0col + j) * kRowPitchR + ox] = g.pool_first ? t : tanhf(t);
                         }
                     } else {
 #pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            rbuf[(32 * h + j) * kRowPitchR + ox] =
-                                __fmul_rn(__uint_as_float(v[j]), bnt[32 * h + j]);
+                        for (int j = 0; j < kCols; ++j)
+                            rbuf[(c0col + j) * kRowPitchR + ox] =
+                                __fmul_rn(__uint_as_float(v[j]), bnt[c0col + j]);
                     }
                 }
             }
             fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(bar_tempty + 8 * buf);
-            epi_bar();
+            epi_bar<kEW>();
             // horizontal 3-max (window 2px-1 .. 2px+1, clipped) of this conv row, folded
             // into the pooled rows: an odd conv row completes pooled row (oy - 1) / 2
             // and starts (oy + 1) / 2, an even one is the middle row of oy / 2
@@ -707,7 +719,7 @@ __global__ void __launch_bounds__(kPThreads, 1) conv_pool_kernel(const __grid_co
                     cur[i] = odd ? m : fmaxf(cur[i], m);
                 }
             }
-            epi_bar();  // the row buffer is free for the next conv row
+            epi_bar<kEW>();  // the row buffer is free for the next conv row
         }
         if (g.mode == 0 && !(oy_e & 1) && (oy_e >> 1) < py1) emit(oy_e >> 1);  // last pooled row without a row below
         POOL_ITEMS_END
@@ -816,17 +828,21 @@ int launch_conv_bn_relu_maxpool_tc(const float *x, int64_t B, int64_t C, int64_t
         const PoolSmem L2(g.nch, g.xs_floats);
         static bool configured = false;
         if (!configured) {
-            cudaFuncSetAttribute(conv_pool_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+            cudaFuncSetAttribute(conv_pool_kernel<G, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
             configured = true;
         }
-        conv_pool_kernel<G><<<grid, kPThreads, L2.bytes, s>>>(g);
+        conv_pool_kernel<G, 8><<<grid, PEpi<8>::kThreads, L2.bytes, s>>>(g);
     } else {
         static bool configured = false;
         if (!configured) {
-            cudaFuncSetAttribute(conv_pool_kernel<GeoDyn>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+            cudaFuncSetAttribute(conv_pool_kernel<GeoDyn, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+            cudaFuncSetAttribute(conv_pool_kernel<GeoDyn, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
             configured = true;
         }
-        conv_pool_kernel<GeoDyn><<<grid, kPThreads, L.bytes, s>>>(g);
+        if (mode == 1)
+            conv_pool_kernel<GeoDyn, 16><<<grid, PEpi<16>::kThreads, L.bytes, s>>>(g);
+        else
+            conv_pool_kernel<GeoDyn, 8><<<grid, PEpi<8>::kThreads, L.bytes, s>>>(g);
     }
     return check_launch("conv_pool_kernel");
 }
