@@ -597,6 +597,7 @@ __global__ void __launch_bounds__(PEpi<kEW>::kThreads, 1) conv_pool_kernel(const
         POOL_ITEMS_END
     } else if (warp == kPMmaWarp) {
         // ------------------------------------------------------------ MMA issue
+        const uint64_t dh0 = sw128_desc(s_bhi), dl0 = sw128_desc(s_blo);
         if (lane == 0) {
             int gch = 0, it = 0;
             POOL_ITEMS_BEGIN
@@ -611,12 +612,15 @@ __global__ void __launch_bounds__(PEpi<kEW>::kThreads, 1) conv_pool_kernel(const
                     fence_after();
                     const uint32_t a = tmem + kPAStage0 + st * 2 * KC;
                     const int nkk = (g.dbg & 2) ? 0 : min(KC / 8, (g.K - c * KC + 7) / 8);  // skip all-zero K steps
-                    for (int kk = 0; kk < nkk; ++kk) {
-                        const uint32_t boff = (uint32_t)(c * NF * 128 + kk * 32);
-                        const uint64_t bh = sw128_desc(s_bhi + boff), bl = sw128_desc(s_blo + boff);
-                        mma_tf32_ts(d, a + kk * 8, bh, (c | kk) != 0);
-                        mma_tf32_ts(d, a + kk * 8, bl, 1u);
-                        mma_tf32_ts(d, a + KC + kk * 8, bh, 1u);
+                    // descriptors by integer adds on the start-address field (16-byte units):
+                    // + 8192 B per chunk, + 32 B per K step
+                    const uint64_t ch = dh0 + (uint64_t)(c * (NF * 128 / 16)), cl = dl0 + (uint64_t)(c * (NF * 128 / 16));
+#pragma unroll
+                    for (int kk = 0; kk < KC / 8; ++kk) {
+                        if (kk >= nkk) break;
+                        mma_tf32_ts(d, a + kk * 8, ch + 2 * kk, (c | kk) != 0);
+                        mma_tf32_ts(d, a + kk * 8, cl + 2 * kk, 1u);
+                        mma_tf32_ts(d, a + KC + kk * 8, ch + 2 * kk, 1u);
                     }
                     umma_commit(bar_empty + 8 * st);
                 }
