@@ -1120,6 +1120,18 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                     }
                 }
             }
+            if constexpr (Store::kSwap) {
+                // swapped orientation: for filter nc + lane the warp's 32 pixels are one
+                // contiguous 128-byte run of the residual (one prefetch per lane)
+                if (store.res && mq < M) {
+                    for (int c = h; c * 32 < BN; c += C::kEpiWarps / 4) {
+                        const int64_t nc = n0 + c * 32;
+                        if (nc + lane >= N) break;
+                        const float *pr = store.res + store.row_off(mq) + (nc + lane) * store.ohw;
+                        asm volatile("prefetch.global.L2 [%0];\n" ::"l"(pr));
+                    }
+                }
+            }
             mbar_wait_sleep(bar_tfull + 8 * buf, (uint32_t)(it / C::kAccBufs) & 1u);
             mbar_wait_sleep(bar_pfull + 8 * buf, (uint32_t)(it / C::kAccBufs) & 1u);
             fence_after();
