@@ -288,6 +288,28 @@ class BitplanePlan(_Plan):
         return self.y
 
 
+def _count_lib_launches(fn) -> int:
+    from . import _lib
+    n = [0]
+    real_call, real_status = _lib.call, _lib.call_status
+    quiet = ("bnn_set_", "bnn_last_error", "bnn_status_string", "bnn_abi_version",
+             "bnn_conv_channel_words", "bnn_device_sm_count")
+
+    def counted(f):
+        def wrap(name, *args):
+            if not name.startswith(quiet):
+                n[0] += 1
+            return f(name, *args)
+        return wrap
+
+    _lib.call, _lib.call_status = counted(real_call), counted(real_status)
+    try:
+        fn()
+    finally:
+        _lib.call, _lib.call_status = real_call, real_status
+    return n[0]
+
+
 class NetPlan(_Plan):
     """Whole-network inference step (LeNet C3 / ResNet-18 C4) on a resident batch.
 
@@ -306,8 +328,10 @@ class NetPlan(_Plan):
             layer.flags = self.flags
         self.x = torch.empty((batch,) + self.chw, dtype=torch.float32, device="cuda")
         self.ops_per_image = binary_ops_per_image(net, self.chw)
-        self.y = net.forward(self.x, self.mode)
-        self.launches_per_step = 2 * len(net.binary_layers())
+        self.y = net.forward(self.x, self.mode)  # (first call: weight re-layouts, probes)
+        # this library's kernel launches per step: every C-ABI compute call of a warm
+        # forward launches one kernel (the float layers' torch kernels are not counted)
+        self.launches_per_step = _count_lib_launches(lambda: net.forward(self.x, self.mode))
 
     @property
     def binary_ops(self) -> int:
