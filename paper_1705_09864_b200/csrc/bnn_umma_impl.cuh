@@ -1748,6 +1748,12 @@ static int choose_bn(int64_t M, int64_t N, bool fp4 = false, bool wide = false) 
     // (small N tiles give small problems enough CTAs: every tile runs the full K loop)
     static const int cands4[] = {224, 208, 192, 176, 160, 128, 96, 64, 32, 16};
     if (fp4) {
+        static int force = -1;  // tuning / debug override of the kind::mxf4 tile N
+        if (force < 0) {
+            const char *e = getenv("BNN_FP4_BN");
+            force = e ? atoi(e) : 0;
+        }
+        if (force > 0) return force;
         const int64_t sms = sm_count(), tm = ceil_div(M, umma::BM);
         int best = 192;
         int64_t best_cost = -1;
