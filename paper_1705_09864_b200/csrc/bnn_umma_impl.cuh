@@ -1753,7 +1753,7 @@ static int choose_bn(int64_t M, int64_t N, bool fp4 = false, bool wide = false) 
             const char *e = getenv("BNN_FP4_BN");
             force = e ? atoi(e) : 0;
         }
-        if (force > 0) return force;
+        if (force > 0 && (force <= 224 || wide)) return force;  // (wide tiles: one expander set)
         const int64_t sms = sm_count(), tm = ceil_div(M, umma::BM);
         int best = 192;
         int64_t best_cost = -1;
@@ -1824,6 +1824,8 @@ static int launch_fp4(const ALoad &a, const BLoad &b, const Store &st, const Epi
         case 208: return launch_umma_cfg<208, false, 4, ALoad, BLoad, S, 1, true, kSets>(a, b, st, ep, M, N, kw32, s);
         default: return launch_umma_cfg<224, false, 4, ALoad, BLoad, S, 1, true, kSets>(a, b, st, ep, M, N, kw32, s);
     }
+    // (wide tiles with two expander sets: not instantiated, take the widest narrow tile)
+    return launch_umma_cfg<224, false, 4, ALoad, BLoad, S, 1, true, kSets>(a, b, st, ep, M, N, kw32, s);
 }
 
 // variant 3: kind::mxf4 with the expanded A operand in TMEM (tcgen05.st) instead of
