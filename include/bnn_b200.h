@@ -246,6 +246,14 @@ int bnn_set_tanh_pool_first(int on);
 int bnn_maxpool_packed(const uint64_t *in, int64_t B, int64_t H, int64_t W, int64_t Cw, int k,
                        int stride, uint64_t *out, bnn_stream_t stream);
 
+/* A residual block's output y = a + residual (NCHW f32, f32 add as torch) and its
+ * sign-packed NHWC words (the next block's conv input); flags as the pack kernels.
+ * (Used after 64-filter convs, where the conv epilogue without the shortcut add is
+ * faster than the fused one.) */
+int bnn_add_pack_nchw_f32(const float *a, const float *residual, int64_t B, int64_t C, int64_t H,
+                          int64_t W, float *y, uint64_t *out_words, int32_t *flags,
+                          bnn_stream_t stream);
+
 /* Words per pixel of the packed NHWC activation layout: ceil(C / 64). */
 int64_t bnn_conv_channel_words(int64_t C);
 

@@ -71,6 +71,8 @@ int launch_conv_bn_relu_maxpool_tc(const float *, int64_t, int64_t, int64_t, int
                                    const float *, int, float *, cudaStream_t, int);
 int launch_maxpool_packed(const uint64_t *, int64_t, int64_t, int64_t, int64_t, int, int,
                           uint64_t *, cudaStream_t);
+int launch_add_pack_nchw(const float *, const float *, int64_t, int64_t, int64_t, int64_t, float *,
+                         uint64_t *, int32_t *, cudaStream_t);
 int launch_bconv2d_popc(const uint64_t *, int64_t, int64_t, int64_t, int64_t, const uint64_t *,
                         int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,
                         int64_t, float *, const Epilogue &, cudaStream_t, const float *);
@@ -351,6 +353,14 @@ int bnn_maxpool_packed(const uint64_t *in, int64_t B, int64_t H, int64_t W, int6
     BNN_REQUIRE(B == 0 || (in && out), BNN_EINVAL, "null pointer");
     BNN_REQUIRE(ceil_div(B * H * W * Cw, 256) < (1ll << 31), BNN_EUNSUP, "tensor too large");
     return launch_maxpool_packed(in, B, H, W, Cw, k, stride, out, as_stream(stream));
+}
+
+int bnn_add_pack_nchw_f32(const float *a, const float *residual, int64_t B, int64_t C, int64_t H,
+                          int64_t W, float *y, uint64_t *out_words, int32_t *flags,
+                          bnn_stream_t stream) {
+    BNN_REQUIRE(B >= 0 && C >= 1 && H >= 1 && W >= 1, BNN_EGEOM, "invalid shape");
+    BNN_REQUIRE(B == 0 || (a && residual && y && out_words), BNN_EINVAL, "null pointer");
+    return launch_add_pack_nchw(a, residual, B, C, H, W, y, out_words, flags, as_stream(stream));
 }
 
 int64_t bnn_conv_channel_words(int64_t C) { return C > 0 ? ceil_div(C, 64) : 0; }

@@ -607,7 +607,52 @@ __global__ void maxpool_packed_kernel(const uint64_t *__restrict__ in, int64_t H
     out[i] = v;
 }
 
+// Shortcut add + sign-pack: y = a + r (f32, the block output, same rounding as
+// torch) and the packed NHWC sign words of y for the next block's convs.  One
+// thread per (pixel, 32-channel word); the warp's threads are consecutive pixels,
+// so every channel plane is read and written in 128-byte runs.
+__global__ void add_pack_nchw_kernel(const float *__restrict__ a, const float *__restrict__ r,
+                                     int64_t B, int64_t C, int64_t HW, int64_t cs32,
+                                     float *__restrict__ y, uint32_t *__restrict__ out32,
+                                     int32_t *flags) {
+    const int64_t gp = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // pixel over B * HW
+    const int64_t wi = blockIdx.y;                                        // u32 word in pixel
+    int f = 0;
+    if (gp < B * HW) {
+        const int64_t b = gp / HW, p = gp - b * HW, c0 = wi * 32;
+        const int nc = (int)(C - c0 < 32 ? (C - c0 > 0 ? C - c0 : 0) : 32);
+        const int64_t base = (b * C + c0) * HW + p;
+        float va[32], vr[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            va[j] = j < nc ? __ldcs(a + base + (int64_t)j * HW) : -1.0f;
+            vr[j] = j < nc ? __ldcs(r + base + (int64_t)j * HW) : 0.0f;
+        }
+        uint32_t w = 0;
+        float nf = 0.0f;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const float v = __fadd_rn(va[j], vr[j]);
+            if (j < nc) y[base + (int64_t)j * HW] = v;
+            w |= (v >= 0.0f ? 1u : 0u) << j;  // sign(-0) = +1; channels past C: -1 -> 0
+            nf = __fmaf_rn(v, 0.0f, nf);
+        }
+        if (nf != 0.0f) f |= BNN_FLAG_NONFINITE;
+        out32[gp * cs32 + wi] = w;
+    }
+    flush_flags(f, flags);
+}
+
 // ================================================================ launchers
+int launch_add_pack_nchw(const float *a, const float *r, int64_t B, int64_t C, int64_t H,
+                         int64_t W, float *y, uint64_t *out, int32_t *flags, cudaStream_t s) {
+    const int64_t HW = H * W, Cw = ceil_div(C, 64);
+    if (B == 0 || HW == 0) return BNN_OK;
+    dim3 g((unsigned)ceil_div(B * HW, 128), (unsigned)(2 * Cw));
+    add_pack_nchw_kernel<<<g, 128, 0, s>>>(a, r, B, C, HW, 2 * Cw, y,
+                                           reinterpret_cast<uint32_t *>(out), flags);
+    return check_launch("add_pack_nchw_kernel");
+}
 int launch_maxpool_packed(const uint64_t *in, int64_t B, int64_t H, int64_t W, int64_t Cw, int k,
                           int st, uint64_t *out, cudaStream_t s) {
     const int64_t OH = (H - k) / st + 1, OW = (W - k) / st + 1;

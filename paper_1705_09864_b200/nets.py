@@ -368,6 +368,7 @@ class BinaryBasicBlock:
     # block's convs), so no standalone pack pass runs inside the network
     packed_io = True
     emit_packed = True  # False for the last block (a float layer consumes it)
+    split_shortcut = True  # conv2 epilogue without the add + one add/sign-pack pass
 
     def forward(self, x, mode=INFER_FLOAT):
         if mode == INFER_PACKED and self.fused and self.packed_io:
@@ -375,6 +376,18 @@ class BinaryBasicBlock:
                 x = PackedNHWC.from_f32(x, self.conv1._flags())
             h = self.conv1.forward_fused(x, self.bn1, pack_out=True, f32_out=False)
             sc = x.float() if self.down is None else self.down.forward_fused(x, self.bnd)
+            if self.split_shortcut:
+                # the conv epilogue without the shortcut is faster on every ResNet shape
+                # (profiles/r01/resnet_layer_epilogues.txt: f32 vs pack+f32+res), so the
+                # add and the sign-pack run as one streaming pass (bit-identical)
+                y = self.conv2.forward_fused(h, self.bn2)
+                b, f, oh, ow = y.shape
+                words = torch.empty((b, oh, ow, (f + 63) // 64), dtype=torch.uint64,
+                                    device=y.device)
+                _lib.call("bnn_add_pack_nchw_f32", _lib.ptr(y), _lib.ptr(sc.contiguous()), b, f,
+                          oh, ow, _lib.ptr(y), _lib.ptr(words), _lib.ptr(self.conv2._flags()),
+                          _lib.stream_ptr())
+                return PackedNHWC(words, y.shape, y) if self.emit_packed else y
             return self.conv2.forward_fused(h, self.bn2, residual=sc, pack_out=self.emit_packed)
         if isinstance(x, PackedNHWC):
             x = x.float()

@@ -77,6 +77,10 @@ def test_resnet18_c4_cross_mode(nets):
     assert torch.equal(yf, yp)
     # activations kept sign-packed between the binary convs (conv epilogues emit the
     # packed words) == a pack pass over every f32 block output
+    for layer in net.layers:  # the shortcut add inside the conv2 epilogue
+        if isinstance(layer, nets.BinaryBasicBlock):
+            layer.split_shortcut = False
+    assert torch.equal(net.forward(x, bnn.INFER_PACKED), yf)
     for layer in net.layers:
         if isinstance(layer, nets.BinaryBasicBlock):
             layer.packed_io = False

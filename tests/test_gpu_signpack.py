@@ -181,3 +181,23 @@ def test_sign_pack_flags_nonfinite_and_validation(bnn):
     with pytest.raises(ValueError, match="null"):
         _lib.call("bnn_xnor_gemm_ex", _lib.ptr(wa), wa.stride(0), _lib.ptr(xb), xb.stride(0), m, n,
                   k, 0, 0, None, n, 1, ctypes.byref(e3), _lib.ALGOS["auto"], _lib.stream_ptr())
+
+
+@pytest.mark.parametrize("shape", [(2, 64, 9, 9), (3, 100, 5, 7), (1, 32, 4, 4)])
+def test_add_pack_nchw(bnn, shape):
+    """bnn_add_pack_nchw_f32: y = a + r (f32) and the packed sign words of y."""
+    from paper_1705_09864_b200 import _lib
+    g = torch.Generator().manual_seed(sum(shape))
+    a = torch.randn(shape, generator=g).cuda()
+    r = torch.randn(shape, generator=g).cuda()
+    a.view(-1)[::7] = 0.0
+    r.view(-1)[::7] = -0.0
+    b, c, h, w = shape
+    y = torch.empty_like(a)
+    words = torch.empty((b, h, w, (c + 63) // 64), dtype=torch.uint64, device="cuda")
+    flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+    _lib.call("bnn_add_pack_nchw_f32", _lib.ptr(a), _lib.ptr(r), b, c, h, w, _lib.ptr(y),
+              _lib.ptr(words), _lib.ptr(flags), _lib.stream_ptr())
+    assert torch.equal(y, a + r)
+    assert np.array_equal(words.cpu().numpy(), bnn.pack_nchw(a + r).cpu().numpy())
+    assert int(flags.item()) == 0
