@@ -221,6 +221,16 @@ int bnn_conv_bn_relu_maxpool_f32_tc(const float *x, int64_t B, int64_t C, int64_
                                     const float *mean, const float *inv_std, const float *gamma,
                                     const float *beta, int relu, float *y, bnn_stream_t stream);
 
+/* The same, also writing the sign-packed NHWC words of y (the first binary
+ * block's input; flags as the pack kernels), so no pack pass follows the stem. */
+int bnn_conv_bn_relu_maxpool_pack_f32_tc(const float *x, int64_t B, int64_t C, int64_t H,
+                                         int64_t W, const float *w, int64_t F, int64_t kh,
+                                         int64_t kw, int64_t sh, int64_t sw, int64_t ph, int64_t pw,
+                                         const float *mean, const float *inv_std,
+                                         const float *gamma, const float *beta, int relu,
+                                         float *y, uint64_t *out_words, int32_t *flags,
+                                         bnn_stream_t stream);
+
 /* LeNet's float stem as one kernel: y = maxpool_2x2/2(tanh(conv(x, w) + bias))
  * (reference Conv2d -> Tanh -> MaxPool2d, layers.py:81-141, 480-540), the same
  * per-element f32 ops as the unfused sequence; bias may be null.  BNN_EUNSUP

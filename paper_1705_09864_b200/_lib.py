@@ -52,6 +52,9 @@ SIGNATURES = {
     "bnn_conv_bn_relu_maxpool_f32_tc": (_i32, [_vp, _i64, _i64, _i64, _i64, _vp, _i64, _i64, _i64,
                                                _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _i32,
                                                _vp, _vp]),
+    "bnn_conv_bn_relu_maxpool_pack_f32_tc": (_i32, [_vp, _i64, _i64, _i64, _i64, _vp, _i64, _i64,
+                                                    _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp,
+                                                    _vp, _i32, _vp, _vp, _vp, _vp]),
     "bnn_conv_tanh_maxpool2_f32_tc": (_i32, [_vp, _i64, _i64, _i64, _i64, _vp, _vp, _i64, _i64,
                                              _i64, _i64, _i64, _i64, _i64, _vp, _vp]),
     "bnn_probe_tanh_monotone": (_i32, [_vp, _vp]),

@@ -68,7 +68,8 @@ int launch_conv2d_f32_tc(const float *, int64_t, int64_t, int64_t, int64_t, cons
 int launch_conv_bn_relu_maxpool_tc(const float *, int64_t, int64_t, int64_t, int64_t,
                                    const float *, int64_t, int64_t, int64_t, int64_t, int64_t,
                                    int64_t, int64_t, const float *, const float *, const float *,
-                                   const float *, int, float *, cudaStream_t, int);
+                                   const float *, int, float *, cudaStream_t, int, uint64_t *,
+                                   int32_t *);
 int launch_maxpool_packed(const uint64_t *, int64_t, int64_t, int64_t, int64_t, int, int,
                           uint64_t *, cudaStream_t);
 int launch_add_pack_nchw(const float *, const float *, int64_t, int64_t, int64_t, int64_t, float *,
@@ -329,7 +330,26 @@ int bnn_conv_bn_relu_maxpool_f32_tc(const float *x, int64_t B, int64_t C, int64_
                 BNN_EGEOM, "invalid convolution geometry");
     BNN_REQUIRE(x && w && y && mean && inv_std && gamma && beta, BNN_EINVAL, "null pointer");
     return launch_conv_bn_relu_maxpool_tc(x, B, C, H, W, w, F, kh, kw, sh, sw, ph, pw, mean,
-                                          inv_std, gamma, beta, relu, y, as_stream(stream), 0);
+                                          inv_std, gamma, beta, relu, y, as_stream(stream), 0,
+                                          nullptr, nullptr);
+}
+
+int bnn_conv_bn_relu_maxpool_pack_f32_tc(const float *x, int64_t B, int64_t C, int64_t H,
+                                         int64_t W, const float *w, int64_t F, int64_t kh,
+                                         int64_t kw, int64_t sh, int64_t sw, int64_t ph, int64_t pw,
+                                         const float *mean, const float *inv_std,
+                                         const float *gamma, const float *beta, int relu,
+                                         float *y, uint64_t *out_words, int32_t *flags,
+                                         bnn_stream_t stream) {
+    BNN_REQUIRE(B >= 0 && C >= 1 && H >= 1 && W >= 1 && F >= 1 && kh >= 1 && kw >= 1 &&
+                    sh >= 1 && sw >= 1 && ph >= 0 && pw >= 0 && H + 2 * ph >= kh &&
+                    W + 2 * pw >= kw,
+                BNN_EGEOM, "invalid convolution geometry");
+    BNN_REQUIRE(x && w && y && mean && inv_std && gamma && beta && out_words, BNN_EINVAL,
+                "null pointer");
+    return launch_conv_bn_relu_maxpool_tc(x, B, C, H, W, w, F, kh, kw, sh, sw, ph, pw, mean,
+                                          inv_std, gamma, beta, relu, y, as_stream(stream), 0,
+                                          out_words, flags);
 }
 
 int bnn_conv_tanh_maxpool2_f32_tc(const float *x, int64_t B, int64_t C, int64_t H, int64_t W,
@@ -342,7 +362,8 @@ int bnn_conv_tanh_maxpool2_f32_tc(const float *x, int64_t B, int64_t C, int64_t 
                 BNN_EGEOM, "invalid convolution geometry");
     BNN_REQUIRE(x && w && y, BNN_EINVAL, "null pointer");
     return launch_conv_bn_relu_maxpool_tc(x, B, C, H, W, w, F, kh, kw, sh, sw, ph, pw, bias,
-                                          nullptr, nullptr, nullptr, 0, y, as_stream(stream), 1);
+                                          nullptr, nullptr, nullptr, 0, y, as_stream(stream), 1,
+                                          nullptr, nullptr);
 }
 
 int bnn_maxpool_packed(const uint64_t *in, int64_t B, int64_t H, int64_t W, int64_t Cw, int k,

@@ -335,6 +335,8 @@ struct PoolGeom {
     int mode;  // 0: BN + ReLU? + maxpool 3x3/2/1; 1: + bias, tanh, maxpool 2x2/2/0 (LeNet)
     int R;     // conv rows per tile (mode 1: an even number of narrow rows fills the lanes)
     int pool_first;  // mode 1: tanhf is monotone (probed): max-pool, then one tanh per output
+    uint16_t *pack16;    // mode 0, optional: sign-packed NHWC words of y as 16-bit pieces
+    int32_t *pack_flags;
     int NR;    // staged input rows per channel: (R - 1) * sh + kh
     int dbg;  // debug (BNN_STEM_DEBUG, wrong results): 1 no gather loads, 2 no MMAs,
               // 4 no epilogue work, 8 no loader loads
@@ -634,25 +636,38 @@ __global__ void __launch_bounds__(PEpi<kEW>::kThreads, 1) conv_pool_kernel(const
         const int q = warp & 3, et = tid - kPEpiWarp0 * 32;
         const int hsel = (warp - kPEpiWarp0) >> 2;  // TMEM columns [32 hsel, 32 hsel + 32)
         const int ox = q * 32 + lane;
-        const int px = et & 63, c0 = et >> 6;  // pooled column, channel group (c = c0 + kPCG i)
+        const int px = et & 63, c0 = et >> 6;  // pooled column, channel run c0 * kPCPer + i
         float cur[kPCPer];
         int it = 0;
         POOL_ITEMS_BEGIN
 #pragma unroll
         for (int i = 0; i < kPCPer; ++i) cur[i] = -INFINITY;
         float *yb = g.y + (int64_t)b * NF * g.PH * g.PW;
+        // sign-pack of an emitted pooled pixel: this thread's kPCPer channels are one
+        // kPCPer-bit piece of the pixel's packed NHWC word(s)
+        auto put_bits = [&](int py, uint32_t bits, float nf) {
+            if (kPCPer != 16 || !g.pack16) return;
+            const int64_t pix = ((int64_t)b * g.PH + py) * g.PW + px;
+            g.pack16[pix * (NF / 16) + c0] = (uint16_t)bits;
+            if (g.pack_flags && nf != 0.0f) atomicOr(g.pack_flags, 1);
+        };
         auto emit = [&](int py) {
             if (px >= g.PW) return;
+            uint32_t bits = 0;
+            float nf = 0.0f;
 #pragma unroll
             for (int i = 0; i < kPCPer; ++i) {
-                const int c = c0 + kPCG * i;
+                const int c = c0 * kPCPer + i;
                 float v = __fmul_rn(cur[i], bnt[c]);
                 v = __fadd_rn(__fmul_rn(bnt[3 * NF + c], __fmul_rn(__fsub_rn(v, bnt[NF + c]),
                                                                     bnt[2 * NF + c])),
                               bnt[4 * NF + c]);
                 if (g.relu) v = fmaxf(v, 0.0f);
                 yb[((int64_t)c * g.PH + py) * g.PW + px] = v;
+                bits |= (v >= 0.0f ? 1u : 0u) << i;
+                nf = __fmaf_rn(v, 0.0f, nf);
             }
+            put_bits(py, bits, nf);
         };
         for (int oy = oy_s; oy <= oy_e; oy += g.R, ++it) {
             const int buf = it % kPAcc;
@@ -695,7 +710,7 @@ __global__ void __launch_bounds__(PEpi<kEW>::kThreads, 1) conv_pool_kernel(const
                     const int o0 = 2 * r * g.OW + 2 * px, o1 = o0 + g.OW;
 #pragma unroll 8
                     for (int i = 0; i < kPCPer; ++i) {
-                        const int c = c0 + kPCG * i;
+                        const int c = c0 * kPCPer + i;
                         const float *rr = rbuf + c * kRowPitchR;
                         const float m = fmaxf(fmaxf(rr[o0], rr[o0 + 1]), fmaxf(rr[o1], rr[o1 + 1]));
                         yrow[(int64_t)c * g.PH * g.PW] = g.pool_first ? tanhf(m) : m;
@@ -705,9 +720,11 @@ __global__ void __launch_bounds__(PEpi<kEW>::kThreads, 1) conv_pool_kernel(const
                 const int xl = 2 * px - 1, xr = 2 * px + 1;
                 const bool odd = oy & 1, done = odd && ((oy - 1) >> 1) >= py0;
                 float *yrow = yb + (int64_t)((oy - 1) >> 1) * g.PW + px;
+                uint32_t bits = 0;
+                float nf = 0.0f;
 #pragma unroll
                 for (int i = 0; i < kPCPer; ++i) {
-                    const int c = c0 + kPCG * i;
+                    const int c = c0 * kPCPer + i;
                     const float *rr = rbuf + c * kRowPitchR;
                     float m = rr[2 * px];
                     if (xl >= 0) m = fmaxf(m, rr[xl]);
@@ -719,9 +736,12 @@ __global__ void __launch_bounds__(PEpi<kEW>::kThreads, 1) conv_pool_kernel(const
                                       bnt[4 * NF + c]);
                         if (g.relu) v = fmaxf(v, 0.0f);
                         yrow[(int64_t)c * g.PH * g.PW] = v;
+                        bits |= (v >= 0.0f ? 1u : 0u) << i;
+                        nf = __fmaf_rn(v, 0.0f, nf);
                     }
                     cur[i] = odd ? m : fmaxf(cur[i], m);
                 }
+                if (done) put_bits((oy - 1) >> 1, bits, nf);
             }
             epi_bar<kEW>();  // the row buffer is free for the next conv row
         }
@@ -781,7 +801,8 @@ int launch_conv_bn_relu_maxpool_tc(const float *x, int64_t B, int64_t C, int64_t
                                    const float *w, int64_t F, int64_t kh, int64_t kw, int64_t sh,
                                    int64_t sw, int64_t ph, int64_t pw, const float *mean,
                                    const float *inv, const float *gamma, const float *beta,
-                                   int relu, float *y, cudaStream_t s, int mode) {
+                                   int relu, float *y, cudaStream_t s, int mode,
+                                   uint64_t *pack_words, int32_t *pack_flags) {
     using namespace stem;
     const int64_t K = C * kh * kw;
     const int64_t OH = (H + 2 * ph - kh) / sh + 1, OW = (W + 2 * pw - kw) / sw + 1;
@@ -795,6 +816,8 @@ int launch_conv_bn_relu_maxpool_tc(const float *x, int64_t B, int64_t C, int64_t
     g.x = x, g.w = w, g.mean = mean, g.inv = inv, g.gamma = gamma, g.beta = beta, g.y = y;
     g.relu = relu;
     g.mode = mode;
+    g.pack16 = mode == 0 ? reinterpret_cast<uint16_t *>(pack_words) : nullptr;
+    g.pack_flags = pack_flags;
     g.pool_first = mode == 1 && g_tanh_pool_first;
     {
         const char *e = getenv("BNN_STEM_DEBUG");

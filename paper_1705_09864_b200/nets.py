@@ -174,7 +174,8 @@ class StemPost:
         return (conv.engine == "tc" and conv.tc_supported() and conv.bias is None and
                 (p.k, p.stride, p.pad) == (3, 2, 1))
 
-    def forward_fused_conv(self, conv: "Conv2d", x: torch.Tensor) -> torch.Tensor:
+    def forward_fused_conv(self, conv: "Conv2d", x: torch.Tensor, pack: bool = False,
+                           flags: torch.Tensor | None = None):
         """maxpool(relu(BN(conv(x)))) in one kernel (bnn_conv_bn_relu_maxpool_f32_tc):
         the pool runs on sign-adjusted conv outputs before the BatchNorm, which is
         exact because the rounded BN + ReLU is monotone per channel."""
@@ -185,11 +186,17 @@ class StemPost:
         ph, pw = (oh - 1) // 2 + 1, (ow - 1) // 2 + 1
         y = torch.empty((b, conv.cout, ph, pw), dtype=torch.float32, device=x.device)
         mean, inv, gamma, beta = self.bn.device_params()
-        st = _lib.call_status("bnn_conv_bn_relu_maxpool_f32_tc", _lib.ptr(x), b, c, h, w,
-                              _lib.ptr(conv._dev("weight")), conv.cout, conv.k, conv.k,
-                              conv.stride, conv.stride, conv.pad, conv.pad, _lib.ptr(mean),
-                              _lib.ptr(inv), _lib.ptr(gamma), _lib.ptr(beta), 1, _lib.ptr(y),
-                              _lib.stream_ptr())
+        args = (_lib.ptr(x), b, c, h, w, _lib.ptr(conv._dev("weight")), conv.cout, conv.k,
+                conv.k, conv.stride, conv.stride, conv.pad, conv.pad, _lib.ptr(mean),
+                _lib.ptr(inv), _lib.ptr(gamma), _lib.ptr(beta), 1, _lib.ptr(y))
+        if pack and conv.cout == 64:  # + the sign-packed words of y for the first block
+            words = torch.empty((b, ph, pw, 1), dtype=torch.uint64, device=x.device)
+            st = _lib.call_status("bnn_conv_bn_relu_maxpool_pack_f32_tc", *args, _lib.ptr(words),
+                                  _lib.ptr(flags), _lib.stream_ptr())
+            if st == _lib.OK:
+                return PackedNHWC(words, y.shape, y)
+        else:
+            st = _lib.call_status("bnn_conv_bn_relu_maxpool_f32_tc", *args, _lib.stream_ptr())
         if st == _lib.EUNSUP:  # shape outside the fused kernel: two kernels
             return self.forward(conv.forward(x), INFER_PACKED)
         _lib.check(st, "bnn_conv_bn_relu_maxpool_f32_tc")
@@ -240,10 +247,14 @@ class Sequential:
                 continue
             if (mode == INFER_PACKED and self.fuse_stem and isinstance(layer, Conv2d)
                     and isinstance(nxt, StemPost) and nxt.fusable(layer)):
-                x = nxt.forward_fused_conv(layer, x)  # conv + BN + ReLU + maxpool, one kernel
+                after = self.layers[i + 2] if i + 2 < n else None
+                pack = isinstance(after, BinaryBasicBlock) and after.fused and after.packed_io
+                # conv + BN + ReLU + maxpool (+ the first block's sign-pack), one kernel
+                x = nxt.forward_fused_conv(layer, x, pack=pack,
+                                           flags=after.conv1._flags() if pack else None)
                 if capture is not None:
                     capture.append(None)
-                    capture.append(x)
+                    capture.append(x.float() if isinstance(x, PackedNHWC) else x)
                 i += 2
                 continue
             if (mode == INFER_PACKED and self.fuse_bn and isinstance(nxt, BatchNorm)

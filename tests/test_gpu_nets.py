@@ -248,3 +248,17 @@ def test_lenet_packed_tail_equals_float_path(nets):
     x = torch.randn((6, 64, 14, 14), generator=torch.Generator().manual_seed(5)).cuda()
     x.view(-1)[::13] = 0.0
     assert torch.equal(tail.forward(x, bnn.INFER_PACKED), tail.forward(x, bnn.INFER_FLOAT))
+
+
+def test_fused_stem_sign_pack(nets):
+    """The stem kernel's packed output == packing its f32 output (the first block's input)."""
+    import paper_1705_09864_b200 as bnn
+    rng = np.random.default_rng(17)
+    conv = nets.Conv2d(3, 64, 7, stride=2, pad=3, bias=False, rng=rng)
+    post = nets.StemPost(64, rng, 3, 2, 1)
+    post.bn.gamma[::3] *= -1.0
+    x = torch.randn((2, 3, 64, 64), generator=torch.Generator().manual_seed(3)).cuda()
+    out = post.forward_fused_conv(conv, x, pack=True)
+    assert isinstance(out, nets.PackedNHWC)
+    assert torch.equal(out.f32, post.forward_fused_conv(conv, x))
+    assert np.array_equal(out.words.cpu().numpy(), bnn.pack_nchw(out.f32).cpu().numpy())
