@@ -1858,7 +1858,9 @@ static int launch_umma(const ALoad &a, const BLoad &b, const Store &st, const Ep
         // variant 0 (128 x 256 tiles, A and B through SMEM) also by default for cp.async-fed
         // shapes with M <= 64 (e.g. ResNet-18 layer1 convs, 64 filters): measured 1.1-1.4x
         // the A-in-TMEM engine there (tools/l1_variants.sh)
-        const bool small_m = (umma_variant() == 2 || umma_variant() == 4) && M <= 64 &&
+        // (and for every cp.async-fed conv: C % 256 != 0; measured 1.0-1.1x, profiles/r01)
+        const bool small_m = (umma_variant() == 2 || umma_variant() == 4) &&
+                             (M <= 64 || std::is_same<BLoad, ConvRows>::value) &&
                              !umma::is_tma<ALoad>::value;
         if (umma_variant() == 0 || small_m)
             return launch_umma_cfg<256, false, kVec>(a, b, st, ep, M, N, kw32, s);

@@ -204,3 +204,22 @@ def test_lenet_stem_and_packed_pool_validation(lib):
     assert lib.bnn_conv_tanh_maxpool2_f32_tc(*args[:5], None, *args[6:]) == -1
     args[7] = 32  # F != 64
     assert lib.bnn_conv_tanh_maxpool2_f32_tc(*args) == -7
+
+
+def test_network_launch_counter():
+    """plan._count_lib_launches counts the library's compute calls of a step (the
+    bench's gpu_launches for the network workloads), not its queries / setters."""
+    from paper_1705_09864_b200 import _lib, plan
+
+    def step():
+        _lib.call("bnn_conv_channel_words", 64)  # query: not a launch
+        for _ in range(3):
+            try:  # rejected in validation before any CUDA call, but counted as a launch
+                _lib.call("bnn_maxpool_packed", None, 1, 4, 4, 1, 2, 2, None, None)
+            except ValueError:
+                pass
+        _lib.call_status("bnn_conv2d_f32_tc", None, 1, 3, 8, 8, None, None, 64, 7, 7, 2, 2, 3,
+                         3, None, None)
+
+    assert plan._count_lib_launches(step) == 4
+    assert _lib.call.__name__ == "call"  # restored
