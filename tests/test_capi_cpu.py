@@ -212,7 +212,7 @@ def test_network_launch_counter():
     from paper_1705_09864_b200 import _lib, plan
 
     def step():
-        _lib.call("bnn_conv_channel_words", 64)  # query: not a launch
+        _lib.call("bnn_set_tanh_pool_first", 0)  # setter: not a launch
         for _ in range(3):
             try:  # rejected in validation before any CUDA call, but counted as a launch
                 _lib.call("bnn_maxpool_packed", None, 1, 4, 4, 1, 2, 2, None, None)
