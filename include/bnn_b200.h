@@ -264,6 +264,16 @@ int bnn_add_pack_nchw_f32(const float *a, const float *residual, int64_t B, int6
                           int64_t W, float *y, uint64_t *out_words, int32_t *flags,
                           bnn_stream_t stream);
 
+/* Split-K combine (small GEMMs such as config 1: too few output tiles to fill
+ * the SMs, so the caller runs word-aligned K ranges as concurrent popcount-
+ * domain GEMMs into `splits` partial buffers, partial s at partials + s*stride,
+ * and sums them here):  out[i] = sum_s partials[s*stride + i], or 2*sum - K
+ * when domain == BNN_DOT.  The partials are integer counts < 2^24, so the
+ * result is bit-identical to one unsplit bnn_xnor_gemm (the reference's
+ * int32 accumulation, gemm.py:128-139, then .astype(float32)). */
+int bnn_sum_partials_f32(const float *partials, int splits, int64_t count, int64_t stride,
+                         int domain, int64_t K, float *out, bnn_stream_t stream);
+
 /* Words per pixel of the packed NHWC activation layout: ceil(C / 64). */
 int64_t bnn_conv_channel_words(int64_t C);
 

@@ -54,6 +54,7 @@ int launch_xnor_gemm_bmma(const uint64_t *, int64_t, const uint64_t *, int64_t, 
 int launch_bconv2d_bmma(const uint64_t *, int64_t, int64_t, int64_t, int64_t, const uint64_t *,
                         int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,
                         int64_t, float *, const Epilogue &, cudaStream_t, const float *);
+int launch_sum_partials(const float *, int, int64_t, int64_t, float, float, float *, cudaStream_t);
 int launch_pack_planes(const float *, int64_t, int64_t, int64_t, int, int, uint64_t *, int64_t,
                        int64_t, int32_t *, cudaStream_t);
 int launch_bitplane_gemm_umma(const uint64_t *, int64_t, int64_t, const uint64_t *, int64_t,
@@ -374,6 +375,19 @@ int bnn_maxpool_packed(const uint64_t *in, int64_t B, int64_t H, int64_t W, int6
     BNN_REQUIRE(B == 0 || (in && out), BNN_EINVAL, "null pointer");
     BNN_REQUIRE(ceil_div(B * H * W * Cw, 256) < (1ll << 31), BNN_EUNSUP, "tensor too large");
     return launch_maxpool_packed(in, B, H, W, Cw, k, stride, out, as_stream(stream));
+}
+
+int bnn_sum_partials_f32(const float *partials, int splits, int64_t count, int64_t stride,
+                         int domain, int64_t K, float *out, bnn_stream_t stream) {
+    BNN_REQUIRE(splits >= 1 && count >= 0, BNN_EINVAL, "invalid size");
+    BNN_REQUIRE(splits == 1 || stride >= count, BNN_EALIGN, "stride smaller than count");
+    BNN_REQUIRE(domain == BNN_POPCOUNT || domain == BNN_DOT, BNN_EINVAL, "bad domain %d", domain);
+    int rc = check_gemm_dims(1, 1, K);
+    if (rc) return rc;
+    BNN_REQUIRE(count == 0 || (partials && out), BNN_EINVAL, "null pointer");
+    const float alpha = domain == BNN_DOT ? 2.0f : 1.0f;
+    const float beta = domain == BNN_DOT ? -(float)K : 0.0f;
+    return launch_sum_partials(partials, splits, count, stride, alpha, beta, out, as_stream(stream));
 }
 
 int bnn_add_pack_nchw_f32(const float *a, const float *residual, int64_t B, int64_t C, int64_t H,

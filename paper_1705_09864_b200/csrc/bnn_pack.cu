@@ -830,4 +830,45 @@ int launch_conv_weights_reorder(const uint64_t *w_ref, int64_t F, int64_t C, int
     return check_launch("conv_weights_reorder_kernel");
 }
 
+
+// ---------------------------------------------------------------------------
+// split-K combine: out = alpha * sum_s partials[s] + beta.  The partials are
+// popcount-domain counts of disjoint, word-aligned K ranges (integers < 2^24),
+// so every f32 add is exact and the result is bit-identical to one unsplit
+// launch: P = sum_s P_s (popcount domain) or 2P - K (dot domain, qmath.py:102-109).
+// Streaming, HBM-bound: splits x 4 B read + 4 B written per output.
+__global__ void sum_partials_kernel(const float *__restrict__ p, int splits, int64_t count,
+                                    int64_t stride, float alpha, float beta,
+                                    float *__restrict__ out, bool vec) {
+    const int64_t n4 = vec ? count >> 2 : 0;
+    const int64_t step = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += step) {
+        float4 acc = __ldcs(reinterpret_cast<const float4 *>(p) + i);
+        for (int s = 1; s < splits; ++s) {
+            const float4 v = __ldcs(reinterpret_cast<const float4 *>(p + s * stride) + i);
+            acc.x += v.x, acc.y += v.y, acc.z += v.z, acc.w += v.w;
+        }
+        acc.x = fmaf(alpha, acc.x, beta), acc.y = fmaf(alpha, acc.y, beta);
+        acc.z = fmaf(alpha, acc.z, beta), acc.w = fmaf(alpha, acc.w, beta);
+        reinterpret_cast<float4 *>(out)[i] = acc;
+    }
+    for (int64_t i = 4 * n4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += step) {
+        float acc = p[i];
+        for (int s = 1; s < splits; ++s) acc += p[s * stride + i];
+        out[i] = fmaf(alpha, acc, beta);
+    }
+}
+
+int launch_sum_partials(const float *p, int splits, int64_t count, int64_t stride, float alpha,
+                        float beta, float *out, cudaStream_t s) {
+    if (count == 0) return BNN_OK;
+    const int64_t blocks = ceil_div(ceil_div(count, 4), 256);
+    const int64_t cap = 8LL * 148;
+    const bool vec = ((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(out)) & 15) == 0 &&
+                     (stride & 3) == 0;
+    sum_partials_kernel<<<(unsigned)(blocks < cap ? blocks : cap), 256, 0, s>>>(
+        p, splits, count, stride, alpha, beta, out, vec);
+    return check_launch("sum_partials_kernel");
+}
+
 }  // namespace bnn

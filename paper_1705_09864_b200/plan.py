@@ -11,6 +11,8 @@ reference's ValueError on non-finite input (bitpack.py:37-38).
 
 from __future__ import annotations
 
+import os
+
 import torch
 
 from . import _lib
@@ -185,6 +187,33 @@ class DensePlan(_Plan):
         self._alloc_common()
         self.lib = _lib.load()
         self.m, self.n, self.k = layer.units, batch, k
+        self.chunks = self._k_chunks() if self.algo == _lib.ALGOS["auto"] else [(0, self.k)]
+        if len(self.chunks) > 1:
+            self.part = torch.empty((len(self.chunks), batch, layer.units), dtype=torch.float32,
+                                    device="cuda")
+            self._kstreams = [torch.cuda.Stream() for _ in self.chunks]
+            self.launches_per_step = 2 + len(self.chunks)
+
+    def _k_chunks(self):
+        """Split-K (opt-in, BNN_DENSE_SPLITK=<ranges>): word-aligned K ranges of
+        >= 512 bits run as popcount-domain GEMMs on forked streams and
+        bnn_sum_partials_f32 adds the exact integer counts (bit-identical to one
+        launch).  Meant for GEMMs with too few output tiles to fill the SMs
+        (config 1: 16 tiles of 128 x 128 on 148 SMs), but measured slower there
+        (tools/splitk_diag.py, profiles/r01/splitk_c1.txt): a K=512 launch costs
+        8.3 us against 16.4 us for all of K=4096 -- the per-tile fixed latency
+        (setup, first TMA round trip, epilogue) dominates -- and the forked
+        launches did not overlap.  Off by default."""
+        words = words_per_bits(self.k)
+        env = os.environ.get("BNN_DENSE_SPLITK")
+        if env is None:
+            return [(0, self.k)]
+        splits = min(int(env), words // 4)
+        if splits < 2:
+            return [(0, self.k)]
+        step = -(-words // splits)
+        step = -(-step // 4) * 4  # whole 256-bit superstages per range
+        return [(64 * w0, min(self.k, 64 * (w0 + step))) for w0 in range(0, words, step)]
 
     @property
     def binary_ops(self) -> int:
@@ -198,10 +227,28 @@ class DensePlan(_Plan):
 
     def kernel(self, stream: int | None = None):
         s = _lib.stream_ptr() if stream is None else stream
+        if len(self.chunks) > 1 and stream is None:
+            return self._kernel_split()
         _lib.check(self.lib.bnn_xnor_gemm(self.wa.data_ptr(), self.wa.shape[1], self.xw.data_ptr(),
                                           self.xw.shape[1], self.m, self.n, self.k, 0, 0,
                                           self.y.data_ptr(), 1, self.m, self.layer.domain, None,
                                           None, self.algo, s), "xnor_gemm")
+
+    def _kernel_split(self):
+        cur = torch.cuda.current_stream()
+        for i, ((k0, k1), st) in enumerate(zip(self.chunks, self._kstreams)):
+            st.wait_stream(cur)
+            w0 = k0 // 64
+            _lib.check(self.lib.bnn_xnor_gemm(
+                self.wa.data_ptr() + 8 * w0, self.wa.shape[1], self.xw.data_ptr() + 8 * w0,
+                self.xw.shape[1], self.m, self.n, k1 - k0, 0, 0, self.part[i].data_ptr(), 1,
+                self.m, _lib.POPCOUNT, None, None, self.algo, st.cuda_stream), "xnor_gemm")
+        for st in self._kstreams:
+            cur.wait_stream(st)
+        _lib.check(self.lib.bnn_sum_partials_f32(self.part.data_ptr(), len(self.chunks),
+                                                 self.y.numel(), self.y.numel(), self.layer.domain,
+                                                 self.k, self.y.data_ptr(), cur.cuda_stream),
+                   "sum_partials")
 
     def run_device(self):
         self.pack()

@@ -587,3 +587,52 @@ def test_cta_pair_route_bit_exact(bnn, monkeypatch):
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120,
                        env=env, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert "PAIR_OK" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("domain", ["dot", "popcount"])
+def test_dense_plan_split_k_config1(bnn, golden_dir, monkeypatch, domain):
+    """Opt-in split-K: DensePlan runs word-aligned K ranges as GEMMs on forked
+    streams and sums the exact counts (bnn_sum_partials_f32).  Bit-identical
+    to the reference (golden SHA-256) and to the unsplit launch, eager and
+    under CUDA-graph capture."""
+    from paper_1705_09864_b200.plan import DensePlan
+    monkeypatch.setenv("BNN_DENSE_SPLITK", "8")
+    a, w = wl.config1_inputs()
+    layer = bnn.QFullyConnected(4096, 1024, domain=domain)
+    layer.weight = w
+    layer.pack()
+    plan = DensePlan(layer, a.shape[0])
+    assert len(plan.chunks) > 1
+    plan.x.copy_(torch.from_numpy(a))
+    y = plan.run_device().cpu().numpy()
+    one = layer.forward(torch.from_numpy(a).cuda(), bnn.INFER_PACKED).cpu().numpy()
+    assert np.array_equal(y, one)
+    if domain == "dot":
+        cfg = json.load(open(os.path.join(golden_dir, "configs.json")))["c1"]
+        assert _sha(y) == cfg["sha256"]
+    plan.y.zero_()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        plan.run_device()
+    g.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(plan.y.cpu().numpy(), one)
+
+
+@pytest.mark.parametrize("splits,b,k,u", [(2, 300, 1000, 130), (3, 256, 4096, 1024), (5, 64, 2047, 257),
+                                          (16, 129, 8192, 200)])
+def test_dense_plan_split_k_ragged(bnn, monkeypatch, splits, b, k, u):
+    """Forced split counts over ragged K (tail in the last range only), odd units."""
+    from paper_1705_09864_b200.plan import DensePlan
+    monkeypatch.setenv("BNN_DENSE_SPLITK", str(splits))
+    rng = np.random.default_rng(splits * 31 + k)
+    x = rng.standard_normal((b, k), dtype=np.float32)
+    wt = rng.standard_normal((u, k), dtype=np.float32)
+    layer = bnn.QFullyConnected(k, u)
+    layer.weight = wt
+    layer.pack()
+    plan = DensePlan(layer, b)
+    assert len(plan.chunks) > 1 and plan.chunks[-1][1] == k
+    plan.x.copy_(torch.from_numpy(x))
+    y = plan.run_device().cpu().numpy()
+    assert np.array_equal(y, orc.qdense_packed(orc.binarize(x), wt))
