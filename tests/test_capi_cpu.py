@@ -86,6 +86,13 @@ def test_conv_and_pack_validation(lib):
     assert lib.bnn_pack_cols_f32(1, 4, 4, 4, 1, 4, 0, 5, None, None) == -1
     assert lib.bnn_conv_channel_words(64) == 1 and lib.bnn_conv_channel_words(65) == 2
     assert lib.bnn_audit_padding(1, 1, 70, 1, 1, 3, 1, None) == -4
+    # split-K combine: sizes, stride, domain and GemmDims' K bound, checked before any launch
+    assert lib.bnn_sum_partials_f32(1, 0, 4, 4, 0, 64, 1, None) == -1
+    assert lib.bnn_sum_partials_f32(1, 2, 8, 4, 0, 64, 1, None) == -5  # stride < count
+    assert lib.bnn_sum_partials_f32(1, 2, 4, 4, 5, 64, 1, None) == -1
+    assert lib.bnn_sum_partials_f32(1, 2, 4, 4, 1, 1 << 24, 1, None) == -3
+    assert lib.bnn_sum_partials_f32(None, 2, 4, 4, 0, 64, None, None) == -1
+    assert lib.bnn_sum_partials_f32(None, 2, 0, 0, 0, 64, None, None) == 0  # empty: no launch
 
 
 def test_host_gemm_dims_and_workers(monkeypatch):
