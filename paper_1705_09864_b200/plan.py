@@ -201,9 +201,9 @@ class DensePlan(_Plan):
         launch).  Meant for GEMMs with too few output tiles to fill the SMs
         (config 1: 16 tiles of 128 x 128 on 148 SMs), but measured slower there
         (tools/splitk_diag.py, profiles/r01/splitk_c1.txt): a K=512 launch costs
-        8.3 us against 16.4 us for all of K=4096 -- the per-tile fixed latency
-        (setup, first TMA round trip, epilogue) dominates -- and the forked
-        launches did not overlap.  Off by default."""
+        8.3 us against 16.4 us for all of K=4096 -- the per-launch fixed latency
+        dominates -- and the engine already spreads config 1 over 128 CTAs
+        (128 x 16 tiles), so the forked launches cannot overlap.  Off by default."""
         words = words_per_bits(self.k)
         env = os.environ.get("BNN_DENSE_SPLITK")
         if env is None:

@@ -49,6 +49,11 @@ def graph_time(fn):
 
 
 cur = lambda: torch.cuda.current_stream().cuda_stream
+if "--ncu" in sys.argv:  # launch list only: one unsplit GEMM, then one split step
+    gemm(0, 4096, cur(), plan.y)
+    plan._kernel_split()
+    torch.cuda.synchronize()
+    sys.exit(0)
 print("full K=4096 eager us", timeit(lambda: gemm(0, 4096, cur(), plan.y)))
 print("one chunk K=512 eager us", timeit(lambda: gemm(0, 512, cur(), plan.part[0])))
 print("one chunk K=512 graph us", graph_time(lambda: gemm(0, 512, cur(), plan.part[0])))
