@@ -1,4 +1,5 @@
-"""Per-superstage pipeline timeline of CTA 0 for the c2 conv (debug; BNN_UMMA_DEBUG=16)."""
+"""Per-superstage pipeline timeline of CTA 0 of one bench workload's tcgen05 kernel
+(default c2; `python tools/umma_stages_conv.py c1`; debug trace buffer)."""
 import sys
 import numpy as np
 import torch
@@ -8,7 +9,8 @@ import bench
 import paper_1705_09864_b200 as bnn
 
 lib = bnn.load_library()
-plan, host_x = bench.build_plan("c2", "umma")
+WL = sys.argv[1] if len(sys.argv) > 1 else "c2"
+plan, host_x = bench.build_plan(WL, "umma")
 plan.pack()
 for _ in range(3):
     plan.kernel()
@@ -18,7 +20,7 @@ s.record()
 for _ in range(10):
     plan.kernel()
 e.record(); e.synchronize()
-print(f"c2 conv kernel (eager launches): {s.elapsed_time(e) / 10 * 1e3:.1f} us")
+print(f"{WL} kernel (eager launches): {s.elapsed_time(e) / 10 * 1e3:.1f} us")
 g = torch.cuda.CUDAGraph()
 side = torch.cuda.Stream(); side.wait_stream(torch.cuda.current_stream())
 with torch.cuda.stream(side):
@@ -29,7 +31,7 @@ with torch.cuda.graph(g):
         plan.kernel()
 g.replay(); torch.cuda.synchronize()
 s.record(); g.replay(); e.record(); e.synchronize()
-print(f"c2 conv kernel (graph, back to back): {s.elapsed_time(e) / 10 * 1e3:.1f} us")
+print(f"{WL} kernel (graph, back to back): {s.elapsed_time(e) / 10 * 1e3:.1f} us")
 tr = torch.zeros(8192, dtype=torch.int64, device="cuda")
 lib.bnn_umma_trace(tr.data_ptr())
 torch.cuda.synchronize()
