@@ -95,6 +95,25 @@ def test_conv_and_pack_validation(lib):
     assert lib.bnn_sum_partials_f32(None, 2, 0, 0, 0, 64, None, None) == 0  # empty: no launch
 
 
+def test_host_split_k_ranges(monkeypatch):
+    """DensePlan's opt-in split-K ranges: word-aligned, whole 256-bit superstages,
+    contiguous, covering [0, K) with the tail in the last range only."""
+    from types import SimpleNamespace
+    from paper_1705_09864_b200.plan import DensePlan
+    monkeypatch.delenv("BNN_DENSE_SPLITK", raising=False)
+    assert DensePlan._k_chunks(SimpleNamespace(k=4096)) == [(0, 4096)]  # off by default
+    for splits, k in [(8, 4096), (3, 4096), (2, 1000), (5, 2047), (16, 8192), (4, 200), (7, 64)]:
+        monkeypatch.setenv("BNN_DENSE_SPLITK", str(splits))
+        ch = DensePlan._k_chunks(SimpleNamespace(k=k))
+        assert ch[0][0] == 0 and ch[-1][1] == k
+        assert all(a1 == b0 for (_, a1), (b0, _) in zip(ch[:-1], ch[1:]))
+        assert all(k0 % 256 == 0 and k1 > k0 for k0, k1 in ch)
+        assert all((k1 - k0) % 256 == 0 for k0, k1 in ch[:-1])
+        assert 1 <= len(ch) <= splits
+    monkeypatch.setenv("BNN_DENSE_SPLITK", "8")
+    assert DensePlan._k_chunks(SimpleNamespace(k=4096)) == [(512 * i, 512 * (i + 1)) for i in range(8)]
+
+
 def test_host_gemm_dims_and_workers(monkeypatch):
     from paper_1705_09864_b200 import gemm
     d = gemm.GemmDims(2, 3, 65)
