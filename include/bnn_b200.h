@@ -4,12 +4,17 @@
  *
  * Every entry point takes plain device pointers allocated by the caller
  * (PyTorch in the Python host layer), sizes as int64_t, and an explicit CUDA
- * stream.  Nothing allocates device memory internally, there is no global
- * mutable state apart from the thread-local error message, and every call is
- * asynchronous on `stream`.  Return value: 0 on success, a negative BNN_E*
+ * stream.  Nothing allocates device memory internally, every option is a
+ * per-call argument (engine and tcgen05 variant in `algo`, epilogue in
+ * bnn_epilogue), and every call is asynchronous on `stream`.  The only global
+ * mutable state is the thread-local error message and the DEBUG knobs at the
+ * end of this file (process-wide, not thread-safe, off by default, never set
+ * by the product path).  Return value: 0 on success, a negative BNN_E*
  * code for an invalid argument (the reference raises ValueError for these),
  * or BNN_ECUDA (> 0) when a CUDA launch failed.  bnn_last_error() returns a
  * thread-local message for the last failing call.
+ *
+ * ABI version 2 (bnn_abi_version).
  *
  * Word format (reference bitpack.py:1-16): bit k of a packed vector is bit
  * k % 64 of u64 word k / 64 (LSB-first); bit 1 <=> sign +1, bit 0 <=> -1.
@@ -62,12 +67,28 @@ enum bnn_domain {
     BNN_DOT = 1        /* 2P - K, the signed dot product                    */
 };
 
-/* Inner-product engine.  AUTO picks the measured winner for the shape. */
+/* Inner-product engine.  AUTO picks the measured winner for the shape (the
+ * tcgen05 engine, variant 2).  The explicit tcgen05 variants exist for the
+ * engine contest and as independent parity checks; all results are identical. */
 enum bnn_algo {
     BNN_ALGO_AUTO = 0,
     BNN_ALGO_POPC = 1, /* CUDA cores: LOP3 xor + POPC                        */
-    BNN_ALGO_BMMA = 2, /* warp mma.sync m16n8k256 b1 .and.popc               */
-    BNN_ALGO_UMMA = 3  /* tcgen05.mma kind::i8 on bits expanded in SMEM      */
+    BNN_ALGO_BMMA = 2, /* warp mma.sync m16n8k256 b1 .and.popc (emulated     */
+                       /* on sm_100a: IMMA.U8 subroutine calls)              */
+    BNN_ALGO_UMMA = 3, /* tcgen05.mma on bits expanded in SMEM = variant 2   */
+    /* tcgen05 engine variants (BNN_ALGO_UMMA_V0 + v):
+     *   V0: kind::i8, 128 x 256 tiles, A and B through SMEM
+     *   V1: kind::i8, expanded weights in TMEM, tile N from {128..192}
+     *   V2: kind::mxf4 (e2m1 expansion, 2x the i8 MMA rate) for TMA-fed operands,
+     *       kind::i8 V0/V1 for cp.async-fed shapes (the default)
+     *   V3: kind::mxf4 with the expanded A operand in TMEM (N tiles <= 192)
+     *   V4: V2, and convs with <= 64 filters in the swapped orientation
+     *       (rows = output pixels, 128 x 64 tiles) */
+    BNN_ALGO_UMMA_V0 = 16,
+    BNN_ALGO_UMMA_V1 = 17,
+    BNN_ALGO_UMMA_V2 = 18,
+    BNN_ALGO_UMMA_V3 = 19,
+    BNN_ALGO_UMMA_V4 = 20
 };
 
 /* Flags written (OR-ed) by the pack kernels into a caller int32. */
@@ -233,21 +254,19 @@ int bnn_conv_bn_relu_maxpool_pack_f32_tc(const float *x, int64_t B, int64_t C, i
 
 /* LeNet's float stem as one kernel: y = maxpool_2x2/2(tanh(conv(x, w) + bias))
  * (reference Conv2d -> Tanh -> MaxPool2d, layers.py:81-141, 480-540), the same
- * per-element f32 ops as the unfused sequence; bias may be null.  BNN_EUNSUP
- * outside F == 64, C*kh*kw <= 320, conv width <= 128, W % 4 == 0. */
+ * per-element f32 ops as the unfused sequence; bias may be null.  pool_first = 1
+ * pools before the tanh (exact iff bnn_probe_tanh_monotone reported 0 violations
+ * on this device; measured no faster, so callers pass 0).  BNN_EUNSUP outside
+ * F == 64, C*kh*kw <= 320, conv width <= 128, W % 4 == 0. */
 int bnn_conv_tanh_maxpool2_f32_tc(const float *x, int64_t B, int64_t C, int64_t H, int64_t W,
                                   const float *w, const float *bias, int64_t F, int64_t kh,
                                   int64_t kw, int64_t sh, int64_t sw, int64_t ph, int64_t pw,
-                                  float *y, bnn_stream_t stream);
+                                  int pool_first, float *y, bnn_stream_t stream);
 
 /* Adds to *violations_dev (device u64) the number of adjacent finite floats
  * a < b with tanhf(a) > tanhf(b) (exhaustive, ~4e9 evaluations).  0 means the
  * f32 tanh is monotone, which makes pooling before the tanh exact. */
 int bnn_probe_tanh_monotone(unsigned long long *violations_dev, bnn_stream_t stream);
-
-/* Let bnn_conv_tanh_maxpool2_f32_tc pool before the tanh (exact iff
- * bnn_probe_tanh_monotone reported 0 violations on this device). */
-int bnn_set_tanh_pool_first(int on);
 
 /* Max pooling of sign-packed NHWC words: out bit = OR over the k x k / stride
  * window (no padding) = sign(maxpool(x)) (x >= 0 is monotone: the max is >= 0
@@ -295,17 +314,6 @@ int bnn_bconv2d(const uint64_t *x_words, int64_t B, int64_t C, int64_t H, int64_
                 int64_t ph, int64_t pw, float *y, int domain, const float *scale,
                 const float *shift, int algo, bnn_stream_t stream);
 
-/* Select the tcgen05 engine variant (process-wide tuning knob, default 1):
- * 0 = 128x256 tiles, both expanded operands in SMEM; 1 = 128x192 tiles,
- * expanded weights in TMEM (only activations cross SMEM). */
-int bnn_set_umma_variant(int variant);
-
-/* Debug timeline of the tcgen05 engine: buf is a device array of
- * (#SMs x 16) u64 %globaltimer stamps written by later launches
- * (slot 0 start, 1 setup done, 2 first stage consumed, 3/6/9 tile MMA done,
- * 4/7/10 epilogue start, 5/8/11 epilogue end, 12 exit); null disables. */
-int bnn_umma_trace(uint64_t *buf);
-
 
 /* Roofline probe (synchronous): measured issue rate of a pipe on the
  * current device.  pipe 0 = POPC (32-bit population counts per second);
@@ -320,8 +328,33 @@ int bnn_bconv2d_ex(const uint64_t *x_words, int64_t B, int64_t C, int64_t H, int
                    int64_t sw, int64_t ph, int64_t pw, float *y, const bnn_epilogue *ep, int algo,
                    bnn_stream_t stream);
 
-/* Debug: arm the tcgen05 engine's wait watchdog with a device u64[65] log (a wait that
- * does not complete in ~2 s records block / warp / barrier / parity and traps), or null. */
+/* ------------------------------------------------------------------------
+ * DEBUG knobs.  Process-wide, NOT thread-safe, all off by default; the product
+ * path never sets them (they serve the experiment scripts under tools/).  Some
+ * produce wrong results on purpose (timing ablations).
+ * ------------------------------------------------------------------------ */
+enum bnn_debug_knob {
+    BNN_DEBUG_UMMA_BITS = 1,       /* tcgen05 engine debug bit flags                 */
+    BNN_DEBUG_FP4_BN = 2,          /* force the kind::mxf4 tile N (0 = by shape)     */
+    BNN_DEBUG_PAIR_KW32 = 3,       /* 2-CTA pairs from this K in u32 words (0 = off) */
+    BNN_DEBUG_STEM_BITS = 4,       /* float-stem kernel debug bit flags              */
+    BNN_DEBUG_PACK_PIX = 5,        /* NCHW pack kernel variant (0 = default)         */
+    BNN_DEBUG_PACK_CH = 6,         /* NCHW pack channels per lane (0 = default 8)    */
+    BNN_DEBUG_STEMPOST_SIMPLE = 7  /* unbanded BN/ReLU/maxpool kernel                */
+};
+int bnn_debug_set(int knob, int64_t value);
+
+/* Debug timeline of the tcgen05 engine: buf is a device array of
+ * (#SMs x 16) u64 %globaltimer stamps written by later launches
+ * (slot 0 start, 1 setup done, 2 first stage consumed, 3/6/9 tile MMA done,
+ * 4/7/10 epilogue start, 5/8/11 epilogue end, 12 exit); null disables. */
+int bnn_umma_trace(uint64_t *buf);
+
+/* Debug: arm the tcgen05 engine's wait watchdog (the plain-epilogue kernels) with
+ * a device log of BNN_WATCHDOG_WORDS u64 (word 0 count, 1..64 records of a wait
+ * that did not complete in ~2 s -- block / warp / barrier / parity --, then the
+ * progress marks and raw barrier words; the kernel traps), or null. */
+#define BNN_WATCHDOG_WORDS 225
 int bnn_umma_watchdog(uint64_t *log);
 
 /* Debug: *dst = %globaltimer (ns) when a one-thread kernel on `stream` runs. */

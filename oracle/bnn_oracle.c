@@ -33,8 +33,8 @@ static inline int64_t words_per_bits(int64_t n) { return (n + 63) / 64; }
 
 /* ------------------------------------------------------------------ */
 /* simple static row partition over pthreads: same contract as
- * gemm.py:505-515 (contiguous disjoint spans, result independent of the
- * worker count).                                                       */
+ * xnor_gemm_parallel, gemm.py:254-284 (contiguous disjoint spans,
+ * result independent of the worker count).                             */
 typedef void (*span_fn)(void *ctx, int64_t lo, int64_t hi);
 typedef struct { span_fn fn; void *ctx; int64_t lo, hi; } span_job;
 

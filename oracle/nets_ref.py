@@ -21,10 +21,11 @@ def _np(t):
 
 
 def _conv_f32(x, w, b, stride, pad, threads=None):
+    """stride / pad: (h, w) pairs."""
     n, c, h, ww = x.shape
     f, _, kh, kw = w.shape
-    oh, ow = orc.conv_output_hw(h, ww, kh, kw, (stride, stride), (pad, pad))
-    cols = orc.im2col(x, kh, kw, (stride, stride), (pad, pad), threads)
+    oh, ow = orc.conv_output_hw(h, ww, kh, kw, stride, pad)
+    cols = orc.im2col(x, kh, kw, stride, pad, threads)
     out = w.reshape(f, -1) @ cols
     if b is not None:
         out = out + b[:, None]
@@ -68,7 +69,7 @@ def forward(net, x: np.ndarray, threads=None) -> np.ndarray:
     for layer in net.layers:
         if isinstance(layer, nets.Conv2d):
             x = _conv_f32(x, _np(layer.weight), None if layer.bias is None else _np(layer.bias),
-                          layer.stride, layer.pad, threads)
+                          (layer.sh, layer.sw), (layer.ph, layer.pw), threads)
         elif isinstance(layer, nets.Dense):
             x = x @ _np(layer.weight).T
             if layer.bias is not None:

@@ -18,7 +18,13 @@ LIB_PATH = os.environ.get("BNN_LIB_PATH") or os.path.join(_PKG, "libbnn_b200.so"
 OK, EINVAL, EDIMS, EKEXACT, EPAD, EALIGN, EGEOM, EUNSUP, ECUDA = 0, -1, -2, -3, -4, -5, -6, -7, 1
 POPCOUNT, DOT = 0, 1
 ALGO_AUTO, ALGO_POPC, ALGO_BMMA, ALGO_UMMA = 0, 1, 2, 3
-ALGOS = {"auto": ALGO_AUTO, "popc": ALGO_POPC, "bmma": ALGO_BMMA, "umma": ALGO_UMMA}
+ALGO_UMMA_V0 = 16  # tcgen05 engine variant v = ALGO_UMMA_V0 + v (v in 0..4)
+ALGOS = {"auto": ALGO_AUTO, "popc": ALGO_POPC, "bmma": ALGO_BMMA, "umma": ALGO_UMMA,
+         **{f"umma{v}": ALGO_UMMA_V0 + v for v in range(5)}}
+# debug knobs (bnn_debug_set; process-wide, experiment scripts only)
+DEBUG_UMMA_BITS, DEBUG_FP4_BN, DEBUG_PAIR_KW32, DEBUG_STEM_BITS = 1, 2, 3, 4
+DEBUG_PACK_PIX, DEBUG_PACK_CH, DEBUG_STEMPOST_SIMPLE = 5, 6, 7
+WATCHDOG_WORDS = 225
 FLAG_NONFINITE, FLAG_NOTSIGN, FLAG_RANGE = 1, 2, 4
 GRID_UNSIGNED, GRID_SIGNED = 0, 1
 PACK_SIGN, PACK_STRICT = 0, 1
@@ -46,7 +52,7 @@ SIGNATURES = {
     "bnn_pack_planes_f32": (_i32, [_vp, _i64, _i64, _i64, _i32, _i32, _vp, _i64, _i64, _vp, _vp]),
     "bnn_bitplane_gemm": (_i32, [_vp, _i64, _i64, _i32, _vp, _i64, _i64, _i32, _i32, _i64, _i64,
                                  _i64, _vp, _i64, _i64, _vp]),
-    "bnn_set_umma_variant": (_i32, [_i32]),
+    "bnn_debug_set": (_i32, [_i32, _i64]),
     "bnn_bn_relu_maxpool_f32": (_i32, [_vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _i32, _i32,
                                        _i32, _i32, _vp, _vp]),
     "bnn_conv_bn_relu_maxpool_f32_tc": (_i32, [_vp, _i64, _i64, _i64, _i64, _vp, _i64, _i64, _i64,
@@ -56,9 +62,8 @@ SIGNATURES = {
                                                     _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp,
                                                     _vp, _i32, _vp, _vp, _vp, _vp]),
     "bnn_conv_tanh_maxpool2_f32_tc": (_i32, [_vp, _i64, _i64, _i64, _i64, _vp, _vp, _i64, _i64,
-                                             _i64, _i64, _i64, _i64, _i64, _vp, _vp]),
+                                             _i64, _i64, _i64, _i64, _i64, _i32, _vp, _vp]),
     "bnn_probe_tanh_monotone": (_i32, [_vp, _vp]),
-    "bnn_set_tanh_pool_first": (_i32, [_i32]),
     "bnn_sum_partials_f32": (_i32, [_vp, _i32, _i64, _i64, _i32, _i64, _vp, _vp]),
     "bnn_add_pack_nchw_f32": (_i32, [_vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp]),
     "bnn_maxpool_packed": (_i32, [_vp, _i64, _i64, _i64, _i64, _i32, _i32, _vp, _vp]),

@@ -10,6 +10,7 @@
 namespace bnn {
 
 static thread_local char g_err[512] = "";
+DebugKnobs g_debug;
 
 int set_error(int status, const char *fmt, ...) {
     va_list ap;
@@ -70,7 +71,7 @@ int launch_conv_bn_relu_maxpool_tc(const float *, int64_t, int64_t, int64_t, int
                                    const float *, int64_t, int64_t, int64_t, int64_t, int64_t,
                                    int64_t, int64_t, const float *, const float *, const float *,
                                    const float *, int, float *, cudaStream_t, int, uint64_t *,
-                                   int32_t *);
+                                   int32_t *, int);
 int launch_maxpool_packed(const uint64_t *, int64_t, int64_t, int64_t, int64_t, int, int,
                           uint64_t *, cudaStream_t);
 int launch_add_pack_nchw(const float *, const float *, int64_t, int64_t, int64_t, int64_t, float *,
@@ -92,7 +93,20 @@ static const int64_t kMaxKExact = 1 << 24;  // gemm.py:43-44
 
 extern "C" {
 
-int bnn_abi_version(void) { return 1; }
+int bnn_abi_version(void) { return 2; }
+
+int bnn_debug_set(int knob, int64_t value) {
+    switch (knob) {
+        case BNN_DEBUG_UMMA_BITS: g_debug.umma_bits = value; return BNN_OK;
+        case BNN_DEBUG_FP4_BN: g_debug.fp4_bn = value; return BNN_OK;
+        case BNN_DEBUG_PAIR_KW32: g_debug.pair_kw32 = value; return BNN_OK;
+        case BNN_DEBUG_STEM_BITS: g_debug.stem_bits = value; return BNN_OK;
+        case BNN_DEBUG_PACK_PIX: g_debug.pack_pix = value; return BNN_OK;
+        case BNN_DEBUG_PACK_CH: g_debug.pack_ch = value; return BNN_OK;
+        case BNN_DEBUG_STEMPOST_SIMPLE: g_debug.stempost_simple = value; return BNN_OK;
+        default: return set_error(BNN_EINVAL, "unknown debug knob %d", knob);
+    }
+}
 
 const char *bnn_last_error(void) { return g_err; }
 
@@ -183,6 +197,23 @@ static int check_gemm_dims(int64_t M, int64_t N, int64_t K) {
     return BNN_OK;
 }
 
+// engine of an algo code: POPC / BMMA / UMMA (AUTO and the tcgen05 variants map to
+// UMMA, the variant recorded in ep.variant), or -1 for an unknown code
+static int engine_of(int algo, Epilogue &ep) {
+    if (algo >= BNN_ALGO_UMMA_V0 && algo <= BNN_ALGO_UMMA_V4) {
+        ep.variant = algo - BNN_ALGO_UMMA_V0;
+        return BNN_ALGO_UMMA;
+    }
+    ep.variant = 2;
+    if (algo == BNN_ALGO_AUTO || algo == BNN_ALGO_UMMA) return BNN_ALGO_UMMA;
+    if (algo == BNN_ALGO_POPC || algo == BNN_ALGO_BMMA) return algo;
+    return -1;
+}
+static bool is_umma(int algo) {
+    return algo == BNN_ALGO_AUTO || algo == BNN_ALGO_UMMA ||
+           (algo >= BNN_ALGO_UMMA_V0 && algo <= BNN_ALGO_UMMA_V4);
+}
+
 static void fill_epilogue(Epilogue &ep, const bnn_epilogue *e) {
     ep.scale = e->scale;
     ep.shift = e->shift;
@@ -201,7 +232,7 @@ static int check_pack_out(const bnn_epilogue *e, int64_t M, int algo, const floa
         BNN_REQUIRE(out, BNN_EINVAL, "null pointer");
         return BNN_OK;
     }
-    BNN_REQUIRE(algo == BNN_ALGO_AUTO || algo == BNN_ALGO_UMMA, BNN_EUNSUP,
+    BNN_REQUIRE(is_umma(algo), BNN_EUNSUP,
                 "the fused sign-pack epilogue runs on the tcgen05 engine only");
     BNN_REQUIRE(e->pack_ld >= ceil_div(M, 64), BNN_EALIGN, "pack_ld=%lld smaller than ceil(M/64)=%lld",
                 (long long)e->pack_ld, (long long)ceil_div(M, 64));
@@ -231,14 +262,13 @@ int bnn_xnor_gemm_ex(const uint64_t *A, int64_t lda, const uint64_t *B, int64_t 
     const int64_t tail = (64 * W - K) * (int64_t)(a_pad ^ b_pad);
     Epilogue ep{(int32_t)(K + tail), (int32_t)K, domain, nullptr, nullptr};
     fill_epilogue(ep, e);
-    switch (algo) {
+    switch (engine_of(algo, ep)) {
         case BNN_ALGO_POPC:
             return launch_xnor_gemm_popc(A, lda, B, ldb, M, N, K, C, ldc_m, ldc_n, ep,
                                          as_stream(stream), e->residual);
         case BNN_ALGO_BMMA:
             return launch_xnor_gemm_bmma(A, lda, B, ldb, M, N, K, C, ldc_m, ldc_n, ep,
                                          as_stream(stream), e->residual);
-        case BNN_ALGO_AUTO:
         case BNN_ALGO_UMMA:
             return launch_xnor_gemm_umma(A, lda, B, ldb, M, N, K, C, ldc_m, ldc_n, ep,
                                          as_stream(stream), e->residual);
@@ -332,7 +362,7 @@ int bnn_conv_bn_relu_maxpool_f32_tc(const float *x, int64_t B, int64_t C, int64_
     BNN_REQUIRE(x && w && y && mean && inv_std && gamma && beta, BNN_EINVAL, "null pointer");
     return launch_conv_bn_relu_maxpool_tc(x, B, C, H, W, w, F, kh, kw, sh, sw, ph, pw, mean,
                                           inv_std, gamma, beta, relu, y, as_stream(stream), 0,
-                                          nullptr, nullptr);
+                                          nullptr, nullptr, 0);
 }
 
 int bnn_conv_bn_relu_maxpool_pack_f32_tc(const float *x, int64_t B, int64_t C, int64_t H,
@@ -350,13 +380,13 @@ int bnn_conv_bn_relu_maxpool_pack_f32_tc(const float *x, int64_t B, int64_t C, i
                 "null pointer");
     return launch_conv_bn_relu_maxpool_tc(x, B, C, H, W, w, F, kh, kw, sh, sw, ph, pw, mean,
                                           inv_std, gamma, beta, relu, y, as_stream(stream), 0,
-                                          out_words, flags);
+                                          out_words, flags, 0);
 }
 
 int bnn_conv_tanh_maxpool2_f32_tc(const float *x, int64_t B, int64_t C, int64_t H, int64_t W,
                                   const float *w, const float *bias, int64_t F, int64_t kh,
                                   int64_t kw, int64_t sh, int64_t sw, int64_t ph, int64_t pw,
-                                  float *y, bnn_stream_t stream) {
+                                  int pool_first, float *y, bnn_stream_t stream) {
     BNN_REQUIRE(B >= 0 && C >= 1 && H >= 1 && W >= 1 && F >= 1 && kh >= 1 && kw >= 1 &&
                     sh >= 1 && sw >= 1 && ph >= 0 && pw >= 0 && H + 2 * ph >= kh &&
                     W + 2 * pw >= kw,
@@ -364,7 +394,7 @@ int bnn_conv_tanh_maxpool2_f32_tc(const float *x, int64_t B, int64_t C, int64_t 
     BNN_REQUIRE(x && w && y, BNN_EINVAL, "null pointer");
     return launch_conv_bn_relu_maxpool_tc(x, B, C, H, W, w, F, kh, kw, sh, sw, ph, pw, bias,
                                           nullptr, nullptr, nullptr, 0, y, as_stream(stream), 1,
-                                          nullptr, nullptr);
+                                          nullptr, nullptr, pool_first);
 }
 
 int bnn_maxpool_packed(const uint64_t *in, int64_t B, int64_t H, int64_t W, int64_t Cw, int k,
@@ -434,14 +464,13 @@ int bnn_bconv2d_ex(const uint64_t *x_words, int64_t B, int64_t C, int64_t H, int
     BNN_REQUIRE(H * W * bnn_conv_channel_words(C) < (1ll << 31), BNN_EUNSUP, "image too large");
     Epilogue ep{(int32_t)K, (int32_t)K, domain, nullptr, nullptr};  // all tails are 0
     fill_epilogue(ep, e);
-    switch (algo) {
+    switch (engine_of(algo, ep)) {
         case BNN_ALGO_POPC:
             return launch_bconv2d_popc(x_words, B, C, H, W, w_dev, F, kh, kw, sh, sw, ph, pw, oh,
                                        ow, y, ep, as_stream(stream), e->residual);
         case BNN_ALGO_BMMA:
             return launch_bconv2d_bmma(x_words, B, C, H, W, w_dev, F, kh, kw, sh, sw, ph, pw, oh,
                                        ow, y, ep, as_stream(stream), e->residual);
-        case BNN_ALGO_AUTO:
         case BNN_ALGO_UMMA:
             return launch_bconv2d_umma(x_words, B, C, H, W, w_dev, F, kh, kw, sh, sw, ph, pw, oh,
                                        ow, y, ep, as_stream(stream), e->residual);

@@ -14,6 +14,20 @@ int check_launch(const char *what);
 
 inline cudaStream_t as_stream(bnn_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Debug knobs (bnn_debug_set, include/bnn_b200.h): process-wide, not thread-safe,
+// all 0 by default; the product path never sets them (tools/ experiments only).
+struct DebugKnobs {
+    int64_t umma_bits = 0;      // BNN_DEBUG_UMMA_BITS: tcgen05 engine debug bit flags
+    int64_t fp4_bn = 0;         // BNN_DEBUG_FP4_BN: force the kind::mxf4 tile N
+    int64_t pair_kw32 = 0;      // BNN_DEBUG_PAIR_KW32: 2-CTA pairs from this K (u32 words)
+    int64_t stem_bits = 0;      // BNN_DEBUG_STEM_BITS: stem kernel debug bit flags
+    int64_t pack_pix = 0;       // BNN_DEBUG_PACK_PIX: pack kernel variant (0 = default)
+    int64_t pack_ch = 0;        // BNN_DEBUG_PACK_CH: channels per lane (0 = default 8)
+    int64_t stempost_simple = 0;  // BNN_DEBUG_STEMPOST_SIMPLE: unbanded stem post-op
+    uint64_t *trace_buf = nullptr;  // bnn_umma_trace
+};
+extern DebugKnobs g_debug;
+
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // Epilogue parameters common to the GEMM and conv kernels.
@@ -38,6 +52,9 @@ struct Epilogue {
     uint32_t *pack_out = nullptr;
     int64_t pack_ld32 = 0;
     int32_t *pack_flags = nullptr;
+    // host-side dispatch: tcgen05 engine variant of this call (BNN_ALGO_UMMA_V0 + v;
+    // AUTO / UMMA = 2), read by the launcher only
+    int32_t variant = 2;
     __device__ __forceinline__ float bn(float f, int m) const {
         if (!bn_mean) return f;
         const float xh = __fmul_rn(__fsub_rn(f, __ldg(bn_mean + m)), __ldg(bn_inv + m));

@@ -4,9 +4,6 @@
 
 namespace bnn {
 
-uint64_t *g_trace_buf = nullptr;
-int g_dbg = -1;
-int g_umma_variant = -1;
 
 int launch_xnor_gemm_umma_pk(const uint64_t *A, int64_t lda, const uint64_t *B, int64_t ldb,
                              int64_t M, int64_t N, int64_t K, float *C, int64_t ldc_m,
@@ -58,7 +55,8 @@ int launch_bconv2d_umma(const uint64_t *x, int64_t B, int64_t C, int64_t H, int6
 
 }  // namespace bnn
 
-// debug: arm the wait watchdog (buf = device u64[65]: count, then packed records), or null
+// debug: arm the wait watchdog of this translation unit's kernels (the plain-epilogue
+// instantiations; buf = device u64[BNN_WATCHDOG_WORDS]: count, records, marks), or null
 extern "C" int bnn_umma_watchdog(uint64_t *buf) {
     cudaMemcpyToSymbol(bnn::umma::g_wait_log, &buf, sizeof(buf));
     return bnn::check_launch("bnn_umma_watchdog");
@@ -66,12 +64,6 @@ extern "C" int bnn_umma_watchdog(uint64_t *buf) {
 
 extern "C" int bnn_umma_trace(uint64_t *buf) {
     // debug: buf = device array of (#SMs x 16) u64 timestamps, or null to disable
-    bnn::g_trace_buf = buf;
-    return BNN_OK;
-}
-
-extern "C" int bnn_set_umma_variant(int v) {
-    if (v < 0 || v > 4) return bnn::set_error(BNN_EINVAL, "umma variant must be 0 .. 4");
-    bnn::g_umma_variant = v;
+    bnn::g_debug.trace_buf = buf;
     return BNN_OK;
 }

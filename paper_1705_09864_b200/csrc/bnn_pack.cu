@@ -611,9 +611,11 @@ __global__ void maxpool_packed_kernel(const uint64_t *__restrict__ in, int64_t H
 // torch) and the packed NHWC sign words of y for the next block's convs.  One
 // thread per (pixel, 32-channel word); the warp's threads are consecutive pixels,
 // so every channel plane is read and written in 128-byte runs.
-__global__ void add_pack_nchw_kernel(const float *__restrict__ a, const float *__restrict__ r,
+// (a and y may alias: the networks add in place; every element is read before the
+// same thread writes it, so no __restrict__ on them)
+__global__ void add_pack_nchw_kernel(const float *a, const float *__restrict__ r,
                                      int64_t B, int64_t C, int64_t HW, int64_t cs32,
-                                     float *__restrict__ y, uint32_t *__restrict__ out32,
+                                     float *y, uint32_t *__restrict__ out32,
                                      int32_t *flags) {
     const int64_t gp = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // pixel over B * HW
     const int64_t wi = blockIdx.y;                                        // u32 word in pixel
@@ -707,19 +709,11 @@ int launch_pack_nchw(const float *x, int64_t B, int64_t C, int64_t H, int64_t W,
     uint32_t *o32 = reinterpret_cast<uint32_t *>(out);
     const bool strict = mode == BNN_PACK_STRICT;
     const bool vec4 = (HW % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
-    static int pix = -1;
-    if (pix < 0) {
-        const char *e = getenv("BNN_PACK_PIX");  // 0 (default): direct kernel
-        pix = e ? atoi(e) : 0;
-        if (pix != 0 && pix != 64 && pix != 128 && pix != 256) pix = 0;
-    }
+    int pix = (int)g_debug.pack_pix;  // debug knob; 0 (default): direct kernel
+    if (pix != 0 && pix != 64 && pix != 128 && pix != 256) pix = 0;
     if (pix == 0 && vec4) {
-        static int ch = 0;
-        if (ch == 0) {
-            const char *e = getenv("BNN_PACK_CH");  // channels per lane: 8 (default), 16, 32
-            ch = e ? atoi(e) : 8;
-            if (ch != 8 && ch != 16 && ch != 32) ch = 8;
-        }
+        int ch = (int)g_debug.pack_ch;  // debug knob: channels per lane 8 (default), 16, 32
+        if (ch != 8 && ch != 16 && ch != 32) ch = 8;
         const int64_t threads = ceil_div(B * HW, 4) * (32 / ch);
         dim3 g((unsigned)ceil_div(threads, 256), (unsigned)(2 * Cw));
 #define BNN_QUAD(K)                                                                            \
@@ -786,7 +780,7 @@ int launch_bn_relu_maxpool(const float *x, int64_t B, int64_t C, int64_t H, int6
     const int64_t band_bytes = (((R - 1) * st + k) * W) * 4;
     const int64_t nbands = ceil_div(OH, R);
     if (band_bytes <= 48 * 1024 && OH * OW < (1ll << 31) && H * W < (1ll << 31) &&
-        B * C * nbands <= 0x7fffffffll && !getenv("BNN_STEMPOST_SIMPLE")) {
+        B * C * nbands <= 0x7fffffffll && !g_debug.stempost_simple) {
         bn_relu_maxpool_band_kernel<<<(unsigned)(B * C * nbands), 256, (size_t)band_bytes, s>>>(
             x, (int)C, (int)H, (int)W, mean, inv, gamma, beta, relu, k, st, pd, (int)OH, (int)OW,
             (int)R, (int)nbands, y);

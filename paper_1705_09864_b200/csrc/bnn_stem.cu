@@ -794,15 +794,12 @@ int launch_conv2d_f32_tc(const float *x, int64_t B, int64_t C, int64_t H, int64_
 
 // conv (3xTF32) + BN + ReLU + maxpool 3x3/2/1 fused; BNN_EUNSUP when the shape
 // does not fit (the caller then runs the conv and the post-op separately)
-// set by bnn_set_tanh_pool_first once bnn_probe_tanh_monotone found tanhf monotone
-int g_tanh_pool_first = 0;
-
 int launch_conv_bn_relu_maxpool_tc(const float *x, int64_t B, int64_t C, int64_t H, int64_t W,
                                    const float *w, int64_t F, int64_t kh, int64_t kw, int64_t sh,
                                    int64_t sw, int64_t ph, int64_t pw, const float *mean,
                                    const float *inv, const float *gamma, const float *beta,
                                    int relu, float *y, cudaStream_t s, int mode,
-                                   uint64_t *pack_words, int32_t *pack_flags) {
+                                   uint64_t *pack_words, int32_t *pack_flags, int pool_first) {
     using namespace stem;
     const int64_t K = C * kh * kw;
     const int64_t OH = (H + 2 * ph - kh) / sh + 1, OW = (W + 2 * pw - kw) / sw + 1;
@@ -818,11 +815,8 @@ int launch_conv_bn_relu_maxpool_tc(const float *x, int64_t B, int64_t C, int64_t
     g.mode = mode;
     g.pack16 = mode == 0 ? reinterpret_cast<uint16_t *>(pack_words) : nullptr;
     g.pack_flags = pack_flags;
-    g.pool_first = mode == 1 && g_tanh_pool_first;
-    {
-        const char *e = getenv("BNN_STEM_DEBUG");
-        g.dbg = e ? atoi(e) : 0;
-    }
+    g.pool_first = mode == 1 && pool_first;
+    g.dbg = (int)g_debug.stem_bits;
     g.C = (int)C, g.H = (int)H, g.W = (int)W, g.kh = (int)kh, g.kw = (int)kw, g.sh = (int)sh;
     g.sw = (int)sw, g.ph = (int)ph, g.pw = (int)pw, g.OH = (int)OH, g.OW = (int)OW;
     g.PH = (int)PH, g.PW = (int)PW, g.K = (int)K, g.nch = (int)ceil_div(K, KC);
@@ -876,7 +870,4 @@ int launch_conv_bn_relu_maxpool_tc(const float *x, int64_t B, int64_t C, int64_t
 
 }  // namespace bnn
 
-extern "C" int bnn_set_tanh_pool_first(int on) {
-    bnn::g_tanh_pool_first = on ? 1 : 0;
-    return BNN_OK;
-}
+

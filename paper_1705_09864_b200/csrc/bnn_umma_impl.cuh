@@ -1557,15 +1557,8 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
 
 }  // namespace umma
 
-extern uint64_t *g_trace_buf;  // debug timeline (bnn_umma_trace)
-extern int g_dbg;              // debug: BNN_UMMA_DEBUG bit flags (wrong results)
-static int umma_dbg() {
-    if (g_dbg < 0) {
-        const char *e = getenv("BNN_UMMA_DEBUG");
-        g_dbg = e ? atoi(e) : 0;
-    }
-    return g_dbg;
-}
+// debug bit flags (bnn_debug_set(BNN_DEBUG_UMMA_BITS); some give wrong results)
+static inline int umma_dbg() { return (int)g_debug.umma_bits; }
 
 static int sm_count() {
     static int n = 0;
@@ -1719,11 +1712,11 @@ static int launch_umma_cfg(const ALoad &a_in, const BLoad &b_in, const Store &st
     attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = (kPair || force_cluster) ? 2 : 1;
-    cudaLaunchKernelEx(&cfg, kern, a, b, st, ep, kw32, tmap, g_trace_buf, umma_dbg());
+    cudaLaunchKernelEx(&cfg, kern, a, b, st, ep, kw32, tmap, g_debug.trace_buf, umma_dbg());
     return check_launch("xnor_umma_kernel");
 }
 
-// engine variants (bnn_set_umma_variant / env BNN_UMMA_VARIANT):
+// engine variants (per call: algo = BNN_ALGO_UMMA_V0 + v, carried in Epilogue::variant):
 //   0: 128x256 tiles, u8 expansion, A and B through SMEM (kind::i8)
 //   1: u8 expansion, A in TMEM, B through SMEM (kind::i8), tile N chosen per shape
 //      from {128, 160, 176, 192} to minimise (waves x N) on the SMs of this GPU
@@ -1734,25 +1727,13 @@ static int launch_umma_cfg(const ALoad &a_in, const BLoad &b_in, const Store &st
 //   4: variant 2, and convs with <= 64 filters always in the swapped orientation
 //      (rows = pixels, 128 x 64 tiles); variant 2 takes it only for convs with a
 //      fused shortcut add, where it beats variant 0
-extern int g_umma_variant;
-static int umma_variant() {
-    if (g_umma_variant < 0) {
-        const char *e = getenv("BNN_UMMA_VARIANT");
-        g_umma_variant = e ? atoi(e) : 2;
-    }
-    return g_umma_variant;
-}
 
 static int choose_bn(int64_t M, int64_t N, bool fp4 = false, bool wide = false) {
     static const int cands[] = {192, 176, 160, 128};
     // (small N tiles give small problems enough CTAs: every tile runs the full K loop)
     static const int cands4[] = {224, 208, 192, 176, 160, 128, 96, 64, 32, 16};
     if (fp4) {
-        static int force = -1;  // tuning / debug override of the kind::mxf4 tile N
-        if (force < 0) {
-            const char *e = getenv("BNN_FP4_BN");
-            force = e ? atoi(e) : 0;
-        }
+        const int force = (int)g_debug.fp4_bn;  // tuning / debug override of the tile N
         if (force > 0 && (force <= 224 || wide)) return force;  // (wide tiles: one expander set)
         const int64_t sms = sm_count(), tm = ceil_div(M, umma::BM);
         int best = 192;
@@ -1859,26 +1840,22 @@ static int launch_umma(const ALoad &a, const BLoad &b, const Store &st, const Ep
         // shapes with M <= 64 (e.g. ResNet-18 layer1 convs, 64 filters): measured 1.1-1.4x
         // the A-in-TMEM engine there (tools/l1_variants.sh)
         // (and for every cp.async-fed conv: C % 256 != 0; measured 1.0-1.1x, profiles/r01)
-        const bool small_m = (umma_variant() == 2 || umma_variant() == 4) &&
+        const bool small_m = (ep.variant == 2 || ep.variant == 4) &&
                              (M <= 64 || std::is_same<BLoad, ConvRows>::value) &&
                              !umma::is_tma<ALoad>::value;
-        if (umma_variant() == 0 || small_m)
+        if (ep.variant == 0 || small_m)
             return launch_umma_cfg<256, false, kVec>(a, b, st, ep, M, N, kw32, s);
     }
     if constexpr (umma::is_tma<ALoad>::value) {
-        if (umma_variant() == 3) {
+        if (ep.variant == 3) {
             if (kw32 >= BNN_FP4_SETS_KW32) return launch_fp4_tm<2>(a, b, st, ep, M, N, kw32, s);
             return launch_fp4_tm<1>(a, b, st, ep, M, N, kw32, s);
         }
-        if (umma_variant() == 2 || umma_variant() == 4) {
+        if (ep.variant == 2 || ep.variant == 4) {
             // long K (>= 24 superstages per tile): two expander sets on alternate
             // superstages; short K: one set and 8 epilogue warps (tiles end often)
             // long K and M >= 256: CTA pairs (cta_group::2); long K otherwise: two expander sets
-            static int64_t pair_kw32 = -1;
-            if (pair_kw32 < 0) {
-                const char *e = getenv("BNN_PAIR_KW32");  // tuning / debug override
-                pair_kw32 = e ? atoll(e) : BNN_FP4_PAIR_KW32;
-            }
+            const int64_t pair_kw32 = g_debug.pair_kw32 > 0 ? g_debug.pair_kw32 : BNN_FP4_PAIR_KW32;
             if (kw32 >= pair_kw32 && M >= 2 * umma::BM && !(umma_dbg() & 8192))
                 return launch_fp4_pair(a, b, st, ep, M, N, kw32, s);
             if (kw32 >= BNN_FP4_SETS_KW32) return launch_fp4<2>(a, b, st, ep, M, N, kw32, s);
@@ -1936,7 +1913,7 @@ static int launch_bconv2d_umma_t(const uint64_t *x, int64_t B, int64_t C, int64_
     // im2col TMA: whole 32-byte tap chunks (C % 256 == 0), corner offsets and
     // strides within the tensor-map limits, A-in-TMEM engine (superstages of 2)
     const int64_t up_w = (ow - 1) * sw - pw - (W - 1), up_h = (oh - 1) * sh - ph - (H - 1);
-    const bool im2col = vec4 && cs32 % 8 == 0 && umma_variant() >= 1 && !(umma_dbg() & 256) &&
+    const bool im2col = vec4 && cs32 % 8 == 0 && ep.variant >= 1 && !(umma_dbg() & 256) &&
                         ph <= 128 && pw <= 128 && up_w >= -128 && up_w <= 127 && up_h >= -128 &&
                         up_h <= 127 && sh <= 8 && sw <= 8 && kh <= 128 && kw <= 128;
     if (im2col) {
@@ -1953,7 +1930,7 @@ static int launch_bconv2d_umma_t(const uint64_t *x, int64_t B, int64_t C, int64_
     // instead of half of them (tools/layer_bench.py)
     // (measured on ResNet's layer 1: the swapped route wins with a shortcut add --
     // 333 vs 381 us --, variant 0 without -- 200 vs 242 us; profiles/r01)
-    if (F <= 64 && (umma_variant() == 4 || (umma_variant() == 2 && res != nullptr))) {
+    if (F <= 64 && (ep.variant == 4 || (ep.variant == 2 && res != nullptr))) {
         using ST = typename std::conditional<CS::kPack, ConvStoreTPk, ConvStoreT>::type;
         ST ts{};
         ts.y = y, ts.F = F, ts.ohw = oh * ow, ts.npix = npix, ts.res = res;

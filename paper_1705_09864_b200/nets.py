@@ -51,7 +51,9 @@ class _Lazy:
 class Conv2d(_Lazy):
     """Full-precision convolution (layers.py:81-141), NCHW f32.
 
-    ``engine="tc"`` (default where supported: 64 filters, C*k*k <= 320 -- the
+    ``k``, ``stride`` and ``pad`` are ints or (h, w) pairs, like the reference's
+    ``Conv2d(cin, cout, (kh, kw), stride=(sh, sw), pad=(ph, pw))``.
+    ``engine="tc"`` (default where supported: 64 filters, C*kh*kw <= 320 -- the
     ResNet-18 and LeNet stems): ``bnn_conv2d_f32_tc``, tcgen05 kind::tf32 with a
     three-term hi/lo split (f32 accuracy).  ``engine="cudnn"``: cuDNN f32 with
     TF32 off.  Both modes of a network use the same engine, so the cross-mode
@@ -61,34 +63,69 @@ class Conv2d(_Lazy):
     engine = "tc"
 
     def __init__(self, cin, cout, k, stride=1, pad=0, bias=True, rng=None):
-        self.cin, self.k, self.cout, self.stride, self.pad = cin, k, cout, stride, pad
-        fan_in, fan_out = cin * k * k, cout * k * k
-        self.weight = _uniform_init(rng, (cout, cin, k, k), fan_in, fan_out) if rng is not None \
-            else np.zeros((cout, cin, k, k), np.float32)
+        self.cin, self.cout = cin, cout
+        self.kh, self.kw = _pair(k)
+        self.stride, self.pad = stride, pad
+        fan_in, fan_out = cin * self.kh * self.kw, cout * self.kh * self.kw
+        shape = (cout, cin, self.kh, self.kw)
+        self.weight = _uniform_init(rng, shape, fan_in, fan_out) if rng is not None \
+            else np.zeros(shape, np.float32)
         self.bias = np.zeros(cout, np.float32) if bias else None
 
+    # (stride / pad may be re-assigned as ints or pairs, e.g. by the .bmx reader)
+    @property
+    def sh(self):
+        return _pair(self.stride)[0]
+
+    @property
+    def sw(self):
+        return _pair(self.stride)[1]
+
+    @property
+    def ph(self):
+        return _pair(self.pad)[0]
+
+    @property
+    def pw(self):
+        return _pair(self.pad)[1]
+
+    def output_hw(self, h, w):
+        return ((h + 2 * self.ph - self.kh) // self.sh + 1,
+                (w + 2 * self.pw - self.kw) // self.sw + 1)
+
+    def geometry(self):
+        """(kh, kw, sh, sw, ph, pw) in the C ABI's argument order."""
+        return self.kh, self.kw, self.sh, self.sw, self.ph, self.pw
+
     def tc_supported(self) -> bool:
-        return self.cout == 64 and self.cin * self.k * self.k <= 320
+        return self.cout == 64 and self.cin * self.kh * self.kw <= 320
 
     def forward(self, x, mode=INFER_FLOAT):
         if self.engine == "tc" and self.tc_supported():
             x = x.contiguous()
             b, c, h, w = x.shape
-            oh = (h + 2 * self.pad - self.k) // self.stride + 1
-            ow = (w + 2 * self.pad - self.k) // self.stride + 1
+            oh, ow = self.output_hw(h, w)
             y = torch.empty((b, self.cout, oh, ow), dtype=torch.float32, device=x.device)
             _lib.call("bnn_conv2d_f32_tc", _lib.ptr(x), b, c, h, w, _lib.ptr(self._dev("weight")),
-                      _lib.ptr(self._dev("bias")), self.cout, self.k, self.k, self.stride,
-                      self.stride, self.pad, self.pad, _lib.ptr(y), _lib.stream_ptr())
+                      _lib.ptr(self._dev("bias")), self.cout, *self.geometry(), _lib.ptr(y),
+                      _lib.stream_ptr())
             return y
         prev = torch.backends.cudnn.allow_tf32
         torch.backends.cudnn.allow_tf32 = False
         torch.backends.cudnn.benchmark = True  # fastest exact-fp32 algorithm for the shape
         try:
-            return F.conv2d(x, self._dev("weight"), self._dev("bias"), stride=self.stride,
-                            padding=self.pad)
+            return F.conv2d(x, self._dev("weight"), self._dev("bias"), stride=(self.sh, self.sw),
+                            padding=(self.ph, self.pw))
         finally:
             torch.backends.cudnn.allow_tf32 = prev
+
+
+def _pair(v):
+    if isinstance(v, (tuple, list)):
+        if len(v) != 2:
+            raise ValueError(f"expected an int or an (h, w) pair, got {v!r}")
+        return int(v[0]), int(v[1])
+    return int(v), int(v)
 
 
 class Dense(_Lazy):
@@ -181,13 +218,12 @@ class StemPost:
         exact because the rounded BN + ReLU is monotone per channel."""
         x = x.contiguous()
         b, c, h, w = x.shape
-        oh = (h + 2 * conv.pad - conv.k) // conv.stride + 1
-        ow = (w + 2 * conv.pad - conv.k) // conv.stride + 1
+        oh, ow = conv.output_hw(h, w)
         ph, pw = (oh - 1) // 2 + 1, (ow - 1) // 2 + 1
         y = torch.empty((b, conv.cout, ph, pw), dtype=torch.float32, device=x.device)
         mean, inv, gamma, beta = self.bn.device_params()
-        args = (_lib.ptr(x), b, c, h, w, _lib.ptr(conv._dev("weight")), conv.cout, conv.k,
-                conv.k, conv.stride, conv.stride, conv.pad, conv.pad, _lib.ptr(mean),
+        args = (_lib.ptr(x), b, c, h, w, _lib.ptr(conv._dev("weight")), conv.cout,
+                *conv.geometry(), _lib.ptr(mean),
                 _lib.ptr(inv), _lib.ptr(gamma), _lib.ptr(beta), 1, _lib.ptr(y))
         if pack and conv.cout == 64:  # + the sign-packed words of y for the first block
             words = torch.empty((b, ph, pw, 1), dtype=torch.uint64, device=x.device)
@@ -297,8 +333,8 @@ _TANH_MONOTONE = None
 
 def tanh_is_monotone() -> bool:
     """Exhaustive device check (once per process) that the f32 tanh is monotone, which
-    makes maxpool(tanh(v)) == tanh(maxpool(v)) exact (`bnn_set_tanh_pool_first` lets the
-    fused LeNet stem pool first; measured no faster, so it stays off by default)."""
+    makes maxpool(tanh(v)) == tanh(maxpool(v)) exact (the fused LeNet stem's ``pool_first``
+    argument; measured no faster, so it stays off by default)."""
     global _TANH_MONOTONE
     if _TANH_MONOTONE is None:
         v = torch.zeros(1, dtype=torch.int64, device="cuda")
@@ -307,18 +343,16 @@ def tanh_is_monotone() -> bool:
     return _TANH_MONOTONE
 
 
-def _lenet_stem_forward(conv: "Conv2d", x: torch.Tensor) -> torch.Tensor:
+def _lenet_stem_forward(conv: "Conv2d", x: torch.Tensor, pool_first: bool = False) -> torch.Tensor:
     """maxpool2x2(tanh(conv(x) + b)) in one kernel (bnn_conv_tanh_maxpool2_f32_tc): the
     same per-element f32 ops as the three torch calls, the conv output never written."""
     x = x.contiguous()
     b, c, h, w = x.shape
-    oh = (h + 2 * conv.pad - conv.k) // conv.stride + 1
-    ow = (w + 2 * conv.pad - conv.k) // conv.stride + 1
+    oh, ow = conv.output_hw(h, w)
     y = torch.empty((b, conv.cout, oh // 2, ow // 2), dtype=torch.float32, device=x.device)
     st = _lib.call_status("bnn_conv_tanh_maxpool2_f32_tc", _lib.ptr(x), b, c, h, w,
                           _lib.ptr(conv._dev("weight")), _lib.ptr(conv._dev("bias")), conv.cout,
-                          conv.k, conv.k, conv.stride, conv.stride, conv.pad, conv.pad,
-                          _lib.ptr(y), _lib.stream_ptr())
+                          *conv.geometry(), int(pool_first), _lib.ptr(y), _lib.stream_ptr())
     if st == _lib.EUNSUP:
         return MaxPool2d(2).forward(torch.tanh(conv.forward(x)))
     _lib.check(st, "bnn_conv_tanh_maxpool2_f32_tc")
@@ -449,8 +483,7 @@ def binary_ops_per_image(net: Sequential, chw) -> int:
 
     for layer in net.layers:
         if isinstance(layer, Conv2d):
-            h = (h + 2 * layer.pad - layer.k) // layer.stride + 1
-            w = (w + 2 * layer.pad - layer.k) // layer.stride + 1
+            h, w = layer.output_hw(h, w)
             c = layer.cout
         elif isinstance(layer, (MaxPool2d, StemPost)):
             pl = layer if isinstance(layer, MaxPool2d) else layer.pool

@@ -6,7 +6,8 @@ contiguous slice of B, and the shards are gathered with one
 ``all_gather_into_tensor`` (NCCL over NVLink on the B200 box).  Output is
 N-major ([N, M]) so each shard is one contiguous block and the gather is a
 pure copy -- results are bit-identical for any world size, the GPU analogue of
-the reference's disjoint row partition (gemm.py:505-515, test_gemm.py:52-59).
+the reference's disjoint row partition (xnor_gemm_parallel, gemm.py:254-284;
+test_gemm.py:52-59).
 
 Whole-network inference shards by batch with no collective (replicas).
 
@@ -59,6 +60,9 @@ def nsplit_xnor_gemm(a_rows: torch.Tensor, b_rows: torch.Tensor, k: int, *,
     if n1 > n0:
         compute(a_rows, b_rows[n0:n1], k, local[: n1 - n0])
     if world == 1:
+        if out is not None:
+            out.copy_(local[:n])
+            return out
         return local[:n]
     full = torch.empty((shard * world, m), dtype=torch.float32, device=a_rows.device)
     dist.all_gather_into_tensor(full, local, group=group)

@@ -11,7 +11,6 @@ reference's ValueError on non-finite input (bitpack.py:37-38).
 
 from __future__ import annotations
 
-import os
 
 import torch
 
@@ -28,7 +27,10 @@ class _Plan:
         self.flags_host = torch.zeros(1, dtype=torch.int32).pin_memory()
 
     def check_flags(self):
+        """Raise the reference's ValueError for what the steps since the last check saw,
+        then clear the flag word (the pack kernels only ever OR into it)."""
         f = int(self.flags.item())
+        self.flags.zero_()
         if f & _lib.FLAG_NONFINITE:
             raise ValueError("binarize requires finite inputs")
         if f & _lib.FLAG_NOTSIGN:
@@ -74,6 +76,7 @@ class _Plan:
     def _host_schedule(self, x_host: torch.Tensor, y_host: torch.Tensor):
         chunks = min(self.host_chunks, self.b) if hasattr(self, "run_device_range") else 1
         cur = torch.cuda.current_stream()
+        self.flags.zero_()  # this call's flags only (a memset node inside the graph)
         if chunks <= 1:
             self.x.copy_(x_host, non_blocking=True)
             self.run_device()
@@ -173,7 +176,8 @@ class ConvPlan(_Plan):
 class DensePlan(_Plan):
     """sign+pack rows (bnn_pack_rows_f32) -> xnor GEMM (bnn_xnor_gemm), out [B, units]."""
 
-    def __init__(self, layer: QDense, batch: int, strict: bool = False):
+    def __init__(self, layer: QDense, batch: int, strict: bool = False,
+                 host_splitk: int | None = None):
         self.layer = layer
         self.b = batch
         k = layer.in_features
@@ -187,15 +191,16 @@ class DensePlan(_Plan):
         self._alloc_common()
         self.lib = _lib.load()
         self.m, self.n, self.k = layer.units, batch, k
-        self.chunks = self._k_chunks() if self.algo == _lib.ALGOS["auto"] else [(0, self.k)]
+        self.chunks = self._k_chunks(host_splitk) if self.algo == _lib.ALGOS["auto"] \
+            else [(0, self.k)]
         if len(self.chunks) > 1:
             self.part = torch.empty((len(self.chunks), batch, layer.units), dtype=torch.float32,
                                     device="cuda")
             self._kstreams = [torch.cuda.Stream() for _ in self.chunks]
             self.launches_per_step = 2 + len(self.chunks)
 
-    def _k_chunks(self):
-        """Split-K (opt-in, BNN_DENSE_SPLITK=<ranges>): word-aligned K ranges of
+    def _k_chunks(self, splits):
+        """Host split-K (opt-in, ``host_splitk=<ranges>``): word-aligned K ranges of
         >= 512 bits run as popcount-domain GEMMs on forked streams and
         bnn_sum_partials_f32 adds the exact integer counts (bit-identical to one
         launch).  Meant for GEMMs with too few output tiles to fill the SMs
@@ -205,10 +210,9 @@ class DensePlan(_Plan):
         dominates -- and the engine already spreads config 1 over 128 CTAs
         (128 x 16 tiles), so the forked launches cannot overlap.  Off by default."""
         words = words_per_bits(self.k)
-        env = os.environ.get("BNN_DENSE_SPLITK")
-        if env is None:
+        if splits is None:
             return [(0, self.k)]
-        splits = min(int(env), words // 4)
+        splits = min(int(splits), words // 4)
         if splits < 2:
             return [(0, self.k)]
         step = -(-words // splits)
@@ -339,7 +343,7 @@ def _count_lib_launches(fn) -> int:
     from . import _lib
     n = [0]
     real_call, real_status = _lib.call, _lib.call_status
-    quiet = ("bnn_set_", "bnn_last_error", "bnn_status_string", "bnn_abi_version",
+    quiet = ("bnn_set_", "bnn_debug_set", "bnn_last_error", "bnn_status_string", "bnn_abi_version",
              "bnn_conv_channel_words", "bnn_device_sm_count")
 
     def counted(f):
@@ -373,7 +377,8 @@ class NetPlan(_Plan):
         for layer in net.binary_layers():
             layer.sync_checks = False
             layer.flags = self.flags
-        self.x = torch.empty((batch,) + self.chw, dtype=torch.float32, device="cuda")
+        # zeros, not empty: the warm-up forward below must not see NaN bit patterns
+        self.x = torch.zeros((batch,) + self.chw, dtype=torch.float32, device="cuda")
         self.ops_per_image = binary_ops_per_image(net, self.chw)
         self.y = net.forward(self.x, self.mode)  # (first call: weight re-layouts, probes)
         # this library's kernel launches per step: every C-ABI compute call of a warm

@@ -185,10 +185,46 @@ def gen_bmx(out):
     (out / "golden_bmx.json").write_text(json.dumps(meta, indent=1))
 
 
+def gen_lenet_bmx(out):
+    """The reference's own binary LeNet (layers.build_lenet(binary=True): kernel given as a
+    (5, 5) tuple, MaxPool2d(), QDense 1024 -> 1000) written by its modelio and converted to
+    packed weights; probe probabilities of both modes from the reference's forward."""
+    from bitnn import modelio
+    net = layers.build_lenet(binary=True, seed=0)
+    # BatchNorm running statistics calibrated on a separate batch (the reference's own
+    # train-mode statistics): an untrained net with unit statistics saturates its tanh
+    # and maps every image to the same output
+    rng = np.random.default_rng(11)
+    t = (rng.standard_normal((64, 1, 28, 28)) * 2).astype(np.float32)
+    for layer in net.layers:
+        if isinstance(layer, layers.BatchNorm):
+            c = layer.channels
+            axes = (0, 2, 3) if t.ndim == 4 else (0,)
+            layer.gamma = (0.5 + rng.random(c)).astype(np.float32)
+            layer.beta = (rng.standard_normal(c) * 0.1).astype(np.float32)
+            layer.running_mean = t.mean(axis=axes).astype(np.float32)
+            layer.running_var = (t.var(axis=axes) + 1.0).astype(np.float32)
+        t = layer.forward(t, layers.INFER_FLOAT)
+    fp, pp = out / "_lenet_float.bmx", out / "lenet_packed.bmx"
+    modelio.save_model(net, fp)
+    modelio.convert(fp, pp)
+    fp.unlink()
+    x = (np.random.default_rng(7).standard_normal((4, 1, 28, 28)) * 2).astype(np.float32)
+    packed = modelio.load_model(pp)
+    meta = {"packed_sha256": hashlib.sha256(pp.read_bytes()).hexdigest(),
+            "probe_seed": 7, "probe_shape": [4, 1, 28, 28],
+            "probs_packed": packed.forward(x, layers.INFER_PACKED).tolist(),
+            "probs_float_of_seed0": net.forward(x, layers.INFER_FLOAT).tolist()}
+    (out / "lenet_bmx.json").write_text(json.dumps(meta, indent=1))
+
+
 def main():
     out = HERE
+    only = set(sys.argv[1:])  # optional: names of the generators to run
     for fn in (gen_pack_cases, gen_gemm40, gen_conv, gen_layers, gen_qmath, gen_sweep504,
-               gen_configs, gen_bmx):
+               gen_configs, gen_bmx, gen_lenet_bmx):
+        if only and fn.__name__ not in only:
+            continue
         t0 = time.time()
         fn(out)
         print(f"{fn.__name__}: {time.time() - t0:.1f}s", flush=True)

@@ -49,7 +49,7 @@ def test_library_is_sm100a_only():
 
 
 def test_status_strings(lib):
-    assert lib.bnn_abi_version() == 1
+    assert lib.bnn_abi_version() == 2
     assert lib.bnn_status_string(0) == b"ok"
     assert b"float32" in lib.bnn_status_string(-3)
 
@@ -95,23 +95,20 @@ def test_conv_and_pack_validation(lib):
     assert lib.bnn_sum_partials_f32(None, 2, 0, 0, 0, 64, None, None) == 0  # empty: no launch
 
 
-def test_host_split_k_ranges(monkeypatch):
-    """DensePlan's opt-in split-K ranges: word-aligned, whole 256-bit superstages,
+def test_host_split_k_ranges():
+    """DensePlan's opt-in host split-K ranges: word-aligned, whole 256-bit superstages,
     contiguous, covering [0, K) with the tail in the last range only."""
     from types import SimpleNamespace
     from paper_1705_09864_b200.plan import DensePlan
-    monkeypatch.delenv("BNN_DENSE_SPLITK", raising=False)
-    assert DensePlan._k_chunks(SimpleNamespace(k=4096)) == [(0, 4096)]  # off by default
+    assert DensePlan._k_chunks(SimpleNamespace(k=4096), None) == [(0, 4096)]  # off by default
     for splits, k in [(8, 4096), (3, 4096), (2, 1000), (5, 2047), (16, 8192), (4, 200), (7, 64)]:
-        monkeypatch.setenv("BNN_DENSE_SPLITK", str(splits))
-        ch = DensePlan._k_chunks(SimpleNamespace(k=k))
+        ch = DensePlan._k_chunks(SimpleNamespace(k=k), splits)
         assert ch[0][0] == 0 and ch[-1][1] == k
         assert all(a1 == b0 for (_, a1), (b0, _) in zip(ch[:-1], ch[1:]))
         assert all(k0 % 256 == 0 and k1 > k0 for k0, k1 in ch)
         assert all((k1 - k0) % 256 == 0 for k0, k1 in ch[:-1])
         assert 1 <= len(ch) <= splits
-    monkeypatch.setenv("BNN_DENSE_SPLITK", "8")
-    assert DensePlan._k_chunks(SimpleNamespace(k=4096)) == [(512 * i, 512 * (i + 1)) for i in range(8)]
+    assert DensePlan._k_chunks(SimpleNamespace(k=4096), 8) == [(512 * i, 512 * (i + 1)) for i in range(8)]
 
 
 def test_host_gemm_dims_and_workers(monkeypatch):
@@ -226,7 +223,7 @@ def test_lenet_stem_and_packed_pool_validation(lib):
     assert lib.bnn_maxpool_packed(16, 1, 1, 4, 1, 2, 2, 16, None) == -6  # window taller than H
     assert lib.bnn_maxpool_packed(16, 1, 4, 4, 1, 2, 0, 16, None) == -6  # stride 0
     assert lib.bnn_maxpool_packed(None, 1, 4, 4, 1, 2, 2, 16, None) == -1
-    args = [16, 1, 1, 28, 28, 16, None, 64, 5, 5, 1, 1, 2, 2, 16, None]
+    args = [16, 1, 1, 28, 28, 16, None, 64, 5, 5, 1, 1, 2, 2, 0, 16, None]
     assert lib.bnn_conv_tanh_maxpool2_f32_tc(*args[:5], None, *args[6:]) == -1
     args[7] = 32  # F != 64
     assert lib.bnn_conv_tanh_maxpool2_f32_tc(*args) == -7
@@ -238,7 +235,7 @@ def test_network_launch_counter():
     from paper_1705_09864_b200 import _lib, plan
 
     def step():
-        _lib.call("bnn_set_tanh_pool_first", 0)  # setter: not a launch
+        _lib.call("bnn_debug_set", _lib.DEBUG_FP4_BN, 0)  # setter: not a launch
         for _ in range(3):
             try:  # rejected in validation before any CUDA call, but counted as a launch
                 _lib.call("bnn_maxpool_packed", None, 1, 4, 4, 1, 2, 2, None, None)

@@ -206,15 +206,10 @@ def test_lenet_fused_stem_bit_identical(nets):
     conv.bias = rng.standard_normal(64).astype(np.float32) * 0.1
     x = torch.rand((5, 1, 28, 28), generator=torch.Generator().manual_seed(1)).cuda()
     ref = F.max_pool2d(torch.tanh(conv.forward(x)), 2)
-    from paper_1705_09864_b200 import _lib
     monotone = nets.tanh_is_monotone()
-    try:
-        for pool_first in ([0, 1] if monotone else [0]):  # tanh per element / pool first
-            _lib.call("bnn_set_tanh_pool_first", pool_first)
-            fused = nets._lenet_stem_forward(conv, x)
-            assert fused.shape == ref.shape and torch.equal(fused, ref), pool_first
-    finally:
-        _lib.call("bnn_set_tanh_pool_first", 0)
+    for pool_first in ([False, True] if monotone else [False]):  # tanh per element / pool first
+        fused = nets._lenet_stem_forward(conv, x, pool_first=pool_first)
+        assert fused.shape == ref.shape and torch.equal(fused, ref), pool_first
 
 
 @pytest.mark.parametrize("shape,k", [((3, 14, 14, 1), 2), ((2, 9, 7, 3), 3), ((1, 6, 10, 2), 2)])

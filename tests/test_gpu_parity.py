@@ -23,11 +23,7 @@ ALGOS = ["popc", "bmma", "umma0", "umma1", "umma2", "umma3", "umma4"]
 
 
 def A(algo):
-    """Engine id for the C ABI; umma0/umma1 select the tcgen05 variant first."""
-    if algo.startswith("umma"):
-        from paper_1705_09864_b200 import _lib
-        _lib.call("bnn_set_umma_variant", int(algo[4:]))
-        return "umma"
+    """Engine id for the C ABI: umma<v> = the tcgen05 engine's variant v (per call)."""
     return algo
 
 
@@ -471,10 +467,8 @@ def test_umma_repeat_runs_identical(bnn, variant):
     a = torch.randint(-2**63, 2**63 - 1, (m, k // 64), device="cuda", generator=g).view(torch.uint64)
     b = torch.randint(-2**63, 2**63 - 1, (n, k // 64), device="cuda", generator=g).view(torch.uint64)
     ref = bnn.xnor_rows_gemm(a, b, k, algo="popc")
-    _lib.call("bnn_set_umma_variant", variant)
     for _ in range(12):
-        assert torch.equal(bnn.xnor_rows_gemm(a, b, k, algo="umma"), ref)
-    _lib.call("bnn_set_umma_variant", 2)
+        assert torch.equal(bnn.xnor_rows_gemm(a, b, k, algo=f"umma{variant}"), ref)
 
 
 @pytest.mark.parametrize("which", ["conv", "dense"])
@@ -510,6 +504,21 @@ def test_plan_run_host_pipelined_equals_single_pass(bnn, which):
     assert np.array_equal(outs[0], expect)
     for o in outs[1:]:
         assert np.array_equal(o, outs[0])
+    # a non-finite input raises binarize's ValueError for that call only: the flag word
+    # is cleared per call, so the next finite input runs normally
+    bad = xh.clone().pin_memory()
+    bad.view(-1)[5] = float("nan")
+    yh = torch.empty(plan.y.shape, dtype=torch.float32).pin_memory()
+    with pytest.raises(ValueError, match="finite"):
+        plan.run_host(bad, yh)
+    assert np.array_equal(plan.run_host(xh, yh).numpy(), outs[-1])
+    plan.x.copy_(bad)
+    plan.run_device()
+    with pytest.raises(ValueError, match="finite"):
+        plan.check_flags()
+    plan.x.copy_(xh)
+    plan.run_device()
+    plan.check_flags()  # cleared by the previous check
 
 
 @pytest.mark.parametrize("r,k,pad", [(3, 1, 0), (5, 200, 1), (256, 4096, 0), (7, 1000, 1), (2, 70000, 0)])
@@ -576,6 +585,8 @@ def test_cta_pair_route_bit_exact(bnn, monkeypatch):
     code = (
         "import sys, torch; sys.path.insert(0, '.');"
         "import paper_1705_09864_b200 as bnn; bnn.load_library();"
+        "from paper_1705_09864_b200 import _lib\n"
+        "_lib.call('bnn_debug_set', _lib.DEBUG_PAIR_KW32, 1)\n"
         "ok = True\n"
         "for m, n, k in ((256, 128, 256), (512, 448, 4096), (1000, 1000, 8192), (300, 64, 2048)):\n"
         "    W = (k + 63) // 64; g = torch.Generator(device='cuda').manual_seed(m + n + k)\n"
@@ -583,25 +594,23 @@ def test_cta_pair_route_bit_exact(bnn, monkeypatch):
         "    b = torch.randint(-2**63, 2**63 - 1, (n, W), device='cuda', generator=g).view(torch.uint64)\n"
         "    ok &= torch.equal(bnn.xnor_rows_gemm(a, b, k, algo='umma'), bnn.xnor_rows_gemm(a, b, k, algo='popc'))\n"
         "print('PAIR_OK' if ok else 'PAIR_BAD')")
-    env = dict(os.environ, BNN_PAIR_KW32="1")
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120,
-                       env=env, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert "PAIR_OK" in r.stdout, r.stdout + r.stderr
 
 
 @pytest.mark.parametrize("domain", ["dot", "popcount"])
-def test_dense_plan_split_k_config1(bnn, golden_dir, monkeypatch, domain):
+def test_dense_plan_split_k_config1(bnn, golden_dir, domain):
     """Opt-in split-K: DensePlan runs word-aligned K ranges as GEMMs on forked
     streams and sums the exact counts (bnn_sum_partials_f32).  Bit-identical
     to the reference (golden SHA-256) and to the unsplit launch, eager and
     under CUDA-graph capture."""
     from paper_1705_09864_b200.plan import DensePlan
-    monkeypatch.setenv("BNN_DENSE_SPLITK", "8")
     a, w = wl.config1_inputs()
     layer = bnn.QFullyConnected(4096, 1024, domain=domain)
     layer.weight = w
     layer.pack()
-    plan = DensePlan(layer, a.shape[0])
+    plan = DensePlan(layer, a.shape[0], host_splitk=8)
     assert len(plan.chunks) > 1
     plan.x.copy_(torch.from_numpy(a))
     y = plan.run_device().cpu().numpy()
@@ -621,17 +630,16 @@ def test_dense_plan_split_k_config1(bnn, golden_dir, monkeypatch, domain):
 
 @pytest.mark.parametrize("splits,b,k,u", [(2, 300, 1000, 130), (3, 256, 4096, 1024), (5, 64, 2047, 257),
                                           (16, 129, 8192, 200)])
-def test_dense_plan_split_k_ragged(bnn, monkeypatch, splits, b, k, u):
+def test_dense_plan_split_k_ragged(bnn, splits, b, k, u):
     """Forced split counts over ragged K (tail in the last range only), odd units."""
     from paper_1705_09864_b200.plan import DensePlan
-    monkeypatch.setenv("BNN_DENSE_SPLITK", str(splits))
     rng = np.random.default_rng(splits * 31 + k)
     x = rng.standard_normal((b, k), dtype=np.float32)
     wt = rng.standard_normal((u, k), dtype=np.float32)
     layer = bnn.QFullyConnected(k, u)
     layer.weight = wt
     layer.pack()
-    plan = DensePlan(layer, b)
+    plan = DensePlan(layer, b, host_splitk=splits)
     assert len(plan.chunks) > 1 and plan.chunks[-1][1] == k
     plan.x.copy_(torch.from_numpy(x))
     y = plan.run_device().cpu().numpy()

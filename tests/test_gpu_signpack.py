@@ -67,50 +67,46 @@ CASES = [
 @pytest.mark.parametrize("variant", [2, 1, 0, 4])
 @pytest.mark.parametrize("with_res", [False, True])
 def test_conv_sign_pack_epilogue(bnn, case, variant, with_res):
-    from paper_1705_09864_b200 import _lib
     from paper_1705_09864_b200.layers import PackedNHWC
     b, c, h, w, f, kh, kw, stride, pad, seed = case
-    _lib.call("bnn_set_umma_variant", variant)
-    try:
-        x, wt = wl.conv_case_inputs(case)
-        layer = bnn.QConvolution(c, f, (kh, kw), stride, pad, domain="dot")
-        layer.weight = wt
-        layer.pack()
-        bn = _BN(f, c * kh * kw, seed)
-        oh, ow = layer.output_hw(h, w)
-        res = None
-        if with_res:
-            res = torch.from_numpy(np.random.default_rng(seed + 50).standard_normal(
-                (b, f, oh, ow)).astype(np.float32)).cuda()
-            res.view(-1)[::9] = 0.0
-        xd = torch.from_numpy(x).cuda()
-        plain = layer.forward_fused(xd, bn, residual=res)
-        out = layer.forward_fused(xd, bn, residual=res, pack_out=True)
-        assert isinstance(out, PackedNHWC) and out.shape == (b, f, oh, ow)
-        y = plain.cpu().numpy()
-        assert np.array_equal(out.f32.cpu().numpy(), y)  # f32 output unchanged
-        # the unfused composition: conv -> BN -> (+ res) in the reference op order
-        p = orc.qconv_packed(x, wt, stride, pad).astype(np.float32)
-        ref = 2 * p - np.float32(c * kh * kw)
-        sh = (1, -1, 1, 1)
-        ref = bn.gamma.reshape(sh) * ((ref - bn.mean.reshape(sh)) * bn.inv.reshape(sh)) + \
-            bn.beta.reshape(sh)
-        if with_res:
-            ref = ref + res.cpu().numpy()
-        assert np.array_equal(y, ref.astype(np.float32))
-        words = out.words.cpu().numpy()
-        assert np.array_equal(words, _oracle_pack_nhwc(y))
-        assert np.array_equal(words, bnn.pack_nchw(plain).cpu().numpy())
-        # packed-only output (the f32 tensor is never written)
-        only = layer.forward_fused(xd, bn, residual=res, pack_out=True, f32_out=False)
-        assert only.f32 is None and np.array_equal(only.words.cpu().numpy(), words)
-        # a consumer conv reading the packed words == reading the f32 tensor
-        nxt = bnn.QConvolution(f, 40, (3, 3), (1, 1), (1, 1), domain="dot")
-        nxt.weight = np.random.default_rng(seed + 9).standard_normal((40, f, 3, 3)).astype(np.float32)
-        nxt.pack()
-        assert torch.equal(nxt.forward_fused(only), nxt.forward_fused(plain))
-    finally:
-        _lib.call("bnn_set_umma_variant", 2)
+    x, wt = wl.conv_case_inputs(case)
+    layer = bnn.QConvolution(c, f, (kh, kw), stride, pad, domain="dot")
+    layer.weight = wt
+    layer.pack()
+    layer.algo = f"umma{variant}"
+    bn = _BN(f, c * kh * kw, seed)
+    oh, ow = layer.output_hw(h, w)
+    res = None
+    if with_res:
+        res = torch.from_numpy(np.random.default_rng(seed + 50).standard_normal(
+            (b, f, oh, ow)).astype(np.float32)).cuda()
+        res.view(-1)[::9] = 0.0
+    xd = torch.from_numpy(x).cuda()
+    plain = layer.forward_fused(xd, bn, residual=res)
+    out = layer.forward_fused(xd, bn, residual=res, pack_out=True)
+    assert isinstance(out, PackedNHWC) and out.shape == (b, f, oh, ow)
+    y = plain.cpu().numpy()
+    assert np.array_equal(out.f32.cpu().numpy(), y)  # f32 output unchanged
+    # the unfused composition: conv -> BN -> (+ res) in the reference op order
+    p = orc.qconv_packed(x, wt, stride, pad).astype(np.float32)
+    ref = 2 * p - np.float32(c * kh * kw)
+    sh = (1, -1, 1, 1)
+    ref = bn.gamma.reshape(sh) * ((ref - bn.mean.reshape(sh)) * bn.inv.reshape(sh)) + \
+        bn.beta.reshape(sh)
+    if with_res:
+        ref = ref + res.cpu().numpy()
+    assert np.array_equal(y, ref.astype(np.float32))
+    words = out.words.cpu().numpy()
+    assert np.array_equal(words, _oracle_pack_nhwc(y))
+    assert np.array_equal(words, bnn.pack_nchw(plain).cpu().numpy())
+    # packed-only output (the f32 tensor is never written)
+    only = layer.forward_fused(xd, bn, residual=res, pack_out=True, f32_out=False)
+    assert only.f32 is None and np.array_equal(only.words.cpu().numpy(), words)
+    # a consumer conv reading the packed words == reading the f32 tensor
+    nxt = bnn.QConvolution(f, 40, (3, 3), (1, 1), (1, 1), domain="dot")
+    nxt.weight = np.random.default_rng(seed + 9).standard_normal((40, f, 3, 3)).astype(np.float32)
+    nxt.pack()
+    assert torch.equal(nxt.forward_fused(only), nxt.forward_fused(plain))
 
 
 def _gemm_ex(bnn, a, bw, m, n, k, c, ldc_m, ldc_n, e, algo="auto"):

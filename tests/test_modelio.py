@@ -85,3 +85,45 @@ def test_flipped_tail_bit_is_rejected(tmp_path):
     p.write_bytes(bytes(data))
     with pytest.raises(ModelFormatError, match="padding audit"):
         load_model(p)
+
+
+def test_reference_lenet_file_is_the_reference_bytes():
+    meta = json.load(open(os.path.join(GOLD, "lenet_bmx.json")))
+    data = open(os.path.join(GOLD, "lenet_packed.bmx"), "rb").read()
+    assert hashlib.sha256(data).hexdigest() == meta["packed_sha256"]
+
+
+def test_conv2d_accepts_pairs_like_the_reference():
+    """Reference Conv2d takes (kh, kw) / (sh, sw) / (ph, pw) tuples (layers.py:86-141);
+    the .bmx reader installs them as read (tuples), the builders as ints."""
+    from paper_1705_09864_b200 import nets
+    c = nets.Conv2d(3, 8, (5, 3), stride=(2, 1), pad=(2, 0), bias=False)
+    assert c.weight.shape == (8, 3, 5, 3)
+    assert c.geometry() == (5, 3, 2, 1, 2, 0)
+    assert c.output_hw(28, 28) == (14, 26)
+    c.stride, c.pad = (1, 1), (0, 0)  # as modelio._Conv2d re-assigns them
+    assert c.output_hw(28, 28) == (24, 26)
+    assert nets.Conv2d(1, 64, 5, pad=2).geometry() == (5, 5, 1, 1, 2, 2)
+
+
+@pytest.mark.gpu
+def test_reference_lenet_round_trip_forward():
+    """The reference's own build_lenet(binary=True) -- conv kernel given as a (5, 5) tuple,
+    64 filters, so the tensor-core stem engine runs -- saved and converted by the
+    reference's modelio, loaded here and run in infer_packed mode: probabilities equal to
+    the reference's forward of the same file (float stem / BN / tanh rounding only)."""
+    import paper_1705_09864_b200 as bnn
+    from paper_1705_09864_b200.modelio import load_model
+    meta = json.load(open(os.path.join(GOLD, "lenet_bmx.json")))
+    net = load_model(os.path.join(GOLD, "lenet_packed.bmx"))
+    conv = net.layers[0]
+    assert conv.tc_supported() and conv.geometry() == (5, 5, 1, 1, 0, 0)
+    x = (np.random.default_rng(meta["probe_seed"]).standard_normal(meta["probe_shape"])
+         * 2).astype(np.float32)
+    want = np.array(meta["probs_packed"])
+    probs = net.forward(x, bnn.INFER_PACKED)
+    assert probs.shape == want.shape
+    assert np.array_equal(probs.argmax(1), want.argmax(1))
+    assert np.allclose(probs, want, atol=2e-5, rtol=0)
+    conv.engine = "cudnn"  # the other float engine agrees as well
+    assert np.allclose(net.forward(x, bnn.INFER_PACKED), want, atol=2e-5, rtol=0)

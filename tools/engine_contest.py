@@ -40,7 +40,7 @@ for m, n, k in shapes:
     cells = []
     for name, algo, var in engines:
         if var is not None:
-            lib.bnn_set_umma_variant(var)
+            algo = f"umma{var}"
         big = 2 * m * n * k
         if algo != "umma" and big > 3e12:
             cells.append("—")
@@ -50,5 +50,4 @@ for m, n, k in shapes:
         reps = max(1, min(20, int(2e13 / big)))
         t = timed(lambda: bnn.xnor_rows_gemm(a, b, k, algo=algo, out=out), reps)
         cells.append(f"{big / (t * 1e-3) / 1e12:.0f}{'' if ok else ' (MISMATCH)'}")
-    lib.bnn_set_umma_variant(2)
     print(f"| {m} x {n} x {k} | " + " | ".join(cells) + " |", flush=True)

@@ -8,7 +8,6 @@ import paper_1705_09864_b200 as bnn
 lib = bnn.load_library()
 what = sys.argv[1]
 variant = int(sys.argv[5]) if len(sys.argv) > 5 else 1
-lib.bnn_set_umma_variant(variant)
 if what == "conv":
     import bench
     plan, _ = bench.build_plan("c2", "auto")
@@ -20,6 +19,6 @@ else:
     a = torch.randint(-2**63, 2**63 - 1, (m, W), device="cuda").view(torch.uint64)
     b = torch.randint(-2**63, 2**63 - 1, (n, W), device="cuda").view(torch.uint64)
     for _ in range(3):
-        bnn.xnor_rows_gemm(a, b, k, algo="umma")
+        bnn.xnor_rows_gemm(a, b, k, algo=f"umma{variant}")
 torch.cuda.synchronize()
 print("ok")

@@ -9,6 +9,8 @@ import bench
 import paper_1705_09864_b200 as bnn
 
 lib = bnn.load_library()
+from paper_1705_09864_b200 import _lib  # noqa: E402
+_lib.call("bnn_debug_set", _lib.DEBUG_UMMA_BITS, 16)  # per-superstage stamps of CTAs 0, 1
 WL = sys.argv[1] if len(sys.argv) > 1 else "c2"
 plan, host_x = bench.build_plan(WL, "umma")
 plan.pack()
