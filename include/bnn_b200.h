@@ -23,6 +23,8 @@
  * Reference interface each entry point replaces (paths relative to
  * /root/reference/pkg/src/bitnn):
  *   bnn_binarize_f32        bitpack.binarize              bitpack.py:30-42
+ *   bnn_popcount64          bitpack.popcount64 / popcount64_soft
+ *                                                         bitpack.py:49-66
  *   bnn_pack_rows_f32       bitpack.pack_matrix_a(binarize(x)) / pack_row
  *                                                         bitpack.py:144-149,172-182
  *   bnn_pack_cols_f32       bitpack.pack_matrix_b         bitpack.py:152-169
@@ -120,6 +122,11 @@ int bnn_device_sm_count(void);
  * BNN_FLAG_NONFINITE in *flags (if non-null) when an input is not finite. */
 int bnn_binarize_f32(const float *x, int64_t n, float *out, int32_t *flags,
                      bnn_stream_t stream);
+
+/* bitpack.popcount64 (soft = 0, hardware POPC) / popcount64_soft (soft = 1, the
+ * shift/mask sequence): out[i] = popcount(words[i]) as u8, i < n. */
+int bnn_popcount64(const uint64_t *words, int64_t n, uint8_t *out, int soft,
+                   bnn_stream_t stream);
 
 /* pack_matrix_a(binarize(x)): x [R, K] f32, row stride ldx elements ->
  * out [R, ldo] u64 words (ldo >= ceil(K/64)); tail bits of the last word =

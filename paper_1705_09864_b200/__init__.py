@@ -9,7 +9,7 @@ hand-written sm_100a CUDA kernels in ``libbnn_b200.so`` (C ABI:
 from . import _lib
 from .bitpack import (BitMatrix, WORD_BITS, audit_padding, binarize, dot_xnor_popcount,
                       pack_matrix_a, pack_matrix_b, pack_nchw, pack_row, pack_rows_device,
-                      unpack_row, words_per_bits, words_transpose)
+                      popcount64, popcount64_soft, unpack_row, words_per_bits, words_transpose)
 from .gemm import (KERNEL_IDS, BenchRecord, GemmDims, benchmark_kernel, run_kernel,
                    xnor_gemm_b200, xnor_gemm_base, xnor_gemm_base_soft, xnor_gemm_blocked,
                    xnor_gemm_parallel, xnor_gemm_unrolled, xnor_rows_gemm)

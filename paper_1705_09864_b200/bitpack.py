@@ -291,6 +291,25 @@ def audit_padding(bm: BitMatrix) -> None:
                          f"are not all {bm.pad_fill}")
 
 
+def _popcount64(words, soft: int):
+    was_np = not isinstance(words, torch.Tensor)
+    w = to_device_words(np.asarray(words, dtype=np.uint64) if was_np else words)
+    out = torch.empty(w.shape, dtype=torch.uint8, device=w.device)
+    _lib.call("bnn_popcount64", _lib.ptr(w), w.numel(), _lib.ptr(out), soft, _lib.stream_ptr())
+    return out.cpu().numpy() if was_np else out
+
+
+def popcount64(words):
+    """popcount64 (bitpack.py:49-52): per-element popcount of u64 words (POPC), as u8."""
+    return _popcount64(words, 0)
+
+
+def popcount64_soft(words):
+    """popcount64_soft (bitpack.py:55-66): the shift/mask popcount, bit-identical to
+    ``popcount64`` (the reference pins the two against each other)."""
+    return _popcount64(words, 1)
+
+
 def dot_xnor_popcount(a_words, b_words, n_bits: int) -> int:
     """dot_xnor_popcount (bitpack.py:218-231): agreement count of two packed vectors.
 

@@ -28,6 +28,7 @@ int check_launch(const char *what) {
 
 // engines (defined in the kernel translation units)
 int launch_binarize(const float *, int64_t, float *, int32_t *, cudaStream_t);
+int launch_popcount64(const uint64_t *, int64_t, uint8_t *, int, cudaStream_t);
 int launch_pack_rows(const float *, int64_t, int64_t, int64_t, uint64_t *, int64_t, int, int,
                      int32_t *, int32_t *, cudaStream_t);
 int launch_pack_cols(const float *, int64_t, int64_t, int64_t, uint64_t *, int64_t, int, int,
@@ -136,6 +137,13 @@ int bnn_binarize_f32(const float *x, int64_t n, float *out, int32_t *flags, bnn_
     BNN_REQUIRE(n >= 0, BNN_EINVAL, "n must be non-negative");
     BNN_REQUIRE(n == 0 || (x && out), BNN_EINVAL, "null pointer");
     return launch_binarize(x, n, out, flags, as_stream(stream));
+}
+
+int bnn_popcount64(const uint64_t *words, int64_t n, uint8_t *out, int soft,
+                   bnn_stream_t stream) {
+    BNN_REQUIRE(n >= 0, BNN_EINVAL, "n must be non-negative");
+    BNN_REQUIRE(n == 0 || (words && out), BNN_EINVAL, "null pointer");
+    return launch_popcount64(words, n, out, soft, as_stream(stream));
 }
 
 int bnn_pack_rows_f32(const float *x, int64_t R, int64_t K, int64_t ldx, uint64_t *out,

@@ -645,7 +645,33 @@ __global__ void add_pack_nchw_kernel(const float *a, const float *__restrict__ r
     flush_flags(f, flags);
 }
 
+// popcount64 (bitpack.py:49-52, hardware POPC) and popcount64_soft (:55-66, the
+// shift/mask SWAR sequence with the same constants), one u64 word per thread
+template <bool kSoft>
+__global__ void popcount64_kernel(const uint64_t *__restrict__ w, int64_t n,
+                                  uint8_t *__restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t x = __ldg(w + i);
+        if (kSoft) {
+            x -= (x >> 1) & 0x5555555555555555ull;
+            x = (x & 0x3333333333333333ull) + ((x >> 2) & 0x3333333333333333ull);
+            x = (x + (x >> 4)) & 0x0F0F0F0F0F0F0F0Full;
+            out[i] = (uint8_t)((x * 0x0101010101010101ull) >> 56);
+        } else {
+            out[i] = (uint8_t)__popcll(x);
+        }
+    }
+}
+
 // ================================================================ launchers
+int launch_popcount64(const uint64_t *w, int64_t n, uint8_t *out, int soft, cudaStream_t s) {
+    if (n == 0) return BNN_OK;
+    const int64_t blocks = ceil_div(n, 256) < 4096 ? ceil_div(n, 256) : 4096;
+    if (soft) popcount64_kernel<true><<<(unsigned)blocks, 256, 0, s>>>(w, n, out);
+    else popcount64_kernel<false><<<(unsigned)blocks, 256, 0, s>>>(w, n, out);
+    return check_launch("popcount64_kernel");
+}
 int launch_add_pack_nchw(const float *a, const float *r, int64_t B, int64_t C, int64_t H,
                          int64_t W, float *y, uint64_t *out, int32_t *flags, cudaStream_t s) {
     const int64_t HW = H * W, Cw = ceil_div(C, 64);

@@ -64,6 +64,38 @@ def test_frozen_words_and_sign_convention(bnn):
         bnn.pack_matrix_a(np.ones(4))
 
 
+def test_popcount_hardware_matches_software(bnn):
+    """test_bitpack.py:136-147: POPC == the shift/mask sequence == int.bit_count."""
+    rng = np.random.default_rng(8)
+    words = rng.integers(0, 2**64, size=5000, dtype=np.uint64)
+    words[:4] = [0, 1, 2**64 - 1, 0x8000000000000000]
+    hw = bnn.popcount64(words)
+    sw = bnn.popcount64_soft(words)
+    assert hw.dtype == np.uint8 and hw.shape == words.shape
+    assert np.array_equal(hw, sw)
+    assert np.array_equal(hw, np.bitwise_count(words))
+    for i in range(200):
+        assert int(hw[i]) == int(words[i]).bit_count()
+    dev = torch.from_numpy(words).cuda()
+    assert torch.equal(bnn.popcount64(dev).cpu(), torch.from_numpy(hw))
+
+
+@pytest.mark.parametrize("n", [1, 63, 64, 65, 200, 1000])
+def test_dot_xnor_popcount_pair(bnn, n):
+    """dot_xnor_popcount (bitpack.py:218-231) on the 'a'/'b' packing pair == the
+    agreement count; 2p - n == the +-1 dot product (test_bitpack.py:150-178)."""
+    rng = np.random.default_rng(n)
+    a = rng.choice(np.array([-1.0, 1.0], np.float32), size=n)
+    b = rng.choice(np.array([-1.0, 1.0], np.float32), size=n)
+    aw = bnn.pack_row(a, 0)
+    bw = bnn.pack_row(b, 1)
+    p = bnn.dot_xnor_popcount(aw, bw, n)
+    assert p == int((a == b).sum())
+    assert 2 * p - n == int(np.dot(a, b))
+    with pytest.raises(ValueError):
+        bnn.dot_xnor_popcount(aw[:0] if len(aw) > 1 else np.zeros(2, np.uint64), bw, n)
+
+
 def test_pack_cases_bit_exact(bnn, golden):
     g = golden["pack_cases"]
     i = 0
