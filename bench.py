@@ -1,17 +1,25 @@
 #!/usr/bin/env python
 """Benchmark of the B200 binarise -> bit-pack -> xnor-popcount hot path.
 
-Default workload = BASELINE.json configs[1]: QConvolution 3x3, 256 -> 256
-filters, input 32x256x28x28 f32 ~ N(0,1), stride 1, pad 1 (GEMM view M=256,
-N=32*28*28=25088, K=2304).  A step = sign+pack of the f32 activations
-resident in HBM + the implicit-im2col xnor conv writing f32 NCHW output.
-Metric: binary TOPS = 2*M*N*K / step time (BASELINE.json).
+Default workload = BASELINE.json configs[3]: binary ResNet-18 inference,
+256 x 3 x 224 x 224 f32 ~ N(0,1) images, random-init weights, batch-sharded
+across the GPUs (metric: images/s).  A step = the whole ``infer_packed``
+forward of the resident batch (float stem, every binary conv with its fused
+BN / sign-pack epilogue, residual adds, classifier head), one CUDA graph.
+Other workloads: ``c2`` (configs[1], QConvolution 3x3 256->256 on
+32x256x28x28, binary TOPS = 2MNK / step), ``c1`` (configs[0] QFullyConnected),
+``gemm4096|gemm8192|gemm16384|gemm4096k65536|gemm4096_2bit`` (configs[4]),
+``lenet`` (configs[2]).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                    [--workload c2|c1|gemm4096|gemm8192|gemm16384|gemm4096k65536]
+                    [--workload resnet18|lenet|c2|c1|gemm4096|...]
 
-N > 1 runs under torchrun: every rank runs its own replica of the batch
-(weak scaling, no collective on the data path); time = max over ranks.
+N > 1: one process per GPU over NCCL (launched by torchrun, or by this script
+itself when WORLD_SIZE is unset).  Networks shard the fixed 256 (1024) image
+batch over the ranks (``"scaling": "strong"``, BASELINE configs[3]) and also
+report the weak-scaling figure (every rank a full batch); configs[4] GEMMs
+split N over the ranks and all-gather the output shards (strong); the single
+layers c1 / c2 run one replica per rank (weak).  Time = max over ranks.
 ``--impl reference`` times the reference's CPU algorithm (the pinned oracle
 port, oracle/, all host threads) on the same workload; rank 0 only.
 """
@@ -21,7 +29,9 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -50,20 +60,28 @@ def parse():
     p.add_argument("--steps", type=int, default=30)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=("b200", "reference"), default="b200")
-    p.add_argument("--workload", choices=WORKLOADS, default="c2")
+    p.add_argument("--workload", choices=WORKLOADS, default="resnet18")
     p.add_argument("--algo", default="auto")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    # test hook: gloo ranks sharing the visible GPU(s) (host-staged gathers; no kernel
+    # waits on another rank) to exercise the N > 1 code paths on a one-GPU box
+    p.add_argument("--backend", choices=("nccl", "gloo"), default="nccl")
     return p.parse_args()
 
 
 # ----------------------------------------------------------------- workloads
+SCALING = {"resnet18": "strong", "lenet": "strong", "gemm4096": "strong", "gemm8192": "strong",
+           "gemm16384": "strong", "gemm4096k65536": "strong", "gemm4096_2bit": "strong",
+           "c1": "weak", "c2": "weak"}
+
+
 def workload_desc(name):
     import workloads as wl
     if name in NET_WORKLOADS:
         desc, batch, chw = NET_WORKLOADS[name]
-        return dict(workload=desc + f", batch {batch} per GPU, input {chw} "
-                    + ("U[0,1]" if name == "lenet" else "N(0,1)") + ", random-init weights",
+        return dict(workload=desc + f", batch {batch} " + ("U[0,1]" if name == "lenet" else "N(0,1)")
+                    + f" images {chw}, random-init weights",
                     M=0, N=0, K=0, batch=batch, seed=3 if name == "lenet" else 4)
     if name == "c2":
         c = wl.C2
@@ -87,12 +105,16 @@ def workload_desc(name):
                 batch=n, seed=m + n + k)
 
 
-def build_plan(name, algo):
+def build_plan(name, algo, world=1, rank=0, weak=False):
+    """The workload's plan for this rank.  Networks: this rank's batch shard (strong
+    scaling; ``weak`` = a full batch per rank); configs[4] GEMMs at world > 1: this
+    rank's N shard + all-gather; c1 / c2: one full replica per rank."""
     import torch
 
     import workloads as wl
     import paper_1705_09864_b200 as bnn
-    from paper_1705_09864_b200.plan import ConvPlan, DensePlan, GemmPlan
+    from paper_1705_09864_b200.parallel import shard_bounds
+    from paper_1705_09864_b200.plan import ConvPlan, DensePlan, GemmPlan, NsplitGemmPlan
 
     if name == "c2":
         c = wl.C2
@@ -120,14 +142,15 @@ def build_plan(name, algo):
         from paper_1705_09864_b200 import nets
         from paper_1705_09864_b200.plan import NetPlan
         _, batch, chw = NET_WORKLOADS[name]
+        b0, b1 = (0, batch) if weak else shard_bounds(batch, world, rank)[:2]
         net = nets.lenet_c3(d["seed"]) if name == "lenet" else nets.resnet18_c4(d["seed"])
         net.pack_for_inference()
         g = torch.Generator(device="cuda").manual_seed(d["seed"])
-        plan = NetPlan(net, batch, chw)
-        if name == "lenet":
-            plan.x.copy_(torch.rand(plan.x.shape, device="cuda", generator=g))
-        else:
-            plan.x.copy_(torch.randn(plan.x.shape, device="cuda", generator=g))
+        full = (torch.rand if name == "lenet" else torch.randn)((batch,) + chw, device="cuda",
+                                                             generator=g)
+        plan = NetPlan(net, b1 - b0, chw)
+        plan.x.copy_(full[b0:b1])
+        del full
         return plan, plan.x.cpu().pin_memory()
     if name.endswith("_2bit"):
         from paper_1705_09864_b200.bitpack import pack_planes_device
@@ -137,11 +160,27 @@ def build_plan(name, algo):
         xf = torch.rand((d["N"], d["K"]), device="cuda", generator=g)
         ap = pack_planes_device(wf, 2, "unsigned")
         bp = pack_planes_device(xf, 2, "unsigned")
+        if world > 1:
+            from paper_1705_09864_b200.gemm import bitplane_gemm
+            n0, n1, _ = shard_bounds(d["N"], world, rank)
+            bs = bp[:, n0:n1].contiguous()
+
+            def compute(a_, b_, k_, out):
+                bitplane_gemm(a_, b_, k_, a_grid="unsigned", b_grid="unsigned", out=out,
+                              transpose_out=True)
+            plan = NsplitGemmPlan(ap, bs, d["K"], d["N"], algo=algo)
+            plan.ns._compute = compute
+            return plan, bs.cpu().pin_memory()
         return BitplanePlan(ap, bp, d["K"]), bp.cpu().pin_memory()
     g = torch.Generator(device="cuda").manual_seed(d["seed"])
     W = (d["K"] + 63) // 64
     aw = torch.randint(-2**63, 2**63 - 1, (d["M"], W), device="cuda", generator=g).view(torch.uint64)
     bw = torch.randint(-2**63, 2**63 - 1, (d["N"], W), device="cuda", generator=g).view(torch.uint64)
+    if world > 1:
+        n0, n1, _ = shard_bounds(d["N"], world, rank)
+        bs = bw[n0:n1].clone()
+        del bw
+        return NsplitGemmPlan(aw, bs, d["K"], d["N"], algo=algo), bs.cpu().pin_memory()
     plan = GemmPlan(aw, bw, d["K"], algo=algo)
     return plan, bw.cpu().pin_memory()
 
@@ -322,12 +361,20 @@ def run_reference_arm(args, rank, world):
     line = {
         "impl": "reference", "metric": metric, "value": value, "unit": unit, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / len(times) * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "higher_is_better": True,
+        "scaling": SCALING[name] if args.gpus > 1 else ("strong" if is_net else "weak"),
+        "vs_baseline": None, "dtype": "u64 (xor / popcount words)",
         "data": "synthetic (seeded, BASELINE.json shapes)",
+        # the same config keys and workload as the GPU arm
         "config": {"workload": d["workload"], "M": d["M"], "N": d["N"], "K": d["K"],
-                   "parallelism": "host threads"},
+                   "batch_per_gpu": d["batch"],
+                   "parallelism": f"{os.cpu_count()} host threads (rank 0 only)",
+                   "l2": "n/a (host)", "launch": "host calls", "algo": "reference CPU port"},
         "cpu_baseline": {"value": value, "unit": unit, "cores": os.cpu_count(), "kind": "port",
-                         "sample": desc},
+                         "sample": desc + " (the oracle/ C port of the reference composition; "
+                                          "the Python/numba reference itself cannot travel to "
+                                          "the GPU box and is ~8x slower, so this arm is "
+                                          "conservative)"},
         "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -407,33 +454,13 @@ def pipe_peak(algo, workload="c2"):
                            "(32 bits x {xor, add})", "popc_peak": popc}
 
 
-def run_gpu_arm(args, rank, world, local_rank):
+def _graphs(plan):
+    """(step graph, kernel-only graph) or (None, None) for plans whose step holds a
+    collective (replayed eagerly)."""
     import torch
-    import torch.distributed as dist
-
-    torch.cuda.set_device(local_rank)
-    import paper_1705_09864_b200 as bnn
-    bnn.load_library()
-
-    plan, host_x = build_plan(args.workload, args.algo)
-    d = workload_desc(args.workload)
-    ops = plan.binary_ops
-    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MiB > L2
-    flush_rd = torch.zeros(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
-    flush_sink = torch.empty((), dtype=torch.float32, device="cuda")
-
-    def l2_flush():
-        # write a buffer larger than L2 (evicts every line of this step's data), then
-        # read another one so the dirty lines of the write are written back here, outside
-        # the timed region, instead of inside the next timed kernel (a steady-state L2
-        # holds clean data, not 126 MB of dirty scratch)
-        flush.zero_()
-        torch.amax(flush_rd, dim=0, out=flush_sink)
+    if not getattr(plan, "graph_ok", True):
+        return None, None
     stream = torch.cuda.current_stream()
-
-    # Each step is replayed from a CUDA graph (pack + kernel) so the events time
-    # GPU work only; the kernel alone is a second graph, timed the same way,
-    # for the roofline.  Capture happens on a side stream (torch requirement).
     g_step, g_kern = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
     side = torch.cuda.Stream()
     side.wait_stream(stream)
@@ -444,49 +471,120 @@ def run_gpu_arm(args, rank, world, local_rank):
         plan.run_device()
     with torch.cuda.graph(g_kern):
         plan.kernel()
-    for _ in range(args.warmup):
-        g_step.replay()
-    torch.cuda.synchronize()
+    return g_step, g_kern
 
+
+def _timed_steps(step, steps, l2_flush, world, sampler=None):
+    """Per-step CUDA-event times (ms) on the launching stream, L2 flushed between steps
+    outside the events; barrier + synchronize on both sides of the timed region."""
+    import torch
+    import torch.distributed as dist
+    stream = torch.cuda.current_stream()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
-    evk = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
+          for _ in range(steps)]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local_rank) as clk:
-        for i in range(args.steps):
-            l2_flush()  # L2 flush between timed steps (outside the events)
+    if sampler is not None:
+        sampler.__enter__()
+    try:
+        for i in range(steps):
+            l2_flush()
             s, e = ev[i]
             s.record(stream)
-            g_step.replay()
+            step()
             e.record(stream)
         torch.cuda.synchronize()
+    finally:
+        if sampler is not None:
+            sampler.__exit__(None, None, None)
     if world > 1:
         dist.barrier()
-    for i in range(args.steps):  # kernel alone, same flush discipline
-        l2_flush()
-        s, e = evk[i]
-        s.record(stream)
-        g_kern.replay()
-        e.record(stream)
+    return [s.elapsed_time(e) for s, e in ev]
+
+
+def _max_over_ranks(v, world):
+    import torch
+    import torch.distributed as dist
+    if world == 1:
+        return v
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _kernel_families(plan):
+    """Per-family device time of one network step (NetPlan.kernel_breakdown): the binary
+    convs / GEMMs (xnor_umma_kernel), the float stem, the rest of this library's kernels."""
+    fam = {}
+    for name, ms, ops in plan.kernel_breakdown():
+        if name.startswith(("bnn_bconv2d", "bnn_xnor_gemm")):
+            key = "binary conv / GEMM (xnor_umma_kernel)"
+        elif "f32_tc" in name:
+            key = "float stem (conv_pool_kernel, tcgen05 kind::tf32 x3)"
+        else:
+            key = "other (" + name + ")"
+        f = fam.setdefault(key, {"ms": 0.0, "launches": 0, "binary_ops": 0})
+        f["ms"] += ms
+        f["launches"] += 1
+        f["binary_ops"] += ops
+    return fam
+
+
+def run_gpu_arm(args, rank, world, local_rank):
+    import torch
+
+    torch.cuda.set_device(local_rank % torch.cuda.device_count())
+    import paper_1705_09864_b200 as bnn
+    bnn.load_library()
+
+    name = args.workload
+    is_net = name in NET_WORKLOADS
+    scaling = SCALING[name] if world > 1 else ("strong" if is_net else "weak")
+    plan, host_x = build_plan(name, args.algo, world, rank)
+    d = workload_desc(name)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MiB > L2
+    flush_rd = torch.zeros(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    flush_sink = torch.empty((), dtype=torch.float32, device="cuda")
+
+    def l2_flush():
+        # write a buffer larger than L2 (evicts every line of this step's data), then
+        # read another one so the dirty lines of the write are written back here, outside
+        # the timed region, instead of inside the next timed kernel
+        flush.zero_()
+        torch.amax(flush_rd, dim=0, out=flush_sink)
+
+    # each step is one CUDA-graph replay (the GPU work only); the kernel alone is a second
+    # graph, timed the same way, for the roofline.  Plans whose step holds a collective
+    # (N-split GEMM at world > 1) run eagerly.
+    g_step, g_kern = _graphs(plan)
+    step = g_step.replay if g_step is not None else plan.run_device
+    kern = g_kern.replay if g_kern is not None else plan.kernel
+    for _ in range(args.warmup):
+        step()
     torch.cuda.synchronize()
-    step_ms = [s.elapsed_time(e) for s, e in ev]
-    kern_ms = [s.elapsed_time(e) for s, e in evk]
-    pack_ms = [max(0.0, a - b) for a, b in zip(step_ms, kern_ms)]
-    total_ms = sum(step_ms)
+    clk = ClockSampler(local_rank % torch.cuda.device_count())
+    step_ms = _timed_steps(step, args.steps, l2_flush, world, clk)
+    kern_ms = _timed_steps(kern, args.steps, l2_flush, world)
     plan.check_flags()
-    if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = _max_over_ranks(sum(step_ms), world)
     ms_per_step = total_ms / args.steps
-    is_net = args.workload in NET_WORKLOADS
-    units_per_step = d["batch"] if is_net else ops / 1e12  # images or tera-ops
-    metric = NET_WORKLOADS[args.workload][0] if is_net else METRIC
+    units = d["batch"] if is_net else plan.binary_ops / 1e12  # whole-job images or tera-ops
+    if scaling == "weak" and world > 1:
+        units *= world  # every rank ran a full replica
+    metric = NET_WORKLOADS[name][0] if is_net else METRIC
     unit = "images/s" if is_net else UNIT
-    value = world * units_per_step / (ms_per_step * 1e-3)
+    value = units / (ms_per_step * 1e-3)
+
+    gather = None
+    if isinstance(plan, _nsplit_type()):
+        # the collective alone (the step is GEMM + all-gather)
+        gms = _timed_steps(plan.ns.gather, args.steps, lambda: None, world)
+        gather = {"ms_per_step": _max_over_ranks(statistics.mean(gms), world),
+                  "bytes_per_rank": plan.ns.full.numel() * 4,
+                  "what": "torch.distributed.all_gather_into_tensor (NCCL) of the [N/g, M] f32 "
+                          "output shards"}
 
     # end to end through the public plan API with pinned host buffers
     e2e = None
@@ -494,8 +592,10 @@ def run_gpu_arm(args, rank, world, local_rank):
         y_host = torch.empty(plan.y.shape, dtype=plan.y.dtype).pin_memory()
         for _ in range(2):
             plan.run_host(host_x, y_host)
+        import torch.distributed as dist
         if world > 1:
             dist.barrier()
+        stream = torch.cuda.current_stream()
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
@@ -504,58 +604,125 @@ def run_gpu_arm(args, rank, world, local_rank):
             plan.run_host(host_x, y_host)
         t1.record(stream)
         torch.cuda.synchronize()
-        e2e_ms = t0.elapsed_time(t1)
-        if world > 1:
-            t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = float(t.item())
-        e2e = {"value": world * units_per_step / (e2e_ms / args.steps * 1e-3), "unit": unit,
+        e2e_ms = _max_over_ranks(t0.elapsed_time(t1), world) / args.steps
+        e2e = {"value": units / (e2e_ms * 1e-3), "unit": unit,
                "h2d_bytes_per_step": plan.h2d_bytes, "d2h_bytes_per_step": plan.d2h_bytes,
-               "ms_per_step": e2e_ms / args.steps,
-               "path": "plan.run_host: pinned H2D -> pack -> kernel -> D2H -> sync (one CUDA-graph "
-                       "replay per call, pipelined over "
-                       f"{getattr(plan, 'host_chunks', 1)} batch slices on 3 streams)"}
+               "ms_per_step": e2e_ms,
+               "path": (f"{type(plan).__name__}.run_host: pinned H2D -> pack -> kernels -> "
+                        "D2H -> sync (one CUDA-graph replay per call, pipelined over "
+                        f"{getattr(plan, 'host_chunks', 1)} batch slices on 3 streams)")
+               if getattr(plan, "graph_ok", True) else
+               (f"{type(plan).__name__}.run_host: pinned H2D of this rank's packed B shard -> "
+                "GEMM -> all-gather -> D2H of the full result -> sync (eager)")}
 
-    peak = pipe_peak(args.algo, args.workload)
+    # weak-scaling companion of a strong-scaled network (every rank a full batch)
+    weak = None
+    if is_net and world > 1:
+        wplan, _ = build_plan(name, args.algo, world, rank, weak=True)
+        wg, _ = _graphs(wplan)
+        for _ in range(args.warmup):
+            wg.replay()
+        wms = _timed_steps(wg.replay, args.steps, l2_flush, world)
+        w_ms = _max_over_ranks(sum(wms), world) / args.steps
+        weak = {"value": world * d["batch"] / (w_ms * 1e-3), "unit": unit, "ms_per_step": w_ms,
+                "batch_per_gpu": d["batch"]}
+        del wplan, wg
+
     kern_avg = statistics.mean(kern_ms)
-    achieved = ops / (kern_avg * 1e-3) / 1e12
-    roof = {"bound": peak["bound"], "achieved": achieved, "peak": peak["peak"],
-            "unit": peak["unit"], "frac": achieved / peak["peak"],
-            "traffic": load_traffic(args.workload, args.algo), "kernel_ms": kern_avg,
-            "pack_ms_est": statistics.mean(pack_ms), "peak_source": peak["peak_source"],
-            "ops_per_launch": ops, "popc_pipe_peak_tops": peak["popc_peak"]}
+    ops_rank = getattr(plan, "local_ops", plan.binary_ops)
+    if is_net:
+        fams = _kernel_families(plan)
+        step_dev = sum(f["ms"] for f in fams.values())
+        key = "binary conv / GEMM (xnor_umma_kernel)"
+        bf = fams[key]
+        peak = pipe_peak(args.algo, name)
+        achieved = bf["binary_ops"] / (bf["ms"] * 1e-3) / 1e12
+        roof = {"bound": peak["bound"], "achieved": achieved, "peak": peak["peak"],
+                "unit": peak["unit"], "frac": achieved / peak["peak"],
+                "traffic": load_traffic(name, args.algo),
+                "kernel": key + f": {bf['launches']} launches per step",
+                "kernel_ms": bf["ms"], "ops_per_step": bf["binary_ops"],
+                "share_of_step": bf["ms"] / step_dev,
+                "families": {k: dict(v, share=v["ms"] / step_dev) for k, v in fams.items()},
+                "peak_source": peak["peak_source"], "popc_pipe_peak_tops": peak["popc_peak"],
+                "note": "per-launch CUDA events of one eager step queued behind a sleep kernel "
+                        "(no host gaps inside the intervals); achieved = 2MNK of every binary "
+                        "conv / GEMM launch / their summed device time"}
+    else:
+        peak = pipe_peak(args.algo, name)
+        achieved = ops_rank / (kern_avg * 1e-3) / 1e12
+        roof = {"bound": peak["bound"], "achieved": achieved, "peak": peak["peak"],
+                "unit": peak["unit"], "frac": achieved / peak["peak"],
+                "traffic": load_traffic(name, args.algo), "kernel_ms": kern_avg,
+                "pack_ms_est": statistics.mean(max(0.0, a - b) for a, b in zip(step_ms, kern_ms)),
+                "peak_source": peak["peak_source"], "ops_per_launch": ops_rank,
+                "popc_pipe_peak_tops": peak["popc_peak"]}
     if "cublas_int8_tops" in peak:
         roof["cublas_int8_tops"] = peak["cublas_int8_tops"]
-    if is_net:
-        roof["note"] = ("whole-network step: achieved = binary ops of all binary layers / step "
-                        "time (float stem / classifier / BN / pooling included in the time)")
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args.workload)
+        cpu = cpu_baseline(name)
 
     if rank == 0:
+        if is_net:
+            par = f"batch-sharded dp{world} ({plan.b} images per GPU)" if world > 1 \
+                else f"1 GPU, batch {plan.b}"
+        elif scaling == "strong" and world > 1:
+            par = f"N split over {world} GPUs + NCCL all-gather of the output shards"
+        else:
+            par = f"replicas x{world}"
         line = {
             "metric": metric, "value": value, "unit": unit, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": (("b1 planes -> u8 (tcgen05 kind::i8), s32" if args.workload.endswith("2bit")
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
+            "dtype": (("b1 planes -> u8 (tcgen05 kind::i8), s32" if name.endswith("2bit")
                        else DTYPE) if args.algo in ("auto", "umma") else "u32 (xor/popc words)"),
             "data": "synthetic (seeded, BASELINE.json shapes)",
             "config": {"workload": d["workload"], "M": d["M"], "N": d["N"], "K": d["K"],
-                       "batch_per_gpu": d["batch"], "parallelism": f"replicas x{world}",
+                       "batch_per_gpu": plan.b if is_net else d["batch"], "parallelism": par,
                        "l2": "flushed between timed steps (256 MiB write, then 256 MiB read so the "
                              "write-backs land outside the timed region)",
-                       "launch": "CUDA graph per step (pack + kernel)",
+                       "launch": "CUDA graph per step" if g_step is not None else
+                                 "eager step (kernel + collective)",
                        "algo": args.algo},
             "e2e": e2e, "gpu_launches": plan.launches_per_step * args.steps,
             "roofline": roof, "cpu_baseline": cpu, "clocks": clk.summary(),
         }
+        if weak is not None:
+            line["weak_scaling"] = weak
+        if gather is not None:
+            line["gather"] = gather
         print(json.dumps(line), flush=True)
+
+
+def _nsplit_type():
+    from paper_1705_09864_b200.plan import NsplitGemmPlan
+    return NsplitGemmPlan
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def spawn_ranks(args) -> int:
+    """``bench.py --gpus N`` without a torchrun environment: launch N ranks (one process
+    per GPU) through torch.distributed.run on 127.0.0.1 and return its exit code; rank 0
+    prints the JSON line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
     args = parse()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl != "reference":
+        sys.exit(spawn_ranks(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -565,9 +732,12 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.backend == "nccl":
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group("gloo")
     try:
         run_gpu_arm(args, rank, world, local_rank)
     finally:

@@ -300,6 +300,16 @@ int bnn_add_pack_nchw_f32(const float *a, const float *residual, int64_t B, int6
 int bnn_sum_partials_f32(const float *partials, int splits, int64_t count, int64_t stride,
                          int domain, int64_t K, float *out, bnn_stream_t stream);
 
+/* A network's classifier head, GlobalAvgPool -> Dense (layers.py:266-317):
+ * y[b, o] = sum_c (sum_t x[b, c, t] / HW) * w[o, c] + bias[o] (bias may be null),
+ * x [B, C, HW] f32, w [O, C] f32, y [B, O] f32, pooled: caller scratch of B * C
+ * f32 (receives the channel means).  Each output is summed in a fixed order that
+ * depends only on its own image, so logits are bit-identical for any batch size or
+ * batch shard (multi-GPU batch sharding).  Two launches (pool, classifier). */
+int bnn_avgpool_fc_f32(const float *x, int64_t B, int64_t C, int64_t HW, const float *w,
+                       const float *bias, int64_t O, float *y, float *pooled,
+                       bnn_stream_t stream);
+
 /* Words per pixel of the packed NHWC activation layout: ceil(C / 64). */
 int64_t bnn_conv_channel_words(int64_t C);
 

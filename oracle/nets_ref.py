@@ -61,7 +61,9 @@ def _qfc(layer, x, threads=None):
     return (2 * p - layer.in_features).astype(np.float32) if layer.domain == 1 else p
 
 
-def forward(net, x: np.ndarray, threads=None) -> np.ndarray:
+def forward(net, x: np.ndarray, threads=None, capture=None) -> np.ndarray:
+    """``capture`` (a list) receives every top-level layer's output, like
+    ``Sequential.forward(..., capture=...)``."""
     from paper_1705_09864_b200 import nets
     from paper_1705_09864_b200.layers import QConvolution, QFullyConnected
 
@@ -101,4 +103,6 @@ def forward(net, x: np.ndarray, threads=None) -> np.ndarray:
         else:
             raise TypeError(f"no reference for {type(layer).__name__}")
         x = np.ascontiguousarray(x, np.float32)
+        if capture is not None:
+            capture.append(x)
     return x

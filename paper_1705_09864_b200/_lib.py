@@ -38,6 +38,7 @@ SIGNATURES = {
     "bnn_device_sm_count": (_i32, []),
     "bnn_binarize_f32": (_i32, [_vp, _i64, _vp, _vp, _vp]),
     "bnn_popcount64": (_i32, [_vp, _i64, _vp, _i32, _vp]),
+    "bnn_avgpool_fc_f32": (_i32, [_vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _vp]),
     "bnn_pack_rows_f32": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _i32, _i32, _vp, _vp, _vp]),
     "bnn_pack_cols_f32": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _i32, _i32, _vp, _vp]),
     "bnn_pack_nchw_f32": (_i32, [_vp, _i64, _i64, _i64, _i64, _vp, _i32, _vp, _vp]),

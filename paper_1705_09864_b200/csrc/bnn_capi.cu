@@ -29,6 +29,8 @@ int check_launch(const char *what) {
 // engines (defined in the kernel translation units)
 int launch_binarize(const float *, int64_t, float *, int32_t *, cudaStream_t);
 int launch_popcount64(const uint64_t *, int64_t, uint8_t *, int, cudaStream_t);
+int launch_avgpool_fc(const float *, int64_t, int64_t, int64_t, const float *, const float *,
+                      int64_t, float *, float *, cudaStream_t);
 int launch_pack_rows(const float *, int64_t, int64_t, int64_t, uint64_t *, int64_t, int, int,
                      int32_t *, int32_t *, cudaStream_t);
 int launch_pack_cols(const float *, int64_t, int64_t, int64_t, uint64_t *, int64_t, int, int,
@@ -434,6 +436,16 @@ int bnn_add_pack_nchw_f32(const float *a, const float *residual, int64_t B, int6
     BNN_REQUIRE(B >= 0 && C >= 1 && H >= 1 && W >= 1, BNN_EGEOM, "invalid shape");
     BNN_REQUIRE(B == 0 || (a && residual && y && out_words), BNN_EINVAL, "null pointer");
     return launch_add_pack_nchw(a, residual, B, C, H, W, y, out_words, flags, as_stream(stream));
+}
+
+int bnn_avgpool_fc_f32(const float *x, int64_t B, int64_t C, int64_t HW, const float *w,
+                       const float *bias, int64_t O, float *y, float *pooled,
+                       bnn_stream_t stream) {
+    BNN_REQUIRE(B >= 0 && C >= 1 && HW >= 1 && O >= 1, BNN_EINVAL, "invalid size");
+    BNN_REQUIRE(B < (1ll << 31) && C * HW < (1ll << 31) && O < (1ll << 31), BNN_EUNSUP,
+                "tensor too large");
+    BNN_REQUIRE(B == 0 || (x && w && y && pooled), BNN_EINVAL, "null pointer");
+    return launch_avgpool_fc(x, B, C, HW, w, bias, O, y, pooled, as_stream(stream));
 }
 
 int64_t bnn_conv_channel_words(int64_t C) { return C > 0 ? ceil_div(C, 64) : 0; }

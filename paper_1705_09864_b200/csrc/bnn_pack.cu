@@ -664,7 +664,82 @@ __global__ void popcount64_kernel(const uint64_t *__restrict__ w, int64_t n,
     }
 }
 
+// The classifier head of a network: y[b, o] = sum_c mean_hw(x[b, c]) * w[o, c] + bias[o]
+// (GlobalAvgPool -> Dense, layers.py:266-317).  Every output is computed in one fixed
+// order that depends only on its own image -- channel means summed over hw in order,
+// then lane-strided partial dot products and a fixed shuffle tree -- so an image's
+// logits are bit-identical whatever batch (or batch shard) it is computed in.
+// Pass 1: one thread per (image, channel) mean.  Pass 2: a CTA per (8 images, 64
+// outputs), pooled rows in SMEM, one warp per output row (W rows read coalesced).
+__global__ void avgpool_kernel(const float *__restrict__ x, int64_t BC, int HW,
+                               float *__restrict__ pooled) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= BC) return;
+    const float *p = x + i * HW;
+    float s = 0.0f;
+    for (int t = 0; t < HW; ++t) s = __fadd_rn(s, __ldg(p + t));
+    pooled[i] = __fdiv_rn(s, (float)HW);
+}
+
+template <int kImg, int kOut>
+__global__ void __launch_bounds__(256) fc_rows_kernel(const float *__restrict__ pooled, int B, int C,
+                                                      const float *__restrict__ w,
+                                                      const float *__restrict__ bias, int O,
+                                                      float *__restrict__ y) {
+    extern __shared__ float sp[];  // [kImg][C]
+    const int b0 = blockIdx.x * kImg, o0 = blockIdx.y * kOut;
+    for (int i = threadIdx.x; i < kImg * C; i += blockDim.x) {
+        const int bi = i / C;
+        sp[i] = b0 + bi < B ? pooled[(int64_t)(b0 + bi) * C + (i - bi * C)] : 0.0f;
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int o = o0 + warp; o < o0 + kOut && o < O; o += blockDim.x >> 5) {
+        float acc[kImg];
+#pragma unroll
+        for (int j = 0; j < kImg; ++j) acc[j] = 0.0f;
+        const float *wr = w + (int64_t)o * C;
+        for (int c = lane; c < C; c += 32) {
+            const float wv = __ldg(wr + c);
+#pragma unroll
+            for (int j = 0; j < kImg; ++j) acc[j] = __fmaf_rn(sp[j * C + c], wv, acc[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < kImg; ++j) {
+#pragma unroll
+            for (int d = 16; d >= 1; d >>= 1) acc[j] = __fadd_rn(acc[j], __shfl_xor_sync(0xffffffffu, acc[j], d));
+        }
+        if (lane < kImg && b0 + lane < B) {
+            float v = acc[0];
+#pragma unroll
+            for (int j = 1; j < kImg; ++j)
+                if (lane == j) v = acc[j];
+            if (bias) v = __fadd_rn(v, __ldg(bias + o));
+            y[(int64_t)(b0 + lane) * O + o] = v;
+        }
+    }
+}
+
 // ================================================================ launchers
+int launch_avgpool_fc(const float *x, int64_t B, int64_t C, int64_t HW, const float *w,
+                      const float *bias, int64_t O, float *y, float *pooled, cudaStream_t s) {
+    if (B == 0) return BNN_OK;
+    constexpr int kImg = 8, kOut = 64;
+    const size_t smem = (size_t)kImg * C * sizeof(float);
+    if (smem > 200 * 1024) return set_error(BNN_EUNSUP, "avgpool_fc: too many channels");
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(fc_rows_kernel<kImg, kOut>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             200 * 1024);
+        configured = true;
+    }
+    avgpool_kernel<<<(unsigned)ceil_div(B * C, 256), 256, 0, s>>>(x, B * C, (int)HW, pooled);
+    int rc = check_launch("avgpool_kernel");
+    if (rc) return rc;
+    dim3 g((unsigned)ceil_div(B, kImg), (unsigned)ceil_div(O, kOut));
+    fc_rows_kernel<kImg, kOut><<<g, 256, smem, s>>>(pooled, (int)B, (int)C, w, bias, (int)O, y);
+    return check_launch("fc_rows_kernel");
+}
 int launch_popcount64(const uint64_t *w, int64_t n, uint8_t *out, int soft, cudaStream_t s) {
     if (n == 0) return BNN_OK;
     const int64_t blocks = ceil_div(n, 256) < 4096 ? ceil_div(n, 256) : 4096;

@@ -196,6 +196,21 @@ class GlobalAvgPool:
         return x.mean(dim=(2, 3))
 
 
+def avgpool_dense(x: torch.Tensor, dense: "Dense") -> torch.Tensor:
+    """GlobalAvgPool -> Dense as one kernel (bnn_avgpool_fc_f32), used in both modes:
+    each image's logits are summed in an order of their own, so batch shards of a
+    network (multi-GPU batch sharding) reproduce the one-GPU logits bit for bit."""
+    x = x.contiguous()
+    b, c, h, w = x.shape
+    wt = dense._dev("weight")
+    y = torch.empty((b, wt.shape[0]), dtype=torch.float32, device=x.device)
+    pooled = torch.empty((b, c), dtype=torch.float32, device=x.device)
+    _lib.call("bnn_avgpool_fc_f32", _lib.ptr(x), b, c, h * w, _lib.ptr(wt),
+              _lib.ptr(dense._dev("bias")), wt.shape[0], _lib.ptr(y), _lib.ptr(pooled),
+              _lib.stream_ptr())
+    return y
+
+
 class StemPost:
     """BatchNorm -> ReLU -> MaxPool of a full-precision stem as one kernel in
     ``infer_packed`` mode (bnn_bn_relu_maxpool_f32, bit-identical); the three
@@ -267,6 +282,12 @@ class Sequential:
             nxt = self.layers[i + 1] if i + 1 < n else None
             if isinstance(x, PackedNHWC) and not isinstance(layer, BinaryBasicBlock):
                 x = x.float()  # a float consumer of a packed activation
+            if isinstance(layer, GlobalAvgPool) and isinstance(nxt, Dense) and x.dim() == 4:
+                x = avgpool_dense(x, nxt)  # classifier head, one kernel (both modes)
+                if capture is not None:
+                    capture += [None, x]
+                i += 2
+                continue
             if mode == INFER_PACKED and self.fuse_stem and _lenet_stem(self.layers[i:i + 3]):
                 x = _lenet_stem_forward(self.layers[i], x)  # conv + tanh + maxpool, one kernel
                 if capture is not None:

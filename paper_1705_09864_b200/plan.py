@@ -346,10 +346,12 @@ def _count_lib_launches(fn) -> int:
     quiet = ("bnn_set_", "bnn_debug_set", "bnn_last_error", "bnn_status_string", "bnn_abi_version",
              "bnn_conv_channel_words", "bnn_device_sm_count")
 
+    kernels_per_call = {"bnn_avgpool_fc_f32": 2}  # entry points launching > 1 kernel
+
     def counted(f):
         def wrap(name, *args):
             if not name.startswith(quiet):
-                n[0] += 1
+                n[0] += kernels_per_call.get(name, 1)
             return f(name, *args)
         return wrap
 
@@ -399,3 +401,104 @@ class NetPlan(_Plan):
 
     def run_device(self):
         return self.kernel()
+
+    # end to end: the batch is pipelined over slices (images are independent; the
+    # classifier head's per-image order makes every slice's logits equal the full
+    # batch's), H2D of slice i+1 under the forward of slice i
+    host_chunks = 4
+
+    def run_device_range(self, i0: int, i1: int, stream: int):
+        """Forward of images [i0, i1) on the current stream (the caller's context)."""
+        out = self.net.forward(self.x[i0:i1], self.mode)
+        self.y[i0:i1].copy_(out)
+
+    def kernel_breakdown(self):
+        """One forward with CUDA events around every C-ABI compute call, measured on the
+        launching stream while a leading sleep kernel holds the GPU until the whole
+        forward is queued (so no host launch gap lands inside an interval).  Returns
+        [(entry point, ms, binary ops)]; binary ops for the GEMM / conv calls (2MNK),
+        0 otherwise."""
+        from . import _lib
+        recs = []
+        real_call, real_status = _lib.call, _lib.call_status
+        quiet = ("bnn_set_", "bnn_debug_set", "bnn_last_error", "bnn_status_string",
+                 "bnn_abi_version", "bnn_conv_channel_words", "bnn_device_sm_count")
+
+        def ops_of(name, a):
+            if name.startswith("bnn_bconv2d"):
+                B, C, H, W, F, kh, kw, sh, sw, ph, pw = a[1:5] + a[6:13]
+                oh, ow = (H + 2 * ph - kh) // sh + 1, (W + 2 * pw - kw) // sw + 1
+                return 2 * F * B * oh * ow * C * kh * kw
+            if name.startswith("bnn_xnor_gemm"):
+                return 2 * a[4] * a[5] * a[6]
+            return 0
+
+        def timed(f):
+            def wrap(name, *a):
+                if name.startswith(quiet):
+                    return f(name, *a)
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s.record()
+                r = f(name, *a)
+                e.record()
+                recs.append((name, s, e, ops_of(name, a)))
+                return r
+            return wrap
+
+        torch.cuda.synchronize()
+        torch.cuda._sleep(200_000_000)  # ~0.1 s at ~2 GHz: the forward queues behind it
+        _lib.call, _lib.call_status = timed(real_call), timed(real_status)
+        try:
+            self.net.forward(self.x, self.mode)
+        finally:
+            _lib.call, _lib.call_status = real_call, real_status
+        torch.cuda.synchronize()
+        return [(n, s.elapsed_time(e), ops) for n, s, e, ops in recs]
+
+
+class NsplitGemmPlan(_Plan):
+    """Config-5 GEMM on N GPUs: this rank's N shard of the packed
+    activations, one tcgen05 GEMM into its N-major [shard, M] output, then one
+    all-gather of the shards into the full [N, M] result on every rank
+    (parallel.NsplitGemm).  Bit-identical to the one-GPU GEMM for any world size."""
+
+    launches_per_step = 1
+    graph_ok = False  # the step contains a collective: replayed eagerly
+
+    def __init__(self, a_rows: torch.Tensor, b_shard: torch.Tensor, k: int, n_total: int,
+                 algo="auto", group=None):
+        from .parallel import NsplitGemm
+        self.ns = NsplitGemm(a_rows, b_shard, k, n_total, group=group, algo=algo)
+        self.m, self.n, self.k = self.ns.m, n_total, k
+        self.x = b_shard
+        self.y = self.ns.full[:n_total]
+        self.b = b_shard.shape[-2]
+        self._alloc_common()
+        self.gather_ms = []
+
+    @property
+    def binary_ops(self) -> int:
+        return 2 * self.m * self.n * self.k  # whole-job work (all shards)
+
+    @property
+    def local_ops(self) -> int:
+        return 2 * self.m * (self.ns.n1 - self.ns.n0) * self.k
+
+    def pack(self, stream=None):
+        pass
+
+    def kernel(self, stream=None):
+        self.ns.compute()
+
+    def run_device(self):
+        self.ns.compute()
+        return self.ns.gather()
+
+    def run_host(self, x_host: torch.Tensor, y_host: torch.Tensor) -> torch.Tensor:
+        """H2D of this rank's packed B shard, GEMM, all-gather, D2H of the full [N, M]
+        result; eager (no graph around the collective)."""
+        self.x.copy_(x_host, non_blocking=True)
+        self.run_device()
+        y_host.copy_(self.y[: self.n], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return y_host

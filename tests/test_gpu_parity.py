@@ -357,8 +357,12 @@ def test_config2_qconv_golden(bnn, golden_dir, algo):
     assert _sha(y) == cfg["sha256"]
 
 
-@pytest.mark.parametrize("algo", ALGOS)
-@pytest.mark.parametrize("mnk", [(4096, 4096, 4096), (4096, 4096, 65536), (8192, 8192, 8192)])
+LARGE = ([(a, mnk) for a in ALGOS for mnk in [(4096, 4096, 4096), (4096, 4096, 65536),
+                                             (8192, 8192, 8192)]] +
+         [(a, (16384, 16384, 16384)) for a in ("umma2", "popc")])  # BASELINE configs[4]
+
+
+@pytest.mark.parametrize("algo,mnk", LARGE)
 def test_large_gemm_properties(bnn, algo, mnk):
     """Full-size C5 shapes: exact row/column checksums + sampled exact entries.
 
@@ -373,6 +377,7 @@ def test_large_gemm_properties(bnn, algo, mnk):
     c = bnn.xnor_rows_gemm(aw, bw, k, algo=A(algo))
     assert float(c.min()) >= 0 and float(c.max()) <= k
     a_np, b_np = aw.cpu().numpy(), bw.cpu().numpy()
+    del aw, bw
 
     def bits(x, lo, hi):
         return np.unpackbits(x[lo:hi].view(np.uint8), axis=1, bitorder="little")
@@ -388,16 +393,16 @@ def test_large_gemm_properties(bnn, algo, mnk):
             out.append(bits(x, lo, lo + 1024).astype(np.float64) @ coef)
         return (np.concatenate(out) + float((n_other - ones).sum())).astype(np.int64)
 
-    row_got = c.to(torch.float64).sum(1).cpu().numpy().astype(np.int64)
+    row_got = c.sum(1, dtype=torch.float64).cpu().numpy().astype(np.int64)
     assert np.array_equal(row_got, side_sums(a_np, b_np, n))
-    col_got = c.to(torch.float64).sum(0).cpu().numpy().astype(np.int64)
+    col_got = c.sum(0, dtype=torch.float64).cpu().numpy().astype(np.int64)
     assert np.array_equal(col_got, side_sums(b_np, a_np, m))
     rng = np.random.default_rng(0)
     idx_m, idx_n = rng.integers(0, m, 64), rng.integers(0, n, 64)
-    cs = c.cpu().numpy()
-    for i, j in zip(idx_m, idx_n):
+    got = c[torch.from_numpy(idx_m).cuda(), torch.from_numpy(idx_n).cuda()].cpu().numpy()
+    for v, i, j in zip(got, idx_m, idx_n):
         x = int(np.bitwise_count(a_np[i] ^ b_np[j]).sum())
-        assert cs[i, j] == k - x
+        assert v == k - x
 
 
 # ------------------------------------------------------------------ multi-bit (bit planes)
@@ -449,9 +454,10 @@ def test_bitplane_gemm_matches_reference_float64(bnn, golden):
     assert np.all(np.abs(y - ref) <= 1e-5 * np.maximum(1.0, np.abs(ref)))
 
 
-@pytest.mark.parametrize("m,n,k", [(40, 64, 96), (300, 257, 1000), (1024, 512, 4096)])
-@pytest.mark.parametrize("grids", [("signed", "signed"), ("unsigned", "unsigned"),
-                                   ("signed", "unsigned")])
+@pytest.mark.parametrize("m,n,k,grids", [
+    (m, n, k, g) for m, n, k in [(40, 64, 96), (300, 257, 1000), (1024, 512, 4096)]
+    for g in [("signed", "signed"), ("unsigned", "unsigned"), ("signed", "unsigned")]] +
+    [(4096, 4096, 4096, ("unsigned", "unsigned"))])  # BASELINE configs[4] 2-bit at full size
 def test_bitplane_gemm_exact_integer_decode(bnn, m, n, k, grids):
     rng = np.random.default_rng(m + n + k)
     ga, gb = grids
@@ -464,7 +470,8 @@ def test_bitplane_gemm_exact_integer_decode(bnn, m, n, k, grids):
     ca, cb = _codes_np(w, ga), _codes_np(x, gb)
     aa, ba = (2, -3) if ga == "signed" else (1, 0)
     ab, bb = (2, -3) if gb == "signed" else (1, 0)
-    num = (aa * ca + ba) @ (ab * cb + bb).T  # exact int64
+    # exact integer numerator (float64 BLAS: every partial sum < 2^53)
+    num = (aa * ca + ba).astype(np.float64) @ (ab * cb + bb).astype(np.float64).T
     exact = num / 9.0
     assert np.all(np.abs(y - exact) <= 2e-7 * np.maximum(1.0, np.abs(exact))), (m, n, k)
 

@@ -16,7 +16,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1705_09864_b200.parallel import batch_shard, nsplit_xnor_gemm, shard_bounds
+from paper_1705_09864_b200.parallel import NsplitGemm, batch_shard, nsplit_xnor_gemm, shard_bounds
 
 
 def _free_port():
@@ -46,12 +46,16 @@ def _worker(rank, world, port, m, n, k, seed, q):
             a[:, -1] &= (1 << (k % 64)) - 1
             b[:, -1] &= (1 << (k % 64)) - 1
         c = nsplit_xnor_gemm(a, b, k, compute=_oracle_compute)
+        n0, n1, _ = shard_bounds(n, world, rank)
+        plan = NsplitGemm(a, b[n0:n1], k, n, compute=_oracle_compute)  # the bench's step
+        c2 = plan.run()
+        assert torch.equal(c, c2)
         q.put((rank, c.numpy().copy()))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("m,n,k", [(8, 13, 130), (5, 2, 64), (16, 31, 1000)])
+@pytest.mark.parametrize("m,n,k", [(8, 13, 130), (5, 2, 64), (16, 31, 1000), (3, 1, 70)])
 def test_nsplit_matches_single_process(m, n, k):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -94,3 +98,23 @@ def test_shard_bounds_partition():
     assert batch_shard(256, 8, 7) == (224, 256)
     with pytest.raises(ValueError):
         shard_bounds(10, 2, 2)
+
+
+def test_bench_self_launch_command(monkeypatch):
+    """``bench.py --gpus N`` without WORLD_SIZE re-launches itself as N ranks through
+    torch.distributed.run on 127.0.0.1 (the driver's own launch line)."""
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import bench
+    seen = {}
+    monkeypatch.setattr(bench.subprocess, "call", lambda cmd: seen.setdefault("cmd", cmd) and 0)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--steps", "3"])
+    args = bench.parse()
+    assert args.workload == "resnet18" and args.gpus == 4
+    bench.spawn_ranks(args)
+    cmd = seen["cmd"]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"]
+    assert "--nproc-per-node=4" in cmd and "--master-addr=127.0.0.1" in cmd
+    assert cmd[-4:] == ["--gpus", "4", "--steps", "3"]
+    assert bench.SCALING["resnet18"] == "strong" and bench.SCALING["c2"] == "weak"
