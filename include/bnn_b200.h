@@ -335,7 +335,8 @@ int bnn_bconv2d(const uint64_t *x_words, int64_t B, int64_t C, int64_t H, int64_
 /* Roofline probe (synchronous): measured issue rate of a pipe on the
  * current device.  pipe 0 = POPC (32-bit population counts per second);
  * pipe 1 = dense tcgen05.mma kind::i8 and pipe 2 = kind::mxf4 (MACs per
- * second, one CTA per SM issuing 128x256 MMAs back to back).
+ * second, one CTA per SM issuing 128x256 MMAs back to back); pipes 3 / 4 / 5 =
+ * kind::mxf4 128x64 with A in TMEM / 128x64 from SMEM / 128x256 with A in TMEM.
  * `sink` is a caller-allocated device u32 the kernel may write. */
 int bnn_probe_pipe_peak(int pipe, int64_t iters, uint32_t *sink, double *ops_per_sec,
                         bnn_stream_t stream);
@@ -357,7 +358,8 @@ enum bnn_debug_knob {
     BNN_DEBUG_STEM_BITS = 4,       /* float-stem kernel debug bit flags              */
     BNN_DEBUG_PACK_PIX = 5,        /* NCHW pack kernel variant (0 = default)         */
     BNN_DEBUG_PACK_CH = 6,         /* NCHW pack channels per lane (0 = default 8)    */
-    BNN_DEBUG_STEMPOST_SIMPLE = 7  /* unbanded BN/ReLU/maxpool kernel                */
+    BNN_DEBUG_STEMPOST_SIMPLE = 7, /* unbanded BN/ReLU/maxpool kernel                */
+    BNN_DEBUG_GRID_CAP = 8         /* tcgen05 kernels: at most this many CTAs (0 = #SMs) */
 };
 int bnn_debug_set(int knob, int64_t value);
 

@@ -23,7 +23,7 @@ ALGOS = {"auto": ALGO_AUTO, "popc": ALGO_POPC, "bmma": ALGO_BMMA, "umma": ALGO_U
          **{f"umma{v}": ALGO_UMMA_V0 + v for v in range(5)}}
 # debug knobs (bnn_debug_set; process-wide, experiment scripts only)
 DEBUG_UMMA_BITS, DEBUG_FP4_BN, DEBUG_PAIR_KW32, DEBUG_STEM_BITS = 1, 2, 3, 4
-DEBUG_PACK_PIX, DEBUG_PACK_CH, DEBUG_STEMPOST_SIMPLE = 5, 6, 7
+DEBUG_PACK_PIX, DEBUG_PACK_CH, DEBUG_STEMPOST_SIMPLE, DEBUG_GRID_CAP = 5, 6, 7, 8
 WATCHDOG_WORDS = 225
 FLAG_NONFINITE, FLAG_NOTSIGN, FLAG_RANGE = 1, 2, 4
 GRID_UNSIGNED, GRID_SIGNED = 0, 1

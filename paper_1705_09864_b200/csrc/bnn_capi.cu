@@ -107,6 +107,7 @@ int bnn_debug_set(int knob, int64_t value) {
         case BNN_DEBUG_PACK_PIX: g_debug.pack_pix = value; return BNN_OK;
         case BNN_DEBUG_PACK_CH: g_debug.pack_ch = value; return BNN_OK;
         case BNN_DEBUG_STEMPOST_SIMPLE: g_debug.stempost_simple = value; return BNN_OK;
+        case BNN_DEBUG_GRID_CAP: g_debug.grid_cap = value; return BNN_OK;
         default: return set_error(BNN_EINVAL, "unknown debug knob %d", knob);
     }
 }

@@ -24,6 +24,8 @@ struct DebugKnobs {
     int64_t pack_pix = 0;       // BNN_DEBUG_PACK_PIX: pack kernel variant (0 = default)
     int64_t pack_ch = 0;        // BNN_DEBUG_PACK_CH: channels per lane (0 = default 8)
     int64_t stempost_simple = 0;  // BNN_DEBUG_STEMPOST_SIMPLE: unbanded stem post-op
+    int64_t grid_cap = 0;       // BNN_DEBUG_GRID_CAP: persistent tcgen05 kernels use <= this many
+                                // CTAs (tests: many tiles per CTA, every ring wraps)
     uint64_t *trace_buf = nullptr;  // bnn_umma_trace
 };
 extern DebugKnobs g_debug;

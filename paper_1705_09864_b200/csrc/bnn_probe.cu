@@ -33,14 +33,15 @@ __device__ __forceinline__ uint64_t probe_sw128(uint32_t saddr) {
     return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
            ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
-template <int kKind>
-__global__ void __launch_bounds__(128) probe_mma_kernel(int reps, uint32_t *sink) {
+template <int kKind, int kN = 256, bool kTS = false>
+__global__ void __launch_bounds__(512) probe_mma_kernel(int reps, uint32_t *sink) {
     extern __shared__ __align__(1024) uint8_t psm[];
     __shared__ uint32_t tmem_base;
     __shared__ __align__(8) uint64_t bar;
+    __shared__ __align__(8) uint64_t bar2;
     const int tid = threadIdx.x, warp = tid >> 5;
     uint8_t *ops = psm + ((1024 - (probe_smem_u32(psm) & 1023)) & 1023);
-    for (int i = tid; i < (128 + 256) * 128 / 4; i += blockDim.x)
+    for (int i = tid; i < (kKind >= 8 ? 3 * 16384 + 3 * 8192 : (128 + 256) * 128) / 4; i += blockDim.x)
         reinterpret_cast<uint32_t *>(ops)[i] = 0x11111111u * (i & 3);
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
@@ -49,6 +50,7 @@ __global__ void __launch_bounds__(128) probe_mma_kernel(int reps, uint32_t *sink
     }
     if (tid == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(probe_smem_u32(&bar)));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(probe_smem_u32(&bar2)));
         asm volatile("fence.mbarrier_init.release.cluster;\n");
     }
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -67,7 +69,68 @@ __global__ void __launch_bounds__(128) probe_mma_kernel(int reps, uint32_t *sink
     asm volatile("tcgen05.fence::before_thread_sync;\n");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n");
-    if (tid == 0) {
+    __shared__ int probe_done;
+    if (tid == 0) probe_done = 0;
+    __syncthreads();
+    if (kKind >= 10 && tid >= 128) {
+        // other warps poll a shared flag while warp 0 issues (kKind 10: tight spin,
+        // 11: with nanosleep backoff) -- the interference of waiting warps
+        while (*(volatile int *)&probe_done == 0) {
+            if (kKind == 11) __nanosleep(64);
+        }
+    }
+    if (kKind >= 6 && tid == 0) {
+        // kind::mxf4 SS 128 x kN, 9 MMAs per group with varying descriptors (the small-
+        // channel conv's tile), one commit per group; kKind 7 also waits for each group's
+        // commit before issuing the next (a serialised pipeline)
+        const uint32_t a = probe_smem_u32(ops), b = a + (kKind >= 8 ? 3 * 16384 : 128 * 128);  // (kinds 8-11)
+        const uint32_t idesc = (1u << 7) | (1u << 10) | ((uint32_t)(kN >> 3) << 17) | (1u << 23) | (8u << 24);
+        uint32_t phase = 0;
+        for (int i = 0; i < reps / 9; ++i) {
+            for (int s = 0; s < 9; ++s) {
+                // the small-channel conv's pattern: A over 16 KB blocks, B over 8 KB blocks
+                const uint64_t ad = probe_sw128(a + (kKind >= 8 ? (s >> 2) * 16384 : 0) + (s & 3) * 32);
+                const uint64_t bd = probe_sw128(b + (kKind >= 8 ? (s >> 2) * 8192 : 0) + (s & 3) * 32);
+                asm volatile(
+                    "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                    "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n}\n" ::"r"(
+                        tmem + (kKind >= 8 ? (i & 3) * 64 : (i & 1) * 128)),
+                    "l"(ad), "l"(bd), "r"(idesc), "r"(s ? 1u : 0u), "r"(tmem + (kKind >= 8 ? 256 : 384)),
+                    "r"(tmem + (kKind >= 8 ? 256 : 384)));
+            }
+            asm volatile(
+                "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                    probe_smem_u32(&bar))
+                : "memory");
+            if (kKind == 7 || kKind >= 9) {
+                uint32_t done = 0;
+                do {
+                    asm volatile(
+                        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                        "selp.u32 %0, 1, 0, p;\n}\n"
+                        : "=r"(done)
+                        : "r"(probe_smem_u32(&bar)), "r"(phase)
+                        : "memory");
+                } while (!done);
+                phase ^= 1;
+            }
+        }
+        uint32_t done = 0;  // drain: one more commit, wait for everything
+        asm volatile(
+            "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                probe_smem_u32(&bar2))
+            : "memory");
+        do {
+            asm volatile(
+                "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n"
+                "selp.u32 %0, 1, 0, p;\n}\n"
+                : "=r"(done)
+                : "r"(probe_smem_u32(&bar2))
+                : "memory");
+        } while (!done);
+        *(volatile int *)&probe_done = 1;
+    }
+    if (kKind < 6 && tid == 0) {
         const uint32_t a = probe_smem_u32(ops), b = a + 128 * 128;
         for (int i = 0; i < reps; ++i) {
             const int kk = i & 3;
@@ -78,8 +141,18 @@ __global__ void __launch_bounds__(128) probe_mma_kernel(int reps, uint32_t *sink
                     "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
                     "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
                     "l"(ad), "l"(bd), "r"(idesc), "r"(1u));
+            } else if (kTS) {  // A from TMEM (columns 256.., 8 per K = 64 step)
+                const uint32_t idesc = (1u << 7) | (1u << 10) | ((uint32_t)(kN >> 3) << 17) |
+                                       (1u << 23) | (8u << 24);
+                asm volatile(
+                    "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                    "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], [%1], %2, %3, [%5], [%6], p;\n}\n" ::"r"(
+                        tmem),
+                    "r"(tmem + 256 + kk * 8), "l"(bd), "r"(idesc), "r"(1u), "r"(tmem + 384),
+                    "r"(tmem + 384));
             } else {
-                const uint32_t idesc = (1u << 7) | (1u << 10) | (32u << 17) | (1u << 23) | (8u << 24);
+                const uint32_t idesc = (1u << 7) | (1u << 10) | ((uint32_t)(kN >> 3) << 17) |
+                                       (1u << 23) | (8u << 24);
                 asm volatile(
                     "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
                     "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n}\n" ::"r"(
@@ -116,7 +189,7 @@ using namespace bnn;
 
 extern "C" int bnn_probe_pipe_peak(int pipe, int64_t iters, uint32_t *sink,
                                    double *ops_per_sec, bnn_stream_t stream) {
-    if (pipe < 0 || pipe > 2 || iters < 1 || !ops_per_sec || !sink)
+    if (pipe < 0 || pipe > 11 || iters < 1 || !ops_per_sec || !sink)
         return set_error(BNN_EINVAL,
                          "probe: pipe must be 0 (POPC), 1 (tcgen05 i8) or 2 (tcgen05 mxf4), "
                          "iters >= 1, sink non-null");
@@ -137,16 +210,30 @@ extern "C" int bnn_probe_pipe_peak(int pipe, int64_t iters, uint32_t *sink,
         rc = check_launch("probe_popc_kernel");
         work = (double)blocks * threads * (double)iters * 8.0;  // 32-bit popcounts
     } else {
-        const int smem = (128 + 256) * 128 + 1024;
+        const int smem = (pipe >= 8 ? 3 * 16384 + 3 * 8192 : (128 + 256) * 128) + 1024;
         const int reps = (int)(iters < (1 << 20) ? iters : (1 << 20));
-        auto kern = pipe == 1 ? probe_mma_kernel<1> : probe_mma_kernel<2>;
+        // 3: kind::mxf4 with A in TMEM, N = 64; 4: kind::mxf4 SS, N = 64; 5: TS, N = 256
+        auto kern = pipe == 1 ? probe_mma_kernel<1>
+                    : pipe == 2 ? probe_mma_kernel<2>
+                    : pipe == 3 ? probe_mma_kernel<2, 64, true>
+                    : pipe == 4 ? probe_mma_kernel<2, 64, false>
+                    : pipe == 5 ? probe_mma_kernel<2, 256, true>
+                    : pipe == 6 ? probe_mma_kernel<6, 64, false>
+                    : pipe == 7 ? probe_mma_kernel<7, 64, false>
+                    : pipe == 8 ? probe_mma_kernel<8, 64, false>
+                    : pipe == 9 ? probe_mma_kernel<9, 64, false>
+                    : pipe == 10 ? probe_mma_kernel<10, 64, false>
+                                 : probe_mma_kernel<11, 64, false>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        kern<<<sms, 128, smem, s>>>(reps / 8 + 1, sink);  // warm-up
+        const int nthr = pipe >= 10 ? 448 : 128;
+        kern<<<sms, nthr, smem, s>>>(reps / 8 + 1, sink);  // warm-up
         cudaEventRecord(e0, s);
-        kern<<<sms, 128, smem, s>>>(reps, sink);
+        kern<<<sms, nthr, smem, s>>>(reps, sink);
         cudaEventRecord(e1, s);
         rc = check_launch("probe_mma_kernel");
-        work = (double)sms * reps * 128.0 * 256.0 * (pipe == 1 ? 32.0 : 64.0);  // MACs
+        const double n = (pipe == 3 || pipe == 4 || pipe >= 6) ? 64.0 : 256.0;
+        const double nmma = pipe >= 6 ? (double)(reps / 9) * 9.0 : (double)reps;
+        work = (double)sms * nmma * 128.0 * n * (pipe == 1 ? 32.0 : 64.0);  // MACs
     }
     cudaEventSynchronize(e1);
     float ms = 0.f;

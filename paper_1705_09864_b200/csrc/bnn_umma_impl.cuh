@@ -341,6 +341,20 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
             : "memory");
     } while (!done);
 }
+// latency-critical waits: spin on test_wait (no suspension, so no wake-up latency
+// after the phase completes)
+__device__ __forceinline__ void mbar_wait_spin(uint32_t bar, uint32_t phase) {
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{\n.reg .pred p;\n"
+            "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(bar), "r"(phase)
+            : "memory");
+    } while (!done);
+}
 // long waits (epilogue): the thread sleeps in try_wait until the phase completes
 // instead of spinning on the issue slots the producers need
 __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t phase) {
@@ -1696,6 +1710,7 @@ static int launch_umma_cfg(const ALoad &a_in, const BLoad &b_in, const Store &st
     // one CTA (pair of CTAs) per SM (pair of SMs), persistent over the tiles
     const int64_t units = kPair ? sm_count() / 2 : sm_count();
     int grid = (int)((ntiles < units ? ntiles : units) * (kPair ? 2 : 1));
+    if (g_debug.grid_cap > 0 && grid > g_debug.grid_cap) grid = (int)((g_debug.grid_cap + 1) & ~1);
     const bool force_cluster = !kPair && (umma_dbg() & 32768);  // debug: cluster launch of 1-CTA code
     if (force_cluster) grid = (grid + 1) & ~1;
     cudaLaunchConfig_t cfg = {};
@@ -1893,11 +1908,23 @@ static int launch_xnor_gemm_umma_t(const uint64_t *A, int64_t lda, const uint64_
                 : launch_umma<2>(a, b, st, ep, M, N, kw32, s);
 }
 
+// small-channel convs (C, F in {64, 128}): filter-stationary kernel with pixels as the
+// TMEM A operand (bnn_sconv.cu); BNN_EUNSUP for other shapes
+int launch_sconv(const uint64_t *x, int64_t B, int64_t C, int64_t H, int64_t W,
+                 const uint64_t *w, int64_t F, int64_t kh, int64_t kw, int64_t sh, int64_t sw,
+                 int64_t ph, int64_t pw, int64_t oh, int64_t ow, float *y, const Epilogue &ep,
+                 cudaStream_t s, const float *res);
+
 template <class CS>
 static int launch_bconv2d_umma_t(const uint64_t *x, int64_t B, int64_t C, int64_t H, int64_t W,
                         const uint64_t *w, int64_t F, int64_t kh, int64_t kw, int64_t sh,
                         int64_t sw, int64_t ph, int64_t pw, int64_t oh, int64_t ow, float *y,
                         const Epilogue &ep, cudaStream_t s, const float *res) {
+    if (ep.variant == 2 && !(umma_dbg() & 262144)) {
+        const int rc = launch_sconv(x, B, C, H, W, w, F, kh, kw, sh, sw, ph, pw, oh, ow, y, ep, s,
+                                    res);
+        if (rc != BNN_EUNSUP) return rc;
+    }
     const int64_t cw64 = ceil_div(C, 64);
     const int64_t cs32 = 2 * cw64;
     const int64_t kw32 = kh * kw * cs32;

@@ -197,3 +197,79 @@ def test_add_pack_nchw(bnn, shape):
     assert torch.equal(y, a + r)
     assert np.array_equal(words.cpu().numpy(), bnn.pack_nchw(a + r).cpu().numpy())
     assert int(flags.item()) == 0
+
+
+# Small-channel kernel (bnn_sconv.cu: C, F in {64, 128}, pixels in TMEM, filter-stationary
+# weights): every epilogue combination against the oracle composition and against the
+# general engine (variant 4 -- no small-channel route) on the same inputs.  Shapes: ResNet
+# layer 1/2 geometry at small batch, strided 3x3 and 1x1 downsamples, images whose tiles
+# straddle images and rows, odd image widths (falls back when W * C / 64 is odd), pad 0.
+SCONV_CASES = [
+    (2, 64, 56, 56, 64, 3, 3, (1, 1), (1, 1), 11),
+    (3, 64, 56, 56, 128, 3, 3, (2, 2), (1, 1), 12),
+    (2, 128, 28, 28, 128, 3, 3, (1, 1), (1, 1), 13),
+    (3, 64, 56, 56, 128, 1, 1, (2, 2), (0, 0), 14),
+    (5, 64, 10, 12, 64, 3, 3, (1, 1), (1, 1), 15),
+    (2, 128, 9, 6, 64, 3, 3, (1, 1), (0, 0), 16),
+    (1, 64, 7, 9, 128, 3, 3, (2, 2), (1, 1), 17),
+    (4, 128, 14, 14, 128, 1, 1, (1, 1), (0, 0), 18),
+    (2, 64, 33, 20, 64, 3, 3, (2, 1), (1, 1), 19),
+]
+
+
+@pytest.fixture(params=[0, 3], ids=["grid_sms", "grid_cap3"])
+def grid_cap(request):
+    """0: one CTA per SM; 3: three persistent CTAs, so every CTA walks many tiles and
+    every ring (bands, A chunks, accumulators, popcounts) wraps around."""
+    from paper_1705_09864_b200 import _lib
+    _lib.call("bnn_debug_set", _lib.DEBUG_GRID_CAP, request.param)
+    yield request.param
+    _lib.call("bnn_debug_set", _lib.DEBUG_GRID_CAP, 0)
+
+
+@pytest.mark.parametrize("case", SCONV_CASES)
+@pytest.mark.parametrize("epi", ["plain", "bn_pack", "bn_res_pack", "bn_res"])
+def test_small_channel_conv_kernel(bnn, case, epi, grid_cap):
+    from paper_1705_09864_b200.layers import PackedNHWC
+    b, c, h, w, f, kh, kw, stride, pad, seed = case
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((b, c, h, w)).astype(np.float32)
+    x.reshape(-1)[::17] = 0.0
+    wt = rng.standard_normal((f, c, kh, kw)).astype(np.float32)
+    layer = bnn.QConvolution(c, f, (kh, kw), stride, pad, domain="dot")
+    layer.weight = wt
+    layer.pack()
+    oh, ow = layer.output_hw(h, w)
+    xd = torch.from_numpy(x).cuda()
+    p = orc.qconv_packed(x, wt, stride, pad).astype(np.float32)
+    ref = 2 * p - np.float32(c * kh * kw)
+    if epi == "plain":
+        y = layer.forward_fused(xd)
+        assert np.array_equal(y.cpu().numpy(), ref)
+        return
+    bn = _BN(f, c * kh * kw, seed)
+    # constant-sign channels (zero / negative-zero gamma) and huge gammas (outputs that
+    # overflow to +-inf: the packed-only path keeps the full chain and raises the flag)
+    bn.gamma[:3] = [0.0, -0.0, 1e-30]
+    bn.beta[:3] = [-0.0, 1.0, -1.0]
+    sh = (1, -1, 1, 1)
+    ref = bn.gamma.reshape(sh) * ((ref - bn.mean.reshape(sh)) * bn.inv.reshape(sh)) + \
+        bn.beta.reshape(sh)
+    res = None
+    if "res" in epi:
+        res = torch.from_numpy(rng.standard_normal((b, f, oh, ow)).astype(np.float32)).cuda()
+        res.view(-1)[::9] = 0.0
+        ref = ref + res.cpu().numpy()
+    ref = ref.astype(np.float32)
+    pack = "pack" in epi
+    out = layer.forward_fused(xd, bn, residual=res, pack_out=pack)
+    y = out.f32 if pack else out
+    assert np.array_equal(y.cpu().numpy(), ref)
+    if pack:
+        assert isinstance(out, PackedNHWC)
+        assert np.array_equal(out.words.cpu().numpy(), _oracle_pack_nhwc(ref))
+        only = layer.forward_fused(xd, bn, residual=res, pack_out=True, f32_out=False)
+        assert np.array_equal(only.words.cpu().numpy(), out.words.cpu().numpy())
+    layer.algo = "umma4"  # the general engine on the same inputs
+    other = layer.forward_fused(xd, bn, residual=res, pack_out=pack)
+    assert torch.equal(other.f32 if pack else other, y)

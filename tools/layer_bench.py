@@ -14,6 +14,7 @@ from paper_1705_09864_b200 import nets  # noqa: E402
 from paper_1705_09864_b200.layers import PackedNHWC  # noqa: E402
 
 SHAPES = [(256, 64, 56, 56, 64, 3, 1, 1), (256, 64, 56, 56, 128, 3, 2, 1),
+          (256, 64, 56, 56, 128, 1, 2, 0),
           (256, 128, 28, 28, 128, 3, 1, 1), (256, 128, 28, 28, 256, 3, 2, 1),
           (256, 256, 14, 14, 256, 3, 1, 1), (256, 512, 7, 7, 512, 3, 1, 1),
           (32, 256, 28, 28, 256, 3, 1, 1)]
@@ -49,17 +50,19 @@ def main():
         oh, ow = conv.output_hw(h, w)
         res = torch.randn((b, f, oh, ow), device="cuda")
         out = torch.empty_like(res)
-        t = {
-            "f32": timeit(lambda: conv.forward_fused(xp, bn, out=out)),
-            "f32+res": timeit(lambda: conv.forward_fused(xp, bn, residual=res, out=out)),
-            "pack": timeit(lambda: conv.forward_fused(xp, bn, pack_out=True, f32_out=False)),
-            "pack+f32+res": timeit(lambda: conv.forward_fused(xp, bn, residual=res, out=out,
-                                                              pack_out=True)),
-        }
-        ops = 2 * f * b * oh * ow * c * k * k
-        print(f"B{b} C{c} {h}x{w} F{f} k{k} s{s}: " +
-              "  ".join(f"{n} {us:7.1f}us ({ops / us / 1e6:6.0f} TOPS)" for n, us in t.items()),
-              flush=True)
+        for algo in ("auto", "umma4"):
+            conv.algo = algo
+            t = {
+                "f32": timeit(lambda: conv.forward_fused(xp, bn, out=out)),
+                "f32+res": timeit(lambda: conv.forward_fused(xp, bn, residual=res, out=out)),
+                "pack": timeit(lambda: conv.forward_fused(xp, bn, pack_out=True, f32_out=False)),
+                "pack+f32+res": timeit(lambda: conv.forward_fused(xp, bn, residual=res, out=out,
+                                                                  pack_out=True)),
+            }
+            ops = 2 * f * b * oh * ow * c * k * k
+            print(f"B{b} C{c} {h}x{w} F{f} k{k} s{s} [{algo}]: " +
+                  "  ".join(f"{n} {us:7.1f}us ({ops / us / 1e6:6.0f} TOPS)" for n, us in t.items()),
+                  flush=True)
 
 
 if __name__ == "__main__":
