@@ -1031,28 +1031,29 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                         // K = 64 e2m1 per MMA = 32 bytes of the superstage row
                         const uint32_t a_addr = s_exp + sb * C::kSuperBytes;
                         const uint32_t b_addr = a_addr + C::kFp4A;
+                        // descriptors: base + constant start-address increments (16-byte
+                        // units; 32 B per K = 64 step) -- no per-MMA descriptor arithmetic
+                        // on the issue thread's critical path
+                        const uint64_t da = sw128_desc(a_addr), db = sw128_desc(b_addr);
+                        const uint64_t db2 = sw128_desc(b_addr + C::kMmaN * 128);
+                        const uint32_t sfc = tmem + C::kSfCol;
+                        const uint32_t ta = tmem + C::kAStageCol + sb * C::kAStageCols;
+                        const int nk = (dbg & 2) ? 0 : 2 * (int)nsub;
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk) {
-                            if ((dbg & 2) || kk >= 2 * (int)nsub) break;
+                            if (kk >= nk) break;
                             const uint32_t acc = (kt | kk) != 0 ? 1u : 0u;
                             if constexpr (kPair) {  // 256 x BN: A and B halves from both CTAs
-                                mma_fp4_pair<C::kIdescFp4>(d, sw128_desc(a_addr + kk * 32),
-                                                           sw128_desc(b_addr + kk * 32),
-                                                           tmem + C::kSfCol, tmem + C::kSfCol, acc);
+                                mma_fp4_pair<C::kIdescFp4>(d, da + 2 * kk, db + 2 * kk, sfc, sfc, acc);
                                 continue;
                             }
                             if constexpr (kATmem)
-                                mma_fp4_ts<C::kIdescFp4>(d, tmem + C::kAStageCol + sb * C::kAStageCols + kk * 8,
-                                                         sw128_desc(b_addr + kk * 32), tmem + C::kSfCol,
-                                                         tmem + C::kSfCol, acc);
+                                mma_fp4_ts<C::kIdescFp4>(d, ta + kk * 8, db + 2 * kk, sfc, sfc, acc);
                             else
-                                mma_fp4<C::kIdescFp4>(d, sw128_desc(a_addr + kk * 32),
-                                                      sw128_desc(b_addr + kk * 32), tmem + C::kSfCol,
-                                                      tmem + C::kSfCol, acc);
+                                mma_fp4<C::kIdescFp4>(d, da + 2 * kk, db + 2 * kk, sfc, sfc, acc);
                             if constexpr (C::kNMma == 2)  // columns [N/2, N): B rows N/2..N-1
-                                mma_fp4<C::kIdescFp4>(d + C::kMmaN, sw128_desc(a_addr + kk * 32),
-                                                      sw128_desc(b_addr + C::kMmaN * 128 + kk * 32),
-                                                      tmem + C::kSfCol, tmem + C::kSfCol, acc);
+                                mma_fp4<C::kIdescFp4>(d + C::kMmaN, da + 2 * kk, db2 + 2 * kk, sfc,
+                                                      sfc, acc);
                         }
                     }
 #pragma unroll
@@ -1060,16 +1061,16 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                         if (kFp4 || u >= nsub) break;
                         const uint32_t stage = s_exp + sb * C::kSuperBytes + u * C::kStageBytes;
                         const uint32_t b_addr = stage + C::kStageA;
+                        const uint64_t da = sw128_desc(stage), db = sw128_desc(b_addr);
+                        const uint32_t ta = tmem + C::kAStageCol + (sb * kSub + u) * 32;
 #pragma unroll
                         for (int kk = 0; kk < kRowBytes / 32; ++kk) {
                             if (dbg & 2) break;
                             const uint32_t acc = ((kt + u) | kk) != 0 ? 1u : 0u;
                             if constexpr (kATmem)
-                                mma_ts<C::kIdesc>(d, tmem + C::kAStageCol + (sb * kSub + u) * 32 + kk * 8,
-                                                  sw128_desc(b_addr + kk * 32), acc);
+                                mma_ts<C::kIdesc>(d, ta + kk * 8, db + 2 * kk, acc);
                             else
-                                mma_ss<C::kIdesc>(d, sw128_desc(stage + kk * 32),
-                                                  sw128_desc(b_addr + kk * 32), acc);
+                                mma_ss<C::kIdesc>(d, da + 2 * kk, db + 2 * kk, acc);
                         }
                     }
                     if constexpr (kPair) umma_commit_pair(bar_empty + 8 * sb);

@@ -276,6 +276,18 @@ class Sequential:
     fuse_stem = True  # infer_packed: float stem conv + StemPost as one tensor-core kernel
 
     def forward(self, x, mode=INFER_FLOAT, capture=None):
+        if capture is not None:  # per-layer capture reads every block's f32 output
+            saved = [(l, l.needs_f32_out) for l in self.layers if isinstance(l, BinaryBasicBlock)]
+            for l, _ in saved:
+                l.needs_f32_out = True
+            try:
+                return self._forward(x, mode, capture)
+            finally:
+                for l, v in saved:
+                    l.needs_f32_out = v
+        return self._forward(x, mode, capture)
+
+    def _forward(self, x, mode=INFER_FLOAT, capture=None):
         i, n = 0, len(self.layers)
         while i < n:
             layer = self.layers[i]
@@ -434,7 +446,17 @@ class BinaryBasicBlock:
     # block's convs), so no standalone pack pass runs inside the network
     packed_io = True
     emit_packed = True  # False for the last block (a float layer consumes it)
+    # False when no consumer reads the f32 block output: the next block has a
+    # downsample shortcut (it reads the packed words only) -- conv2's epilogue then
+    # computes BN + shortcut for the sign and writes the packed words alone
+    needs_f32_out = True
     split_shortcut = True  # conv2 epilogue without the add + one add/sign-pack pass
+    # (for the convs the small-channel kernel runs -- C, F <= 128 -- the shortcut add
+    # stays in conv2's epilogue, whose residual reads are coalesced there)
+
+    def _fused_shortcut(self, h) -> bool:
+        c, f = self.conv2.in_channels, self.conv2.filters
+        return not self.split_shortcut or (c in (64, 128) and f in (64, 128))
 
     def forward(self, x, mode=INFER_FLOAT):
         if mode == INFER_PACKED and self.fused and self.packed_io:
@@ -442,10 +464,13 @@ class BinaryBasicBlock:
                 x = PackedNHWC.from_f32(x, self.conv1._flags())
             h = self.conv1.forward_fused(x, self.bn1, pack_out=True, f32_out=False)
             sc = x.float() if self.down is None else self.down.forward_fused(x, self.bnd)
-            if self.split_shortcut:
-                # the conv epilogue without the shortcut is faster on every ResNet shape
-                # (profiles/r01/resnet_layer_epilogues.txt: f32 vs pack+f32+res), so the
-                # add and the sign-pack run as one streaming pass (bit-identical)
+            if self.emit_packed and not self.needs_f32_out:
+                return self.conv2.forward_fused(h, self.bn2, residual=sc, pack_out=True,
+                                                f32_out=False)
+            if not self._fused_shortcut(h):
+                # the conv epilogue without the shortcut is faster on the general engine's
+                # shapes (profiles/r01/resnet_layer_epilogues.txt: f32 vs pack+f32+res), so
+                # the add and the sign-pack run as one streaming pass (bit-identical)
                 y = self.conv2.forward_fused(h, self.bn2)
                 b, f, oh, ow = y.shape
                 words = torch.empty((b, oh, ow, (f + 63) // 64), dtype=torch.uint64,
@@ -489,6 +514,9 @@ def resnet18_c4(seed: int = 0, num_classes: int = 1000) -> Sequential:
         layers.append(BinaryBasicBlock(cout, cout, 1, rng))
         cin = cout
     layers[-1].emit_packed = False  # the average pool reads the f32 output
+    blocks = [l for l in layers if isinstance(l, BinaryBasicBlock)]
+    for blk, nxt in zip(blocks[:-1], blocks[1:]):
+        blk.needs_f32_out = nxt.down is None  # identity shortcuts read the f32 output
     layers += [GlobalAvgPool(), Dense(512, num_classes, rng=rng)]
     return Sequential(layers)
 
