@@ -681,42 +681,101 @@ __global__ void avgpool_kernel(const float *__restrict__ x, int64_t BC, int HW,
     pooled[i] = __fdiv_rn(s, (float)HW);
 }
 
-template <int kImg, int kOut>
-__global__ void __launch_bounds__(256) fc_rows_kernel(const float *__restrict__ pooled, int B, int C,
-                                                      const float *__restrict__ w,
-                                                      const float *__restrict__ bias, int O,
-                                                      float *__restrict__ y) {
-    extern __shared__ float sp[];  // [kImg][C]
-    const int b0 = blockIdx.x * kImg, o0 = blockIdx.y * kOut;
-    for (int i = threadIdx.x; i < kImg * C; i += blockDim.x) {
-        const int bi = i / C;
-        sp[i] = b0 + bi < B ? pooled[(int64_t)(b0 + bi) * C + (i - bi * C)] : 0.0f;
+// Pass 2: a CTA of 64 threads per (16 images, 64 outputs) tile, k in tiles of 64 staged
+// in SMEM row-major with a 65-float pitch (coalesced fills, conflict-free column reads);
+// each thread a 4 x 4 register tile, every output a sequential k = 0 .. C-1 FMA chain --
+// the same order for every image, any batch.
+constexpr int kFcImg = 16, kFcOut = 64, kFcK = 64, kFcPitch = kFcK + 1;
+__global__ void __launch_bounds__(64) fc_rows_kernel(const float *__restrict__ pooled, int B, int C,
+                                                     const float *__restrict__ w,
+                                                     const float *__restrict__ bias, int O,
+                                                     float *__restrict__ y) {
+    __shared__ float sp[kFcImg * kFcPitch];
+    __shared__ float sw[kFcOut * kFcPitch];
+    const int b0 = blockIdx.x * kFcImg, o0 = blockIdx.y * kFcOut;
+    const int t = threadIdx.x, og = t & 15, ig = t >> 4;  // outputs 4 og .. +3, images 4 ig .. +3
+    float acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
+    for (int k0 = 0; k0 < C; k0 += kFcK) {
+        const int kn = C - k0 < kFcK ? C - k0 : kFcK;
+        // (all of a thread's tile loads in flight before its SMEM stores)
+        {
+            constexpr int kP = kFcImg * kFcK / 64, kW = kFcOut * kFcK / 64;
+            float vp[kP], vw[kW];
+#pragma unroll
+            for (int u = 0; u < kP; ++u) {
+                const int i = t + 64 * u, r = i / kFcK, k = i - r * kFcK;
+                vp[u] = (b0 + r < B && k < kn) ? __ldg(pooled + (int64_t)(b0 + r) * C + k0 + k) : 0.0f;
+            }
+#pragma unroll
+            for (int u = 0; u < kW; ++u) {
+                const int i = t + 64 * u, r = i / kFcK, k = i - r * kFcK;
+                vw[u] = (o0 + r < O && k < kn) ? __ldg(w + (int64_t)(o0 + r) * C + k0 + k) : 0.0f;
+            }
+#pragma unroll
+            for (int u = 0; u < kP; ++u) {
+                const int i = t + 64 * u, r = i / kFcK, k = i - r * kFcK;
+                sp[r * kFcPitch + k] = vp[u];
+            }
+#pragma unroll
+            for (int u = 0; u < kW; ++u) {
+                const int i = t + 64 * u, r = i / kFcK, k = i - r * kFcK;
+                sw[r * kFcPitch + k] = vw[u];
+            }
+        }
+        __syncthreads();
+        for (int k = 0; k < kn; ++k) {
+            float p4[4], w4[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) p4[i] = sp[(4 * ig + i) * kFcPitch + k];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) w4[j] = sw[(4 * og + j) * kFcPitch + k];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = __fmaf_rn(p4[i], w4[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int bi = b0 + 4 * ig + i, o = o0 + 4 * og + j;
+            if (bi < B && o < O) {
+                float v = acc[i][j];
+                if (bias) v = __fadd_rn(v, __ldg(bias + o));
+                y[(int64_t)bi * O + o] = v;
+            }
+        }
+}
+
+// Pass 1: a CTA per 64 consecutive (image, channel) rows, staged in SMEM by coalesced
+// 16-byte loads; each thread sums its row in order t = 0 .. HW-1, then / HW
+__global__ void __launch_bounds__(128) avgpool_rows_kernel(const float *__restrict__ x, int64_t BC,
+                                                           int HW, float *__restrict__ pooled) {
+    extern __shared__ float rows[];  // [64][HW]
+    const int64_t r0 = (int64_t)blockIdx.x * 64;
+    const int nr = BC - r0 < 64 ? (int)(BC - r0) : 64;
+    const float *src = x + r0 * HW;
+    const int n = nr * HW;
+    if (((reinterpret_cast<uintptr_t>(src)) & 15) == 0) {
+        const int n4 = n >> 2;
+        for (int i = threadIdx.x; i < n4; i += blockDim.x)
+            reinterpret_cast<float4 *>(rows)[i] = __ldg(reinterpret_cast<const float4 *>(src) + i);
+        for (int i = 4 * n4 + threadIdx.x; i < n; i += blockDim.x) rows[i] = __ldg(src + i);
+    } else {
+        for (int i = threadIdx.x; i < n; i += blockDim.x) rows[i] = __ldg(src + i);
     }
     __syncthreads();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int o = o0 + warp; o < o0 + kOut && o < O; o += blockDim.x >> 5) {
-        float acc[kImg];
-#pragma unroll
-        for (int j = 0; j < kImg; ++j) acc[j] = 0.0f;
-        const float *wr = w + (int64_t)o * C;
-        for (int c = lane; c < C; c += 32) {
-            const float wv = __ldg(wr + c);
-#pragma unroll
-            for (int j = 0; j < kImg; ++j) acc[j] = __fmaf_rn(sp[j * C + c], wv, acc[j]);
-        }
-#pragma unroll
-        for (int j = 0; j < kImg; ++j) {
-#pragma unroll
-            for (int d = 16; d >= 1; d >>= 1) acc[j] = __fadd_rn(acc[j], __shfl_xor_sync(0xffffffffu, acc[j], d));
-        }
-        if (lane < kImg && b0 + lane < B) {
-            float v = acc[0];
-#pragma unroll
-            for (int j = 1; j < kImg; ++j)
-                if (lane == j) v = acc[j];
-            if (bias) v = __fadd_rn(v, __ldg(bias + o));
-            y[(int64_t)(b0 + lane) * O + o] = v;
-        }
+    if (threadIdx.x < nr) {
+        const float *p = rows + threadIdx.x * HW;
+        float s = 0.0f;
+        for (int t = 0; t < HW; ++t) s = __fadd_rn(s, p[t]);
+        pooled[r0 + threadIdx.x] = __fdiv_rn(s, (float)HW);
     }
 }
 
@@ -724,20 +783,15 @@ __global__ void __launch_bounds__(256) fc_rows_kernel(const float *__restrict__ 
 int launch_avgpool_fc(const float *x, int64_t B, int64_t C, int64_t HW, const float *w,
                       const float *bias, int64_t O, float *y, float *pooled, cudaStream_t s) {
     if (B == 0) return BNN_OK;
-    constexpr int kImg = 8, kOut = 64;
-    const size_t smem = (size_t)kImg * C * sizeof(float);
-    if (smem > 200 * 1024) return set_error(BNN_EUNSUP, "avgpool_fc: too many channels");
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(fc_rows_kernel<kImg, kOut>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             200 * 1024);
-        configured = true;
-    }
-    avgpool_kernel<<<(unsigned)ceil_div(B * C, 256), 256, 0, s>>>(x, B * C, (int)HW, pooled);
+    if (HW <= 256)  // (64 rows of HW floats staged in SMEM)
+        avgpool_rows_kernel<<<(unsigned)ceil_div(B * C, 64), 128, (size_t)64 * HW * 4, s>>>(
+            x, B * C, (int)HW, pooled);
+    else
+        avgpool_kernel<<<(unsigned)ceil_div(B * C, 256), 256, 0, s>>>(x, B * C, (int)HW, pooled);
     int rc = check_launch("avgpool_kernel");
     if (rc) return rc;
-    dim3 g((unsigned)ceil_div(B, kImg), (unsigned)ceil_div(O, kOut));
-    fc_rows_kernel<kImg, kOut><<<g, 256, smem, s>>>(pooled, (int)B, (int)C, w, bias, (int)O, y);
+    dim3 g((unsigned)ceil_div(B, kFcImg), (unsigned)ceil_div(O, kFcOut));
+    fc_rows_kernel<<<g, 64, 0, s>>>(pooled, (int)B, (int)C, w, bias, (int)O, y);
     return check_launch("fc_rows_kernel");
 }
 int launch_popcount64(const uint64_t *w, int64_t n, uint8_t *out, int soft, cudaStream_t s) {

@@ -464,10 +464,11 @@ class BinaryBasicBlock:
                 x = PackedNHWC.from_f32(x, self.conv1._flags())
             h = self.conv1.forward_fused(x, self.bn1, pack_out=True, f32_out=False)
             sc = x.float() if self.down is None else self.down.forward_fused(x, self.bnd)
-            if self.emit_packed and not self.needs_f32_out:
+            fused_sc = self._fused_shortcut(h)
+            if self.emit_packed and not self.needs_f32_out and fused_sc:
                 return self.conv2.forward_fused(h, self.bn2, residual=sc, pack_out=True,
                                                 f32_out=False)
-            if not self._fused_shortcut(h):
+            if not fused_sc:
                 # the conv epilogue without the shortcut is faster on the general engine's
                 # shapes (profiles/r01/resnet_layer_epilogues.txt: f32 vs pack+f32+res), so
                 # the add and the sign-pack run as one streaming pass (bit-identical)
