@@ -760,6 +760,12 @@ __global__ void __launch_bounds__(PEpi<kEW>::kThreads, 1) conv_pool_kernel(const
 
 }  // namespace stem
 
+bool stem_s2_supported(int64_t C, int64_t H, int64_t W, int64_t F, int64_t kh, int64_t kw, int64_t sh,
+                       int64_t sw, int64_t ph, int64_t pw);
+int launch_stem_s2(const float *x, int64_t B, int64_t H, const float *w, const float *bias,
+                   const float *mean, const float *inv, const float *gamma, const float *beta, int relu,
+                   int raw, float *y, uint64_t *pack_words, int32_t *pack_flags, cudaStream_t s);
+
 int launch_conv2d_f32_tc(const float *x, int64_t B, int64_t C, int64_t H, int64_t W,
                          const float *w, const float *bias, int64_t F, int64_t kh, int64_t kw,
                          int64_t sh, int64_t sw, int64_t ph, int64_t pw, int64_t oh, int64_t ow,
@@ -772,6 +778,10 @@ int launch_conv2d_f32_tc(const float *x, int64_t B, int64_t C, int64_t H, int64_
                          kMaxChunks * KC);
     const int64_t npix = B * oh * ow;
     if (npix == 0) return BNN_OK;
+    // ResNet-18's stem geometry: the gather-free stride-2 kernel (bnn_stem_s2.cu)
+    if (stem_s2_supported(C, H, W, F, kh, kw, sh, sw, ph, pw) && !(reinterpret_cast<uintptr_t>(x) & 7) &&
+        !(reinterpret_cast<uintptr_t>(y) & 15))
+        return launch_stem_s2(x, B, H, w, bias, nullptr, nullptr, nullptr, nullptr, 0, 1, y, nullptr, nullptr, s);
     if (C * H * W >= (1ll << 31) || npix / stem::BM >= (1ll << 31))
         return set_error(BNN_EUNSUP, "tensor-core f32 conv: tensor too large");
     Geom g{};
@@ -805,6 +815,9 @@ int launch_conv_bn_relu_maxpool_tc(const float *x, int64_t B, int64_t C, int64_t
     const int64_t OH = (H + 2 * ph - kh) / sh + 1, OW = (W + 2 * pw - kw) / sw + 1;
     const int64_t PH = mode ? OH / 2 : (OH + 2 - 3) / 2 + 1, PW = mode ? OW / 2 : (OW + 2 - 3) / 2 + 1;
     if (mode && (PH < 1 || PW < 1)) return set_error(BNN_EUNSUP, "fused stem: pool does not fit");
+    if (mode == 0 && stem_s2_supported(C, H, W, F, kh, kw, sh, sw, ph, pw) &&
+        !(reinterpret_cast<uintptr_t>(x) & 7) && !(reinterpret_cast<uintptr_t>(y) & 15))
+        return launch_stem_s2(x, B, H, w, nullptr, mean, inv, gamma, beta, relu, 0, y, pack_words, pack_flags, s);
     if (F != NF || K > kMaxChunks * KC || OW > stem::BM || OW < 2 || OH < 2 || W % 4 != 0 ||
         (reinterpret_cast<uintptr_t>(x) & 15) || PW > 64 || C * H * W >= (1ll << 31) ||
         C * kh > 2 * kPLoadBatch || W / 4 > 64 * 8)

@@ -24,6 +24,10 @@ def t(fn, n=5):
 
 
 bnn.load_library()
+import os
+from paper_1705_09864_b200 import _lib
+if os.environ.get("BNN_STEM_OLD"):
+    _lib.call("bnn_debug_set", 4, 16)  # BNN_DEBUG_STEM_BITS bit 4: the gather kernel (bnn_stem.cu)
 b = int(sys.argv[1]) if len(sys.argv) > 1 else 256
 rng = np.random.default_rng(0)
 conv = nets.Conv2d(3, 64, 7, stride=2, pad=3, bias=False, rng=rng)
