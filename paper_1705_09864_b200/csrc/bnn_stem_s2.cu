@@ -44,13 +44,15 @@ constexpr int kNP = 8;                      // ring slots (input row pairs)
 constexpr int kAcc = 3;                     // accumulators: TMEM columns 0, 112, 224
 constexpr int kACol0 = kAcc * kOW;          // weights: columns [336, 504)
 static_assert(kACol0 + 8 * kSlices <= 512, "TMEM budget");
-constexpr int kEpiWarps = 8, kLoadWarp0 = 8, kLoadWarps = 4, kMmaWarp = 12;
-constexpr int kThreads = (kMmaWarp + 1) * 32;
+constexpr int kEpiWarps = 8, kLoadWarp0 = 8, kLoadWarps = 4, kMmaWarp = 12, kMmaWarps = 2;
+constexpr int kThreads = (kMmaWarp + kMmaWarps) * 32;
+constexpr int kTPitch = 58;  // per-warp store transpose buffer: 16 filters x kTPitch floats
 // kind::tf32: D f32, A / B TF32, K-major, N = 112, M = 128
 constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kOW >> 3) << 17) |
                             ((uint32_t)(128 >> 4) << 24);
-constexpr int kOffBars = kNP * kPairB;
-constexpr int kNumBars = 2 * kNP + 2 * kAcc;
+constexpr int kOffTr = kNP * kPairB;
+constexpr int kOffBars = kOffTr + kEpiWarps * 16 * kTPitch * 4;
+constexpr int kNumBars = 2 * kNP + 2 * kAcc + 2;
 constexpr int kSmemBytes = kOffBars + kNumBars * 8 + 16 + 128;
 static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
 
@@ -62,11 +64,16 @@ struct Geom {
     int relu, raw;
     int H, OH, PH;
     int rpb, nbands, items;  // rows per band (raw: conv rows, pooled: pooled rows)
+    int dbg;  // BNN_DEBUG_STEM_BITS (wrong results): 1 no input loads, 2 no MMAs, 4 no epilogue math / stores
+    long long *trace;  // BNN_DEBUG_STEM_BITS & 8 with bnn_umma_trace: CTA 0 writes clock64 at [event * 64 + row]
 };
 
 struct Rows {
     int b, oy_s, oy_e, py0, py1;
 };
+__device__ __forceinline__ void trace(const Geom &g, int ev, int idx) {
+    if (g.trace && blockIdx.x == 0 && idx < 64) g.trace[ev * 64 + idx] = clock64();
+}
 __device__ __forceinline__ Rows item_rows(const Geom &g, int item) {
     Rows r;
     r.b = item / g.nbands;
@@ -81,19 +88,19 @@ __device__ __forceinline__ Rows item_rows(const Geom &g, int item) {
     return r;
 }
 
-__device__ __forceinline__ void wait_backoff(uint32_t bar, uint32_t phase) {
+// plain parked wait (umma::mbar_wait reads the watchdog pointer from global memory on
+// every call: an L1 miss per wait here, where the loader streams the images through L1)
+__device__ __forceinline__ void wait_parked(uint32_t bar, uint32_t phase) {
     uint32_t done = 0;
-    while (true) {
+    do {
         asm volatile(
             "{\n.reg .pred p;\n"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
             "selp.u32 %0, 1, 0, p;\n}\n"
             : "=r"(done)
-            : "r"(bar), "r"(phase)
+            : "r"(bar), "r"(phase), "r"(1000000u)
             : "memory");
-        if (done) return;
-        __nanosleep(64);
-    }
+    } while (!done);
 }
 __device__ __forceinline__ uint32_t tf32_hi(float v) { return __float_as_uint(v) & 0xFFFFE000u; }
 __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t bdesc, uint32_t acc) {
@@ -122,18 +129,22 @@ __global__ void __launch_bounds__(kThreads, 1) stem_s2_kernel(const __grid_const
     uint8_t *smem = smem_raw + (base - raw);
     const uint32_t bar_full = base + kOffBars, bar_empty = bar_full + 8 * kNP;
     const uint32_t bar_tfull = bar_empty + 8 * kNP, bar_tempty = bar_tfull + 8 * kAcc;
+    const uint32_t bar_stagger = bar_tempty + 8 * kAcc;
     uint32_t *s_tmem = reinterpret_cast<uint32_t *>(smem + kOffBars + kNumBars * 8);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
+    if (tid == 0) trace(g, 7, 0);
     if (tid == 0) {
         for (int s = 0; s < kNP; ++s) {
             mbar_init(bar_full + 8 * s, kLoadWarps);
-            mbar_init(bar_empty + 8 * s, 1);
+            mbar_init(bar_empty + 8 * s, 2);  // both MMA issuers (see the release rule below)
         }
         for (int b = 0; b < kAcc; ++b) {
             mbar_init(bar_tfull + 8 * b, 1);
             mbar_init(bar_tempty + 8 * b, kEpiWarps);
         }
+        mbar_init(bar_stagger, 1);
+        mbar_init(bar_stagger + 8, 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     if (warp == kMmaWarp) {
@@ -189,7 +200,7 @@ __global__ void __launch_bounds__(kThreads, 1) stem_s2_kernel(const __grid_const
             return start(p.item + (int)gridDim.x);
         };
         auto load = [&](const PairPos &p, float2(&v)[12]) {
-            const bool live = p.item < g.items;
+            const bool live = p.item < g.items && !(g.dbg & 1);
 #pragma unroll
             for (int r = 0; r < 2; ++r) {
                 const int y = 2 * p.jp - kPad + r;
@@ -212,8 +223,9 @@ __global__ void __launch_bounds__(kThreads, 1) stem_s2_kernel(const __grid_const
         while (p0.item < g.items) {
             load(p2, v2);
             const int slot = pc % kNP;
-            wait_backoff(bar_empty + 8 * slot, ((pc / kNP) & 1) ^ 1);
-            if (act) {
+            wait_parked(bar_empty + 8 * slot, ((pc / kNP) & 1) ^ 1);
+            if (q == 0) trace(g, 0, pc);
+            if (act && !(g.dbg & 64)) {
                 const uint32_t dst = base + slot * kPairB + q * 16;
 #pragma unroll
                 for (int rc = 0; rc < 2 * kC; ++rc) {
@@ -236,26 +248,44 @@ __global__ void __launch_bounds__(kThreads, 1) stem_s2_kernel(const __grid_const
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(bar_full + 8 * slot);
+            if (q == 0) trace(g, 1, pc);
             ++pc;
             p0 = p1, p1 = p2, p2 = next(p2);
 #pragma unroll
             for (int i = 0; i < 12; ++i) v0[i] = v1[i], v1[i] = v2[i];
         }
-    } else if (warp == kMmaWarp) {
+    } else if (warp >= kMmaWarp) {
         // ------------------------------------------------------------ MMA issue
+        // Two issuer threads take alternate conv rows, unsynchronised: a single thread
+        // issues one MMA per ~60 cycles plus ~360 cycles of barrier work per row and
+        // starves the pipe (56 cycles per MMA).  Rows use different accumulators, so
+        // their MMAs may interleave freely.  tcgen05.commit only tracks the issuing
+        // thread's MMAs, hence every ring slot is released by two commits: one from each
+        // of the last two rows that read it (count 2; the first row of a band, which has
+        // no predecessor, commits twice).
+        const int which = warp - kMmaWarp;
         if (lane == 0) {
             // no-swizzle K-major descriptor: LBO = 32 B (K chunk 1 = two entries on),
             // SBO = 128 B (8 pixels), version 1
             const uint64_t dbase = ((uint64_t)(32 >> 4) << 16) | ((uint64_t)(128 >> 4) << 32) | ((uint64_t)1 << 46);
+            auto rel = [&](int p) { umma_commit(bar_empty + 8 * (p % kNP)); };
             int pc0 = 0, it = 0;
             for (int item = blockIdx.x; item < g.items; item += gridDim.x) {
                 const Rows r = item_rows(g, item);
-                for (int oy = r.oy_s; oy <= r.oy_e; ++oy, ++it) {
+                const int n = r.oy_e - r.oy_s + 1;
+                for (int rr = 0; rr < n; ++rr, ++it) {
+                    if ((it & 1) != which) continue;
                     const int buf = it % kAcc;
-                    mbar_wait(bar_tempty + 8 * buf, ((it / kAcc) & 1) ^ 1);
-                    const int pc = pc0 + (oy - r.oy_s);  // the pair holding input rows 2 oy - 3, 2 oy - 2
-                    mbar_wait(bar_full + 8 * ((pc + 3) % kNP), ((pc + 3) / kNP) & 1);
+                    wait_parked(bar_tempty + 8 * buf, ((it / kAcc) & 1) ^ 1);
+                    const int pc = pc0 + rr;  // the pair holding input rows 2 oy - 3, 2 oy - 2
+                    wait_parked(bar_full + 8 * ((pc + 3) % kNP), ((pc + 3) / kNP) & 1);
+                    // half-row stagger, enforced every row: a row starts only once the other
+                    // issuer is half way through the row before it.  In phase (where equal
+                    // sharing of the pipe would keep them) both issuers would do their per-row
+                    // barrier work at the same time with the pipe idle.
+                    if (it > 0) wait_parked(bar_stagger + 8 * (which ^ 1), ((it - 1) >> 1) & 1);
                     fence_after();
+                    if (which == 0) trace(g, 2, it);
                     uint64_t sb[4];
 #pragma unroll
                     for (int i = 0; i < 4; ++i)
@@ -263,20 +293,30 @@ __global__ void __launch_bounds__(kThreads, 1) stem_s2_kernel(const __grid_const
                     const uint32_t d = tmem + buf * kOW;
 #pragma unroll
                     for (int s = 0; s < kSlices; ++s) {
+                        if (s == kSlices / 2) mbar_arrive(bar_stagger + 8 * which);
+                        if (g.dbg & 2) continue;
                         const int c = s / kKH, ky = s % kKH;
                         const uint64_t dh = sb[ky >> 1] + (uint64_t)((((ky & 1) * kC + c) * 2 * kRowB) >> 4);
                         mma_ts(d, tmem + kACol0 + 8 * s, dh, s != 0);
                         mma_ts(d, tmem + kACol0 + 8 * s, dh + (uint64_t)(kRowB >> 4), 1u);
                     }
-                    umma_commit(bar_empty + 8 * (pc % kNP));
-                    if (oy == r.oy_e) {  // the band's last row also releases its look-ahead pairs
-                        umma_commit(bar_empty + 8 * ((pc + 1) % kNP));
-                        umma_commit(bar_empty + 8 * ((pc + 2) % kNP));
-                        umma_commit(bar_empty + 8 * ((pc + 3) % kNP));
+                    // pair p is last read by row min(p, last row) and the row before it
+                    rel(pc);
+                    if (rr == 0) rel(pc);
+                    if (rr == n - 1) {
+                        for (int k = 1; k <= 3; ++k) {
+                            rel(pc + k);
+                            if (n == 1) rel(pc + k);
+                        }
+                    } else if (rr + 1 < n - 1) {
+                        rel(pc + 1);
+                    } else {  // the next row is the band's last: its own pair and its look-ahead pairs
+                        for (int k = 1; k <= 4; ++k) rel(pc + k);
                     }
                     umma_commit(bar_tfull + 8 * buf);
+                    if (which == 0) trace(g, 3, it);
                 }
-                pc0 += r.oy_e - r.oy_s + 4;
+                pc0 += n + 3;
             }
         }
         __syncwarp();
@@ -289,8 +329,9 @@ __global__ void __launch_bounds__(kThreads, 1) stem_s2_kernel(const __grid_const
         const float bn_mean = g.raw ? 0.0f : __ldg(g.mean + f), bn_inv = g.raw ? 0.0f : __ldg(g.inv + f);
         const float bn_gamma = g.raw ? 0.0f : __ldg(g.gamma + f), bn_beta = g.raw ? 0.0f : __ldg(g.beta + f);
         const float bias = (g.raw && g.bias) ? __ldg(g.bias + f) : 0.0f;
-        const int col0 = 56 * h + 28 * sub;  // this thread's conv columns col0 .. col0 + 27 (s[1..28])
         const int pcol0 = 28 * h + 14 * sub;  // and pooled columns pcol0 .. pcol0 + 13
+        float *tb = reinterpret_cast<float *>(smem + kOffTr) + warp * 16 * kTPitch;  // this warp's store transpose
+        const int fl = lane & 15;
         float cur[14];
         int it = 0;
         for (int item = blockIdx.x; item < g.items; item += gridDim.x) {
@@ -299,7 +340,6 @@ __global__ void __launch_bounds__(kThreads, 1) stem_s2_kernel(const __grid_const
             for (int i = 0; i < 14; ++i) cur[i] = -INFINITY;
             // BN -> ReLU of a finished pooled row (undo the sign), store it and its sign bits
             auto finish = [&](int py, const float(&mx)[14]) {
-                float *yrow = g.y + (((int64_t)r.b * kNF + f) * g.PH + py) * kPW + pcol0;
                 float o[14];
                 uint32_t mine = 0;
                 float nf = 0.0f;
@@ -315,9 +355,17 @@ __global__ void __launch_bounds__(kThreads, 1) stem_s2_kernel(const __grid_const
                         nf = __fmaf_rn(v, 0.0f, nf);
                     }
                 }
+                // through the warp's transpose buffer: one 112-byte run per filter and store
+                // instead of 32 scattered 8-byte pieces
 #pragma unroll
-                for (int j = 0; j < 14; j += 2)
-                    *reinterpret_cast<float2 *>(yrow + j) = make_float2(o[j], o[j + 1]);
+                for (int j = 0; j < 14; ++j) tb[fl * kTPitch + 14 * sub + j] = o[j];
+                __syncwarp();
+                if (lane < 28) {
+                    float *yw = g.y + (((int64_t)r.b * kNF + 16 * q) * g.PH + py) * kPW + 28 * h + lane;
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) yw[(int64_t)k * g.PH * kPW] = tb[k * kTPitch + lane];
+                }
+                __syncwarp();
                 if (g.pack16) {
                     if ((lane & 15) < 14) {
                         const int64_t pix = ((int64_t)r.b * g.PH + py) * kPW + pcol0 + (lane & 15);
@@ -328,15 +376,20 @@ __global__ void __launch_bounds__(kThreads, 1) stem_s2_kernel(const __grid_const
             };
             for (int oy = r.oy_s; oy <= r.oy_e; ++oy, ++it) {
                 const int buf = it % kAcc;
-                mbar_wait_sleep(bar_tfull + 8 * buf, (it / kAcc) & 1);
+                wait_parked(bar_tfull + 8 * buf, (it / kAcc) & 1);
                 fence_after();
+                if (tid == 0) trace(g, 4, it);
+                if (tid == 0 && it >= 64 && (it & 7) == 0) trace(g, 7, 2 + ((it - 64) >> 3));
                 // v[i] <-> conv column 56 h - 1 + i
                 uint32_t v[57];
                 const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + buf * kOW + 56 * h;
 #pragma unroll
-                for (int k = 0; k < 7; ++k) ld8(ta + 8 * k, v + 1 + 8 * k);
+                for (int k = 0; k < 7; ++k) v[1 + 8 * k] = 0u;  // (debug bit 32 leaves them unloaded)
+#pragma unroll
+                for (int k = 0; k < 7; ++k)
+                    if (!(g.dbg & 32)) ld8(ta + 8 * k, v + 1 + 8 * k);
                 v[0] = 0u;
-                if (h) {
+                if (h && !(g.dbg & 32)) {
                     uint32_t t8[8];
                     ld8(ta - 8, t8);
                     v[0] = t8[7];
@@ -345,6 +398,8 @@ __global__ void __launch_bounds__(kThreads, 1) stem_s2_kernel(const __grid_const
                 fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(bar_tempty + 8 * buf);
+                if (tid == 0) trace(g, 5, it);
+                if (g.dbg & 4) continue;
                 // hi + lo lane halves; the low 16 lanes keep columns v[0..28], the high 16
                 // lanes v[28..56]: s[i] <-> conv column col0 - 1 + i
                 float s[29];
@@ -358,12 +413,19 @@ __global__ void __launch_bounds__(kThreads, 1) stem_s2_kernel(const __grid_const
                     s[i] = __fadd_rn(a, b);
                 }
                 if (g.raw) {
-                    float *yrow = g.y + (((int64_t)r.b * kNF + f) * g.OH + oy) * kOW + col0;
 #pragma unroll
-                    for (int i = 0; i < 28; i += 4)
-                        __stcs(reinterpret_cast<float4 *>(yrow + i),
-                               make_float4(__fadd_rn(s[1 + i], bias), __fadd_rn(s[2 + i], bias),
-                                           __fadd_rn(s[3 + i], bias), __fadd_rn(s[4 + i], bias)));
+                    for (int i = 0; i < 28; i += 2)
+                        *reinterpret_cast<float2 *>(tb + fl * kTPitch + 28 * sub + i) =
+                            make_float2(__fadd_rn(s[1 + i], bias), __fadd_rn(s[2 + i], bias));
+                    __syncwarp();
+                    if (lane < 28) {  // 224 contiguous bytes per filter and store
+                        float *yw = g.y + (((int64_t)r.b * kNF + 16 * q) * g.OH + oy) * kOW + 56 * h + 2 * lane;
+#pragma unroll
+                        for (int k = 0; k < 16; ++k)
+                            __stcs(reinterpret_cast<float2 *>(yw + (int64_t)k * g.OH * kOW),
+                                   *reinterpret_cast<const float2 *>(tb + k * kTPitch + 2 * lane));
+                    }
+                    __syncwarp();
                     continue;
                 }
 #pragma unroll
@@ -381,6 +443,7 @@ __global__ void __launch_bounds__(kThreads, 1) stem_s2_kernel(const __grid_const
                 }
 #pragma unroll
                 for (int j = 0; j < 14; ++j) cur[j] = odd ? m[j] : fmaxf(cur[j], m[j]);
+                if (tid == 0) trace(g, 6, it);
             }
             // last pooled row without a conv row below it (odd OH)
             if (!g.raw && !(r.oy_e & 1) && (r.oy_e >> 1) < r.py1) finish(r.oy_e >> 1, cur);
@@ -388,6 +451,7 @@ __global__ void __launch_bounds__(kThreads, 1) stem_s2_kernel(const __grid_const
     }
     fence_before();
     __syncthreads();
+    if (tid == 0) trace(g, 7, 1);
     if (warp == kMmaWarp) {
         fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
@@ -416,6 +480,8 @@ int launch_stem_s2(const float *x, int64_t B, int64_t H, const float *w, const f
     g.pack16 = raw ? nullptr : reinterpret_cast<uint16_t *>(pack_words);
     g.pack_flags = pack_flags;
     g.relu = relu, g.raw = raw;
+    g.dbg = (int)(g_debug.stem_bits & (7 | 32 | 64));  // 32: no TMEM loads, 64: no loader stores
+    g.trace = (g_debug.stem_bits & 8) ? reinterpret_cast<long long *>(g_debug.trace_buf) : nullptr;
     g.H = (int)H, g.OH = (int)((H + 2 * kPad - kKH) / 2 + 1), g.PH = (g.OH - 1) / 2 + 1;
     g.rpb = raw ? 28 : 14;
     g.nbands = (int)ceil_div(raw ? g.OH : g.PH, g.rpb);
