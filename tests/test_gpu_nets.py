@@ -350,6 +350,41 @@ def test_fused_stem_sign_pack(nets):
     assert np.array_equal(out.words.cpu().numpy(), bnn.pack_nchw(out.f32).cpu().numpy())
 
 
+@pytest.mark.parametrize("shape", [(2, 3, 224, 224), (1, 3, 37, 224), (3, 3, 8, 224), (2, 3, 1, 224),
+                                   (1, 3, 225, 224), (5, 3, 58, 224)])
+def test_stride2_stem_kernel(nets, shape):
+    """The gather-free stride-2 stem kernel (bnn_stem_s2.cu; W = 224, conv7x7/2 pad 3, 64
+    filters): its raw conv output (with a bias) is f32-accurate against a float64
+    convolution, and its fused BN -> ReLU -> maxpool output and sign-packed words equal the
+    post-op applied to its own raw output bit for bit -- for odd heights, single-row
+    images, several bands per image and repeated launches."""
+    import torch.nn.functional as F
+    import paper_1705_09864_b200 as bnn
+    rng = np.random.default_rng(shape[0] * 1000 + shape[2])
+    conv = nets.Conv2d(3, 64, 7, stride=2, pad=3, bias=True, rng=rng)
+    conv.bias = rng.standard_normal(64).astype(np.float32)
+    x = torch.randn(shape, generator=torch.Generator().manual_seed(shape[2])).cuda()
+    y = conv.forward(x)
+    ref = F.conv2d(x.cpu().double(), torch.from_numpy(conv.weight).double(),
+                   torch.from_numpy(conv.bias).double(), stride=2, padding=3)
+    err = (y.cpu().double() - ref).abs()
+    assert y.shape == ref.shape
+    assert bool((err <= 1e-5 * ref.abs().clamp(min=1.0)).all()), float(err.max())
+    conv.bias = None
+    conv.__dict__.pop("_dev_cache", None)  # (device copies are cached per attribute)
+    post = nets.StemPost(64, rng, 3, 2, 1)
+    post.bn.gamma[::3] *= -1.0
+    post.bn.gamma[1] = 0.0
+    raw = conv.forward(x)
+    fused = post.forward_fused_conv(conv, x, pack=True)
+    assert isinstance(fused, nets.PackedNHWC)
+    assert torch.equal(fused.f32, post.forward(raw, bnn.INFER_FLOAT))
+    assert torch.equal(fused.f32, post.forward_fused_conv(conv, x))
+    assert np.array_equal(fused.words.cpu().numpy(), bnn.pack_nchw(fused.f32).cpu().numpy())
+    # repeated launches (ring / accumulator phases restart cleanly) are bit-identical
+    assert torch.equal(post.forward_fused_conv(conv, x), fused.f32)
+
+
 def test_classifier_head_is_batch_independent(nets):
     """bnn_avgpool_fc_f32 (GlobalAvgPool -> Dense): f32-accurate against float64 and each
     image's logits bit-identical in any batch / shard (what multi-GPU batch sharding
