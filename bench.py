@@ -520,9 +520,9 @@ def _kernel_families(plan):
     fam = {}
     for name, ms, ops in plan.kernel_breakdown():
         if name.startswith(("bnn_bconv2d", "bnn_xnor_gemm")):
-            key = "binary conv / GEMM (xnor_umma_kernel)"
+            key = "binary conv / GEMM (xnor_umma_kernel, xnor_sconv_kernel)"
         elif "f32_tc" in name:
-            key = "float stem (conv_pool_kernel, tcgen05 kind::tf32 x3)"
+            key = "float stem (stem_s2_kernel / conv_pool_kernel, tcgen05 kind::tf32 split)"
         else:
             key = "other (" + name + ")"
         f = fam.setdefault(key, {"ms": 0.0, "launches": 0, "binary_ops": 0})
@@ -633,7 +633,7 @@ def run_gpu_arm(args, rank, world, local_rank):
     if is_net:
         fams = _kernel_families(plan)
         step_dev = sum(f["ms"] for f in fams.values())
-        key = "binary conv / GEMM (xnor_umma_kernel)"
+        key = "binary conv / GEMM (xnor_umma_kernel, xnor_sconv_kernel)"
         bf = fams[key]
         peak = pipe_peak(args.algo, name)
         achieved = bf["binary_ops"] / (bf["ms"] * 1e-3) / 1e12
