@@ -1916,12 +1916,19 @@ int launch_sconv(const uint64_t *x, int64_t B, int64_t C, int64_t H, int64_t W,
                  int64_t ph, int64_t pw, int64_t oh, int64_t ow, float *y, const Epilogue &ep,
                  cudaStream_t s, const float *res);
 
+// stride-1 small-channel convs: shifted-window kernel (bnn_wconv.cu), every pixel expanded once
+int launch_wconv(const uint64_t *x, int64_t B, int64_t C, int64_t H, int64_t W, const uint64_t *w,
+                 int64_t F, int64_t kh, int64_t kw, int64_t sh, int64_t sw, int64_t ph, int64_t pw,
+                 int64_t oh, int64_t ow, float *y, const Epilogue &ep, cudaStream_t s, const float *res);
+
 template <class CS>
 static int launch_bconv2d_umma_t(const uint64_t *x, int64_t B, int64_t C, int64_t H, int64_t W,
                         const uint64_t *w, int64_t F, int64_t kh, int64_t kw, int64_t sh,
                         int64_t sw, int64_t ph, int64_t pw, int64_t oh, int64_t ow, float *y,
                         const Epilogue &ep, cudaStream_t s, const float *res) {
     if (ep.variant == 2 && !(umma_dbg() & 262144)) {
+        const int rw = launch_wconv(x, B, C, H, W, w, F, kh, kw, sh, sw, ph, pw, oh, ow, y, ep, s, res);
+        if (rw != BNN_EUNSUP) return rw;
         const int rc = launch_sconv(x, B, C, H, W, w, F, kh, kw, sh, sw, ph, pw, oh, ow, y, ep, s,
                                     res);
         if (rc != BNN_EUNSUP) return rc;
