@@ -54,6 +54,7 @@ struct Geom {
     float *y;           // f32 NCHW [B, F, OH, OW] (may be null)
     const float *res;   // residual, same layout (may be null)
     int B, H, W, Hp, Wp, OH, OW, kh, kw, ph, pw, K;
+    int Ftot, fgroups, nranges;  // all filters; groups of kF filters; tile ranges (grid = fgroups * nranges)
     int total_rows;     // B * Hp
     int P;              // positions: total_rows * Wp
     int ntiles, tpi;
@@ -87,7 +88,7 @@ struct Cfg {
 };
 
 struct Smem {
-    uint32_t w, band, pc, par, aff, thr, thu, popc_f, bars, tmem, total;
+    uint32_t w, band, pc, par, aff, thr, thu, popc_f, popc_ff, bars, tmem, total;
     __host__ __device__ Smem(int F, int K, int planes, int plane_bytes, int band_pos) {
         const int wblocks = (K + 255) / 256;
         w = 0;                                        // expanded weights (SW128 blocks, 1024-aligned)
@@ -98,7 +99,8 @@ struct Smem {
         thr = aff + 128 * 8;                          // float2 [128] sign thresholds (+ int [8] flags)
         thu = thr + 128 * 8 + 64;                     // float [128] compare thresholds U, u64 [2] flip masks
         popc_f = thu + 128 * 4 + 16;
-        bars = popc_f + 128 * 4;
+        popc_ff = popc_f + 128 * 4;                   // the same as f32 (no I2F per output element)
+        bars = popc_ff + 128 * 4;
         tmem = bars + 32 * 8;
         total = tmem + 16;
     }
@@ -157,6 +159,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     float *s_thu = reinterpret_cast<float *>(sgen + L.thu);
     uint32_t *s_flip = reinterpret_cast<uint32_t *>(sgen + L.thu + 128 * 4);  // [kF / 32]
     int32_t *s_popc_f = reinterpret_cast<int32_t *>(sgen + L.popc_f);
+    float *s_popc_ff = reinterpret_cast<float *>(sgen + L.popc_ff);
     const uint32_t bar_bfull = sbase + L.bars;               // [kBands] band expanded
     const uint32_t bar_bempty = bar_bfull + 8 * kBands;      // [kBands] MMAs + epilogue done with it
     const uint32_t bar_tfull = bar_bempty + 8 * kBands;      // [kAcc] accumulator ready
@@ -164,6 +167,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t *s_tmem = reinterpret_cast<uint32_t *>(sgen + L.tmem);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int ohw = g.OH * g.OW;
+    const int fg = blockIdx.x % g.fgroups, rg = blockIdx.x / g.fgroups;  // filter group, tile range
+    const int f0 = fg * kF;  // this CTA's first filter
     if (tid == 0) stamp(g, 7, 0);
 
     if (tid == 0) {
@@ -189,37 +194,67 @@ __global__ void __launch_bounds__(kThreads, 1)
     // programmatic dependent launch: the setup above overlaps the previous kernel
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
 
+    if (tid == 0) stamp(g, 7, 3);
     // ---- weights: expanded once into the SW128 K-major B operand (+ filter popcounts),
     // per-filter epilogue parameters and sign thresholds (same construction as bnn_sconv.cu)
     {
         const int kw32 = g.K / 32;
         const uint32_t *w32 = reinterpret_cast<const uint32_t *>(g.w);
-        for (int f = warp; f < kF; f += kThreads / 32) {
-            int32_t pc = 0;
-            for (int q = lane; q < kw32; q += 32) {
-                const uint32_t v = __ldg(w32 + (int64_t)f * kw32 + q);
-                pc += __popc(v);
-                uint32_t r4[4];
-                expand_fp4_b(v, r4);
-                const uint32_t addr = s_w + (q >> 3) * (kF * 128) + f * 128 + (((q & 7) ^ (f & 7)) << 4);
-                asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};\n" ::"r"(addr), "r"(r4[0]),
-                             "r"(r4[1]), "r"(r4[2]), "r"(r4[3]));
+        // (flat over the group's kF x kw32 words, eight loads in flight per thread: the
+        // group's rows are contiguous in the tap-major weight array; (filter, word) advance
+        // incrementally, no division per word)
+        const int total = kF * kw32;
+        const uint32_t *wg = w32 + (int64_t)f0 * kw32;
+        const int df = kThreads / kw32, dq = kThreads - df * kw32;
+        int wf = tid / kw32, wq = tid - wf * kw32;
+#pragma unroll 1
+        for (int base = tid; base < total; base += 8 * kThreads) {
+            uint32_t v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int idx = base + u * kThreads;
+                v[u] = idx < total ? __ldg(wg + idx) : 0u;
             }
 #pragma unroll
-            for (int d = 16; d >= 1; d >>= 1) pc += __shfl_xor_sync(0xffffffffu, pc, d);
-            if (lane == 0) s_popc_f[f] = pc;
+            for (int u = 0; u < 8; ++u) {
+                if (base + u * kThreads < total) {
+                    uint32_t r4[4];
+                    expand_fp4_b(v[u], r4);
+                    const uint32_t addr = s_w + (wq >> 3) * (kF * 128) + wf * 128 + (((wq & 7) ^ (wf & 7)) << 4);
+                    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};\n" ::"r"(addr), "r"(r4[0]),
+                                 "r"(r4[1]), "r"(r4[2]), "r"(r4[3]));
+                }
+                wf += df, wq += dq;
+                if (wq >= kw32) wq -= kw32, ++wf;
+            }
         }
+        // filter popcounts: a warp per filter (the words are L1 / L2 hits now), four filters'
+        // loads in flight
+#pragma unroll 1
+        for (int fb = warp * 4; fb < kF; fb += (kThreads / 32) * 4) {
+            int32_t pc[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (fb + u < kF)
+                    for (int q = lane; q < kw32; q += 32) pc[u] += __popc(__ldg(wg + (fb + u) * kw32 + q));
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int sum = __reduce_add_sync(0xffffffffu, pc[u]);
+                if (lane == 0 && fb + u < kF) s_popc_f[fb + u] = sum, s_popc_ff[fb + u] = (float)sum;
+            }
+        }
+        if (tid == 0) stamp(g, 7, 4);
         for (int f = tid; f < kF; f += kThreads) {
             float4 bp = make_float4(0.0f, 1.0f, 1.0f, 0.0f);
             if (ep.bn_mean != nullptr) {
-                bp.x = ep.bn_mean[f];
-                bp.y = ep.bn_inv[f];
-                bp.z = ep.bn_gamma[f];
-                bp.w = ep.bn_beta[f];
+                bp.x = ep.bn_mean[f0 + f];
+                bp.y = ep.bn_inv[f0 + f];
+                bp.z = ep.bn_gamma[f0 + f];
+                bp.w = ep.bn_beta[f0 + f];
             }
             float2 af = make_float2(1.0f, 0.0f);
-            if (ep.scale != nullptr) af.x = ep.scale[f];
-            if (ep.shift != nullptr) af.y = ep.shift[f];
+            if (ep.scale != nullptr) af.x = ep.scale[f0 + f];
+            if (ep.shift != nullptr) af.y = ep.shift[f0 + f];
             s_par[f] = bp;
             s_aff[f] = af;
         }
@@ -234,6 +269,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         fence_before();
         __syncthreads();
         fence_after();
+        if (tid == 0) stamp(g, 7, 5);
         // monotone sign thresholds for packed-only outputs: bit = S * a - V >= 0 on
         // a = 2C + (K - popc(pixel)) = P + popc(filter) (see bnn_sconv.cu)
         for (int f = tid; f < kF; f += kThreads) {
@@ -289,8 +325,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (tid == 0) stamp(g, 7, 1);
     // this CTA's contiguous tile range, in items of tpi tiles
-    const int tb = (int)((int64_t)blockIdx.x * g.ntiles / gridDim.x);
-    const int te = (int)((int64_t)(blockIdx.x + 1) * g.ntiles / gridDim.x);
+    const int tb = (int)((int64_t)rg * g.ntiles / g.nranges);
+    const int te = (int)((int64_t)(rg + 1) * g.ntiles / g.nranges);
     const int Wp = g.Wp;
     // first padded row and number of rows of the band of tiles [T0, T1)
     // items: the first one is short, so that the MMAs start after a small band
@@ -315,13 +351,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lw == 0 && lane == 0) stamp(g, 0, ii);
             const uint32_t band = s_band + bb * kPlanes * g.plane_bytes;
             int32_t *pcb = s_pc + bb * g.band_pos;
+            // kU rows (two 32-column passes each) per iteration: all loads in flight before
+            // the first expansion (Wp <= 64 is a launch precondition)
+            constexpr int kU = kCw <= 2 ? 4 : (kCw == 4 ? 2 : 1);
 #pragma unroll 1
-            for (int r0 = lw; r0 < nrows && !(g.dbg & 8); r0 += 4 * kLoadWarps) {
-                // four rows (two 32-column passes each) per iteration: all loads in flight
-                // before the first expansion (Wp <= 64 is a launch precondition)
-                uint64_t wd[4][2][kCw];
+            for (int r0 = lw; r0 < nrows && !(g.dbg & 8); r0 += kU * kLoadWarps) {
+                uint64_t wd[kU][2][kCw];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
+                for (int u = 0; u < kU; ++u) {
                     const int r = r0 + u * kLoadWarps, R = Ra + r;
                     const int b = R / g.Hp, iy = R - b * g.Hp - g.ph;
                     const bool rok = r < nrows && R < g.total_rows && (unsigned)iy < (unsigned)g.H && !(g.dbg & 4);
@@ -329,13 +366,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int it = 0; it < 2; ++it) {
                         const int ix = lane + 32 * it - g.pw;
-                        const bool ok = rok && (unsigned)ix < (unsigned)g.W;
+                        const bool ok = rok && (unsigned)ix < (unsigned)g.W && lane + 32 * it < Wp;
 #pragma unroll
                         for (int c = 0; c < kCw; ++c) wd[u][it][c] = ~0ull;  // out of image: "+1" (G2)
                         if (ok) {
-                            if constexpr (kCw == 2) {
-                                const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2 *>(xrow + (int64_t)ix * 2));
-                                wd[u][it][0] = v.x, wd[u][it][1] = v.y;
+                            if constexpr (kCw >= 2) {
+#pragma unroll
+                                for (int c = 0; c < kCw; c += 2) {
+                                    const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2 *>(
+                                        xrow + (int64_t)ix * kCw + c));
+                                    wd[u][it][c] = v.x, wd[u][it][c + 1] = v.y;
+                                }
                             } else {
                                 wd[u][it][0] = __ldg(xrow + ix);
                             }
@@ -343,7 +384,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
+                for (int u = 0; u < kU; ++u) {
                     const int r = r0 + u * kLoadWarps;
                     if (r >= nrows) break;
 #pragma unroll
@@ -488,6 +529,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             band_of(T0, T1, Ra, nrows);
             wait_parked(bar_bfull + 8 * bb, (ii >> 1) & 1);  // (the band's popcounts)
             const int32_t *pcb = s_pc + bb * g.band_pos;
+            bool released = false;
 #pragma unroll 1
             for (int T = T0; T < T1; ++T, ++tc) {
                 if ((tc & 1) != h) continue;
@@ -503,7 +545,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 const bool mok = t < (uint32_t)g.P && oy < (uint32_t)g.OH && col < (uint32_t)g.OW;
                 const int64_t m = ((int64_t)b * g.OH + oy) * g.OW + col;  // pixel index (NHWC order)
-                const int64_t obase = (int64_t)b * kF * ohw + (int64_t)oy * g.OW + col;
+                const int64_t obase = ((int64_t)b * g.Ftot + f0) * ohw + (int64_t)oy * g.OW + col;
                 int32_t pcs = 0;
                 {
                     const int32_t *pw0 = pcb + ((int)t - Ra * Wp);
@@ -518,6 +560,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
                 const float rowf = kf - (float)pcs;
+                if (T + 2 >= T1) {  // this warp's last tile of the item: the band's popcounts are consumed
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(bar_bempty + 8 * bb);
+                    released = true;
+                }
                 if (q == 0 && lane == 0) stamp(g, 4, tc);
                 // the first 32 columns' residuals: in flight while the tile's MMAs finish
                 float r[32];
@@ -554,7 +601,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             w2[j >> 5] |= dmask & (1u << (j & 31));
                         }
                         bits = ((uint64_t)(w2[1] ^ s_flip[(c0 >> 5) + 1]) << 32) | (w2[0] ^ s_flip[c0 >> 5]);
-                        if (mok) pack64[m * pack_ld64 + (c0 >> 6)] = bits;
+                        if (mok) pack64[m * pack_ld64 + ((f0 + c0) >> 6)] = bits;
                         continue;
                     }
                     float nf = 0.0f;
@@ -572,7 +619,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int j = 0; j < 32; ++j) {
                             const int n = c1 + j;
                             // P = K - popc(pixel) - popc(filter) + 2C, exact in f32
-                            const float P = __fmaf_rn(2.0f, __uint_as_float(v[j]), rowf - (float)s_popc_f[n]);
+                            const float P = __fmaf_rn(2.0f, __uint_as_float(v[j]), rowf - s_popc_ff[n]);
                             float x = dot ? __fmaf_rn(2.0f, P, -kf) : P;
                             if (affine) {
                                 const float2 a = s_aff[n];
@@ -605,7 +652,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     if constexpr (kPack) {
                         if (mok) {
-                            pack64[m * pack_ld64 + (c0 >> 6)] = bits;
+                            pack64[m * pack_ld64 + ((f0 + c0) >> 6)] = bits;
                             if (ep.pack_flags && nf != 0.0f) atomicOr(ep.pack_flags, BNN_FLAG_NONFINITE);
                         }
                     }
@@ -615,8 +662,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (lane == 0) mbar_arrive(bar_tempty + 8 * buf);
                 if (q == 0 && lane == 0) stamp(g, 6, tc);
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(bar_bempty + 8 * bb);  // (the band's popcounts are consumed)
+            if (!released) {  // (no tile of this warp's parity in the item)
+                __syncwarp();
+                if (lane == 0) mbar_arrive(bar_bempty + 8 * bb);
+            }
         }
     }
     fence_before();
@@ -626,21 +675,27 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 }  // namespace wconv
 
-// Eligible: stride 1, C in {64, 128}, F in {64, 128}, kh, kw <= 3, padding <= kernel - 1,
-// positions < 2^24 and a double-buffered band that fits in SMEM next to the weights.
-// Returns BNN_EUNSUP otherwise (the caller tries bnn_sconv.cu, then the general engine).
+// Eligible: stride 1, C a multiple of 64 up to 512, F a multiple of 64, kh, kw <= 3, padding <=
+// kernel - 1, padded width <= 64, positions < 2^24, and two band buffers that fit in SMEM next to
+// one filter group's expanded weights (groups of 128 filters when they fit, else 64; a CTA
+// owns one filter group and a contiguous range of tiles).  Returns BNN_EUNSUP otherwise (the
+// caller tries bnn_sconv.cu, then the general engine).
 int launch_wconv(const uint64_t *x, int64_t B, int64_t C, int64_t H, int64_t W, const uint64_t *w,
                  int64_t F, int64_t kh, int64_t kw, int64_t sh, int64_t sw, int64_t ph, int64_t pw,
                  int64_t oh, int64_t ow, float *y, const Epilogue &ep, cudaStream_t s, const float *res) {
     using namespace wconv;
     const int64_t Cw = C / 64;
-    if (sh != 1 || sw != 1 || C % 64 != 0 || (Cw != 1 && Cw != 2) || (F != 64 && F != 128) || kh > 3 ||
-        kw > 3 || ph > kh - 1 || pw > kw - 1 || (g_debug.umma_bits & (1 << 19)))
+    if (sh != 1 || sw != 1 || C % 64 != 0 || (Cw != 1 && Cw != 2 && Cw != 4 && Cw != 8) || F % 64 != 0 ||
+        kh > 3 || kw > 3 || ph > kh - 1 || pw > kw - 1 || (g_debug.umma_bits & (1 << 19)))
         return BNN_EUNSUP;
+    // C >= 256 is built and parity-tested (debug bit 18 routes it here) but measured no faster
+    // than the TMA im2col engine on C2 / ResNet layers 3-4 (few tiles per CTA: the per-CTA weight
+    // expansion and the f32 store epilogue dominate), so those shapes keep the general engine
+    if (Cw > 2 && !(g_debug.umma_bits & (1 << 18))) return BNN_EUNSUP;
     if (ep.pack_out && (ep.pack_ld32 < F / 32 || (ep.pack_ld32 & 1) ||
                         (reinterpret_cast<uintptr_t>(ep.pack_out) & 7)))
         return BNN_EUNSUP;
-    if ((reinterpret_cast<uintptr_t>(x) & 15) != 0 && Cw == 2) return BNN_EUNSUP;
+    if ((reinterpret_cast<uintptr_t>(x) & 15) != 0 && Cw >= 2) return BNN_EUNSUP;
     const int64_t Hp = H + 2 * ph, Wp = W + 2 * pw;
     const int64_t total_rows = B * Hp, P = total_rows * Wp;
     if (P <= 0) return BNN_OK;
@@ -652,28 +707,35 @@ int launch_wconv(const uint64_t *x, int64_t B, int64_t C, int64_t H, int64_t W, 
     g.kh = (int)kh, g.kw = (int)kw, g.ph = (int)ph, g.pw = (int)pw, g.K = (int)(C * kh * kw);
     g.total_rows = (int)total_rows, g.P = (int)P;
     g.ntiles = (int)ceil_div(P, kRows);
+    g.Ftot = (int)F;
     g.dbg = (int)((g_debug.umma_bits >> 21) & 15);
     g.trace = (g_debug.umma_bits & 16) ? reinterpret_cast<long long *>(g_debug.trace_buf) : nullptr;
     const int planes = (int)(2 * Cw);
-    // the largest tpi <= 16 whose two band buffers fit
-    int tpi = 0;
-    for (int t = 16; t >= 1; --t) {
-        const int rows = (int)((t * kRows + (kh - 1) * Wp + (kw - 1) + Wp - 1) / Wp + 1);
-        const int pos = (int)(rows * Wp), pb = pos * 16;
-        const Smem L((int)F, g.K, planes, pb, pos);
-        if (L.total + 1024 <= 200 * 1024 && pb < (1 << 18)) {
-            tpi = t, g.band_rows = rows, g.band_pos = pos, g.plane_bytes = pb;
-            break;
+    // filter group size and the largest tpi <= 16 whose two band buffers fit
+    int FG = 0, tpi = 0;
+    for (int fgs = 128; fgs >= 64 && tpi == 0; fgs -= 64) {
+        if (F % fgs != 0) continue;
+        for (int t = 16; t >= 1; --t) {
+            const int rows = (int)((t * kRows + (kh - 1) * Wp + (kw - 1) + Wp - 1) / Wp + 1);
+            const int pos = (int)(rows * Wp), pb = pos * 16;
+            const Smem L(fgs, g.K, planes, pb, pos);
+            if (L.total + 1024 <= 225 * 1024 && pb < (1 << 18)) {
+                FG = fgs, tpi = t, g.band_rows = rows, g.band_pos = pos, g.plane_bytes = pb;
+                break;
+            }
         }
     }
     if (tpi == 0) return BNN_EUNSUP;
     g.tpi = tpi;
-    const Smem L((int)F, g.K, planes, g.plane_bytes, g.band_pos);
+    g.fgroups = (int)(F / FG);
+    const Smem L(FG, g.K, planes, g.plane_bytes, g.band_pos);
     const int smem = (int)L.total + 1024;
     int sms = bnn_device_sm_count();
     if (sms <= 0) sms = 148;
-    int grid = g.ntiles < sms ? g.ntiles : sms;
-    if (g_debug.grid_cap > 0 && grid > g_debug.grid_cap) grid = (int)g_debug.grid_cap;
+    if (g_debug.grid_cap > 0 && sms > g_debug.grid_cap) sms = (int)g_debug.grid_cap;
+    g.nranges = sms / g.fgroups < 1 ? 1 : sms / g.fgroups;
+    if (g.nranges > g.ntiles) g.nranges = g.ntiles;
+    const int grid = g.nranges * g.fgroups;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(kThreads);
@@ -686,7 +748,7 @@ int launch_wconv(const uint64_t *x, int64_t B, int64_t C, int64_t H, int64_t W, 
     cfg.numAttrs = 1;
     const bool pack = ep.pack_out != nullptr;
 #define BNN_WCONV(KF, KCW)                                                                          \
-    if (F == KF && Cw == KCW) {                                                                     \
+    if (FG == KF && Cw == KCW) {                                                                    \
         static bool configured = false;                                                             \
         if (!configured) {                                                                          \
             cudaFuncSetAttribute(xnor_wconv_kernel<KF, KCW, true>,                                  \
@@ -701,8 +763,12 @@ int launch_wconv(const uint64_t *x, int64_t B, int64_t C, int64_t H, int64_t W, 
     }
     BNN_WCONV(64, 1)
     BNN_WCONV(128, 1)
-    BNN_WCONV(128, 2)
     BNN_WCONV(64, 2)
+    BNN_WCONV(128, 2)
+    BNN_WCONV(64, 4)
+    BNN_WCONV(128, 4)
+    BNN_WCONV(64, 8)
+    BNN_WCONV(128, 8)
 #undef BNN_WCONV
     return BNN_EUNSUP;
 }

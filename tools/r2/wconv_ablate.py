@@ -10,7 +10,10 @@ from paper_1705_09864_b200.layers import PackedNHWC  # noqa: E402
 
 SHAPES = [(256, 64, 56, 56, 64, 3, 1, 1, "pack"), (256, 64, 56, 56, 64, 3, 1, 1, "res"),
           (256, 128, 28, 28, 128, 3, 1, 1, "pack"), (256, 128, 28, 28, 128, 3, 1, 1, "res"),
-          (1, 64, 56, 56, 64, 3, 1, 1, "pack"), (6, 64, 56, 56, 64, 3, 1, 1, "pack")]
+          (1, 64, 56, 56, 64, 3, 1, 1, "pack"), (6, 64, 56, 56, 64, 3, 1, 1, "pack"),
+          (32, 256, 28, 28, 256, 3, 1, 1, "plain"), (256, 256, 14, 14, 256, 3, 1, 1, "pack"),
+          (256, 256, 14, 14, 256, 3, 1, 1, "bnf32"), (256, 512, 7, 7, 512, 3, 1, 1, "pack"),
+          (256, 512, 7, 7, 512, 3, 1, 1, "bnf32")]
 bnn.load_library()
 rng = np.random.default_rng(0)
 
@@ -46,6 +49,10 @@ for i in idx:
     res = torch.randn((b, f, oh, ow), device="cuda")
     if kind == "pack":
         run = lambda: conv.forward_fused(xp, bn, pack_out=True, f32_out=False)  # noqa: E731
+    elif kind == "plain":
+        run = lambda: conv.forward_fused(xp)  # noqa: E731
+    elif kind == "bnf32":
+        run = lambda: conv.forward_fused(xp, bn)  # noqa: E731
     else:
         run = lambda: conv.forward_fused(xp, bn, residual=res, pack_out=True)  # noqa: E731
     for d in bits:

@@ -8,7 +8,7 @@ import paper_1705_09864_b200 as bnn  # noqa: E402
 from paper_1705_09864_b200 import nets, _lib  # noqa: E402
 from paper_1705_09864_b200.layers import PackedNHWC  # noqa: E402
 
-SHAPES = [(256, 64, 56, 56, 64, 3, 1, 1, "pack"), (256, 64, 56, 56, 64, 3, 1, 1, "res"),
+SHAPES = [(256, 64, 56, 56, 64, 3, 1, 1, "pack"), (256, 64, 56, 56, 64, 3, 1, 1, "res"), (32, 256, 28, 28, 256, 3, 1, 1, "plain"),
           (256, 128, 28, 28, 128, 3, 1, 1, "pack"), (256, 128, 28, 28, 128, 3, 1, 1, "res")]
 i = int(sys.argv[1]) if len(sys.argv) > 1 else 0
 extra = int(sys.argv[2]) if len(sys.argv) > 2 else 0
@@ -23,6 +23,7 @@ xp = PackedNHWC.from_f32(torch.randn((b, c, h, w), device="cuda"))
 oh, ow = conv.output_hw(h, w)
 res = torch.randn((b, f, oh, ow), device="cuda")
 run = (lambda: conv.forward_fused(xp, bn, pack_out=True, f32_out=False)) if kind == "pack" else \
+    (lambda: conv.forward_fused(xp)) if kind == "plain" else \
     (lambda: conv.forward_fused(xp, bn, residual=res, pack_out=True))
 for _ in range(3):
     run()
@@ -36,6 +37,7 @@ _lib.call("bnn_debug_set", _lib.DEBUG_UMMA_BITS, 0)
 lib.bnn_umma_trace(None)
 t = tr.view(8, 64).cpu().numpy()
 t0 = int(t[7, 0])
+print("prologue stamps (after alloc+pdl wait, after weights, after params/sf):", [int(t[7, k]) - t0 for k in (3, 4, 5)])
 print(f"shape {SHAPES[i]}: entry 0, prologue done {int(t[7, 1]) - t0}, exit {int(t[7, 2]) - t0} cycles")
 names = ["ld bempty ok", "ld arrived", "mma tempty ok", "mma committed", "epi coords", "epi tfull", "epi end"]
 print("idx  " + " ".join(f"{n:>13s}" for n in names) + "   (loader idx = item, others = tile; epilogue = warp 0 / 4 by parity)")
