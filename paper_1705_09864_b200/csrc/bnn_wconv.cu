@@ -44,7 +44,8 @@ using umma::sw128_desc;
 using umma::umma_commit;
 
 constexpr int kRows = 128;
-constexpr int kEpiWarps = 8, kLoadWarp0 = 8, kLoadWarps = 4, kMmaWarp = 12;
+// (12 warps: registers are allocated per 4 warps, so a 13th warp would cap every thread at 128)
+constexpr int kEpiWarps = 8, kLoadWarp0 = 8, kLoadWarps = 3, kMmaWarp = 11;
 constexpr int kThreads = (kMmaWarp + 1) * 32;
 constexpr int kBands = 2;
 
@@ -228,15 +229,24 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (wq >= kw32) wq -= kw32, ++wf;
             }
         }
+        if (tid == 0) stamp(g, 7, 6);
         // filter popcounts: a warp per filter (the words are L1 / L2 hits now), four filters'
         // loads in flight
 #pragma unroll 1
         for (int fb = warp * 4; fb < kF; fb += (kThreads / 32) * 4) {
             int32_t pc[4] = {0, 0, 0, 0};
+            uint32_t wv[4][5];  // (kw32 <= 160: C * kh * kw <= 5120; all loads in flight)
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-                if (fb + u < kF)
-                    for (int q = lane; q < kw32; q += 32) pc[u] += __popc(__ldg(wg + (fb + u) * kw32 + q));
+#pragma unroll
+                for (int i = 0; i < 5; ++i) {
+                    const int q = lane + 32 * i;
+                    wv[u][i] = (fb + u < kF && q < kw32) ? __ldg(wg + (fb + u) * kw32 + q) : 0u;
+                }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int i = 0; i < 5; ++i) pc[u] += __popc(wv[u][i]);
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int sum = __reduce_add_sync(0xffffffffu, pc[u]);
@@ -566,12 +576,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                     released = true;
                 }
                 if (q == 0 && lane == 0) stamp(g, 4, tc);
-                // the first 32 columns' residuals: in flight while the tile's MMAs finish
-                float r[32];
+                // the first 64 columns' residuals: in flight while the tile's MMAs finish
+                float r[64];
                 const bool use_res = g.res != nullptr && mok;
                 if (use_res) {
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) r[j] = __ldg(g.res + obase + (int64_t)j * ohw);
+                    for (int j = 0; j < 64; ++j) r[j] = __ldg(g.res + obase + (int64_t)j * ohw);
                 }
                 if (g.dbg & 4) wait_parked(bar_tfull + 8 * buf, (uint32_t)(tc / kAcc) & 1u);
                 else {
@@ -605,12 +615,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                         continue;
                     }
                     float nf = 0.0f;
-#pragma unroll 1
-                    for (int c1 = c0; c1 < c0 + 64; c1 += 32) {
-                        if (use_res && c1 != 0) {
+                    if (use_res && c0 != 0) {
 #pragma unroll
-                            for (int j = 0; j < 32; ++j) r[j] = __ldg(g.res + obase + (int64_t)(c1 + j) * ohw);
-                        }
+                        for (int j = 0; j < 64; ++j) r[j] = __ldg(g.res + obase + (int64_t)(c0 + j) * ohw);
+                    }
+#pragma unroll
+                    for (int c1 = c0; c1 < c0 + 64; c1 += 32) {
                         uint32_t v[32];  // counts C, then (in place) the f32 outputs
                         ld16(tacc + c1, v);
                         ld16(tacc + c1 + 16, v + 16);
@@ -629,7 +639,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 const float4 bp = s_par[n];  // reference op order, layers.py:598-602
                                 x = __fadd_rn(__fmul_rn(bp.z, __fmul_rn(__fsub_rn(x, bp.x), bp.y)), bp.w);
                             }
-                            if (use_res) x = __fadd_rn(x, r[j]);
+                            if (use_res) x = __fadd_rn(x, r[(c1 - c0) + j]);
                             v[j] = __float_as_uint(x);
                         }
                         if (mok) {
@@ -688,10 +698,10 @@ int launch_wconv(const uint64_t *x, int64_t B, int64_t C, int64_t H, int64_t W, 
     if (sh != 1 || sw != 1 || C % 64 != 0 || (Cw != 1 && Cw != 2 && Cw != 4 && Cw != 8) || F % 64 != 0 ||
         kh > 3 || kw > 3 || ph > kh - 1 || pw > kw - 1 || (g_debug.umma_bits & (1 << 19)))
         return BNN_EUNSUP;
-    // C >= 256 is built and parity-tested (debug bit 18 routes it here) but measured no faster
+    // C >= 256 is built and parity-tested (debug bit 17 routes it here) but measured no faster
     // than the TMA im2col engine on C2 / ResNet layers 3-4 (few tiles per CTA: the per-CTA weight
     // expansion and the f32 store epilogue dominate), so those shapes keep the general engine
-    if (Cw > 2 && !(g_debug.umma_bits & (1 << 18))) return BNN_EUNSUP;
+    if (Cw > 2 && !(g_debug.umma_bits & (1 << 17))) return BNN_EUNSUP;
     if (ep.pack_out && (ep.pack_ld32 < F / 32 || (ep.pack_ld32 & 1) ||
                         (reinterpret_cast<uintptr_t>(ep.pack_out) & 7)))
         return BNN_EUNSUP;
