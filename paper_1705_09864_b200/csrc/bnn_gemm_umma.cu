@@ -13,11 +13,19 @@ int launch_bconv2d_umma_pk(const uint64_t *x, int64_t B, int64_t C, int64_t H, i
                            int64_t sw, int64_t ph, int64_t pw, int64_t oh, int64_t ow, float *y,
                            const Epilogue &ep, cudaStream_t s, const float *res);
 
+int launch_xnor_gemm_splitk(const uint64_t *A, int64_t lda, const uint64_t *B, int64_t ldb, int64_t M,
+                            int64_t N, int64_t K, float *C, int64_t ldc_m, int64_t ldc_n,
+                            const Epilogue &ep, cudaStream_t s, const float *res);
+
 int launch_xnor_gemm_umma(const uint64_t *A, int64_t lda, const uint64_t *B, int64_t ldb,
                           int64_t M, int64_t N, int64_t K, float *C, int64_t ldc_m, int64_t ldc_n,
                           const Epilogue &ep, cudaStream_t s, const float *res) {
     if (ep.pack_out)
         return launch_xnor_gemm_umma_pk(A, lda, B, ldb, M, N, K, C, ldc_m, ldc_n, ep, s, res);
+    if (ep.variant == 2) {  // small GEMMs: one cluster per row tile, in-kernel split-K
+        const int rc = launch_xnor_gemm_splitk(A, lda, B, ldb, M, N, K, C, ldc_m, ldc_n, ep, s, res);
+        if (rc != BNN_EUNSUP) return rc;
+    }
     return launch_xnor_gemm_umma_t<GemmStore>(A, lda, B, ldb, M, N, K, C, ldc_m, ldc_n, ep, s, res);
 }
 

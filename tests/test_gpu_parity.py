@@ -616,6 +616,46 @@ def test_randomized_shapes_umma_routes_equal_popc(bnn):
         assert np.array_equal(outs[2], outs[0]), ("conv", i)
 
 
+@pytest.mark.parametrize("m,n,k", [(1024, 256, 4096), (1000, 200, 4096), (130, 17, 1024), (128, 256, 2048),
+                                   (77, 64, 3000), (2304, 129, 4033), (300, 1, 1088), (64, 256, 1024)])
+def test_small_gemm_cluster_split_k(bnn, m, n, k):
+    """The in-kernel split-K route (bnn_gemm_splitk.cu: an 8-CTA cluster per 128-row tile, DSMEM
+    reduction of exact integer partials) against the independently tested POPC engine: both
+    domains, every pad-fill combination, affine epilogue, residual, [N, M] output, ragged M / N /
+    K, K slices that leave some cluster ranks empty; repeated launches are bit-identical."""
+    from paper_1705_09864_b200 import _lib
+    W = (k + 63) // 64
+    g = torch.Generator(device="cuda").manual_seed(m * 3 + n * 5 + k)
+    a = torch.randint(-2**63, 2**63 - 1, (m, W), device="cuda", generator=g).view(torch.uint64)
+    b = torch.randint(-2**63, 2**63 - 1, (n, W), device="cuda", generator=g).view(torch.uint64)
+    sc = torch.randn(m, device="cuda", generator=g)
+    sh = torch.randn(m, device="cuda", generator=g)
+    for ap, bp in ((0, 0), (1, 0), (0, 1), (1, 1)):
+        if k % 64:
+            mask = (1 << (k % 64)) - 1
+            for t, pad in ((a, ap), (b, bp)):
+                last = t.view(torch.int64)[:, -1]
+                last &= mask
+                if pad:
+                    last |= ~mask
+        for dom in (_lib.POPCOUNT, _lib.DOT):
+            ref = bnn.xnor_rows_gemm(a, b, k, a_pad=ap, b_pad=bp, algo="popc", domain=dom)
+            got = bnn.xnor_rows_gemm(a, b, k, a_pad=ap, b_pad=bp, algo="umma", domain=dom)
+            assert torch.equal(got, ref), (m, n, k, ap, bp, dom)
+            assert torch.equal(bnn.xnor_rows_gemm(a, b, k, a_pad=ap, b_pad=bp, algo="umma", domain=dom), ref)
+    ref = bnn.xnor_rows_gemm(a, b, k, algo="popc", domain=_lib.DOT, scale=sc, shift=sh, transpose_out=True)
+    got = bnn.xnor_rows_gemm(a, b, k, algo="umma", domain=_lib.DOT, scale=sc, shift=sh, transpose_out=True)
+    assert got.shape == (n, m) and torch.equal(got, ref)
+    # the route is really the cluster kernel for these shapes: turning it off (debug bit 15)
+    # gives the same numbers from the general engine
+    _lib.call("bnn_debug_set", _lib.DEBUG_UMMA_BITS, 1 << 15)
+    try:
+        assert torch.equal(bnn.xnor_rows_gemm(a, b, k, algo="umma", domain=_lib.DOT, scale=sc, shift=sh,
+                                              transpose_out=True), ref)
+    finally:
+        _lib.call("bnn_debug_set", _lib.DEBUG_UMMA_BITS, 0)
+
+
 def test_cta_pair_route_bit_exact(bnn, monkeypatch):
     """The experimental 2-CTA (cta_group::2) kind::mxf4 route, forced on through a fresh
     process (the threshold is read once per process): bit-exact against the POPC engine."""
