@@ -103,6 +103,15 @@ __device__ __forceinline__ void wait_parked(uint32_t bar, uint32_t phase) {
     } while (!done);
 }
 __device__ __forceinline__ uint32_t tf32_hi(float v) { return __float_as_uint(v) & 0xFFFFE000u; }
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n.reg .pred p;\n"
+        "elect.sync _|p, 0xffffffff;\n"
+        "selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(pred));
+    return pred != 0;
+}
 __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t bdesc, uint32_t acc) {
     asm volatile(
         "{\n.reg .pred p;\n"
@@ -264,11 +273,16 @@ __global__ void __launch_bounds__(kThreads, 1) stem_s2_kernel(const __grid_const
         // of the last two rows that read it (count 2; the first row of a band, which has
         // no predecessor, commits twice).
         const int which = warp - kMmaWarp;
-        if (lane == 0) {
+        // (the whole warp runs the loop with warp-uniform values -- descriptors and TMEM addresses
+        // stay in uniform registers, no R2UR per MMA operand; one elected lane issues)
+        {
             // no-swizzle K-major descriptor: LBO = 32 B (K chunk 1 = two entries on),
             // SBO = 128 B (8 pixels), version 1
             const uint64_t dbase = ((uint64_t)(32 >> 4) << 16) | ((uint64_t)(128 >> 4) << 32) | ((uint64_t)1 << 46);
-            auto rel = [&](int p) { umma_commit(bar_empty + 8 * (p % kNP)); };
+            auto rel = [&](int p) {
+                if (elect_one()) umma_commit(bar_empty + 8 * (p % kNP));
+                __syncwarp();
+            };
             int pc0 = 0, it = 0;
             for (int item = blockIdx.x; item < g.items; item += gridDim.x) {
                 const Rows r = item_rows(g, item);
@@ -285,21 +299,24 @@ __global__ void __launch_bounds__(kThreads, 1) stem_s2_kernel(const __grid_const
                     // barrier work at the same time with the pipe idle.
                     if (it > 0) wait_parked(bar_stagger + 8 * (which ^ 1), ((it - 1) >> 1) & 1);
                     fence_after();
-                    if (which == 0) trace(g, 2, it);
+                    if (which == 0 && lane == 0) trace(g, 2, it);
                     uint64_t sb[4];
 #pragma unroll
                     for (int i = 0; i < 4; ++i)
                         sb[i] = dbase + (uint64_t)((base + ((pc + i) % kNP) * kPairB) >> 4);
                     const uint32_t d = tmem + buf * kOW;
+                    if (elect_one()) {
 #pragma unroll
-                    for (int s = 0; s < kSlices; ++s) {
-                        if (s == kSlices / 2) mbar_arrive(bar_stagger + 8 * which);
-                        if (g.dbg & 2) continue;
-                        const int c = s / kKH, ky = s % kKH;
-                        const uint64_t dh = sb[ky >> 1] + (uint64_t)((((ky & 1) * kC + c) * 2 * kRowB) >> 4);
-                        mma_ts(d, tmem + kACol0 + 8 * s, dh, s != 0);
-                        mma_ts(d, tmem + kACol0 + 8 * s, dh + (uint64_t)(kRowB >> 4), 1u);
+                        for (int s = 0; s < kSlices; ++s) {
+                            if (s == kSlices / 2) mbar_arrive(bar_stagger + 8 * which);
+                            if (g.dbg & 2) continue;
+                            const int c = s / kKH, ky = s % kKH;
+                            const uint64_t dh = sb[ky >> 1] + (uint64_t)((((ky & 1) * kC + c) * 2 * kRowB) >> 4);
+                            mma_ts(d, tmem + kACol0 + 8 * s, dh, s != 0);
+                            mma_ts(d, tmem + kACol0 + 8 * s, dh + (uint64_t)(kRowB >> 4), 1u);
+                        }
                     }
+                    __syncwarp();
                     // pair p is last read by row min(p, last row) and the row before it
                     rel(pc);
                     if (rr == 0) rel(pc);
@@ -313,8 +330,9 @@ __global__ void __launch_bounds__(kThreads, 1) stem_s2_kernel(const __grid_const
                     } else {  // the next row is the band's last: its own pair and its look-ahead pairs
                         for (int k = 1; k <= 4; ++k) rel(pc + k);
                     }
-                    umma_commit(bar_tfull + 8 * buf);
-                    if (which == 0) trace(g, 3, it);
+                    if (elect_one()) umma_commit(bar_tfull + 8 * buf);
+                    __syncwarp();
+                    if (which == 0 && lane == 0) trace(g, 3, it);
                 }
                 pc0 += n + 3;
             }
