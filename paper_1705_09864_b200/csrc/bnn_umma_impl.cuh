@@ -409,6 +409,15 @@ __device__ __forceinline__ void mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_
         "r"(tmem_a), "l"(bdesc), "r"(kIdesc), "r"(accumulate));
 }
 
+__device__ __forceinline__ bool elect_one_sync() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n.reg .pred p;\n"
+        "elect.sync _|p, 0xffffffff;\n"
+        "selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(pred));
+    return pred != 0;
+}
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
     asm volatile(
         "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar)
@@ -993,7 +1002,10 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
         __syncwarp();
     } else if (warp == C::kMmaWarp) {
         // ================================================================ MMA issuer
-        if (lane == 0) {
+        // (the whole warp runs the loop with warp-uniform values, which the compiler keeps in
+        // uniform registers -- a single divergent lane pays an R2UR per MMA operand and falls
+        // behind the tensor pipe on wide tiles; one elected lane issues each MMA / commit)
+        {
             uint32_t gs = 0;
             const uint32_t kt32 = (uint32_t)ktiles;
             constexpr uint32_t kSub = C::kSub;
@@ -1007,7 +1019,8 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                     for (uint32_t kt = 0; kt < kt32; kt += kSub, ++gs) {
                         const int sb = (int)(gs % ES);
                         mbar_wait(bar_full + 8 * sb, (gs / ES) & 1u);
-                        mbar_arrive_cluster(mapa_shared(bar_full + 8 * sb, 0));
+                        if (lane == 0) mbar_arrive_cluster(mapa_shared(bar_full + 8 * sb, 0));
+                        __syncwarp();
                     }
                     continue;
                 }
@@ -1020,13 +1033,14 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                 for (uint32_t kt = 0; kt < kt32; kt += kSub, ++gs) {
                     const uint32_t nsub = kt32 - kt < kSub ? kt32 - kt : kSub;
                     const int sb = (int)(gs % ES);
-                    if (gs == 0) progress_mark(1, 1);
+                    if (gs == 0 && lane == 0) progress_mark(1, 1);
                     if constexpr (kPair) mbar_wait_cluster(bar_full + 8 * sb, (gs / ES) & 1u);
                     else mbar_wait(bar_full + 8 * sb, (gs / ES) & 1u);
-                    if (gs == 0) progress_mark(2, 2);
-                    tr(7, gs);
-                    if (gs == 0) trace(2);
+                    if (gs == 0 && lane == 0) progress_mark(2, 2);
+                    if (lane == 0) tr(7, gs);
+                    if (gs == 0 && lane == 0) trace(2);
                     fence_after();
+                    const bool leader = elect_one_sync();
                     if constexpr (kFp4) {
                         // K = 64 e2m1 per MMA = 32 bytes of the superstage row
                         const uint32_t a_addr = s_exp + sb * C::kSuperBytes;
@@ -1038,7 +1052,7 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                         const uint64_t db2 = sw128_desc(b_addr + C::kMmaN * 128);
                         const uint32_t sfc = tmem + C::kSfCol;
                         const uint32_t ta = tmem + C::kAStageCol + sb * C::kAStageCols;
-                        const int nk = (dbg & 2) ? 0 : 2 * (int)nsub;
+                        const int nk = ((dbg & 2) || !leader) ? 0 : 2 * (int)nsub;
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk) {
                             if (kk >= nk) break;
@@ -1058,7 +1072,7 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                     }
 #pragma unroll
                     for (uint32_t u = 0; u < kSub; ++u) {
-                        if (kFp4 || u >= nsub) break;
+                        if (kFp4 || u >= nsub || !leader) break;
                         const uint32_t stage = s_exp + sb * C::kSuperBytes + u * C::kStageBytes;
                         const uint32_t b_addr = stage + C::kStageA;
                         const uint64_t da = sw128_desc(stage), db = sw128_desc(b_addr);
@@ -1073,13 +1087,19 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                                 mma_ss<C::kIdesc>(d, da + 2 * kk, db + 2 * kk, acc);
                         }
                     }
-                    if constexpr (kPair) umma_commit_pair(bar_empty + 8 * sb);
-                    else umma_commit(bar_empty + 8 * sb);
-                    tr(8, gs);
+                    if (leader) {
+                        if constexpr (kPair) umma_commit_pair(bar_empty + 8 * sb);
+                        else umma_commit(bar_empty + 8 * sb);
+                    }
+                    __syncwarp();
+                    if (lane == 0) tr(8, gs);
                 }
-                if constexpr (kPair) umma_commit_pair(bar_tfull + 8 * buf);
-                else umma_commit(bar_tfull + 8 * buf);
-                if (it < 3) trace(3 + 3 * it);
+                if (elect_one_sync()) {
+                    if constexpr (kPair) umma_commit_pair(bar_tfull + 8 * buf);
+                    else umma_commit(bar_tfull + 8 * buf);
+                }
+                __syncwarp();
+                if (it < 3 && lane == 0) trace(3 + 3 * it);
             }
             // release TMEM as soon as the epilogue has drained the last two
             // accumulators, overlapping the dealloc with the final stores

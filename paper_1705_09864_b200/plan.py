@@ -39,6 +39,7 @@ class _Plan:
     # batch slices the end-to-end call is pipelined over (H2D of slice i+1, compute of
     # slice i and D2H of slice i-1 overlap; PCIe is full duplex); 1 = no pipelining
     host_chunks = 4
+    host_taper = None  # optional relative slice sizes overriding the equal split
 
     def run_host(self, x_host: torch.Tensor, y_host: torch.Tensor) -> torch.Tensor:
         """End to end from pinned host memory: H2D, pack, kernel, D2H, one sync.
@@ -49,7 +50,7 @@ class _Plan:
         pinned host buffers the whole schedule is captured once per (x_host,
         y_host) pair into a CUDA graph and replayed, so a call costs one launch.
         """
-        key = (x_host.data_ptr(), y_host.data_ptr(), self.host_chunks)
+        key = (x_host.data_ptr(), y_host.data_ptr(), self.host_chunks, tuple(self.host_taper or ()))
         graphs = self.__dict__.setdefault("_host_graphs", {})
         g = graphs.get(key)
         if g is None and x_host.is_pinned() and y_host.is_pinned():
@@ -74,7 +75,8 @@ class _Plan:
         return y_host
 
     def _host_schedule(self, x_host: torch.Tensor, y_host: torch.Tensor):
-        chunks = min(self.host_chunks, self.b) if hasattr(self, "run_device_range") else 1
+        chunks = min(len(self.host_taper) if self.host_taper else self.host_chunks, self.b) \
+            if hasattr(self, "run_device_range") else 1
         cur = torch.cuda.current_stream()
         self.flags.zero_()  # this call's flags only (a memset node inside the graph)
         if chunks <= 1:
@@ -88,6 +90,12 @@ class _Plan:
             for st in self._streams:
                 st.wait_stream(cur)
             bounds = [self.b * i // chunks for i in range(chunks + 1)]
+            if self.host_taper:  # relative slice sizes, e.g. (4, 2, 1): a short last slice = a short drain
+                tot, acc, bounds = sum(self.host_taper), 0, [0]
+                for wgt in self.host_taper:
+                    acc += wgt
+                    bounds.append(max(bounds[-1] + 1, self.b * acc // tot) if acc < tot else self.b)
+                bounds = [min(v, self.b) for v in bounds]
             for i0, i1 in zip(bounds[:-1], bounds[1:]):
                 with torch.cuda.stream(h2d):
                     self.x[i0:i1].copy_(x_host[i0:i1], non_blocking=True)
