@@ -273,3 +273,66 @@ def test_small_channel_conv_kernel(bnn, case, epi, grid_cap):
     layer.algo = "umma4"  # the general engine on the same inputs
     other = layer.forward_fused(xd, bn, residual=res, pack_out=pack)
     assert torch.equal(other.f32 if pack else other, y)
+
+
+# Shifted-window kernel (bnn_wconv.cu: stride 1, every pixel expanded once, taps = shifted
+# no-swizzle descriptors).  Geometries beyond the ResNet ones: asymmetric / zero padding,
+# non-square kernels and images, the widest padded row (Wp = 64), bands that cross images,
+# one-pixel images, 64 <-> 128 channel / filter mixes; C >= 256 with filter groups runs here
+# only behind debug bit 17 and is covered too.
+WCONV_CASES = [
+    (3, 64, 17, 62, 64, 3, 3, (1, 1), 31),
+    (2, 128, 9, 11, 64, 3, 3, (0, 1), 32),
+    (2, 64, 12, 7, 128, 3, 3, (1, 0), 33),
+    (4, 64, 6, 5, 128, 1, 3, (0, 1), 34),
+    (2, 128, 8, 8, 128, 3, 1, (1, 0), 35),
+    (5, 64, 1, 1, 64, 3, 3, (1, 1), 36),
+    (2, 64, 30, 30, 64, 2, 2, (1, 1), 37),
+    (9, 128, 4, 4, 128, 3, 3, (2, 2), 38),
+    (2, 256, 10, 12, 256, 3, 3, (1, 1), 39),
+    (2, 512, 5, 6, 192, 3, 3, (1, 1), 40),
+]
+
+
+@pytest.mark.parametrize("case", WCONV_CASES)
+@pytest.mark.parametrize("epi", ["plain", "bn_pack", "bn_res_pack"])
+def test_shifted_window_conv_kernel(bnn, case, epi, grid_cap):
+    from paper_1705_09864_b200 import _lib
+    from paper_1705_09864_b200.layers import PackedNHWC
+    b, c, h, w, f, kh, kw, pad, seed = case
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((b, c, h, w)).astype(np.float32)
+    x.reshape(-1)[::13] = 0.0
+    wt = rng.standard_normal((f, c, kh, kw)).astype(np.float32)
+    layer = bnn.QConvolution(c, f, (kh, kw), (1, 1), pad, domain="dot")
+    layer.weight = wt
+    layer.pack()
+    oh, ow = layer.output_hw(h, w)
+    xd = torch.from_numpy(x).cuda()
+    p = orc.qconv_packed(x, wt, (1, 1), pad).astype(np.float32)
+    ref = 2 * p - np.float32(c * kh * kw)
+    _lib.call("bnn_debug_set", _lib.DEBUG_UMMA_BITS, 1 << 17)  # C >= 256 on this kernel too
+    try:
+        if epi == "plain":
+            assert np.array_equal(layer.forward_fused(xd).cpu().numpy(), ref)
+            return
+        bn = _BN(f, c * kh * kw, seed)
+        bn.gamma[:3] = [0.0, -0.0, 1e-30]
+        bn.beta[:3] = [-0.0, 1.0, -1.0]
+        sh = (1, -1, 1, 1)
+        ref = bn.gamma.reshape(sh) * ((ref - bn.mean.reshape(sh)) * bn.inv.reshape(sh)) + bn.beta.reshape(sh)
+        res = None
+        if "res" in epi:
+            res = torch.from_numpy(rng.standard_normal((b, f, oh, ow)).astype(np.float32)).cuda()
+            ref = ref + res.cpu().numpy()
+        ref = ref.astype(np.float32)
+        out = layer.forward_fused(xd, bn, residual=res, pack_out=True)
+        assert isinstance(out, PackedNHWC)
+        assert np.array_equal(out.f32.cpu().numpy(), ref)
+        assert np.array_equal(out.words.cpu().numpy(), _oracle_pack_nhwc(ref))
+        only = layer.forward_fused(xd, bn, residual=res, pack_out=True, f32_out=False)
+        assert np.array_equal(only.words.cpu().numpy(), out.words.cpu().numpy())
+        again = layer.forward_fused(xd, bn, residual=res, pack_out=True, f32_out=False)
+        assert np.array_equal(again.words.cpu().numpy(), out.words.cpu().numpy())
+    finally:
+        _lib.call("bnn_debug_set", _lib.DEBUG_UMMA_BITS, 0)
