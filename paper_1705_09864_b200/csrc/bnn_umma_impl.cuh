@@ -541,6 +541,10 @@ __device__ __forceinline__ void store_row32(const uint32_t (&r)[8], uint32_t row
 
 struct TileMap {
     int tiles_m, ntiles;
+    // dense kind::mxf4 operands: superstages fetched per TMA load (1 or 2).  The TMA unit is
+    // row-rate bound on 32-byte rows (352 rows per superstage ~ 545 ns at 8192^3, exactly the
+    // superstage cadence): 64-byte rows (SWIZZLE_64B) halve the rows per K
+    int wide = 1;
     __device__ void decode(int t, int &tm, int &tn) const {
         tm = t % tiles_m;
         tn = t / tiles_m;
@@ -574,6 +578,10 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
     static_assert(kTma == is_tma<BLoad>::value && (!kTma || kPlanes == 1), "TMA: both operands");
     using C = Cfg<BN, kATmem, kPlanes, kTma, kFp4, kSets, kPair>;
     constexpr int ES = C::ES;
+    constexpr bool kWideOk = kTma && kFp4 && !kPair && !kATmem && BN <= 256 && C::kSub == 2 &&
+                             !std::is_same<BLoad, TmaConv>::value;
+    const uint32_t wide = kWideOk ? (uint32_t)tmap.wide : 1u;  // superstages per TMA load
+    const uint32_t nslots = (uint32_t)C::kTmaSlots / wide;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t sbase_raw = smem_u32(smem_raw);
     const uint32_t sbase = (sbase_raw + 1023u) & ~1023u;
@@ -614,7 +622,7 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
         }
         for (int r = 0; r < C::kTmaSlots; ++r) {
             mbar_init(bar_ld + 8 * r, 1);
-            mbar_init(bar_free + 8 * r, C::kProducerWarps);
+            mbar_init(bar_free + 8 * r, C::kProducerWarps * wide);
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
@@ -755,15 +763,19 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                     uint32_t wv[kSub][4], wv1[kSub][4] = {};
                     if constexpr (kTma) {
                         // this superstage's packed rows, landed by the TMA warp
-                        const uint32_t ts = gs % C::kTmaSlots;
-                        mbar_wait(bar_ld + 8 * ts, (gs / C::kTmaSlots) & 1u);
+                        const uint32_t gl = gs / wide, ts = gl % nslots;
+                        mbar_wait(bar_ld + 8 * ts, (gl / nslots) & 1u);
                         if (lane == 0 && (warp == 0 || warp == C::kProducerWarps - 1)) tr(warp ? 6 : 3, gs);
-                        const uint32_t rbase = s_pk + ts * C::kTmaSlotBytes +
-                                               (is_a ? row * kSub * 16 : C::kTmaA + row * kSub * 16);
+                        const uint32_t rbase = s_pk + ts * C::kTmaSlotBytes * wide +
+                                               (is_a ? row * kSub * 16 * wide
+                                                     : C::kTmaA * wide + row * kSub * 16 * wide);
     #pragma unroll
                         for (uint32_t u = 0; u < kSub; ++u) {
-                            // SWIZZLE_32B (kSub == 2): 16-B chunk u of row r sits at u ^ bit 2 of r
-                            const uint32_t a = rbase + (kSub == 2 ? ((u ^ ((row >> 2) & 1)) * 16) : 0);
+                            // SWIZZLE_32B (kSub == 2): 16-B chunk u of row r sits at u ^ bit 2 of r;
+                            // wide loads (64-byte rows, SWIZZLE_64B): chunk c = 2 (gs % 2) + u of row r
+                            // sits at c ^ bits 1-2 of r
+                            const uint32_t a = rbase + (wide == 2 ? (((gs & 1u) * kSub + u) ^ ((row >> 1) & 3)) * 16
+                                                                  : (kSub == 2 ? ((u ^ ((row >> 2) & 1)) * 16) : 0));
                             asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n"
                                          : "=r"(wv[u][0]), "=r"(wv[u][1]), "=r"(wv[u][2]), "=r"(wv[u][3])
                                          : "r"(a)
@@ -964,10 +976,10 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                     }
 #pragma unroll 1
                     for (uint32_t kt = 0; kt < kt32; kt += C::kSub, ++g) {
-                        const uint32_t ts = g % C::kTmaSlots;
-                        if (g >= (uint32_t)C::kTmaSlots)
-                            mbar_wait(bar_free + 8 * ts, ((g / C::kTmaSlots) - 1) & 1u);
-                        uint32_t dst = s_pk + ts * C::kTmaSlotBytes;
+                        if (wide == 2 && (g & 1u)) continue;  // fetched with the superstage before it
+                        const uint32_t gl = g / wide, ts = gl % nslots;
+                        if (gl >= nslots) mbar_wait(bar_free + 8 * ts, ((gl / nslots) - 1) & 1u);
+                        uint32_t dst = s_pk + ts * C::kTmaSlotBytes * wide;
                         uint32_t ldbar = bar_ld + 8 * ts;
                         if (kPair && (dbg & 131072)) {  // debug: explicit shared::cluster addresses
                             dst = mapa_shared(dst, crank);
@@ -975,7 +987,7 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                         }
                         tr(0, g);
                         if (g == 0) progress_mark(0, 1000 + (uint64_t)tm * 100 + tn);
-                        mbar_arrive_expect_tx(bar_ld + 8 * ts, C::kTmaA + C::kTmaB);
+                        mbar_arrive_expect_tx(bar_ld + 8 * ts, (C::kTmaA + C::kTmaB) * wide);
                         tma_load_2d(dst, &aload.map, (int)(kt * kWordsPerStage),
                                     tm * C::kTmBM + (int)crank * BM, ldbar);
                         if constexpr (std::is_same<BLoad, TmaConv>::value) {
@@ -988,7 +1000,7 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                                 if (++cj == bload.kw) cj = 0, ++ci;
                             }
                         } else {
-                            tma_load_2d(dst + C::kTmaA, &bload.map, (int)(kt * kWordsPerStage),
+                            tma_load_2d(dst + C::kTmaA * wide, &bload.map, (int)(kt * kWordsPerStage),
                                         tn * BN + (int)crank * C::kBRows, ldbar);
                             if constexpr (BN > 256)  // second box of a wide tile
                                 tma_load_2d(dst + C::kTmaA + C::kTmaBoxB * C::kSub * 16, &bload.map,
@@ -1630,8 +1642,9 @@ static int encode_rows(TmaRows &t, int box_words, int box_rows) {
     const cuuint64_t strides[1] = {(cuuint64_t)t.ld32 * 4};
     const cuuint32_t box[2] = {(cuuint32_t)box_words, (cuuint32_t)box_rows};
     const cuuint32_t estr[2] = {1, 1};
-    const CUtensorMapSwizzle sw = box_words * 4 == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
-                                                      : CU_TENSOR_MAP_SWIZZLE_NONE;
+    const CUtensorMapSwizzle sw = box_words * 4 == 32   ? CU_TENSOR_MAP_SWIZZLE_32B
+                                  : box_words * 4 == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                        : CU_TENSOR_MAP_SWIZZLE_NONE;
     CUresult r = fn(&t.map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint32_t *>(t.base), dims,
                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -1709,13 +1722,20 @@ static int launch_umma_cfg(const ALoad &a_in, const BLoad &b_in, const Store &st
     auto kern = umma::xnor_umma_kernel<BN, kATmem, kVec, ALoad, BLoad, Store, kPlanes, kFp4, kSets, kPair>;
     ALoad a = a_in;
     BLoad b = b_in;
+    // dense kind::mxf4 operands with K a multiple of 512 bits: two superstages per TMA load --
+    // built and parity-tested, but measured 3-5% slower at 8192^3 / 16384^3 (the TMA round trip drops
+    // from ~1.5 to ~0.9 us, yet the superstage cadence stays ~545 ns: the row rate of the TMA unit
+    // is not what paces the pipeline), so it is opt-in (debug bit 16384)
+    constexpr bool kWideOk = kTma && kFp4 && !kPair && !kATmem && BN <= 256 && C::kSub == 2 &&
+                             !std::is_same<BLoad, TmaConv>::value && C::kTmaSlots % 2 == 0;
+    const int wide = (kWideOk && kw32 % 16 == 0 && (umma_dbg() & 16384)) ? 2 : 1;
     if constexpr (kTma) {
-        int rc = encode_rows(a, 4 * C::kSub, umma::BM);
+        int rc = encode_rows(a, 4 * C::kSub * wide, umma::BM);
         if constexpr (std::is_same<BLoad, TmaConv>::value) {
             static_assert(C::kSub == 2, "im2col TMA: one 32-byte tap chunk per superstage");
             if (rc == BNN_OK) rc = encode_conv(b, 4 * C::kSub, C::kBRows, b.npix / ((int64_t)b.oh * b.ow));
         } else {
-            if (rc == BNN_OK) rc = encode_rows(b, 4 * C::kSub, C::kTmaBoxB);
+            if (rc == BNN_OK) rc = encode_rows(b, 4 * C::kSub * wide, C::kTmaBoxB);
         }
         if (rc != BNN_OK) return rc;
     }
@@ -1728,6 +1748,7 @@ static int launch_umma_cfg(const ALoad &a_in, const BLoad &b_in, const Store &st
     const int64_t ntiles = tiles_m * tiles_n;
     if (ntiles > (1ll << 30)) return set_error(BNN_EUNSUP, "too many tiles");
     umma::TileMap tmap{(int)tiles_m, (int)ntiles};
+    tmap.wide = wide;
     // one CTA (pair of CTAs) per SM (pair of SMs), persistent over the tiles
     const int64_t units = kPair ? sm_count() / 2 : sm_count();
     int grid = (int)((ntiles < units ? ntiles : units) * (kPair ? 2 : 1));
