@@ -49,6 +49,9 @@
 #include "bnn_loaders.cuh"
 
 // build-time tuning knobs of the kind::mxf4 engine (tools/build_variant.sh)
+#ifndef BNN_WAIT_SLEEP_NS
+#define BNN_WAIT_SLEEP_NS 0  // (32: measured -12% at 8192^3 -- polling warps take the expanders' issue slots)
+#endif
 #ifndef BNN_FP4_ES
 #define BNN_FP4_ES 3
 #endif
@@ -332,6 +335,19 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
     const bool watch = g_wait_log != nullptr;  // (one global load per wait, not per probe)
     do {
         if (watch && ++tries > (1u << 22)) wait_timeout(bar, phase, tries);
+#if BNN_WAIT_SLEEP_NS
+        // short sleeps between probes instead of parking in try_wait: parked warps on one
+        // barrier wake up one after another (the last of an expander set ~1 us after the
+        // first, tools/umma_stages_conv.py), and the stragglers pace every superstage
+        asm volatile(
+            "{\n.reg .pred p;\n"
+            "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(bar), "r"(phase)
+            : "memory");
+        if (!done) __nanosleep(BNN_WAIT_SLEEP_NS);
+#else
         asm volatile(
             "{\n.reg .pred p;\n"
             "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
@@ -339,6 +355,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
             : "=r"(done)
             : "r"(bar), "r"(phase), "r"(0x989680u)
             : "memory");
+#endif
     } while (!done);
 }
 // latency-critical waits: spin on test_wait (no suspension, so no wake-up latency
@@ -926,6 +943,8 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
                     }
                     __syncwarp();  // every lane's writes + fence precede the warp's arrival
                     if (lane == 0 && (warp == 0 || warp == C::kProducerWarps - 1)) tr(warp ? 5 : 2, gs);
+                    else if (lane == 0 && (warp % C::kProducerWarps) >= 1 && (warp % C::kProducerWarps) <= 7)
+                        tr(8 + (warp % C::kProducerWarps), gs);  // (debug timeline: the other warps' arrivals)
                     if (lane == 0) {
                         mbar_arrive(bar_full + 8 * sb);  // (pair: rank 1 relays to the leader)
                     }

@@ -41,10 +41,10 @@ plan.kernel()
 torch.cuda.synchronize()
 lib.bnn_umma_trace(None)
 t = tr[4096:].view(16, 256).cpu().numpy().astype(np.int64)
-names = ["tma_issue", "A_empty_ok", "A_done", "A_data", "B_empty_ok", "B_done", "B_data", "mma_full", "mma_commit"]
+names = ["tma_issue", "A_empty_ok", "A_done", "A_data", "B_empty_ok", "B_done", "B_data", "mma_full", "mma_commit"] + [f"w{i}_done" for i in range(1, 8)]
 t0 = t[7, 0]
 print("super " + " ".join(f"{x:>10s}" for x in names))
-for g in range(0, 24):
+for g in range(0, int(sys.argv[2]) if len(sys.argv) > 2 else 24):
     print(f"{g:5d} " + " ".join(f"{(t[ev, g] - t0) if t[ev, g] else -1:10d}" for ev in range(len(names))))
 c = tr[:148 * 16].view(148, 16).cpu().numpy().astype(np.float64)
 c = c[c[:, 0] > 0]  # CTAs of the launch (grid may be < 148)
