@@ -595,7 +595,7 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
     static_assert(kTma == is_tma<BLoad>::value && (!kTma || kPlanes == 1), "TMA: both operands");
     using C = Cfg<BN, kATmem, kPlanes, kTma, kFp4, kSets, kPair>;
     constexpr int ES = C::ES;
-    constexpr bool kWideOk = kTma && kFp4 && !kPair && !kATmem && BN <= 256 && C::kSub == 2 &&
+    constexpr bool kWideOk = kTma && kFp4 && !kATmem && BN <= 256 && C::kSub == 2 &&
                              !std::is_same<BLoad, TmaConv>::value;
     const uint32_t wide = kWideOk ? (uint32_t)tmap.wide : 1u;  // superstages per TMA load
     const uint32_t nslots = (uint32_t)C::kTmaSlots / wide;
@@ -1745,7 +1745,7 @@ static int launch_umma_cfg(const ALoad &a_in, const BLoad &b_in, const Store &st
     // built and parity-tested, but measured 3-5% slower at 8192^3 / 16384^3 (the TMA round trip drops
     // from ~1.5 to ~0.9 us, yet the superstage cadence stays ~545 ns: the row rate of the TMA unit
     // is not what paces the pipeline), so it is opt-in (debug bit 16384)
-    constexpr bool kWideOk = kTma && kFp4 && !kPair && !kATmem && BN <= 256 && C::kSub == 2 &&
+    constexpr bool kWideOk = kTma && kFp4 && !kATmem && BN <= 256 && C::kSub == 2 &&
                              !std::is_same<BLoad, TmaConv>::value && C::kTmaSlots % 2 == 0;
     const int wide = (kWideOk && kw32 % 16 == 0 && (umma_dbg() & 16384)) ? 2 : 1;
     if constexpr (kTma) {

@@ -13,8 +13,9 @@ for n in sizes:
     b = torch.randint(-2**63, 2**63 - 1, (n, n // 64), device="cuda", generator=g).view(torch.uint64)
     out = torch.empty((n, n), device="cuda")
     ref = None
-    for pair in (0, 1):
+    for pair, wide in ((0, 0), (0, 1), (1, 0), (1, 1)):
         _lib.call("bnn_debug_set", _lib.DEBUG_PAIR_KW32, 1 if pair else 0)
+        _lib.call("bnn_debug_set", _lib.DEBUG_UMMA_BITS, 16384 if wide else 0)
         run = lambda: bnn.xnor_rows_gemm(a, b, n, algo="umma", out=out)  # noqa: E731
         for _ in range(2):
             run()
@@ -29,5 +30,6 @@ for n in sizes:
         chk = float(out.double().sum().item())
         if ref is None:
             ref = chk
-        print(f"{n}^3 pair={pair}: {ms:.4f} ms  {2 * n**3 / ms / 1e9:.0f} TOPS  checksum equal {chk == ref}", flush=True)
+        print(f"{n}^3 pair={pair} wide={wide}: {ms:.4f} ms  {2 * n**3 / ms / 1e9:.0f} TOPS  checksum equal {chk == ref}", flush=True)
     _lib.call("bnn_debug_set", _lib.DEBUG_PAIR_KW32, 0)
+    _lib.call("bnn_debug_set", _lib.DEBUG_UMMA_BITS, 0)
