@@ -78,6 +78,10 @@ enum bnn_algo {
     BNN_ALGO_BMMA = 2, /* warp mma.sync m16n8k256 b1 .and.popc (emulated     */
                        /* on sm_100a: IMMA.U8 subroutine calls)              */
     BNN_ALGO_UMMA = 3, /* tcgen05.mma on bits expanded in SMEM = variant 2   */
+    /* AUTO / UMMA route by shape (all bit-identical): stride-1 convs with C <= 128 ->
+     * the shifted-window kernel (bnn_wconv.cu), other small-channel convs ->
+     * bnn_sconv.cu, GEMMs with N <= 256 and K <= 4096 -> the 8-CTA-cluster split-K
+     * kernel (bnn_gemm_splitk.cu), everything else -> the general engine below.   */
     /* tcgen05 engine variants (BNN_ALGO_UMMA_V0 + v):
      *   V0: kind::i8, 128 x 256 tiles, A and B through SMEM
      *   V1: kind::i8, expanded weights in TMEM, tile N from {128..192}
@@ -228,9 +232,11 @@ int bnn_bn_relu_maxpool_f32(const float *x, int64_t B, int64_t C, int64_t H, int
 /* Full-precision convolution of a network's float stem layer (reference
  * Conv2d, layers.py:81-141; ResNet-18 conv7x7/2 3->64, LeNet conv5x5 1->64):
  * y[B, F, oh, ow] = conv(x[B, C, H, W], w[F, C, kh, kw]) (+ bias[F]), zero
- * padding, NCHW f32.  tcgen05 kind::tf32 with a three-term hi/lo split
- * (x_hi w_hi + x_hi w_lo + x_lo w_hi, f32 accumulate): f32 accuracy, rounding
- * differs from a CUDA-core f32 conv only in summation order.  F == 64 and
+ * padding, NCHW f32.  tcgen05 kind::tf32 with a hi/lo operand split (three
+ * terms x_hi w_hi + x_hi w_lo + x_lo w_hi; the ResNet-18 geometry -- C = 3, 7x7,
+ * stride 2, pad 3, W = 224 -- runs the gather-free kernel bnn_stem_s2.cu, which
+ * accumulates all four terms), f32 accumulate: f32 accuracy, rounding differs
+ * from a CUDA-core f32 conv only in summation order.  F == 64 and
  * C*kh*kw <= 320 (BNN_EUNSUP otherwise). */
 int bnn_conv2d_f32_tc(const float *x, int64_t B, int64_t C, int64_t H, int64_t W,
                       const float *w, const float *bias, int64_t F, int64_t kh, int64_t kw,
@@ -352,10 +358,16 @@ int bnn_bconv2d_ex(const uint64_t *x_words, int64_t B, int64_t C, int64_t H, int
  * produce wrong results on purpose (timing ablations).
  * ------------------------------------------------------------------------ */
 enum bnn_debug_knob {
-    BNN_DEBUG_UMMA_BITS = 1,       /* tcgen05 engine debug bit flags                 */
+    BNN_DEBUG_UMMA_BITS = 1,       /* tcgen05 engine debug bit flags: 16 timelines into the
+                                    * bnn_umma_trace buffer, 1 << 15 no cluster split-K,
+                                    * 1 << 17 shifted-window conv also for C >= 256,
+                                    * 1 << 19 no shifted-window conv, 1 << 14 two
+                                    * superstages per TMA load, 1 << 18 no small-channel
+                                    * kernels, bits 21-24 role ablations (wrong results) */
     BNN_DEBUG_FP4_BN = 2,          /* force the kind::mxf4 tile N (0 = by shape)     */
     BNN_DEBUG_PAIR_KW32 = 3,       /* 2-CTA pairs from this K in u32 words (0 = off) */
-    BNN_DEBUG_STEM_BITS = 4,       /* float-stem kernel debug bit flags              */
+    BNN_DEBUG_STEM_BITS = 4,       /* float-stem kernels: 1 / 2 / 4 ablations (wrong results),
+                                    * 8 timeline, 16 the im2col-gather kernel for every shape */
     BNN_DEBUG_PACK_PIX = 5,        /* NCHW pack kernel variant (0 = default)         */
     BNN_DEBUG_PACK_CH = 6,         /* NCHW pack channels per lane (0 = default 8)    */
     BNN_DEBUG_STEMPOST_SIMPLE = 7, /* unbanded BN/ReLU/maxpool kernel                */
