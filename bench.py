@@ -532,6 +532,27 @@ def _kernel_families(plan):
     return fam
 
 
+def _stem_roofline(fams, batch):
+    """The float stem's own roofline (the second-largest share of the ResNet-18 step): tensor
+    cores, kind::tf32.  bnn_stem_s2.cu issues 2 x 21 MMAs of 128 x 112 x 8 per conv row (four
+    hi/lo split products on a K padded from 147 to 168) for 4 bands x 29 rows per image; peak =
+    half the measured dense bf16 rate of MEASURED_PEAKS.json (TF32 runs at half the bf16 rate;
+    tools/probes/tf32_overlap.cu measures 2,048 MAC/clk/SM), else the B200 nominal 1.1 PFLOP/s."""
+    ms = sum(v["ms"] for k, v in fams.items() if k.startswith("float stem"))
+    issued = 2.0 * 2 * 21 * 128 * 112 * 8 * (4 * 29) * batch
+    algorithmic = 2.0 * 64 * 147 * 112 * 112 * batch
+    peak, src = 1100.0, "fallback: B200 nominal dense TF32"
+    try:
+        pk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        peak, src = pk["bf16_tflops"] / 2, "MEASURED_PEAKS.json bf16_tflops (burst) / 2"
+    except Exception:
+        pass
+    ach = issued / (ms * 1e-3) / 1e12
+    return {"bound": "tensor", "kernel": "stem_s2_kernel (tcgen05 kind::tf32)", "kernel_ms": ms,
+            "achieved": ach, "peak": peak, "unit": "TFLOP/s (TF32 MMA flops issued)", "frac": ach / peak,
+            "algorithmic_f32_tflops": algorithmic / (ms * 1e-3) / 1e12, "peak_source": src}
+
+
 def run_gpu_arm(args, rank, world, local_rank):
     import torch
 
@@ -648,6 +669,8 @@ def run_gpu_arm(args, rank, world, local_rank):
                 "note": "per-launch CUDA events of one eager step queued behind a sleep kernel "
                         "(no host gaps inside the intervals); achieved = 2MNK of every binary "
                         "conv / GEMM launch / their summed device time"}
+        if name == "resnet18":
+            roof["stem"] = _stem_roofline(fams, plan.b)
     else:
         peak = pipe_peak(args.algo, name)
         achieved = ops_rank / (kern_avg * 1e-3) / 1e12

@@ -681,28 +681,33 @@ __global__ void avgpool_kernel(const float *__restrict__ x, int64_t BC, int HW,
     pooled[i] = __fdiv_rn(s, (float)HW);
 }
 
-// Pass 2: a CTA of 64 threads per (16 images, 64 outputs) tile, k in tiles of 64 staged
-// in SMEM row-major with a 65-float pitch (coalesced fills, conflict-free column reads);
-// each thread a 4 x 4 register tile, every output a sequential k = 0 .. C-1 FMA chain --
-// the same order for every image, any batch.
-constexpr int kFcImg = 16, kFcOut = 64, kFcK = 64, kFcPitch = kFcK + 1;
-__global__ void __launch_bounds__(64) fc_rows_kernel(const float *__restrict__ pooled, int B, int C,
-                                                     const float *__restrict__ w,
-                                                     const float *__restrict__ bias, int O,
-                                                     float *__restrict__ y) {
-    __shared__ float sp[kFcImg * kFcPitch];
-    __shared__ float sw[kFcOut * kFcPitch];
+// Pass 2: a CTA per (16 images, 64 outputs) tile; four groups of 64 threads each take a
+// quarter of K (k tiles of 32 staged in SMEM row-major with a 33-float pitch: coalesced
+// fills, conflict-free column reads), each thread a 4 x 4 register tile with a sequential
+// FMA chain over its quarter; the four partial sums are added in the fixed order
+// ((q0 + q1) + q2) + q3 -- the same order for every image, any batch.  (One group walking
+// all of K took 35 us for 512 -> 1000 at batch 256: eight serial load-latency rounds.)
+constexpr int kFcImg = 16, kFcOut = 64, kFcK = 32, kFcPitch = kFcK + 1, kFcGroups = 4;
+__global__ void __launch_bounds__(64 * kFcGroups) fc_rows_kernel(const float *__restrict__ pooled, int B,
+                                                                 int C, const float *__restrict__ w,
+                                                                 const float *__restrict__ bias, int O,
+                                                                 float *__restrict__ y) {
+    __shared__ float sp_all[kFcGroups][kFcImg * kFcPitch];
+    __shared__ float sw_all[kFcGroups][kFcOut * kFcPitch];
     const int b0 = blockIdx.x * kFcImg, o0 = blockIdx.y * kFcOut;
-    const int t = threadIdx.x, og = t & 15, ig = t >> 4;  // outputs 4 og .. +3, images 4 ig .. +3
+    const int grp = threadIdx.x >> 6, t = threadIdx.x & 63;
+    const int og = t & 15, ig = t >> 4;  // outputs 4 og .. +3, images 4 ig .. +3
+    float *sp = sp_all[grp], *sw = sw_all[grp];
+    const int kq = (C + kFcGroups - 1) / kFcGroups;  // this group's K range [kb, ke)
+    const int kb = grp * kq, ke = kb + kq < C ? kb + kq : C;
     float acc[4][4];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
-    for (int k0 = 0; k0 < C; k0 += kFcK) {
-        const int kn = C - k0 < kFcK ? C - k0 : kFcK;
-        // (all of a thread's tile loads in flight before its SMEM stores)
-        {
+    for (int k0 = kb; k0 < kb + kq; k0 += kFcK) {  // (every group runs the same trip count: the barriers)
+        const int kn = ke - k0 < kFcK ? (ke - k0 > 0 ? ke - k0 : 0) : kFcK;
+        {   // all of a thread's tile loads in flight before its SMEM stores
             constexpr int kP = kFcImg * kFcK / 64, kW = kFcOut * kFcK / 64;
             float vp[kP], vw[kW];
 #pragma unroll
@@ -740,17 +745,30 @@ __global__ void __launch_bounds__(64) fc_rows_kernel(const float *__restrict__ p
         }
         __syncthreads();
     }
+    // partial sums of groups 1..3 -> SMEM (the weight tiles are consumed), group 0 adds them in order
+    float *red = &sw_all[0][0];  // [3][64 threads][16]
+    if (grp > 0) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int bi = b0 + 4 * ig + i, o = o0 + 4 * og + j;
-            if (bi < B && o < O) {
+            for (int j = 0; j < 4; ++j) red[((grp - 1) * 64 + t) * 16 + 4 * i + j] = acc[i][j];
+    }
+    __syncthreads();
+    if (grp == 0) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int bi = b0 + 4 * ig + i, o = o0 + 4 * og + j;
                 float v = acc[i][j];
-                if (bias) v = __fadd_rn(v, __ldg(bias + o));
-                y[(int64_t)bi * O + o] = v;
+#pragma unroll
+                for (int q = 0; q < kFcGroups - 1; ++q) v = __fadd_rn(v, red[(q * 64 + t) * 16 + 4 * i + j]);
+                if (bi < B && o < O) {
+                    if (bias) v = __fadd_rn(v, __ldg(bias + o));
+                    y[(int64_t)bi * O + o] = v;
+                }
             }
-        }
+    }
 }
 
 // Pass 1: a CTA per 64 consecutive (image, channel) rows, staged in SMEM by coalesced
@@ -791,7 +809,7 @@ int launch_avgpool_fc(const float *x, int64_t B, int64_t C, int64_t HW, const fl
     int rc = check_launch("avgpool_kernel");
     if (rc) return rc;
     dim3 g((unsigned)ceil_div(B, kFcImg), (unsigned)ceil_div(O, kFcOut));
-    fc_rows_kernel<<<g, 64, 0, s>>>(pooled, (int)B, (int)C, w, bias, (int)O, y);
+    fc_rows_kernel<<<g, 64 * kFcGroups, 0, s>>>(pooled, (int)B, (int)C, w, bias, (int)O, y);
     return check_launch("fc_rows_kernel");
 }
 int launch_popcount64(const uint64_t *w, int64_t n, uint8_t *out, int soft, cudaStream_t s) {
