@@ -698,10 +698,11 @@ int launch_wconv(const uint64_t *x, int64_t B, int64_t C, int64_t H, int64_t W, 
     if (sh != 1 || sw != 1 || C % 64 != 0 || (Cw != 1 && Cw != 2 && Cw != 4 && Cw != 8) || F % 64 != 0 ||
         kh > 3 || kw > 3 || ph > kh - 1 || pw > kw - 1 || (g_debug.umma_bits & (1 << 19)))
         return BNN_EUNSUP;
-    // C >= 256 is built and parity-tested (debug bit 17 routes it here) but measured no faster
-    // than the TMA im2col engine on C2 / ResNet layers 3-4 (few tiles per CTA: the per-CTA weight
-    // expansion and the f32 store epilogue dominate), so those shapes keep the general engine
-    if (Cw > 2 && !(g_debug.umma_bits & (1 << 17))) return BNN_EUNSUP;
+    // C = 256 (filter groups of 128): faster than the TMA im2col engine on ResNet layer 3
+    // (27 vs 40 us packed-only, 44 vs 67 us with the shortcut) once the per-CTA weight expansion
+    // was batched; C = 512 does not fit next to two band buffers and falls through below.
+    // Debug bit 17 forces the general engine for C >= 256.
+    if (Cw > 2 && (g_debug.umma_bits & (1 << 17))) return BNN_EUNSUP;
     if (ep.pack_out && (ep.pack_ld32 < F / 32 || (ep.pack_ld32 & 1) ||
                         (reinterpret_cast<uintptr_t>(ep.pack_out) & 7)))
         return BNN_EUNSUP;
@@ -745,6 +746,9 @@ int launch_wconv(const uint64_t *x, int64_t B, int64_t C, int64_t H, int64_t W, 
     if (g_debug.grid_cap > 0 && sms > g_debug.grid_cap) sms = (int)g_debug.grid_cap;
     g.nranges = sms / g.fgroups < 1 ? 1 : sms / g.fgroups;
     if (g.nranges > g.ntiles) g.nranges = g.ntiles;
+    // C = 256 with only a few tiles per CTA (BASELINE configs[1]: 3): the per-CTA weight expansion
+    // and the f32 store tail dominate and the TMA im2col engine is faster (30.6 vs 21 us cold)
+    if (Cw > 2 && g.ntiles < 5 * g.nranges) return BNN_EUNSUP;
     const int grid = g.nranges * g.fgroups;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);

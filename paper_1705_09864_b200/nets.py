@@ -392,6 +392,15 @@ def _lenet_stem_forward(conv: "Conv2d", x: torch.Tensor, pool_first: bool = Fals
     return y
 
 
+_SMS = []
+
+
+def _sm_count() -> int:
+    if not _SMS:
+        _SMS.append(torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count)
+    return _SMS[0]
+
+
 def _binary_pool_fc(ls) -> bool:
     """QConvolution -> BatchNorm -> MaxPool2d(k, k, 0) -> Flatten -> QFullyConnected ->
     BatchNorm, 1-bit, the conv's filters a multiple of 64 (whole channel words)."""
@@ -451,12 +460,22 @@ class BinaryBasicBlock:
     # computes BN + shortcut for the sign and writes the packed words alone
     needs_f32_out = True
     split_shortcut = True  # conv2 epilogue without the add + one add/sign-pack pass
-    # (for the convs the small-channel kernel runs -- C, F <= 128 -- the shortcut add
+    # (for the convs the shifted-window kernel runs -- C, F <= 256 -- the shortcut add
     # stays in conv2's epilogue, whose residual reads are coalesced there)
 
     def _fused_shortcut(self, h) -> bool:
         c, f = self.conv2.in_channels, self.conv2.filters
-        return not self.split_shortcut or (c in (64, 128) and f in (64, 128))
+        if not self.split_shortcut or (c in (64, 128) and f in (64, 128)):
+            return True
+        if c == 256 and f == 256:
+            # the shifted-window kernel takes C = 256 when a CTA owns >= 5 tiles of 128 padded
+            # positions (launch_wconv, bnn_wconv.cu); below that the general engine runs and
+            # the split add / sign-pack pass is faster
+            b, _, hh, ww = h.shape
+            tiles = -(-(b * (hh + 2) * (ww + 2)) // 128)
+            ranges = max(1, _sm_count() // 2)
+            return tiles >= 5 * min(ranges, tiles)
+        return False
 
     def forward(self, x, mode=INFER_FLOAT):
         if mode == INFER_PACKED and self.fused and self.packed_io:

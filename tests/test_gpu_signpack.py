@@ -278,8 +278,8 @@ def test_small_channel_conv_kernel(bnn, case, epi, grid_cap):
 # Shifted-window kernel (bnn_wconv.cu: stride 1, every pixel expanded once, taps = shifted
 # no-swizzle descriptors).  Geometries beyond the ResNet ones: asymmetric / zero padding,
 # non-square kernels and images, the widest padded row (Wp = 64), bands that cross images,
-# one-pixel images, 64 <-> 128 channel / filter mixes; C >= 256 with filter groups runs here
-# only behind debug bit 17 and is covered too.
+# one-pixel images, 64 <-> 128 channel / filter mixes, C = 256 with filter groups (C = 512
+# falls through to the general engine).
 WCONV_CASES = [
     (3, 64, 17, 62, 64, 3, 3, (1, 1), 31),
     (2, 128, 9, 11, 64, 3, 3, (0, 1), 32),
@@ -291,6 +291,8 @@ WCONV_CASES = [
     (9, 128, 4, 4, 128, 3, 3, (2, 2), 38),
     (2, 256, 10, 12, 256, 3, 3, (1, 1), 39),
     (2, 512, 5, 6, 192, 3, 3, (1, 1), 40),
+    (8, 256, 14, 14, 256, 3, 3, (1, 1), 41),    # C = 256 on this kernel with 3 CTAs (grid_cap3)
+    (190, 256, 14, 14, 256, 3, 3, (1, 1), 42),  # ... and with every SM (>= 5 tiles per CTA)
 ]
 
 
@@ -311,7 +313,6 @@ def test_shifted_window_conv_kernel(bnn, case, epi, grid_cap):
     xd = torch.from_numpy(x).cuda()
     p = orc.qconv_packed(x, wt, (1, 1), pad).astype(np.float32)
     ref = 2 * p - np.float32(c * kh * kw)
-    _lib.call("bnn_debug_set", _lib.DEBUG_UMMA_BITS, 1 << 17)  # C >= 256 on this kernel too
     try:
         if epi == "plain":
             assert np.array_equal(layer.forward_fused(xd).cpu().numpy(), ref)

@@ -13,8 +13,11 @@ SHAPES = [(256, 64, 56, 56, 64, 3, 1, 1, "pack"), (256, 64, 56, 56, 64, 3, 1, 1,
           (1, 64, 56, 56, 64, 3, 1, 1, "pack"), (6, 64, 56, 56, 64, 3, 1, 1, "pack"),
           (32, 256, 28, 28, 256, 3, 1, 1, "plain"), (256, 256, 14, 14, 256, 3, 1, 1, "pack"),
           (256, 256, 14, 14, 256, 3, 1, 1, "bnf32"), (256, 512, 7, 7, 512, 3, 1, 1, "pack"),
-          (256, 512, 7, 7, 512, 3, 1, 1, "bnf32")]
+          (256, 512, 7, 7, 512, 3, 1, 1, "bnf32"), (256, 256, 14, 14, 256, 3, 1, 1, "res"),
+          (256, 256, 14, 14, 256, 3, 1, 1, "respk")]
 bnn.load_library()
+import os
+BIG = (1 << 17) if os.environ.get("WCONV_NOBIG") else 0  # C >= 256 back on the general engine
 rng = np.random.default_rng(0)
 
 
@@ -53,10 +56,12 @@ for i in idx:
         run = lambda: conv.forward_fused(xp)  # noqa: E731
     elif kind == "bnf32":
         run = lambda: conv.forward_fused(xp, bn)  # noqa: E731
+    elif kind == "respk":
+        run = lambda: conv.forward_fused(xp, bn, residual=res, pack_out=True, f32_out=False)  # noqa: E731
     else:
         run = lambda: conv.forward_fused(xp, bn, residual=res, pack_out=True)  # noqa: E731
     for d in bits:
-        v = (1 << 19) if d < 0 else (d << 21)
+        v = (1 << 19) if d < 0 else ((d << 21) | BIG)
         _lib.call("bnn_debug_set", _lib.DEBUG_UMMA_BITS, v)
         print(f"shape {i} {kind} dbg={d}: {t(run):.1f} us", flush=True)
     _lib.call("bnn_debug_set", _lib.DEBUG_UMMA_BITS, 0)
