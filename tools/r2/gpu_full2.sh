@@ -12,3 +12,6 @@ for w in c2 c1 gemm8192 lenet; do
   timeout 400 python bench.py --workload $w --steps 10 --warmup 3 --no-cpu-baseline >> $O/bench_sweep.log 2>&1
 done
 grep '^{' $O/bench_sweep.log | cut -c1-260
+timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_reference.log 2>&1; tail -1 $O/bench_reference.log | cut -c1-400
+PROF="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/resnet18_bench_launches.csv $PROF > $O/ncu_launches.log 2>&1
