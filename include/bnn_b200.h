@@ -94,7 +94,12 @@ enum bnn_algo {
     BNN_ALGO_UMMA_V1 = 17,
     BNN_ALGO_UMMA_V2 = 18,
     BNN_ALGO_UMMA_V3 = 19,
-    BNN_ALGO_UMMA_V4 = 20
+    BNN_ALGO_UMMA_V4 = 20,
+    /* bnn_xnor_gemm_ws only: force the pre-expanded engine (bnn_gemm_xp.cu): both operands
+     * expanded once in HBM to e2m1 +-1 codes, then a 2-CTA (cta_group::2) TMA-fed kind::mxf4
+     * GEMM whose accumulator is the signed dot product itself.  AUTO takes it for large
+     * shapes when a workspace is given; BNN_EUNSUP without one. */
+    BNN_ALGO_UMMA_XP = 24
 };
 
 /* Flags written (OR-ed) by the pack kernels into a caller int32. */
@@ -170,6 +175,18 @@ int bnn_xnor_gemm(const uint64_t *A, int64_t lda, const uint64_t *B, int64_t ldb
                   int64_t N, int64_t K, int a_pad, int b_pad, float *C, int64_t ldc_m,
                   int64_t ldc_n, int domain, const float *scale, const float *shift, int algo,
                   bnn_stream_t stream);
+
+/* bnn_xnor_gemm with a device workspace (same reference functions, gemm.py:226-291; plain
+ * DOT / POPCOUNT output, no affine).  With ws_bytes >= bnn_xnor_gemm_ws_bytes(M, N, K)
+ * (128-byte aligned; (M + N) * ceil(K / 64) * 32 bytes) large GEMMs run the pre-expanded
+ * engine (BNN_ALGO_UMMA_XP above); every other case, and ws == NULL, is exactly
+ * bnn_xnor_gemm.  Results are bit-identical either way.  The workspace is scratch: it is
+ * overwritten by every call and must not be shared by calls on different streams. */
+int64_t bnn_xnor_gemm_ws_bytes(int64_t M, int64_t N, int64_t K);
+int bnn_xnor_gemm_ws(const uint64_t *A, int64_t lda, const uint64_t *B, int64_t ldb, int64_t M,
+                     int64_t N, int64_t K, int a_pad, int b_pad, float *C, int64_t ldc_m,
+                     int64_t ldc_n, int domain, int algo, void *ws, int64_t ws_bytes,
+                     bnn_stream_t stream);
 
 /* Multi-bit path (act_bit = weight_bit = bits):
  * k-bit quantize + bit-plane pack, x [R, K] f32 -> out[p * plane_stride + r * ldo + w]

@@ -19,8 +19,9 @@ OK, EINVAL, EDIMS, EKEXACT, EPAD, EALIGN, EGEOM, EUNSUP, ECUDA = 0, -1, -2, -3, 
 POPCOUNT, DOT = 0, 1
 ALGO_AUTO, ALGO_POPC, ALGO_BMMA, ALGO_UMMA = 0, 1, 2, 3
 ALGO_UMMA_V0 = 16  # tcgen05 engine variant v = ALGO_UMMA_V0 + v (v in 0..4)
+ALGO_UMMA_XP = 24  # bnn_xnor_gemm_ws: pre-expanded operands + 2-CTA kind::mxf4 GEMM
 ALGOS = {"auto": ALGO_AUTO, "popc": ALGO_POPC, "bmma": ALGO_BMMA, "umma": ALGO_UMMA,
-         **{f"umma{v}": ALGO_UMMA_V0 + v for v in range(5)}}
+         "xp": ALGO_UMMA_XP, **{f"umma{v}": ALGO_UMMA_V0 + v for v in range(5)}}
 # debug knobs (bnn_debug_set; process-wide, experiment scripts only)
 DEBUG_UMMA_BITS, DEBUG_FP4_BN, DEBUG_PAIR_KW32, DEBUG_STEM_BITS = 1, 2, 3, 4
 DEBUG_PACK_PIX, DEBUG_PACK_CH, DEBUG_STEMPOST_SIMPLE, DEBUG_GRID_CAP = 5, 6, 7, 8
@@ -46,6 +47,9 @@ SIGNATURES = {
     "bnn_audit_padding": (_i32, [_vp, _i64, _i64, _i64, _i64, _i32, _vp, _vp]),
     "bnn_xnor_gemm": (_i32, [_vp, _i64, _vp, _i64, _i64, _i64, _i64, _i32, _i32, _vp, _i64,
                              _i64, _i32, _vp, _vp, _i32, _vp]),
+    "bnn_xnor_gemm_ws_bytes": (_i64, [_i64, _i64, _i64]),
+    "bnn_xnor_gemm_ws": (_i32, [_vp, _i64, _vp, _i64, _i64, _i64, _i64, _i32, _i32, _vp, _i64,
+                                _i64, _i32, _i32, _vp, _i64, _vp]),
     "bnn_conv_channel_words": (_i64, [_i64]),
     "bnn_conv_weights_reorder": (_i32, [_vp, _i64, _i64, _i64, _i64, _vp, _vp]),
     "bnn_bconv2d": (_i32, [_vp, _i64, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _i64,

@@ -46,6 +46,14 @@ int launch_conv_weights_reorder(const uint64_t *, int64_t, int64_t, int64_t, int
 int launch_xnor_gemm_popc(const uint64_t *, int64_t, const uint64_t *, int64_t, int64_t,
                           int64_t, int64_t, float *, int64_t, int64_t, const Epilogue &,
                           cudaStream_t, const float *);
+int launch_xnor_gemm_xp(const uint64_t *, int64_t, const uint64_t *, int64_t, int64_t, int64_t, int64_t,
+                        float *, int64_t, int64_t, const Epilogue &, cudaStream_t, const float *, void *,
+                        int64_t);
+int64_t xnor_gemm_xp_workspace(int64_t M, int64_t N, int64_t K);
+// AUTO: shapes from which the pre-expanded engine wins (measured, profiles/r02)
+static bool xp_auto(int64_t M, int64_t N, int64_t K) {
+    return M >= 1024 && N >= 1024 && K >= 2048 && (double)M * (double)N * (double)K >= 3.0e10;
+}
 int launch_xnor_gemm_umma(const uint64_t *, int64_t, const uint64_t *, int64_t, int64_t,
                           int64_t, int64_t, float *, int64_t, int64_t, const Epilogue &,
                           cudaStream_t, const float *);
@@ -216,7 +224,7 @@ static int engine_of(int algo, Epilogue &ep) {
         return BNN_ALGO_UMMA;
     }
     ep.variant = 2;
-    if (algo == BNN_ALGO_AUTO || algo == BNN_ALGO_UMMA) return BNN_ALGO_UMMA;
+    if (algo == BNN_ALGO_AUTO || algo == BNN_ALGO_UMMA || algo == BNN_ALGO_UMMA_XP) return BNN_ALGO_UMMA;
     if (algo == BNN_ALGO_POPC || algo == BNN_ALGO_BMMA) return algo;
     return -1;
 }
@@ -250,9 +258,10 @@ static int check_pack_out(const bnn_epilogue *e, int64_t M, int algo, const floa
     return BNN_OK;
 }
 
-int bnn_xnor_gemm_ex(const uint64_t *A, int64_t lda, const uint64_t *B, int64_t ldb, int64_t M,
-                     int64_t N, int64_t K, int a_pad, int b_pad, float *C, int64_t ldc_m,
-                     int64_t ldc_n, const bnn_epilogue *e, int algo, bnn_stream_t stream) {
+static int xnor_gemm_impl(const uint64_t *A, int64_t lda, const uint64_t *B, int64_t ldb, int64_t M,
+                          int64_t N, int64_t K, int a_pad, int b_pad, float *C, int64_t ldc_m,
+                          int64_t ldc_n, const bnn_epilogue *e, int algo, bnn_stream_t stream,
+                          void *ws, int64_t ws_bytes) {
     int rc = check_gemm_dims(M, N, K);
     if (rc) return rc;
     BNN_REQUIRE(e != nullptr, BNN_EINVAL, "null epilogue");
@@ -281,11 +290,43 @@ int bnn_xnor_gemm_ex(const uint64_t *A, int64_t lda, const uint64_t *B, int64_t 
             return launch_xnor_gemm_bmma(A, lda, B, ldb, M, N, K, C, ldc_m, ldc_n, ep,
                                          as_stream(stream), e->residual);
         case BNN_ALGO_UMMA:
+            // large GEMMs with a workspace: operands expanded once in HBM, 2-CTA TMA-fed
+            // kind::mxf4 GEMM (bnn_gemm_xp.cu); AUTO takes it from xp_auto_min_ops on
+            if (algo == BNN_ALGO_UMMA_XP || (algo == BNN_ALGO_AUTO && ws && xp_auto(M, N, K))) {
+                rc = launch_xnor_gemm_xp(A, lda, B, ldb, M, N, K, C, ldc_m, ldc_n, ep,
+                                         as_stream(stream), e->residual, ws, ws_bytes);
+                if (rc != BNN_EUNSUP) return rc;
+                if (algo == BNN_ALGO_UMMA_XP)
+                    return set_error(BNN_EUNSUP, "pre-expanded engine: plain epilogue and a 128-byte aligned "
+                                     "workspace of bnn_xnor_gemm_ws_bytes() needed");
+            }
             return launch_xnor_gemm_umma(A, lda, B, ldb, M, N, K, C, ldc_m, ldc_n, ep,
                                          as_stream(stream), e->residual);
         default:
             return set_error(BNN_EUNSUP, "algorithm %d not available", algo);
     }
+}
+
+int bnn_xnor_gemm_ex(const uint64_t *A, int64_t lda, const uint64_t *B, int64_t ldb, int64_t M,
+                     int64_t N, int64_t K, int a_pad, int b_pad, float *C, int64_t ldc_m,
+                     int64_t ldc_n, const bnn_epilogue *e, int algo, bnn_stream_t stream) {
+    return xnor_gemm_impl(A, lda, B, ldb, M, N, K, a_pad, b_pad, C, ldc_m, ldc_n, e, algo, stream,
+                          nullptr, 0);
+}
+
+int64_t bnn_xnor_gemm_ws_bytes(int64_t M, int64_t N, int64_t K) {
+    if (M < 1 || N < 1 || K < 1) return 0;
+    return xnor_gemm_xp_workspace(M, N, K);
+}
+
+int bnn_xnor_gemm_ws(const uint64_t *A, int64_t lda, const uint64_t *B, int64_t ldb, int64_t M,
+                     int64_t N, int64_t K, int a_pad, int b_pad, float *C, int64_t ldc_m,
+                     int64_t ldc_n, int domain, int algo, void *ws, int64_t ws_bytes,
+                     bnn_stream_t stream) {
+    bnn_epilogue e{domain, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    BNN_REQUIRE(ws_bytes >= 0 && (ws || ws_bytes == 0), BNN_EINVAL, "bad workspace");
+    return xnor_gemm_impl(A, lda, B, ldb, M, N, K, a_pad, b_pad, C, ldc_m, ldc_n, &e, algo, stream, ws,
+                          ws_bytes);
 }
 
 int bnn_xnor_gemm(const uint64_t *A, int64_t lda, const uint64_t *B, int64_t ldb, int64_t M,

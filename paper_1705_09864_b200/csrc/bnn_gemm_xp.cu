@@ -1,0 +1,400 @@
+// Large xnor-popcount GEMMs on pre-expanded operands (bnn_xnor_gemm_ws): the
+// bits of both packed operands are expanded ONCE, by an HBM-bound pass, into
+// e2m1 codes +1.0 / -1.0 (k >= K: 0.0) in a caller-provided workspace, and a
+// persistent 2-CTA tcgen05 GEMM (cta_group::2, kind::mxf4, 256 x BN tiles)
+// streams the codes straight from the workspace into SWIZZLE_128B operand
+// tiles with TMA.  The f32 accumulator is then the signed dot product
+// D = sum_k a_k b_k = 2P - K itself (gemm.py:3-8, 128-139: P = K - popcount(a ^ b)),
+// exact for K < 2^24, so no row popcounts and no in-CTA expansion are needed.
+//
+// Why: the in-CTA expansion of bnn_umma_impl.cuh moves ~112 KB through shared
+// memory per 448 tensor cycles (TMA write, expander reads, expanded stores, MMA
+// reads) and is SMEM-bound near 0.45 of the kind::mxf4 issue rate.  Here a CTA
+// of the pair moves 30 KB in and 30 KB out per 448 cycles, the B operand is
+// shared by the two SMs of the pair, and no warp touches operand data.
+//
+// Same results as bnn_xnor_gemm (bit-identical f32), same reference functions
+// (gemm.py:80-159, 226-291).  Epilogues other than the plain DOT / POPCOUNT
+// decode return BNN_EUNSUP from the launcher and the caller falls back to the
+// packed engine.
+#include "bnn_umma_impl.cuh"
+
+namespace bnn {
+namespace xp {
+
+using namespace umma;
+
+// ------------------------------------------------------------------ expansion
+struct ExpandOp {
+    const uint32_t *src;  // [rows, ld32] packed words
+    uint4 *dst;           // [rows, kw32] 16-byte groups of 32 e2m1 codes
+    int64_t ld32, rows;
+};
+
+// word w (bits 32 w .. 32 w + 31 of a row) -> 16 bytes: register j, nibble n <- bit
+// 4 n + j as the e2m1 code 0x2 (+1.0) for a set bit, 0xA (-1.0) for a clear bit and
+// 0x0 for positions >= K (tail bits of the last words, whatever the pad fill was).
+// Both operands use the same permutation of K, which a dot product does not see.
+__global__ void __launch_bounds__(256) expand_pm1_kernel(ExpandOp a, ExpandOp b, int64_t kw32,
+                                                         int64_t K) {
+    const ExpandOp op = blockIdx.z == 0 ? a : b;
+    for (int64_t r = blockIdx.y; r < op.rows; r += gridDim.y) {
+        const uint32_t *src = op.src + r * op.ld32;
+        uint4 *dst = op.dst + r * kw32;
+        for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < kw32;
+             w += (int64_t)gridDim.x * blockDim.x) {
+            const uint32_t x = __ldg(src + w);
+            uint32_t v[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) v[j] = 0xAAAAAAAAu ^ (((x >> j) & 0x11111111u) << 3);
+            const int64_t left = K - 32 * w;
+            if (left < 32) {
+                const uint32_t vm = left <= 0 ? 0u : ((1u << left) - 1u);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) v[j] &= ((vm >> j) & 0x11111111u) * 0xFu;
+            }
+            dst[w] = make_uint4(v[0], v[1], v[2], v[3]);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ GEMM
+template <int BN>
+struct Cfg {
+    static_assert(BN % 32 == 0 && BN >= 64 && BN <= 224, "pair tile N");
+    static constexpr int kStages = 6;
+    static constexpr int kABytes = BM * 128;           // this CTA's 128 A rows x 256 codes
+    static constexpr int kBRows = BN / 2;              // this CTA's half of the B rows
+    static constexpr int kBBytes = kBRows * 128;
+    static constexpr int kStageBytes = kABytes + kBBytes;
+    static_assert(kStageBytes % 1024 == 0, "SW128 atoms");
+    static constexpr int kTmaWarp = 0, kMmaWarp = 1, kEpiWarp0 = 2, kEpiWarps = 4;
+    static constexpr int kThreads = (kEpiWarp0 + kEpiWarps) * 32;
+    static constexpr int kStgBytes = 32 * 128;         // one 32 x 32 f32 block
+    static constexpr int off_stage = 0;
+    static constexpr int off_epi = kStages * kStageBytes;
+    static constexpr int off_bars = off_epi + kEpiWarps * 2 * kStgBytes;
+    static constexpr int kNumBars = 2 * kStages + 4;
+    static constexpr int off_tmem = off_bars + kNumBars * 8;
+    static constexpr int kSmemBytes = off_tmem + 16 + 1024;
+    static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
+    static constexpr int kSfCol = 2 * BN;              // UE8M0 scales (all 1.0) from here
+    static_assert(kSfCol + 64 <= 512, "TMEM budget");
+    // kind::mxf4: E2M1 x E2M1, UE8M0 scales, f32 accumulate, M = 256 (pair), N = BN
+    static constexpr uint32_t kIdesc = (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                                       (1u << 23) | ((uint32_t)(2 * BM >> 4) << 24);
+};
+
+struct Params {
+    float *C;
+    int64_t ldc_m, ldc_n, M, N;
+    int32_t kstages, tiles_m, ntiles;
+    int32_t k_logical, domain;
+    int32_t tma_store;
+};
+
+// TMA load into this CTA's SMEM, completing on the mbarrier of the pair's leader CTA
+// (same offset, CTA-rank bit of the shared::cluster address cleared)
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap *map, int c0, int c1,
+                                                 uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3}], [%4];\n" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+        : "memory");
+}
+
+template <int BN>
+__global__ void __launch_bounds__(Cfg<BN>::kThreads, 1)
+    xnor_xp_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
+                   const __grid_constant__ CUtensorMap omap, Params p, uint64_t *trace_buf) {
+    using C = Cfg<BN>;
+    constexpr int S = C::kStages;
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t sbase_raw = smem_u32(smem_raw);
+    const uint32_t sbase = (sbase_raw + 1023u) & ~1023u;
+    uint8_t *sgen = smem_raw + (sbase - sbase_raw);
+    const uint32_t s_stage = sbase + C::off_stage;
+    const uint32_t s_epi = sbase + C::off_epi;
+    const uint32_t bar_full = sbase + C::off_bars;   // [S] leader: both CTAs' TMA bytes landed
+    const uint32_t bar_empty = bar_full + S * 8;     // [S] MMAs that read the stage retired
+    const uint32_t bar_tfull = bar_empty + S * 8;    // [2] accumulator complete
+    const uint32_t bar_tempty = bar_tfull + 2 * 8;   // [2] leader: both CTAs' epilogues drained it
+    uint32_t *s_tmem = reinterpret_cast<uint32_t *>(sgen + C::off_tmem);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    uint32_t crank;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(crank));
+    const int t0 = (int)(blockIdx.x >> 1), tstep = (int)(gridDim.x >> 1);
+    const uint32_t kstages = (uint32_t)p.kstages;
+
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(bar_full + 8 * s, 1);
+            mbar_init(bar_empty + 8 * s, 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(bar_tfull + 8 * b, 1);
+            mbar_init(bar_tempty + 8 * b, 2 * C::kEpiWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&amap)));
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&bmap)));
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&omap)));
+    }
+    if (warp == C::kMmaWarp) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+            smem_u32(s_tmem)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *s_tmem;
+    if (warp >= C::kEpiWarp0) {  // block scales 2^0 in this CTA's TMEM lanes
+        const uint32_t one[8] = {0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu,
+                                 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu};
+        for (int col = C::kSfCol; col < 512; col += 8)
+            tmem_st8(tmem + ((uint32_t)((warp & 3) * 32) << 16) + col, one);
+        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+    }
+    fence_before();
+    __syncthreads();
+    cluster_sync();  // the peer's barriers and scales exist before any remote arrival / MMA
+    fence_after();
+    if (trace_buf && tid == 0) trace_at(trace_buf, 1);
+
+    if (warp == C::kTmaWarp) {
+        // ================================================================ TMA producer
+        if (lane == 0) {
+            uint32_t g = 0;
+            const uint32_t lead_full = bar_full & 0xFEFFFFFFu;
+#pragma unroll 1
+            for (int tile = t0; tile < p.ntiles; tile += tstep) {
+                const int tm = tile % p.tiles_m, tn = tile / p.tiles_m;
+                const int arow = tm * 2 * BM + (int)crank * BM;
+                const int brow = tn * BN + (int)crank * C::kBRows;
+#pragma unroll 1
+                for (uint32_t ks = 0; ks < kstages; ++ks, ++g) {
+                    const uint32_t s = g % S;
+                    if (g >= S) mbar_wait(bar_empty + 8 * s, ((g / S) - 1) & 1u);
+                    if (crank == 0) mbar_arrive_expect_tx(bar_full + 8 * s, 2 * C::kStageBytes);
+                    const uint32_t dst = s_stage + s * C::kStageBytes;
+                    tma_load_2d_pair(dst, &amap, (int)(ks * 128), arow, lead_full + 8 * s);
+                    tma_load_2d_pair(dst + C::kABytes, &bmap, (int)(ks * 128), brow, lead_full + 8 * s);
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == C::kMmaWarp) {
+        // ================================================================ MMA issuer (leader CTA)
+        if (crank == 0) {
+            uint32_t g = 0;
+            int it = 0;
+            const uint32_t sfc = tmem + C::kSfCol;
+#pragma unroll 1
+            for (int tile = t0; tile < p.ntiles; tile += tstep, ++it) {
+                const int buf = it & 1;
+                if (it >= 2) mbar_wait_cluster(bar_tempty + 8 * buf, (uint32_t)((it >> 1) - 1) & 1u);
+                fence_after();
+                const uint32_t d = tmem + buf * BN;
+#pragma unroll 1
+                for (uint32_t ks = 0; ks < kstages; ++ks, ++g) {
+                    const uint32_t s = g % S;
+                    mbar_wait(bar_full + 8 * s, (g / S) & 1u);
+                    fence_after();
+                    const uint32_t a_addr = s_stage + s * C::kStageBytes;
+                    const uint64_t da = sw128_desc(a_addr), db = sw128_desc(a_addr + C::kABytes);
+                    if (elect_one_sync()) {
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk)
+                            mma_fp4_pair<C::kIdesc>(d, da + 2 * kk, db + 2 * kk, sfc, sfc,
+                                                    (ks | (uint32_t)kk) != 0 ? 1u : 0u);
+                        umma_commit_pair(bar_empty + 8 * s);
+                    }
+                    __syncwarp();
+                }
+                if (elect_one_sync()) umma_commit_pair(bar_tfull + 8 * buf);
+                __syncwarp();
+            }
+        }
+    } else {
+        // ================================================================ epilogue
+        const int e = warp - C::kEpiWarp0, q = warp & 3;
+        const uint32_t stg0 = s_epi + e * 2 * C::kStgBytes;
+        const uint32_t lead_tempty = mapa_shared(bar_tempty, 0);
+        const bool dot = p.domain == BNN_DOT;
+        const float kf = (float)p.k_logical;
+        int it = 0;
+        uint32_t nst = 0;  // staged blocks so far (staging buffer parity)
+#pragma unroll 1
+        for (int tile = t0; tile < p.ntiles; tile += tstep, ++it) {
+            const int buf = it & 1;
+            const int tm = tile % p.tiles_m, tn = tile / p.tiles_m;
+            const int64_t mq = (int64_t)tm * 2 * BM + crank * BM + q * 32, n0 = (int64_t)tn * BN;
+            const int64_t m = mq + lane;
+            mbar_wait_sleep(bar_tfull + 8 * buf, (uint32_t)(it >> 1) & 1u);
+            fence_after();
+            const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + buf * BN;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t v[32];
+                tmem_ld32(taddr + c * 32, v);
+                const int64_t nc = n0 + c * 32;
+                if (mq >= p.M || nc >= p.N) continue;  // (warp-uniform)
+                float f[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const float dsum = __uint_as_float(v[j]);
+                    f[j] = dot ? dsum : __fmul_rn(__fadd_rn(dsum, kf), 0.5f);
+                }
+                if (p.tma_store) {
+                    const uint32_t stg = stg0 + (nst & 1u) * C::kStgBytes;
+                    ++nst;
+                    if (lane == 0) bulk_wait_read<1>();  // the store two blocks back has read its buffer
+                    __syncwarp();
+                    const uint32_t row = stg + lane * 128;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(
+                                         row + ((j ^ (lane & 7)) << 4)),
+                                     "f"(f[4 * j]), "f"(f[4 * j + 1]), "f"(f[4 * j + 2]), "f"(f[4 * j + 3]));
+                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) {  // (the TMA unit clips rows past M and columns past N)
+                        asm volatile(
+                            "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(
+                                reinterpret_cast<uint64_t>(&omap)),
+                            "r"((int)nc), "r"((int)mq), "r"(stg)
+                            : "memory");
+                        bulk_commit();
+                    }
+                } else if (m < p.M) {  // [N, M] outputs: lanes = consecutive addresses (any strides work)
+                    float *col = p.C + m * p.ldc_m + nc * p.ldc_n;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        if (nc + j < p.N) col[j * p.ldc_n] = f[j];
+                }
+            }
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(lead_tempty + 8 * buf);
+        }
+        if (lane == 0) bulk_wait_all();
+    }
+
+    fence_before();
+    __syncthreads();
+    cluster_sync();  // the peer reads this CTA's SMEM and arrives on its barriers until here
+    if (warp == C::kMmaWarp) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+    }
+    if (trace_buf && tid == 0) trace_at(trace_buf, 12);
+}
+
+// [rows, kb bytes] u8 view of an expanded operand; box = 128 bytes x box_rows, SWIZZLE_128B
+static int encode_codes(CUtensorMap &map, const void *base, int64_t rows, int64_t kb, int box_rows) {
+    EncodeTiledFn fn = encode_tiled();
+    if (!fn) return set_error(BNN_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t dims[2] = {(cuuint64_t)kb, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)kb};
+    const cuuint32_t box[2] = {128, (cuuint32_t)box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(base), dims, strides, box,
+                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_error(BNN_ECUDA, "cuTensorMapEncodeTiled failed (codes)");
+    return BNN_OK;
+}
+
+template <int BN>
+static int launch_cfg(const void *ea, const void *eb, int64_t kb, const GemmStore &st, const Epilogue &ep,
+                      int64_t M, int64_t N, cudaStream_t s) {
+    using C = Cfg<BN>;
+    auto kern = xnor_xp_kernel<BN>;
+    CUtensorMap amap, bmap;
+    int rc = encode_codes(amap, ea, M, kb, BM);
+    if (rc == BNN_OK) rc = encode_codes(bmap, eb, N, kb, C::kBRows);
+    if (rc != BNN_OK) return rc;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+        configured = true;
+    }
+    const int64_t tiles_m = ceil_div(M, 2 * BM), tiles_n = ceil_div(N, BN);
+    const int64_t ntiles = tiles_m * tiles_n;
+    if (ntiles > (1ll << 30)) return set_error(BNN_EUNSUP, "too many tiles");
+    Params p{};
+    p.C = st.C, p.ldc_m = st.ldc_m, p.ldc_n = st.ldc_n, p.M = M, p.N = N;
+    p.kstages = (int32_t)ceil_div(kb, 128), p.tiles_m = (int32_t)tiles_m, p.ntiles = (int32_t)ntiles;
+    p.k_logical = ep.k_logical, p.domain = ep.domain;
+    p.tma_store = st.has_map;
+    const int64_t pairs = sm_count() / 2;
+    int grid = (int)(ntiles < pairs ? ntiles : pairs) * 2;
+    if (g_debug.grid_cap > 0 && grid > g_debug.grid_cap) grid = (int)((g_debug.grid_cap + 1) & ~1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(C::kThreads);
+    cfg.dynamicSmemBytes = C::kSmemBytes;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, amap, bmap, st.omap, p, g_debug.trace_buf);
+    return check_launch("xnor_xp_kernel");
+}
+
+}  // namespace xp
+
+int64_t xnor_gemm_xp_workspace(int64_t M, int64_t N, int64_t K) {
+    const int64_t kw32 = 2 * ceil_div(K, 64);
+    return (M + N) * kw32 * 16;
+}
+
+// BNN_EUNSUP: shape / epilogue / workspace not eligible (the caller runs the packed engine)
+int launch_xnor_gemm_xp(const uint64_t *A, int64_t lda, const uint64_t *B, int64_t ldb, int64_t M,
+                        int64_t N, int64_t K, float *C, int64_t ldc_m, int64_t ldc_n, const Epilogue &ep,
+                        cudaStream_t s, const float *res, void *ws, int64_t ws_bytes) {
+    using namespace xp;
+    if (ep.scale || ep.shift || ep.bn_mean || ep.pack_out || res || !C) return BNN_EUNSUP;
+    if (ep.a_alpha != 1 || ep.a_beta != 0 || ep.b_alpha != 1 || ep.b_beta != 0) return BNN_EUNSUP;
+    if (!ws || ws_bytes < xnor_gemm_xp_workspace(M, N, K) || (reinterpret_cast<uintptr_t>(ws) & 127))
+        return BNN_EUNSUP;
+    if (M > (1ll << 30) || N > (1ll << 30)) return BNN_EUNSUP;
+    const int64_t kw32 = 2 * ceil_div(K, 64), kb = kw32 * 16;
+    GemmStore st{};
+    st.C = C, st.ldc_m = ldc_m, st.ldc_n = ldc_n, st.M = M, st.N = N;
+    if (ldc_n == 1) encode_out(st);  // (row-major outputs TMA cannot address: plain stores)
+    uint8_t *ea = static_cast<uint8_t *>(ws), *eb = ea + M * kb;
+    ExpandOp oa{reinterpret_cast<const uint32_t *>(A), reinterpret_cast<uint4 *>(ea), 2 * lda, M};
+    ExpandOp ob{reinterpret_cast<const uint32_t *>(B), reinterpret_cast<uint4 *>(eb), 2 * ldb, N};
+    const int64_t rows = M > N ? M : N;
+    dim3 grid((unsigned)(kw32 > 1024 ? ceil_div(kw32, 1024) : 1), (unsigned)(rows < 32768 ? rows : 32768), 2);
+    expand_pm1_kernel<<<grid, 256, 0, s>>>(oa, ob, kw32, K);
+    int rc = check_launch("expand_pm1_kernel");
+    if (rc != BNN_OK) return rc;
+    // tile N from {224, 192, 160, 128}: waves over the SM pairs x (N + fixed per-tile cost)
+    static const int cands[] = {224, 192, 160, 128};
+    const int64_t pairs = sm_count() / 2, tm = ceil_div(M, 2 * umma::BM);
+    int best = 224;
+    int64_t best_cost = -1;
+    for (int bn : cands) {
+        const int64_t cost = ceil_div(tm * ceil_div(N, bn), pairs) * (bn + 16);
+        if (best_cost < 0 || cost < best_cost) best = bn, best_cost = cost;
+    }
+    if (g_debug.fp4_bn == 128 || g_debug.fp4_bn == 160 || g_debug.fp4_bn == 192 || g_debug.fp4_bn == 224)
+        best = (int)g_debug.fp4_bn;
+    switch (best) {
+        case 128: return launch_cfg<128>(ea, eb, kb, st, ep, M, N, s);
+        case 160: return launch_cfg<160>(ea, eb, kb, st, ep, M, N, s);
+        case 192: return launch_cfg<192>(ea, eb, kb, st, ep, M, N, s);
+        default: return launch_cfg<224>(ea, eb, kb, st, ep, M, N, s);
+    }
+}
+
+}  // namespace bnn

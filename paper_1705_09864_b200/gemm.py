@@ -93,7 +93,8 @@ def _check_operands(a: BitMatrix, b: BitMatrix) -> None:
 def xnor_rows_gemm(a_rows: torch.Tensor, b_rows: torch.Tensor, k: int, *, a_pad: int = 0,
                    b_pad: int = 0, domain: int = _lib.POPCOUNT, out: torch.Tensor | None = None,
                    transpose_out: bool = False, scale: torch.Tensor | None = None,
-                   shift: torch.Tensor | None = None, algo: int | str = "auto") -> torch.Tensor:
+                   shift: torch.Tensor | None = None, algo: int | str = "auto",
+                   workspace_in: torch.Tensor | None = None) -> torch.Tensor:
     """Core entry: both operands K-contiguous [M, W] / [N, W] CUDA u64 words.
 
     Returns f32 [M, N] (or [N, M] with ``transpose_out``), popcount domain
@@ -109,10 +110,39 @@ def xnor_rows_gemm(a_rows: torch.Tensor, b_rows: torch.Tensor, k: int, *, a_pad:
         out = torch.empty((n, m) if transpose_out else (m, n), dtype=torch.float32,
                           device=a_rows.device)
     ldc_m, ldc_n = (1, out.stride(0)) if transpose_out else (out.stride(0), 1)
+    if scale is None and shift is None and (algo == _lib.ALGO_UMMA_XP or
+                                            (algo == _lib.ALGO_AUTO and xp_eligible(m, n, k))):
+        # large GEMMs: operands expanded once into a scratch buffer, 2-CTA TMA-fed engine
+        ws = workspace(m, n, k, a_rows.device) if workspace_in is None else workspace_in
+        _lib.call("bnn_xnor_gemm_ws", _lib.ptr(a_rows), a_rows.stride(0), _lib.ptr(b_rows),
+                  b_rows.stride(0), m, n, k, a_pad, b_pad, _lib.ptr(out), ldc_m, ldc_n, domain,
+                  algo, _lib.ptr(ws), ws.numel(), _lib.stream_ptr())
+        return out
     _lib.call("bnn_xnor_gemm", _lib.ptr(a_rows), a_rows.stride(0), _lib.ptr(b_rows),
               b_rows.stride(0), m, n, k, a_pad, b_pad, _lib.ptr(out), ldc_m, ldc_n, domain,
               _lib.ptr(scale), _lib.ptr(shift), algo, _lib.stream_ptr())
     return out
+
+
+def xp_eligible(m: int, n: int, k: int) -> bool:
+    """Shapes AUTO hands to the pre-expanded engine when a workspace comes with the call
+    (mirrors xp_auto in csrc/bnn_capi.cu)."""
+    return m >= 1024 and n >= 1024 and k >= 2048 and float(m) * n * k >= 3.0e10
+
+
+_WORKSPACES: dict = {}
+
+
+def workspace(m: int, n: int, k: int, device) -> torch.Tensor:
+    """Scratch for bnn_xnor_gemm_ws: one growing u8 buffer per (device, stream) -- calls on
+    one stream are ordered, so they can share it."""
+    need = int(_lib.load().bnn_xnor_gemm_ws_bytes(m, n, k))
+    key = (torch.device(device).index, int(torch.cuda.current_stream().cuda_stream))
+    ws = _WORKSPACES.get(key)
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(need, dtype=torch.uint8, device=device)
+        _WORKSPACES[key] = ws
+    return ws
 
 
 def bitplane_gemm(a_planes: torch.Tensor, b_planes: torch.Tensor, k: int, *,

@@ -295,6 +295,15 @@ class GemmPlan(_Plan):
         self.domain = domain
         self._alloc_common()
         self.lib = _lib.load()
+        # large shapes: scratch for the pre-expanded engine (bnn_xnor_gemm_ws); both the
+        # expansion pass and the GEMM run inside every step
+        self.ws = None
+        from .gemm import xp_eligible
+        if self.algo == _lib.ALGO_UMMA_XP or (self.algo == _lib.ALGO_AUTO and
+                                              xp_eligible(self.m, self.n, self.k)):
+            self.ws = torch.empty(int(self.lib.bnn_xnor_gemm_ws_bytes(self.m, self.n, self.k)),
+                                  dtype=torch.uint8, device="cuda")
+            self.launches_per_step = 2
 
     @property
     def binary_ops(self) -> int:
@@ -305,6 +314,13 @@ class GemmPlan(_Plan):
 
     def kernel(self, stream: int | None = None):
         s = _lib.stream_ptr() if stream is None else stream
+        if self.ws is not None:
+            _lib.check(self.lib.bnn_xnor_gemm_ws(self.a.data_ptr(), self.a.stride(0),
+                                                 self.bw.data_ptr(), self.bw.stride(0), self.m,
+                                                 self.n, self.k, 0, 0, self.y.data_ptr(), self.n, 1,
+                                                 self.domain, self.algo, self.ws.data_ptr(),
+                                                 self.ws.numel(), s), "xnor_gemm_ws")
+            return
         _lib.check(self.lib.bnn_xnor_gemm(self.a.data_ptr(), self.a.stride(0), self.bw.data_ptr(),
                                           self.bw.stride(0), self.m, self.n, self.k, 0, 0,
                                           self.y.data_ptr(), self.n, 1, self.domain, None, None,
