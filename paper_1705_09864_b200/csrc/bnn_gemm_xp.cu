@@ -26,43 +26,58 @@ using namespace umma;
 
 // ------------------------------------------------------------------ expansion
 struct ExpandOp {
-    const uint32_t *src;  // [rows, ld32] packed words
-    uint4 *dst;           // [rows, kw32] 16-byte groups of 32 e2m1 codes
-    int64_t ld32, rows;
+    const uint2 *src;  // [rows, ld64] packed u64 words
+    uint4 *dst;        // [rows, kw32] 16-byte groups of 32 e2m1 codes
+    int64_t ld64, rows;
 };
 
-// word w (bits 32 w .. 32 w + 31 of a row) -> 16 bytes: register j, nibble n <- bit
+// u32 word w (bits 32 w .. 32 w + 31 of a row) -> 16 bytes: register j, nibble n <- bit
 // 4 n + j as the e2m1 code 0x2 (+1.0) for a set bit, 0xA (-1.0) for a clear bit and
 // 0x0 for positions >= K (tail bits of the last words, whatever the pad fill was).
 // Both operands use the same permutation of K, which a dot product does not see.
-__global__ void __launch_bounds__(256) expand_pm1_kernel(ExpandOp a, ExpandOp b, int64_t kw32,
+__device__ __forceinline__ uint4 expand_pm1(uint32_t x, int64_t left) {
+    uint32_t v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v[j] = 0xAAAAAAAAu ^ (((x >> j) & 0x11111111u) << 3);
+    if (left < 32) {
+        const uint32_t vm = left <= 0 ? 0u : ((1u << left) - 1u);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] &= ((vm >> j) & 0x11111111u) * 0xFu;
+    }
+    return make_uint4(v[0], v[1], v[2], v[3]);
+}
+
+// HBM-bound pass over both operands: a thread takes one u64 word of kRows consecutive
+// rows (kRows loads in flight), a warp writes 1 KB runs of codes
+constexpr int kExpRows = 4;
+__global__ void __launch_bounds__(128) expand_pm1_kernel(ExpandOp a, ExpandOp b, int64_t kw64,
                                                          int64_t K) {
     const ExpandOp op = blockIdx.z == 0 ? a : b;
-    for (int64_t r = blockIdx.y; r < op.rows; r += gridDim.y) {
-        const uint32_t *src = op.src + r * op.ld32;
-        uint4 *dst = op.dst + r * kw32;
-        for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < kw32;
-             w += (int64_t)gridDim.x * blockDim.x) {
-            const uint32_t x = __ldg(src + w);
-            uint32_t v[4];
+    const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= kw64) return;
+    for (int64_t r0 = (int64_t)blockIdx.y * kExpRows; r0 < op.rows; r0 += (int64_t)gridDim.y * kExpRows) {
+        uint2 x[kExpRows];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) v[j] = 0xAAAAAAAAu ^ (((x >> j) & 0x11111111u) << 3);
-            const int64_t left = K - 32 * w;
-            if (left < 32) {
-                const uint32_t vm = left <= 0 ? 0u : ((1u << left) - 1u);
+        for (int i = 0; i < kExpRows; ++i)
+            x[i] = r0 + i < op.rows ? __ldg(op.src + (r0 + i) * op.ld64 + w) : make_uint2(0u, 0u);
 #pragma unroll
-                for (int j = 0; j < 4; ++j) v[j] &= ((vm >> j) & 0x11111111u) * 0xFu;
-            }
-            dst[w] = make_uint4(v[0], v[1], v[2], v[3]);
+        for (int i = 0; i < kExpRows; ++i) {
+            if (r0 + i >= op.rows) break;
+            uint4 *dst = op.dst + (r0 + i) * 2 * kw64 + 2 * w;
+            dst[0] = expand_pm1(x[i].x, K - 64 * w);
+            dst[1] = expand_pm1(x[i].y, K - 64 * w - 32);
         }
     }
 }
 
 // ------------------------------------------------------------------ GEMM
-template <int BN>
+// kStaged: outputs leave through a per-warp SMEM block and TMA stores (6 operand stages fit);
+// otherwise straight from registers (16 B per row per instruction; outputs TMA cannot address)
+// and the 32 KB of staging become a 7th operand stage
+template <int BN, bool kStaged>
 struct Cfg {
     static_assert(BN % 32 == 0 && BN >= 64 && BN <= 224, "pair tile N");
-    static constexpr int kStages = 6;
+    static constexpr int kStages = kStaged ? 6 : 7;
     static constexpr int kABytes = BM * 128;           // this CTA's 128 A rows x 256 codes
     static constexpr int kBRows = BN / 2;              // this CTA's half of the B rows
     static constexpr int kBBytes = kBRows * 128;
@@ -73,7 +88,7 @@ struct Cfg {
     static constexpr int kStgBytes = 32 * 128;         // one 32 x 32 f32 block
     static constexpr int off_stage = 0;
     static constexpr int off_epi = kStages * kStageBytes;
-    static constexpr int off_bars = off_epi + kEpiWarps * 2 * kStgBytes;
+    static constexpr int off_bars = off_epi + (kStaged ? kEpiWarps * 2 * kStgBytes : 0);
     static constexpr int kNumBars = 2 * kStages + 4;
     static constexpr int off_tmem = off_bars + kNumBars * 8;
     static constexpr int kSmemBytes = off_tmem + 16 + 1024;
@@ -90,7 +105,7 @@ struct Params {
     int64_t ldc_m, ldc_n, M, N;
     int32_t kstages, tiles_m, ntiles;
     int32_t k_logical, domain;
-    int32_t tma_store;
+    int32_t tma_store, vec4, park;
 };
 
 // TMA load into this CTA's SMEM, completing on the mbarrier of the pair's leader CTA
@@ -104,11 +119,11 @@ __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap
         : "memory");
 }
 
-template <int BN>
-__global__ void __launch_bounds__(Cfg<BN>::kThreads, 1)
+template <int BN, bool kStaged>
+__global__ void __launch_bounds__(Cfg<BN, kStaged>::kThreads, 1)
     xnor_xp_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
                    const __grid_constant__ CUtensorMap omap, Params p, uint64_t *trace_buf) {
-    using C = Cfg<BN>;
+    using C = Cfg<BN, kStaged>;
     constexpr int S = C::kStages;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t sbase_raw = smem_u32(smem_raw);
@@ -177,7 +192,10 @@ __global__ void __launch_bounds__(Cfg<BN>::kThreads, 1)
 #pragma unroll 1
                 for (uint32_t ks = 0; ks < kstages; ++ks, ++g) {
                     const uint32_t s = g % S;
-                    if (g >= S) mbar_wait(bar_empty + 8 * s, ((g / S) - 1) & 1u);
+                    if (g >= S) {
+                        if (p.park) mbar_wait(bar_empty + 8 * s, ((g / S) - 1) & 1u);
+                        else mbar_wait_spin(bar_empty + 8 * s, ((g / S) - 1) & 1u);
+                    }
                     if (crank == 0) mbar_arrive_expect_tx(bar_full + 8 * s, 2 * C::kStageBytes);
                     const uint32_t dst = s_stage + s * C::kStageBytes;
                     tma_load_2d_pair(dst, &amap, (int)(ks * 128), arow, lead_full + 8 * s);
@@ -201,7 +219,8 @@ __global__ void __launch_bounds__(Cfg<BN>::kThreads, 1)
 #pragma unroll 1
                 for (uint32_t ks = 0; ks < kstages; ++ks, ++g) {
                     const uint32_t s = g % S;
-                    mbar_wait(bar_full + 8 * s, (g / S) & 1u);
+                    if (p.park) mbar_wait(bar_full + 8 * s, (g / S) & 1u);
+                    else mbar_wait_spin(bar_full + 8 * s, (g / S) & 1u);
                     fence_after();
                     const uint32_t a_addr = s_stage + s * C::kStageBytes;
                     const uint64_t da = sw128_desc(a_addr), db = sw128_desc(a_addr + C::kABytes);
@@ -248,7 +267,7 @@ __global__ void __launch_bounds__(Cfg<BN>::kThreads, 1)
                     const float dsum = __uint_as_float(v[j]);
                     f[j] = dot ? dsum : __fmul_rn(__fadd_rn(dsum, kf), 0.5f);
                 }
-                if (p.tma_store) {
+                if (kStaged && p.tma_store) {
                     const uint32_t stg = stg0 + (nst & 1u) * C::kStgBytes;
                     ++nst;
                     if (lane == 0) bulk_wait_read<1>();  // the store two blocks back has read its buffer
@@ -269,11 +288,17 @@ __global__ void __launch_bounds__(Cfg<BN>::kThreads, 1)
                             : "memory");
                         bulk_commit();
                     }
-                } else if (m < p.M) {  // [N, M] outputs: lanes = consecutive addresses (any strides work)
+                } else if (m < p.M) {
                     float *col = p.C + m * p.ldc_m + nc * p.ldc_n;
+                    if (p.vec4 && nc + 32 <= p.N) {  // row-major: 128 contiguous bytes per lane
 #pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        if (nc + j < p.N) col[j * p.ldc_n] = f[j];
+                        for (int j = 0; j < 8; ++j)
+                            reinterpret_cast<float4 *>(col)[j] = make_float4(f[4 * j], f[4 * j + 1], f[4 * j + 2], f[4 * j + 3]);
+                    } else {  // [N, M] outputs: lanes = consecutive addresses (any strides work)
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (nc + j < p.N) col[j * p.ldc_n] = f[j];
+                    }
                 }
             }
             fence_before();
@@ -308,11 +333,11 @@ static int encode_codes(CUtensorMap &map, const void *base, int64_t rows, int64_
     return BNN_OK;
 }
 
-template <int BN>
+template <int BN, bool kStaged>
 static int launch_cfg(const void *ea, const void *eb, int64_t kb, const GemmStore &st, const Epilogue &ep,
                       int64_t M, int64_t N, cudaStream_t s) {
-    using C = Cfg<BN>;
-    auto kern = xnor_xp_kernel<BN>;
+    using C = Cfg<BN, kStaged>;
+    auto kern = xnor_xp_kernel<BN, kStaged>;
     CUtensorMap amap, bmap;
     int rc = encode_codes(amap, ea, M, kb, BM);
     if (rc == BNN_OK) rc = encode_codes(bmap, eb, N, kb, C::kBRows);
@@ -330,6 +355,8 @@ static int launch_cfg(const void *ea, const void *eb, int64_t kb, const GemmStor
     p.kstages = (int32_t)ceil_div(kb, 128), p.tiles_m = (int32_t)tiles_m, p.ntiles = (int32_t)ntiles;
     p.k_logical = ep.k_logical, p.domain = ep.domain;
     p.tma_store = st.has_map;
+    p.park = (umma_dbg() & (1 << 21)) ? 1 : 0;
+    p.vec4 = st.ldc_n == 1 && st.ldc_m % 4 == 0 && (reinterpret_cast<uintptr_t>(st.C) & 15) == 0;
     const int64_t pairs = sm_count() / 2;
     int grid = (int)(ntiles < pairs ? ntiles : pairs) * 2;
     if (g_debug.grid_cap > 0 && grid > g_debug.grid_cap) grid = (int)((g_debug.grid_cap + 1) & ~1);
@@ -371,29 +398,37 @@ int launch_xnor_gemm_xp(const uint64_t *A, int64_t lda, const uint64_t *B, int64
     st.C = C, st.ldc_m = ldc_m, st.ldc_n = ldc_n, st.M = M, st.N = N;
     if (ldc_n == 1) encode_out(st);  // (row-major outputs TMA cannot address: plain stores)
     uint8_t *ea = static_cast<uint8_t *>(ws), *eb = ea + M * kb;
-    ExpandOp oa{reinterpret_cast<const uint32_t *>(A), reinterpret_cast<uint4 *>(ea), 2 * lda, M};
-    ExpandOp ob{reinterpret_cast<const uint32_t *>(B), reinterpret_cast<uint4 *>(eb), 2 * ldb, N};
-    const int64_t rows = M > N ? M : N;
-    dim3 grid((unsigned)(kw32 > 1024 ? ceil_div(kw32, 1024) : 1), (unsigned)(rows < 32768 ? rows : 32768), 2);
-    expand_pm1_kernel<<<grid, 256, 0, s>>>(oa, ob, kw32, K);
+    ExpandOp oa{reinterpret_cast<const uint2 *>(A), reinterpret_cast<uint4 *>(ea), lda, M};
+    ExpandOp ob{reinterpret_cast<const uint2 *>(B), reinterpret_cast<uint4 *>(eb), ldb, N};
+    const int64_t rows = M > N ? M : N, kw64 = kw32 / 2, rgroups = ceil_div(rows, kExpRows);
+    dim3 grid((unsigned)ceil_div(kw64, 128), (unsigned)(rgroups < 32768 ? rgroups : 32768), 2);
+    expand_pm1_kernel<<<grid, 128, 0, s>>>(oa, ob, kw64, K);
     int rc = check_launch("expand_pm1_kernel");
     if (rc != BNN_OK) return rc;
-    // tile N from {224, 192, 160, 128}: waves over the SM pairs x (N + fixed per-tile cost)
+    // tile N from {224, 192, 160, 128}: waves over the SM pairs x the cycles of a K = 256 stage.
+    // A stage is bound by the SM's shared-memory port, not the tensor pipe: the TMA writes
+    // (128 + N/2) rows of 128 B and the MMA reads 128 + N rows (its own A rows and ALL of B, the
+    // peer's half included) = 128 B x (256 + 1.5 N) at 128 B/clk, against 2 N tensor cycles
+    // (profiles/r02: 578 cycles per stage measured at N = 224, tensor pipe 79% active)
     static const int cands[] = {224, 192, 160, 128};
     const int64_t pairs = sm_count() / 2, tm = ceil_div(M, 2 * umma::BM);
     int best = 224;
     int64_t best_cost = -1;
     for (int bn : cands) {
-        const int64_t cost = ceil_div(tm * ceil_div(N, bn), pairs) * (bn + 16);
+        const int64_t cost = ceil_div(tm * ceil_div(N, bn), pairs) * (512 + 3 * bn);
         if (best_cost < 0 || cost < best_cost) best = bn, best_cost = cost;
     }
     if (g_debug.fp4_bn == 128 || g_debug.fp4_bn == 160 || g_debug.fp4_bn == 192 || g_debug.fp4_bn == 224)
         best = (int)g_debug.fp4_bn;
+    // row-major outputs leave through SMEM staging + TMA stores (6 operand stages); register
+    // stores with a 7th stage measured slower (8192^3: 207 vs 198 us, 4096^3: 54 vs 44 us;
+    // debug bit 1 << 20 selects them, bit 1 << 21 parks the TMA / MMA waits instead of spinning)
+    const bool staged = st.has_map && !(umma_dbg() & (1 << 20));
     switch (best) {
-        case 128: return launch_cfg<128>(ea, eb, kb, st, ep, M, N, s);
-        case 160: return launch_cfg<160>(ea, eb, kb, st, ep, M, N, s);
-        case 192: return launch_cfg<192>(ea, eb, kb, st, ep, M, N, s);
-        default: return launch_cfg<224>(ea, eb, kb, st, ep, M, N, s);
+        case 128: return staged ? launch_cfg<128, true>(ea, eb, kb, st, ep, M, N, s) : launch_cfg<128, false>(ea, eb, kb, st, ep, M, N, s);
+        case 160: return staged ? launch_cfg<160, true>(ea, eb, kb, st, ep, M, N, s) : launch_cfg<160, false>(ea, eb, kb, st, ep, M, N, s);
+        case 192: return staged ? launch_cfg<192, true>(ea, eb, kb, st, ep, M, N, s) : launch_cfg<192, false>(ea, eb, kb, st, ep, M, N, s);
+        default: return staged ? launch_cfg<224, true>(ea, eb, kb, st, ep, M, N, s) : launch_cfg<224, false>(ea, eb, kb, st, ep, M, N, s);
     }
 }
 

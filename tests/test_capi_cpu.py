@@ -75,6 +75,27 @@ def test_gemm_validation_mirrors_gemmdims(lib):
     assert _gemm(lib, algo=2, M=0) == -2  # validation precedes engine dispatch
 
 
+def test_gemm_ws_validation_and_workspace_size(lib):
+    # bnn_xnor_gemm_ws: the same GemmDims validation, before any dispatch; workspace =
+    # 16 bytes of e2m1 codes per 32 bits of every operand row
+    assert lib.bnn_xnor_gemm_ws_bytes(256, 224, 256) == (256 + 224) * 8 * 16
+    assert lib.bnn_xnor_gemm_ws_bytes(3, 5, 65) == 8 * 4 * 16
+    assert lib.bnn_xnor_gemm_ws_bytes(0, 5, 65) == 0
+    base = [1, 1, 1, 1, 4, 4, 64, 0, 0, 1, 4, 1, 0, 0, None, 0, None]
+    for pos, bad, rc in ((4, 0, -2), (6, 1 << 24, -3), (7, 2, -4), (12, 7, -1), (13, 99, -7)):
+        a = list(base)
+        a[pos] = bad
+        if pos == 6:
+            a[1] = a[3] = 1 << 18
+        assert lib.bnn_xnor_gemm_ws(*a) == rc, (pos, bad)
+    a = list(base)
+    a[15] = -1
+    assert lib.bnn_xnor_gemm_ws(*a) == -1  # negative workspace size
+    from paper_1705_09864_b200.gemm import xp_eligible
+    assert xp_eligible(8192, 8192, 8192) and xp_eligible(4096, 4096, 4096)
+    assert not xp_eligible(256, 1024, 4096) and not xp_eligible(4096, 4096, 1024)
+
+
 def test_conv_and_pack_validation(lib):
     # tensor.conv_output_hw (tensor.py:15-27): kernel must fit, stride >= 1
     rc = lib.bnn_bconv2d(1, 1, 1, 3, 3, 1, 1, 5, 5, 1, 1, 0, 0, 1, 0, None, None, 0, None)

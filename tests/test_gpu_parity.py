@@ -20,6 +20,9 @@ from oracle import oracle as orc
 pytestmark = pytest.mark.gpu
 
 ALGOS = ["popc", "bmma", "umma0", "umma1", "umma2", "umma3", "umma4"]
+# GEMM-only engines: "xp" = operands pre-expanded in a workspace + the 2-CTA kind::mxf4 GEMM
+# (bnn_xnor_gemm_ws); "auto" routes the large shapes there
+GEMM_ALGOS = ALGOS + ["xp"]
 
 
 def A(algo):
@@ -160,7 +163,7 @@ def test_pack_nchw_matches_oracle(bnn):
 
 
 # ------------------------------------------------------------------ gemm
-@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("algo", GEMM_ALGOS)
 def test_gemm40_bit_exact(bnn, golden, algo):
     g = golden["gemm40"]
     for i, (m, n, k, seed) in enumerate(wl.gemm40_cases()):
@@ -195,7 +198,7 @@ def test_operand_validation(bnn):
         bnn.xnor_gemm_base(abm, short)
 
 
-@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("algo", GEMM_ALGOS)
 def test_sweep504_bit_exact(bnn, golden_dir, algo):
     rows = json.load(open(os.path.join(golden_dir, "sweep504.json")))
     got = []
@@ -206,7 +209,7 @@ def test_sweep504_bit_exact(bnn, golden_dir, algo):
     assert got == rows
 
 
-@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("algo", GEMM_ALGOS)
 def test_gemm_tail_and_layout_variants(bnn, algo):
     """Row-row operands, every pad combination, both domains, odd ld, transposed out."""
     rng = np.random.default_rng(5)
@@ -359,7 +362,9 @@ def test_config2_qconv_golden(bnn, golden_dir, algo):
 
 LARGE = ([(a, mnk) for a in ALGOS for mnk in [(4096, 4096, 4096), (4096, 4096, 65536),
                                              (8192, 8192, 8192)]] +
-         [(a, (16384, 16384, 16384)) for a in ("umma2", "popc")])  # BASELINE configs[4]
+         [(a, mnk) for a in ("xp", "auto") for mnk in [(4096, 4096, 4096), (4096, 4096, 65536),
+                                                        (8192, 8192, 8192)]] +
+         [(a, (16384, 16384, 16384)) for a in ("umma2", "popc", "xp", "auto")])  # BASELINE configs[4]
 
 
 @pytest.mark.parametrize("algo,mnk", LARGE)

@@ -1,9 +1,9 @@
 #!/bin/bash
 mkdir -p gpurun_out/r2
 O=gpurun_out/r2
-timeout 300 python tools/r2/xp_check.py check > $O/xp_check.log 2>&1; echo "rc=$?" >> $O/xp_check.log
-tail -40 $O/xp_check.log
-if grep -q "rc=0" $O/xp_check.log; then
-timeout 300 python tools/r2/xp_check.py time 4096x4096x4096 8192x8192x8192 16384x16384x16384 4096x4096x65536 > $O/xp_time.log 2>&1
-cat $O/xp_time.log
-fi
+timeout 1500 python -m pytest -q -x -m gpu tests/test_gpu_parity.py -k "gemm40 or sweep504 or tail_and_layout or large_gemm" > $O/xp_tests.log 2>&1; echo "rc=$?" >> $O/xp_tests.log
+tail -4 $O/xp_tests.log
+for w in gemm4096 gemm8192 gemm16384 gemm4096k65536; do
+timeout 600 python bench.py --workload $w --steps 10 --warmup 3 --no-cpu-baseline 2>/dev/null | tail -1 | cut -c1-1500
+done > $O/xp_bench.log
+cat $O/xp_bench.log

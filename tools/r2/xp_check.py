@@ -43,6 +43,30 @@ if mode == "check":
                     print(d.tolist(), ref[ref != got][:5].tolist(), got[ref != got][:5].tolist())
     sys.exit(1 if bad else 0)
 
+if mode == "bn":  # tile-N sweep of the pre-expanded engine (debug knob)
+    m = n = k = int(sys.argv[2]) if len(sys.argv) > 2 else 8192
+    a, b = words(m, k, 1, 0), words(n, k, 2, 0)
+    out = torch.empty((m, n), device="cuda")
+    bits = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+    _lib.call("bnn_debug_set", _lib.DEBUG_UMMA_BITS, bits)
+    print("debug bits", bits)
+    for bn in (128, 160, 192, 224):
+        _lib.call("bnn_debug_set", _lib.DEBUG_FP4_BN, bn)
+        for _ in range(3):
+            bnn.xnor_rows_gemm(a, b, k, algo="xp", out=out)
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(True), torch.cuda.Event(True)
+        s.record()
+        for _ in range(10):
+            bnn.xnor_rows_gemm(a, b, k, algo="xp", out=out)
+        e.record()
+        e.synchronize()
+        ms = s.elapsed_time(e) / 10
+        print(f"{m}^3 BN={bn}: {ms:.4f} ms {2 * m * n * k / ms / 1e9:.0f} TOPS", flush=True)
+    _lib.call("bnn_debug_set", _lib.DEBUG_FP4_BN, 0)
+    _lib.call("bnn_debug_set", _lib.DEBUG_UMMA_BITS, 0)
+    sys.exit(0)
+
 sizes = [tuple(int(x) for x in a.split("x")) for a in sys.argv[2:]] or [(8192, 8192, 8192)]
 for (m, n, k) in sizes:
     a, b = words(m, k, 1, 0), words(n, k, 2, 0)
