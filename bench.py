@@ -442,12 +442,17 @@ def pipe_peak(algo, workload="c2"):
     """Roofline denominator for the engine that ran (all measured on this GPU)."""
     popc = popc_peak_tops()
     if algo in ("auto", "umma"):
-        # TMA-fed shapes run the kind::mxf4 engine (variant 2); the 2-bit planes run kind::i8
-        kind = "i8" if workload.endswith("2bit") else "mxf4"
+        # every workload's dominant kernel runs kind::mxf4: on bits expanded in SMEM (convs, small
+        # GEMMs), or -- configs[4], 1-bit and 2-bit -- on operands pre-expanded to e2m1 values in
+        # HBM by a pass that is part of the timed step (bnn_gemm_xp.cu, 2-CTA pairs)
+        kind = "mxf4"
+        how = ("operands expanded once per step to e2m1 values in HBM, 2-CTA TMA-fed GEMM "
+               "(bnn_gemm_xp.cu; the expansion pass is inside kernel_ms)"
+               if workload.startswith("gemm") else "bits expanded in SMEM")
         return {"bound": "tensor", "peak": tcgen05_peak_tops(kind), "unit": "TOPS",
                 "peak_source": f"measured: dense tcgen05.mma kind::{kind} issue rate, one CTA per "
                                "SM, 128x256 MMAs back to back (bnn_probe_pipe_peak); the engine "
-                               f"runs kind::{kind} on bits expanded in SMEM",
+                               f"runs kind::{kind} on {how}",
                 "popc_peak": popc, "cublas_int8_tops": int8_tensor_peak_tops()}
     return {"bound": "popc", "peak": popc, "unit": "TOPS",
             "peak_source": "measured: bnn_probe_pipe_peak POPC rate x 64 binary ops "
@@ -699,7 +704,8 @@ def run_gpu_arm(args, rank, world, local_rank):
             "metric": metric, "value": value, "unit": unit, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
-            "dtype": (("b1 planes -> u8 (tcgen05 kind::i8), s32" if name.endswith("2bit")
+            "dtype": (("2-bit codes -> e2m1 grid values (tcgen05 kind::mxf4), exact f32 numerator"
+                       if name.endswith("2bit")
                        else DTYPE) if args.algo in ("auto", "umma") else "u32 (xor/popc words)"),
             "data": "synthetic (seeded, BASELINE.json shapes)",
             "config": {"workload": d["workload"], "M": d["M"], "N": d["N"], "K": d["K"],

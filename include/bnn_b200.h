@@ -205,6 +205,16 @@ int bnn_bitplane_gemm(const uint64_t *A, int64_t lda, int64_t a_plane_stride, in
                       int bits, int64_t M, int64_t N, int64_t K, float *C, int64_t ldc_m,
                       int64_t ldc_n, bnn_stream_t stream);
 
+/* bnn_bitplane_gemm with a device workspace of bnn_xnor_gemm_ws_bytes(M, N, K) bytes: large
+ * shapes (and algo == BNN_ALGO_UMMA_XP) write each 2-bit code's grid value as an e2m1 number
+ * (0..3 or -3, -1, +1, +3: exact) into the workspace and run the pre-expanded 2-CTA
+ * kind::mxf4 GEMM, whose f32 accumulator is the integer numerator itself (9 K < 2^24); same
+ * single f32 rounding, bit-identical outputs.  algo: AUTO, UMMA (planes engine) or UMMA_XP. */
+int bnn_bitplane_gemm_ws(const uint64_t *A, int64_t lda, int64_t a_plane_stride, int a_grid,
+                         const uint64_t *B, int64_t ldb, int64_t b_plane_stride, int b_grid,
+                         int bits, int64_t M, int64_t N, int64_t K, float *C, int64_t ldc_m,
+                         int64_t ldc_n, int algo, void *ws, int64_t ws_bytes, bnn_stream_t stream);
+
 /* Fused epilogue of the GEMM / conv (all fields optional except domain):
  *   v  = domain == BNN_DOT ? 2P - K : P
  *   v  = v * scale[m] + shift[m]                                  (affine)

@@ -50,6 +50,8 @@ SIGNATURES = {
     "bnn_xnor_gemm_ws_bytes": (_i64, [_i64, _i64, _i64]),
     "bnn_xnor_gemm_ws": (_i32, [_vp, _i64, _vp, _i64, _i64, _i64, _i64, _i32, _i32, _vp, _i64,
                                 _i64, _i32, _i32, _vp, _i64, _vp]),
+    "bnn_bitplane_gemm_ws": (_i32, [_vp, _i64, _i64, _i32, _vp, _i64, _i64, _i32, _i32, _i64, _i64,
+                                    _i64, _vp, _i64, _i64, _i32, _vp, _i64, _vp]),
     "bnn_conv_channel_words": (_i64, [_i64]),
     "bnn_conv_weights_reorder": (_i32, [_vp, _i64, _i64, _i64, _i64, _vp, _vp]),
     "bnn_bconv2d": (_i32, [_vp, _i64, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _i64,

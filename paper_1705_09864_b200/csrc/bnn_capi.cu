@@ -50,6 +50,9 @@ int launch_xnor_gemm_xp(const uint64_t *, int64_t, const uint64_t *, int64_t, in
                         float *, int64_t, int64_t, const Epilogue &, cudaStream_t, const float *, void *,
                         int64_t);
 int64_t xnor_gemm_xp_workspace(int64_t M, int64_t N, int64_t K);
+int launch_bitplane_gemm_xp(const uint64_t *, int64_t, int64_t, const uint64_t *, int64_t, int64_t, int64_t,
+                            int64_t, int64_t, float *, int64_t, int64_t, const Epilogue &, cudaStream_t,
+                            void *, int64_t);
 // AUTO: shapes from which the pre-expanded engine wins (measured, profiles/r02)
 static bool xp_auto(int64_t M, int64_t N, int64_t K) {
     return M >= 1024 && N >= 1024 && K >= 2048 && (double)M * (double)N * (double)K >= 3.0e10;
@@ -355,6 +358,14 @@ int bnn_bitplane_gemm(const uint64_t *A, int64_t lda, int64_t a_plane_stride, in
                       const uint64_t *B, int64_t ldb, int64_t b_plane_stride, int b_grid,
                       int bits, int64_t M, int64_t N, int64_t K, float *C, int64_t ldc_m,
                       int64_t ldc_n, bnn_stream_t stream) {
+    return bnn_bitplane_gemm_ws(A, lda, a_plane_stride, a_grid, B, ldb, b_plane_stride, b_grid, bits, M,
+                                N, K, C, ldc_m, ldc_n, 0, nullptr, 0, stream);
+}
+
+int bnn_bitplane_gemm_ws(const uint64_t *A, int64_t lda, int64_t a_plane_stride, int a_grid,
+                         const uint64_t *B, int64_t ldb, int64_t b_plane_stride, int b_grid,
+                         int bits, int64_t M, int64_t N, int64_t K, float *C, int64_t ldc_m,
+                         int64_t ldc_n, int algo, void *ws, int64_t ws_bytes, bnn_stream_t stream) {
     int rc = check_gemm_dims(M, N, K);
     if (rc) return rc;
     BNN_REQUIRE(bits == 2, BNN_EUNSUP, "bit-plane path supports bits == 2, got %d", bits);
@@ -372,6 +383,18 @@ int bnn_bitplane_gemm(const uint64_t *A, int64_t lda, int64_t a_plane_stride, in
     ep.b_alpha = b_grid == BNN_GRID_SIGNED ? 2 : 1;
     ep.b_beta = b_grid == BNN_GRID_SIGNED ? -L : 0;
     ep.inv_gamma = 1.0f / (float)(L * L);
+    BNN_REQUIRE(algo == BNN_ALGO_AUTO || algo == BNN_ALGO_UMMA || algo == BNN_ALGO_UMMA_XP, BNN_EUNSUP,
+                "bit-plane GEMM: algo must be AUTO, UMMA or UMMA_XP");
+    BNN_REQUIRE(ws_bytes >= 0 && (ws || ws_bytes == 0), BNN_EINVAL, "bad workspace");
+    // codes as e2m1 grid values in a workspace + the 2-CTA kind::mxf4 GEMM (bnn_gemm_xp.cu)
+    if (algo == BNN_ALGO_UMMA_XP || (algo == BNN_ALGO_AUTO && ws && xp_auto(M, N, K))) {
+        rc = launch_bitplane_gemm_xp(A, lda, a_plane_stride, B, ldb, b_plane_stride, M, N, K, C, ldc_m,
+                                     ldc_n, ep, as_stream(stream), ws, ws_bytes);
+        if (rc != BNN_EUNSUP) return rc;
+        if (algo == BNN_ALGO_UMMA_XP)
+            return set_error(BNN_EUNSUP, "pre-expanded engine: 9 K < 2^24 and a 128-byte aligned "
+                             "workspace of bnn_xnor_gemm_ws_bytes() needed");
+    }
     return launch_bitplane_gemm_umma(A, lda, a_plane_stride, B, ldb, b_plane_stride, M, N, K, C,
                                      ldc_m, ldc_n, ep, as_stream(stream));
 }

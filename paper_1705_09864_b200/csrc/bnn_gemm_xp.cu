@@ -70,6 +70,48 @@ __global__ void __launch_bounds__(128) expand_pm1_kernel(ExpandOp a, ExpandOp b,
     }
 }
 
+// Multi-bit operands (bits == 2): planes 0 / 1 of a code c = b0 + 2 b1 -> the e2m1 code of
+// the code's grid VALUE numerator: unsigned grid c in {0, 1, 2, 3}, signed grid 2c - 3 in
+// {-3, -1, +1, +3} (all exact in e2m1), so the MMA accumulates sum_k v_a v_b directly
+// (layers.py:240-242, 370-377 numerator; the division by L^2 is the epilogue's one rounding).
+struct ExpandOp2 {
+    const uint2 *p0, *p1;  // bit planes [rows, ld64]
+    uint4 *dst;
+    int64_t ld64, rows;
+    int32_t is_signed;
+};
+__device__ __forceinline__ uint4 expand_code2_val(uint32_t w0, uint32_t w1, int64_t left, bool sgn) {
+    uint32_t v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint32_t b0 = (w0 >> j) & 0x11111111u, b1 = (w1 >> j) & 0x11111111u;
+        if (sgn) {  // c: 0 -> 0xD (-3), 1 -> 0xA (-1), 2 -> 0x2 (+1), 3 -> 0x5 (+3)
+            const uint32_t x = b0 ^ b1, nx = x ^ 0x11111111u;
+            v[j] = nx | (x << 1) | (nx << 2) | ((b1 ^ 0x11111111u) << 3);
+        } else {    // c: 0 -> 0x0, 1 -> 0x2 (1), 2 -> 0x4 (2), 3 -> 0x5 (3)
+            v[j] = (b0 & b1) | ((b0 & ~b1) << 1) | (b1 << 2);
+        }
+    }
+    if (left < 32) {
+        const uint32_t vm = left <= 0 ? 0u : ((1u << left) - 1u);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] &= ((vm >> j) & 0x11111111u) * 0xFu;
+    }
+    return make_uint4(v[0], v[1], v[2], v[3]);
+}
+__global__ void __launch_bounds__(128) expand_code2_kernel(ExpandOp2 a, ExpandOp2 b, int64_t kw64,
+                                                           int64_t K) {
+    const ExpandOp2 op = blockIdx.z == 0 ? a : b;
+    const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= kw64) return;
+    for (int64_t r = blockIdx.y; r < op.rows; r += gridDim.y) {
+        const uint2 x0 = __ldg(op.p0 + r * op.ld64 + w), x1 = __ldg(op.p1 + r * op.ld64 + w);
+        uint4 *dst = op.dst + r * 2 * kw64 + 2 * w;
+        dst[0] = expand_code2_val(x0.x, x1.x, K - 64 * w, op.is_signed);
+        dst[1] = expand_code2_val(x0.y, x1.y, K - 64 * w - 32, op.is_signed);
+    }
+}
+
 // ------------------------------------------------------------------ GEMM
 // kStaged: outputs leave through a per-warp SMEM block and TMA stores (6 operand stages fit);
 // otherwise straight from registers (16 B per row per instruction; outputs TMA cannot address)
@@ -104,7 +146,8 @@ struct Params {
     float *C;
     int64_t ldc_m, ldc_n, M, N;
     int32_t kstages, tiles_m, ntiles;
-    int32_t k_logical, domain;
+    int32_t k_logical, domain;  // domain 2: out = accumulator * scale (multi-bit numerator / L^2)
+    float scale;
     int32_t tma_store, vec4, park;
 };
 
@@ -242,7 +285,7 @@ __global__ void __launch_bounds__(Cfg<BN, kStaged>::kThreads, 1)
         const int e = warp - C::kEpiWarp0, q = warp & 3;
         const uint32_t stg0 = s_epi + e * 2 * C::kStgBytes;
         const uint32_t lead_tempty = mapa_shared(bar_tempty, 0);
-        const bool dot = p.domain == BNN_DOT;
+        const bool dot = p.domain == BNN_DOT, scaled = p.domain == 2;
         const float kf = (float)p.k_logical;
         int it = 0;
         uint32_t nst = 0;  // staged blocks so far (staging buffer parity)
@@ -265,7 +308,7 @@ __global__ void __launch_bounds__(Cfg<BN, kStaged>::kThreads, 1)
 #pragma unroll
                 for (int j = 0; j < 32; ++j) {
                     const float dsum = __uint_as_float(v[j]);
-                    f[j] = dot ? dsum : __fmul_rn(__fadd_rn(dsum, kf), 0.5f);
+                    f[j] = scaled ? __fmul_rn(dsum, p.scale) : (dot ? dsum : __fmul_rn(__fadd_rn(dsum, kf), 0.5f));
                 }
                 if (kStaged && p.tma_store) {
                     const uint32_t stg = stg0 + (nst & 1u) * C::kStgBytes;
@@ -354,6 +397,7 @@ static int launch_cfg(const void *ea, const void *eb, int64_t kb, const GemmStor
     p.C = st.C, p.ldc_m = st.ldc_m, p.ldc_n = st.ldc_n, p.M = M, p.N = N;
     p.kstages = (int32_t)ceil_div(kb, 128), p.tiles_m = (int32_t)tiles_m, p.ntiles = (int32_t)ntiles;
     p.k_logical = ep.k_logical, p.domain = ep.domain;
+    p.scale = ep.inv_gamma;
     p.tma_store = st.has_map;
     p.park = (umma_dbg() & (1 << 21)) ? 1 : 0;
     p.vec4 = st.ldc_n == 1 && st.ldc_m % 4 == 0 && (reinterpret_cast<uintptr_t>(st.C) & 15) == 0;
@@ -377,6 +421,36 @@ static int launch_cfg(const void *ea, const void *eb, int64_t kb, const GemmStor
 }
 
 }  // namespace xp
+
+static int launch_tiles(const void *ea, const void *eb, int64_t kb, const GemmStore &st, const Epilogue &ep,
+                        int64_t M, int64_t N, cudaStream_t s) {
+    using namespace xp;
+    // tile N from {224, 192, 160, 128}: waves over the SM pairs x the cycles of a K = 256 stage.
+    // A stage is bound by the SM's shared-memory port, not the tensor pipe: the TMA writes
+    // (128 + N/2) rows of 128 B and the MMA reads 128 + N rows (its own A rows and ALL of B, the
+    // peer's half included) = 128 B x (256 + 1.5 N) at 128 B/clk, against 2 N tensor cycles
+    // (profiles/r02: 578 cycles per stage measured at N = 224, tensor pipe 79% active)
+    static const int cands[] = {224, 192, 160, 128};
+    const int64_t pairs = sm_count() / 2, tm = ceil_div(M, 2 * umma::BM);
+    int best = 224;
+    int64_t best_cost = -1;
+    for (int bn : cands) {
+        const int64_t cost = ceil_div(tm * ceil_div(N, bn), pairs) * (512 + 3 * bn);
+        if (best_cost < 0 || cost < best_cost) best = bn, best_cost = cost;
+    }
+    if (g_debug.fp4_bn == 128 || g_debug.fp4_bn == 160 || g_debug.fp4_bn == 192 || g_debug.fp4_bn == 224)
+        best = (int)g_debug.fp4_bn;
+    // row-major outputs leave through SMEM staging + TMA stores (6 operand stages); register
+    // stores with a 7th stage measured slower (8192^3: 207 vs 198 us, 4096^3: 54 vs 44 us;
+    // debug bit 1 << 20 selects them, bit 1 << 21 parks the TMA / MMA waits instead of spinning)
+    const bool staged = st.has_map && !(umma_dbg() & (1 << 20));
+    switch (best) {
+        case 128: return staged ? launch_cfg<128, true>(ea, eb, kb, st, ep, M, N, s) : launch_cfg<128, false>(ea, eb, kb, st, ep, M, N, s);
+        case 160: return staged ? launch_cfg<160, true>(ea, eb, kb, st, ep, M, N, s) : launch_cfg<160, false>(ea, eb, kb, st, ep, M, N, s);
+        case 192: return staged ? launch_cfg<192, true>(ea, eb, kb, st, ep, M, N, s) : launch_cfg<192, false>(ea, eb, kb, st, ep, M, N, s);
+        default: return staged ? launch_cfg<224, true>(ea, eb, kb, st, ep, M, N, s) : launch_cfg<224, false>(ea, eb, kb, st, ep, M, N, s);
+    }
+}
 
 int64_t xnor_gemm_xp_workspace(int64_t M, int64_t N, int64_t K) {
     const int64_t kw32 = 2 * ceil_div(K, 64);
@@ -405,31 +479,38 @@ int launch_xnor_gemm_xp(const uint64_t *A, int64_t lda, const uint64_t *B, int64
     expand_pm1_kernel<<<grid, 128, 0, s>>>(oa, ob, kw64, K);
     int rc = check_launch("expand_pm1_kernel");
     if (rc != BNN_OK) return rc;
-    // tile N from {224, 192, 160, 128}: waves over the SM pairs x the cycles of a K = 256 stage.
-    // A stage is bound by the SM's shared-memory port, not the tensor pipe: the TMA writes
-    // (128 + N/2) rows of 128 B and the MMA reads 128 + N rows (its own A rows and ALL of B, the
-    // peer's half included) = 128 B x (256 + 1.5 N) at 128 B/clk, against 2 N tensor cycles
-    // (profiles/r02: 578 cycles per stage measured at N = 224, tensor pipe 79% active)
-    static const int cands[] = {224, 192, 160, 128};
-    const int64_t pairs = sm_count() / 2, tm = ceil_div(M, 2 * umma::BM);
-    int best = 224;
-    int64_t best_cost = -1;
-    for (int bn : cands) {
-        const int64_t cost = ceil_div(tm * ceil_div(N, bn), pairs) * (512 + 3 * bn);
-        if (best_cost < 0 || cost < best_cost) best = bn, best_cost = cost;
-    }
-    if (g_debug.fp4_bn == 128 || g_debug.fp4_bn == 160 || g_debug.fp4_bn == 192 || g_debug.fp4_bn == 224)
-        best = (int)g_debug.fp4_bn;
-    // row-major outputs leave through SMEM staging + TMA stores (6 operand stages); register
-    // stores with a 7th stage measured slower (8192^3: 207 vs 198 us, 4096^3: 54 vs 44 us;
-    // debug bit 1 << 20 selects them, bit 1 << 21 parks the TMA / MMA waits instead of spinning)
-    const bool staged = st.has_map && !(umma_dbg() & (1 << 20));
-    switch (best) {
-        case 128: return staged ? launch_cfg<128, true>(ea, eb, kb, st, ep, M, N, s) : launch_cfg<128, false>(ea, eb, kb, st, ep, M, N, s);
-        case 160: return staged ? launch_cfg<160, true>(ea, eb, kb, st, ep, M, N, s) : launch_cfg<160, false>(ea, eb, kb, st, ep, M, N, s);
-        case 192: return staged ? launch_cfg<192, true>(ea, eb, kb, st, ep, M, N, s) : launch_cfg<192, false>(ea, eb, kb, st, ep, M, N, s);
-        default: return staged ? launch_cfg<224, true>(ea, eb, kb, st, ep, M, N, s) : launch_cfg<224, false>(ea, eb, kb, st, ep, M, N, s);
-    }
+    return launch_tiles(ea, eb, kb, st, ep, M, N, s);
+}
+
+// Multi-bit GEMM (bits == 2) on the same engine: ep carries the grid constants (a_alpha = 2 /
+// a_beta = -3 for the signed grid) and inv_gamma = 1 / L^2; domain 2 = scaled accumulator.
+// BNN_EUNSUP when 9 K >= 2^24 (the f32 accumulator would round) or the workspace is too small.
+int launch_bitplane_gemm_xp(const uint64_t *A, int64_t lda, int64_t a_plane, const uint64_t *B, int64_t ldb,
+                            int64_t b_plane, int64_t M, int64_t N, int64_t K, float *C, int64_t ldc_m,
+                            int64_t ldc_n, const Epilogue &ep_in, cudaStream_t s, void *ws,
+                            int64_t ws_bytes) {
+    using namespace xp;
+    if (!C || 9 * K >= (1ll << 24)) return BNN_EUNSUP;
+    if (!ws || ws_bytes < xnor_gemm_xp_workspace(M, N, K) || (reinterpret_cast<uintptr_t>(ws) & 127))
+        return BNN_EUNSUP;
+    if (M > (1ll << 30) || N > (1ll << 30)) return BNN_EUNSUP;
+    const int64_t kw32 = 2 * ceil_div(K, 64), kb = kw32 * 16, kw64 = kw32 / 2;
+    GemmStore st{};
+    st.C = C, st.ldc_m = ldc_m, st.ldc_n = ldc_n, st.M = M, st.N = N;
+    if (ldc_n == 1) encode_out(st);
+    uint8_t *ea = static_cast<uint8_t *>(ws), *eb = ea + M * kb;
+    ExpandOp2 oa{reinterpret_cast<const uint2 *>(A), reinterpret_cast<const uint2 *>(A + a_plane),
+                 reinterpret_cast<uint4 *>(ea), lda, M, ep_in.a_alpha == 2};
+    ExpandOp2 ob{reinterpret_cast<const uint2 *>(B), reinterpret_cast<const uint2 *>(B + b_plane),
+                 reinterpret_cast<uint4 *>(eb), ldb, N, ep_in.b_alpha == 2};
+    const int64_t rows = M > N ? M : N;
+    dim3 grid((unsigned)ceil_div(kw64, 128), (unsigned)(rows < 32768 ? rows : 32768), 2);
+    expand_code2_kernel<<<grid, 128, 0, s>>>(oa, ob, kw64, K);
+    int rc = check_launch("expand_code2_kernel");
+    if (rc != BNN_OK) return rc;
+    Epilogue ep = ep_in;
+    ep.domain = 2;
+    return launch_tiles(ea, eb, kb, st, ep, M, N, s);
 }
 
 }  // namespace bnn

@@ -147,7 +147,8 @@ def workspace(m: int, n: int, k: int, device) -> torch.Tensor:
 
 def bitplane_gemm(a_planes: torch.Tensor, b_planes: torch.Tensor, k: int, *,
                   a_grid: str = "signed", b_grid: str = "signed", out: torch.Tensor | None = None,
-                  transpose_out: bool = False) -> torch.Tensor:
+                  transpose_out: bool = False, algo: int | str = "auto",
+                  workspace_in: torch.Tensor | None = None) -> torch.Tensor:
     """Multi-bit (bit-plane) GEMM: sum_k v_a v_b for [bits, M, W] x [bits, N, W] planes.
 
     The product the reference's float path computes for bits > 1
@@ -163,6 +164,15 @@ def bitplane_gemm(a_planes: torch.Tensor, b_planes: torch.Tensor, k: int, *,
                           device=a_planes.device)
     ldc_m, ldc_n = (1, out.stride(0)) if transpose_out else (out.stride(0), 1)
     g = {"signed": _lib.GRID_SIGNED, "unsigned": _lib.GRID_UNSIGNED}
+    if isinstance(algo, str):
+        algo = _lib.ALGOS[algo]
+    if algo == _lib.ALGO_UMMA_XP or (algo == _lib.ALGO_AUTO and xp_eligible(m, n, k)):
+        # large shapes: code values as e2m1 numbers in a scratch buffer, 2-CTA TMA-fed engine
+        ws = workspace(m, n, k, a_planes.device) if workspace_in is None else workspace_in
+        _lib.call("bnn_bitplane_gemm_ws", _lib.ptr(a_planes), w, m * w, g[a_grid], _lib.ptr(b_planes),
+                  w, n * w, g[b_grid], bits, m, n, k, _lib.ptr(out), ldc_m, ldc_n, algo, _lib.ptr(ws),
+                  ws.numel(), _lib.stream_ptr())
+        return out
     _lib.call("bnn_bitplane_gemm", _lib.ptr(a_planes), w, m * w, g[a_grid], _lib.ptr(b_planes), w,
               n * w, g[b_grid], bits, m, n, k, _lib.ptr(out), ldc_m, ldc_n, _lib.stream_ptr())
     return out

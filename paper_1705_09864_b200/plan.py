@@ -345,6 +345,12 @@ class BitplanePlan(_Plan):
         self.y = torch.empty((self.m, self.n), dtype=torch.float32, device="cuda")
         self.grids = (a_grid, b_grid)
         self._alloc_common()
+        from .gemm import xp_eligible
+        self.ws = None  # large shapes: scratch of the pre-expanded engine (bnn_bitplane_gemm_ws)
+        if xp_eligible(self.m, self.n, self.k):
+            self.ws = torch.empty(int(_lib.load().bnn_xnor_gemm_ws_bytes(self.m, self.n, self.k)),
+                                  dtype=torch.uint8, device="cuda")
+            self.launches_per_step = 2
 
     @property
     def binary_ops(self) -> int:
@@ -356,7 +362,7 @@ class BitplanePlan(_Plan):
     def kernel(self, stream=None):
         from .gemm import bitplane_gemm
         bitplane_gemm(self.a, self.bw, self.k, a_grid=self.grids[0], b_grid=self.grids[1],
-                      out=self.y)
+                      out=self.y, workspace_in=self.ws)
 
     def run_device(self):
         self.kernel()

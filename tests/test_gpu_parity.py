@@ -481,6 +481,27 @@ def test_bitplane_gemm_exact_integer_decode(bnn, m, n, k, grids):
     assert np.all(np.abs(y - exact) <= 2e-7 * np.maximum(1.0, np.abs(exact))), (m, n, k)
 
 
+@pytest.mark.parametrize("m,n,k", [(40, 64, 96), (300, 257, 1000), (1024, 512, 4096),
+                                   (2048, 1024, 2048), (4096, 4096, 4096)])
+def test_bitplane_gemm_pre_expanded_engine_identical(bnn, m, n, k):
+    """bnn_bitplane_gemm_ws (codes as e2m1 grid values + the 2-CTA kind::mxf4 GEMM) against
+    the planes engine: the same integer numerator and the same single rounding, so the f32
+    outputs are bit-identical for every grid pair, both output layouts and ragged shapes."""
+    rng = np.random.default_rng(m * 3 + n + k)
+    for ga, gb in (("signed", "signed"), ("unsigned", "unsigned"), ("signed", "unsigned")):
+        mk = lambda shape, g: (rng.random(shape, dtype=np.float32) if g == "unsigned"
+                               else rng.standard_normal(shape).astype(np.float32))
+        ap = bnn.bitpack.pack_planes_device(torch.from_numpy(mk((m, k), ga)).cuda(), 2, ga)
+        bp = bnn.bitpack.pack_planes_device(torch.from_numpy(mk((n, k), gb)).cuda(), 2, gb)
+        for tr in (False, True):
+            ref = bnn.gemm.bitplane_gemm(ap, bp, k, a_grid=ga, b_grid=gb, transpose_out=tr, algo="umma")
+            got = bnn.gemm.bitplane_gemm(ap, bp, k, a_grid=ga, b_grid=gb, transpose_out=tr, algo="xp")
+            assert torch.equal(ref, got), (m, n, k, ga, gb, tr)
+    if m * n * k >= 3e10:  # AUTO takes the pre-expanded engine here
+        auto = bnn.gemm.bitplane_gemm(ap, bp, k, a_grid=ga, b_grid=gb, transpose_out=True)
+        assert torch.equal(auto, got)
+
+
 def test_qfullyconnected_2bit_packed_equals_float_path(bnn):
     rng = np.random.default_rng(4)
     layer = bnn.QFullyConnected(300, 70, act_bit=2, weight_bit=2, rng=rng)
