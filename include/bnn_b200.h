@@ -248,6 +248,20 @@ int bnn_xnor_gemm_ex(const uint64_t *A, int64_t lda, const uint64_t *B, int64_t 
                      int64_t N, int64_t K, int a_pad, int b_pad, float *C, int64_t ldc_m,
                      int64_t ldc_n, const bnn_epilogue *ep, int algo, bnn_stream_t stream);
 
+/* bnn_bconv2d_ex with a device workspace (QConv2d.forward INFER_PACKED, layers.py:225-245, same
+ * fused epilogue and results).  For C % 256 == 0, F % 64 == 0 and F <= 1024 (any stride <= 8)
+ * and ws_bytes >= bnn_bconv2d_ws_bytes(...) (128-byte aligned), AUTO and BNN_ALGO_UMMA_XP run the
+ * pre-expanded engine: activations (with a physical halo of +1 codes) and weights expanded once
+ * to e2m1 codes in the workspace, im2col-mode TMA loads, 2-CTA kind::mxf4 GEMM with rows =
+ * output pixels.  bnn_bconv2d_ws_bytes returns 0 for geometries the engine does not take;
+ * every other case, and ws == NULL, is exactly bnn_bconv2d_ex.  The workspace is scratch. */
+int64_t bnn_bconv2d_ws_bytes(int64_t B, int64_t C, int64_t H, int64_t W, int64_t F, int64_t kh,
+                             int64_t kw, int64_t sh, int64_t sw, int64_t ph, int64_t pw);
+int bnn_bconv2d_ws(const uint64_t *x_words, int64_t B, int64_t C, int64_t H, int64_t W,
+                   const uint64_t *w_dev, int64_t F, int64_t kh, int64_t kw, int64_t sh, int64_t sw,
+                   int64_t ph, int64_t pw, float *y, const bnn_epilogue *e, int algo, void *ws,
+                   int64_t ws_bytes, bnn_stream_t stream);
+
 /* Float post-op of a full-precision stem conv (ResNet-18, configs[3]):
  * y = maxpool_k/stride/pad(relu?(BN(x))) with BN in the reference's op order,
  * bit-identical to the unfused sequence.  NCHW f32. */

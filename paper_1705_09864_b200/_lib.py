@@ -52,6 +52,9 @@ SIGNATURES = {
                                 _i64, _i32, _i32, _vp, _i64, _vp]),
     "bnn_bitplane_gemm_ws": (_i32, [_vp, _i64, _i64, _i32, _vp, _i64, _i64, _i32, _i32, _i64, _i64,
                                     _i64, _vp, _i64, _i64, _i32, _vp, _i64, _vp]),
+    "bnn_bconv2d_ws_bytes": (_i64, [_i64] * 11),
+    "bnn_bconv2d_ws": (_i32, [_vp, _i64, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _i64,
+                              _i64, _vp, _vp, _i32, _vp, _i64, _vp]),
     "bnn_conv_channel_words": (_i64, [_i64]),
     "bnn_conv_weights_reorder": (_i32, [_vp, _i64, _i64, _i64, _i64, _vp, _vp]),
     "bnn_bconv2d": (_i32, [_vp, _i64, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _i64,

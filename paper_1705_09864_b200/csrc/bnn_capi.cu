@@ -50,6 +50,11 @@ int launch_xnor_gemm_xp(const uint64_t *, int64_t, const uint64_t *, int64_t, in
                         float *, int64_t, int64_t, const Epilogue &, cudaStream_t, const float *, void *,
                         int64_t);
 int64_t xnor_gemm_xp_workspace(int64_t M, int64_t N, int64_t K);
+int launch_bconv2d_xp(const uint64_t *, int64_t, int64_t, int64_t, int64_t, const uint64_t *, int64_t,
+                      int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, float *,
+                      const Epilogue &, cudaStream_t, const float *, void *, int64_t);
+int64_t bconv2d_xp_workspace(int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,
+                             int64_t);
 int launch_bitplane_gemm_xp(const uint64_t *, int64_t, int64_t, const uint64_t *, int64_t, int64_t, int64_t,
                             int64_t, int64_t, float *, int64_t, int64_t, const Epilogue &, cudaStream_t,
                             void *, int64_t);
@@ -232,7 +237,7 @@ static int engine_of(int algo, Epilogue &ep) {
     return -1;
 }
 static bool is_umma(int algo) {
-    return algo == BNN_ALGO_AUTO || algo == BNN_ALGO_UMMA ||
+    return algo == BNN_ALGO_AUTO || algo == BNN_ALGO_UMMA || algo == BNN_ALGO_UMMA_XP ||
            (algo >= BNN_ALGO_UMMA_V0 && algo <= BNN_ALGO_UMMA_V4);
 }
 
@@ -522,10 +527,10 @@ int bnn_conv_weights_reorder(const uint64_t *w_ref, int64_t F, int64_t C, int64_
     return launch_conv_weights_reorder(w_ref, F, C, kh, kw, w_dev, as_stream(stream));
 }
 
-int bnn_bconv2d_ex(const uint64_t *x_words, int64_t B, int64_t C, int64_t H, int64_t W,
-                   const uint64_t *w_dev, int64_t F, int64_t kh, int64_t kw, int64_t sh,
-                   int64_t sw, int64_t ph, int64_t pw, float *y, const bnn_epilogue *e, int algo,
-                   bnn_stream_t stream) {
+static int bconv2d_impl(const uint64_t *x_words, int64_t B, int64_t C, int64_t H, int64_t W,
+                        const uint64_t *w_dev, int64_t F, int64_t kh, int64_t kw, int64_t sh,
+                        int64_t sw, int64_t ph, int64_t pw, float *y, const bnn_epilogue *e, int algo,
+                        bnn_stream_t stream, void *ws, int64_t ws_bytes) {
     // tensor.conv_output_hw (tensor.py:15-27)
     BNN_REQUIRE(B >= 1 && C >= 1 && H >= 1 && W >= 1 && F >= 1 && kh >= 1 && kw >= 1 &&
                     sh >= 1 && sw >= 1 && ph >= 0 && pw >= 0,
@@ -557,11 +562,46 @@ int bnn_bconv2d_ex(const uint64_t *x_words, int64_t B, int64_t C, int64_t H, int
             return launch_bconv2d_bmma(x_words, B, C, H, W, w_dev, F, kh, kw, sh, sw, ph, pw, oh,
                                        ow, y, ep, as_stream(stream), e->residual);
         case BNN_ALGO_UMMA:
+            // C % 256 == 0 with a workspace: activations (+1 halo) and weights expanded once to
+            // e2m1 codes, im2col-TMA-fed 2-CTA kind::mxf4 GEMM with the full fused epilogue
+            if (algo == BNN_ALGO_UMMA_XP || (algo == BNN_ALGO_AUTO && ws)) {
+                rc = launch_bconv2d_xp(x_words, B, C, H, W, w_dev, F, kh, kw, sh, sw, ph, pw, oh, ow, y,
+                                       ep, as_stream(stream), e->residual, ws, ws_bytes);
+                if (rc != BNN_EUNSUP) return rc;
+                if (algo == BNN_ALGO_UMMA_XP)
+                    return set_error(BNN_EUNSUP, "pre-expanded conv engine: C %% 256 == 0, F %% 64 == 0 "
+                                     "and a workspace of bnn_bconv2d_ws_bytes() needed");
+            }
             return launch_bconv2d_umma(x_words, B, C, H, W, w_dev, F, kh, kw, sh, sw, ph, pw, oh,
                                        ow, y, ep, as_stream(stream), e->residual);
         default:
             return set_error(BNN_EUNSUP, "algorithm %d not available", algo);
     }
+}
+
+int bnn_bconv2d_ex(const uint64_t *x_words, int64_t B, int64_t C, int64_t H, int64_t W,
+                   const uint64_t *w_dev, int64_t F, int64_t kh, int64_t kw, int64_t sh,
+                   int64_t sw, int64_t ph, int64_t pw, float *y, const bnn_epilogue *e, int algo,
+                   bnn_stream_t stream) {
+    return bconv2d_impl(x_words, B, C, H, W, w_dev, F, kh, kw, sh, sw, ph, pw, y, e, algo, stream,
+                        nullptr, 0);
+}
+
+int64_t bnn_bconv2d_ws_bytes(int64_t B, int64_t C, int64_t H, int64_t W, int64_t F, int64_t kh,
+                             int64_t kw, int64_t sh, int64_t sw, int64_t ph, int64_t pw) {
+    if (B < 1 || C < 1 || H < 1 || W < 1 || F < 1 || kh < 1 || kw < 1 || sh < 1 || sw < 1 || ph < 0 ||
+        pw < 0 || C % 256 != 0 || F % 64 != 0 || F > 1024 || sh > 8 || sw > 8 || kh > 128 || kw > 128)
+        return 0;
+    return bconv2d_xp_workspace(B, C, H, W, F, kh, kw, ph, pw);
+}
+
+int bnn_bconv2d_ws(const uint64_t *x_words, int64_t B, int64_t C, int64_t H, int64_t W,
+                   const uint64_t *w_dev, int64_t F, int64_t kh, int64_t kw, int64_t sh, int64_t sw,
+                   int64_t ph, int64_t pw, float *y, const bnn_epilogue *e, int algo, void *ws,
+                   int64_t ws_bytes, bnn_stream_t stream) {
+    BNN_REQUIRE(ws_bytes >= 0 && (ws || ws_bytes == 0), BNN_EINVAL, "bad workspace");
+    return bconv2d_impl(x_words, B, C, H, W, w_dev, F, kh, kw, sh, sw, ph, pw, y, e, algo, stream, ws,
+                        ws_bytes);
 }
 
 int bnn_bconv2d(const uint64_t *x_words, int64_t B, int64_t C, int64_t H, int64_t W,

@@ -513,4 +513,445 @@ int launch_bitplane_gemm_xp(const uint64_t *A, int64_t lda, int64_t a_plane, con
     return launch_tiles(ea, eb, kb, st, ep, M, N, s);
 }
 
+// ================================================================== convolution
+// Stride-s convs with C % 256 == 0 on the same engine (bnn_bconv2d_ws): the packed NHWC
+// activations are expanded once into e2m1 codes with a physical halo of +1.0 codes (the
+// reference's zero-pad-then-binarize, tensor.py:73-74 + bitpack.py:39), the weights into
+// [F, K/2] code rows, and the GEMM's A operand (rows = output pixels, one TMEM lane each) is
+// fetched by im2col-mode TMA loads of 128 pixels x 128 bytes (256 channels of one filter tap)
+// per CTA and stage; B = a BN-row slice of the filters.  Lanes = pixels, so for every filter a
+// warp reads / writes 32 consecutive pixels of the NCHW output and shortcut (coalesced), and a
+// pixel's 32 sign bits are one u32 of the next layer's packed NHWC input, built in-lane.
+// Epilogue in the reference op order (layers.py:225-245, 598-602): value -> scale / shift ->
+// BatchNorm -> + shortcut -> f32 store and / or sign-pack.
+namespace xp {
+
+struct ConvExpand {
+    const uint2 *x;   // packed NHWC [B, H, W, cw64]
+    uint4 *e;         // codes [B, Hp, Wp, 2 cw64] uint4 (C / 2 bytes per pixel)
+    const uint2 *w;   // packed weights [F, kw64]
+    uint4 *we;        // codes [F, 2 kw64] uint4
+    int64_t npad, wwords;  // B * Hp * Wp * cw64 activation items, F * kw64 weight items
+    int32_t H, W, Hp, Wp, ph, pw, cw64;
+};
+
+__global__ void __launch_bounds__(256) expand_conv_kernel(ConvExpand c) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (blockIdx.y == 1) {  // weights: every bit is a valid +-1
+        if (i >= c.wwords) return;
+        const uint2 v = __ldg(c.w + i);
+        c.we[2 * i] = expand_pm1(v.x, 64);
+        c.we[2 * i + 1] = expand_pm1(v.y, 64);
+        return;
+    }
+    if (i >= c.npad) return;
+    const int64_t pix = i / c.cw64;
+    const int wd = (int)(i - pix * c.cw64);
+    const int xx = (int)(pix % c.Wp);
+    const int64_t t = pix / c.Wp;
+    const int yy = (int)(t % c.Hp);
+    const int64_t b = t / c.Hp;
+    const int iy = yy - c.ph, ix = xx - c.pw;
+    uint4 lo, hi;
+    if ((unsigned)iy < (unsigned)c.H && (unsigned)ix < (unsigned)c.W) {
+        const uint2 v = __ldg(c.x + ((b * c.H + iy) * c.W + ix) * c.cw64 + wd);
+        lo = expand_pm1(v.x, 64);
+        hi = expand_pm1(v.y, 64);
+    } else {
+        lo = hi = make_uint4(0x22222222u, 0x22222222u, 0x22222222u, 0x22222222u);  // halo: +1
+    }
+    c.e[2 * i] = lo;
+    c.e[2 * i + 1] = hi;
+}
+
+template <int BN>
+struct ConvCfg {
+    static_assert(BN % 32 == 0 && BN >= 64 && BN <= 224, "pair tile N");
+    static constexpr int kStages = 6;
+    static constexpr int kABytes = BM * 128;  // this CTA's 128 pixels x 256 channel codes
+    static constexpr int kBRows = BN / 2;     // this CTA's half of the filter rows
+    static constexpr int kStageBytes = kABytes + kBRows * 128;
+    static constexpr int kTmaWarp = 0, kMmaWarp = 1, kEpiWarp0 = 2, kEpiWarps = 4;
+    static constexpr int kThreads = (kEpiWarp0 + kEpiWarps) * 32;
+    static constexpr int kMaxF = 1024;        // per-filter epilogue parameters staged in SMEM
+    static constexpr int off_par = kStages * kStageBytes;  // [6][kMaxF] f32
+    static constexpr int off_bars = off_par + 6 * kMaxF * 4;
+    static constexpr int kNumBars = 2 * kStages + 4;
+    static constexpr int off_tmem = off_bars + kNumBars * 8;
+    static constexpr int kSmemBytes = off_tmem + 16 + 1024;
+    static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
+    static constexpr int kSfCol = 2 * BN;
+    static constexpr uint32_t kIdesc = (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                                       (1u << 23) | ((uint32_t)(2 * BM >> 4) << 24);
+};
+
+struct ConvParams {
+    float *y;
+    const float *res;
+    uint32_t *pack_out;
+    int64_t pack_ld32;
+    int32_t *pack_flags;
+    const float *scale, *shift, *bn_mean, *bn_inv, *bn_gamma, *bn_beta;
+    int64_t npix, ohw;
+    int32_t F, ow, sh, sw, kw, chunks;  // chunks = C / 256 (stages per filter tap)
+    int32_t kstages, tiles_m, ntiles, k_logical, domain;
+};
+
+__device__ __forceinline__ void tma_load_im2col_pair(uint32_t dst, const CUtensorMap *map, int c, int w,
+                                                     int h, int n, uint16_t off_w, uint16_t off_h,
+                                                     uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.im2col.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3, %4, %5}], [%6], {%7, %8};\n" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c), "r"(w), "r"(h), "r"(n), "r"(bar), "h"(off_w),
+        "h"(off_h)
+        : "memory");
+}
+
+template <int BN>
+__global__ void __launch_bounds__(ConvCfg<BN>::kThreads, 1)
+    xconv_xp_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
+                    ConvParams p) {
+    using C = ConvCfg<BN>;
+    constexpr int S = C::kStages;
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t sbase_raw = smem_u32(smem_raw);
+    const uint32_t sbase = (sbase_raw + 1023u) & ~1023u;
+    uint8_t *sgen = smem_raw + (sbase - sbase_raw);
+    const uint32_t s_stage = sbase;
+    float *s_par = reinterpret_cast<float *>(sgen + C::off_par);
+    const uint32_t bar_full = sbase + C::off_bars;
+    const uint32_t bar_empty = bar_full + S * 8;
+    const uint32_t bar_tfull = bar_empty + S * 8;
+    const uint32_t bar_tempty = bar_tfull + 2 * 8;
+    uint32_t *s_tmem = reinterpret_cast<uint32_t *>(sgen + C::off_tmem);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    uint32_t crank;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(crank));
+    const int t0 = (int)(blockIdx.x >> 1), tstep = (int)(gridDim.x >> 1);
+    const uint32_t kstages = (uint32_t)p.kstages;
+
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(bar_full + 8 * s, 1);
+            mbar_init(bar_empty + 8 * s, 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(bar_tfull + 8 * b, 1);
+            mbar_init(bar_tempty + 8 * b, 2 * C::kEpiWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&amap)));
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&bmap)));
+    }
+    if (warp == C::kMmaWarp) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+            smem_u32(s_tmem)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+    }
+    // per-filter epilogue parameters (identity where absent): scale, shift, mean, inv_std, gamma, beta
+    for (int f = tid; f < p.F; f += blockDim.x) {
+        s_par[f] = p.scale ? __ldg(p.scale + f) : 1.0f;
+        s_par[C::kMaxF + f] = p.shift ? __ldg(p.shift + f) : 0.0f;
+        s_par[2 * C::kMaxF + f] = p.bn_mean ? __ldg(p.bn_mean + f) : 0.0f;
+        s_par[3 * C::kMaxF + f] = p.bn_mean ? __ldg(p.bn_inv + f) : 1.0f;
+        s_par[4 * C::kMaxF + f] = p.bn_mean ? __ldg(p.bn_gamma + f) : 1.0f;
+        s_par[5 * C::kMaxF + f] = p.bn_mean ? __ldg(p.bn_beta + f) : 0.0f;
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *s_tmem;
+    if (warp >= C::kEpiWarp0) {
+        const uint32_t one[8] = {0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu,
+                                 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu};
+        for (int col = C::kSfCol; col < 512; col += 8)
+            tmem_st8(tmem + ((uint32_t)((warp & 3) * 32) << 16) + col, one);
+        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+    }
+    fence_before();
+    __syncthreads();
+    cluster_sync();
+    fence_after();
+
+    if (warp == C::kTmaWarp) {
+        // ================================================================ TMA producer
+        if (lane == 0) {
+            uint32_t g = 0;
+            const uint32_t lead_full = bar_full & 0xFEFFFFFFu;
+#pragma unroll 1
+            for (int tile = t0; tile < p.ntiles; tile += tstep) {
+                const int tm = tile % p.tiles_m, tn = tile / p.tiles_m;
+                // this CTA's first output pixel -> window corner in the padded input
+                int64_t n0 = (int64_t)tm * 2 * BM + crank * BM;
+                if (n0 >= p.npix) n0 = 0;  // (a half-tile past the end: its rows are never stored)
+                const int cb = (int)(n0 / p.ohw);
+                const int pp = (int)(n0 - (int64_t)cb * p.ohw);
+                const int cy = (pp / p.ow) * p.sh, cx = (pp % p.ow) * p.sw;
+                const int brow = tn * BN + (int)crank * C::kBRows;
+                int chunk = 0, ti = 0, tj = 0;
+#pragma unroll 1
+                for (uint32_t ks = 0; ks < kstages; ++ks, ++g) {
+                    const uint32_t s = g % S;
+                    if (g >= S) mbar_wait_spin(bar_empty + 8 * s, ((g / S) - 1) & 1u);
+                    if (crank == 0) mbar_arrive_expect_tx(bar_full + 8 * s, 2 * C::kStageBytes);
+                    const uint32_t dst = s_stage + s * C::kStageBytes;
+                    tma_load_im2col_pair(dst, &amap, chunk * 128, cx, cy, cb, (uint16_t)tj, (uint16_t)ti,
+                                         lead_full + 8 * s);
+                    tma_load_2d_pair(dst + C::kABytes, &bmap, (int)(ks * 128), brow, lead_full + 8 * s);
+                    if (++chunk == p.chunks) {
+                        chunk = 0;
+                        if (++tj == p.kw) tj = 0, ++ti;
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == C::kMmaWarp) {
+        // ================================================================ MMA issuer (leader CTA)
+        if (crank == 0) {
+            uint32_t g = 0;
+            int it = 0;
+            const uint32_t sfc = tmem + C::kSfCol;
+#pragma unroll 1
+            for (int tile = t0; tile < p.ntiles; tile += tstep, ++it) {
+                const int buf = it & 1;
+                if (it >= 2) mbar_wait_cluster(bar_tempty + 8 * buf, (uint32_t)((it >> 1) - 1) & 1u);
+                fence_after();
+                const uint32_t d = tmem + buf * BN;
+#pragma unroll 1
+                for (uint32_t ks = 0; ks < kstages; ++ks, ++g) {
+                    const uint32_t s = g % S;
+                    mbar_wait_spin(bar_full + 8 * s, (g / S) & 1u);
+                    fence_after();
+                    const uint32_t a_addr = s_stage + s * C::kStageBytes;
+                    const uint64_t da = sw128_desc(a_addr), db = sw128_desc(a_addr + C::kABytes);
+                    if (elect_one_sync()) {
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk)
+                            mma_fp4_pair<C::kIdesc>(d, da + 2 * kk, db + 2 * kk, sfc, sfc,
+                                                    (ks | (uint32_t)kk) != 0 ? 1u : 0u);
+                        umma_commit_pair(bar_empty + 8 * s);
+                    }
+                    __syncwarp();
+                }
+                if (elect_one_sync()) umma_commit_pair(bar_tfull + 8 * buf);
+                __syncwarp();
+            }
+        }
+    } else {
+        // ================================================================ epilogue (lane = pixel)
+        const int q = warp & 3;
+        const uint32_t lead_tempty = mapa_shared(bar_tempty, 0);
+        const bool dot = p.domain == BNN_DOT;
+        const bool affine = p.scale != nullptr || p.shift != nullptr, has_bn = p.bn_mean != nullptr;
+        const float kf = (float)p.k_logical;
+        int it = 0;
+#pragma unroll 1
+        for (int tile = t0; tile < p.ntiles; tile += tstep, ++it) {
+            const int buf = it & 1;
+            const int tm = tile % p.tiles_m, tn = tile / p.tiles_m;
+            const int64_t n = (int64_t)tm * 2 * BM + crank * BM + q * 32 + lane;  // output pixel
+            const bool nok = n < p.npix;
+            const int64_t nn = nok ? n : 0;
+            const int64_t b = nn / p.ohw;
+            const int64_t base = b * p.F * p.ohw + (nn - b * p.ohw);  // + f * ohw
+            mbar_wait_sleep(bar_tfull + 8 * buf, (uint32_t)(it >> 1) & 1u);
+            fence_after();
+            const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + buf * BN;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t v[32];
+                tmem_ld32(taddr + c * 32, v);
+                const int f0 = tn * BN + c * 32;
+                if (f0 >= p.F) continue;  // (warp-uniform; F % 32 == 0)
+                float f[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    float x = __uint_as_float(v[j]);
+                    if (!dot) x = __fmul_rn(__fadd_rn(x, kf), 0.5f);
+                    if (affine) x = __fadd_rn(__fmul_rn(x, s_par[f0 + j]), s_par[C::kMaxF + f0 + j]);
+                    if (has_bn)
+                        x = __fadd_rn(__fmul_rn(s_par[4 * C::kMaxF + f0 + j],
+                                                __fmul_rn(__fsub_rn(x, s_par[2 * C::kMaxF + f0 + j]),
+                                                          s_par[3 * C::kMaxF + f0 + j])),
+                                      s_par[5 * C::kMaxF + f0 + j]);
+                    f[j] = x;
+                }
+                if (nok) {
+                    const int64_t o = base + (int64_t)f0 * p.ohw;
+                    if (p.res) {  // all 32 loads in flight before any use
+                        float r[32];
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) r[j] = __ldg(p.res + o + j * p.ohw);
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) f[j] = __fadd_rn(f[j], r[j]);
+                    }
+                    if (p.y) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) p.y[o + j * p.ohw] = f[j];
+                    }
+                    if (p.pack_out) {
+                        uint32_t word = 0;
+                        float nf = 0.0f;
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            word |= (f[j] >= 0.0f ? 1u : 0u) << j;
+                            nf = __fmaf_rn(f[j], 0.0f, nf);
+                        }
+                        p.pack_out[n * p.pack_ld32 + (f0 >> 5)] = word;
+                        if (p.pack_flags && nf != 0.0f) atomicOr(p.pack_flags, 1);
+                    }
+                }
+            }
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(lead_tempty + 8 * buf);
+        }
+    }
+
+    fence_before();
+    __syncthreads();
+    cluster_sync();
+    if (warp == C::kMmaWarp) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+    }
+}
+
+typedef CUresult (*EncodeIm2colU8Fn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                     const cuuint64_t *, const cuuint64_t *, const int *, const int *,
+                                     cuuint32_t, cuuint32_t, const cuuint32_t *, CUtensorMapInterleave,
+                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// im2col map over the halo'd code tensor {C/2 bytes, Wp, Hp, B}: 128 pixels x 128 bytes per load,
+// window corners traversed with the conv strides, no out-of-bounds taps (the halo is physical)
+static int encode_codes_im2col(CUtensorMap &map, const void *e, int64_t cb, int64_t Wp, int64_t Hp,
+                               int64_t B, int64_t ow, int64_t oh, int64_t sw, int64_t sh) {
+    static EncodeIm2colU8Fn fn = nullptr;
+    if (!fn) {
+        void *q = nullptr;
+        cudaDriverEntryPointQueryResult r;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &q, cudaEnableDefault, &r) == cudaSuccess &&
+            r == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeIm2colU8Fn>(q);
+    }
+    if (!fn) return set_error(BNN_ECUDA, "cuTensorMapEncodeIm2col unavailable");
+    const cuuint64_t dims[4] = {(cuuint64_t)cb, (cuuint64_t)Wp, (cuuint64_t)Hp, (cuuint64_t)B};
+    const cuuint64_t strides[3] = {(cuuint64_t)cb, (cuuint64_t)(cb * Wp), (cuuint64_t)(cb * Wp * Hp)};
+    const int lower[2] = {0, 0};
+    const int upper[2] = {(int)((ow - 1) * sw - (Wp - 1)), (int)((oh - 1) * sh - (Hp - 1))};
+    const cuuint32_t estr[4] = {1, (cuuint32_t)sw, (cuuint32_t)sh, 1};
+    CUresult r = fn(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void *>(e), dims, strides, lower,
+                    upper, 128, (cuuint32_t)BM, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_error(BNN_ECUDA, "cuTensorMapEncodeIm2col failed (codes)");
+    return BNN_OK;
+}
+
+template <int BN>
+static int launch_conv_cfg(const CUtensorMap &amap, const void *we, int64_t kb, const ConvParams &p_in,
+                           cudaStream_t s) {
+    using C = ConvCfg<BN>;
+    auto kern = xconv_xp_kernel<BN>;
+    CUtensorMap bmap;
+    int rc = encode_codes(bmap, we, p_in.F, kb, C::kBRows);
+    if (rc != BNN_OK) return rc;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+        configured = true;
+    }
+    ConvParams p = p_in;
+    const int64_t tiles_m = ceil_div(p.npix, 2 * BM), tiles_n = ceil_div((int64_t)p.F, BN);
+    if (tiles_m * tiles_n > (1ll << 30)) return set_error(BNN_EUNSUP, "too many tiles");
+    p.tiles_m = (int32_t)tiles_m, p.ntiles = (int32_t)(tiles_m * tiles_n);
+    const int64_t pairs = sm_count() / 2;
+    int grid = (int)(p.ntiles < pairs ? p.ntiles : pairs) * 2;
+    if (g_debug.grid_cap > 0 && grid > g_debug.grid_cap) grid = (int)((g_debug.grid_cap + 1) & ~1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(C::kThreads);
+    cfg.dynamicSmemBytes = C::kSmemBytes;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, amap, bmap, p);
+    return check_launch("xconv_xp_kernel");
+}
+
+}  // namespace xp
+
+static bool conv_xp_shape_ok(int64_t C, int64_t F, int64_t kh, int64_t kw, int64_t sh, int64_t sw) {
+    return C % 256 == 0 && F % 64 == 0 && F <= xp::ConvCfg<128>::kMaxF && sh <= 8 && sw <= 8 &&
+           kh <= 128 && kw <= 128;
+}
+
+int64_t bconv2d_xp_workspace(int64_t B, int64_t C, int64_t H, int64_t W, int64_t F, int64_t kh, int64_t kw,
+                             int64_t ph, int64_t pw) {
+    const int64_t e = B * (H + 2 * ph) * (W + 2 * pw) * (C / 2);
+    return ((e + 1023) / 1024) * 1024 + F * kh * kw * (C / 2);
+}
+
+// BNN_EUNSUP: geometry / workspace not eligible (the caller runs the packed engines)
+int launch_bconv2d_xp(const uint64_t *x, int64_t B, int64_t C, int64_t H, int64_t W, const uint64_t *w,
+                      int64_t F, int64_t kh, int64_t kw, int64_t sh, int64_t sw, int64_t ph, int64_t pw,
+                      int64_t oh, int64_t ow, float *y, const Epilogue &ep, cudaStream_t s,
+                      const float *res, void *ws, int64_t ws_bytes) {
+    using namespace xp;
+    if (!conv_xp_shape_ok(C, F, kh, kw, sh, sw)) return BNN_EUNSUP;
+    if (!ws || ws_bytes < bconv2d_xp_workspace(B, C, H, W, F, kh, kw, ph, pw) ||
+        (reinterpret_cast<uintptr_t>(ws) & 127))
+        return BNN_EUNSUP;
+    if (ep.a_alpha != 1 || ep.a_beta != 0 || ep.b_alpha != 1 || ep.b_beta != 0) return BNN_EUNSUP;
+    const int64_t Hp = H + 2 * ph, Wp = W + 2 * pw, cb = C / 2, cw64 = C / 64;
+    const int64_t up_w = (ow - 1) * sw - (Wp - 1), up_h = (oh - 1) * sh - (Hp - 1);
+    if (up_w < -128 || up_w > 0 || up_h < -128 || up_h > 0 || Wp > 65535 || Hp > 65535) return BNN_EUNSUP;
+    const int64_t npix = B * oh * ow, K = C * kh * kw, kb = K / 2;
+    if (npix > (1ll << 30) || B * Hp * Wp * cw64 > (1ll << 40)) return BNN_EUNSUP;
+    uint8_t *e = static_cast<uint8_t *>(ws);
+    uint8_t *we = e + ((B * Hp * Wp * cb + 1023) / 1024) * 1024;
+    ConvExpand ce{reinterpret_cast<const uint2 *>(x), reinterpret_cast<uint4 *>(e),
+                  reinterpret_cast<const uint2 *>(w), reinterpret_cast<uint4 *>(we),
+                  B * Hp * Wp * cw64, F * (K / 64), (int32_t)H, (int32_t)W, (int32_t)Hp, (int32_t)Wp,
+                  (int32_t)ph, (int32_t)pw, (int32_t)cw64};
+    const int64_t items = ce.npad > ce.wwords ? ce.npad : ce.wwords;
+    dim3 grid((unsigned)ceil_div(items, 256), 2);
+    expand_conv_kernel<<<grid, 256, 0, s>>>(ce);
+    int rc = check_launch("expand_conv_kernel");
+    if (rc != BNN_OK) return rc;
+    CUtensorMap amap;
+    rc = encode_codes_im2col(amap, e, cb, Wp, Hp, B, ow, oh, sw, sh);
+    if (rc != BNN_OK) return rc;
+    ConvParams p{};
+    p.y = y, p.res = res, p.pack_out = ep.pack_out, p.pack_ld32 = ep.pack_ld32, p.pack_flags = ep.pack_flags;
+    p.scale = ep.scale, p.shift = ep.shift, p.bn_mean = ep.bn_mean, p.bn_inv = ep.bn_inv;
+    p.bn_gamma = ep.bn_gamma, p.bn_beta = ep.bn_beta;
+    p.npix = npix, p.ohw = oh * ow, p.F = (int32_t)F, p.ow = (int32_t)ow, p.sh = (int32_t)sh;
+    p.sw = (int32_t)sw, p.kw = (int32_t)kw, p.chunks = (int32_t)(C / 256);
+    p.kstages = (int32_t)(kh * kw * (C / 256)), p.k_logical = ep.k_logical, p.domain = ep.domain;
+    // filter tile from {224, 192, 160, 128}: waves over the SM pairs x the stage cost model
+    static const int cands[] = {224, 192, 160, 128};
+    const int64_t pairs = sm_count() / 2, tm = ceil_div(npix, 2 * umma::BM);
+    int best = 128;
+    int64_t best_cost = -1;
+    for (int bn : cands) {
+        const int64_t cost = ceil_div(tm * ceil_div(F, bn), pairs) * (512 + 3 * bn);
+        if (best_cost < 0 || cost <= best_cost) best = bn, best_cost = cost;
+    }
+    switch (best) {
+        case 128: return launch_conv_cfg<128>(amap, we, kb, p, s);
+        case 160: return launch_conv_cfg<160>(amap, we, kb, p, s);
+        case 192: return launch_conv_cfg<192>(amap, we, kb, p, s);
+        default: return launch_conv_cfg<224>(amap, we, kb, p, s);
+    }
+}
+
 }  // namespace bnn

@@ -133,16 +133,20 @@ def xp_eligible(m: int, n: int, k: int) -> bool:
 _WORKSPACES: dict = {}
 
 
-def workspace(m: int, n: int, k: int, device) -> torch.Tensor:
-    """Scratch for bnn_xnor_gemm_ws: one growing u8 buffer per (device, stream) -- calls on
-    one stream are ordered, so they can share it."""
-    need = int(_lib.load().bnn_xnor_gemm_ws_bytes(m, n, k))
+def scratch(need: int, device) -> torch.Tensor:
+    """One growing u8 buffer per (device, stream) for the pre-expanded engines -- calls on one
+    stream are ordered, so they can share it."""
     key = (torch.device(device).index, int(torch.cuda.current_stream().cuda_stream))
     ws = _WORKSPACES.get(key)
     if ws is None or ws.numel() < need:
         ws = torch.empty(need, dtype=torch.uint8, device=device)
         _WORKSPACES[key] = ws
     return ws
+
+
+def workspace(m: int, n: int, k: int, device) -> torch.Tensor:
+    """Scratch for bnn_xnor_gemm_ws / bnn_bitplane_gemm_ws."""
+    return scratch(int(_lib.load().bnn_xnor_gemm_ws_bytes(m, n, k)), device)
 
 
 def bitplane_gemm(a_planes: torch.Tensor, b_planes: torch.Tensor, k: int, *,

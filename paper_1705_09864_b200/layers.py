@@ -276,15 +276,38 @@ class QConv2d(_QLayer):
                              f"{self.pad[0]},{self.pad[1]}")
         return oh, ow
 
+    def conv_workspace(self, b: int, h: int, w: int, algo: int):
+        """Scratch of the pre-expanded conv engine (bnn_bconv2d_ws) for this geometry, or None
+        when the engine does not take it (C % 256 != 0, ...) or another engine was asked for.
+        One buffer per (device, stream), shared by all layers: calls on a stream are ordered."""
+        if algo not in (_lib.ALGO_AUTO, _lib.ALGO_UMMA_XP):
+            return None
+        kh, kw = self.kernel
+        need = int(_lib.load().bnn_bconv2d_ws_bytes(b, self.in_channels, h, w, self.filters, kh, kw,
+                                                    self.stride[0], self.stride[1], self.pad[0],
+                                                    self.pad[1]))
+        if need <= 0:
+            return None
+        from .gemm import scratch
+        return scratch(need, "cuda")
+
     def forward_packed_words(self, x_words: torch.Tensor, b: int, h: int, w: int,
                              out: torch.Tensor | None = None, scale=None, shift=None):
         """Conv on already-packed NHWC words -> f32 NCHW (no host sync)."""
+        import ctypes
         kh, kw = self.kernel
         oh, ow = self.output_hw(h, w)
         if out is None:
             out = torch.empty((b, self.filters, oh, ow), dtype=torch.float32, device="cuda")
         wd = self.device_weights()
         algo = _lib.ALGOS[self.algo] if isinstance(self.algo, str) else self.algo
+        ws = self.conv_workspace(b, h, w, algo)
+        if ws is not None:
+            e = make_epilogue(self.domain, scale=scale, shift=shift)
+            _lib.call("bnn_bconv2d_ws", _lib.ptr(x_words), b, self.in_channels, h, w, _lib.ptr(wd),
+                      self.filters, kh, kw, self.stride[0], self.stride[1], self.pad[0], self.pad[1],
+                      _lib.ptr(out), ctypes.byref(e), algo, _lib.ptr(ws), ws.numel(), _lib.stream_ptr())
+            return out
         _lib.call("bnn_bconv2d", _lib.ptr(x_words), b, self.in_channels, h, w, _lib.ptr(wd),
                   self.filters, kh, kw, self.stride[0], self.stride[1], self.pad[0], self.pad[1],
                   _lib.ptr(out), self.domain, _lib.ptr(scale), _lib.ptr(shift), algo,
@@ -336,9 +359,15 @@ class QConv2d(_QLayer):
                           pack_flags=flags if pack_out else None)
         wd = self.device_weights()
         algo = _lib.ALGOS[self.algo] if isinstance(self.algo, str) else self.algo
-        _lib.call("bnn_bconv2d_ex", _lib.ptr(xw), b, self.in_channels, h, w, _lib.ptr(wd),
-                  self.filters, kh, kw, self.stride[0], self.stride[1], self.pad[0], self.pad[1],
-                  _lib.ptr(out), ctypes.byref(e), algo, _lib.stream_ptr())
+        ws = self.conv_workspace(b, h, w, algo)
+        if ws is not None:
+            _lib.call("bnn_bconv2d_ws", _lib.ptr(xw), b, self.in_channels, h, w, _lib.ptr(wd),
+                      self.filters, kh, kw, self.stride[0], self.stride[1], self.pad[0], self.pad[1],
+                      _lib.ptr(out), ctypes.byref(e), algo, _lib.ptr(ws), ws.numel(), _lib.stream_ptr())
+        else:
+            _lib.call("bnn_bconv2d_ex", _lib.ptr(xw), b, self.in_channels, h, w, _lib.ptr(wd),
+                      self.filters, kh, kw, self.stride[0], self.stride[1], self.pad[0], self.pad[1],
+                      _lib.ptr(out), ctypes.byref(e), algo, _lib.stream_ptr())
         self._finish(flags)
         if pack_out:
             return PackedNHWC(pw_out, (b, self.filters, oh, ow), out)

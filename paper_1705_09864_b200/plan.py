@@ -137,6 +137,17 @@ class ConvPlan(_Plan):
         self.lib = _lib.load()
         kh, kw = layer.kernel
         self.m, self.n, self.k = layer.filters, batch * self.oh * self.ow, c * kh * kw
+        # C % 256 == 0: scratch of the pre-expanded conv engine (its own buffer: run_host slices
+        # run on several streams); the expansion pass is part of kernel()
+        self.ws = None
+        need = int(self.lib.bnn_bconv2d_ws_bytes(batch, c, h, w, layer.filters, kh, kw, layer.stride[0],
+                                                 layer.stride[1], layer.pad[0], layer.pad[1]))
+        if need > 0 and self.algo in (_lib.ALGO_AUTO, _lib.ALGO_UMMA_XP):
+            self.ws = torch.empty(need, dtype=torch.uint8, device="cuda")
+            self.ws_slices = {}
+            from .layers import make_epilogue
+            self.ep = make_epilogue(layer.domain)
+            self.launches_per_step = 3  # pack, expand, conv
 
     @property
     def binary_ops(self) -> int:
@@ -153,6 +164,14 @@ class ConvPlan(_Plan):
         s = _lib.stream_ptr() if stream is None else stream
         L = self.layer
         kh, kw = L.kernel
+        if self.ws is not None:
+            import ctypes
+            _lib.check(self.lib.bnn_bconv2d_ws(self.xw.data_ptr(), self.b, L.in_channels, self.h,
+                                               self.w, self.wd.data_ptr(), L.filters, kh, kw,
+                                               L.stride[0], L.stride[1], L.pad[0], L.pad[1],
+                                               self.y.data_ptr(), ctypes.byref(self.ep), self.algo,
+                                               self.ws.data_ptr(), self.ws.numel(), s), "bconv2d_ws")
+            return
         _lib.check(self.lib.bnn_bconv2d(self.xw.data_ptr(), self.b, L.in_channels, self.h,
                                         self.w, self.wd.data_ptr(), L.filters, kh, kw,
                                         L.stride[0], L.stride[1], L.pad[0], L.pad[1],
@@ -175,6 +194,21 @@ class ConvPlan(_Plan):
         _lib.check(self.lib.bnn_pack_nchw_f32(x.data_ptr(), nb, L.in_channels, self.h, self.w,
                                               xw.data_ptr(), self.mode, self.flags.data_ptr(),
                                               stream), "pack")
+        if self.ws is not None:
+            import ctypes
+            # one scratch per image range: the slices of a pipelined run overlap on streams
+            ws = self.ws_slices.get((i0, i1))
+            if ws is None:
+                ws = torch.empty(int(self.lib.bnn_bconv2d_ws_bytes(
+                    nb, L.in_channels, self.h, self.w, L.filters, kh, kw, L.stride[0], L.stride[1],
+                    L.pad[0], L.pad[1])), dtype=torch.uint8, device="cuda")
+                self.ws_slices[(i0, i1)] = ws
+            _lib.check(self.lib.bnn_bconv2d_ws(xw.data_ptr(), nb, L.in_channels, self.h, self.w,
+                                               self.wd.data_ptr(), L.filters, kh, kw, L.stride[0],
+                                               L.stride[1], L.pad[0], L.pad[1], y.data_ptr(),
+                                               ctypes.byref(self.ep), self.algo, ws.data_ptr(),
+                                               ws.numel(), stream), "bconv2d_ws")
+            return
         _lib.check(self.lib.bnn_bconv2d(xw.data_ptr(), nb, L.in_channels, self.h, self.w,
                                         self.wd.data_ptr(), L.filters, kh, kw, L.stride[0],
                                         L.stride[1], L.pad[0], L.pad[1], y.data_ptr(), L.domain,

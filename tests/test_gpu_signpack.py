@@ -109,6 +109,66 @@ def test_conv_sign_pack_epilogue(bnn, case, variant, with_res):
     assert torch.equal(nxt.forward_fused(only), nxt.forward_fused(plain))
 
 
+# pre-expanded conv engine (bnn_bconv2d_ws, C % 256 == 0, F % 64 == 0): strides 1 / 2, 1x1 and
+# 5x5 kernels, asymmetric geometry, image sizes that make 32-pixel lane groups straddle images,
+# pixel counts below / across the 256-row pair tile, ResNet-18 layer-3 / layer-4 shapes
+XP_CASES = [
+    (2, 256, 7, 7, 128, 3, 3, (1, 1), (1, 1), 11),
+    (4, 256, 5, 5, 256, 3, 3, (1, 1), (1, 1), 12),
+    (3, 512, 9, 11, 192, 1, 1, (2, 2), (0, 0), 13),
+    (2, 256, 9, 8, 64, 3, 3, (2, 2), (1, 1), 14),
+    (1, 512, 6, 6, 512, 5, 5, (1, 1), (2, 2), 15),
+    (5, 256, 10, 13, 320, 3, 2, (1, 2), (1, 0), 16),
+    (33, 256, 14, 14, 256, 3, 3, (1, 1), (1, 1), 17),
+    (20, 512, 7, 7, 512, 3, 3, (1, 1), (1, 1), 18),
+]
+
+
+@pytest.mark.parametrize("case", XP_CASES)
+def test_conv_pre_expanded_engine(bnn, case):
+    """Every epilogue form of bnn_bconv2d_ws on the pre-expanded engine: bit-identical to the
+    packed tcgen05 engine, and to the oracle's conv -> BN -> (+ shortcut) composition."""
+    b, c, h, w, f, kh, kw, stride, pad, seed = case
+    x, wt = wl.conv_case_inputs(case)
+    outs = {}
+    bn = _BN(f, c * kh * kw, seed)
+    for algo in ("umma2", "xp", "auto"):
+        layer = bnn.QConvolution(c, f, (kh, kw), stride, pad, domain="dot")
+        layer.weight = wt
+        layer.pack()
+        layer.algo = algo
+        oh, ow = layer.output_hw(h, w)
+        res = torch.from_numpy(np.random.default_rng(seed + 50).standard_normal(
+            (b, f, oh, ow)).astype(np.float32)).cuda()
+        res.view(-1)[::9] = 0.0
+        xd = torch.from_numpy(x).cuda()
+        o = {"plain": layer.forward(xd, bnn.INFER_PACKED),
+             "bn": layer.forward_fused(xd, bn),
+             "bn_res": layer.forward_fused(xd, bn, residual=res)}
+        pk = layer.forward_fused(xd, bn, residual=res, pack_out=True)
+        o["pk_f32"], o["pk_words"] = pk.f32, pk.words
+        o["only_words"] = layer.forward_fused(xd, bn, pack_out=True, f32_out=False).words
+        pop = bnn.QConvolution(c, f, (kh, kw), stride, pad)  # popcount domain
+        pop.weight = wt
+        pop.pack()
+        pop.algo = algo
+        o["popcount"] = pop.forward(xd, bnn.INFER_PACKED)
+        outs[algo] = o
+    for key, ref in outs["umma2"].items():
+        for algo in ("xp", "auto"):
+            assert torch.equal(outs[algo][key], ref), (algo, key)
+    p = orc.qconv_packed(x, wt, stride, pad).astype(np.float32)
+    assert np.array_equal(outs["xp"]["popcount"].cpu().numpy(), p)
+    ref = 2 * p - np.float32(c * kh * kw)
+    assert np.array_equal(outs["xp"]["plain"].cpu().numpy(), ref)
+    sh = (1, -1, 1, 1)
+    ref = bn.gamma.reshape(sh) * ((ref - bn.mean.reshape(sh)) * bn.inv.reshape(sh)) + bn.beta.reshape(sh)
+    assert np.array_equal(outs["xp"]["bn"].cpu().numpy(), ref.astype(np.float32))
+    y = outs["xp"]["bn_res"].cpu().numpy()
+    assert np.array_equal(y, (ref + res.cpu().numpy()).astype(np.float32))
+    assert np.array_equal(outs["xp"]["pk_words"].cpu().numpy(), _oracle_pack_nhwc(y))
+
+
 def _gemm_ex(bnn, a, bw, m, n, k, c, ldc_m, ldc_n, e, algo="auto"):
     from paper_1705_09864_b200 import _lib
     _lib.call("bnn_xnor_gemm_ex", _lib.ptr(a), a.stride(0), _lib.ptr(bw), bw.stride(0), m, n, k,
