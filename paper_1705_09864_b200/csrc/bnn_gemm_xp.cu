@@ -571,7 +571,9 @@ struct ConvCfg {
     static constexpr int kABytes = BM * 128;  // this CTA's 128 pixels x 256 channel codes
     static constexpr int kBRows = BN / 2;     // this CTA's half of the filter rows
     static constexpr int kStageBytes = kABytes + kBRows * 128;
-    static constexpr int kTmaWarp = 0, kMmaWarp = 1, kEpiWarp0 = 2, kEpiWarps = 4;
+    // two epilogue warps per TMEM lane quadrant (alternate 32-filter chunks): a tile has only
+    // kh * kw * C / 256 stages, so its epilogue must finish within a few microseconds
+    static constexpr int kTmaWarp = 0, kMmaWarp = 1, kEpiWarp0 = 2, kEpiWarps = 8;
     static constexpr int kThreads = (kEpiWarp0 + kEpiWarps) * 32;
     static constexpr int kMaxF = 1024;        // per-filter epilogue parameters staged in SMEM
     static constexpr int off_par = kStages * kStageBytes;  // [6][kMaxF] f32
@@ -595,6 +597,7 @@ struct ConvParams {
     int64_t npix, ohw;
     int32_t F, ow, sh, sw, kw, chunks;  // chunks = C / 256 (stages per filter tap)
     int32_t kstages, tiles_m, ntiles, k_logical, domain;
+    int32_t raster, wp, dbg;
 };
 
 __device__ __forceinline__ void tma_load_im2col_pair(uint32_t dst, const CUtensorMap *map, int c, int w,
@@ -611,7 +614,7 @@ __device__ __forceinline__ void tma_load_im2col_pair(uint32_t dst, const CUtenso
 template <int BN>
 __global__ void __launch_bounds__(ConvCfg<BN>::kThreads, 1)
     xconv_xp_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
-                    ConvParams p) {
+                    const __grid_constant__ CUtensorMap rmap, ConvParams p) {
     using C = ConvCfg<BN>;
     constexpr int S = C::kStages;
     extern __shared__ uint8_t smem_raw[];
@@ -663,7 +666,7 @@ __global__ void __launch_bounds__(ConvCfg<BN>::kThreads, 1)
     __syncthreads();
     fence_after();
     const uint32_t tmem = *s_tmem;
-    if (warp >= C::kEpiWarp0) {
+    if (warp >= C::kEpiWarp0 && warp < C::kEpiWarp0 + 4) {
         const uint32_t one[8] = {0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu,
                                  0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu};
         for (int col = C::kSfCol; col < 512; col += 8)
@@ -697,8 +700,11 @@ __global__ void __launch_bounds__(ConvCfg<BN>::kThreads, 1)
                     if (g >= S) mbar_wait_spin(bar_empty + 8 * s, ((g / S) - 1) & 1u);
                     if (crank == 0) mbar_arrive_expect_tx(bar_full + 8 * s, 2 * C::kStageBytes);
                     const uint32_t dst = s_stage + s * C::kStageBytes;
-                    tma_load_im2col_pair(dst, &amap, chunk * 128, cx, cy, cb, (uint16_t)tj, (uint16_t)ti,
-                                         lead_full + 8 * s);
+                    if (p.raster)  // (timing experiment: tiled loads of the same bytes)
+                        tma_load_2d_pair(dst, &rmap, chunk * 128, (int)n0 + ti * p.wp + tj, lead_full + 8 * s);
+                    else
+                        tma_load_im2col_pair(dst, &amap, chunk * 128, cx, cy, cb, (uint16_t)tj, (uint16_t)ti,
+                                             lead_full + 8 * s);
                     tma_load_2d_pair(dst + C::kABytes, &bmap, (int)(ks * 128), brow, lead_full + 8 * s);
                     if (++chunk == p.chunks) {
                         chunk = 0;
@@ -742,7 +748,7 @@ __global__ void __launch_bounds__(ConvCfg<BN>::kThreads, 1)
         }
     } else {
         // ================================================================ epilogue (lane = pixel)
-        const int q = warp & 3;
+        const int q = warp & 3, half = (warp - C::kEpiWarp0) >> 2;
         const uint32_t lead_tempty = mapa_shared(bar_tempty, 0);
         const bool dot = p.domain == BNN_DOT;
         const bool affine = p.scale != nullptr || p.shift != nullptr, has_bn = p.bn_mean != nullptr;
@@ -761,7 +767,8 @@ __global__ void __launch_bounds__(ConvCfg<BN>::kThreads, 1)
             fence_after();
             const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + buf * BN;
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
+            for (int c = half; c < BN / 32; c += 2) {
+                if (p.dbg & 2) break;
                 uint32_t v[32];
                 tmem_ld32(taddr + c * 32, v);
                 const int f0 = tn * BN + c * 32;
@@ -788,7 +795,7 @@ __global__ void __launch_bounds__(ConvCfg<BN>::kThreads, 1)
 #pragma unroll
                         for (int j = 0; j < 32; ++j) f[j] = __fadd_rn(f[j], r[j]);
                     }
-                    if (p.y) {
+                    if (p.y && !(p.dbg & 1)) {
 #pragma unroll
                         for (int j = 0; j < 32; ++j) p.y[o + j * p.ohw] = f[j];
                     }
@@ -852,8 +859,8 @@ static int encode_codes_im2col(CUtensorMap &map, const void *e, int64_t cb, int6
 }
 
 template <int BN>
-static int launch_conv_cfg(const CUtensorMap &amap, const void *we, int64_t kb, const ConvParams &p_in,
-                           cudaStream_t s) {
+static int launch_conv_cfg(const CUtensorMap &amap, const CUtensorMap &rmap, const void *we, int64_t kb,
+                           const ConvParams &p_in, cudaStream_t s) {
     using C = ConvCfg<BN>;
     auto kern = xconv_xp_kernel<BN>;
     CUtensorMap bmap;
@@ -883,7 +890,7 @@ static int launch_conv_cfg(const CUtensorMap &amap, const void *we, int64_t kb, 
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, kern, amap, bmap, p);
+    cudaLaunchKernelEx(&cfg, kern, amap, bmap, rmap, p);
     return check_launch("xconv_xp_kernel");
 }
 
@@ -930,7 +937,12 @@ int launch_bconv2d_xp(const uint64_t *x, int64_t B, int64_t C, int64_t H, int64_
     CUtensorMap amap;
     rc = encode_codes_im2col(amap, e, cb, Wp, Hp, B, ow, oh, sw, sh);
     if (rc != BNN_OK) return rc;
+    CUtensorMap rmap;
+    rc = encode_codes(rmap, e, B * Hp * Wp, cb, BM);
+    if (rc != BNN_OK) return rc;
     ConvParams p{};
+    p.raster = (umma_dbg() & (1 << 22)) ? 1 : 0, p.wp = (int32_t)Wp;
+    p.dbg = (umma_dbg() >> 23) & 3;  // timing experiments: 1 = no global stores, 2 = no epilogue work
     p.y = y, p.res = res, p.pack_out = ep.pack_out, p.pack_ld32 = ep.pack_ld32, p.pack_flags = ep.pack_flags;
     p.scale = ep.scale, p.shift = ep.shift, p.bn_mean = ep.bn_mean, p.bn_inv = ep.bn_inv;
     p.bn_gamma = ep.bn_gamma, p.bn_beta = ep.bn_beta;
@@ -947,10 +959,10 @@ int launch_bconv2d_xp(const uint64_t *x, int64_t B, int64_t C, int64_t H, int64_
         if (best_cost < 0 || cost <= best_cost) best = bn, best_cost = cost;
     }
     switch (best) {
-        case 128: return launch_conv_cfg<128>(amap, we, kb, p, s);
-        case 160: return launch_conv_cfg<160>(amap, we, kb, p, s);
-        case 192: return launch_conv_cfg<192>(amap, we, kb, p, s);
-        default: return launch_conv_cfg<224>(amap, we, kb, p, s);
+        case 128: return launch_conv_cfg<128>(amap, rmap, we, kb, p, s);
+        case 160: return launch_conv_cfg<160>(amap, rmap, we, kb, p, s);
+        case 192: return launch_conv_cfg<192>(amap, rmap, we, kb, p, s);
+        default: return launch_conv_cfg<224>(amap, rmap, we, kb, p, s);
     }
 }
 
