@@ -47,6 +47,13 @@ __device__ __forceinline__ uint4 expand_pm1(uint32_t x, int64_t left) {
     return make_uint4(v[0], v[1], v[2], v[3]);
 }
 
+// one 256-bit store (32-byte aligned): a warp writes 1 KB runs of whole sectors per instruction
+__device__ __forceinline__ void st256(uint4 *dst, const uint4 &lo, const uint4 &hi) {
+    asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"l"(dst), "r"(lo.x),
+                 "r"(lo.y), "r"(lo.z), "r"(lo.w), "r"(hi.x), "r"(hi.y), "r"(hi.z), "r"(hi.w)
+                 : "memory");
+}
+
 // HBM-bound pass over both operands: a thread takes one u64 word of kRows consecutive
 // rows (kRows loads in flight), a warp writes 1 KB runs of codes
 constexpr int kExpRows = 4;
@@ -63,9 +70,8 @@ __global__ void __launch_bounds__(128) expand_pm1_kernel(ExpandOp a, ExpandOp b,
 #pragma unroll
         for (int i = 0; i < kExpRows; ++i) {
             if (r0 + i >= op.rows) break;
-            uint4 *dst = op.dst + (r0 + i) * 2 * kw64 + 2 * w;
-            dst[0] = expand_pm1(x[i].x, K - 64 * w);
-            dst[1] = expand_pm1(x[i].y, K - 64 * w - 32);
+            st256(op.dst + (r0 + i) * 2 * kw64 + 2 * w, expand_pm1(x[i].x, K - 64 * w),
+                  expand_pm1(x[i].y, K - 64 * w - 32));
         }
     }
 }
@@ -106,9 +112,8 @@ __global__ void __launch_bounds__(128) expand_code2_kernel(ExpandOp2 a, ExpandOp
     if (w >= kw64) return;
     for (int64_t r = blockIdx.y; r < op.rows; r += gridDim.y) {
         const uint2 x0 = __ldg(op.p0 + r * op.ld64 + w), x1 = __ldg(op.p1 + r * op.ld64 + w);
-        uint4 *dst = op.dst + r * 2 * kw64 + 2 * w;
-        dst[0] = expand_code2_val(x0.x, x1.x, K - 64 * w, op.is_signed);
-        dst[1] = expand_code2_val(x0.y, x1.y, K - 64 * w - 32, op.is_signed);
+        st256(op.dst + r * 2 * kw64 + 2 * w, expand_code2_val(x0.x, x1.x, K - 64 * w, op.is_signed),
+              expand_code2_val(x0.y, x1.y, K - 64 * w - 32, op.is_signed));
     }
 }
 
@@ -162,7 +167,30 @@ __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap
         : "memory");
 }
 
-template <int BN, bool kStaged>
+// the same, multicast to the CTAs of `mask` (same SMEM offset in each; every destination's
+// bytes complete on the barrier of its own pair's leader)
+__device__ __forceinline__ void tma_load_2d_pair_mc(uint32_t dst, const CUtensorMap *map, int c0, int c1,
+                                                    uint32_t bar, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        ".multicast::cluster [%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar), "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit_mask(uint32_t bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+            bar),
+        "h"(mask)
+        : "memory");
+}
+
+// kQuad: clusters of FOUR CTAs = two pairs working on vertically adjacent tiles (same B tile).
+// Each CTA fetches a quarter of the B tile and multicasts it to the CTA of the same pair rank
+// in the other pair, so a CTA pulls 128 + BN/4 instead of 128 + BN/2 rows per stage through the
+// L2 -> SM fabric (the measured bound of the pair kernel).  A stage may be refilled only when
+// BOTH pairs' MMAs have retired it: every commit is multicast to all four CTAs' empty barriers.
+template <int BN, bool kStaged, bool kQuad>
 __global__ void __launch_bounds__(Cfg<BN, kStaged>::kThreads, 1)
     xnor_xp_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
                    const __grid_constant__ CUtensorMap omap, Params p, uint64_t *trace_buf) {
@@ -181,15 +209,22 @@ __global__ void __launch_bounds__(Cfg<BN, kStaged>::kThreads, 1)
     uint32_t *s_tmem = reinterpret_cast<uint32_t *>(sgen + C::off_tmem);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    uint32_t crank;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(crank));
-    const int t0 = (int)(blockIdx.x >> 1), tstep = (int)(gridDim.x >> 1);
+    uint32_t clrank;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(clrank));
+    const uint32_t crank = clrank & 1u;           // rank in the CTA pair; rank 0 issues the MMAs
+    const uint32_t qidx = kQuad ? clrank >> 1 : 0u;  // which pair of the cluster
+    const uint32_t lead = clrank & ~1u;           // cluster rank of this pair's leader
+    constexpr int kCl = kQuad ? 4 : 2;
+    const int t0 = (int)(blockIdx.x / kCl), tstep = (int)(gridDim.x / kCl);
+    // quad: the tile loop runs over super-tiles of two vertically adjacent tiles
+    const int tiles_mu = kQuad ? (p.tiles_m + 1) / 2 : p.tiles_m;
+    const int nunits = kQuad ? tiles_mu * (p.ntiles / p.tiles_m) : p.ntiles;
     const uint32_t kstages = (uint32_t)p.kstages;
 
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(bar_full + 8 * s, 1);
-            mbar_init(bar_empty + 8 * s, 1);
+            mbar_init(bar_empty + 8 * s, kQuad ? 2 : 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(bar_tfull + 8 * b, 1);
@@ -228,10 +263,10 @@ __global__ void __launch_bounds__(Cfg<BN, kStaged>::kThreads, 1)
             uint32_t g = 0;
             const uint32_t lead_full = bar_full & 0xFEFFFFFFu;
 #pragma unroll 1
-            for (int tile = t0; tile < p.ntiles; tile += tstep) {
-                const int tm = tile % p.tiles_m, tn = tile / p.tiles_m;
-                const int arow = tm * 2 * BM + (int)crank * BM;
-                const int brow = tn * BN + (int)crank * C::kBRows;
+            for (int tile = t0; tile < nunits; tile += tstep) {
+                const int tm = (tile % tiles_mu) * (kQuad ? 2 : 1) + (int)qidx, tn = tile / tiles_mu;
+                const int arow = tm * 2 * BM + (int)crank * BM;  // (past M in an odd last super-tile: zero fill)
+                const int brow = tn * BN + (int)crank * C::kBRows + (int)qidx * (C::kBRows / 2);
 #pragma unroll 1
                 for (uint32_t ks = 0; ks < kstages; ++ks, ++g) {
                     const uint32_t s = g % S;
@@ -242,7 +277,11 @@ __global__ void __launch_bounds__(Cfg<BN, kStaged>::kThreads, 1)
                     if (crank == 0) mbar_arrive_expect_tx(bar_full + 8 * s, 2 * C::kStageBytes);
                     const uint32_t dst = s_stage + s * C::kStageBytes;
                     tma_load_2d_pair(dst, &amap, (int)(ks * 128), arow, lead_full + 8 * s);
-                    tma_load_2d_pair(dst + C::kABytes, &bmap, (int)(ks * 128), brow, lead_full + 8 * s);
+                    if constexpr (kQuad)
+                        tma_load_2d_pair_mc(dst + C::kABytes + qidx * (C::kBRows / 2) * 128, &bmap, (int)(ks * 128),
+                                            brow, lead_full + 8 * s, (uint16_t)(5u << crank));
+                    else
+                        tma_load_2d_pair(dst + C::kABytes, &bmap, (int)(ks * 128), brow, lead_full + 8 * s);
                 }
             }
         }
@@ -254,7 +293,7 @@ __global__ void __launch_bounds__(Cfg<BN, kStaged>::kThreads, 1)
             int it = 0;
             const uint32_t sfc = tmem + C::kSfCol;
 #pragma unroll 1
-            for (int tile = t0; tile < p.ntiles; tile += tstep, ++it) {
+            for (int tile = t0; tile < nunits; tile += tstep, ++it) {
                 const int buf = it & 1;
                 if (it >= 2) mbar_wait_cluster(bar_tempty + 8 * buf, (uint32_t)((it >> 1) - 1) & 1u);
                 fence_after();
@@ -272,11 +311,11 @@ __global__ void __launch_bounds__(Cfg<BN, kStaged>::kThreads, 1)
                         for (int kk = 0; kk < 4; ++kk)
                             mma_fp4_pair<C::kIdesc>(d, da + 2 * kk, db + 2 * kk, sfc, sfc,
                                                     (ks | (uint32_t)kk) != 0 ? 1u : 0u);
-                        umma_commit_pair(bar_empty + 8 * s);
+                        umma_commit_mask(bar_empty + 8 * s, kQuad ? (uint16_t)0xF : (uint16_t)3);
                     }
                     __syncwarp();
                 }
-                if (elect_one_sync()) umma_commit_pair(bar_tfull + 8 * buf);
+                if (elect_one_sync()) umma_commit_mask(bar_tfull + 8 * buf, (uint16_t)(3u << lead));
                 __syncwarp();
             }
         }
@@ -284,15 +323,15 @@ __global__ void __launch_bounds__(Cfg<BN, kStaged>::kThreads, 1)
         // ================================================================ epilogue
         const int e = warp - C::kEpiWarp0, q = warp & 3;
         const uint32_t stg0 = s_epi + e * 2 * C::kStgBytes;
-        const uint32_t lead_tempty = mapa_shared(bar_tempty, 0);
+        const uint32_t lead_tempty = mapa_shared(bar_tempty, lead);
         const bool dot = p.domain == BNN_DOT, scaled = p.domain == 2;
         const float kf = (float)p.k_logical;
         int it = 0;
         uint32_t nst = 0;  // staged blocks so far (staging buffer parity)
 #pragma unroll 1
-        for (int tile = t0; tile < p.ntiles; tile += tstep, ++it) {
+        for (int tile = t0; tile < nunits; tile += tstep, ++it) {
             const int buf = it & 1;
-            const int tm = tile % p.tiles_m, tn = tile / p.tiles_m;
+            const int tm = (tile % tiles_mu) * (kQuad ? 2 : 1) + (int)qidx, tn = tile / tiles_mu;
             const int64_t mq = (int64_t)tm * 2 * BM + crank * BM + q * 32, n0 = (int64_t)tn * BN;
             const int64_t m = mq + lane;
             mbar_wait_sleep(bar_tfull + 8 * buf, (uint32_t)(it >> 1) & 1u);
@@ -376,20 +415,16 @@ static int encode_codes(CUtensorMap &map, const void *base, int64_t rows, int64_
     return BNN_OK;
 }
 
-template <int BN, bool kStaged>
+template <int BN, bool kStaged, bool kQuad>
 static int launch_cfg(const void *ea, const void *eb, int64_t kb, const GemmStore &st, const Epilogue &ep,
                       int64_t M, int64_t N, cudaStream_t s) {
     using C = Cfg<BN, kStaged>;
-    auto kern = xnor_xp_kernel<BN, kStaged>;
+    auto kern = xnor_xp_kernel<BN, kStaged, kQuad>;
+    constexpr int kCl = kQuad ? 4 : 2;
     CUtensorMap amap, bmap;
     int rc = encode_codes(amap, ea, M, kb, BM);
-    if (rc == BNN_OK) rc = encode_codes(bmap, eb, N, kb, C::kBRows);
+    if (rc == BNN_OK) rc = encode_codes(bmap, eb, N, kb, kQuad ? C::kBRows / 2 : C::kBRows);
     if (rc != BNN_OK) return rc;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-        configured = true;
-    }
     const int64_t tiles_m = ceil_div(M, 2 * BM), tiles_n = ceil_div(N, BN);
     const int64_t ntiles = tiles_m * tiles_n;
     if (ntiles > (1ll << 30)) return set_error(BNN_EUNSUP, "too many tiles");
@@ -401,21 +436,33 @@ static int launch_cfg(const void *ea, const void *eb, int64_t kb, const GemmStor
     p.tma_store = st.has_map;
     p.park = (umma_dbg() & (1 << 21)) ? 1 : 0;
     p.vec4 = st.ldc_n == 1 && st.ldc_m % 4 == 0 && (reinterpret_cast<uintptr_t>(st.C) & 15) == 0;
-    const int64_t pairs = sm_count() / 2;
-    int grid = (int)(ntiles < pairs ? ntiles : pairs) * 2;
-    if (g_debug.grid_cap > 0 && grid > g_debug.grid_cap) grid = (int)((g_debug.grid_cap + 1) & ~1);
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(C::kThreads);
     cfg.dynamicSmemBytes = C::kSmemBytes;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.x = kCl;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    // clusters that can be co-resident (one CTA per SM; a cluster lives inside one GPC)
+    static int max_clusters = -1;
+    if (max_clusters < 0) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+        cfg.gridDim = dim3((unsigned)(sm_count() / kCl * kCl));
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) {
+            cudaGetLastError();
+            n = sm_count() / kCl;
+        }
+        max_clusters = n;
+    }
+    const int64_t units = kQuad ? ceil_div(tiles_m, 2) * tiles_n : ntiles;
+    int grid = (int)(units < max_clusters ? units : max_clusters) * kCl;
+    if (g_debug.grid_cap > 0 && grid > g_debug.grid_cap) grid = (int)((g_debug.grid_cap + kCl - 1) / kCl * kCl);
+    cfg.gridDim = dim3((unsigned)grid);
     cudaLaunchKernelEx(&cfg, kern, amap, bmap, st.omap, p, g_debug.trace_buf);
     return check_launch("xnor_xp_kernel");
 }
@@ -444,11 +491,23 @@ static int launch_tiles(const void *ea, const void *eb, int64_t kb, const GemmSt
     // stores with a 7th stage measured slower (8192^3: 207 vs 198 us, 4096^3: 54 vs 44 us;
     // debug bit 1 << 20 selects them, bit 1 << 21 parks the TMA / MMA waits instead of spinning)
     const bool staged = st.has_map && !(umma_dbg() & (1 << 20));
+    // clusters of two pairs sharing the B tile by TMA multicast: bit-exact but measured SLOWER
+    // (8192^3: 211 vs 197 us) -- fewer rows cross the L2 -> SM fabric, yet every CTA's SMEM still
+    // takes the same writes and MMA reads, which is what bounds a stage; debug bit 1 << 26 only
+    const bool quad = staged && M > 2 * umma::BM && (umma_dbg() & (1 << 26)) != 0;
+    if (quad) {
+        switch (best) {
+            case 128: return launch_cfg<128, true, true>(ea, eb, kb, st, ep, M, N, s);
+            case 160: return launch_cfg<160, true, true>(ea, eb, kb, st, ep, M, N, s);
+            case 192: return launch_cfg<192, true, true>(ea, eb, kb, st, ep, M, N, s);
+            default: return launch_cfg<224, true, true>(ea, eb, kb, st, ep, M, N, s);
+        }
+    }
     switch (best) {
-        case 128: return staged ? launch_cfg<128, true>(ea, eb, kb, st, ep, M, N, s) : launch_cfg<128, false>(ea, eb, kb, st, ep, M, N, s);
-        case 160: return staged ? launch_cfg<160, true>(ea, eb, kb, st, ep, M, N, s) : launch_cfg<160, false>(ea, eb, kb, st, ep, M, N, s);
-        case 192: return staged ? launch_cfg<192, true>(ea, eb, kb, st, ep, M, N, s) : launch_cfg<192, false>(ea, eb, kb, st, ep, M, N, s);
-        default: return staged ? launch_cfg<224, true>(ea, eb, kb, st, ep, M, N, s) : launch_cfg<224, false>(ea, eb, kb, st, ep, M, N, s);
+        case 128: return staged ? launch_cfg<128, true, false>(ea, eb, kb, st, ep, M, N, s) : launch_cfg<128, false, false>(ea, eb, kb, st, ep, M, N, s);
+        case 160: return staged ? launch_cfg<160, true, false>(ea, eb, kb, st, ep, M, N, s) : launch_cfg<160, false, false>(ea, eb, kb, st, ep, M, N, s);
+        case 192: return staged ? launch_cfg<192, true, false>(ea, eb, kb, st, ep, M, N, s) : launch_cfg<192, false, false>(ea, eb, kb, st, ep, M, N, s);
+        default: return staged ? launch_cfg<224, true, false>(ea, eb, kb, st, ep, M, N, s) : launch_cfg<224, false, false>(ea, eb, kb, st, ep, M, N, s);
     }
 }
 
@@ -540,8 +599,7 @@ __global__ void __launch_bounds__(256) expand_conv_kernel(ConvExpand c) {
     if (blockIdx.y == 1) {  // weights: every bit is a valid +-1
         if (i >= c.wwords) return;
         const uint2 v = __ldg(c.w + i);
-        c.we[2 * i] = expand_pm1(v.x, 64);
-        c.we[2 * i + 1] = expand_pm1(v.y, 64);
+        st256(c.we + 2 * i, expand_pm1(v.x, 64), expand_pm1(v.y, 64));
         return;
     }
     if (i >= c.npad) return;
@@ -560,8 +618,7 @@ __global__ void __launch_bounds__(256) expand_conv_kernel(ConvExpand c) {
     } else {
         lo = hi = make_uint4(0x22222222u, 0x22222222u, 0x22222222u, 0x22222222u);  // halo: +1
     }
-    c.e[2 * i] = lo;
-    c.e[2 * i + 1] = hi;
+    st256(c.e + 2 * i, lo, hi);
 }
 
 template <int BN>

@@ -410,6 +410,29 @@ def test_large_gemm_properties(bnn, algo, mnk):
         assert v == k - x
 
 
+def test_pre_expanded_engine_variants_bit_exact(bnn):
+    """The experiment routes of bnn_gemm_xp.cu stay correct: clusters of two CTA pairs sharing
+    the B tile by TMA multicast (debug bit 1 << 26), register stores with a 7-stage ring
+    (1 << 20), parked waits (1 << 21) -- all bit-identical to the default pair route, including
+    an odd number of 256-row tiles (the second pair of the last cluster idles) and ragged edges."""
+    from paper_1705_09864_b200 import _lib
+    try:
+        for (m, n, k) in [(512, 224, 256), (300, 500, 1000), (768, 3000, 4160), (1280, 1100, 2048)]:
+            g = torch.Generator(device="cuda").manual_seed(m + n + k)
+            w = (k + 63) // 64
+            a = torch.randint(-2**63, 2**63 - 1, (m, w), device="cuda", generator=g).view(torch.uint64)
+            b = torch.randint(-2**63, 2**63 - 1, (n, w), device="cuda", generator=g).view(torch.uint64)
+            _lib.call("bnn_debug_set", _lib.DEBUG_UMMA_BITS, 0)
+            ref = bnn.xnor_rows_gemm(a, b, k, algo="xp", domain=_lib.DOT)
+            assert torch.equal(ref, bnn.xnor_rows_gemm(a, b, k, algo="popc", domain=_lib.DOT))
+            for bits in (1 << 26, 1 << 20, 1 << 21, (1 << 26) | (1 << 21)):
+                _lib.call("bnn_debug_set", _lib.DEBUG_UMMA_BITS, bits)
+                for _ in range(2):
+                    assert torch.equal(bnn.xnor_rows_gemm(a, b, k, algo="xp", domain=_lib.DOT), ref), (m, n, k, bits)
+    finally:
+        _lib.call("bnn_debug_set", _lib.DEBUG_UMMA_BITS, 0)
+
+
 # ------------------------------------------------------------------ multi-bit (bit planes)
 def _codes_np(x, grid, bits=2):
     L = (1 << bits) - 1
