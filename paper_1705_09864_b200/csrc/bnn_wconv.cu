@@ -556,6 +556,24 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const bool mok = t < (uint32_t)g.P && oy < (uint32_t)g.OH && col < (uint32_t)g.OW;
                 const int64_t m = ((int64_t)b * g.OH + oy) * g.OW + col;  // pixel index (NHWC order)
                 const int64_t obase = ((int64_t)b * g.Ftot + f0) * ohw + (int64_t)oy * g.OW + col;
+                if (g.res != nullptr && T + 2 < te && !(g.dbg & 64)) {
+                    // warm L2 with the shortcut values of this warp's NEXT tile (T + 2, whose raster
+                    // coordinates the advance above just produced): the f32 + shortcut epilogue is
+                    // DRAM-latency-bound.  Lane l covers filters l, l + 32, ... at the first and last
+                    // valid position of the warp's 32 (its span is at most two 128-byte lines per filter)
+                    const bool nv = t + 2 * kRows < (uint32_t)g.P && coy < (uint32_t)g.OH && ccol < (uint32_t)g.OW;
+                    const uint32_t vm = __ballot_sync(0xffffffffu, nv);
+                    if (vm != 0) {
+                        const int64_t nb = ((int64_t)cb * g.Ftot + f0) * ohw + (int64_t)coy * g.OW + ccol;
+                        const int64_t n_lo = __shfl_sync(0xffffffffu, nb, __ffs(vm) - 1);
+                        const int64_t n_hi = __shfl_sync(0xffffffffu, nb, 31 - __clz(vm));
+#pragma unroll
+                        for (int j = 0; j < kF; j += 32) {
+                            asm volatile("prefetch.global.L2 [%0];\n" ::"l"(g.res + n_lo + (int64_t)(j + lane) * ohw));
+                            asm volatile("prefetch.global.L2 [%0];\n" ::"l"(g.res + n_hi + (int64_t)(j + lane) * ohw));
+                        }
+                    }
+                }
                 int32_t pcs = 0;
                 {
                     const int32_t *pw0 = pcb + ((int)t - Ra * Wp);
