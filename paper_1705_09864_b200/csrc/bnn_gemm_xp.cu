@@ -59,6 +59,7 @@ __device__ __forceinline__ void st256(uint4 *dst, const uint4 &lo, const uint4 &
 constexpr int kExpRows = 4;
 __global__ void __launch_bounds__(128) expand_pm1_kernel(ExpandOp a, ExpandOp b, int64_t kw64,
                                                          int64_t K) {
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // (the GEMM's setup overlaps this pass)
     const ExpandOp op = blockIdx.z == 0 ? a : b;
     const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (w >= kw64) return;
@@ -107,6 +108,7 @@ __device__ __forceinline__ uint4 expand_code2_val(uint32_t w0, uint32_t w1, int6
 }
 __global__ void __launch_bounds__(128) expand_code2_kernel(ExpandOp2 a, ExpandOp2 b, int64_t kw64,
                                                            int64_t K) {
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     const ExpandOp2 op = blockIdx.z == 0 ? a : b;
     const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (w >= kw64) return;
@@ -255,6 +257,10 @@ __global__ void __launch_bounds__(Cfg<BN, kStaged>::kThreads, 1)
     __syncthreads();
     cluster_sync();  // the peer's barriers and scales exist before any remote arrival / MMA
     fence_after();
+    // programmatic dependent launch: the setup above overlapped the expansion pass; its codes
+    // (and the previous users of the output buffer) are complete from here on
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
     if (trace_buf && tid == 0) trace_at(trace_buf, 1);
 
     if (warp == C::kTmaWarp) {
@@ -440,13 +446,15 @@ static int launch_cfg(const void *ea, const void *eb, int64_t kb, const GemmStor
     cfg.blockDim = dim3(C::kThreads);
     cfg.dynamicSmemBytes = C::kSmemBytes;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = kCl;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     // clusters that can be co-resident (one CTA per SM; a cluster lives inside one GPC)
     static int max_clusters = -1;
     if (max_clusters < 0) {
@@ -595,6 +603,10 @@ struct ConvExpand {
 };
 
 __global__ void __launch_bounds__(256) expand_conv_kernel(ConvExpand c) {
+    // programmatic dependent launch on both sides: the conv's setup may start while this pass
+    // runs; this pass reads the previous layer's packed output only after that layer completed
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (blockIdx.y == 1) {  // weights: every bit is a valid +-1
         if (i >= c.wwords) return;
@@ -734,6 +746,8 @@ __global__ void __launch_bounds__(ConvCfg<BN>::kThreads, 1)
     __syncthreads();
     cluster_sync();
     fence_after();
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");  // (the expansion pass before us)
 
     if (warp == C::kTmaWarp) {
         // ================================================================ TMA producer
@@ -940,13 +954,15 @@ static int launch_conv_cfg(const CUtensorMap &amap, const CUtensorMap &rmap, con
     cfg.blockDim = dim3(C::kThreads);
     cfg.dynamicSmemBytes = C::kSmemBytes;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     cudaLaunchKernelEx(&cfg, kern, amap, bmap, rmap, p);
     return check_launch("xconv_xp_kernel");
 }
@@ -987,8 +1003,18 @@ int launch_bconv2d_xp(const uint64_t *x, int64_t B, int64_t C, int64_t H, int64_
                   B * Hp * Wp * cw64, F * (K / 64), (int32_t)H, (int32_t)W, (int32_t)Hp, (int32_t)Wp,
                   (int32_t)ph, (int32_t)pw, (int32_t)cw64};
     const int64_t items = ce.npad > ce.wwords ? ce.npad : ce.wwords;
-    dim3 grid((unsigned)ceil_div(items, 256), 2);
-    expand_conv_kernel<<<grid, 256, 0, s>>>(ce);
+    {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)ceil_div(items, 256), 2);
+        cfg.blockDim = dim3(256);
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, expand_conv_kernel, ce);
+    }
     int rc = check_launch("expand_conv_kernel");
     if (rc != BNN_OK) return rc;
     CUtensorMap amap;

@@ -253,8 +253,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     fence_after();
     const uint32_t tmem = *s_tmem;
-    // programmatic dependent launch: the setup above overlaps the previous kernel
-    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // (see bnn_wconv.cu)
 
     // ---- weights: expanded once into the SW128 K-major B operand (+ filter popcounts)
     {
@@ -351,6 +350,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncthreads();
     }
+    // (the setup above reads load-time constants only: it overlaps the previous kernel's tail)
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
 
     const int64_t t0 = blockIdx.x, tstep = gridDim.x;
     // the contiguous range of flat input rows (b * H + iy) a tile's pixels touch

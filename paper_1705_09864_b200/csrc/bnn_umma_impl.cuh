@@ -670,6 +670,7 @@ __global__ void __launch_bounds__(Cfg<BN, kATmem, kPlanes, is_tma<ALoad>::value,
     // programmatic dependent launch: the setup above (barriers, TMEM allocation,
     // descriptor prefetch) overlaps the previous kernel's tail; operand reads and
     // output writes start only once that kernel's results are visible
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // (the next kernel's setup may start)
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     if (tid == 0) trace(1);
 

@@ -192,8 +192,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     fence_after();
     const uint32_t tmem = *s_tmem;
-    // programmatic dependent launch: the setup above overlaps the previous kernel
-    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    // programmatic dependent launch: let the next kernel's CTAs start on SMs this grid frees (its own
+    // griddepcontrol.wait still holds its reads / writes until this grid has completed)
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 
     if (tid == 0) stamp(g, 7, 3);
     // ---- weights: expanded once into the SW128 K-major B operand (+ filter popcounts),
@@ -332,6 +333,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncthreads();
     }
+    // everything above (barriers, TMEM, the weight group's expansion, per-filter parameters and
+    // thresholds) reads only load-time constants and overlaps the previous kernel's tail; the
+    // activations, the shortcut and the outputs are touched after this point
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
 
     if (tid == 0) stamp(g, 7, 1);
     // this CTA's contiguous tile range, in items of tpi tiles

@@ -420,8 +420,12 @@ def test_pre_expanded_engine_variants_bit_exact(bnn):
         for (m, n, k) in [(512, 224, 256), (300, 500, 1000), (768, 3000, 4160), (1280, 1100, 2048)]:
             g = torch.Generator(device="cuda").manual_seed(m + n + k)
             w = (k + 63) // 64
-            a = torch.randint(-2**63, 2**63 - 1, (m, w), device="cuda", generator=g).view(torch.uint64)
-            b = torch.randint(-2**63, 2**63 - 1, (n, w), device="cuda", generator=g).view(torch.uint64)
+            a = torch.randint(-2**63, 2**63 - 1, (m, w), device="cuda", generator=g)
+            b = torch.randint(-2**63, 2**63 - 1, (n, w), device="cuda", generator=g)
+            if k % 64:  # pad fill 0: the bits past K of the last word are clear
+                a[:, -1] &= (1 << (k % 64)) - 1
+                b[:, -1] &= (1 << (k % 64)) - 1
+            a, b = a.view(torch.uint64), b.view(torch.uint64)
             _lib.call("bnn_debug_set", _lib.DEBUG_UMMA_BITS, 0)
             ref = bnn.xnor_rows_gemm(a, b, k, algo="xp", domain=_lib.DOT)
             assert torch.equal(ref, bnn.xnor_rows_gemm(a, b, k, algo="popc", domain=_lib.DOT))
