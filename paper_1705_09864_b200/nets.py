@@ -467,6 +467,12 @@ class BinaryBasicBlock:
         c, f = self.conv2.in_channels, self.conv2.filters
         if not self.split_shortcut or (c in (64, 128) and f in (64, 128)):
             return True
+        if c >= 512 and c % 256 == 0 and f % 64 == 0 and f <= 1024 and \
+                self.conv2.algo in ("auto", "xp", _lib.ALGO_AUTO, _lib.ALGO_UMMA_XP):
+            # the pre-expanded conv engine (bnn_bconv2d_ws, rows = pixels): for every filter a
+            # warp reads / writes 32 consecutive pixels, so the shortcut add and the sign-pack
+            # stay in conv2's epilogue (no f32 round trip, no add / sign-pack pass)
+            return True
         if c == 256 and f == 256:
             # the shifted-window kernel takes C = 256 when a CTA owns >= 5 tiles of 128 padded
             # positions (launch_wconv, bnn_wconv.cu); below that the general engine runs and
