@@ -564,9 +564,10 @@ static int bconv2d_impl(const uint64_t *x_words, int64_t B, int64_t C, int64_t H
         case BNN_ALGO_UMMA:
             // C % 256 == 0 with a workspace: activations (+1 halo) and weights expanded once to
             // e2m1 codes, im2col-TMA-fed 2-CTA kind::mxf4 GEMM with the full fused epilogue
-            // (AUTO: from C = 512 on -- ResNet-18 layer 4, 26 vs 45 us; at C = 256 the expansion pass
-            // and the short per-tile K loop leave it level with the packed engines: C2 21 vs 18 us)
-            if (algo == BNN_ALGO_UMMA_XP || (algo == BNN_ALGO_AUTO && ws && C >= 512)) {
+            // (AUTO: every C % 256 == 0 conv -- ResNet-18 layer 4: 22 vs 45 us per conv; at C = 256,
+            // expansion pass included, level on plain outputs (C2 17.7 vs 17.7 us) and ahead with a fused
+            // shortcut: ResNet-18 213k -> 220k images/s, C2 step 963 -> 1002 TOPS)
+            if (algo == BNN_ALGO_UMMA_XP || (algo == BNN_ALGO_AUTO && ws && C >= 256)) {
                 rc = launch_bconv2d_xp(x_words, B, C, H, W, w_dev, F, kh, kw, sh, sw, ph, pw, oh, ow, y,
                                        ep, as_stream(stream), e->residual, ws, ws_bytes);
                 if (rc != BNN_EUNSUP) return rc;

@@ -282,7 +282,7 @@ class QConv2d(_QLayer):
         One buffer per (device, stream), shared by all layers: calls on a stream are ordered."""
         if algo not in (_lib.ALGO_AUTO, _lib.ALGO_UMMA_XP):
             return None
-        if algo == _lib.ALGO_AUTO and self.in_channels < 512:  # (mirrors bconv2d_impl in bnn_capi.cu)
+        if algo == _lib.ALGO_AUTO and self.in_channels < 256:  # (mirrors bconv2d_impl in bnn_capi.cu)
             return None
         kh, kw = self.kernel
         need = int(_lib.load().bnn_bconv2d_ws_bytes(b, self.in_channels, h, w, self.filters, kh, kw,

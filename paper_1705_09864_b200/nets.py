@@ -460,14 +460,15 @@ class BinaryBasicBlock:
     # computes BN + shortcut for the sign and writes the packed words alone
     needs_f32_out = True
     split_shortcut = True  # conv2 epilogue without the add + one add/sign-pack pass
-    # (for the convs the shifted-window kernel runs -- C, F <= 256 -- the shortcut add
-    # stays in conv2's epilogue, whose residual reads are coalesced there)
+    # (for the convs the shifted-window kernel runs -- C, F <= 128 -- and the pre-expanded conv
+    # engine -- C % 256 == 0 -- the shortcut add stays in conv2's epilogue, whose residual reads
+    # are coalesced there)
 
     def _fused_shortcut(self, h) -> bool:
         c, f = self.conv2.in_channels, self.conv2.filters
         if not self.split_shortcut or (c in (64, 128) and f in (64, 128)):
             return True
-        if c >= 512 and c % 256 == 0 and f % 64 == 0 and f <= 1024 and \
+        if c >= 256 and c % 256 == 0 and f % 64 == 0 and f <= 1024 and \
                 self.conv2.algo in ("auto", "xp", _lib.ALGO_AUTO, _lib.ALGO_UMMA_XP):
             # the pre-expanded conv engine (bnn_bconv2d_ws, rows = pixels): for every filter a
             # warp reads / writes 32 consecutive pixels, so the shortcut add and the sign-pack

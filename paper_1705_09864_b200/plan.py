@@ -142,7 +142,7 @@ class ConvPlan(_Plan):
         self.ws = None
         need = int(self.lib.bnn_bconv2d_ws_bytes(batch, c, h, w, layer.filters, kh, kw, layer.stride[0],
                                                  layer.stride[1], layer.pad[0], layer.pad[1]))
-        if need > 0 and (self.algo == _lib.ALGO_UMMA_XP or (self.algo == _lib.ALGO_AUTO and c >= 512)):
+        if need > 0 and (self.algo == _lib.ALGO_UMMA_XP or (self.algo == _lib.ALGO_AUTO and c >= 256)):
             self.ws = torch.empty(need, dtype=torch.uint8, device="cuda")
             self.ws_slices = {}
             from .layers import make_epilogue
