@@ -541,9 +541,56 @@ class QConvolution(QConv2d):
         self.act_bit = int(act_bit)
         self.weight_bit = int(weight_bit)
         self.domain = _lib.DOT if domain == "dot" else _lib.POPCOUNT
+        self.planes = None
 
     def _strict_input(self) -> bool:
         return False
+
+    # ---- act_bit = weight_bit = 2: bit planes over the same engine (north star; the reference
+    # has a float path only for bits > 1, layers.py:237-244 -- this is its packed counterpart:
+    # zero-pad, quantize_signed (qmath.py), im2col (tensor.py:60-78), sum_k v_w v_x)
+    def pack(self):
+        if self.bits == 1:
+            return super().pack()
+        if self.bits != 2:
+            raise ModeError("packed multi-bit inference supports act_bit = weight_bit = 2")
+        if self.weight is None:
+            raise ModeError("no float weights to pack")
+        w = torch.from_numpy(np.ascontiguousarray(self._flat_weight_np())).cuda()
+        flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.planes = pack_planes_device(w, self.bits, "signed", flags)
+        raise_on_flags(flags, "quantize_signed requires finite inputs")
+        self.packed = self.planes  # marks the layer as packed
+        return self.planes
+
+    def _require_packed(self):
+        if self.bits == 1:
+            return super()._require_packed()
+        if self.packed is None:
+            raise ModeError("layer has no packed weights; pack() or load a converted model")
+
+    def forward(self, x, mode=INFER_FLOAT):
+        if self.bits == 1 or mode != INFER_PACKED:
+            return super().forward(x, mode)
+        _check_mode(mode)
+        self._require_packed()
+        t, was_np = to_device_f32(x)
+        if t.dim() != 4 or t.shape[1] != self.in_channels:
+            raise ValueError(f"expected [B, {self.in_channels}, H, W] input")
+        b, _, h, w = t.shape
+        oh, ow = self.output_hw(h, w)
+        if self.pad != (0, 0):  # G2 generalised: zero-pad, then quantize (0 -> its grid value)
+            t = F.pad(t, (self.pad[1], self.pad[1], self.pad[0], self.pad[0]))
+        # im2col rows [B * OH * OW, C * kh * kw] in the reference's (c, ky, kx) order
+        cols = F.unfold(t, self.kernel, stride=self.stride)
+        rows = cols.transpose(1, 2).reshape(b * oh * ow, self.k_reduce).contiguous()
+        flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+        xp = pack_planes_device(rows, self.bits, "signed", flags)
+        y = bitplane_gemm(self.planes, xp, self.k_reduce, a_grid="signed", b_grid="signed",
+                          transpose_out=True)  # [B * OH * OW, F]
+        raise_on_flags(flags, "quantize_signed requires finite inputs")
+        y = y.view(b, oh, ow, self.filters).permute(0, 3, 1, 2).contiguous()
+        return _ret(y, was_np)
 
 
 class QFullyConnected(QDense):
