@@ -403,7 +403,8 @@ enum bnn_debug_knob {
                                     * bnn_umma_trace buffer, 1 << 15 no cluster split-K,
                                     * 1 << 17 shifted-window conv also for C >= 256,
                                     * 1 << 19 no shifted-window conv, 1 << 14 two
-                                    * superstages per TMA load, 1 << 18 no small-channel
+                                    * superstages per TMA load, 1 << 29 no POPC pointwise
+                                    * (1x1) conv route, 1 << 18 no small-channel
                                     * kernels, bits 21-24 role ablations (wrong results) */
     BNN_DEBUG_FP4_BN = 2,          /* force the kind::mxf4 tile N (0 = by shape)     */
     BNN_DEBUG_PAIR_KW32 = 3,       /* 2-CTA pairs from this K in u32 words (0 = off) */

@@ -68,6 +68,9 @@ int launch_xnor_gemm_umma(const uint64_t *, int64_t, const uint64_t *, int64_t, 
 int launch_bconv2d_umma(const uint64_t *, int64_t, int64_t, int64_t, int64_t, const uint64_t *,
                         int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,
                         int64_t, float *, const Epilogue &, cudaStream_t, const float *);
+int launch_pwconv(const uint64_t *, int64_t, int64_t, int64_t, int64_t, const uint64_t *, int64_t,
+                  int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, float *,
+                  const Epilogue &, cudaStream_t, const float *);
 int launch_xnor_gemm_bmma(const uint64_t *, int64_t, const uint64_t *, int64_t, int64_t,
                           int64_t, int64_t, float *, int64_t, int64_t, const Epilogue &,
                           cudaStream_t, const float *);
@@ -562,6 +565,14 @@ static int bconv2d_impl(const uint64_t *x_words, int64_t B, int64_t C, int64_t H
             return launch_bconv2d_bmma(x_words, B, C, H, W, w_dev, F, kh, kw, sh, sw, ph, pw, oh,
                                        ow, y, ep, as_stream(stream), e->residual);
         case BNN_ALGO_UMMA:
+            // AUTO, 1x1 / pad 0 / C <= 128 with an f32 output (ResNet downsample shortcuts): the
+            // layer is bound by its output stream, and the POPC-pipe pointwise kernel writes it at
+            // HBM speed (bnn_pwconv.cu); debug bit 1 << 29 keeps the tensor-core engines
+            if (algo == BNN_ALGO_AUTO && !(g_debug.umma_bits & (1 << 29))) {
+                rc = launch_pwconv(x_words, B, C, H, W, w_dev, F, kh, kw, sh, sw, ph, pw, oh, ow, y, ep,
+                                   as_stream(stream), e->residual);
+                if (rc != BNN_EUNSUP) return rc;
+            }
             // C % 256 == 0 with a workspace: activations (+1 halo) and weights expanded once to
             // e2m1 codes, im2col-TMA-fed 2-CTA kind::mxf4 GEMM with the full fused epilogue
             // (AUTO: every C % 256 == 0 conv -- ResNet-18 layer 4: 22 vs 45 us per conv; at C = 256,

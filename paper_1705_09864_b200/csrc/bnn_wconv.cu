@@ -128,6 +128,15 @@ __device__ __forceinline__ void ld16(uint32_t taddr, uint32_t *v) {  // (no wait
           "=r"(v[14]), "=r"(v[15])
         : "r"(taddr));
 }
+// base + j * stride_bytes as ONE IMAD.WIDE (j folds to an immediate after unrolling): the NCHW
+// filter stride of the epilogue's residual loads / f32 stores, instead of a 4-instruction
+// 64-bit add + scale per address
+template <typename T>
+__device__ __forceinline__ T *at_stride(T *base, int stride_bytes, int j) {
+    uint64_t d;
+    asm("mad.wide.s32 %0, %1, %2, %3;\n" : "=l"(d) : "r"(stride_bytes), "r"(j), "l"((uint64_t)base));
+    return reinterpret_cast<T *>(d);
+}
 __device__ __forceinline__ void wait_spin(uint32_t bar, uint32_t phase) {
     uint32_t done = 0;
     do {
@@ -168,6 +177,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t *s_tmem = reinterpret_cast<uint32_t *>(sgen + L.tmem);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int ohw = g.OH * g.OW;
+    const int ohw4 = ohw * 4;  // (bytes; positions < 2^24)
     const int fg = blockIdx.x % g.fgroups, rg = blockIdx.x / g.fgroups;  // filter group, tile range
     const int f0 = fg * kF;  // this CTA's first filter
     if (tid == 0) stamp(g, 7, 0);
@@ -536,6 +546,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint64_t *pack64 = reinterpret_cast<uint64_t *>(ep.pack_out);
         const int64_t pack_ld64 = ep.pack_ld32 >> 1;
         int ii = 0, tc = 0;
+        // address of filter column j of an NCHW value: one IMAD.WIDE for 128-filter groups
+        // (measured: layer 2's shortcut conv 83 -> 77 us, and r[] stays in registers); the
+        // 64-filter kernel measured faster with the compiler's own address chains (106 vs 111 us)
+        auto res_at = [&](auto *base, int j) {
+            if constexpr (kF >= 128) return at_stride(base, ohw4, j);
+            else return base + (int64_t)j * ohw;
+        };
 #pragma unroll 1
         for (int T0 = tb, T1 = tb; T0 < te; T0 = T1, ++ii) {
             T1 = item_end(T0, ii);
@@ -604,7 +621,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const bool use_res = g.res != nullptr && mok;
                 if (use_res) {
 #pragma unroll
-                    for (int j = 0; j < 64; ++j) r[j] = __ldg(g.res + obase + (int64_t)j * ohw);
+                    for (int j = 0; j < 64; ++j) r[j] = __ldg(res_at(g.res + obase, j));
                 }
                 if (g.dbg & 4) wait_parked(bar_tfull + 8 * buf, (uint32_t)(tc / kAcc) & 1u);
                 else {
@@ -640,7 +657,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     float nf = 0.0f;
                     if (use_res && c0 != 0) {
 #pragma unroll
-                        for (int j = 0; j < 64; ++j) r[j] = __ldg(g.res + obase + (int64_t)(c0 + j) * ohw);
+                        for (int j = 0; j < 64; ++j)
+                            r[j] = __ldg(res_at(g.res + obase + (int64_t)c0 * ohw, j));
                     }
 #pragma unroll
                     for (int c1 = c0; c1 < c0 + 64; c1 += 32) {
@@ -669,7 +687,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             if (g.y) {
                                 float *yo = g.y + obase + (int64_t)c1 * ohw;
 #pragma unroll
-                                for (int j = 0; j < 32; ++j) yo[(int64_t)j * ohw] = __uint_as_float(v[j]);
+                                for (int j = 0; j < 32; ++j) *res_at(yo, j) = __uint_as_float(v[j]);
                             }
                             if constexpr (kPack) {
                                 uint32_t w32 = 0;

@@ -109,6 +109,58 @@ def test_conv_sign_pack_epilogue(bnn, case, variant, with_res):
     assert torch.equal(nxt.forward_fused(only), nxt.forward_fused(plain))
 
 
+# POPC-pipe pointwise conv (bnn_pwconv.cu, the AUTO route of 1x1 / pad 0 / C <= 256 convs with an
+# f32 output): ResNet-18's three downsample shapes, ragged channels / filters, strides 1-3,
+# asymmetric strides, pixel counts that straddle images inside a warp
+PW_CASES = [
+    (3, 64, 56, 56, 128, 1, 1, (2, 2), (0, 0), 21),
+    (2, 128, 28, 28, 256, 1, 1, (2, 2), (0, 0), 22),
+    (5, 256, 14, 14, 512, 1, 1, (2, 2), (0, 0), 23),
+    (7, 100, 9, 11, 70, 1, 1, (1, 1), (0, 0), 24),
+    (4, 200, 13, 7, 130, 1, 1, (3, 2), (0, 0), 25),
+    (33, 40, 5, 5, 9, 1, 1, (1, 2), (0, 0), 26),
+]
+
+
+@pytest.mark.parametrize("case", PW_CASES)
+@pytest.mark.parametrize("domain", ["dot", "popcount"])
+def test_pointwise_conv_popc_route(bnn, case, domain):
+    """AUTO takes the POPC pointwise kernel here; bit-identical to the tcgen05 engine (umma2),
+    to the CUDA-core engine and to the oracle's conv -> BN (-> + shortcut) composition."""
+    b, c, h, w, f, kh, kw, stride, pad, seed = case
+    x, wt = wl.conv_case_inputs(case)
+    layer = bnn.QConvolution(c, f, (kh, kw), stride, pad, domain=domain)
+    layer.weight = wt
+    layer.pack()
+    bn = _BN(f, c, seed)
+    oh, ow = layer.output_hw(h, w)
+    res = torch.from_numpy(np.random.default_rng(seed + 50).standard_normal(
+        (b, f, oh, ow)).astype(np.float32)).cuda()
+    xd = torch.from_numpy(x).cuda()
+    p = orc.qconv_packed(x, wt, stride, pad).astype(np.float32)
+    base = 2 * p - np.float32(c) if domain == "dot" else p
+    sh = (1, -1, 1, 1)
+    ref_bn = bn.gamma.reshape(sh) * ((base - bn.mean.reshape(sh)) * bn.inv.reshape(sh)) + \
+        bn.beta.reshape(sh)
+    outs = {}
+    for algo in ("auto", "umma2", "popc"):
+        layer.algo = algo
+        outs[algo] = (layer.forward_fused(xd).cpu().numpy(),
+                      layer.forward_fused(xd, bn).cpu().numpy(),
+                      layer.forward_fused(xd, bn, residual=res).cpu().numpy())
+    assert np.array_equal(outs["auto"][0], base)
+    assert np.array_equal(outs["auto"][1], ref_bn.astype(np.float32))
+    assert np.array_equal(outs["auto"][2], (ref_bn + res.cpu().numpy()).astype(np.float32))
+    for algo in ("umma2", "popc"):
+        for a, o in zip(outs["auto"], outs[algo]):
+            assert np.array_equal(a, o), algo
+    # a sign-packed output is not the pointwise kernel's: AUTO falls through, same words
+    layer.algo = "auto"
+    pk = layer.forward_fused(xd, bn, pack_out=True)
+    assert np.array_equal(pk.f32.cpu().numpy(), outs["auto"][1])
+    assert np.array_equal(pk.words.cpu().numpy(), _oracle_pack_nhwc(outs["auto"][1]))
+
+
 # pre-expanded conv engine (bnn_bconv2d_ws, C % 256 == 0, F % 64 == 0): strides 1 / 2, 1x1 and
 # 5x5 kernels, asymmetric geometry, image sizes that make 32-pixel lane groups straddle images,
 # pixel counts below / across the 256-row pair tile, ResNet-18 layer-3 / layer-4 shapes
