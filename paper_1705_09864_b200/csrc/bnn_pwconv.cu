@@ -105,6 +105,84 @@ __global__ void __launch_bounds__(kThreads) xnor_pw_kernel(const Geom g, const E
     }
 }
 
+// OH * OW % 4 == 0: one thread = 4 consecutive pixels of a plane x kFg filters, so every output
+// instruction is a 16-byte store (a warp writes 512 contiguous bytes per filter, as a fill kernel
+// does) and a filter's words / parameters are read from SMEM once per 4 outputs
+template <int CW, int kFg>
+__global__ void __launch_bounds__(kThreads) xnor_pw4_kernel(const Geom g, const Epilogue ep) {
+    __shared__ uint64_t s_w[kFg * CW];
+    __shared__ float4 s_bn[kFg];
+    __shared__ float2 s_aff[kFg];
+    asm volatile("griddepcontrol.launch_dependents;\n");
+    const int f0 = blockIdx.y * kFg;
+    const int nf = g.F - f0 < kFg ? g.F - f0 : kFg;
+    const bool has_bn = ep.bn_mean != nullptr;
+    for (int i = threadIdx.x; i < nf * CW; i += kThreads) s_w[i] = __ldg(g.w + (int64_t)f0 * CW + i);
+    for (int i = threadIdx.x; i < nf; i += kThreads) {
+        if (has_bn)
+            s_bn[i] = make_float4(__ldg(ep.bn_mean + f0 + i), __ldg(ep.bn_inv + f0 + i),
+                                  __ldg(ep.bn_gamma + f0 + i), __ldg(ep.bn_beta + f0 + i));
+        s_aff[i] = make_float2(ep.scale ? __ldg(ep.scale + f0 + i) : 1.0f,
+                               ep.shift ? __ldg(ep.shift + f0 + i) : 0.0f);
+    }
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    __syncthreads();
+    const int64_t m = ((int64_t)blockIdx.x * kThreads + threadIdx.x) * 4;  // first of 4 pixels
+    if (m >= g.NP) return;
+    const int ohw = g.OH * g.OW;
+    const int64_t b = m / ohw;       // (ohw % 4 == 0: the 4 pixels share the image)
+    const int p = (int)(m - b * ohw);
+    uint64_t xw[4][CW];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int pu = p + u;
+        const int oy = pu / g.OW, ox = pu - oy * g.OW;
+        const uint64_t *xin = g.x + ((b * g.H + (int64_t)oy * g.sh) * g.W + (int64_t)ox * g.sw) * CW;
+        if constexpr (CW % 2 == 0) {
+#pragma unroll
+            for (int i = 0; i < CW; i += 2) {
+                const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2 *>(xin + i));
+                xw[u][i] = v.x, xw[u][i + 1] = v.y;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < CW; ++i) xw[u][i] = __ldg(xin + i);
+        }
+    }
+    const int64_t obase = (b * g.F + f0) * ohw + p;
+    float *out = g.y + obase;
+    const float *res = g.res ? g.res + obase : nullptr;
+    const bool dot = ep.domain == BNN_DOT;
+    const bool scale = ep.scale != nullptr, shift = ep.shift != nullptr;
+    const float keff = (float)ep.k_eff, klog = (float)ep.k_logical;
+#pragma unroll 4
+    for (int f = 0; f < nf; ++f) {
+        uint64_t wv[CW];
+#pragma unroll
+        for (int i = 0; i < CW; ++i) wv[i] = s_w[f * CW + i];
+        const float2 a = s_aff[f];
+        const float4 q = s_bn[f];
+        float4 r4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        if (res) r4 = __ldg(reinterpret_cast<const float4 *>(res + (int64_t)f * ohw));
+        const float rr[4] = {r4.x, r4.y, r4.z, r4.w};
+        float o[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            int cnt = 0;
+#pragma unroll
+            for (int i = 0; i < CW; ++i) cnt += __popcll(xw[u][i] ^ wv[i]);
+            const float pc = __fsub_rn(keff, __fsub_rn(__int_as_float(0x4B000000 | cnt), 8388608.0f));
+            float v = dot ? __fmaf_rn(2.0f, pc, -klog) : pc;
+            if (scale) v = __fmul_rn(v, a.x);
+            if (shift) v = __fadd_rn(v, a.y);
+            if (has_bn) v = __fadd_rn(__fmul_rn(q.z, __fmul_rn(__fsub_rn(v, q.x), q.y)), q.w);
+            if (res) v = __fadd_rn(v, rr[u]);
+            o[u] = v;
+        }
+        *reinterpret_cast<float4 *>(out + (int64_t)f * ohw) = make_float4(o[0], o[1], o[2], o[3]);
+    }
+}
+
 }  // namespace pw
 
 // Eligible: 1x1 kernel, no padding, C <= 128 in whole or partial words (tails 0; at C = 256 the
@@ -138,6 +216,18 @@ int launch_pwconv(const uint64_t *x, int64_t B, int64_t C, int64_t H, int64_t W,
     // 64 filters per CTA and the I2F-free count conversion: measured best of {32, 64, 128} x
     // {I2F, magic} at batch 256 (27.5 / 19.8 us for ResNet-18's layer-2 / layer-3 downsample
     // against 35.4 / 26.2 us on the tensor-core engines) and at batch 32 (6.6 vs 10.6 us)
+    // one-word pixels on large batches: the 4-pixel kernel (16-byte stores), 16 filters per CTA
+    // to keep the grid large (ResNet-18 layer-2 downsample at batch 256: 22.9 vs 27.5 us; at
+    // batch 32 and for two-word pixels, which sit on the POPC pipe's rate, the scalar kernel is
+    // as fast or faster)
+    const bool vec4 = CW == 1 && NP >= 131072 && (oh * ow) % 4 == 0 &&
+                      (reinterpret_cast<uintptr_t>(y) & 15) == 0 &&
+                      (res == nullptr || (reinterpret_cast<uintptr_t>(res) & 15) == 0);
+    if (vec4) {
+        cfg.gridDim = dim3((unsigned)ceil_div(NP, kThreads * 4), (unsigned)ceil_div(F, 16));
+        cudaLaunchKernelEx(&cfg, xnor_pw4_kernel<1, 16>, g, ep);
+        return check_launch("xnor_pw4_kernel");
+    }
     cfg.gridDim = dim3((unsigned)ceil_div(NP, kThreads), (unsigned)ceil_div(F, kFgDefault));
     if (CW == 1) cudaLaunchKernelEx(&cfg, xnor_pw_kernel<1, kFgDefault, 1>, g, ep);
     else cudaLaunchKernelEx(&cfg, xnor_pw_kernel<2, kFgDefault, 1>, g, ep);

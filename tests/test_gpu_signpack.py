@@ -119,6 +119,8 @@ PW_CASES = [
     (7, 100, 9, 11, 70, 1, 1, (1, 1), (0, 0), 24),
     (4, 200, 13, 7, 130, 1, 1, (3, 2), (0, 0), 25),
     (33, 40, 5, 5, 9, 1, 1, (1, 2), (0, 0), 26),
+    (24, 64, 112, 112, 24, 1, 1, (1, 1), (0, 0), 27),  # >= 2^17 pixels: the 4-pixel kernel
+    (88, 50, 112, 112, 17, 1, 1, (2, 2), (0, 0), 28),  # the same with stride 2, ragged C / F
 ]
 
 
