@@ -525,7 +525,7 @@ def _kernel_families(plan):
     fam = {}
     for name, ms, ops in plan.kernel_breakdown():
         if name.startswith(("bnn_bconv2d", "bnn_xnor_gemm")):
-            key = "binary conv / GEMM (xnor_umma_kernel, xnor_sconv_kernel)"
+            key = "binary conv / GEMM (xnor_wconv / xnor_sconv / xconv_xp / xnor_umma / xnor_pw kernels)"
         elif "f32_tc" in name:
             key = "float stem (stem_s2_kernel / conv_pool_kernel, tcgen05 kind::tf32 split)"
         else:
@@ -659,7 +659,7 @@ def run_gpu_arm(args, rank, world, local_rank):
     if is_net:
         fams = _kernel_families(plan)
         step_dev = sum(f["ms"] for f in fams.values())
-        key = "binary conv / GEMM (xnor_umma_kernel, xnor_sconv_kernel)"
+        key = "binary conv / GEMM (xnor_wconv / xnor_sconv / xconv_xp / xnor_umma / xnor_pw kernels)"
         bf = fams[key]
         peak = pipe_peak(args.algo, name)
         achieved = bf["binary_ops"] / (bf["ms"] * 1e-3) / 1e12
@@ -674,6 +674,19 @@ def run_gpu_arm(args, rank, world, local_rank):
                 "note": "per-launch CUDA events of one eager step queued behind a sleep kernel "
                         "(no host gaps inside the intervals); achieved = 2MNK of every binary "
                         "conv / GEMM launch / their summed device time"}
+        if roof["traffic"]:
+            # the same family against HBM: the layer-1/2 convs that stream an f32 shortcut in and
+            # an f32 block output out are bound by that stream, not by the tensor pipe
+            try:
+                hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+                src = "MEASURED_PEAKS.json hbm_gbs"
+            except Exception:
+                hbm, src = 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s measured on this pool)"
+            gbs = roof["traffic"] / (bf["ms"] * 1e-3) / 1e9
+            roof["hbm"] = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s",
+                           "frac": gbs / hbm, "peak_source": src,
+                           "note": "ncu DRAM bytes of the family per step (profiles/traffic.json) / "
+                                   "its summed device time"}
         if name == "resnet18":
             roof["stem"] = _stem_roofline(fams, plan.b)
     else:
