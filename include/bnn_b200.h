@@ -81,7 +81,9 @@ enum bnn_algo {
     /* AUTO / UMMA route by shape (all bit-identical): stride-1 convs with C <= 128 ->
      * the shifted-window kernel (bnn_wconv.cu), other small-channel convs ->
      * bnn_sconv.cu, GEMMs with N <= 256 and K <= 4096 -> the 8-CTA-cluster split-K
-     * kernel (bnn_gemm_splitk.cu), everything else -> the general engine below.   */
+     * kernel (bnn_gemm_splitk.cu), everything else -> the general engine below.
+     * AUTO only: 1x1 / pad 0 convs with C <= 128 and an f32 output (no sign-pack output) run
+     * the POPC-pipe pointwise kernel (bnn_pwconv.cu): they are bound by their output stream. */
     /* tcgen05 engine variants (BNN_ALGO_UMMA_V0 + v):
      *   V0: kind::i8, 128 x 256 tiles, A and B through SMEM
      *   V1: kind::i8, expanded weights in TMEM, tile N from {128..192}
