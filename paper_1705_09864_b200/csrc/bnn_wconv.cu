@@ -726,7 +726,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 }  // namespace wconv
 
-// Eligible: stride 1, C a multiple of 64 up to 512, F a multiple of 64, kh, kw <= 3, padding <=
+// Eligible: stride 1, C a multiple of 64 up to 512, F a multiple of 64, kh, kw <= 5 with
+// C * kh * kw <= 5120 (LeNet's 5x5 conv: 38 vs 102 us on bnn_sconv.cu), padding <=
 // kernel - 1, padded width <= 64, positions < 2^24, and two band buffers that fit in SMEM next to
 // one filter group's expanded weights (groups of 128 filters when they fit, else 64; a CTA
 // owns one filter group and a contiguous range of tiles).  Returns BNN_EUNSUP otherwise (the
@@ -737,7 +738,8 @@ int launch_wconv(const uint64_t *x, int64_t B, int64_t C, int64_t H, int64_t W, 
     using namespace wconv;
     const int64_t Cw = C / 64;
     if (sh != 1 || sw != 1 || C % 64 != 0 || (Cw != 1 && Cw != 2 && Cw != 4 && Cw != 8) || F % 64 != 0 ||
-        kh > 3 || kw > 3 || ph > kh - 1 || pw > kw - 1 || (g_debug.umma_bits & (1 << 19)))
+        kh > 5 || kw > 5 || C * kh * kw > 5120 || ph > kh - 1 || pw > kw - 1 ||
+        (g_debug.umma_bits & (1 << 19)))
         return BNN_EUNSUP;
     // C = 256 (filter groups of 128): faster than the TMA im2col engine on ResNet layer 3
     // (27 vs 40 us packed-only, 44 vs 67 us with the shortcut) once the per-CTA weight expansion

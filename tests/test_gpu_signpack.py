@@ -407,6 +407,12 @@ WCONV_CASES = [
     (2, 512, 5, 6, 192, 3, 3, (1, 1), 40),
     (8, 256, 14, 14, 256, 3, 3, (1, 1), 41),    # C = 256 on this kernel with 3 CTAs (grid_cap3)
     (190, 256, 14, 14, 256, 3, 3, (1, 1), 42),  # ... and with every SM (>= 5 tiles per CTA)
+    # kernels up to 5 x 5 (C * kh * kw <= 5120): LeNet's binary conv, non-square / asymmetric ones
+    (37, 64, 14, 14, 64, 5, 5, (2, 2), 43),
+    (3, 64, 9, 20, 128, 5, 3, (2, 0), 44),
+    (2, 128, 11, 8, 64, 4, 5, (3, 4), 45),
+    (2, 64, 7, 7, 64, 5, 5, (0, 0), 46),
+    (2, 128, 6, 9, 128, 5, 5, (4, 1), 47),
 ]
 
 

@@ -14,7 +14,7 @@ SHAPES = [(256, 64, 56, 56, 64, 3, 1, 1, "pack"), (256, 64, 56, 56, 64, 3, 1, 1,
           (32, 256, 28, 28, 256, 3, 1, 1, "plain"), (256, 256, 14, 14, 256, 3, 1, 1, "pack"),
           (256, 256, 14, 14, 256, 3, 1, 1, "bnf32"), (256, 512, 7, 7, 512, 3, 1, 1, "pack"),
           (256, 512, 7, 7, 512, 3, 1, 1, "bnf32"), (256, 256, 14, 14, 256, 3, 1, 1, "res"),
-          (256, 256, 14, 14, 256, 3, 1, 1, "respk")]
+          (256, 256, 14, 14, 256, 3, 1, 1, "respk"), (1024, 64, 14, 14, 64, 5, 1, 2, "pack")]
 bnn.load_library()
 import os
 BIG = (1 << 17) if os.environ.get("WCONV_NOBIG") else 0  # C >= 256 back on the general engine
