@@ -319,6 +319,16 @@ int bnn_conv_tanh_maxpool2_f32_tc(const float *x, int64_t B, int64_t C, int64_t 
                                   int64_t kw, int64_t sh, int64_t sw, int64_t ph, int64_t pw,
                                   int pool_first, float *y, bnn_stream_t stream);
 
+/* The same kernel also writing the sign-packed NHWC words of y (u64 [B, PH, PW, F / 64]: the
+ * next QConvolution's QActivation(act_bit = 1) + pack, bitpack.py:30-42 / 152-169, fused) and
+ * OR-ing BNN_FLAG_NONFINITE into *flags (may be null).  y may be null: a binary consumer reads
+ * only the words, and the f32 tensor is then never written. */
+int bnn_conv_tanh_maxpool2_pack_f32_tc(const float *x, int64_t B, int64_t C, int64_t H, int64_t W,
+                                       const float *w, const float *bias, int64_t F, int64_t kh,
+                                       int64_t kw, int64_t sh, int64_t sw, int64_t ph, int64_t pw,
+                                       int pool_first, float *y, uint64_t *out_words,
+                                       int32_t *flags, bnn_stream_t stream);
+
 /* Adds to *violations_dev (device u64) the number of adjacent finite floats
  * a < b with tanhf(a) > tanhf(b) (exhaustive, ~4e9 evaluations).  0 means the
  * f32 tanh is monotone, which makes pooling before the tanh exact. */

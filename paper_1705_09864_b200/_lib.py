@@ -74,6 +74,9 @@ SIGNATURES = {
                                                     _vp, _i32, _vp, _vp, _vp, _vp]),
     "bnn_conv_tanh_maxpool2_f32_tc": (_i32, [_vp, _i64, _i64, _i64, _i64, _vp, _vp, _i64, _i64,
                                              _i64, _i64, _i64, _i64, _i64, _i32, _vp, _vp]),
+    "bnn_conv_tanh_maxpool2_pack_f32_tc": (_i32, [_vp, _i64, _i64, _i64, _i64, _vp, _vp, _i64, _i64,
+                                                  _i64, _i64, _i64, _i64, _i64, _i32, _vp, _vp, _vp,
+                                                  _vp]),
     "bnn_probe_tanh_monotone": (_i32, [_vp, _vp]),
     "bnn_sum_partials_f32": (_i32, [_vp, _i32, _i64, _i64, _i32, _i64, _vp, _vp]),
     "bnn_add_pack_nchw_f32": (_i32, [_vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp]),

@@ -480,6 +480,21 @@ int bnn_conv_tanh_maxpool2_f32_tc(const float *x, int64_t B, int64_t C, int64_t 
                                           nullptr, nullptr, pool_first);
 }
 
+int bnn_conv_tanh_maxpool2_pack_f32_tc(const float *x, int64_t B, int64_t C, int64_t H, int64_t W,
+                                       const float *w, const float *bias, int64_t F, int64_t kh,
+                                       int64_t kw, int64_t sh, int64_t sw, int64_t ph, int64_t pw,
+                                       int pool_first, float *y, uint64_t *out_words,
+                                       int32_t *flags, bnn_stream_t stream) {
+    BNN_REQUIRE(B >= 0 && C >= 1 && H >= 1 && W >= 1 && F >= 1 && kh >= 1 && kw >= 1 &&
+                    sh >= 1 && sw >= 1 && ph >= 0 && pw >= 0 && H + 2 * ph >= kh &&
+                    W + 2 * pw >= kw,
+                BNN_EGEOM, "invalid convolution geometry");
+    BNN_REQUIRE(x && w && out_words, BNN_EINVAL, "null pointer");
+    return launch_conv_bn_relu_maxpool_tc(x, B, C, H, W, w, F, kh, kw, sh, sw, ph, pw, bias,
+                                          nullptr, nullptr, nullptr, 0, y, as_stream(stream), 1,
+                                          out_words, flags, pool_first);
+}
+
 int bnn_maxpool_packed(const uint64_t *in, int64_t B, int64_t H, int64_t W, int64_t Cw, int k,
                        int stride, uint64_t *out, bnn_stream_t stream) {
     BNN_REQUIRE(B >= 0 && H >= 1 && W >= 1 && Cw >= 1 && k >= 1 && stride >= 1 && H >= k &&

@@ -336,6 +336,7 @@ struct PoolGeom {
     int R;     // conv rows per tile (mode 1: an even number of narrow rows fills the lanes)
     int pool_first;  // mode 1: tanhf is monotone (probed): max-pool, then one tanh per output
     uint16_t *pack16;    // mode 0, optional: sign-packed NHWC words of y as 16-bit pieces
+    uint8_t *pack8;      // mode 1, optional: the same as 8-bit pieces (16 epilogue warps); y may then be null
     int32_t *pack_flags;
     int NR;    // staged input rows per channel: (R - 1) * sh + kh
     int dbg;  // debug (BNN_STEM_DEBUG, wrong results): 1 no gather loads, 2 no MMAs,
@@ -708,12 +709,24 @@ __global__ void __launch_bounds__(PEpi<kEW>::kThreads, 1) conv_pool_kernel(const
                 for (int r = 0; 2 * r + 1 < g.R && oy + 2 * r + 1 <= oy_e; ++r) {
                     float *yrow = yb + (int64_t)((oy >> 1) + r) * g.PW + px;
                     const int o0 = 2 * r * g.OW + 2 * px, o1 = o0 + g.OW;
+                    uint32_t bits = 0;
+                    float nf = 0.0f;
 #pragma unroll 8
                     for (int i = 0; i < kPCPer; ++i) {
                         const int c = c0 * kPCPer + i;
                         const float *rr = rbuf + c * kRowPitchR;
                         const float m = fmaxf(fmaxf(rr[o0], rr[o0 + 1]), fmaxf(rr[o1], rr[o1 + 1]));
-                        yrow[(int64_t)c * g.PH * g.PW] = g.pool_first ? tanhf(m) : m;
+                        const float v = g.pool_first ? tanhf(m) : m;
+                        if (g.y) yrow[(int64_t)c * g.PH * g.PW] = v;
+                        bits |= (v >= 0.0f ? 1u : 0u) << i;  // sign(-0) = +1 (binarize, bitpack.py:30-42)
+                        nf = __fmaf_rn(v, 0.0f, nf);
+                    }
+                    if (kPCPer == 8 && g.pack8) {
+                        // the next binary layer's QActivation + pack: this thread's 8 channels are
+                        // one byte of the pooled pixel's packed NHWC word
+                        const int64_t pix = ((int64_t)b * g.PH + (oy >> 1) + r) * g.PW + px;
+                        g.pack8[pix * (NF / 8) + c0] = (uint8_t)bits;
+                        if (g.pack_flags && nf != 0.0f) atomicOr(g.pack_flags, 1);
                     }
                 }
             } else if (px < g.PW && !(g.dbg & 4)) {
@@ -827,6 +840,7 @@ int launch_conv_bn_relu_maxpool_tc(const float *x, int64_t B, int64_t C, int64_t
     g.relu = relu;
     g.mode = mode;
     g.pack16 = mode == 0 ? reinterpret_cast<uint16_t *>(pack_words) : nullptr;
+    g.pack8 = mode == 1 ? reinterpret_cast<uint8_t *>(pack_words) : nullptr;
     g.pack_flags = pack_flags;
     g.pool_first = mode == 1 && pool_first;
     g.dbg = (int)g_debug.stem_bits;

@@ -292,7 +292,8 @@ class Sequential:
         while i < n:
             layer = self.layers[i]
             nxt = self.layers[i + 1] if i + 1 < n else None
-            if isinstance(x, PackedNHWC) and not isinstance(layer, BinaryBasicBlock):
+            if isinstance(x, PackedNHWC) and not isinstance(layer, BinaryBasicBlock) and not (
+                    mode == INFER_PACKED and self.fuse_bn and _binary_pool_fc(self.layers[i:i + 6])):
                 x = x.float()  # a float consumer of a packed activation
             if isinstance(layer, GlobalAvgPool) and isinstance(nxt, Dense) and x.dim() == 4:
                 x = avgpool_dense(x, nxt)  # classifier head, one kernel (both modes)
@@ -301,9 +302,13 @@ class Sequential:
                 i += 2
                 continue
             if mode == INFER_PACKED and self.fuse_stem and _lenet_stem(self.layers[i:i + 3]):
-                x = _lenet_stem_forward(self.layers[i], x)  # conv + tanh + maxpool, one kernel
+                # conv + tanh + maxpool, one kernel; a binary conv behind it reads only the sign
+                # bits, which the same kernel packs (no f32 tensor, no pack pass)
+                nb = self.fuse_bn and _binary_pool_fc(self.layers[i + 3:i + 9])
+                x = _lenet_stem_forward(self.layers[i], x, pack=nb, f32_out=capture is not None,
+                                        flags=self.layers[i + 3]._flags() if nb else None)
                 if capture is not None:
-                    capture += [None, None, x]
+                    capture += [None, None, x.f32 if isinstance(x, PackedNHWC) else x]
                 i += 3
                 continue
             if mode == INFER_PACKED and self.fuse_bn and _binary_pool_fc(self.layers[i:i + 6]):
@@ -376,12 +381,27 @@ def tanh_is_monotone() -> bool:
     return _TANH_MONOTONE
 
 
-def _lenet_stem_forward(conv: "Conv2d", x: torch.Tensor, pool_first: bool = False) -> torch.Tensor:
+def _lenet_stem_forward(conv: "Conv2d", x: torch.Tensor, pool_first: bool = False, pack: bool = False,
+                        f32_out: bool = True, flags: torch.Tensor | None = None):
     """maxpool2x2(tanh(conv(x) + b)) in one kernel (bnn_conv_tanh_maxpool2_f32_tc): the
-    same per-element f32 ops as the three torch calls, the conv output never written."""
+    same per-element f32 ops as the three torch calls, the conv output never written.
+    ``pack``: the kernel also writes the sign-packed NHWC words for a following binary conv
+    (its QActivation + pack fused) and a ``PackedNHWC`` is returned; with ``f32_out`` False
+    the f32 tensor is never written either."""
     x = x.contiguous()
     b, c, h, w = x.shape
     oh, ow = conv.output_hw(h, w)
+    if pack and conv.cout % 64 == 0:
+        shape = (b, conv.cout, oh // 2, ow // 2)
+        y = torch.empty(shape, dtype=torch.float32, device=x.device) if f32_out else None
+        words = torch.empty((b, oh // 2, ow // 2, conv.cout // 64), dtype=torch.uint64, device=x.device)
+        st = _lib.call_status("bnn_conv_tanh_maxpool2_pack_f32_tc", _lib.ptr(x), b, c, h, w,
+                              _lib.ptr(conv._dev("weight")), _lib.ptr(conv._dev("bias")), conv.cout,
+                              *conv.geometry(), int(pool_first), _lib.ptr(y), _lib.ptr(words),
+                              _lib.ptr(flags), _lib.stream_ptr())
+        if st != _lib.EUNSUP:
+            _lib.check(st, "bnn_conv_tanh_maxpool2_pack_f32_tc")
+            return PackedNHWC(words, shape, y)
     y = torch.empty((b, conv.cout, oh // 2, ow // 2), dtype=torch.float32, device=x.device)
     st = _lib.call_status("bnn_conv_tanh_maxpool2_f32_tc", _lib.ptr(x), b, c, h, w,
                           _lib.ptr(conv._dev("weight")), _lib.ptr(conv._dev("bias")), conv.cout,

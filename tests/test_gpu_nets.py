@@ -301,6 +301,24 @@ def test_lenet_fused_stem_bit_identical(nets):
     for pool_first in ([False, True] if monotone else [False]):  # tanh per element / pool first
         fused = nets._lenet_stem_forward(conv, x, pool_first=pool_first)
         assert fused.shape == ref.shape and torch.equal(fused, ref), pool_first
+        # the same kernel also writing the next binary conv's packed input (sign + pack fused),
+        # with and without the f32 tensor
+        import paper_1705_09864_b200 as bnn
+        flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+        expect = bnn.pack_nchw(ref).cpu().numpy()
+        both = nets._lenet_stem_forward(conv, x, pool_first=pool_first, pack=True, flags=flags)
+        assert both.shape == tuple(ref.shape) and torch.equal(both.f32, ref)
+        assert np.array_equal(both.words.cpu().numpy(), expect)
+        only = nets._lenet_stem_forward(conv, x, pool_first=pool_first, pack=True, f32_out=False,
+                                        flags=flags)
+        assert only.f32 is None and np.array_equal(only.words.cpu().numpy(), expect)
+        assert int(flags.item()) == 0
+    # a non-finite input raises the NONFINITE flag through the fused pack
+    xb = x.clone()
+    xb[2, 0, 5, 5] = float("nan")
+    flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+    nets._lenet_stem_forward(conv, xb, pack=True, f32_out=False, flags=flags)
+    assert int(flags.item()) != 0
 
 
 @pytest.mark.parametrize("shape,k", [((3, 14, 14, 1), 2), ((2, 9, 7, 3), 3), ((1, 6, 10, 2), 2)])
