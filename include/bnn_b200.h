@@ -340,6 +340,11 @@ int bnn_probe_tanh_monotone(unsigned long long *violations_dev, bnn_stream_t str
  * the next binary layer. in [B, H, W, Cw] u64 -> out [B, OH, OW, Cw]. */
 int bnn_maxpool_packed(const uint64_t *in, int64_t B, int64_t H, int64_t W, int64_t Cw, int k,
                        int stride, uint64_t *out, bnn_stream_t stream);
+/* The same with out_batch_stride u64 words between the images of out (>= OH * OW * Cw): a
+ * following QFullyConnected reads each image as one packed row, and an even stride keeps those
+ * rows 16-byte aligned for the TMA-fed engine (LeNet: 49 words per image -> stride 50). */
+int bnn_maxpool_packed_ld(const uint64_t *in, int64_t B, int64_t H, int64_t W, int64_t Cw, int k,
+                          int stride, uint64_t *out, int64_t out_batch_stride, bnn_stream_t stream);
 
 /* A residual block's output y = a + residual (NCHW f32, f32 add as torch) and its
  * sign-packed NHWC words (the next block's conv input); flags as the pack kernels.

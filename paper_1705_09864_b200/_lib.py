@@ -81,6 +81,7 @@ SIGNATURES = {
     "bnn_sum_partials_f32": (_i32, [_vp, _i32, _i64, _i64, _i32, _i64, _vp, _vp]),
     "bnn_add_pack_nchw_f32": (_i32, [_vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp]),
     "bnn_maxpool_packed": (_i32, [_vp, _i64, _i64, _i64, _i64, _i32, _i32, _vp, _vp]),
+    "bnn_maxpool_packed_ld": (_i32, [_vp, _i64, _i64, _i64, _i64, _i32, _i32, _vp, _i64, _vp]),
     "bnn_conv2d_f32_tc": (_i32, [_vp, _i64, _i64, _i64, _i64, _vp, _vp, _i64, _i64, _i64, _i64,
                                  _i64, _i64, _i64, _vp, _vp]),
     "bnn_xnor_gemm_ex": (_i32, [_vp, _i64, _vp, _i64, _i64, _i64, _i64, _i32, _i32, _vp, _i64,

@@ -95,7 +95,7 @@ int launch_conv_bn_relu_maxpool_tc(const float *, int64_t, int64_t, int64_t, int
                                    const float *, int, float *, cudaStream_t, int, uint64_t *,
                                    int32_t *, int);
 int launch_maxpool_packed(const uint64_t *, int64_t, int64_t, int64_t, int64_t, int, int,
-                          uint64_t *, cudaStream_t);
+                          uint64_t *, int64_t, cudaStream_t);
 int launch_add_pack_nchw(const float *, const float *, int64_t, int64_t, int64_t, int64_t, float *,
                          uint64_t *, int32_t *, cudaStream_t);
 int launch_bconv2d_popc(const uint64_t *, int64_t, int64_t, int64_t, int64_t, const uint64_t *,
@@ -502,7 +502,19 @@ int bnn_maxpool_packed(const uint64_t *in, int64_t B, int64_t H, int64_t W, int6
                 BNN_EGEOM, "invalid pooling geometry");
     BNN_REQUIRE(B == 0 || (in && out), BNN_EINVAL, "null pointer");
     BNN_REQUIRE(ceil_div(B * H * W * Cw, 256) < (1ll << 31), BNN_EUNSUP, "tensor too large");
-    return launch_maxpool_packed(in, B, H, W, Cw, k, stride, out, as_stream(stream));
+    return launch_maxpool_packed(in, B, H, W, Cw, k, stride, out, 0, as_stream(stream));
+}
+
+int bnn_maxpool_packed_ld(const uint64_t *in, int64_t B, int64_t H, int64_t W, int64_t Cw, int k,
+                          int stride, uint64_t *out, int64_t out_batch_stride, bnn_stream_t stream) {
+    BNN_REQUIRE(B >= 0 && H >= 1 && W >= 1 && Cw >= 1 && k >= 1 && stride >= 1 && H >= k &&
+                    W >= k,
+                BNN_EGEOM, "invalid pooling geometry");
+    BNN_REQUIRE(B == 0 || (in && out), BNN_EINVAL, "null pointer");
+    BNN_REQUIRE(ceil_div(B * H * W * Cw, 256) < (1ll << 31), BNN_EUNSUP, "tensor too large");
+    const int64_t OH = (H - k) / stride + 1, OW = (W - k) / stride + 1;
+    BNN_REQUIRE(out_batch_stride >= OH * OW * Cw, BNN_EALIGN, "batch stride smaller than an image");
+    return launch_maxpool_packed(in, B, H, W, Cw, k, stride, out, out_batch_stride, as_stream(stream));
 }
 
 int bnn_sum_partials_f32(const float *partials, int splits, int64_t count, int64_t stride,

@@ -595,7 +595,8 @@ __global__ void bn_relu_maxpool_band_kernel(const float *__restrict__ x, int C, 
 // packing the max-pooled f32 tensor.  One thread per output word.
 __global__ void maxpool_packed_kernel(const uint64_t *__restrict__ in, int64_t H, int64_t W,
                                       int64_t Cw, int k, int st, int64_t OH, int64_t OW,
-                                      int64_t total, uint64_t *__restrict__ out) {
+                                      int64_t total, uint64_t *__restrict__ out,
+                                      int64_t out_bstride) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= total) return;
     const int64_t cw = i % Cw, p = i / Cw;
@@ -604,7 +605,8 @@ __global__ void maxpool_packed_kernel(const uint64_t *__restrict__ in, int64_t H
     uint64_t v = 0;
     for (int r = 0; r < k; ++r)
         for (int c = 0; c < k; ++c) v |= __ldg(src + ((int64_t)r * W + c) * Cw);
-    out[i] = v;
+    // (out_bstride: words between images; a consumer GEMM wants 16-byte aligned rows)
+    out[b * out_bstride + (i - b * OH * OW * Cw)] = v;
 }
 
 // Shortcut add + sign-pack: y = a + r (f32, the block output, same rounding as
@@ -829,12 +831,12 @@ int launch_add_pack_nchw(const float *a, const float *r, int64_t B, int64_t C, i
     return check_launch("add_pack_nchw_kernel");
 }
 int launch_maxpool_packed(const uint64_t *in, int64_t B, int64_t H, int64_t W, int64_t Cw, int k,
-                          int st, uint64_t *out, cudaStream_t s) {
+                          int st, uint64_t *out, int64_t out_bstride, cudaStream_t s) {
     const int64_t OH = (H - k) / st + 1, OW = (W - k) / st + 1;
     const int64_t total = B * OH * OW * Cw;
     if (total == 0) return BNN_OK;
-    maxpool_packed_kernel<<<(unsigned)ceil_div(total, 256), 256, 0, s>>>(in, H, W, Cw, k, st, OH,
-                                                                        OW, total, out);
+    maxpool_packed_kernel<<<(unsigned)ceil_div(total, 256), 256, 0, s>>>(
+        in, H, W, Cw, k, st, OH, OW, total, out, out_bstride > 0 ? out_bstride : OH * OW * Cw);
     return check_launch("maxpool_packed_kernel");
 }
 int launch_binarize(const float *x, int64_t n, float *out, int32_t *flags, cudaStream_t s) {

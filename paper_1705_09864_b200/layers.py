@@ -470,7 +470,10 @@ class QDense(_QLayer):
             bits = np.unpackbits(words, axis=1, bitorder="little")[:, :self.in_features]
             bits = bits.reshape(self.units, c, h, w).transpose(0, 2, 3, 1).reshape(self.units, -1)
             packed = np.packbits(bits, axis=1, bitorder="little").view(np.uint64)
-            cache[key] = torch.from_numpy(np.ascontiguousarray(packed)).cuda()
+            rw = packed.shape[1]
+            padded = np.zeros((self.units, rw + (rw & 1)), np.uint64)  # even pitch: 16-byte rows
+            padded[:, :rw] = packed
+            cache[key] = torch.from_numpy(padded).cuda()[:, :rw]
         return cache[key]
 
     def forward_packed_hwc(self, x_words: torch.Tensor, chw, bn=None) -> torch.Tensor:

@@ -339,6 +339,18 @@ def test_maxpool_packed_is_pack_of_maxpool(nets, shape, k):
               _lib.stream_ptr())
     expect = bnn.pack_nchw(F.max_pool2d(x, k)).cpu().numpy()
     assert np.array_equal(out.cpu().numpy(), expect)
+    # the strided form (one padded row per image, what a following QFullyConnected reads)
+    rw = oh * ow * cw
+    pitch = rw + 3
+    rows = torch.full((b, pitch), 0x5A5A, dtype=torch.int64, device="cuda").view(torch.uint64)
+    _lib.call("bnn_maxpool_packed_ld", _lib.ptr(words), b, h, w, cw, k, k, _lib.ptr(rows), pitch,
+              _lib.stream_ptr())
+    got = rows.cpu().numpy()
+    assert np.array_equal(got[:, :rw], expect.reshape(b, rw))
+    assert np.all(got[:, rw:] == 0x5A5A)  # the pad words are not touched
+    with pytest.raises(Exception):
+        _lib.call("bnn_maxpool_packed_ld", _lib.ptr(words), b, h, w, cw, k, k, _lib.ptr(rows), rw - 1,
+                  _lib.stream_ptr())
 
 
 def test_lenet_packed_tail_equals_float_path(nets):
