@@ -707,20 +707,35 @@ __global__ void __launch_bounds__(64 * kFcGroups) fc_rows_kernel(const float *__
     for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
+    // programmatic dependent launch: the first weight tile (a constant of the layer) is loaded
+    // while the pooling kernel finishes; `pooled` is read after griddepcontrol.wait
+    constexpr int kP = kFcImg * kFcK / 64, kW = kFcOut * kFcK / 64;
+    float vw[kW];
+    {
+        const int kn = ke - kb < kFcK ? (ke - kb > 0 ? ke - kb : 0) : kFcK;
+#pragma unroll
+        for (int u = 0; u < kW; ++u) {
+            const int i = t + 64 * u, r = i / kFcK, k = i - r * kFcK;
+            vw[u] = (o0 + r < O && k < kn) ? __ldg(w + (int64_t)(o0 + r) * C + kb + k) : 0.0f;
+        }
+    }
+    asm volatile("griddepcontrol.launch_dependents;\n");
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
     for (int k0 = kb; k0 < kb + kq; k0 += kFcK) {  // (every group runs the same trip count: the barriers)
         const int kn = ke - k0 < kFcK ? (ke - k0 > 0 ? ke - k0 : 0) : kFcK;
         {   // all of a thread's tile loads in flight before its SMEM stores
-            constexpr int kP = kFcImg * kFcK / 64, kW = kFcOut * kFcK / 64;
-            float vp[kP], vw[kW];
+            float vp[kP];
 #pragma unroll
             for (int u = 0; u < kP; ++u) {
                 const int i = t + 64 * u, r = i / kFcK, k = i - r * kFcK;
                 vp[u] = (b0 + r < B && k < kn) ? __ldg(pooled + (int64_t)(b0 + r) * C + k0 + k) : 0.0f;
             }
+            if (k0 != kb) {
 #pragma unroll
-            for (int u = 0; u < kW; ++u) {
-                const int i = t + 64 * u, r = i / kFcK, k = i - r * kFcK;
-                vw[u] = (o0 + r < O && k < kn) ? __ldg(w + (int64_t)(o0 + r) * C + k0 + k) : 0.0f;
+                for (int u = 0; u < kW; ++u) {
+                    const int i = t + 64 * u, r = i / kFcK, k = i - r * kFcK;
+                    vw[u] = (o0 + r < O && k < kn) ? __ldg(w + (int64_t)(o0 + r) * C + k0 + k) : 0.0f;
+                }
             }
 #pragma unroll
             for (int u = 0; u < kP; ++u) {
@@ -778,6 +793,10 @@ __global__ void __launch_bounds__(64 * kFcGroups) fc_rows_kernel(const float *__
 __global__ void __launch_bounds__(128) avgpool_rows_kernel(const float *__restrict__ x, int64_t BC,
                                                            int HW, float *__restrict__ pooled) {
     extern __shared__ float rows[];  // [64][HW]
+    // programmatic dependent launch: the classifier GEMM may start its weight loads now; x is
+    // the previous kernel's output
+    asm volatile("griddepcontrol.launch_dependents;\n");
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
     const int64_t r0 = (int64_t)blockIdx.x * 64;
     const int nr = BC - r0 < 64 ? (int)(BC - r0) : 64;
     const float *src = x + r0 * HW;
@@ -803,15 +822,30 @@ __global__ void __launch_bounds__(128) avgpool_rows_kernel(const float *__restri
 int launch_avgpool_fc(const float *x, int64_t B, int64_t C, int64_t HW, const float *w,
                       const float *bias, int64_t O, float *y, float *pooled, cudaStream_t s) {
     if (B == 0) return BNN_OK;
-    if (HW <= 256)  // (64 rows of HW floats staged in SMEM)
-        avgpool_rows_kernel<<<(unsigned)ceil_div(B * C, 64), 128, (size_t)64 * HW * 4, s>>>(
-            x, B * C, (int)HW, pooled);
-    else
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    if (HW <= 256) {  // (64 rows of HW floats staged in SMEM)
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)ceil_div(B * C, 64));
+        cfg.blockDim = dim3(128);
+        cfg.dynamicSmemBytes = (size_t)64 * HW * 4;
+        cfg.stream = s;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, avgpool_rows_kernel, x, B * C, (int)HW, pooled);
+    } else {
         avgpool_kernel<<<(unsigned)ceil_div(B * C, 256), 256, 0, s>>>(x, B * C, (int)HW, pooled);
+    }
     int rc = check_launch("avgpool_kernel");
     if (rc) return rc;
-    dim3 g((unsigned)ceil_div(B, kFcImg), (unsigned)ceil_div(O, kFcOut));
-    fc_rows_kernel<<<g, 64 * kFcGroups, 0, s>>>(pooled, (int)B, (int)C, w, bias, (int)O, y);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)ceil_div(B, kFcImg), (unsigned)ceil_div(O, kFcOut));
+    cfg.blockDim = dim3(64 * kFcGroups);
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, fc_rows_kernel, (const float *)pooled, (int)B, (int)C, w, bias, (int)O, y);
     return check_launch("fc_rows_kernel");
 }
 int launch_popcount64(const uint64_t *w, int64_t n, uint8_t *out, int soft, cudaStream_t s) {
