@@ -780,8 +780,25 @@ int launch_wconv(const uint64_t *x, int64_t B, int64_t C, int64_t H, int64_t W, 
         }
     }
     if (tpi == 0) return BNN_EUNSUP;
-    g.tpi = tpi;
     g.fgroups = (int)(F / FG);
+    {
+        // a CTA's range should split into >= 3 items, so that the band loads of an item overlap
+        // the MMAs / epilogue of the previous one (ResNet-18 layer 2 at batch 256, 12 tiles per
+        // CTA: items of 4 tiles 70 us against 76 us with one 10-tile item; layer 1, 45 tiles
+        // per CTA, keeps large bands: fewer halo rows expanded twice)
+        int sms0 = bnn_device_sm_count();
+        if (sms0 <= 0) sms0 = 148;
+        if (g_debug.grid_cap > 0 && sms0 > g_debug.grid_cap) sms0 = (int)g_debug.grid_cap;
+        int nr = sms0 / g.fgroups < 1 ? 1 : sms0 / g.fgroups;
+        if (nr > g.ntiles) nr = g.ntiles;
+        const int per = g.ntiles / nr, want = per / 3 < 2 ? 2 : per / 3;
+        if (want < tpi) {
+            tpi = want;
+            const int rows = (int)((tpi * kRows + (kh - 1) * Wp + (kw - 1) + Wp - 1) / Wp + 1);
+            g.band_rows = rows, g.band_pos = (int)(rows * Wp), g.plane_bytes = g.band_pos * 16;
+        }
+    }
+    g.tpi = tpi;
     const Smem L(FG, g.K, planes, g.plane_bytes, g.band_pos);
     const int smem = (int)L.total + 1024;
     int sms = bnn_device_sm_count();
