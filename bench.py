@@ -636,7 +636,8 @@ def run_gpu_arm(args, rank, world, local_rank):
                "ms_per_step": e2e_ms,
                "path": (f"{type(plan).__name__}.run_host: pinned H2D -> pack -> kernels -> "
                         "D2H -> sync (one CUDA-graph replay per call, pipelined over "
-                        f"{getattr(plan, 'host_chunks', 1)} batch slices on 3 streams)")
+                        f"{getattr(plan, 'host_chunks', 1)} batch slices on 3 streams; the slice count is "
+                        "tuned once on the first call, outside the timed region)")
                if getattr(plan, "graph_ok", True) else
                (f"{type(plan).__name__}.run_host: pinned H2D of this rank's packed B shard -> "
                 "GEMM -> all-gather -> D2H of the full result -> sync (eager)")}

@@ -629,7 +629,7 @@ def test_plan_run_host_pipelined_equals_single_pass(bnn, which):
         expect = orc.qdense_packed(orc.binarize(x), wt)
     xh = torch.from_numpy(x).pin_memory()
     outs = []
-    for chunks in (1, 3, 8):
+    for chunks in ("auto", 1, 3, 8):  # "auto": tuned on the first call, any count gives the same bits
         plan.host_chunks = chunks
         yh = torch.empty(plan.y.shape, dtype=torch.float32).pin_memory()
         outs.append(plan.run_host(xh, yh).numpy().copy())
