@@ -85,6 +85,8 @@ class _Plan:
             # the entry keeps the host buffers alive: the graph's copy nodes hold their
             # addresses, and a freed pinned block can come back at the same address
             graphs[key] = (g, x_host, y_host)
+            while len(graphs) > 16:  # bounded: the oldest schedule (and its buffers) goes first
+                graphs.pop(next(iter(graphs)))
         return graphs[key][0]
 
     def _tune_host_chunks(self, x_host: torch.Tensor, y_host: torch.Tensor) -> int:
