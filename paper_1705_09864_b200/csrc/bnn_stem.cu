@@ -339,19 +339,20 @@ struct PoolGeom {
     uint8_t *pack8;      // mode 1, optional: the same as 8-bit pieces (16 epilogue warps); y may then be null
     int32_t *pack_flags;
     int NR;    // staged input rows per channel: (R - 1) * sh + kh
+    int rbufs; // epilogue row buffers: 2 = double-buffered (one CTA-wide barrier per tile instead of two)
     int dbg;  // debug (BNN_STEM_DEBUG, wrong results): 1 no gather loads, 2 no MMAs,
               // 4 no epilogue work, 8 no loader loads
 };
 
 struct PoolSmem {
     int off_bhi, off_blo, off_ktab, off_xs, off_r, off_bn, off_bars, off_tmem, bytes;
-    __host__ __device__ PoolSmem(int nch, int xs_floats) {
+    __host__ __device__ PoolSmem(int nch, int xs_floats, int rbufs = 1) {
         off_bhi = 0;
         off_blo = nch * NF * 128;
         off_ktab = 2 * nch * NF * 128;
         off_xs = off_ktab + nch * KC * 4;
         off_r = off_xs + kPX * xs_floats * 4;
-        off_bn = off_r + NF * kRowPitchR * 4;
+        off_bn = off_r + rbufs * NF * kRowPitchR * 4;
         off_bars = off_bn + 5 * NF * 4;
         off_tmem = off_bars + (2 * kPS + 2 * kPAcc + 2 * kPX) * 8;
         bytes = off_tmem + 16 + 1024;
@@ -403,11 +404,11 @@ __global__ void __launch_bounds__(PEpi<kEW>::kThreads, 1) conv_pool_kernel(const
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
     uint8_t *smem = smem_raw + (base - raw);
-    const PoolSmem L(g.nch, g.xs_floats);
+    const PoolSmem L(g.nch, g.xs_floats, g.rbufs);
     const uint32_t s_bhi = base + L.off_bhi, s_blo = base + L.off_blo;
     int *ktab = reinterpret_cast<int *>(smem + L.off_ktab);
     float *xs = reinterpret_cast<float *>(smem + L.off_xs);
-    float *rbuf = reinterpret_cast<float *>(smem + L.off_r);
+    float *rbuf0 = reinterpret_cast<float *>(smem + L.off_r);
     float *bnt = reinterpret_cast<float *>(smem + L.off_bn);  // sign, mean, inv, gamma, beta
     const uint32_t bar_full = base + L.off_bars, bar_empty = bar_full + 8 * kPS;
     const uint32_t bar_tfull = bar_empty + 8 * kPS, bar_tempty = bar_tfull + 8 * kPAcc;
@@ -672,6 +673,9 @@ __global__ void __launch_bounds__(PEpi<kEW>::kThreads, 1) conv_pool_kernel(const
         };
         for (int oy = oy_s; oy <= oy_e; oy += g.R, ++it) {
             const int buf = it % kPAcc;
+            // (two row buffers: tile i + 1's values are written while slower warps still pool
+            // tile i; the barrier of tile i + 1 orders them against tile i + 2's writes)
+            float *rbuf = rbuf0 + (g.rbufs == 2 ? (it & 1) * (NF * kRowPitchR) : 0);
             mbar_wait_sleep(bar_tfull + 8 * buf, (it / kPAcc) & 1);
             fence_after();
             const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + buf * NF;
@@ -756,7 +760,7 @@ __global__ void __launch_bounds__(PEpi<kEW>::kThreads, 1) conv_pool_kernel(const
                 }
                 if (done) put_bits((oy - 1) >> 1, bits, nf);
             }
-            epi_bar<kEW>();  // the row buffer is free for the next conv row
+            if (g.rbufs != 2) epi_bar<kEW>();  // the row buffer is free for the next conv row
         }
         if (g.mode == 0 && !(oy_e & 1) && (oy_e >> 1) < py1) emit(oy_e >> 1);  // last pooled row without a row below
         POOL_ITEMS_END
@@ -865,7 +869,8 @@ int launch_conv_bn_relu_maxpool_tc(const float *x, int64_t B, int64_t C, int64_t
     g.nbands = (int)ceil_div(PH, pyb);
     if (B * g.nbands >= (1ll << 31)) return set_error(BNN_EUNSUP, "fused stem: too many items");
     g.items = (int)(B * g.nbands);
-    const PoolSmem L(g.nch, g.xs_floats);
+    g.rbufs = PoolSmem(g.nch, g.xs_floats, 2).bytes <= 227 * 1024 && !(g.dbg & 32) ? 2 : 1;
+    const PoolSmem L(g.nch, g.xs_floats, g.rbufs);
     if (L.bytes > 227 * 1024) return set_error(BNN_EUNSUP, "fused stem: shared memory");
     if (B == 0) return BNN_OK;
     const int grid = g.items < sm_count() ? g.items : sm_count();
@@ -873,7 +878,8 @@ int launch_conv_bn_relu_maxpool_tc(const float *x, int64_t B, int64_t C, int64_t
         using G = GeoStride2<3, 7, 7, 234>;
         g.rpitch = 234;
         g.xs_floats = (int)(C * g.NR * 234);
-        const PoolSmem L2(g.nch, g.xs_floats);
+        g.rbufs = PoolSmem(g.nch, g.xs_floats, 2).bytes <= 227 * 1024 && !(g.dbg & 32) ? 2 : 1;
+        const PoolSmem L2(g.nch, g.xs_floats, g.rbufs);
         static bool configured = false;
         if (!configured) {
             cudaFuncSetAttribute(conv_pool_kernel<G, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
