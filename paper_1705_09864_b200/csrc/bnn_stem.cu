@@ -708,9 +708,18 @@ __global__ void __launch_bounds__(PEpi<kEW>::kThreads, 1) conv_pool_kernel(const
             // horizontal 3-max (window 2px-1 .. 2px+1, clipped) of this conv row, folded
             // into the pooled rows: an odd conv row completes pooled row (oy - 1) / 2
             // and starts (oy + 1) / 2, an even one is the middle row of oy / 2
-            if (g.mode == 1 && px < g.PW && !(g.dbg & 4)) {
-                // 2x2/2 pool inside the tile: conv rows (2r, 2r + 1) -> pooled row oy / 2 + r
-                for (int r = 0; 2 * r + 1 < g.R && oy + 2 * r + 1 <= oy_e; ++r) {
+            if (g.mode == 1) {
+                // 2x2/2 pool inside the tile: conv rows (2r, 2r + 1) -> pooled row oy / 2 + r.
+                // When the tile's pooled pixels fit the 64 pixel slots of a channel group, each
+                // thread takes ONE pooled pixel (row r, column px) instead of walking the rows of
+                // its column: twice the active threads, half the serial work (LeNet: 28 pixels)
+                const bool flat = (g.R >> 1) * g.PW <= 64;
+                const int pp = et & 63;
+                const int rf = flat ? pp / g.PW : 0;
+                const int px = flat ? pp - rf * g.PW : pp;
+                const int r_end = flat ? rf + 1 : g.R;
+                if (!(g.dbg & 4) && px < g.PW && (!flat || 2 * rf + 1 < g.R))
+                for (int r = rf; r < r_end && 2 * r + 1 < g.R && oy + 2 * r + 1 <= oy_e; ++r) {
                     float *yrow = yb + (int64_t)((oy >> 1) + r) * g.PW + px;
                     const int o0 = 2 * r * g.OW + 2 * px, o1 = o0 + g.OW;
                     uint32_t bits = 0;

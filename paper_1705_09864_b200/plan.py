@@ -12,6 +12,8 @@ reference's ValueError on non-finite input (bitpack.py:37-38).
 from __future__ import annotations
 
 
+import time
+
 import torch
 
 from . import _lib
@@ -90,28 +92,28 @@ class _Plan:
         return graphs[key][0]
 
     def _tune_host_chunks(self, x_host: torch.Tensor, y_host: torch.Tensor) -> int:
-        """Time the end-to-end schedule per slice count (CUDA events around graph replays)."""
+        """Time the end-to-end schedule per slice count (host clock around replay + sync)."""
         if not hasattr(self, "run_device_range"):
             return 1
-        best, best_ms = 1, None
-        for c in self.host_chunk_candidates:
-            if c > self.b:
-                continue
-            self.host_chunks = c
-            g = self._host_graph(x_host, y_host)
-            run = g.replay if g is not None else (lambda: self._host_schedule(x_host, y_host))
-            run()
-            torch.cuda.synchronize()
-            ms = 0.0
-            for _ in range(4):  # one call at a time, as run_host is used (a sync after each)
-                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                s.record()
+        cands = [c for c in self.host_chunk_candidates if c <= self.b]
+        times = {}
+        for _ in range(2):  # two passes: the first candidate is not the only one timed on cold clocks
+            for c in cands:
+                self.host_chunks = c
+                g = self._host_graph(x_host, y_host)
+                run = g.replay if g is not None else (lambda: self._host_schedule(x_host, y_host))
                 run()
-                e.record()
-                e.synchronize()
-                ms += s.elapsed_time(e)
-            if best_ms is None or ms < best_ms:
-                best, best_ms = c, ms
+                torch.cuda.synchronize()
+                for _ in range(5):  # one call at a time on the host clock, as run_host is used:
+                    t0 = time.perf_counter()  # the launch cost of a many-node graph counts too
+                    run()
+                    torch.cuda.current_stream().synchronize()
+                    t = (time.perf_counter() - t0) * 1e3
+                    times[c] = min(t, times.get(c, t))
+        best, best_ms = 1, None
+        for c in cands:  # (more slices must win by 3% to be taken)
+            if best_ms is None or times[c] < 0.97 * best_ms:
+                best, best_ms = c, times[c]
         graphs = self.__dict__.get("_host_graphs", {})
         for c in self.host_chunk_candidates:  # drop the losing candidates' graphs
             if c != best:
